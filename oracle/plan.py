@@ -1,0 +1,189 @@
+"""TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+The slicing planner of TeraPipe §3.3, written out step by step, plus the
+brute force that defines its optimum and the schedule simulators behind Eq. 5.
+
+Costs are int64 ticks (reading A-15): t(l, c) is the fwd+bwd time of a slice of l units with
+c units of context, given as a table `t[l-1][c]` of shape [n][n+1]
+(units of the granularity g; only l + c <= n is used; used entries must be > 0).
+With integer costs every sum is exact, so "DP == brute force" holds exactly, not within a
+tolerance.
+
+Objective (Eq. 5, generalised by reading A-20 to D jobs per slice index):
+    T(l_1..l_M) = D * sum_i t_i + (K - 1) * max_i t_i,   t_i = t(l_i, sum_{j<i} l_j).
+D = 1 is exactly the paper's Eq. 5.
+
+Parity status: pinned (tests/test_oracle_plan.py) — optimize() == brute_force() exactly on
+random integer instances; SPEC.md:146-147 worked examples (T = 4, T = 10); closed form ==
+flow-shop simulation (SPEC.md:253-264 examples and random vectors); epsilon gap <= K*eps
+(PAPER.md:290); pruning soundness.
+"""
+from __future__ import annotations
+
+import itertools
+from typing import Iterable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+INF = None  # marker for "no feasible scheme"
+
+
+def slice_costs(t: np.ndarray, lengths: Sequence[int]) -> List[int]:
+    """t_i = t_fwd(l_i, sum_{j<i} l_j)."""
+    out, c = [], 0
+    for l in lengths:
+        out.append(int(t[l - 1, c]))
+        c += l
+    return out
+
+
+def objective(t: np.ndarray, lengths: Sequence[int], K: int, D: int = 1) -> int:
+    """Eq. 5 with D jobs per slice index (A-20)."""
+    ts = slice_costs(t, lengths)
+    return D * sum(ts) + (K - 1) * max(ts)
+
+
+def dp_fixed_tmax(t: np.ndarray, n: int, t_max: int) -> Optional[Tuple[int, List[int]]]:
+    """Algorithm 1: S*(0) = 0; for i = 1..n,
+    S*(i) = min_{1<=k<=i} { S*(i-k) + t(k, i-k) | t(k, i-k) <= t_max } (Eq. 8),
+    q_i = argmin (reading A-11: r_{i-k} is S*(i-k); A-12: the smallest k wins ties),
+    then backtrack l.prepend(q_i), i -= q_i. Returns (S*(n), [l_1..l_M]) or None if infeasible."""
+    S: List[Optional[int]] = [None] * (n + 1)
+    q = [0] * (n + 1)
+    S[0] = 0
+    for i in range(1, n + 1):
+        best, arg = None, 0
+        for k in range(1, i + 1):
+            if S[i - k] is None:
+                continue
+            tk = int(t[k - 1, i - k])
+            if tk > t_max:
+                continue
+            v = S[i - k] + tk
+            if best is None or v < best:
+                best, arg = v, k
+        S[i], q[i] = best, arg
+    if S[n] is None:
+        return None
+    lengths: List[int] = []
+    i = n
+    while i > 0:
+        lengths.insert(0, q[i])
+        i -= q[i]
+    return S[n], lengths
+
+
+def candidates(t: np.ndarray, n: int, eps: int = 0) -> List[int]:
+    """All distinct t(k, j), k >= 1, k + j <= n, ascending, thinned so each kept
+    value is >= the last kept one + eps (reading A-13: keep the first of a cluster)."""
+    vals = sorted({int(t[k - 1, j]) for k in range(1, n + 1) for j in range(0, n - k + 1)})
+    if eps <= 0:
+        return vals
+    out: List[int] = []
+    for v in vals:
+        if not out or v >= out[-1] + eps:
+            out.append(v)
+    # reading A-13b: the largest value is always evaluated, so thinning can never make every
+    # evaluated t_max infeasible (at t_max = max t, the all-ones scheme is feasible).
+    if out[-1] != vals[-1]:
+        out.append(vals[-1])
+    return out
+
+
+def optimize(t: np.ndarray, n: int, K: int, D: int = 1, eps: int = 0,
+             prune: bool = True) -> Tuple[int, int, List[int]]:
+    """Enumerate t_max ascending (Eq. 6-7), run Algorithm 1 for each, keep the
+    scheme with the smallest T (replace only on strict improvement, A-12); stop when
+    (D + K - 1) * t_max >= best T (PAPER.md:290 'K * t_max greater than the current best',
+    generalised to D jobs and to >=, reading A-14). Returns (T, t_max_of_scheme, lengths)."""
+    best: Optional[Tuple[int, int, List[int]]] = None
+    for c in candidates(t, n, eps):
+        if prune and best is not None and (D + K - 1) * c >= best[0]:
+            break
+        r = dp_fixed_tmax(t, n, c)
+        if r is None:
+            continue
+        _, lengths = r
+        ts = slice_costs(t, lengths)
+        T = D * sum(ts) + (K - 1) * max(ts)
+        if best is None or T < best[0]:
+            best = (T, max(ts), lengths)
+    if best is None:
+        raise ValueError("infeasible: no slicing scheme")
+    return best
+
+
+def compositions(n: int) -> Iterable[Tuple[int, ...]]:
+    """All 2^(n-1) compositions of n (ordered positive parts)."""
+    for cuts in itertools.product((0, 1), repeat=n - 1):
+        parts, last = [], 0
+        for i, cut in enumerate(cuts, start=1):
+            if cut:
+                parts.append(i - last)
+                last = i
+        parts.append(n - last)
+        yield tuple(parts)
+
+
+def brute_force(t: np.ndarray, n: int, K: int, D: int = 1) -> Tuple[int, int, List[int]]:
+    """The definition of the optimum: score every composition of n with Eq. 5 and take the
+    lexicographic minimum of (T, max t_i, reversed lengths) — the same deterministic tie-break
+    Algorithm 1 with smallest-k backpointers produces (reading A-12)."""
+    if n > 22:
+        raise ValueError("too big for the Python brute force (use oracle/bf_compositions.c)")
+    best = None
+    for comp in compositions(n):
+        ts = slice_costs(t, comp)
+        key = (D * sum(ts) + (K - 1) * max(ts), max(ts), tuple(reversed(comp)))
+        if best is None or key < best:
+            best = key
+    T, m, rev = best
+    return T, m, list(reversed(rev))
+
+
+def uniform_schemes(n: int) -> List[List[int]]:
+    """[n/d] * d for every divisor d of n (SPEC.md:165 'DP dominates uniform')."""
+    return [[n // d] * d for d in range(1, n + 1) if n % d == 0]
+
+
+# ---------------------------------------------------------------- schedule models
+def closed_form(ts: Sequence[float], K: int, D: int = 1):
+    """Eq. 5: sum_i t_i + (K-1) max_j t_j, for D repetitions of the slice list."""
+    return D * sum(ts) + (K - 1) * max(ts)
+
+
+def flowshop_makespan(durations: Sequence[float], K: int):
+    """Pipeline semantics of Fig. 2(c)/Fig. 5: job i on stage k starts when job i-1 left stage k
+    and job i left stage k-1: start(i,k) = max(end(i-1,k), end(i,k-1)), end = start + t_i."""
+    M = len(durations)
+    end = [[0.0] * (K + 1) for _ in range(M + 1)]
+    for i in range(1, M + 1):
+        for k in range(1, K + 1):
+            end[i][k] = max(end[i - 1][k], end[i][k - 1]) + durations[i - 1]
+    return end[M][K]
+
+
+def oplist_makespan(tf: Sequence[Sequence[float]], tb: Sequence[Sequence[float]],
+                    comm: float = 0.0) -> float:
+    """Replays the runtime's per-stage op lists (GPipe order, reading A-21): stage k runs
+    F(j) for j = 0..J-1 then B(j) for j = J-1..0, each op waiting for its cross-stage input
+    (F(j) on k-1, resp. B(j) on k+1; B(j) on the last stage waits for its own F(j)) plus `comm`.
+    tf[k][j], tb[k][j]: per-stage, per-job durations. Returns the makespan."""
+    K, J = len(tf), len(tf[0])
+    fend = [[0.0] * J for _ in range(K)]
+    bend = [[0.0] * J for _ in range(K)]
+    free = [0.0] * K
+    # forward wave: stage-major is a valid topological order for a DAG with edges k-1 -> k
+    for k in range(K):
+        for j in range(J):
+            dep = fend[k - 1][j] + comm if k > 0 else 0.0
+            st = max(free[k], dep)
+            fend[k][j] = st + tf[k][j]
+            free[k] = fend[k][j]
+    for k in reversed(range(K)):
+        for j in reversed(range(J)):
+            dep = bend[k + 1][j] + comm if k < K - 1 else fend[k][j]
+            st = max(free[k], dep)
+            bend[k][j] = st + tb[k][j]
+            free[k] = bend[k][j]
+    return max(free)

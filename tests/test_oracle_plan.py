@@ -1,0 +1,130 @@
+"""Pins for oracle/plan.py (CPU only).
+
+  * SPEC.md:135-147 worked examples (T = 4 and T = 10, dp_fixed_tmax examples);
+  * SPEC.md:253-264 schedule examples ([1,3],K=2 -> 7; [1,3,1],K=3 -> 11);
+  * Algorithm 1 + enumeration == brute force over all compositions (the definition), exactly,
+    on random integer instances including heavy ties (BASELINE.json:5 invariant (b));
+  * closed form (Eq. 5) == flow-shop simulation (invariant (c)) and the fwd+bwd GPipe-order
+    op-list replay == D*sum(tf+tb) + (K-1)(max tf + max tb) (reading A-19);
+  * pruning soundness and the epsilon gap <= K*eps of PAPER.md:290.
+"""
+import subprocess
+import os
+
+import numpy as np
+import pytest
+
+from oracle import plan as op
+from synth import random_int_table, gpu_like_table
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BF = os.path.join(ROOT, "oracle", "bf_compositions")
+
+
+def table_from(fn, n):
+    t = np.zeros((n, n + 1), dtype=np.int64)
+    for l in range(1, n + 1):
+        for c in range(0, n - l + 1):
+            t[l - 1, c] = fn(l, c)
+    return t
+
+
+def test_spec_examples():
+    t = table_from(lambda l, c: l, 3)
+    assert op.dp_fixed_tmax(t, 3, 1) == (3, [1, 1, 1])
+    T, m, lens = op.optimize(t, 3, K=2)
+    assert (T, lens) == (4, [1, 1, 1])
+    t = table_from(lambda l, c: 1 + l, 3)
+    T, m, lens = op.optimize(t, 3, K=3)
+    assert (T, lens) == (10, [1, 1, 1])
+    const = table_from(lambda l, c: 5, 6)
+    assert op.dp_fixed_tmax(const, 6, 5) == (5, [6])
+    assert op.dp_fixed_tmax(const, 6, 4) is None
+    assert op.optimize(const, 6, K=1) == (5, 5, [6])
+
+
+def test_schedule_examples_and_closed_form():
+    assert op.flowshop_makespan([1, 3], 2) == 7
+    assert op.closed_form([1, 3], 2) == 7
+    assert op.closed_form([1, 3, 1], 3) == 11 == op.flowshop_makespan([1, 3, 1], 3)
+    assert op.flowshop_makespan([4.5], 5) == 5 * 4.5
+    rng = np.random.default_rng(0)
+    for _ in range(1000):
+        M, K, D = rng.integers(1, 12), rng.integers(1, 9), rng.integers(1, 4)
+        ts = list(rng.integers(1, 100, size=M))
+        assert op.flowshop_makespan(ts * D, K) == op.closed_form(ts, K, D)
+
+
+def test_oplist_replay_matches_two_wave_closed_form():
+    rng = np.random.default_rng(1)
+    for _ in range(300):
+        M, K, D = rng.integers(1, 7), rng.integers(1, 6), rng.integers(1, 4)
+        tf = list(rng.integers(1, 50, size=M)) * D
+        tb = list(rng.integers(1, 90, size=M)) * D
+        ms = op.oplist_makespan([tf] * K, [tb] * K)
+        assert ms == sum(tf) + sum(tb) + (K - 1) * (max(tf) + max(tb))
+        # with t_b proportional to t_f it reduces to Eq. 5 on t_f + t_b
+        tb2 = [2 * x for x in tf]
+        assert op.oplist_makespan([tf] * K, [tb2] * K) == op.closed_form(
+            [a + b for a, b in zip(tf, tb2)], K)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_dp_equals_brute_force_random(seed):
+    rng = np.random.default_rng(100 + seed)
+    for trial in range(30):
+        n = int(rng.integers(1, 12))
+        K = int(rng.integers(1, 5))
+        D = int(rng.choice([1, 2, 8]))
+        hi = int(rng.choice([3, 10, 1000]))
+        t = random_int_table(n, rng, 1, hi)
+        bf = op.brute_force(t, n, K, D)
+        dp = op.optimize(t, n, K, D)
+        assert dp == bf, (n, K, D, t, dp, bf)
+        assert op.optimize(t, n, K, D, prune=False)[0] == bf[0]              # pruning soundness
+
+
+def test_dp_dominates_uniform_and_eps_gap():
+    rng = np.random.default_rng(7)
+    for _ in range(20):
+        n = int(rng.integers(8, 33))
+        K = int(rng.integers(1, 9))
+        t = gpu_like_table(n, rng)
+        T0, _, lens = op.optimize(t, n, K)
+        assert sum(lens) == n and min(lens) >= 1
+        for u in op.uniform_schemes(n):
+            assert T0 <= op.objective(t, u, K)
+        for eps in (5_000, 10_000, 50_000):                                   # ticks (ns)
+            Te, _, _ = op.optimize(t, n, K, eps=eps)
+            assert T0 <= Te <= T0 + K * eps
+
+
+def _c_brute(t, n, K, D):
+    inp = f"{n} {K} {D}\n" + " ".join(str(int(v)) for v in t.reshape(-1)) + "\n"
+    r = subprocess.run([BF], input=inp, capture_output=True, text=True, check=True, timeout=600)
+    v = [int(x) for x in r.stdout.split()]
+    return v[0], v[1], v[3:3 + v[2]]
+
+
+@pytest.fixture(scope="module")
+def c_brute():
+    if not os.path.exists(BF):
+        subprocess.run(["gcc", "-O2", "-fopenmp", "-o", BF, BF + ".c"], check=True)
+    return _c_brute
+
+
+def test_c_brute_force_matches_python(c_brute):
+    rng = np.random.default_rng(5)
+    for _ in range(40):
+        n = int(rng.integers(1, 14))
+        K, D = int(rng.integers(1, 5)), int(rng.choice([1, 2, 8]))
+        t = random_int_table(n, rng, 1, int(rng.choice([3, 50])))
+        assert c_brute(t, n, K, D) == op.brute_force(t, n, K, D)
+
+
+@pytest.mark.slow
+def test_tiny_config_dp_equals_c_brute_force_2pow31(c_brute):
+    """Tiny config (BASELINE.json:7): s = 32, g = 1, K = 2, D = 1 — all 2^31 compositions."""
+    rng = np.random.default_rng(32)
+    t = gpu_like_table(32, rng, knee=4, base_ns=10_000, per_unit_ns=900, ctx_ns=300)
+    assert c_brute(t, 32, 2, 1) == op.optimize(t, 32, 2, 1)
