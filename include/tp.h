@@ -1,0 +1,183 @@
+/*
+ * tp.h — C ABI of the B200-native TeraPipe hot path (arXiv 2102.07988).
+ *
+ * Two calls follow the paper's problem statement (§3.3): "given a partitioned
+ * Transformer-based LM F = c_K o ... o c_1 and a training input sequence of length L, find the
+ * slicing scheme l_1..l_M to minimize the total forward and backward propagation latency":
+ *   tp_plan  — the dynamic program of §3.3 (Eq. 5-8, Algorithm 1) over a
+ *              t_fwd+bwd(slice_len, context_len) cost table;
+ *   tp_step  — one synchronous forward+backward of a causal GPT stack,
+ *              token-sliced and pipelined over K stages.
+ * The rest (tp_init, tp_load_params, tp_profile, getters) is the plumbing those two need.
+ *
+ * Conventions
+ *   - Every call returns tp_status (0 = TP_OK, < 0 = error). On error, tp_last_error() returns a
+ *     thread-local, NUL-terminated message valid until the next failing call on that thread.
+ *   - Bad arguments are rejected, never clamped (TP_EINVAL). No call falls back to a CPU path:
+ *     without a usable sm_100a GPU, tp_init fails with TP_ECUDA.
+ *   - The caller owns every host buffer passed in; the library copies what it keeps and never
+ *     retains a caller pointer past the call. The library owns all device memory, CUDA streams and
+ *     the NCCL communicator inside a tp_ctx.
+ *   - Host integers are little-endian; all sizes are element counts unless named *_bytes.
+ *
+ * Parameter layout (shared DATA, not code, with oracle/ and synth/): for stage k of K, one flat
+ * float32 array, in this order —
+ *     stage 0 only:   wte[V][H], wpe[s][H]
+ *     each owned layer l (layers k*n/K .. (k+1)*n/K - 1, uniform cells):
+ *         ln1_g[H], ln1_b[H], w_qkv[H][3H], b_qkv[3H], w_o[H][H], b_o[H],
+ *         ln2_g[H], ln2_b[H], w_1[H][4H], b_1[4H], w_2[4H][H], b_2[H]
+ *       (matrices row-major [in][out]; w_qkv columns are [q | k | v], head j at j*d..(j+1)*d)
+ *     stage K-1 only: lnf_g[H], lnf_b[H], w_out[H][V]
+ *   A context that owns several stages (loopback, world == 1) uses the concatenation in stage
+ *   order. Gradients (tp_get_grads) use exactly the same layout.
+ */
+#ifndef TP_H_
+#define TP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TP_OK = 0,
+  TP_EINVAL = -1,       /* bad argument / shape (SPEC.md exit code 2)                        */
+  TP_EINFEASIBLE = -2,  /* no slicing satisfies the constraints (SPEC.md exit code 3)       */
+  TP_ETOOBIG = -3,      /* instance too large for the requested operation                  */
+  TP_ECUDA = -4,        /* CUDA runtime/driver error, or no sm_100 device                   */
+  TP_ENCCL = -5,        /* NCCL error                                                      */
+  TP_ENOMEM = -6,       /* device or host allocation failed                                */
+  TP_ESTATE = -7        /* call not valid in the context's current state                   */
+} tp_status;
+
+enum { TP_BF16 = 0, /* bf16 GEMM/attention operands, fp32 accumulation, fp32 residual stream,
+                       softmax, LayerNorm statistics and stage messages (A-23)      */
+       TP_FP32 = 1  /* true fp32 arithmetic everywhere (SIMT FFMA; A-18)           */ };
+
+enum { TP_FLAG_KEEP_LOGITS = 1,   /* keep fp32 logits of the last step for tp_get_logits     */
+       TP_FLAG_KERNEL_STATS = 2,  /* bracket launches with CUDA events (tp_kernel_stats)      */
+       TP_FLAG_FORCE_SIMT = 4     /* bf16 mode: use SIMT GEMM/attention (kernel cross-checks)  */ };
+
+/* Model shape. n_layer % n_stages == 0; hidden % n_head == 0; head_dim = hidden / n_head must be
+ * a multiple of 16 and <= 128; hidden % 64 == 0; seq_len >= 1. */
+typedef struct {
+  int32_t n_layer, hidden, n_head, vocab, seq_len, n_stages;
+} tp_model_cfg;
+
+/* Cost table t_{fwd+bwd}(l, c) of ONE pipeline stage (the bottleneck stage; A-16), in
+ * integer ticks (A-15). l and c are in units of `granularity` tokens (g | seq_len, n_units =
+ * seq_len / g). ticks[(l-1)*(n_units+1) + c] = t(l*g tokens, c*g tokens of context), for
+ * 1 <= l, 0 <= c, l + c <= n_units; other entries are ignored. Used entries must be > 0.
+ * ticks_per_ms is informational (e.g. 1000000 for ns). Caller-owned, read-only during the call. */
+typedef struct {
+  int32_t granularity;
+  int32_t n_units;
+  const int64_t* ticks;
+  int64_t ticks_per_ms;
+} tp_cost_table;
+
+/* A slicing scheme [(b, [l_1..l_M])] * (B/b) in the paper's notation.
+ * lengths: caller-owned array of `capacity` int32 (tokens; multiples of g, sum = seq_len).
+ * batch_slice b: sequences per job (this build runs b = 1; other values -> TP_EINVAL in tp_step). */
+typedef struct {
+  int32_t batch_slice;
+  int32_t n_slices;          /* M                                          */
+  int32_t capacity;          /* size of `lengths` (>= n_units for tp_plan) */
+  int32_t* lengths;          /* l_1..l_M in tokens                         */
+  int64_t t_max_ticks;       /* max_i t_i of the scheme (tp_plan output)   */
+  int64_t predicted_ticks;   /* n_micro * sum t_i + (K-1) * max t_i        */
+} tp_slicing;
+
+/* ---------------------------------------------------------------- planner (host only) */
+/* The paper's DP: candidates = the distinct table values, ascending, thinned
+ * so each evaluated t_max is >= the previous evaluated one + eps_ticks (the largest
+ * value is always evaluated); for each, Algorithm 1 with smallest-k
+ * backpointers; keep the scheme minimising T = n_micro * sum t_i + (K-1) * max t_i (Eq. 5 with
+ * D = n_micro jobs per slice index, A-20; n_micro = 1 is Eq. 5 exactly), replacing only
+ * on strict improvement; stop once (n_micro + K - 1) * t_max >= best (A-14).
+ * eps_ticks = 0 gives the exact optimum, identical (T and boundaries) to brute force over all
+ * compositions with the tie-break (T, max t, reversed lengths). n_layer and hidden are validated
+ * (n_layer % n_stages == 0, hidden > 0) and otherwise informational. Pure, deterministic,
+ * thread-safe. Threads: env TP_PLAN_THREADS (default: hardware concurrency, max 64).
+ * Errors: TP_EINVAL (shape, table, capacity), TP_EINFEASIBLE (cannot happen for valid tables). */
+tp_status tp_plan(int32_t n_layer, int32_t hidden, int32_t seq_len, int32_t n_stages,
+                  const tp_cost_table* cost, int32_t n_micro, int64_t eps_ticks, tp_slicing* out);
+
+/* Number of float32 parameters of stage `stage` (see "Parameter layout"). */
+tp_status tp_stage_param_count(const tp_model_cfg* cfg, int32_t stage, size_t* out);
+
+/* ---------------------------------------------------------------- runtime (one process per GPU) */
+typedef struct tp_ctx tp_ctx;
+
+/* Writes a fresh 128-byte ncclUniqueId into out128 (rank 0 calls it; the harness broadcasts it). */
+tp_status tp_nccl_unique_id(void* out128);
+
+/* Creates a context on CUDA device `device`.
+ *  world == 1: this context owns ALL cfg->n_stages stages on one GPU ("loopback": stage messages
+ *              are device copies; no NCCL; nccl_id may be NULL).
+ *  world == cfg->n_stages > 1: this context owns stage `rank`; neighbours exchange slice
+ *              activations / gradients with ncclSend/ncclRecv over NVLink.
+ * precision: TP_BF16 or TP_FP32. max_batch: largest `batch` tp_step will be called with (sizes the
+ * store-all activation buffers). flags: TP_FLAG_*. */
+tp_status tp_init(const tp_model_cfg* cfg, int32_t rank, int32_t world, const void* nccl_id,
+                  int32_t precision, int32_t max_batch, int32_t device, int32_t flags,
+                  tp_ctx** out);
+
+/* Total float32 parameter count of the stages this context owns. */
+tp_status tp_param_count(const tp_ctx* ctx, size_t* out);
+
+/* Copies host parameters (stage-local flat layout, n == tp_param_count) to the device. In bf16
+ * mode matrices are rounded to bf16 (round-to-nearest-even) on the device. */
+tp_status tp_load_params(tp_ctx* ctx, const float* host_params, size_t n);
+
+/* One synchronous forward+backward of one batch with the given slicing: gradients are zeroed on
+ * entry, every stage runs F(d,i) for d = 0..B-1, i = 1..M, then B(d,i) in exact reverse order
+ * (GPipe order, store-all, A-21); weight gradients are accumulated per sequence.
+ * tokens: HOST int32 [batch][seq_len+1] (input = [:, :s], target = [:, 1:], A-8); read by the
+ * first and last stage. loss_out (may be NULL): mean cross-entropy over batch*seq_len targets,
+ * identical on every rank. Returns after all local device work has completed. */
+tp_status tp_step(tp_ctx* ctx, const tp_slicing* slicing, const int32_t* tokens, int32_t batch,
+                  float* loss_out);
+
+/* Same as tp_step with DEVICE tokens (already resident in HBM on this context's device). */
+tp_status tp_step_device(tp_ctx* ctx, const tp_slicing* slicing, const int32_t* dev_tokens,
+                         int32_t batch, float* loss_out);
+
+/* Copies the last step's gradients (same layout as tp_load_params) to host_out[n]. */
+tp_status tp_get_grads(tp_ctx* ctx, float* host_out, size_t n);
+
+/* Copies the last step's logits, float32 [batch][seq_len][vocab], to host_out[n]. Requires
+ * TP_FLAG_KEEP_LOGITS and a context owning the last stage (else TP_ESTATE). */
+tp_status tp_get_logits(tp_ctx* ctx, float* host_out, size_t n);
+
+/* Measures this context's (first owned) stage: t_{fwd+bwd}(l, c) of one job of l tokens with c
+ * tokens of context, in ns (median of `reps` after 2 warm-ups). The base curve t(l, 0) is measured
+ * for every l = g, 2g, .., s and t_ctx(l, c) = a0 + a1 l + a2 c + a3 l c is least-squares fitted on
+ * a subset of (l, c); ticks_out[(l/g-1)*(n+1) + c/g] = t(l,0) + t_ctx(l,c)
+ * (n = s/g; caller-owned, n*(n+1) int64). fit_out (may be NULL): a0..a3 (ns, ns/token, ns/token,
+ * ns/token^2) and the max relative error of the fit on the samples. Parameters must be loaded. */
+tp_status tp_profile(tp_ctx* ctx, int32_t granularity, int32_t reps, int64_t* ticks_out,
+                     double* fit_out /* [5] */);
+
+/* The CUDA stream (cudaStream_t) all compute of this context is issued on. */
+tp_status tp_get_stream(tp_ctx* ctx, void** stream_out);
+
+/* Kernel statistics collected while TP_FLAG_KERNEL_STATS is set: for class index i (0 <= i <
+ * *n_classes), name (<= 31 chars), launches, summed device ms (CUDA events on the launching
+ * stream), summed algorithmic FLOPs and bytes. tp_kernel_stats_reset clears them. */
+tp_status tp_kernel_stats(tp_ctx* ctx, int32_t i, char* name32, int64_t* launches, double* ms,
+                          double* flops, double* bytes, int32_t* n_classes);
+tp_status tp_kernel_stats_reset(tp_ctx* ctx);
+
+/* Number of kernel launches issued by the last tp_step (device work only, this context). */
+tp_status tp_last_step_launches(tp_ctx* ctx, int64_t* out);
+
+void tp_destroy(tp_ctx* ctx);
+const char* tp_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TP_H_ */

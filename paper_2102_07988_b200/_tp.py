@@ -1,0 +1,230 @@
+"""ctypes binding of include/tp.h — argument marshalling only; every step runs in libtp.so.
+
+Loading fails loudly (ImportError) when libtp.so is missing: there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtp.so")
+
+TP_OK, TP_EINVAL, TP_EINFEASIBLE, TP_ETOOBIG, TP_ECUDA, TP_ENCCL, TP_ENOMEM, TP_ESTATE = 0, -1, -2, -3, -4, -5, -6, -7
+TP_BF16, TP_FP32 = 0, 1
+TP_FLAG_KEEP_LOGITS, TP_FLAG_KERNEL_STATS, TP_FLAG_FORCE_SIMT = 1, 2, 4
+
+EXPORTED = ["tp_plan", "tp_stage_param_count", "tp_nccl_unique_id", "tp_init", "tp_param_count",
+            "tp_load_params", "tp_step", "tp_step_device", "tp_get_grads", "tp_get_logits",
+            "tp_profile", "tp_get_stream", "tp_kernel_stats", "tp_kernel_stats_reset",
+            "tp_last_step_launches", "tp_destroy", "tp_last_error"]
+
+
+class TpError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"tp status {status}: {msg}")
+        self.status = status
+
+
+class ModelCfgC(C.Structure):
+    _fields_ = [("n_layer", C.c_int32), ("hidden", C.c_int32), ("n_head", C.c_int32),
+                ("vocab", C.c_int32), ("seq_len", C.c_int32), ("n_stages", C.c_int32)]
+
+
+class CostTableC(C.Structure):
+    _fields_ = [("granularity", C.c_int32), ("n_units", C.c_int32),
+                ("ticks", C.POINTER(C.c_int64)), ("ticks_per_ms", C.c_int64)]
+
+
+class SlicingC(C.Structure):
+    _fields_ = [("batch_slice", C.c_int32), ("n_slices", C.c_int32), ("capacity", C.c_int32),
+                ("lengths", C.POINTER(C.c_int32)), ("t_max_ticks", C.c_int64),
+                ("predicted_ticks", C.c_int64)]
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built — run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    P = C.c_void_p
+    sigs = {
+        "tp_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(CostTableC), C.c_int32,
+                              C.c_int64, C.POINTER(SlicingC)]),
+        "tp_stage_param_count": (C.c_int, [C.POINTER(ModelCfgC), C.c_int32, C.POINTER(C.c_size_t)]),
+        "tp_nccl_unique_id": (C.c_int, [P]),
+        "tp_init": (C.c_int, [C.POINTER(ModelCfgC), C.c_int32, C.c_int32, P, C.c_int32, C.c_int32, C.c_int32,
+                              C.c_int32, C.POINTER(P)]),
+        "tp_param_count": (C.c_int, [P, C.POINTER(C.c_size_t)]),
+        "tp_load_params": (C.c_int, [P, P, C.c_size_t]),
+        "tp_step": (C.c_int, [P, C.POINTER(SlicingC), P, C.c_int32, C.POINTER(C.c_float)]),
+        "tp_step_device": (C.c_int, [P, C.POINTER(SlicingC), P, C.c_int32, C.POINTER(C.c_float)]),
+        "tp_get_grads": (C.c_int, [P, P, C.c_size_t]),
+        "tp_get_logits": (C.c_int, [P, P, C.c_size_t]),
+        "tp_profile": (C.c_int, [P, C.c_int32, C.c_int32, P, P]),
+        "tp_get_stream": (C.c_int, [P, C.POINTER(P)]),
+        "tp_kernel_stats": (C.c_int, [P, C.c_int32, C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
+        "tp_kernel_stats_reset": (C.c_int, [P]),
+        "tp_last_step_launches": (C.c_int, [P, C.POINTER(C.c_int64)]),
+        "tp_destroy": (None, [P]),
+        "tp_last_error": (C.c_char_p, []),
+    }
+    for name, (res, args) in sigs.items():
+        f = getattr(lib, name)
+        f.restype, f.argtypes = res, args
+    return lib
+
+
+_lib = _load()
+
+
+def lib() -> C.CDLL:
+    return _lib
+
+
+def _check(st: int) -> None:
+    if st != TP_OK:
+        raise TpError(st, (_lib.tp_last_error() or b"").decode())
+
+
+def _cfg(cfg) -> ModelCfgC:
+    return ModelCfgC(cfg.n_layer, cfg.hidden, cfg.n_head, cfg.vocab, cfg.seq_len, cfg.n_stages)
+
+
+class Slicing:
+    """A slicing scheme [(b, [l_1..l_M])] * (B/b) (PAPER.md:494-641 notation)."""
+
+    def __init__(self, lengths: Sequence[int], batch_slice: int = 1, t_max: int = 0, predicted: int = 0):
+        self.lengths = [int(x) for x in lengths]
+        self.batch_slice = int(batch_slice)
+        self.t_max = int(t_max)
+        self.predicted = int(predicted)
+        self._arr = (C.c_int32 * max(1, len(self.lengths)))(*self.lengths)
+        self._c = SlicingC(self.batch_slice, len(self.lengths), len(self.lengths), self._arr,
+                           self.t_max, self.predicted)
+
+    @property
+    def c(self) -> SlicingC:
+        return self._c
+
+    def notation(self, batch: int) -> str:
+        return f"[({self.batch_slice}, {self.lengths})] * {batch // self.batch_slice}"
+
+    def __repr__(self):
+        return f"Slicing({self.lengths})"
+
+
+def plan(ticks: np.ndarray, granularity: int, n_layer: int, hidden: int, seq_len: int, n_stages: int,
+         n_micro: int = 1, eps_ticks: int = 0, ticks_per_ms: int = 1_000_000) -> Slicing:
+    """tp_plan (include/tp.h): the DP of PAPER.md:254-290 over t[l-1][c] (int64 ticks, [n][n+1])."""
+    n = seq_len // granularity if granularity > 0 else 0
+    t = np.ascontiguousarray(ticks, dtype=np.int64)
+    if t.shape != (n, n + 1):
+        raise TpError(TP_EINVAL, f"ticks shape {t.shape} != ({n}, {n + 1})")
+    table = CostTableC(granularity, n, t.ctypes.data_as(C.POINTER(C.c_int64)), ticks_per_ms)
+    buf = (C.c_int32 * max(1, n))()
+    out = SlicingC(1, 0, n, buf, 0, 0)
+    _check(_lib.tp_plan(n_layer, hidden, seq_len, n_stages, C.byref(table), n_micro, eps_ticks, C.byref(out)))
+    return Slicing([buf[i] for i in range(out.n_slices)], out.batch_slice, out.t_max_ticks, out.predicted_ticks)
+
+
+def stage_param_count(cfg, stage: int) -> int:
+    n = C.c_size_t()
+    _check(_lib.tp_stage_param_count(C.byref(_cfg(cfg)), stage, C.byref(n)))
+    return n.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.tp_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Context:
+    """tp_ctx: one process per GPU (or all stages on one GPU when world == 1)."""
+
+    def __init__(self, cfg, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
+                 precision: int = TP_BF16, max_batch: int = 1, device: int = 0, flags: int = 0):
+        self.cfg = cfg
+        self.max_batch = max_batch
+        self._h = C.c_void_p()
+        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        _check(_lib.tp_init(C.byref(_cfg(cfg)), rank, world, idbuf, precision, max_batch, device, flags,
+                            C.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            _lib.tp_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def param_count(self) -> int:
+        n = C.c_size_t()
+        _check(_lib.tp_param_count(self._h, C.byref(n)))
+        return n.value
+
+    def load_params(self, flat: np.ndarray) -> None:
+        a = np.ascontiguousarray(flat, dtype=np.float32)
+        _check(_lib.tp_load_params(self._h, a.ctypes.data, a.size))
+
+    def step(self, slicing: Slicing, tokens: np.ndarray) -> float:
+        tok = np.ascontiguousarray(tokens, dtype=np.int32)
+        loss = C.c_float()
+        _check(_lib.tp_step(self._h, C.byref(slicing.c), tok.ctypes.data, tok.shape[0], C.byref(loss)))
+        return loss.value
+
+    def step_device(self, slicing: Slicing, dev_tokens_ptr: int, batch: int) -> float:
+        loss = C.c_float()
+        _check(_lib.tp_step_device(self._h, C.byref(slicing.c), C.c_void_p(dev_tokens_ptr), batch, C.byref(loss)))
+        return loss.value
+
+    def grads(self) -> np.ndarray:
+        out = np.empty(self.param_count(), dtype=np.float32)
+        _check(_lib.tp_get_grads(self._h, out.ctypes.data, out.size))
+        return out
+
+    def logits(self, batch: int) -> np.ndarray:
+        c = self.cfg
+        out = np.empty((batch, c.seq_len, c.vocab), dtype=np.float32)
+        _check(_lib.tp_get_logits(self._h, out.ctypes.data, out.size))
+        return out
+
+    def profile(self, granularity: int, reps: int = 5) -> Tuple[np.ndarray, np.ndarray]:
+        n = self.cfg.seq_len // granularity
+        ticks = np.zeros((n, n + 1), dtype=np.int64)
+        fit = np.zeros(5, dtype=np.float64)
+        _check(_lib.tp_profile(self._h, granularity, reps, ticks.ctypes.data, fit.ctypes.data))
+        return ticks, fit
+
+    def stream(self) -> int:
+        p = C.c_void_p()
+        _check(_lib.tp_get_stream(self._h, C.byref(p)))
+        return p.value or 0
+
+    def kernel_stats(self) -> Dict[str, Dict[str, float]]:
+        n = C.c_int32()
+        _check(_lib.tp_kernel_stats(self._h, -1, None, None, None, None, None, C.byref(n)))
+        out = {}
+        for i in range(n.value):
+            name = C.create_string_buffer(32)
+            la, ms, fl, by = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+            _check(_lib.tp_kernel_stats(self._h, i, name, C.byref(la), C.byref(ms), C.byref(fl), C.byref(by), None))
+            out[name.value.decode()] = {"launches": la.value, "ms": ms.value, "flops": fl.value, "bytes": by.value}
+        return out
+
+    def kernel_stats_reset(self) -> None:
+        _check(_lib.tp_kernel_stats_reset(self._h))
+
+    def last_step_launches(self) -> int:
+        n = C.c_int64()
+        _check(_lib.tp_last_step_launches(self._h, C.byref(n)))
+        return n.value

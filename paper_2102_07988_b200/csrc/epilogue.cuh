@@ -1,0 +1,110 @@
+// epilogue.cuh — fused GEMM epilogues shared by the tcgen05 GEMM (gemm_sm100.cu) and the SIMT
+// GEMM (gemm_simt.cu). A GEMM computes acc[m][n] = sum_k A[m][k] B[n][k] in fp32; the epilogue
+// turns a run of NV consecutive columns of one row into the layer's output:
+//   EPI_STORE : out[m][n] = acc + bias[n]                        (out: T or fp32)
+//   EPI_RESID : out[m][n] = resid[m][n] + acc + bias[n]          (fp32 residual stream, A-23)
+//   EPI_GELU  : U = acc + bias;  out = U (T);  out2 = gelu(U) (T)     (Eq. 3; A-2)
+//   EPI_DGELU : out[m][n] = acc * gelu'(aux[m][n])               (dU from dG and stored U)
+//   EPI_QKV   : v = acc + bias; column n -> (part = n / H, head = (n % H) / d, e = n % d);
+//               part 0 -> q, 1 -> k, 2 -> v, each [a][s][d] at row (row0 + m): the slice's
+//               queries and its K/V appended to the per-layer prefix cache
+//   EPI_ACCUM : out[m][n] += acc                                (fp32 weight-gradient accumulate)
+#pragma once
+#include "dtypes.cuh"
+
+namespace tp {
+
+enum EpiKind : int { EPI_STORE = 0, EPI_RESID = 1, EPI_GELU = 2, EPI_DGELU = 3, EPI_QKV = 4, EPI_ACCUM = 5 };
+
+struct Epi {
+  int kind = EPI_STORE;
+  const float* bias = nullptr;
+  void* out = nullptr;        // STORE/RESID/GELU(U)/DGELU/ACCUM
+  int64_t ldo = 0;
+  int out_f32 = 0;            // STORE: 1 -> fp32 output, 0 -> T output
+  const float* resid = nullptr;
+  int64_t ldr = 0;
+  void* out2 = nullptr;       // GELU: G
+  int64_t ldo2 = 0;
+  const void* aux = nullptr;  // DGELU: U
+  int64_t ld_aux = 0;
+  void* q = nullptr;          // QKV scatter targets, [a][s][d] of the current sequence
+  void* k = nullptr;
+  void* v = nullptr;
+  int s_len = 0, head_dim = 0, hidden = 0, row0 = 0;
+};
+
+__device__ __forceinline__ float gelu_f(float u) {
+  const float c = 0.7978845608028654f;  // sqrt(2/pi)
+  return 0.5f * u * (1.f + tanhf(c * (u + 0.044715f * u * u * u)));
+}
+__device__ __forceinline__ float gelu_grad_f(float u) {
+  const float c = 0.7978845608028654f;
+  const float t = tanhf(c * (u + 0.044715f * u * u * u));
+  return 0.5f * (1.f + t) + 0.5f * u * (1.f - t * t) * c * (1.f + 3.f * 0.044715f * u * u);
+}
+
+// Applies the epilogue to columns [n0, n0+8) of row m; n0 % 8 == 0, caller guarantees m < M and
+// n0 + 8 <= N.
+template <typename T>
+__device__ __forceinline__ void epi_apply8(const Epi& e, int m, int n0, float (&v)[8]) {
+  if (e.kind != EPI_DGELU && e.kind != EPI_ACCUM && e.bias) {
+    float b[8];
+    load8<float>(e.bias + n0, b);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] += b[i];
+  }
+  switch (e.kind) {
+    case EPI_STORE:
+      if (e.out_f32) store8<float>(reinterpret_cast<float*>(e.out) + (int64_t)m * e.ldo + n0, v);
+      else store8<T>(reinterpret_cast<T*>(e.out) + (int64_t)m * e.ldo + n0, v);
+      break;
+    case EPI_RESID: {
+      float r[8];
+      load8<float>(e.resid + (int64_t)m * e.ldr + n0, r);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] += r[i];
+      store8<float>(reinterpret_cast<float*>(e.out) + (int64_t)m * e.ldo + n0, v);
+      break;
+    }
+    case EPI_GELU: {
+      // U is rounded to T first so that G = gelu(U) and gelu'(U) in backward see the same U.
+      float u[8], g[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) u[i] = to_f<T>(from_f<T>(v[i]));
+#pragma unroll
+      for (int i = 0; i < 8; ++i) g[i] = gelu_f(u[i]);
+      store8<T>(reinterpret_cast<T*>(e.out) + (int64_t)m * e.ldo + n0, u);
+      store8<T>(reinterpret_cast<T*>(e.out2) + (int64_t)m * e.ldo2 + n0, g);
+      break;
+    }
+    case EPI_DGELU: {
+      float u[8];
+      load8<T>(reinterpret_cast<const T*>(e.aux) + (int64_t)m * e.ld_aux + n0, u);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] *= gelu_grad_f(u[i]);
+      store8<T>(reinterpret_cast<T*>(e.out) + (int64_t)m * e.ldo + n0, v);
+      break;
+    }
+    case EPI_QKV: {
+      const int part = n0 / e.hidden;
+      const int within = n0 - part * e.hidden;
+      const int head = within / e.head_dim;
+      const int dd = within - head * e.head_dim;
+      T* base = reinterpret_cast<T*>(part == 0 ? e.q : (part == 1 ? e.k : e.v));
+      store8<T>(base + ((int64_t)head * e.s_len + e.row0 + m) * e.head_dim + dd, v);
+      break;
+    }
+    case EPI_ACCUM: {
+      float* o = reinterpret_cast<float*>(e.out) + (int64_t)m * e.ldo + n0;
+      float r[8];
+      load8<float>(o, r);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) r[i] += v[i];
+      store8<float>(o, r);
+      break;
+    }
+  }
+}
+
+}  // namespace tp

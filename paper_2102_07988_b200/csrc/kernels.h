@@ -1,0 +1,65 @@
+// kernels.h — host launchers of every device kernel of the hot path (all asynchronous on `st`).
+// Layout conventions:
+//   token-major activations  X[t][C]  (row t = position c + r of the job's slice), ld = C
+//   per-sequence head-major  Q/K/V[a][s][d]   (the per-layer prefix cache, appended per slice)
+//   fp32 dK/dV accumulators  [a][s][d]
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dtypes.cuh"
+#include "epilogue.cuh"
+
+namespace tp {
+
+struct GemmDesc {
+  int M = 0, N = 0, K = 0;
+  const void* A = nullptr;
+  int64_t lda = 0;
+  bool a_mn = false;  // false: A[m*lda + k];  true: A[k*lda + m]
+  const void* B = nullptr;
+  int64_t ldb = 0;
+  bool b_mn = false;  // false: B[n*ldb + k];  true: B[k*ldb + n]
+};
+
+template <typename T> cudaError_t gemm_simt(const GemmDesc& g, const Epi& e, cudaStream_t st);
+// tcgen05 / TMEM / TMA GEMM for sm_100a, bf16 operands, fp32 accumulation (gemm_sm100.cu).
+cudaError_t gemm_sm100(const GemmDesc& g, const Epi& e, cudaStream_t st);
+bool gemm_sm100_supported(const GemmDesc& g);
+
+template <typename T>
+cudaError_t layernorm_fwd(const float* x, const float* gam, const float* bet, T* y, float* mean,
+                          float* rstd, int rows, int H, cudaStream_t st);
+template <typename T>
+cudaError_t layernorm_bwd(const float* dy, const float* x, const float* mean, const float* rstd,
+                          const float* gam, const float* resid, float* dx_out, T* dx_copy,
+                          float* dgam, float* dbet, int rows, int H, cudaStream_t st);
+
+cudaError_t embed_fwd(const int32_t* tok, const float* wte, const float* wpe, float* h, int c, int l,
+                      int H, int V, cudaStream_t st);
+cudaError_t embed_bwd(const int32_t* tok, const float* dh, float* gwte, float* gwpe, int c, int l,
+                      int H, cudaStream_t st);
+
+template <typename T>
+cudaError_t ce_fwd_bwd(T* logits_inout, const int32_t* targets, float* loss_rows, float* logits_copy,
+                       int rows, int V, float scale, cudaStream_t st);
+cudaError_t sum_rows(const float* x, int n, float* out, cudaStream_t st);
+
+template <typename T>
+cudaError_t attn_fwd_simt(const T* q, const T* k, const T* v, T* o, int64_t ldo, float* lse, int a,
+                          int s, int d, int c, int l, cudaStream_t st);
+template <typename T>
+cudaError_t attn_bwd_simt(const T* dO, int64_t ld_do, const T* o, int64_t ldo, const T* q, const T* k,
+                          const T* v, const float* lse, float* Dvec, T* dq, int64_t ldq, float* dk_acc,
+                          float* dv_acc, int a, int s, int d, int c, int l, cudaStream_t st);
+template <typename T>
+cudaError_t attn_dkv_finalize(const float* dk_acc, const float* dv_acc, T* dqkv, int64_t ld, int a,
+                              int s, int d, int c, int l, cudaStream_t st);
+
+template <typename T> cudaError_t convert_f32(const float* src, T* dst, int64_t n, cudaStream_t st);
+template <typename T>
+cudaError_t transpose_convert(const float* src, T* dst, int R, int C, cudaStream_t st);
+template <typename T>
+cudaError_t colsum_accum(const T* src, int64_t ld, float* out, int rows, int N, cudaStream_t st);
+
+}  // namespace tp

@@ -1,0 +1,884 @@
+// runtime.cu — tp_ctx: stage executor, per-stage op lists and the pipeline schedule of tp_step.
+//
+// Hot path (BASELINE.json:5; §3.2): stage k owns layers [k n/K, (k+1) n/K)
+// (uniform cells) and processes one token slice of one sequence at a time.
+// For every layer it runs the slice's QKV / out-projection / MLP GEMMs, causal attention of the
+// slice's queries against the per-layer prefix K/V cache, and in backward the dK/dV push into
+// the earlier slices' rows. Slice activations go to stage k+1 and gradients return to stage k-1
+// — as device copies in loopback mode (world == 1) or ncclSend/ncclRecv over
+// NVLink (world == K).
+//
+// Schedule (A-21): each stage runs F(d, i) for d = 0..B-1, i = 1..M, then B(d, i) in
+// exact reverse order (GPipe order, store-all); the weight gradients of sequence d
+// are accumulated once its last backward slice B(d, 1) is done (deferred dW, K-dim = s).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <array>
+#include <type_traits>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "kernels.h"
+
+namespace tp {
+
+#define CU(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      return ::tp::fail(TP_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #x, cudaGetErrorString(e_)); \
+  } while (0)
+#define NC(x)                                                                              \
+  do {                                                                                     \
+    ncclResult_t r_ = (x);                                                                 \
+    if (r_ != ncclSuccess)                                                                 \
+      return ::tp::fail(TP_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #x, ncclGetErrorString(r_)); \
+  } while (0)
+#define TRY(x)                      \
+  do {                              \
+    tp_status s_ = (x);             \
+    if (s_ != TP_OK) return s_;     \
+  } while (0)
+
+struct ModelShape {
+  int n_layer, H, a, d, V, s, K;
+};
+
+// Offsets (in floats) of every tensor inside one stage's flat parameter array (include/tp.h).
+struct LayerOff {
+  size_t ln1_g, ln1_b, w_qkv, b_qkv, w_o, b_o, ln2_g, ln2_b, w_1, b_1, w_2, b_2;
+};
+struct StageLayout {
+  size_t wte = 0, wpe = 0, lnf_g = 0, lnf_b = 0, w_out = 0, total = 0;
+  std::vector<LayerOff> layers;
+};
+
+static StageLayout stage_layout(const ModelShape& m, int k) {
+  StageLayout L;
+  size_t o = 0;
+  const size_t H = m.H;
+  if (k == 0) { L.wte = o; o += (size_t)m.V * H; L.wpe = o; o += (size_t)m.s * H; }
+  const int nl = m.n_layer / m.K;
+  for (int j = 0; j < nl; ++j) {
+    LayerOff f;
+    f.ln1_g = o; o += H; f.ln1_b = o; o += H;
+    f.w_qkv = o; o += H * 3 * H; f.b_qkv = o; o += 3 * H;
+    f.w_o = o; o += H * H; f.b_o = o; o += H;
+    f.ln2_g = o; o += H; f.ln2_b = o; o += H;
+    f.w_1 = o; o += H * 4 * H; f.b_1 = o; o += 4 * H;
+    f.w_2 = o; o += 4 * H * H; f.b_2 = o; o += H;
+    L.layers.push_back(f);
+  }
+  if (k == m.K - 1) { L.lnf_g = o; o += H; L.lnf_b = o; o += H; L.w_out = o; o += H * (size_t)m.V; }
+  L.total = o;
+  return L;
+}
+
+// ---------------------------------------------------------------- kernel statistics
+struct KStat {
+  const char* name;
+  int64_t launches = 0;
+  double ms = 0, flops = 0, bytes = 0;
+};
+enum KClass {
+  KC_GEMM_FWD = 0, KC_GEMM_DX, KC_GEMM_DW, KC_ATTN_FWD, KC_ATTN_BWD, KC_LN, KC_EMBED, KC_CE, KC_MISC, KC_COMM, KC_N
+};
+static const char* kKClassNames[KC_N] = {"gemm_fwd", "gemm_dx", "gemm_dw", "attn_fwd", "attn_bwd",
+                                          "layernorm", "embed", "cross_entropy", "misc", "p2p"};
+
+struct Pending {
+  int cls;
+  double flops, bytes;
+  cudaEvent_t a, b;
+};
+
+class Instr {
+ public:
+  bool on = false;
+  int64_t launches = 0;
+  KStat stats[KC_N];
+  std::vector<cudaEvent_t> pool;
+  std::vector<Pending> pending;
+  size_t next = 0;
+  Instr() { for (int i = 0; i < KC_N; ++i) stats[i].name = kKClassNames[i]; }
+  ~Instr() { for (auto e : pool) cudaEventDestroy(e); }
+  cudaEvent_t ev() {
+    if (next == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[next++];
+  }
+  void begin(cudaStream_t st, int cls, double flops, double bytes, Pending& p) {
+    ++launches;
+    if (!on) return;
+    p.cls = cls; p.flops = flops; p.bytes = bytes;
+    p.a = ev(); p.b = ev();
+    cudaEventRecord(p.a, st);
+  }
+  void end(cudaStream_t st, Pending& p) {
+    if (!on) return;
+    cudaEventRecord(p.b, st);
+    pending.push_back(p);
+  }
+  void resolve() {  // after a device sync
+    for (auto& p : pending) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, p.a, p.b);
+      stats[p.cls].launches++;
+      stats[p.cls].ms += ms;
+      stats[p.cls].flops += p.flops;
+      stats[p.cls].bytes += p.bytes;
+    }
+    pending.clear();
+    next = 0;
+  }
+};
+
+// ---------------------------------------------------------------- engine
+struct EngineBase {
+  virtual ~EngineBase() = default;
+  virtual tp_status load(const float* host, size_t n) = 0;
+  virtual tp_status step(const tp_slicing* sl, const int32_t* tokens, bool host_tokens, int batch, float* loss) = 0;
+  virtual tp_status grads(float* host, size_t n) = 0;
+  virtual tp_status logits(float* host, size_t n) = 0;
+  virtual tp_status profile(int g, int reps, int64_t* ticks, double* fit) = 0;
+  virtual size_t param_count() const = 0;
+  Instr instr;
+  cudaStream_t stream = nullptr;
+};
+
+template <typename T>
+struct Stage {
+  int k = 0, nl = 0;
+  StageLayout L;
+  float* pflat = nullptr;  // fp32 params (flat layout)
+  float* gflat = nullptr;  // fp32 grads (flat layout)
+  // GEMM operands in T: *_t = [out][in] (K-major B for fwd), *_io = [in][out] (K-major B for dX)
+  std::vector<T*> wqkv_t, wqkv_io, wo_t, wo_io, w1_t, w1_io, w2_t, w2_io;
+  T *wout_t = nullptr, *wout_io = nullptr;
+  // activations, store-all over [B][s]
+  std::vector<float*> hs;    // nl+1 of [B][s][H] fp32; hs[0] = stage input, hs[nl] = stage output
+  std::vector<float*> hmid;  // [B][s][H] fp32
+  std::vector<T*> A1, A2, O;      // [B][s][H]
+  std::vector<float*> st1, st2;   // [2][B][s] (mean, rstd)
+  std::vector<T*> Q, Kc, Vc;      // [B][a][s][d]
+  std::vector<float*> LSE;        // [B][a][s]
+  std::vector<T*> U, G;           // [B][s][4H]
+  T* Af = nullptr; float* stf = nullptr;
+  T* Z = nullptr;                 // [B][s][V] logits -> dlogits in place
+  float* loss_rows = nullptr;     // [B][s]
+  float* logits_keep = nullptr;   // [B][s][V] (TP_FLAG_KEEP_LOGITS)
+  float* grad_out = nullptr;      // [B][s][H] dloss/d(stage output)
+  float* grad_in = nullptr;       // [B][s][H] dloss/d(stage input)
+  // backward stash of ONE sequence (deferred dW)
+  std::vector<T*> dQKV, dhmid_b, dU, dhout_b;
+  std::vector<float*> dk_acc, dv_acc;  // [a][s][d]
+  float *gA = nullptr, *gB = nullptr, *gm = nullptr, *dA = nullptr, *Dvec = nullptr;
+  T* dO = nullptr;
+};
+
+template <typename T>
+class Engine final : public EngineBase {
+ public:
+  ModelShape m;
+  int rank, world, k0, k1, precision, flags, max_batch, device;
+  bool force_simt;
+  std::vector<Stage<T>> stages;
+  std::vector<void*> allocs;
+  int32_t* d_tokens = nullptr;
+  float* d_loss = nullptr;
+  float* h_loss = nullptr;  // pinned
+  int last_batch = 0;
+  // NCCL (multi-rank)
+  ncclComm_t base = nullptr, commF[2] = {nullptr, nullptr}, commB[2] = {nullptr, nullptr};
+  cudaStream_t s_recv_f = nullptr, s_send_f = nullptr, s_recv_b = nullptr, s_send_b = nullptr;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_next = 0;
+
+  ~Engine() override {
+    if (stream) cudaStreamSynchronize(stream);
+    for (ncclComm_t c : {commF[0], commF[1], commB[0], commB[1], base})
+      if (c) ncclCommDestroy(c);
+    for (void* p : allocs) cudaFree(p);
+    if (h_loss) cudaFreeHost(h_loss);
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    for (cudaStream_t s : {s_recv_f, s_send_f, s_recv_b, s_send_b, stream})
+      if (s) cudaStreamDestroy(s);
+  }
+
+  size_t param_count() const override {
+    size_t n = 0;
+    for (auto& st : stages) n += st.L.total;
+    return n;
+  }
+
+  template <typename U_>
+  tp_status alloc(U_** p, size_t count) {
+    if (count == 0) { *p = nullptr; return TP_OK; }
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, count * sizeof(U_));
+    if (e != cudaSuccess)
+      return fail(TP_ENOMEM, "cudaMalloc(%zu bytes) failed: %s", count * sizeof(U_), cudaGetErrorString(e));
+    allocs.push_back(q);
+    *p = reinterpret_cast<U_*>(q);
+    return TP_OK;
+  }
+
+  cudaEvent_t event() {
+    if (ev_next == ev_pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_next++];
+  }
+
+  tp_status init(const tp_model_cfg* cfg, int rank_, int world_, const void* nccl_id, int precision_,
+                 int max_batch_, int device_, int flags_) {
+    m = {cfg->n_layer, cfg->hidden, cfg->n_head, cfg->hidden / cfg->n_head, cfg->vocab, cfg->seq_len, cfg->n_stages};
+    rank = rank_; world = world_; precision = precision_; flags = flags_; max_batch = max_batch_; device = device_;
+    force_simt = (flags & TP_FLAG_FORCE_SIMT) != 0 || precision == TP_FP32;
+    instr.on = (flags & TP_FLAG_KERNEL_STATS) != 0;
+    if (world == 1) { k0 = 0; k1 = m.K; } else { k0 = rank; k1 = rank + 1; }
+    CU(cudaSetDevice(device));
+    int major = 0;
+    CU(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    if (major != 10) return fail(TP_ECUDA, "device %d has compute capability %d.x; this build targets sm_100a", device, major);
+    int lo = 0, hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, hi));
+    CU(cudaHostAlloc(&h_loss, sizeof(float), cudaHostAllocDefault));
+    TRY(alloc(&d_tokens, (size_t)max_batch * (m.s + 1)));
+    TRY(alloc(&d_loss, 4));
+    stages.resize(k1 - k0);
+    for (int k = k0; k < k1; ++k) TRY(alloc_stage(stages[k - k0], k));
+    if (world > 1) {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof id);
+      NC(ncclCommInitRank(&base, world, id, rank));
+      // one communicator per (direction, edge parity): each rank uses each communicator from
+      // exactly one stream, so p2p ops on a communicator are issued in one order on both ends.
+      for (int i = 0; i < 2; ++i) {
+        NC(ncclCommSplit(base, 0, rank, &commF[i], nullptr));
+        NC(ncclCommSplit(base, 0, rank, &commB[i], nullptr));
+      }
+      CU(cudaStreamCreateWithPriority(&s_recv_f, cudaStreamNonBlocking, hi));
+      CU(cudaStreamCreateWithPriority(&s_send_f, cudaStreamNonBlocking, hi));
+      CU(cudaStreamCreateWithPriority(&s_recv_b, cudaStreamNonBlocking, hi));
+      CU(cudaStreamCreateWithPriority(&s_send_b, cudaStreamNonBlocking, hi));
+    }
+    CU(cudaStreamSynchronize(stream));
+    return TP_OK;
+  }
+
+  tp_status alloc_stage(Stage<T>& S, int k) {
+    S.k = k;
+    S.nl = m.n_layer / m.K;
+    S.L = stage_layout(m, k);
+    const size_t B = max_batch, s = m.s, H = m.H, a = m.a, nl = S.nl;
+    TRY(alloc(&S.pflat, S.L.total));
+    TRY(alloc(&S.gflat, S.L.total));
+    auto vec = [&](auto& v, size_t n, size_t count) -> tp_status {
+      v.resize(n);
+      for (size_t i = 0; i < n; ++i) TRY(alloc(&v[i], count));
+      return TP_OK;
+    };
+    TRY(vec(S.wqkv_t, nl, 3 * H * H)); TRY(vec(S.wqkv_io, nl, 3 * H * H));
+    TRY(vec(S.wo_t, nl, H * H)); TRY(vec(S.wo_io, nl, H * H));
+    TRY(vec(S.w1_t, nl, 4 * H * H)); TRY(vec(S.w1_io, nl, 4 * H * H));
+    TRY(vec(S.w2_t, nl, 4 * H * H)); TRY(vec(S.w2_io, nl, 4 * H * H));
+    const bool first = k == 0, last = k == m.K - 1;
+    if (last) { TRY(alloc(&S.wout_t, H * m.V)); TRY(alloc(&S.wout_io, H * m.V)); }
+    S.hs.assign(nl + 1, nullptr);
+    // loopback: stage k's input buffer IS stage k-1's output buffer (the "send" is free)
+    const bool alias = world == 1 && k > k0;
+    if (alias) S.hs[0] = stages[k - 1 - k0].hs[stages[k - 1 - k0].nl];
+    for (size_t j = alias ? 1 : 0; j <= nl; ++j) TRY(alloc(&S.hs[j], B * s * H));
+    TRY(vec(S.hmid, nl, B * s * H));
+    TRY(vec(S.A1, nl, B * s * H)); TRY(vec(S.A2, nl, B * s * H)); TRY(vec(S.O, nl, B * s * H));
+    TRY(vec(S.st1, nl, 2 * B * s)); TRY(vec(S.st2, nl, 2 * B * s));
+    TRY(vec(S.Q, nl, B * s * H)); TRY(vec(S.Kc, nl, B * s * H)); TRY(vec(S.Vc, nl, B * s * H));
+    TRY(vec(S.LSE, nl, B * a * s));
+    TRY(vec(S.U, nl, B * s * 4 * H)); TRY(vec(S.G, nl, B * s * 4 * H));
+    if (last) {
+      TRY(alloc(&S.Af, B * s * H)); TRY(alloc(&S.stf, 2 * B * s));
+      TRY(alloc(&S.Z, B * s * (size_t)m.V)); TRY(alloc(&S.loss_rows, B * s));
+      if (flags & TP_FLAG_KEEP_LOGITS) TRY(alloc(&S.logits_keep, B * s * (size_t)m.V));
+    }
+    TRY(alloc(&S.grad_out, B * s * H));
+    if (alias) {
+      // stage k-1's grad_out IS stage k's grad_in
+      Stage<T>& P = stages[k - 1 - k0];
+      S.grad_in = P.grad_out;
+    } else {
+      TRY(alloc(&S.grad_in, B * s * H));
+    }
+    (void)first;
+    TRY(vec(S.dQKV, nl, s * 3 * H)); TRY(vec(S.dhmid_b, nl, s * H));
+    TRY(vec(S.dU, nl, s * 4 * H)); TRY(vec(S.dhout_b, nl, s * H));
+    TRY(vec(S.dk_acc, nl, s * H)); TRY(vec(S.dv_acc, nl, s * H));
+    TRY(alloc(&S.gA, s * H)); TRY(alloc(&S.gB, s * H)); TRY(alloc(&S.gm, s * H)); TRY(alloc(&S.dA, s * H));
+    TRY(alloc(&S.Dvec, a * s)); TRY(alloc(&S.dO, s * H));
+    return TP_OK;
+  }
+
+  // ------------------------------------------------------------ parameter load
+  tp_status load(const float* host, size_t n) override {
+    if (n != param_count()) return fail(TP_EINVAL, "tp_load_params: n=%zu, expected %zu", n, param_count());
+    size_t off = 0;
+    for (auto& S : stages) {
+      CU(cudaMemcpyAsync(S.pflat, host + off, S.L.total * sizeof(float), cudaMemcpyHostToDevice, stream));
+      off += S.L.total;
+      const int H = m.H;
+      for (int j = 0; j < S.nl; ++j) {
+        const LayerOff& f = S.L.layers[j];
+        CU(transpose_convert<T>(S.pflat + f.w_qkv, S.wqkv_t[j], H, 3 * H, stream));
+        CU(convert_f32<T>(S.pflat + f.w_qkv, S.wqkv_io[j], (int64_t)H * 3 * H, stream));
+        CU(transpose_convert<T>(S.pflat + f.w_o, S.wo_t[j], H, H, stream));
+        CU(convert_f32<T>(S.pflat + f.w_o, S.wo_io[j], (int64_t)H * H, stream));
+        CU(transpose_convert<T>(S.pflat + f.w_1, S.w1_t[j], H, 4 * H, stream));
+        CU(convert_f32<T>(S.pflat + f.w_1, S.w1_io[j], (int64_t)H * 4 * H, stream));
+        CU(transpose_convert<T>(S.pflat + f.w_2, S.w2_t[j], 4 * H, H, stream));
+        CU(convert_f32<T>(S.pflat + f.w_2, S.w2_io[j], (int64_t)4 * H * H, stream));
+      }
+      if (S.k == m.K - 1) {
+        CU(transpose_convert<T>(S.pflat + S.L.w_out, S.wout_t, H, m.V, stream));
+        CU(convert_f32<T>(S.pflat + S.L.w_out, S.wout_io, (int64_t)H * m.V, stream));
+      }
+    }
+    CU(cudaStreamSynchronize(stream));
+    return TP_OK;
+  }
+
+  // ------------------------------------------------------------ launch helpers
+  tp_status gemm(int cls, const GemmDesc& g, const Epi& e) {
+    Pending p;
+    instr.begin(stream, cls, 2.0 * g.M * g.N * g.K, 0, p);
+    cudaError_t err;
+    if (!force_simt && std::is_same<T, bf16>::value && gemm_sm100_supported(g)) err = gemm_sm100(g, e, stream);
+    else err = gemm_simt<T>(g, e, stream);
+    instr.end(stream, p);
+    if (err != cudaSuccess) return fail(TP_ECUDA, "gemm M=%d N=%d K=%d: %s", g.M, g.N, g.K, cudaGetErrorString(err));
+    return TP_OK;
+  }
+  template <typename F>
+  tp_status launch(int cls, double flops, double bytes, F&& f) {
+    Pending p;
+    instr.begin(stream, cls, flops, bytes, p);
+    cudaError_t err = f();
+    instr.end(stream, p);
+    if (err != cudaSuccess) return fail(TP_ECUDA, "launch (%s): %s", kKClassNames[cls], cudaGetErrorString(err));
+    return TP_OK;
+  }
+  static GemmDesc gd(int M, int N, int K, const void* A, int64_t lda, bool amn, const void* B, int64_t ldb, bool bmn) {
+    GemmDesc g;
+    g.M = M; g.N = N; g.K = K; g.A = A; g.lda = lda; g.a_mn = amn; g.B = B; g.ldb = ldb; g.b_mn = bmn;
+    return g;
+  }
+
+  // ------------------------------------------------------------ forward of one job on one stage
+  tp_status fwd(Stage<T>& S, int d, int c, int l, int batch) {
+    const int H = m.H, s = m.s, a = m.a, dh = m.d, V = m.V;
+    const size_t row = (size_t)d * s + c;  // first row of this job in [B][s] buffers
+    const double ebytes = sizeof(T);
+    if (S.k == 0) {
+      TRY(launch(KC_EMBED, 0, 8.0 * l * H, [&] {
+        return embed_fwd(d_tokens + (size_t)d * (s + 1), S.pflat + S.L.wte, S.pflat + S.L.wpe, S.hs[0] + row * H, c, l, H, V, stream);
+      }));
+    }
+    for (int j = 0; j < S.nl; ++j) {
+      const LayerOff& f = S.L.layers[j];
+      const float* P = S.pflat;
+      float* x = S.hs[j] + row * H;
+      float* st1 = S.st1[j];
+      TRY(launch(KC_LN, 0, (4.0 + ebytes) * l * H, [&] {
+        return layernorm_fwd<T>(x, P + f.ln1_g, P + f.ln1_b, S.A1[j] + row * H, st1 + row, st1 + (size_t)batch * s + row, l, H, stream);
+      }));
+      Epi eq; eq.kind = EPI_QKV; eq.bias = P + f.b_qkv;
+      eq.q = S.Q[j] + (size_t)d * s * H; eq.k = S.Kc[j] + (size_t)d * s * H; eq.v = S.Vc[j] + (size_t)d * s * H;
+      eq.s_len = s; eq.head_dim = dh; eq.hidden = H; eq.row0 = c;
+      TRY(gemm(KC_GEMM_FWD, gd(l, 3 * H, H, S.A1[j] + row * H, H, false, S.wqkv_t[j], H, false), eq));
+      T* o = S.O[j] + row * H;
+      float* lse = S.LSE[j] + (size_t)d * a * s;
+      const double attn_flops = 4.0 * H * ((double)l * c + 0.5 * l * (l + 1.0));
+      TRY(launch(KC_ATTN_FWD, attn_flops, ebytes * (2.0 * H * (c + l) + 2.0 * H * l), [&] {
+        return attn_fwd_simt<T>(S.Q[j] + (size_t)d * s * H, S.Kc[j] + (size_t)d * s * H, S.Vc[j] + (size_t)d * s * H, o, H, lse, a, s, dh, c, l, stream);
+      }));
+      Epi er; er.kind = EPI_RESID; er.bias = P + f.b_o; er.out = S.hmid[j] + row * H; er.ldo = H; er.resid = x; er.ldr = H;
+      TRY(gemm(KC_GEMM_FWD, gd(l, H, H, o, H, false, S.wo_t[j], H, false), er));
+      float* st2 = S.st2[j];
+      TRY(launch(KC_LN, 0, (4.0 + ebytes) * l * H, [&] {
+        return layernorm_fwd<T>(S.hmid[j] + row * H, P + f.ln2_g, P + f.ln2_b, S.A2[j] + row * H, st2 + row, st2 + (size_t)batch * s + row, l, H, stream);
+      }));
+      Epi eg; eg.kind = EPI_GELU; eg.bias = P + f.b_1; eg.out = S.U[j] + row * 4 * H; eg.ldo = 4 * H; eg.out2 = S.G[j] + row * 4 * H; eg.ldo2 = 4 * H;
+      TRY(gemm(KC_GEMM_FWD, gd(l, 4 * H, H, S.A2[j] + row * H, H, false, S.w1_t[j], H, false), eg));
+      Epi e2; e2.kind = EPI_RESID; e2.bias = P + f.b_2; e2.out = S.hs[j + 1] + row * H; e2.ldo = H; e2.resid = S.hmid[j] + row * H; e2.ldr = H;
+      TRY(gemm(KC_GEMM_FWD, gd(l, H, 4 * H, S.G[j] + row * 4 * H, 4 * H, false, S.w2_t[j], 4 * H, false), e2));
+    }
+    if (S.k == m.K - 1) {
+      const float* P = S.pflat;
+      float* x = S.hs[S.nl] + row * H;
+      TRY(launch(KC_LN, 0, (4.0 + ebytes) * l * H, [&] {
+        return layernorm_fwd<T>(x, P + S.L.lnf_g, P + S.L.lnf_b, S.Af + row * H, S.stf + row, S.stf + (size_t)batch * s + row, l, H, stream);
+      }));
+      Epi ez; ez.kind = EPI_STORE; ez.out = S.Z + row * V; ez.ldo = V;
+      TRY(gemm(KC_GEMM_FWD, gd(l, V, H, S.Af + row * H, H, false, S.wout_t, H, false), ez));
+      const float scale = 1.0f / (float)((double)batch * s);
+      float* keep = S.logits_keep ? S.logits_keep + row * V : nullptr;
+      TRY(launch(KC_CE, 0, 2.0 * ebytes * l * V, [&] {
+        return ce_fwd_bwd<T>(S.Z + row * V, d_tokens + (size_t)d * (s + 1) + c + 1, S.loss_rows + row, keep, l, V, scale, stream);
+      }));
+    }
+    return TP_OK;
+  }
+
+  // ------------------------------------------------------------ backward of one job on one stage
+  tp_status bwd(Stage<T>& S, int d, int c, int l, int batch, bool first_bwd_slice) {
+    const int H = m.H, s = m.s, a = m.a, dh = m.d, V = m.V;
+    const size_t row = (size_t)d * s + c;
+    const double ebytes = sizeof(T);
+    float* g = S.grad_out + row * H;  // fp32 gradient at the stage output, rows of this job
+    if (S.k == m.K - 1) {
+      const float* P = S.pflat;
+      Epi e; e.kind = EPI_STORE; e.out = S.dA; e.ldo = H; e.out_f32 = 1;
+      TRY(gemm(KC_GEMM_DX, gd(l, H, V, S.Z + row * V, V, false, S.wout_io, V, false), e));
+      TRY(launch(KC_LN, 0, (12.0 + ebytes) * l * H, [&] {
+        return layernorm_bwd<T>(S.dA, S.hs[S.nl] + row * H, S.stf + row, S.stf + (size_t)batch * s + row, P + S.L.lnf_g, nullptr, g,
+                                S.dhout_b[S.nl - 1] + (size_t)c * H, S.gflat + S.L.lnf_g, S.gflat + S.L.lnf_b, l, H, stream);
+      }));
+    } else {
+      TRY(launch(KC_MISC, 0, (4.0 + ebytes) * l * H, [&] {
+        return convert_f32<T>(g, S.dhout_b[S.nl - 1] + (size_t)c * H, (int64_t)l * H, stream);
+      }));
+    }
+    for (int j = S.nl - 1; j >= 0; --j) {
+      const LayerOff& f = S.L.layers[j];
+      const float* P = S.pflat;
+      float* GR = S.gflat;
+      // FFN: dU = (dh W_2^T) * gelu'(U)
+      Epi e1; e1.kind = EPI_DGELU; e1.out = S.dU[j] + (size_t)c * 4 * H; e1.ldo = 4 * H; e1.aux = S.U[j] + row * 4 * H; e1.ld_aux = 4 * H;
+      TRY(gemm(KC_GEMM_DX, gd(l, 4 * H, H, S.dhout_b[j] + (size_t)c * H, H, false, S.w2_io[j], H, false), e1));
+      Epi e2; e2.kind = EPI_STORE; e2.out = S.dA; e2.ldo = H; e2.out_f32 = 1;
+      TRY(gemm(KC_GEMM_DX, gd(l, H, 4 * H, S.dU[j] + (size_t)c * 4 * H, 4 * H, false, S.w1_io[j], 4 * H, false), e2));
+      float* st2 = S.st2[j];
+      TRY(launch(KC_LN, 0, (16.0 + ebytes) * l * H, [&] {
+        return layernorm_bwd<T>(S.dA, S.hmid[j] + row * H, st2 + row, st2 + (size_t)batch * s + row, P + f.ln2_g, g, S.gm,
+                                S.dhmid_b[j] + (size_t)c * H, GR + f.ln2_g, GR + f.ln2_b, l, H, stream);
+      }));
+      // attention: dO = dh_mid W_o^T, then slice-vs-prefix attention backward with dK/dV push
+      Epi e3; e3.kind = EPI_STORE; e3.out = S.dO; e3.ldo = H;
+      TRY(gemm(KC_GEMM_DX, gd(l, H, H, S.dhmid_b[j] + (size_t)c * H, H, false, S.wo_io[j], H, false), e3));
+      if (first_bwd_slice) {
+        // the last slice is processed first and touches every prefix row: start from zero
+        TRY(launch(KC_MISC, 0, 8.0 * (c + l) * H, [&] {
+          cudaError_t e = cudaMemsetAsync(S.dk_acc[j], 0, sizeof(float) * (size_t)s * H, stream);
+          if (e != cudaSuccess) return e;
+          return cudaMemsetAsync(S.dv_acc[j], 0, sizeof(float) * (size_t)s * H, stream);
+        }));
+      }
+      const double attn_flops = 8.0 * H * ((double)l * c + 0.5 * l * (l + 1.0));
+      T* dq = S.dQKV[j] + (size_t)c * 3 * H;
+      TRY(launch(KC_ATTN_BWD, attn_flops, ebytes * 4.0 * H * (c + l) + 16.0 * H * (c + l), [&] {
+        return attn_bwd_simt<T>(S.dO, H, S.O[j] + row * H, H, S.Q[j] + (size_t)d * s * H, S.Kc[j] + (size_t)d * s * H,
+                                S.Vc[j] + (size_t)d * s * H, S.LSE[j] + (size_t)d * a * s, S.Dvec, dq, 3 * H, S.dk_acc[j],
+                                S.dv_acc[j], a, s, dh, c, l, stream);
+      }));
+      TRY(launch(KC_MISC, 0, (8.0 + 2 * ebytes) * l * H, [&] {
+        return attn_dkv_finalize<T>(S.dk_acc[j], S.dv_acc[j], dq, 3 * H, a, s, dh, c, l, stream);
+      }));
+      Epi e4; e4.kind = EPI_STORE; e4.out = S.dA; e4.ldo = H; e4.out_f32 = 1;
+      TRY(gemm(KC_GEMM_DX, gd(l, H, 3 * H, dq, 3 * H, false, S.wqkv_io[j], 3 * H, false), e4));
+      float* gnext = j == 0 ? S.grad_in + row * H : (g == S.gA ? S.gB : S.gA);
+      T* copy = j == 0 ? nullptr : S.dhout_b[j - 1] + (size_t)c * H;
+      float* st1 = S.st1[j];
+      TRY(launch(KC_LN, 0, (16.0 + ebytes) * l * H, [&] {
+        return layernorm_bwd<T>(S.dA, S.hs[j] + row * H, st1 + row, st1 + (size_t)batch * s + row, P + f.ln1_g, S.gm, gnext, copy,
+                                GR + f.ln1_g, GR + f.ln1_b, l, H, stream);
+      }));
+      g = gnext;
+    }
+    if (S.k == 0) {
+      TRY(launch(KC_EMBED, 0, 12.0 * l * H, [&] {
+        return embed_bwd(d_tokens + (size_t)d * (s + 1), S.grad_in + row * H, S.gflat + S.L.wte, S.gflat + S.L.wpe, c, l, H, stream);
+      }));
+    }
+    return TP_OK;
+  }
+
+  // ------------------------------------------------------------ deferred weight gradients of sequence d
+  tp_status wgrad(Stage<T>& S, int d) {
+    const int H = m.H, s = m.s, V = m.V;
+    const size_t row = (size_t)d * s;
+    float* GR = S.gflat;
+    for (int j = 0; j < S.nl; ++j) {
+      const LayerOff& f = S.L.layers[j];
+      Epi e; e.kind = EPI_ACCUM;
+      e.out = GR + f.w_qkv; e.ldo = 3 * H;
+      TRY(gemm(KC_GEMM_DW, gd(H, 3 * H, s, S.A1[j] + row * H, H, true, S.dQKV[j], 3 * H, true), e));
+      e.out = GR + f.w_o; e.ldo = H;
+      TRY(gemm(KC_GEMM_DW, gd(H, H, s, S.O[j] + row * H, H, true, S.dhmid_b[j], H, true), e));
+      e.out = GR + f.w_1; e.ldo = 4 * H;
+      TRY(gemm(KC_GEMM_DW, gd(H, 4 * H, s, S.A2[j] + row * H, H, true, S.dU[j], 4 * H, true), e));
+      e.out = GR + f.w_2; e.ldo = H;
+      TRY(gemm(KC_GEMM_DW, gd(4 * H, H, s, S.G[j] + row * 4 * H, 4 * H, true, S.dhout_b[j], H, true), e));
+      TRY(launch(KC_MISC, 0, sizeof(T) * 9.0 * s * H, [&] {
+        cudaError_t r = colsum_accum<T>(S.dQKV[j], 3 * H, GR + f.b_qkv, s, 3 * H, stream);
+        if (r == cudaSuccess) r = colsum_accum<T>(S.dhmid_b[j], H, GR + f.b_o, s, H, stream);
+        if (r == cudaSuccess) r = colsum_accum<T>(S.dU[j], 4 * H, GR + f.b_1, s, 4 * H, stream);
+        if (r == cudaSuccess) r = colsum_accum<T>(S.dhout_b[j], H, GR + f.b_2, s, H, stream);
+        return r;
+      }));
+    }
+    if (S.k == m.K - 1) {
+      Epi e; e.kind = EPI_ACCUM; e.out = GR + S.L.w_out; e.ldo = V;
+      TRY(gemm(KC_GEMM_DW, gd(H, V, s, S.Af + row * H, H, true, S.Z + row * V, V, true), e));
+    }
+    return TP_OK;
+  }
+
+  // ------------------------------------------------------------ p2p (multi-rank)
+  tp_status recv_fwd(Stage<T>& S, size_t row, int l) {  // activation from stage k-1
+    cudaEvent_t e = event();
+    Pending p;
+    instr.begin(s_recv_f, KC_COMM, 0, 4.0 * l * m.H, p);
+    NC(ncclRecv(S.hs[0] + row * m.H, (size_t)l * m.H, ncclFloat32, S.k - 1, commF[(S.k - 1) & 1], s_recv_f));
+    instr.end(s_recv_f, p);
+    CU(cudaEventRecord(e, s_recv_f));
+    CU(cudaStreamWaitEvent(stream, e, 0));
+    return TP_OK;
+  }
+  tp_status send_fwd(Stage<T>& S, size_t row, int l) {
+    cudaEvent_t e = event();
+    CU(cudaEventRecord(e, stream));
+    CU(cudaStreamWaitEvent(s_send_f, e, 0));
+    NC(ncclSend(S.hs[S.nl] + row * m.H, (size_t)l * m.H, ncclFloat32, S.k + 1, commF[S.k & 1], s_send_f));
+    return TP_OK;
+  }
+  tp_status recv_bwd(Stage<T>& S, size_t row, int l) {  // gradient from stage k+1
+    cudaEvent_t e = event();
+    NC(ncclRecv(S.grad_out + row * m.H, (size_t)l * m.H, ncclFloat32, S.k + 1, commB[S.k & 1], s_recv_b));
+    CU(cudaEventRecord(e, s_recv_b));
+    CU(cudaStreamWaitEvent(stream, e, 0));
+    return TP_OK;
+  }
+  tp_status send_bwd(Stage<T>& S, size_t row, int l) {
+    cudaEvent_t e = event();
+    CU(cudaEventRecord(e, stream));
+    CU(cudaStreamWaitEvent(s_send_b, e, 0));
+    NC(ncclSend(S.grad_in + row * m.H, (size_t)l * m.H, ncclFloat32, S.k - 1, commB[(S.k - 1) & 1], s_send_b));
+    return TP_OK;
+  }
+
+  // ------------------------------------------------------------ one step
+  tp_status step(const tp_slicing* sl, const int32_t* tokens, bool host_tokens, int batch, float* loss_out) override {
+    if (!sl || !sl->lengths) return fail(TP_EINVAL, "tp_step: null slicing");
+    if (batch < 1 || batch > max_batch) return fail(TP_EINVAL, "tp_step: batch %d not in [1, max_batch=%d]", batch, max_batch);
+    if (sl->batch_slice != 1) return fail(TP_EINVAL, "tp_step: batch_slice %d unsupported (this build runs b = 1)", sl->batch_slice);
+    const int M = sl->n_slices;
+    if (M < 1 || M > m.s) return fail(TP_EINVAL, "tp_step: n_slices %d", M);
+    std::vector<int> off(M + 1, 0);
+    for (int i = 0; i < M; ++i) {
+      if (sl->lengths[i] <= 0) return fail(TP_EINVAL, "tp_step: slice %d has length %d", i, sl->lengths[i]);
+      off[i + 1] = off[i] + sl->lengths[i];
+    }
+    if (off[M] != m.s) return fail(TP_EINVAL, "tp_step: slice lengths sum to %d, seq_len is %d", off[M], m.s);
+    if (!tokens) return fail(TP_EINVAL, "tp_step: null tokens");
+    CU(cudaSetDevice(device));
+    instr.launches = 0;
+    ev_next = 0;
+    last_batch = batch;
+    const size_t ntok = (size_t)batch * (m.s + 1);
+    CU(cudaMemcpyAsync(d_tokens, tokens, ntok * sizeof(int32_t), host_tokens ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, stream));
+    for (auto& S : stages) CU(cudaMemsetAsync(S.gflat, 0, S.L.total * sizeof(float), stream));
+    const bool multi = world > 1;
+    // forward: F(d, i) for d = 0..B-1, i = 1..M (stage order inside a job in loopback)
+    for (int d = 0; d < batch; ++d)
+      for (int i = 0; i < M; ++i)
+        for (auto& S : stages) {
+          const size_t row = (size_t)d * m.s + off[i];
+          if (multi && S.k > 0) TRY(recv_fwd(S, row, sl->lengths[i]));
+          TRY(fwd(S, d, off[i], sl->lengths[i], batch));
+          if (multi && S.k < m.K - 1) TRY(send_fwd(S, row, sl->lengths[i]));
+        }
+    // backward: exact reverse order; deferred dW of sequence d after its slice 1
+    for (int d = batch - 1; d >= 0; --d) {
+      for (int i = M - 1; i >= 0; --i)
+        for (int si = (int)stages.size() - 1; si >= 0; --si) {
+          Stage<T>& S = stages[si];
+          const size_t row = (size_t)d * m.s + off[i];
+          if (multi && S.k < m.K - 1) TRY(recv_bwd(S, row, sl->lengths[i]));
+          TRY(bwd(S, d, off[i], sl->lengths[i], batch, i == M - 1));
+          if (multi && S.k > 0) TRY(send_bwd(S, row, sl->lengths[i]));
+        }
+      for (auto& S : stages) TRY(wgrad(S, d));
+    }
+    // loss: sum of per-token NLL on the last stage, mean over batch*seq_len (A-9)
+    Stage<T>* last = nullptr;
+    for (auto& S : stages) if (S.k == m.K - 1) last = &S;
+    if (last) {
+      TRY(launch(KC_MISC, 0, 4.0 * batch * m.s, [&] { return sum_rows(last->loss_rows, batch * m.s, d_loss, stream); }));
+    } else {
+      CU(cudaMemsetAsync(d_loss, 0, sizeof(float), stream));
+    }
+    if (multi) {
+      // the comm streams must have drained before the step ends
+      for (cudaStream_t cs : {s_send_f, s_recv_f, s_send_b, s_recv_b}) {
+        cudaEvent_t e = event();
+        CU(cudaEventRecord(e, cs));
+        CU(cudaStreamWaitEvent(stream, e, 0));
+      }
+      NC(ncclAllReduce(d_loss, d_loss, 1, ncclFloat32, ncclSum, base, stream));
+    }
+    CU(cudaMemcpyAsync(h_loss, d_loss, sizeof(float), cudaMemcpyDeviceToHost, stream));
+    CU(cudaStreamSynchronize(stream));
+    CU(cudaGetLastError());
+    instr.resolve();
+    if (loss_out) *loss_out = (float)(*h_loss / ((double)batch * m.s));
+    return TP_OK;
+  }
+
+  tp_status grads(float* host, size_t n) override {
+    if (n != param_count()) return fail(TP_EINVAL, "tp_get_grads: n=%zu, expected %zu", n, param_count());
+    size_t off = 0;
+    for (auto& S : stages) {
+      CU(cudaMemcpy(host + off, S.gflat, S.L.total * sizeof(float), cudaMemcpyDeviceToHost));
+      off += S.L.total;
+    }
+    return TP_OK;
+  }
+  tp_status logits(float* host, size_t n) override {
+    Stage<T>* last = nullptr;
+    for (auto& S : stages) if (S.k == m.K - 1) last = &S;
+    if (!last || !last->logits_keep) return fail(TP_ESTATE, "tp_get_logits: needs TP_FLAG_KEEP_LOGITS and the last stage");
+    const size_t need = (size_t)last_batch * m.s * m.V;
+    if (n != need) return fail(TP_EINVAL, "tp_get_logits: n=%zu, expected %zu", n, need);
+    CU(cudaMemcpy(host, last->logits_keep, need * sizeof(float), cudaMemcpyDeviceToHost));
+    return TP_OK;
+  }
+  tp_status profile(int g, int reps, int64_t* ticks, double* fit) override;
+};
+
+// ---------------------------------------------------------------- tp_profile
+// measure t(l, 0) for every l, fit t_ctx(l, c) = a0 + a1 l + a2 c + a3 l c on a
+// subset of (l, c) by least squares, fill the table with t(l, 0) + t_ctx(l, c).
+template <typename T>
+tp_status Engine<T>::profile(int g, int reps, int64_t* ticks, double* fit) {
+  if (g < 1 || m.s % g != 0) return fail(TP_EINVAL, "tp_profile: granularity %d must divide seq_len %d", g, m.s);
+  if (reps < 1) return fail(TP_EINVAL, "tp_profile: reps must be >= 1");
+  if (!ticks) return fail(TP_EINVAL, "tp_profile: null ticks_out");
+  const int n = m.s / g;
+  Stage<T>& S = stages[0];
+  cudaEvent_t e0, e1;
+  CU(cudaEventCreate(&e0));
+  CU(cudaEventCreate(&e1));
+  // tokens for sequence 0 (values do not affect dense cost)
+  CU(cudaMemsetAsync(d_tokens, 0, sizeof(int32_t) * (m.s + 1), stream));
+  auto time_job = [&](int l, int c, double* out_ns) -> tp_status {
+    std::vector<float> v;
+    for (int r = 0; r < reps + 2; ++r) {
+      CU(cudaEventRecord(e0, stream));
+      TRY(fwd(S, 0, c, l, 1));
+      TRY(bwd(S, 0, c, l, 1, true));
+      CU(cudaEventRecord(e1, stream));
+      CU(cudaEventSynchronize(e1));
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, e0, e1));
+      if (r >= 2) v.push_back(ms);
+    }
+    std::sort(v.begin(), v.end());
+    *out_ns = 1e6 * v[v.size() / 2];
+    return TP_OK;
+  };
+  bool saved = instr.on;
+  instr.on = false;
+  std::vector<double> base(n + 1, 0.0);
+  for (int u = 1; u <= n; ++u) TRY(time_job(u * g, 0, &base[u]));
+  // context samples: l in {g * 2^k}, c in {0, s/8, s/4, s/2, s - l}
+  std::vector<std::array<double, 3>> samp;  // (l, c, t_ctx)
+  for (int lu = 1; lu <= n; lu *= 2) {
+    const int l = lu * g;
+    int cs[5] = {0, m.s / 8, m.s / 4, m.s / 2, m.s - l};
+    for (int c : cs) {
+      c = (c / g) * g;
+      if (c < 0 || c + l > m.s) continue;
+      double t;
+      TRY(time_job(l, c, &t));
+      samp.push_back({(double)l, (double)c, t - base[lu]});
+    }
+  }
+  instr.on = saved;
+  CU(cudaEventDestroy(e0));
+  CU(cudaEventDestroy(e1));
+  // least squares for a0..a3 via normal equations (4x4, Gaussian elimination with pivoting)
+  double A[4][5] = {};
+  for (auto& sp : samp) {
+    const double x[4] = {1.0, sp[0], sp[1], sp[0] * sp[1]};
+    for (int i = 0; i < 4; ++i) {
+      for (int j = 0; j < 4; ++j) A[i][j] += x[i] * x[j];
+      A[i][4] += x[i] * sp[2];
+    }
+  }
+  double coef[4] = {0, 0, 0, 0};
+  {
+    int piv[4] = {0, 1, 2, 3};
+    bool ok = true;
+    for (int col = 0; col < 4 && ok; ++col) {
+      int best = col;
+      for (int r = col + 1; r < 4; ++r) if (std::fabs(A[r][col]) > std::fabs(A[best][col])) best = r;
+      if (std::fabs(A[best][col]) < 1e-30) { ok = false; break; }
+      for (int j = 0; j < 5; ++j) std::swap(A[col][j], A[best][j]);
+      for (int r = 0; r < 4; ++r) {
+        if (r == col) continue;
+        const double f = A[r][col] / A[col][col];
+        for (int j = 0; j < 5; ++j) A[r][j] -= f * A[col][j];
+      }
+    }
+    (void)piv;
+    if (ok) for (int i = 0; i < 4; ++i) coef[i] = A[i][4] / A[i][i];
+  }
+  double maxrel = 0.0;
+  for (auto& sp : samp) {
+    const double pred = coef[0] + coef[1] * sp[0] + coef[2] * sp[1] + coef[3] * sp[0] * sp[1];
+    const int lu = (int)sp[0] / g;
+    const double full = base[lu] + sp[2];
+    if (full > 0) maxrel = std::max(maxrel, std::fabs(base[lu] + pred - full) / full);
+  }
+  for (int lu = 1; lu <= n; ++lu)
+    for (int cu = 0; cu + lu <= n; ++cu) {
+      const double l = lu * g, c = cu * g;
+      double t = base[lu] + coef[0] + coef[1] * l + coef[2] * c + coef[3] * l * c;
+      if (cu == 0) t = base[lu];
+      ticks[(size_t)(lu - 1) * (n + 1) + cu] = std::max<int64_t>(1, (int64_t)std::llround(t));
+    }
+  if (fit) { for (int i = 0; i < 4; ++i) fit[i] = coef[i]; fit[4] = maxrel; }
+  return TP_OK;
+}
+
+}  // namespace tp
+
+// ==================================================================== C ABI
+struct tp_ctx {
+  std::unique_ptr<tp::EngineBase> eng;
+};
+
+using namespace tp;
+
+extern "C" tp_status tp_stage_param_count(const tp_model_cfg* cfg, int32_t stage, size_t* out) {
+  TP_CHECK_ARG(cfg && out, "tp_stage_param_count: null argument");
+  TP_CHECK_ARG(cfg->n_stages >= 1 && stage >= 0 && stage < cfg->n_stages, "tp_stage_param_count: bad stage");
+  TP_CHECK_ARG(cfg->n_layer % cfg->n_stages == 0, "n_layer %% n_stages != 0");
+  ModelShape m{cfg->n_layer, cfg->hidden, cfg->n_head, cfg->n_head ? cfg->hidden / cfg->n_head : 0,
+               cfg->vocab, cfg->seq_len, cfg->n_stages};
+  *out = stage_layout(m, stage).total;
+  return TP_OK;
+}
+
+extern "C" tp_status tp_nccl_unique_id(void* out128) {
+  TP_CHECK_ARG(out128, "tp_nccl_unique_id: null");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(TP_ENCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out128, &id, sizeof id);
+  return TP_OK;
+}
+
+extern "C" tp_status tp_init(const tp_model_cfg* cfg, int32_t rank, int32_t world, const void* nccl_id,
+                             int32_t precision, int32_t max_batch, int32_t device, int32_t flags, tp_ctx** out) {
+  TP_CHECK_ARG(cfg && out, "tp_init: null argument");
+  *out = nullptr;
+  TP_CHECK_ARG(cfg->n_layer >= 1 && cfg->n_stages >= 1 && cfg->n_layer % cfg->n_stages == 0,
+               "tp_init: n_layer (%d) must be a positive multiple of n_stages (%d)", cfg->n_layer, cfg->n_stages);
+  TP_CHECK_ARG(cfg->n_head >= 1 && cfg->hidden % cfg->n_head == 0, "tp_init: hidden %% n_head != 0");
+  const int d = cfg->hidden / cfg->n_head;
+  TP_CHECK_ARG(d % 16 == 0 && d <= 128, "tp_init: head_dim %d must be a multiple of 16 and <= 128", d);
+  TP_CHECK_ARG(cfg->hidden % 64 == 0, "tp_init: hidden %d must be a multiple of 64", cfg->hidden);
+  TP_CHECK_ARG(cfg->vocab >= 1 && cfg->vocab % 8 == 0, "tp_init: vocab %d must be a positive multiple of 8", cfg->vocab);
+  TP_CHECK_ARG(cfg->seq_len >= 1, "tp_init: seq_len must be >= 1");
+  TP_CHECK_ARG(world == 1 || world == cfg->n_stages, "tp_init: world (%d) must be 1 (loopback) or n_stages (%d)", world, cfg->n_stages);
+  TP_CHECK_ARG(rank >= 0 && rank < world, "tp_init: rank %d not in [0, %d)", rank, world);
+  TP_CHECK_ARG(world == 1 || nccl_id, "tp_init: nccl_id required for world > 1");
+  TP_CHECK_ARG(precision == TP_BF16 || precision == TP_FP32, "tp_init: bad precision %d", precision);
+  TP_CHECK_ARG(max_batch >= 1, "tp_init: max_batch must be >= 1");
+  auto ctx = std::make_unique<tp_ctx>();
+  tp_status st;
+  if (precision == TP_BF16) {
+    auto e = std::make_unique<Engine<bf16>>();
+    st = e->init(cfg, rank, world, nccl_id, precision, max_batch, device, flags);
+    ctx->eng = std::move(e);
+  } else {
+    auto e = std::make_unique<Engine<float>>();
+    st = e->init(cfg, rank, world, nccl_id, precision, max_batch, device, flags);
+    ctx->eng = std::move(e);
+  }
+  if (st != TP_OK) return st;
+  *out = ctx.release();
+  return TP_OK;
+}
+
+extern "C" tp_status tp_param_count(const tp_ctx* ctx, size_t* out) {
+  TP_CHECK_ARG(ctx && out, "tp_param_count: null argument");
+  *out = ctx->eng->param_count();
+  return TP_OK;
+}
+extern "C" tp_status tp_load_params(tp_ctx* ctx, const float* host, size_t n) {
+  TP_CHECK_ARG(ctx && host, "tp_load_params: null argument");
+  return ctx->eng->load(host, n);
+}
+extern "C" tp_status tp_step(tp_ctx* ctx, const tp_slicing* sl, const int32_t* tokens, int32_t batch, float* loss) {
+  TP_CHECK_ARG(ctx, "tp_step: null ctx");
+  return ctx->eng->step(sl, tokens, true, batch, loss);
+}
+extern "C" tp_status tp_step_device(tp_ctx* ctx, const tp_slicing* sl, const int32_t* tokens, int32_t batch, float* loss) {
+  TP_CHECK_ARG(ctx, "tp_step_device: null ctx");
+  return ctx->eng->step(sl, tokens, false, batch, loss);
+}
+extern "C" tp_status tp_get_grads(tp_ctx* ctx, float* host, size_t n) {
+  TP_CHECK_ARG(ctx && host, "tp_get_grads: null argument");
+  return ctx->eng->grads(host, n);
+}
+extern "C" tp_status tp_get_logits(tp_ctx* ctx, float* host, size_t n) {
+  TP_CHECK_ARG(ctx && host, "tp_get_logits: null argument");
+  return ctx->eng->logits(host, n);
+}
+extern "C" tp_status tp_profile(tp_ctx* ctx, int32_t g, int32_t reps, int64_t* ticks, double* fit) {
+  TP_CHECK_ARG(ctx, "tp_profile: null ctx");
+  return ctx->eng->profile(g, reps, ticks, fit);
+}
+extern "C" tp_status tp_get_stream(tp_ctx* ctx, void** out) {
+  TP_CHECK_ARG(ctx && out, "tp_get_stream: null argument");
+  *out = (void*)ctx->eng->stream;
+  return TP_OK;
+}
+extern "C" tp_status tp_kernel_stats(tp_ctx* ctx, int32_t i, char* name32, int64_t* launches, double* ms,
+                                     double* flops, double* bytes, int32_t* n_classes) {
+  TP_CHECK_ARG(ctx, "tp_kernel_stats: null ctx");
+  if (n_classes) *n_classes = KC_N;
+  if (i < 0 || i >= KC_N) return i == -1 ? TP_OK : fail(TP_EINVAL, "tp_kernel_stats: class %d", i);
+  const KStat& s = ctx->eng->instr.stats[i];
+  if (name32) { std::strncpy(name32, s.name, 31); name32[31] = 0; }
+  if (launches) *launches = s.launches;
+  if (ms) *ms = s.ms;
+  if (flops) *flops = s.flops;
+  if (bytes) *bytes = s.bytes;
+  return TP_OK;
+}
+extern "C" tp_status tp_kernel_stats_reset(tp_ctx* ctx) {
+  TP_CHECK_ARG(ctx, "tp_kernel_stats_reset: null ctx");
+  for (auto& s : ctx->eng->instr.stats) { s.launches = 0; s.ms = s.flops = s.bytes = 0; }
+  return TP_OK;
+}
+extern "C" tp_status tp_last_step_launches(tp_ctx* ctx, int64_t* out) {
+  TP_CHECK_ARG(ctx && out, "tp_last_step_launches: null argument");
+  *out = ctx->eng->instr.launches;
+  return TP_OK;
+}
+extern "C" void tp_destroy(tp_ctx* ctx) { delete ctx; }

@@ -1,0 +1,135 @@
+"""C ABI on the CPU host: libtp.so loads, exports every symbol include/tp.h declares, validates
+arguments, and tp_plan (host-only) equals the oracle's brute force bit-exactly (BASELINE.json:5
+invariant (b)). No GPU compute is called here."""
+import os
+import re
+import subprocess
+import time
+
+import numpy as np
+import pytest
+
+import paper_2102_07988_b200 as tp
+from oracle import plan as op
+from synth import CONFIGS, ModelCfg, gpu_like_table, random_int_table, stage_param_count
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "tp.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:tp_status|void|const char\*)\s+(tp_\w+)\s*\(", src, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    syms = declared_symbols()
+    assert len(syms) >= 15
+    out = subprocess.run(["nm", "-D", "--defined-only", tp.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r" T (tp_\w+)$", out, re.M))
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    assert sorted(tp.EXPORTED) == syms
+    for s in syms:
+        getattr(tp.lib(), s)
+
+
+def test_stage_param_count_matches_layout():
+    for name in ("tiny", "gpt3-1b", "gpt3-13b", "small"):
+        cfg, _ = CONFIGS[name]
+        for k in range(cfg.n_stages):
+            assert tp.stage_param_count(cfg, k) == stage_param_count(cfg, k)
+
+
+def test_init_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    cfg, _ = CONFIGS["tiny"]
+    with pytest.raises(tp.TpError) as e:
+        tp.Context(cfg)
+    assert e.value.status == tp.TP_ECUDA
+
+
+def test_init_rejects_bad_shapes():
+    with pytest.raises(tp.TpError) as e:
+        tp.Context(ModelCfg(3, 64, 4, 128, 32, 2))       # n_layer % n_stages
+    assert e.value.status == tp.TP_EINVAL
+    with pytest.raises(tp.TpError) as e:
+        tp.Context(ModelCfg(2, 96, 4, 128, 32, 1))       # head_dim 24 not a multiple of 16
+    assert e.value.status == tp.TP_EINVAL
+
+
+def _plan(t, n, K, D=1, eps=0, g=1):
+    return tp.plan(t, g, n_layer=K, hidden=64, seq_len=n * g, n_stages=K, n_micro=D, eps_ticks=eps)
+
+
+def test_plan_spec_examples():
+    t = np.zeros((3, 4), np.int64)
+    for l in range(1, 4):
+        for c in range(0, 4 - l):
+            t[l - 1, c] = l
+    s = _plan(t, 3, 2)
+    assert s.lengths == [1, 1, 1] and s.predicted == 4
+    t2 = t + (t > 0)
+    s = _plan(t2, 3, 3)
+    assert s.lengths == [1, 1, 1] and s.predicted == 10
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_plan_bit_exact_vs_brute_force(seed):
+    rng = np.random.default_rng(1000 + seed)
+    for _ in range(40):
+        n = int(rng.integers(1, 13))
+        K = int(rng.integers(1, 5))
+        D = int(rng.choice([1, 2, 8]))
+        t = random_int_table(n, rng, 1, int(rng.choice([3, 12, 10 ** 6])))
+        T, m, lens = op.brute_force(t, n, K, D)
+        s = _plan(t, n, K, D)
+        assert (s.predicted, s.t_max, s.lengths) == (T, m, lens)
+
+
+def test_plan_matches_oracle_dp_with_eps_and_threads(monkeypatch):
+    rng = np.random.default_rng(9)
+    for n in (16, 40):
+        t = gpu_like_table(n, rng)
+        for K in (2, 8):
+            for eps in (0, 20_000):
+                T, m, lens = op.optimize(t, n, K, 1, eps)
+                s = tp.plan(t, 8, n_layer=K, hidden=64, seq_len=8 * n, n_stages=K, eps_ticks=eps)
+                assert s.lengths == [8 * x for x in lens] and s.predicted == T and s.t_max == m
+
+
+def test_plan_rejects_bad_tables():
+    t = np.ones((4, 5), np.int64)
+    t[1, 2] = 0
+    with pytest.raises(tp.TpError) as e:
+        _plan(t, 4, 2)
+    assert e.value.status == tp.TP_EINVAL
+    with pytest.raises(tp.TpError):
+        tp.plan(np.ones((4, 5), np.int64), 4, n_layer=2, hidden=64, seq_len=12, n_stages=2)  # n_units mismatch
+
+
+def test_plan_s2048_g8_within_a_minute():
+    """PAPER.md:290 'the dynamic programming can finish within a minute' — s = 2048, g = 8, exact."""
+    rng = np.random.default_rng(2048)
+    t = gpu_like_table(256, rng, knee=32, base_ns=1_500_000, per_unit_ns=45_000, ctx_ns=2_000)
+    t0 = time.time()
+    s = tp.plan(t, 8, n_layer=40, hidden=5120, seq_len=2048, n_stages=8, n_micro=8)
+    assert time.time() - t0 < 60
+    assert sum(s.lengths) == 2048
+
+
+@pytest.mark.slow
+def test_plan_tiny_config_vs_2pow31_brute_force():
+    """Tiny config (BASELINE.json:7): s = 32, g = 1, K = 2, D = 1 against all 2^31 compositions."""
+    bf = os.path.join(ROOT, "oracle", "bf_compositions")
+    if not os.path.exists(bf):
+        subprocess.run(["gcc", "-O2", "-fopenmp", "-o", bf, bf + ".c"], check=True)
+    rng = np.random.default_rng(31)
+    for trial in range(2):
+        t = gpu_like_table(32, rng, knee=4, base_ns=10_000, per_unit_ns=900, ctx_ns=300) if trial == 0 \
+            else random_int_table(32, rng, 1, 40)
+        inp = "32 2 1\n" + " ".join(str(int(v)) for v in t.reshape(-1))
+        out = [int(x) for x in subprocess.run([bf], input=inp, capture_output=True, text=True, check=True).stdout.split()]
+        s = _plan(t, 32, 2)
+        assert (s.predicted, s.t_max, s.lengths) == (out[0], out[1], out[3:3 + out[2]])

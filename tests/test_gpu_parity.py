@@ -1,0 +1,85 @@
+"""GPU parity: tp_step (token-sliced, pipelined over K stages) against the fp64 oracle's unsliced
+forward/backward — invariant (a) of BASELINE.json:5 — within 2e-2 (bf16) / 1e-4 (fp32) per-tensor
+relative L2 (A-23), on seeded random weights and tokens, for many slicings including
+[s], [1]*s, ragged and paper-shaped (non-monotone) ones. All calls go through the C ABI."""
+import numpy as np
+import pytest
+
+import paper_2102_07988_b200 as tp
+from synth import CONFIGS, ModelCfg
+from tests.gpu_util import gpu_run, oracle_run, rel, worst_errors
+
+pytestmark = pytest.mark.gpu
+
+TINY, _ = CONFIGS["tiny"]
+SMALL, SMALL_B = CONFIGS["small"]
+TINY_SLICINGS = [[32], [1] * 32, [5, 9, 2, 16], [16, 8, 8], [3, 29], [8, 8, 8, 8]]
+
+
+def check(errs, tol):
+    bad = {k: v for k, v in errs.items() if not v < tol}
+    assert not bad, (bad, max(errs.values()))
+
+
+@pytest.mark.parametrize("lengths", TINY_SLICINGS)
+def test_tiny_fp32(lengths):
+    params, tokens, ref = oracle_run(TINY, 1, 0, False)
+    loss, logits, grads, _ = gpu_run(TINY, 1, params, tokens, lengths, tp.TP_FP32)
+    check(worst_errors(loss, logits, grads, ref), 1e-4)
+
+
+@pytest.mark.parametrize("lengths", TINY_SLICINGS)
+def test_tiny_bf16(lengths):
+    params, tokens, ref = oracle_run(TINY, 1, 0, True)
+    loss, logits, grads, launches = gpu_run(TINY, 1, params, tokens, lengths, tp.TP_BF16)
+    assert launches > 0
+    check(worst_errors(loss, logits, grads, ref), 2e-2)
+
+
+@pytest.mark.parametrize("K", [1, 2, 4])
+def test_small_bf16_stages(K):
+    cfg = SMALL.with_(n_stages=K)
+    params, tokens, ref = oracle_run(cfg, SMALL_B, 3, True)
+    loss, logits, grads, _ = gpu_run(cfg, SMALL_B, params, tokens, [40, 24, 64], tp.TP_BF16)
+    check(worst_errors(loss, logits, grads, ref), 2e-2)
+
+
+def test_small_fp32_batch2():
+    params, tokens, ref = oracle_run(SMALL, SMALL_B, 4, False)
+    loss, logits, grads, _ = gpu_run(SMALL, SMALL_B, params, tokens, [8, 56, 8, 56], tp.TP_FP32)
+    check(worst_errors(loss, logits, grads, ref), 1e-4)
+
+
+def test_fp32_sliced_equals_unsliced_on_gpu():
+    params, tokens, _ = oracle_run(SMALL, SMALL_B, 5, False)
+    a = gpu_run(SMALL, SMALL_B, params, tokens, [128], tp.TP_FP32)
+    b = gpu_run(SMALL, SMALL_B, params, tokens, [8] * 16, tp.TP_FP32)
+    assert abs(a[0] - b[0]) < 1e-6 * abs(a[0])
+    assert rel(b[1], a[1]) < 1e-5
+    for k in a[2]:
+        assert rel(b[2][k], a[2][k]) < 1e-5, k
+
+
+def test_bf16_default_vs_force_simt():
+    """The tensor-core kernels against the independent SIMT kernels on identical inputs."""
+    params, tokens, ref = oracle_run(SMALL, SMALL_B, 6, True)
+    a = gpu_run(SMALL, SMALL_B, params, tokens, [72, 56], tp.TP_BF16)
+    b = gpu_run(SMALL, SMALL_B, params, tokens, [72, 56], tp.TP_BF16, tp.TP_FLAG_KEEP_LOGITS | tp.TP_FLAG_FORCE_SIMT)
+    check(worst_errors(*a[:3], ref), 2e-2)
+    check(worst_errors(*b[:3], ref), 2e-2)
+
+
+def test_parity_mid_13b_width():
+    """SURVEY.md §8(c) parity-mid: 2 layers at the real 13B width (H=5120, a=40, d=128), s=512,
+    unaligned slice offsets."""
+    cfg, B = CONFIGS["parity-mid"]
+    params, tokens, ref = oracle_run(cfg, B, 7, True)
+    loss, logits, grads, _ = gpu_run(cfg, B, params, tokens, [200, 136, 104, 72], tp.TP_BF16)
+    check(worst_errors(loss, logits, grads, ref), 2e-2)
+
+
+def test_rejects_bad_slicing():
+    params, tokens, _ = oracle_run(TINY, 1, 0, True)
+    with pytest.raises(tp.TpError) as e:
+        gpu_run(TINY, 1, params, tokens, [16, 8], tp.TP_BF16)
+    assert e.value.status == tp.TP_EINVAL
