@@ -21,6 +21,7 @@ EXPORTED = ["tp_plan", "tp_stage_param_count", "tp_nccl_unique_id", "tp_init", "
             "tp_load_params", "tp_step", "tp_step_device", "tp_get_grads", "tp_get_logits",
             "tp_profile", "tp_get_stream", "tp_kernel_stats", "tp_kernel_stats_reset",
             "tp_last_step_launches", "tp_destroy", "tp_last_error"]
+KEXPORTED = ["tpk_gemm", "tpk_attention_fwd", "tpk_attention_bwd"]
 
 
 class TpError(RuntimeError):
@@ -71,6 +72,12 @@ def _load() -> C.CDLL:
         "tp_kernel_stats_reset": (C.c_int, [P]),
         "tp_last_step_launches": (C.c_int, [P, C.POINTER(C.c_int64)]),
         "tp_destroy": (None, [P]),
+        "tpk_gemm": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, P, C.c_int64, C.c_int32, P, C.c_int64, C.c_int32,
+                               P, C.c_int64, C.c_int32, P]),
+        "tpk_attention_fwd": (C.c_int, [P, P, P, P, P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                        C.c_int32, P]),
+        "tpk_attention_bwd": (C.c_int, [P, P, P, P, P, P, P, C.c_int64, P, P, C.c_int32, C.c_int32, C.c_int32,
+                                        C.c_int32, C.c_int32, C.c_int32, C.c_int32, P]),
         "tp_last_error": (C.c_char_p, []),
     }
     for name, (res, args) in sigs.items():
@@ -228,3 +235,17 @@ class Context:
         n = C.c_int64()
         _check(_lib.tp_last_step_launches(self._h, C.byref(n)))
         return n.value
+
+
+# ---------------------------------------------------------------- kernel-level entry points (tp_kernels.h)
+def k_gemm(M, N, K, A_ptr, lda, a_mn, B_ptr, ldb, b_mn, out_ptr, ldo, impl=0, stream=0):
+    _check(_lib.tpk_gemm(M, N, K, A_ptr, lda, int(a_mn), B_ptr, ldb, int(b_mn), out_ptr, ldo, impl, stream))
+
+
+def k_attention_fwd(q, k, v, o, lse, a, s, d, c, l, impl=0, stream=0):
+    _check(_lib.tpk_attention_fwd(q, k, v, o, lse, a, s, d, c, l, impl, stream))
+
+
+def k_attention_bwd(dO, o, q, k, v, lse, dq, ldq, dk_acc, dv_acc, a, s, d, c, l, accumulate, impl=0, stream=0):
+    _check(_lib.tpk_attention_bwd(dO, o, q, k, v, lse, dq, ldq, dk_acc, dv_acc, a, s, d, c, l, accumulate, impl,
+                                  stream))

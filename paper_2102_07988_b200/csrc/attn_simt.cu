@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(WARPS * 32) attn_bwd_dkv_kernel(const T* __res
                                                                   const T* __restrict__ q, const T* __restrict__ k,
                                                                   const T* __restrict__ v, const float* __restrict__ lse,
                                                                   const float* __restrict__ Dvec, float* __restrict__ dk_acc,
-                                                                  float* __restrict__ dv_acc, int s, int d, int c, int l) {
+                                                                  float* __restrict__ dv_acc, int s, int d, int c, int l,
+                                                                  int accumulate) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int j = blockIdx.x * WARPS + w, head = blockIdx.y;
   if (j >= c + l) return;
@@ -128,7 +129,10 @@ __global__ void __launch_bounds__(WARPS * 32) attn_bwd_dkv_kernel(const T* __res
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int e = lane + 32 * i;
-    if (e < d) { dkr[e] += dk[i] * scale; dvr[e] += dv[i]; }
+    if (e < d) {
+      if (accumulate) { dkr[e] += dk[i] * scale; dvr[e] += dv[i]; }
+      else { dkr[e] = dk[i] * scale; dvr[e] = dv[i]; }
+    }
   }
 }
 
@@ -158,12 +162,12 @@ cudaError_t attn_fwd_simt(const T* q, const T* k, const T* v, T* o, int64_t ldo,
 template <typename T>
 cudaError_t attn_bwd_simt(const T* dO, int64_t ld_do, const T* o, int64_t ldo, const T* q, const T* k, const T* v,
                           const float* lse, float* Dvec, T* dq, int64_t ldq, float* dk_acc, float* dv_acc, int a,
-                          int s, int d, int c, int l, cudaStream_t st) {
+                          int s, int d, int c, int l, int accumulate, cudaStream_t st) {
   if (l == 0) return cudaSuccess;
   dim3 g1((l + WARPS - 1) / WARPS, a);
   attn_bwd_dq_kernel<T><<<g1, WARPS * 32, 0, st>>>(dO, ld_do, o, ldo, q, k, v, lse, Dvec, dq, ldq, s, d, c, l);
   dim3 g2((c + l + WARPS - 1) / WARPS, a);
-  attn_bwd_dkv_kernel<T><<<g2, WARPS * 32, 0, st>>>(dO, ld_do, q, k, v, lse, Dvec, dk_acc, dv_acc, s, d, c, l);
+  attn_bwd_dkv_kernel<T><<<g2, WARPS * 32, 0, st>>>(dO, ld_do, q, k, v, lse, Dvec, dk_acc, dv_acc, s, d, c, l, accumulate);
   return cudaGetLastError();
 }
 
@@ -179,7 +183,7 @@ cudaError_t attn_dkv_finalize(const float* dk_acc, const float* dv_acc, T* dqkv,
   template cudaError_t attn_fwd_simt<T>(const T*, const T*, const T*, T*, int64_t, float*, int, int, int, int, int, \
                                         cudaStream_t);                                                          \
   template cudaError_t attn_bwd_simt<T>(const T*, int64_t, const T*, int64_t, const T*, const T*, const T*,         \
-                                        const float*, float*, T*, int64_t, float*, float*, int, int, int, int, int, \
+                                        const float*, float*, T*, int64_t, float*, float*, int, int, int, int, int, int, \
                                         cudaStream_t);                                                          \
   template cudaError_t attn_dkv_finalize<T>(const float*, const float*, T*, int64_t, int, int, int, int, int,       \
                                             cudaStream_t);

@@ -1,6 +1,316 @@
-// gemm_sm100.cu — placeholder until the tcgen05 kernel lands (returns "unsupported").
+// gemm_sm100.cu — the dense contractions of the hot path on 5th-generation tensor cores.
+//
+//   acc[m][n] = sum_k A(m, k) B(n, k)   (bf16 operands, fp32 accumulation in TMEM)
+//
+// Every projection of a TeraPipe job is one of these: forward QKV / out-proj /
+// FC1 / FC2 / LM head with M = slice tokens, their dX counterparts, and the deferred per-sequence
+// weight gradients (K = seq_len, both operands MN-major). The fused epilogues (bias, GeLU,
+// residual, Q/K/V scatter into the prefix cache, fp32 accumulate) are in epilogue.cuh.
+//
+// Design (sm_100a):
+//   * persistent CTAs (grid = min(tiles, #SMs)), 128 x BN output tiles (BN = 256 or 128),
+//     tile order m-fastest so the weight tile is reused from L2 by consecutive CTAs;
+//   * warp-specialised: warp 0 = TMA producer (one thread), warp 1 = tcgen05.mma issuer (one
+//     thread), warps 2..5 = epilogue (TMEM -> registers -> fused epilogue -> global);
+//   * operands staged by TMA (cp.async.bulk.tensor, 128-byte swizzle) into an NS-deep mbarrier
+//     ring; K-major operands are one box per stage, MN-major operands (dW) are 64-wide boxes placed
+//     at LBO = 8 KiB steps, described to the tensor core with the canonical SW128 layouts;
+//   * the accumulator is double-buffered in TMEM (2 x BN fp32 columns of the 512) so the epilogue
+//     of tile t overlaps the MMAs of tile t+1.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "kernels.h"
+
 namespace tp {
-bool gemm_sm100_supported(const GemmDesc&) { return false; }
-cudaError_t gemm_sm100(const GemmDesc&, const Epi&, cudaStream_t) { return cudaErrorNotSupported; }
+
+namespace {
+
+constexpr int BM = 128, BK = 64;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// Shared-memory matrix descriptor (tcgen05 "version 1"), 128-byte swizzle.
+__device__ __forceinline__ uint64_t make_desc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;  // version
+  d |= 2ull << 61;  // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int BN>
+struct Cfg {
+  static constexpr int NS = BN == 256 ? 4 : 6;  // pipeline depth
+  static constexpr uint32_t A_BYTES = BM * BK * 2;
+  static constexpr uint32_t B_BYTES = BN * BK * 2;
+  static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
+  static constexpr uint32_t SMEM = NS * STAGE + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;  // double-buffered fp32 accumulator
+};
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(192, 1)
+    gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                      int K, Epi epi) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::NS * C::STAGE);
+  uint64_t* empty = full + C::NS;
+  uint64_t* tfull = empty + C::NS;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m_tiles = (M + BM - 1) / BM, n_tiles = (N + BN - 1) / BN;
+  const int tiles = m_tiles * n_tiles, kbs = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::NS; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, 128); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      const int m0 = (tile % m_tiles) * BM, n0 = (tile / m_tiles) * BN;
+      for (int kb = 0; kb < kbs; ++kb) {
+        mbar_wait(empty + stage, phase ^ 1);
+        mbar_expect_tx(full + stage, C::STAGE);
+        uint8_t* a_dst = smem + stage * C::STAGE;
+        uint8_t* b_dst = a_dst + C::A_BYTES;
+        if (!A_MN) tma_load_2d(a_dst, &tmA, kb * BK, m0, full + stage);
+        else
+#pragma unroll
+          for (int i = 0; i < BM / 64; ++i) tma_load_2d(a_dst + i * 8192, &tmA, m0 + i * 64, kb * BK, full + stage);
+        if (!B_MN) tma_load_2d(b_dst, &tmB, kb * BK, n0, full + stage);
+        else
+#pragma unroll
+          for (int i = 0; i < BN / 64; ++i) tma_load_2d(b_dst + i * 8192, &tmB, n0 + i * 64, kb * BK, full + stage);
+        if (++stage == C::NS) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer (one thread issues for the whole CTA)
+    const uint32_t idesc = (1u << 4)                       // D = fp32
+                           | (1u << 7) | (1u << 10)        // A, B = bf16
+                           | ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16)
+                           | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      mbar_wait(tempty + acc, acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < kbs; ++kb) {
+        mbar_wait(full + stage, phase);
+        tc_fence_after();
+        const uint32_t a_base = smem_u32(smem + stage * C::STAGE);
+        const uint32_t b_base = a_base + C::A_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          const uint64_t ad = A_MN ? make_desc(a_base + k * 2048, 8192, 1024) : make_desc(a_base + k * 32, 16, 1024);
+          const uint64_t bd = B_MN ? make_desc(b_base + k * 2048, 8192, 1024) : make_desc(b_base + k * 32, 16, 1024);
+          mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+        }
+        mma_commit(empty + stage);  // frees the smem slot once these MMAs have read it
+        if (++stage == C::NS) { stage = 0; phase ^= 1; }
+      }
+      mma_commit(tfull + acc);      // accumulator ready for the epilogue
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  } else if (warp >= 2) {
+    // ---------------- epilogue: TMEM lanes (warp % 4) * 32 .. +31 = tile rows
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      const int m0 = (tile % m_tiles) * BM, n0 = (tile / m_tiles) * BN;
+      mbar_wait(tfull + acc, acc_phase);
+      tc_fence_after();
+      const int row = m0 + q * 32 + lane;
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 32, r);
+        if (row < M) {
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const int n = n0 + ch * 32 + g * 8;
+            if (n < N) {
+              float v[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[g * 8 + i]);
+              epi_apply8<bf16>(epi, row, n, v);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty + acc);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+int g_num_sms = 0;
+std::once_flag g_once;
+
+void init_once() {
+  std::call_once(g_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  });
+}
+
+// 2-D bf16 tensor map: inner dimension `inner` (contiguous), `outer` rows of stride ld elements.
+bool make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+              uint32_t box_outer) {
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
+  using C = Cfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t r = cudaFuncSetAttribute(gemm_sm100_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)C::SMEM);
+    if (r != cudaSuccess) return r;
+    attr_set = true;
+  }
+  CUtensorMap ta, tb;
+  bool ok = A_MN ? make_map(&ta, g.A, g.M, g.K, g.lda, 64, 64) : make_map(&ta, g.A, g.K, g.M, g.lda, 64, BM);
+  ok = ok && (B_MN ? make_map(&tb, g.B, g.N, g.K, g.ldb, 64, 64) : make_map(&tb, g.B, g.K, g.N, g.ldb, 64, BN));
+  if (!ok) return cudaErrorInvalidValue;
+  const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+  const int grid = std::min(tiles, g_num_sms);
+  gemm_sm100_kernel<BN, A_MN, B_MN><<<grid, 192, C::SMEM, st>>>(ta, tb, g.M, g.N, g.K, e);
+  return cudaGetLastError();
+}
+
+template <int BN>
+cudaError_t launch_major(const GemmDesc& g, const Epi& e, cudaStream_t st) {
+  if (!g.a_mn && !g.b_mn) return launch_bn<BN, false, false>(g, e, st);
+  if (g.a_mn && g.b_mn) return launch_bn<BN, true, true>(g, e, st);
+  if (g.a_mn) return launch_bn<BN, true, false>(g, e, st);
+  return launch_bn<BN, false, true>(g, e, st);
+}
+
+}  // namespace
+
+bool gemm_sm100_supported(const GemmDesc& g) {
+  init_once();
+  if (!g_encode || g_num_sms <= 0) return false;
+  if (g.M < 1 || g.N < 1 || g.K < 1) return false;
+  if (g.N % 8 || g.lda % 8 || g.ldb % 8) return false;
+  if ((reinterpret_cast<uintptr_t>(g.A) | reinterpret_cast<uintptr_t>(g.B)) & 15) return false;
+  return true;
+}
+
+cudaError_t gemm_sm100(const GemmDesc& g, const Epi& e, cudaStream_t st) {
+  init_once();
+  // BN = 256 when that still gives at least one wave of tiles, else 128 (small-M slices).
+  const int t256 = ((g.M + BM - 1) / BM) * ((g.N + 255) / 256);
+  if (g.N >= 256 && t256 >= g_num_sms) return launch_major<256>(g, e, st);
+  return launch_major<128>(g, e, st);
+}
+
 }  // namespace tp

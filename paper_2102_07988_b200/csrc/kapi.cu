@@ -1,0 +1,64 @@
+// kapi.cu — include/tp_kernels.h: single-kernel entry points for unit tests and kernel benchmarks.
+#include <cuda_runtime.h>
+
+#include "common.h"
+#include "kernels.h"
+#include "tp_kernels.h"
+
+using namespace tp;
+
+namespace {
+tp_status cu(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) return fail(TP_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return TP_OK;
+}
+}  // namespace
+
+extern "C" tp_status tpk_gemm(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_mn,
+                              const void* B, int64_t ldb, int32_t b_mn, float* out, int64_t ldo, int32_t impl,
+                              void* stream) {
+  TP_CHECK_ARG(A && B && out && M >= 0 && N >= 0 && K >= 1, "tpk_gemm: bad arguments");
+  TP_CHECK_ARG(N % 8 == 0 && lda % 8 == 0 && ldb % 8 == 0 && ldo % 8 == 0, "tpk_gemm: N/lda/ldb/ldo must be multiples of 8");
+  GemmDesc g;
+  g.M = M; g.N = N; g.K = K; g.A = A; g.lda = lda; g.a_mn = a_mn != 0; g.B = B; g.ldb = ldb; g.b_mn = b_mn != 0;
+  Epi e;
+  e.kind = EPI_STORE; e.out = out; e.ldo = ldo; e.out_f32 = 1;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (impl == 0) {
+    if (!gemm_sm100_supported(g)) return fail(TP_EINVAL, "tpk_gemm: shape/alignment not supported by the sm100 kernel");
+    return cu(gemm_sm100(g, e, st), "gemm_sm100");
+  }
+  return cu(gemm_simt<bf16>(g, e, st), "gemm_simt");
+}
+
+extern "C" tp_status tpk_attention_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int32_t a,
+                                       int32_t s, int32_t d, int32_t c, int32_t l, int32_t impl, void* stream) {
+  TP_CHECK_ARG(q && k && v && o && lse, "tpk_attention_fwd: null pointer");
+  TP_CHECK_ARG(a >= 1 && d % 16 == 0 && d <= 128 && c >= 0 && l >= 0 && c + l <= s, "tpk_attention_fwd: bad shape");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bf16 *Q = (const bf16*)q, *Kp = (const bf16*)k, *Vp = (const bf16*)v;
+  if (impl == 0) return cu(attn_fwd_tc(Q, Kp, Vp, (bf16*)o, (int64_t)a * d, lse, a, s, d, c, l, st), "attn_fwd_tc");
+  return cu(attn_fwd_simt<bf16>(Q, Kp, Vp, (bf16*)o, (int64_t)a * d, lse, a, s, d, c, l, st), "attn_fwd_simt");
+}
+
+extern "C" tp_status tpk_attention_bwd(const void* dO, const void* o, const void* q, const void* k, const void* v,
+                                       const float* lse, void* dq, int64_t ldq, float* dk_acc, float* dv_acc, int32_t a,
+                                       int32_t s, int32_t d, int32_t c, int32_t l, int32_t accumulate, int32_t impl,
+                                       void* stream) {
+  TP_CHECK_ARG(dO && o && q && k && v && lse && dq && dk_acc && dv_acc, "tpk_attention_bwd: null pointer");
+  TP_CHECK_ARG(a >= 1 && d % 16 == 0 && d <= 128 && c >= 0 && l >= 1 && c + l <= s, "tpk_attention_bwd: bad shape");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  float* Dvec = nullptr;
+  tp_status r = cu(cudaMallocAsync(&Dvec, sizeof(float) * a * l, st), "cudaMallocAsync");
+  if (r != TP_OK) return r;
+  const int64_t H = (int64_t)a * d;
+  if (impl == 0)
+    r = cu(attn_bwd_tc((const bf16*)dO, H, (const bf16*)o, H, (const bf16*)q, (const bf16*)k, (const bf16*)v, lse, Dvec,
+                       (bf16*)dq, ldq, dk_acc, dv_acc, a, s, d, c, l, accumulate, st), "attn_bwd_tc");
+  else
+    r = cu(attn_bwd_simt<bf16>((const bf16*)dO, H, (const bf16*)o, H, (const bf16*)q, (const bf16*)k, (const bf16*)v,
+                               lse, Dvec, (bf16*)dq, ldq, dk_acc, dv_acc, a, s, d, c, l, accumulate, st),
+           "attn_bwd_simt");
+  cudaFreeAsync(Dvec, st);
+  return r;
+}

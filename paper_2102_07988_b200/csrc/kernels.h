@@ -51,7 +51,13 @@ cudaError_t attn_fwd_simt(const T* q, const T* k, const T* v, T* o, int64_t ldo,
 template <typename T>
 cudaError_t attn_bwd_simt(const T* dO, int64_t ld_do, const T* o, int64_t ldo, const T* q, const T* k,
                           const T* v, const float* lse, float* Dvec, T* dq, int64_t ldq, float* dk_acc,
-                          float* dv_acc, int a, int s, int d, int c, int l, cudaStream_t st);
+                          float* dv_acc, int a, int s, int d, int c, int l, int accumulate, cudaStream_t st);
+// Tensor-core (bf16) slice-vs-prefix attention (attn_tc.cu); same contract as the SIMT versions.
+cudaError_t attn_fwd_tc(const bf16* q, const bf16* k, const bf16* v, bf16* o, int64_t ldo, float* lse, int a, int s,
+                        int d, int c, int l, cudaStream_t st);
+cudaError_t attn_bwd_tc(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ldo, const bf16* q, const bf16* k,
+                        const bf16* v, const float* lse, float* Dvec, bf16* dq, int64_t ldq, float* dk_acc,
+                        float* dv_acc, int a, int s, int d, int c, int l, int accumulate, cudaStream_t st);
 template <typename T>
 cudaError_t attn_dkv_finalize(const float* dk_acc, const float* dv_acc, T* dqkv, int64_t ld, int a,
                               int s, int d, int c, int l, cudaStream_t st);

@@ -410,7 +410,10 @@ class Engine final : public EngineBase {
       float* lse = S.LSE[j] + (size_t)d * a * s;
       const double attn_flops = 4.0 * H * ((double)l * c + 0.5 * l * (l + 1.0));
       TRY(launch(KC_ATTN_FWD, attn_flops, ebytes * (2.0 * H * (c + l) + 2.0 * H * l), [&] {
-        return attn_fwd_simt<T>(S.Q[j] + (size_t)d * s * H, S.Kc[j] + (size_t)d * s * H, S.Vc[j] + (size_t)d * s * H, o, H, lse, a, s, dh, c, l, stream);
+        const T *q = S.Q[j] + (size_t)d * s * H, *kk = S.Kc[j] + (size_t)d * s * H, *vv = S.Vc[j] + (size_t)d * s * H;
+        if constexpr (std::is_same<T, bf16>::value)
+          if (!force_simt) return attn_fwd_tc(q, kk, vv, o, H, lse, a, s, dh, c, l, stream);
+        return attn_fwd_simt<T>(q, kk, vv, o, H, lse, a, s, dh, c, l, stream);
       }));
       Epi er; er.kind = EPI_RESID; er.bias = P + f.b_o; er.out = S.hmid[j] + row * H; er.ldo = H; er.resid = x; er.ldr = H;
       TRY(gemm(KC_GEMM_FWD, gd(l, H, H, o, H, false, S.wo_t[j], H, false), er));
@@ -476,20 +479,17 @@ class Engine final : public EngineBase {
       // attention: dO = dh_mid W_o^T, then slice-vs-prefix attention backward with dK/dV push
       Epi e3; e3.kind = EPI_STORE; e3.out = S.dO; e3.ldo = H;
       TRY(gemm(KC_GEMM_DX, gd(l, H, H, S.dhmid_b[j] + (size_t)c * H, H, false, S.wo_io[j], H, false), e3));
-      if (first_bwd_slice) {
-        // the last slice is processed first and touches every prefix row: start from zero
-        TRY(launch(KC_MISC, 0, 8.0 * (c + l) * H, [&] {
-          cudaError_t e = cudaMemsetAsync(S.dk_acc[j], 0, sizeof(float) * (size_t)s * H, stream);
-          if (e != cudaSuccess) return e;
-          return cudaMemsetAsync(S.dv_acc[j], 0, sizeof(float) * (size_t)s * H, stream);
-        }));
-      }
       const double attn_flops = 8.0 * H * ((double)l * c + 0.5 * l * (l + 1.0));
       T* dq = S.dQKV[j] + (size_t)c * 3 * H;
       TRY(launch(KC_ATTN_BWD, attn_flops, ebytes * 4.0 * H * (c + l) + 16.0 * H * (c + l), [&] {
-        return attn_bwd_simt<T>(S.dO, H, S.O[j] + row * H, H, S.Q[j] + (size_t)d * s * H, S.Kc[j] + (size_t)d * s * H,
-                                S.Vc[j] + (size_t)d * s * H, S.LSE[j] + (size_t)d * a * s, S.Dvec, dq, 3 * H, S.dk_acc[j],
-                                S.dv_acc[j], a, s, dh, c, l, stream);
+        const T *q = S.Q[j] + (size_t)d * s * H, *kk = S.Kc[j] + (size_t)d * s * H, *vv = S.Vc[j] + (size_t)d * s * H;
+        const int accum = first_bwd_slice ? 0 : 1;
+        if constexpr (std::is_same<T, bf16>::value)
+          if (!force_simt)
+            return attn_bwd_tc(S.dO, H, S.O[j] + row * H, H, q, kk, vv, S.LSE[j] + (size_t)d * a * s, S.Dvec, dq, 3 * H,
+                               S.dk_acc[j], S.dv_acc[j], a, s, dh, c, l, accum, stream);
+        return attn_bwd_simt<T>(S.dO, H, S.O[j] + row * H, H, q, kk, vv, S.LSE[j] + (size_t)d * a * s, S.Dvec, dq, 3 * H,
+                                S.dk_acc[j], S.dv_acc[j], a, s, dh, c, l, accum, stream);
       }));
       TRY(launch(KC_MISC, 0, (8.0 + 2 * ebytes) * l * H, [&] {
         return attn_dkv_finalize<T>(S.dk_acc[j], S.dv_acc[j], dq, 3 * H, a, s, dh, c, l, stream);

@@ -16,20 +16,22 @@ from synth import CONFIGS, ModelCfg, gpu_like_table, random_int_table, stage_par
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_symbols():
-    src = open(os.path.join(ROOT, "include", "tp.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:tp_status|void|const char\*)\s+(tp_\w+)\s*\(", src, re.M)))
+def declared_symbols(header="tp.h"):
+    src = open(os.path.join(ROOT, "include", header)).read()
+    return sorted(set(re.findall(r"^\s*(?:tp_status|void|const char\*)\s+(tpk?_\w+)\s*\(", src, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
     syms = declared_symbols()
     assert len(syms) >= 15
     out = subprocess.run(["nm", "-D", "--defined-only", tp.LIB_PATH], capture_output=True, text=True, check=True).stdout
-    exported = set(re.findall(r" T (tp_\w+)$", out, re.M))
+    exported = set(re.findall(r" T (tpk?_\w+)$", out, re.M))
     missing = [s for s in syms if s not in exported]
     assert not missing, missing
     assert sorted(tp.EXPORTED) == syms
-    for s in syms:
+    ksyms = declared_symbols("tp_kernels.h")
+    assert sorted(tp.KEXPORTED) == ksyms and all(s in exported for s in ksyms)
+    for s in syms + ksyms:
         getattr(tp.lib(), s)
 
 

@@ -1,0 +1,95 @@
+"""GPU unit tests of the hot-path kernels through include/tp_kernels.h, against plain PyTorch fp32
+math on the same bf16 inputs (and the SIMT kernels against the tensor-core kernels)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2102_07988_b200 as tp
+
+pytestmark = pytest.mark.gpu
+dev = "cuda"
+
+
+def ptr(t):
+    return t.data_ptr()
+
+
+def rel(a, b):
+    a = a.double(); b = b.double()
+    return float((a - b).norm() / b.norm().clamp_min(1e-30))
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (200, 384, 320), (37, 136, 72), (512, 5120, 2048),
+                                   (1000, 1536, 512), (2048, 2048, 2048), (8, 64, 32)])
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 1), (1, 0), (0, 1)])
+@pytest.mark.parametrize("impl", [0, 1])
+def test_gemm(M, N, K, a_mn, b_mn, impl):
+    if impl == 1 and M * N * K > 2 ** 30:
+        pytest.skip("SIMT kernel: small shapes only")
+    g = torch.Generator(device="cpu").manual_seed(M * 7 + N + K)
+    A = torch.randn(M, K, generator=g).to(dev, torch.bfloat16)   # logical A[m][k]
+    B = torch.randn(N, K, generator=g).to(dev, torch.bfloat16)   # logical B[n][k]
+    ref = A.float() @ B.float().T
+    Ast = A.T.contiguous() if a_mn else A
+    Bst = B.T.contiguous() if b_mn else B
+    out = torch.full((M, N), float("nan"), device=dev)
+    tp.k_gemm(M, N, K, ptr(Ast), M if a_mn else K, a_mn, ptr(Bst), N if b_mn else K, b_mn, ptr(out), N, impl)
+    torch.cuda.synchronize()
+    assert rel(out, ref) < 1e-5, rel(out, ref)
+
+
+def attn_ref(q, k, v, c, l):
+    """fp32 math on the bf16 inputs: rows [c, c+l) vs keys [0, c+l), causal at absolute positions."""
+    a, s, d = q.shape
+    qs = q[:, c:c + l].float()
+    ks = k[:, :c + l].float()
+    vs = v[:, :c + l].float()
+    S = qs @ ks.transpose(1, 2) / math.sqrt(d)
+    mask = torch.arange(c + l, device=dev)[None, :] > (c + torch.arange(l, device=dev))[:, None]
+    S = S.masked_fill(mask, float("-inf"))
+    lse = torch.logsumexp(S, -1)
+    P = torch.softmax(S, -1)
+    return P @ vs, lse, P
+
+
+@pytest.mark.parametrize("a,s,d,c,l", [(2, 200, 128, 72, 96), (3, 64, 16, 0, 64), (2, 512, 128, 448, 64),
+                                       (1, 300, 64, 0, 300), (4, 256, 32, 100, 37), (2, 2048, 128, 1536, 512)])
+@pytest.mark.parametrize("impl", [0, 1])
+def test_attention_fwd_bwd(a, s, d, c, l, impl):
+    g = torch.Generator(device="cpu").manual_seed(a * 1000 + s + c + l)
+    q, k, v = (torch.randn(a, s, d, generator=g).to(dev, torch.bfloat16) for _ in range(3))
+    o = torch.zeros(l, a * d, device=dev, dtype=torch.bfloat16)
+    lse = torch.zeros(a, s, device=dev)
+    tp.k_attention_fwd(ptr(q), ptr(k), ptr(v), ptr(o), ptr(lse), a, s, d, c, l, impl)
+    torch.cuda.synchronize()
+    o_ref, lse_ref, P = attn_ref(q, k, v, c, l)
+    o_ref_tok = o_ref.transpose(0, 1).reshape(l, a * d)
+    assert rel(o.float(), o_ref_tok) < 1e-2
+    assert rel(lse[:, c:c + l], lse_ref) < 1e-4
+    # backward with the kernel's own O (bf16) as the saved output
+    dO = torch.randn(l, a * d, generator=g).to(dev, torch.bfloat16)
+    dq = torch.zeros(l, 3 * a * d, device=dev, dtype=torch.bfloat16)
+    dk = torch.full((a, s, d), 0.5, device=dev)
+    dv = torch.full((a, s, d), -0.25, device=dev)
+    tp.k_attention_bwd(ptr(dO), ptr(o), ptr(q), ptr(k), ptr(v), ptr(lse), ptr(dq), 3 * a * d, ptr(dk), ptr(dv),
+                       a, s, d, c, l, 1, impl)
+    torch.cuda.synchronize()
+    dOh = dO.float().view(l, a, d).transpose(0, 1)                    # [a][l][d]
+    Oh = o.float().view(l, a, d).transpose(0, 1)
+    dV = P.transpose(1, 2) @ dOh
+    dP = dOh @ v[:, :c + l].float().transpose(1, 2)
+    Dv = (dOh * Oh).sum(-1, keepdim=True)
+    dS = P * (dP - Dv)
+    dQ = dS @ k[:, :c + l].float() / math.sqrt(d)
+    dK = dS.transpose(1, 2) @ q[:, c:c + l].float() / math.sqrt(d)
+    assert rel(dq[:, :a * d].float(), dQ.transpose(0, 1).reshape(l, a * d)) < 2e-2
+    assert rel(dk[:, :c + l] - 0.5, dK) < 2e-2
+    assert rel(dv[:, :c + l] + 0.25, dV) < 2e-2
+    assert torch.all(dk[:, c + l:] == 0.5) and torch.all(dv[:, c + l:] == -0.25)   # rows past c+l untouched
+    # accumulate = 0 overwrites
+    tp.k_attention_bwd(ptr(dO), ptr(o), ptr(q), ptr(k), ptr(v), ptr(lse), ptr(dq), 3 * a * d, ptr(dk), ptr(dv),
+                       a, s, d, c, l, 0, impl)
+    torch.cuda.synchronize()
+    assert rel(dk[:, :c + l], dK) < 2e-2 and rel(dv[:, :c + l], dV) < 2e-2
