@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""bench.py — one JSON line for the driver.
+
+A step = one synchronous tp_step: token-sliced, pipelined forward+backward of one batch of a GPT-3
+shaped model (BASELINE.json:5, metric BASELINE.json:2) with the slicing chosen by tp_plan from a
+cost table that tp_profile measured on this box (the max over stages, A-16). The unsliced GPipe
+schedule [(1, [s])] * B on the same kernels is timed beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config gpt3-1b] [--impl reference]
+
+N = 1: the GPT-3 1B config (BASELINE.json:8) on one GPU (K = 1 stage). N > 1 (torchrun): K = N
+pipeline stages, one process per GPU, NCCL send/recv between neighbours; total work is fixed
+(strong scaling). `value` = tokens of the batch / max-over-ranks device time per step.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd iteration latency & tokens/s, 1/2/4/8 B200, MFU vs unsliced pipeline"
+
+
+def model_flops(cfg, B):
+    """Algorithmic FLOPs of one iteration: B*[n*(72 s H^2 + 6 H s (s+1)) + 6 s H V]."""
+    n, H, s, V = cfg.n_layer, cfg.hidden, cfg.seq_len, cfg.vocab
+    return B * (n * (72.0 * s * H * H + 6.0 * H * s * (s + 1)) + 6.0 * s * H * V)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), p["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = str(gpu_index)
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8 or parts[0] != self.idx:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_oracle_sample(cfg, B, reps=1, warmup=0):
+    """The fp64 oracle (oracle/model.py) as it stands, on a bounded sample of the workload: one
+    sequence through embedding + ONE layer + LM head at the config's full width, seq_len and vocab,
+    fwd+bwd (median of `reps` timed runs after `warmup`). Extrapolated to the whole model with the
+    algorithmic FLOP model (n layers + head), reported as tokens/s."""
+    from oracle.model import gpt_forward_backward
+    from synth import make_params, make_tokens
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    one = cfg.with_(n_layer=1, n_stages=1)
+    params = make_params(one, seed=0, init="gpt2")
+    tokens = make_tokens(one, 1, seed=1)
+    times = []
+    for i in range(warmup + reps):
+        t0 = time.time()
+        gpt_forward_backward(params, tokens, 1, one.n_head)
+        if i >= warmup:
+            times.append(time.time() - t0)
+    dt = statistics.median(times)
+    H, s, V, n = cfg.hidden, cfg.seq_len, cfg.vocab, cfg.n_layer
+    layer = 72.0 * s * H * H + 6.0 * H * s * (s + 1)
+    head = 6.0 * s * H * V
+    t_seq = dt * (n * layer + head) / (layer + head)
+    tokps = s / t_seq
+    return {"value": tokps, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": f"fp64 numpy oracle, 1 sequence x (embed + 1 of {n} layers + LM head) at H={H}, s={s}, "
+                      f"V={V}, fwd+bwd, median {dt:.1f} s of {reps}; extrapolated by algorithmic FLOPs to {n} layers "
+                      f"(t_seq = {t_seq:.0f} s)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="gpt3-1b")
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--granularity", type=int, default=64)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-gpipe", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slicing", default="dp", help="dp | gpipe | comma-separated lengths")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    from synth import CONFIGS, make_stage_flat, make_tokens
+    base_cfg, B0 = CONFIGS[args.config]
+    B = args.batch or B0
+    K = max(world, 1)
+    cfg = base_cfg.with_(n_stages=K)
+
+    if args.impl == "reference":
+        # The reference arm is the CPU oracle (tier framing): rank 0 only, on the host cores.
+        if rank != 0:
+            return 0
+        cpu = cpu_oracle_sample(cfg, B, reps=max(1, args.steps), warmup=min(args.warmup, 1))
+        per_step_s = B * cfg.seq_len / cpu["value"]
+        line = {"impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": "tokens/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_s * 1e3, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": args.config, "batch": B, "stages": K},
+                "cpu_baseline": cpu, "e2e": {"value": cpu["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                                             "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+    import paper_2102_07988_b200 as tp
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    # --- NCCL unique id for the library's own communicator
+    nid = None
+    if world > 1:
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(tp.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nid = bytes(idt.cpu().numpy().tobytes())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        return float(t.item())
+
+    stage = rank if world > 1 else 0
+    ctx = tp.Context(cfg, rank=rank, world=world, nccl_id=nid, precision=tp.TP_BF16, max_batch=B,
+                     device=local_rank, flags=0)
+    flat = make_stage_flat(cfg, stage, seed=0) if world > 1 else np.concatenate(
+        [make_stage_flat(cfg, k, seed=0) for k in range(K)])
+    ctx.load_params(flat)
+    del flat
+    tokens = make_tokens(cfg, B, seed=1)
+    tok_dev = torch.from_numpy(tokens).cuda()
+    tok_pin = torch.from_numpy(tokens).pin_memory()
+    stream = torch.cuda.ExternalStream(ctx.stream())
+
+    # --- cost table (this stage; max over stages = bottleneck table, A-16) and the DP plan
+    g = args.granularity
+    t_prof = time.time()
+    ticks, fit = ctx.profile(g, reps=3)
+    if world > 1:
+        tt = torch.from_numpy(ticks).cuda()
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ticks = tt.cpu().numpy()
+    t_prof = time.time() - t_prof
+    t_plan = time.time()
+    dp = tp.plan(ticks, g, cfg.n_layer, cfg.hidden, cfg.seq_len, K, n_micro=B, eps_ticks=0)
+    t_plan = time.time() - t_plan
+    gpipe = tp.Slicing([cfg.seq_len])
+    if args.slicing == "dp":
+        main_sl = dp
+    elif args.slicing == "gpipe":
+        main_sl = gpipe
+    else:
+        main_sl = tp.Slicing([int(x) for x in args.slicing.split(",")])
+
+    def timed(sl, steps, device_tokens=True):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        loss = None
+        for _ in range(steps):
+            if device_tokens:
+                loss = ctx.step_device(sl, tok_dev.data_ptr(), B)
+            else:
+                    loss = ctx.step(sl, tok_pin.numpy())
+        e1.record(stream)
+        e1.synchronize()
+        barrier()
+        return allmax(e0.elapsed_time(e1) / steps), loss
+
+    for _ in range(args.warmup):
+        ctx.step_device(main_sl, tok_dev.data_ptr(), B)
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    ms, loss = timed(main_sl, args.steps)
+    clk = clocks.stop()
+    launches = allsum(ctx.last_step_launches()) * args.steps
+    # e2e through the public API with host tokens (pinned) and the loss read back every step
+    ms_e2e, _ = timed(main_sl, args.steps, device_tokens=False)
+    # unsliced GPipe on the same kernels
+    ms_gpipe = None
+    if not args.no_gpipe and main_sl.lengths != gpipe.lengths:
+        for _ in range(1):
+            ctx.step_device(gpipe, tok_dev.data_ptr(), B)
+        ms_gpipe, _ = timed(gpipe, args.steps)
+    elif main_sl.lengths == gpipe.lengths:
+        ms_gpipe = ms
+    # kernel statistics: a second timed region with CUDA events around every launch (on the
+    # library's stream, which every kernel is launched on)
+    ctx.kernel_stats_reset()
+    ctx.kernel_stats_enable(True)
+    ms_instr, _ = timed(main_sl, args.steps)
+    ctx.kernel_stats_enable(False)
+    kstats = ctx.kernel_stats()
+    peak_burst, peak_sust, hbm, peak_kind = load_peaks()
+    tokens_per_step = B * cfg.seq_len
+    flops = model_flops(cfg, B)
+    value = tokens_per_step / (ms / 1e3)
+    mfu = flops / (ms / 1e3) / (args.gpus * peak_burst * 1e12)
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": args.config, "n_layer": cfg.n_layer, "hidden": cfg.hidden, "heads": cfg.n_head,
+                   "seq_len": cfg.seq_len, "batch": B, "vocab": cfg.vocab, "stages": K,
+                   "parallelism": f"pipeline{K}", "slicing": main_sl.notation(B), "granularity": g,
+                   "l2": "working set > L2 (bf16 weights alone exceed 126 MB); no flush"},
+        "mfu": mfu, "mfu_sustained_peak": flops / (ms / 1e3) / (args.gpus * peak_sust * 1e12),
+        "gpipe": None if ms_gpipe is None else {
+            "slicing": gpipe.notation(B), "ms_per_step": ms_gpipe, "tokens_per_s": tokens_per_step / (ms_gpipe / 1e3),
+            "mfu": flops / (ms_gpipe / 1e3) / (args.gpus * peak_burst * 1e12),
+            "speedup_of_dp": ms_gpipe / ms},
+        "plan": {"predicted_ms": dp.predicted / 1e6, "t_max_ms": dp.t_max / 1e6, "profile_s": t_prof, "plan_s": t_plan,
+                 "fit": {"a": [float(x) for x in fit[:4]], "max_rel_err": float(fit[4])}},
+        "loss": loss,
+        "clocks": clk,
+        "e2e": {"value": tokens_per_step / (ms_e2e / 1e3), "unit": "tokens/s",
+                "h2d_bytes_per_step": int(tokens.nbytes), "d2h_bytes_per_step": 4},
+        "gpu_launches": int(launches),
+    }
+    # roofline + cpu baseline are filled by the rank-0 tail below
+    if rank == 0:
+        line["roofline"] = roofline(kstats, ms_instr, args.steps, peak_sust, hbm, peak_kind)
+        line["kernel_classes"] = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+                                      "tflops": (v["flops"] / (v["ms"] * 1e9)) if v["ms"] > 0 and v["flops"] > 0 else None}
+                                  for k, v in kstats.items() if v["launches"]}
+        line["ms_per_step_instrumented"] = ms_instr
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_oracle_sample(cfg, B)
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def roofline(kstats, ms_step, steps, peak_tflops, hbm_gbs, peak_kind):
+    """Dominant kernel class of the step (largest summed device time): its ALGORITHMIC FLOPs (or
+    bytes) per launch / its mean CUDA-event launch duration, against the measured sustained bf16
+    peak (a kernel timed inside a long step) or the measured HBM copy bandwidth."""
+    live = {k: v for k, v in kstats.items() if v["launches"] and v["ms"] > 0}
+    if not live:
+        return None
+    name, v = max(live.items(), key=lambda kv: kv[1]["ms"])
+    per_launch_ms = v["ms"] / v["launches"]
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(name)
+    except Exception:
+        pass
+    if v["flops"] > 0:
+        ach = v["flops"] / v["launches"] / (per_launch_ms * 1e-3) / 1e12
+        return {"kernel": name, "bound": "tensor", "achieved": ach, "peak": peak_tflops, "unit": "TFLOP/s",
+                "frac": ach / peak_tflops, "traffic": traffic, "peak_kind": f"{peak_kind} sustained bf16",
+                "share_of_step": v["ms"] / steps / ms_step, "launches_per_step": v["launches"] / steps,
+                "flops_per_launch": v["flops"] / v["launches"]}
+    ach = v["bytes"] / v["launches"] / (per_launch_ms * 1e-3) / 1e9
+    return {"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm_gbs, "unit": "GB/s", "frac": ach / hbm_gbs,
+            "traffic": traffic, "peak_kind": peak_kind, "share_of_step": v["ms"] / steps / ms_step}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -170,6 +170,8 @@ tp_status tp_get_stream(tp_ctx* ctx, void** stream_out);
 tp_status tp_kernel_stats(tp_ctx* ctx, int32_t i, char* name32, int64_t* launches, double* ms,
                           double* flops, double* bytes, int32_t* n_classes);
 tp_status tp_kernel_stats_reset(tp_ctx* ctx);
+/* Turns the per-launch CUDA-event bracketing of TP_FLAG_KERNEL_STATS on (1) or off (0). */
+tp_status tp_kernel_stats_enable(tp_ctx* ctx, int32_t on);
 
 /* Number of kernel launches issued by the last tp_step (device work only, this context). */
 tp_status tp_last_step_launches(tp_ctx* ctx, int64_t* out);

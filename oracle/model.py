@@ -87,6 +87,11 @@ def causal_attention_backward(dO, q, k, v, P):
 
 
 # ---------------------------------------------------------------- full model
+def _wgrad(x: np.ndarray, dy: np.ndarray) -> np.ndarray:
+    """dW = sum over all (batch, position) rows of x^T dy, i.e. X^T dY with rows flattened."""
+    return x.reshape(-1, x.shape[-1]).T @ dy.reshape(-1, dy.shape[-1])
+
+
 def _p(params, name):
     return np.asarray(params[name], dtype=np.float64)
 
@@ -156,7 +161,7 @@ def gpt_forward_backward(params: Dict[str, np.ndarray], tokens: np.ndarray, n_la
     dz = np.exp(z - lse[..., None])
     np.put_along_axis(dz, y[..., None], np.take_along_axis(dz, y[..., None], axis=-1) - 1.0, axis=-1)
     dz /= N
-    grads["w_out"] = np.einsum("bsh,bsv->hv", Af, dz)
+    grads["w_out"] = _wgrad(Af, dz)
     dAf = dz @ _p(params, "w_out").T
     dh, grads["lnf_g"], grads["lnf_b"] = layer_norm_backward(dAf, xhatf, rstdf, _p(params, "lnf_g"))
     dlayer_in = [None] * (n_layer + 1)
@@ -166,18 +171,18 @@ def gpt_forward_backward(params: Dict[str, np.ndarray], tokens: np.ndarray, n_la
         L = lambda n: _p(params, f"l{li}.{n}")
         c = caches[li]
         # FFN backward
-        grads[f"l{li}.w_2"] = np.einsum("bsf,bsh->fh", c["G"], dh)
+        grads[f"l{li}.w_2"] = _wgrad(c["G"], dh)
         grads[f"l{li}.b_2"] = dh.sum(axis=(0, 1))
         dG = dh @ L("w_2").T
         dU = dG * gelu_grad(c["U"])
-        grads[f"l{li}.w_1"] = np.einsum("bsh,bsf->hf", c["A2"], dU)
+        grads[f"l{li}.w_1"] = _wgrad(c["A2"], dU)
         grads[f"l{li}.b_1"] = dU.sum(axis=(0, 1))
         dA2 = dU @ L("w_1").T
         dx, grads[f"l{li}.ln2_g"], grads[f"l{li}.ln2_b"] = layer_norm_backward(
             dA2, c["xhat2"], c["rstd2"], L("ln2_g"))
         dh = dh + dx
         # attention backward
-        grads[f"l{li}.w_o"] = np.einsum("bsh,bsk->hk", c["o"], dh)
+        grads[f"l{li}.w_o"] = _wgrad(c["o"], dh)
         grads[f"l{li}.b_o"] = dh.sum(axis=(0, 1))
         do = dh @ L("w_o").T
         dq, dk, dv = np.zeros_like(do), np.zeros_like(do), np.zeros_like(do)
@@ -187,7 +192,7 @@ def gpt_forward_backward(params: Dict[str, np.ndarray], tokens: np.ndarray, n_la
                 dq[bi, :, cs], dk[bi, :, cs], dv[bi, :, cs] = causal_attention_backward(
                     do[bi, :, cs], c["q"][bi, :, cs], c["k"][bi, :, cs], c["v"][bi, :, cs], c["P"][bi, j])
         dqkv = np.concatenate([dq, dk, dv], axis=-1)
-        grads[f"l{li}.w_qkv"] = np.einsum("bsh,bsk->hk", c["A1"], dqkv)
+        grads[f"l{li}.w_qkv"] = _wgrad(c["A1"], dqkv)
         grads[f"l{li}.b_qkv"] = dqkv.sum(axis=(0, 1))
         dA1 = dqkv @ L("w_qkv").T
         dx, grads[f"l{li}.ln1_g"], grads[f"l{li}.ln1_b"] = layer_norm_backward(

@@ -19,7 +19,7 @@ TP_FLAG_KEEP_LOGITS, TP_FLAG_KERNEL_STATS, TP_FLAG_FORCE_SIMT = 1, 2, 4
 
 EXPORTED = ["tp_plan", "tp_stage_param_count", "tp_nccl_unique_id", "tp_init", "tp_param_count",
             "tp_load_params", "tp_step", "tp_step_device", "tp_get_grads", "tp_get_logits",
-            "tp_profile", "tp_get_stream", "tp_kernel_stats", "tp_kernel_stats_reset",
+            "tp_profile", "tp_get_stream", "tp_kernel_stats", "tp_kernel_stats_reset", "tp_kernel_stats_enable",
             "tp_last_step_launches", "tp_destroy", "tp_last_error"]
 KEXPORTED = ["tpk_gemm", "tpk_attention_fwd", "tpk_attention_bwd"]
 
@@ -70,6 +70,7 @@ def _load() -> C.CDLL:
         "tp_kernel_stats": (C.c_int, [P, C.c_int32, C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                       C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
         "tp_kernel_stats_reset": (C.c_int, [P]),
+        "tp_kernel_stats_enable": (C.c_int, [P, C.c_int32]),
         "tp_last_step_launches": (C.c_int, [P, C.POINTER(C.c_int64)]),
         "tp_destroy": (None, [P]),
         "tpk_gemm": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, P, C.c_int64, C.c_int32, P, C.c_int64, C.c_int32,
@@ -230,6 +231,9 @@ class Context:
 
     def kernel_stats_reset(self) -> None:
         _check(_lib.tp_kernel_stats_reset(self._h))
+
+    def kernel_stats_enable(self, on: bool) -> None:
+        _check(_lib.tp_kernel_stats_enable(self._h, 1 if on else 0))
 
     def last_step_launches(self) -> int:
         n = C.c_int64()

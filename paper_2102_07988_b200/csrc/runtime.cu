@@ -876,6 +876,11 @@ extern "C" tp_status tp_kernel_stats_reset(tp_ctx* ctx) {
   for (auto& s : ctx->eng->instr.stats) { s.launches = 0; s.ms = s.flops = s.bytes = 0; }
   return TP_OK;
 }
+extern "C" tp_status tp_kernel_stats_enable(tp_ctx* ctx, int32_t on) {
+  TP_CHECK_ARG(ctx, "tp_kernel_stats_enable: null ctx");
+  ctx->eng->instr.on = on != 0;
+  return TP_OK;
+}
 extern "C" tp_status tp_last_step_launches(tp_ctx* ctx, int64_t* out) {
   TP_CHECK_ARG(ctx && out, "tp_last_step_launches: null argument");
   *out = ctx->eng->instr.launches;

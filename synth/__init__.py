@@ -197,3 +197,40 @@ def gpu_like_table(n: int, rng: np.random.Generator, knee: int = 32, base_ns: in
             v = (base + ctx_ns * l * c / 8.0) * (1.0 + noise * rng.standard_normal())
             t[l - 1, c] = max(1, int(round(v)))
     return t
+
+
+def _tensor_seed(seed: int, name: str) -> int:
+    h = 1469598103934665603
+    for ch in name.encode():
+        h = ((h ^ ch) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return (h ^ (seed * 0x9E3779B97F4A7C15)) & 0xFFFFFFFFFFFFFFFF
+
+
+def make_stage_flat(cfg: ModelCfg, k: int, seed: int = 0, init: str = "gpt2") -> np.ndarray:
+    """Flat float32 parameters of stage k only (bench at GPT-3 sizes: a rank builds just its stage).
+    Same recipes as make_params, but every tensor is a window, at a per-(seed, name) random offset,
+    of one 2^24-entry N(0, 1) pool, tiled — so multi-GB stages are built at memcpy speed. Values do
+    not affect the dense cost being measured."""
+    pool_rng = np.random.Generator(np.random.PCG64(seed))
+    pool = pool_rng.standard_normal(1 << 24, dtype=np.float32)
+    out = np.empty(stage_param_count(cfg, k), dtype=np.float32)
+    off = 0
+    for name, shape in stage_param_specs(cfg, k):
+        cnt = int(np.prod(shape))
+        base = name.split(".")[-1]
+        dst = out[off:off + cnt]
+        if base.endswith("_g"):
+            dst[:] = 1.0
+        elif init == "gpt2" and (base.startswith("b_") or base.endswith("_b")):
+            dst[:] = 0.0
+        else:
+            start = _tensor_seed(seed, name) % pool.size
+            scale = 0.02 / (math.sqrt(2.0 * cfg.n_layer) if base in ("w_o", "w_2") else 1.0)
+            done = 0
+            while done < cnt:
+                take = min(cnt - done, pool.size - start)
+                np.multiply(pool[start:start + take], scale, out=dst[done:done + take])
+                done += take
+                start = 0
+        off += cnt
+    return out
