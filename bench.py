@@ -214,18 +214,19 @@ def main():
 
     # --- cost table (this stage; max over stages = bottleneck table, A-16) and the DP plan
     g = args.granularity
-    t_prof = time.time()
-    ticks, fit = ctx.profile(g, reps=3)
-    if world > 1:
-        tt = torch.from_numpy(ticks).cuda()
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ticks = tt.cpu().numpy()
-    t_prof = time.time() - t_prof
-    t_plan = time.time()
-    dp = tp.plan(ticks, g, cfg.n_layer, cfg.hidden, cfg.seq_len, K, n_micro=B, eps_ticks=0)
-    t_plan = time.time() - t_plan
     gpipe = tp.Slicing([cfg.seq_len])
+    dp, fit, t_prof, t_plan = None, None, 0.0, 0.0
     if args.slicing == "dp":
+        t_prof = time.time()
+        ticks, fit = ctx.profile(g, reps=3)
+        if world > 1:
+            tt = torch.from_numpy(ticks).cuda()
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ticks = tt.cpu().numpy()
+        t_prof = time.time() - t_prof
+        t_plan = time.time()
+        dp = tp.plan(ticks, g, cfg.n_layer, cfg.hidden, cfg.seq_len, K, n_micro=B, eps_ticks=0)
+        t_plan = time.time() - t_plan
         main_sl = dp
     elif args.slicing == "gpipe":
         main_sl = gpipe
@@ -289,8 +290,9 @@ def main():
             "slicing": gpipe.notation(B), "ms_per_step": ms_gpipe, "tokens_per_s": tokens_per_step / (ms_gpipe / 1e3),
             "mfu": flops / (ms_gpipe / 1e3) / (args.gpus * peak_burst * 1e12),
             "speedup_of_dp": ms_gpipe / ms},
-        "plan": {"predicted_ms": dp.predicted / 1e6, "t_max_ms": dp.t_max / 1e6, "profile_s": t_prof, "plan_s": t_plan,
-                 "fit": {"a": [float(x) for x in fit[:4]], "max_rel_err": float(fit[4])}},
+        "plan": None if dp is None else {
+            "predicted_ms": dp.predicted / 1e6, "t_max_ms": dp.t_max / 1e6, "profile_s": t_prof, "plan_s": t_plan,
+            "fit": {"a": [float(x) for x in fit[:4]], "max_rel_err": float(fit[4])}},
         "loss": loss,
         "clocks": clk,
         "e2e": {"value": tokens_per_step / (ms_e2e / 1e3), "unit": "tokens/s",

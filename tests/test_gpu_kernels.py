@@ -28,6 +28,8 @@ def rel(a, b):
 def test_gemm(M, N, K, a_mn, b_mn, impl):
     if impl == 1 and M * N * K > 2 ** 30:
         pytest.skip("SIMT kernel: small shapes only")
+    if a_mn and M % 8:
+        pytest.skip("MN-major A needs lda = M to be a multiple of 8 (16-byte TMA strides)")
     g = torch.Generator(device="cpu").manual_seed(M * 7 + N + K)
     A = torch.randn(M, K, generator=g).to(dev, torch.bfloat16)   # logical A[m][k]
     B = torch.randn(N, K, generator=g).to(dev, torch.bfloat16)   # logical B[n][k]
