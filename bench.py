@@ -172,14 +172,8 @@ def main():
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    # --- NCCL unique id for the library's own communicator
-    nid = None
-    if world > 1:
-        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(tp.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nid = bytes(idt.cpu().numpy().tobytes())
+    from paper_2102_07988_b200 import dist as tdist
+    nid = tdist.share_nccl_id(rank) if world > 1 else None
 
     def barrier():
         if world > 1:
@@ -187,18 +181,10 @@ def main():
         torch.cuda.synchronize()
 
     def allmax(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return tdist.max_over_ranks(x) if world > 1 else x
 
     def allsum(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t)
-        return float(t.item())
+        return tdist.sum_over_ranks(x) if world > 1 else x
 
     stage = rank if world > 1 else 0
     ctx = tp.Context(cfg, rank=rank, world=world, nccl_id=nid, precision=tp.TP_BF16, max_batch=B,
@@ -220,13 +206,13 @@ def main():
         t_prof = time.time()
         ticks, fit = ctx.profile(g, reps=3)
         if world > 1:
-            tt = torch.from_numpy(ticks).cuda()
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ticks = tt.cpu().numpy()
+            ticks = tdist.bottleneck_table(ticks)
         t_prof = time.time() - t_prof
         t_plan = time.time()
         dp = tp.plan(ticks, g, cfg.n_layer, cfg.hidden, cfg.seq_len, K, n_micro=B, eps_ticks=0)
         t_plan = time.time() - t_plan
+        if world > 1 and not tdist.agreed(dp.lengths):
+            raise RuntimeError("ranks planned different slicings")
         main_sl = dp
     elif args.slicing == "gpipe":
         main_sl = gpipe

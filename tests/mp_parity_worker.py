@@ -1,0 +1,50 @@
+"""torchrun worker for tests/test_gpu_multi.py: one stage per GPU, NCCL send/recv between stages,
+compared with the fp64 oracle on its own stage's gradients (and logits on the last stage)."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+import paper_2102_07988_b200 as tp
+from paper_2102_07988_b200 import dist as tdist
+from oracle.model import gpt_forward_backward
+from synth import CONFIGS, make_params, make_tokens, pack_stage, unpack_stage
+from tests.gpu_util import rel
+
+
+def main():
+    cfg_name, precision, lengths, out_dir = sys.argv[1], sys.argv[2], sys.argv[3], sys.argv[4]
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    base, B = CONFIGS[cfg_name]
+    cfg = base.with_(n_stages=world)
+    prec = tp.TP_BF16 if precision == "bf16" else tp.TP_FP32
+    params = make_params(cfg, seed=11, bf16=(prec == tp.TP_BF16))
+    tokens = make_tokens(cfg, B, seed=12)
+    nid = tdist.share_nccl_id(rank)
+    ctx = tp.Context(cfg, rank=rank, world=world, nccl_id=nid, precision=prec, max_batch=B, device=local,
+                     flags=tp.TP_FLAG_KEEP_LOGITS if rank == world - 1 else 0)
+    ctx.load_params(pack_stage(params, cfg, rank))
+    sl = tp.Slicing([int(x) for x in lengths.split(",")])
+    losses = [ctx.step(sl, tokens) for _ in range(2)]          # twice: grads are re-zeroed per step
+    grads = unpack_stage(ctx.grads(), cfg, rank)
+    ref = gpt_forward_backward(params, tokens, cfg.n_layer, cfg.n_head)
+    errs = {k: rel(v, ref["grads"][k]) for k, v in grads.items()}
+    errs["loss"] = abs(losses[-1] - ref["loss"]) / abs(ref["loss"])
+    errs["loss_repeat"] = abs(losses[0] - losses[1]) / abs(losses[0])
+    if rank == world - 1:
+        errs["logits"] = rel(ctx.logits(B), ref["logits"])
+    with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
+        json.dump(errs, f)
+    ctx.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,34 @@
+"""Multi-GPU (NCCL send/recv over NVLink) parity: K = world stages, one process per GPU, against
+the fp64 oracle. Skipped when fewer GPUs are visible."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def run(world, cfg, precision, lengths, tmp_path):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29531", os.path.join(ROOT, "tests", "mp_parity_worker.py"),
+           cfg, precision, lengths, str(tmp_path)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    return [json.load(open(tmp_path / f"rank{k}.json")) for k in range(world)]
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-4), ("bf16", 2e-2)])
+def test_tiny_two_stages_nccl(precision, tol, tmp_path):
+    for errs in run(2, "tiny", precision, "5,9,2,16", tmp_path):
+        assert max(errs.values()) < tol, errs
+
+
+def test_small_four_stages_nccl(tmp_path):
+    for errs in run(4, "small", "bf16", "40,24,64", tmp_path):
+        assert max(errs.values()) < 2e-2, errs
