@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.h"
@@ -98,21 +99,67 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int BN>
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  const uint16_t mask = 3;
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+// CG = 1: one CTA computes a 128 x BN tile (tcgen05.mma.cta_group::1, M = 128).
+// CG = 2: a CTA pair (cluster of 2 on one TPC) computes a 256 x BN tile with
+//         tcgen05.mma.cta_group::2 (M = 256): each CTA stages its own 128 rows of A and half of
+//         the BN rows of B, the leader issues the MMAs over both CTAs' shared memory, and each
+//         CTA's TMEM receives its 128 rows — halving the per-SM L2->SMEM operand traffic.
+template <int CG, int BN>
 struct Cfg {
-  static constexpr int NS = BN == 256 ? 4 : 6;  // pipeline depth
   static constexpr uint32_t A_BYTES = BM * BK * 2;
-  static constexpr uint32_t B_BYTES = BN * BK * 2;
+  static constexpr uint32_t B_BYTES = (BN / CG) * BK * 2;
   static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
+  static constexpr int NS = (196608 / STAGE) > 8 ? 8 : (196608 / STAGE);  // pipeline depth
   static constexpr uint32_t SMEM = NS * STAGE + 1024 /*align slack*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = 2 * BN;  // double-buffered fp32 accumulator
+  static constexpr int TILE_M = BM * CG;
 };
 
-template <int BN, bool A_MN, bool B_MN>
+template <int CG, int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(192, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                       int K, Epi epi) {
-  using C = Cfg<BN>;
+  using C = Cfg<CG, BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::NS * C::STAGE);
@@ -122,58 +169,81 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m_tiles = (M + BM - 1) / BM, n_tiles = (N + BN - 1) / BN;
+  const uint32_t crank = CG == 2 ? cluster_rank() : 0;
+  const bool leader = crank == 0;
+  const int m_tiles = (M + C::TILE_M - 1) / C::TILE_M, n_tiles = (N + BN - 1) / BN;
   const int tiles = m_tiles * n_tiles, kbs = (K + BK - 1) / BK;
+  const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::NS; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, 128); }
+    for (int i = 0; i < 2; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, 4 * CG); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(C::TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer
+    // ---------------- TMA producer (both CTAs of a pair; bytes land on the leader's barrier)
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      const int m0 = (tile % m_tiles) * BM, n0 = (tile / m_tiles) * BN;
+    for (int tile = unit; tile < tiles; tile += nunits) {
+      const int m0 = (tile % m_tiles) * C::TILE_M + crank * BM;
+      const int nb0 = (tile / m_tiles) * BN + crank * (BN / CG);
       for (int kb = 0; kb < kbs; ++kb) {
         mbar_wait(empty + stage, phase ^ 1);
-        mbar_expect_tx(full + stage, C::STAGE);
+        if (leader) mbar_expect_tx(full + stage, C::STAGE * CG);
         uint8_t* a_dst = smem + stage * C::STAGE;
         uint8_t* b_dst = a_dst + C::A_BYTES;
-        if (!A_MN) tma_load_2d(a_dst, &tmA, kb * BK, m0, full + stage);
-        else
+        if (CG == 1) {
+          if (!A_MN) tma_load_2d(a_dst, &tmA, kb * BK, m0, full + stage);
+          else
 #pragma unroll
-          for (int i = 0; i < BM / 64; ++i) tma_load_2d(a_dst + i * 8192, &tmA, m0 + i * 64, kb * BK, full + stage);
-        if (!B_MN) tma_load_2d(b_dst, &tmB, kb * BK, n0, full + stage);
-        else
+            for (int i = 0; i < BM / 64; ++i) tma_load_2d(a_dst + i * 8192, &tmA, m0 + i * 64, kb * BK, full + stage);
+          if (!B_MN) tma_load_2d(b_dst, &tmB, kb * BK, nb0, full + stage);
+          else
 #pragma unroll
-          for (int i = 0; i < BN / 64; ++i) tma_load_2d(b_dst + i * 8192, &tmB, n0 + i * 64, kb * BK, full + stage);
+            for (int i = 0; i < BN / 64; ++i) tma_load_2d(b_dst + i * 8192, &tmB, nb0 + i * 64, kb * BK, full + stage);
+        } else {
+          const uint32_t bar = map_to_rank(smem_u32(full + stage), 0);
+          if (!A_MN) tma_load_2d_pair(a_dst, &tmA, kb * BK, m0, bar);
+          else
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i) tma_load_2d_pair(a_dst + i * 8192, &tmA, m0 + i * 64, kb * BK, bar);
+          if (!B_MN) tma_load_2d_pair(b_dst, &tmB, kb * BK, nb0, bar);
+          else
+#pragma unroll
+            for (int i = 0; i < BN / CG / 64; ++i) tma_load_2d_pair(b_dst + i * 8192, &tmB, nb0 + i * 64, kb * BK, bar);
+        }
         if (++stage == C::NS) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer (one thread issues for the whole CTA)
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ---------------- MMA issuer (one thread issues for the CTA / CTA pair)
     const uint32_t idesc = (1u << 4)                       // D = fp32
                            | (1u << 7) | (1u << 10)        // A, B = bf16
                            | ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16)
-                           | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+                           | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(C::TILE_M >> 4) << 24);
     int stage = 0, acc = 0;
     uint32_t phase = 0, acc_phase = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    for (int tile = unit; tile < tiles; tile += nunits) {
       mbar_wait(tempty + acc, acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
@@ -186,21 +256,23 @@ __global__ void __launch_bounds__(192, 1)
         for (int k = 0; k < BK / 16; ++k) {
           const uint64_t ad = A_MN ? make_desc(a_base + k * 2048, 8192, 1024) : make_desc(a_base + k * 32, 16, 1024);
           const uint64_t bd = B_MN ? make_desc(b_base + k * 2048, 8192, 1024) : make_desc(b_base + k * 32, 16, 1024);
-          mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          if (CG == 1) mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          else mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
         }
-        mma_commit(empty + stage);  // frees the smem slot once these MMAs have read it
+        if (CG == 1) mma_commit(empty + stage); else mma_commit_pair(empty + stage);  // frees the smem slot(s)
         if (++stage == C::NS) { stage = 0; phase ^= 1; }
       }
-      mma_commit(tfull + acc);      // accumulator ready for the epilogue
+      if (CG == 1) mma_commit(tfull + acc); else mma_commit_pair(tfull + acc);        // accumulator ready
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 2) {
-    // ---------------- epilogue: TMEM lanes (warp % 4) * 32 .. +31 = tile rows
+    // ---------------- epilogue: TMEM lanes (warp % 4) * 32 .. +31 = rows of this CTA's 128
     const int q = warp & 3;
+    const uint32_t tempty_leader = CG == 2 ? map_to_rank(smem_u32(tempty), 0) : 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      const int m0 = (tile % m_tiles) * BM, n0 = (tile / m_tiles) * BN;
+    for (int tile = unit; tile < tiles; tile += nunits) {
+      const int m0 = (tile % m_tiles) * C::TILE_M + crank * BM, n0 = (tile / m_tiles) * BN;
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
@@ -222,21 +294,30 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(tempty + acc);
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 1) mbar_arrive(tempty + acc);
+        else mbar_arrive_cluster(tempty_leader + acc * 8);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync_all(); else __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS)
-                 : "memory");
+    if (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS)
+                   : "memory");
   }
 }
 
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+int g_force_cg = 0;  // test hook: TP_GEMM_CG=1|2 forces the CTA-group size
 int g_num_sms = 0;
 std::once_flag g_once;
 
@@ -249,6 +330,7 @@ void init_once() {
       g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     int dev = 0;
     cudaGetDevice(&dev);
+    if (const char* e = getenv("TP_GEMM_CG")) g_force_cg = atoi(e);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   });
 }
@@ -266,32 +348,43 @@ bool make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int CG, int BN, bool A_MN, bool B_MN>
 cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
-  using C = Cfg<BN>;
+  using C = Cfg<CG, BN>;
+  auto kern = gemm_sm100_kernel<CG, BN, A_MN, B_MN>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t r = cudaFuncSetAttribute(gemm_sm100_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)C::SMEM);
+    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (r != cudaSuccess) return r;
     attr_set = true;
   }
   CUtensorMap ta, tb;
   bool ok = A_MN ? make_map(&ta, g.A, g.M, g.K, g.lda, 64, 64) : make_map(&ta, g.A, g.K, g.M, g.lda, 64, BM);
-  ok = ok && (B_MN ? make_map(&tb, g.B, g.N, g.K, g.ldb, 64, 64) : make_map(&tb, g.B, g.K, g.N, g.ldb, 64, BN));
+  ok = ok && (B_MN ? make_map(&tb, g.B, g.N, g.K, g.ldb, 64, 64) : make_map(&tb, g.B, g.K, g.N, g.ldb, 64, BN / CG));
   if (!ok) return cudaErrorInvalidValue;
-  const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
-  const int grid = std::min(tiles, g_num_sms);
-  gemm_sm100_kernel<BN, A_MN, B_MN><<<grid, 192, C::SMEM, st>>>(ta, tb, g.M, g.N, g.K, e);
-  return cudaGetLastError();
+  const int tiles = ((g.M + C::TILE_M - 1) / C::TILE_M) * ((g.N + BN - 1) / BN);
+  const int units = std::min(tiles, g_num_sms / CG);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(units * CG);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, g.M, g.N, g.K, e);
 }
 
-template <int BN>
+template <int CG, int BN>
 cudaError_t launch_major(const GemmDesc& g, const Epi& e, cudaStream_t st) {
-  if (!g.a_mn && !g.b_mn) return launch_bn<BN, false, false>(g, e, st);
-  if (g.a_mn && g.b_mn) return launch_bn<BN, true, true>(g, e, st);
-  if (g.a_mn) return launch_bn<BN, true, false>(g, e, st);
-  return launch_bn<BN, false, true>(g, e, st);
+  if (!g.a_mn && !g.b_mn) return launch_bn<CG, BN, false, false>(g, e, st);
+  if (g.a_mn && g.b_mn) return launch_bn<CG, BN, true, true>(g, e, st);
+  if (g.a_mn) return launch_bn<CG, BN, true, false>(g, e, st);
+  return launch_bn<CG, BN, false, true>(g, e, st);
 }
 
 }  // namespace
@@ -307,10 +400,15 @@ bool gemm_sm100_supported(const GemmDesc& g) {
 
 cudaError_t gemm_sm100(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   init_once();
-  // BN = 256 when that still gives at least one wave of tiles, else 128 (small-M slices).
-  const int t256 = ((g.M + BM - 1) / BM) * ((g.N + 255) / 256);
-  if (g.N >= 256 && t256 >= g_num_sms) return launch_major<256>(g, e, st);
-  return launch_major<128>(g, e, st);
+  // Pair tiles (256 x BN, cta_group::2) whenever M spans more than one 128-row tile; BN = 256 when
+  // that still gives at least one wave of work units, else 128.
+  int cg = g.M > BM ? 2 : 1;
+  if (g_force_cg) cg = g_force_cg;
+  const int units = g_num_sms / cg;
+  const int t256 = ((g.M + BM * cg - 1) / (BM * cg)) * ((g.N + 255) / 256);
+  const bool bn256 = g.N >= 256 && t256 >= units;
+  if (cg == 2) return bn256 ? launch_major<2, 256>(g, e, st) : launch_major<2, 128>(g, e, st);
+  return bn256 ? launch_major<1, 256>(g, e, st) : launch_major<1, 128>(g, e, st);
 }
 
 }  // namespace tp

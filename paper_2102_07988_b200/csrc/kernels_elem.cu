@@ -2,6 +2,8 @@
 // embedding gather/scatter (A-7), fused cross-entropy fwd+bwd (Eq. 1, A-9),
 // dtype conversion/transposition of parameters, bias-gradient column sums, loss reduction.
 // All use 16-byte vector accesses where the row length allows (H % 8 == 0 is guaranteed).
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace tp {
@@ -9,92 +11,139 @@ namespace tp {
 namespace {
 
 // ---------------------------------------------------------------- LayerNorm
-// one CTA per row; the row is staged in shared memory (H <= 16384 -> 64 KB).
-template <typename T>
-__global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x, const float* __restrict__ gam,
-                                                     const float* __restrict__ bet, T* __restrict__ y,
-                                                     float* __restrict__ mean_out, float* __restrict__ rstd_out,
-                                                     int H) {
-  extern __shared__ float row[];
-  __shared__ float red[8];
-  const int r = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+// Rows are held in registers: thread t owns columns (c*NT + t)*8 .. +7 for chunk c < NCH
+// (16-byte vectors), H <= NT*8*NCH. Two-pass mean/variance from registers.
+template <int NT>
+__device__ __forceinline__ float block_sum(float v, float* red /*[NT/32]*/) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) t += red[w];
+  return t;
+}
+
+template <typename T, int NT, int NCH>
+__global__ void __launch_bounds__(NT) ln_fwd_kernel(const float* __restrict__ x, const float* __restrict__ gam,
+                                                    const float* __restrict__ bet, T* __restrict__ y,
+                                                    float* __restrict__ mean_out, float* __restrict__ rstd_out, int H) {
+  __shared__ float red[2][NT / 32];
+  const int r = blockIdx.x, tid = threadIdx.x;
   const float* xr = x + (int64_t)r * H;
+  float v[NCH][8];
   float s = 0.f;
-  for (int i = tid * 4; i < H; i += 1024) {
-    float4 v = *reinterpret_cast<const float4*>(xr + i);
-    *reinterpret_cast<float4*>(row + i) = v;
-    s += (v.x + v.y) + (v.z + v.w);
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int col = (c * NT + tid) * 8;
+    if (col < H) load8<float>(xr + col, v[c]);
+    else
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[c][i] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += v[c][i];
   }
-  s = warp_sum(s);
-  if (lane == 0) red[wid] = s;
-  __syncthreads();
-  float tot = 0.f;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) tot += red[w];
-  const float mean = tot / H;
-  __syncthreads();
+  const float mean = block_sum<NT>(s, red[0]) / H;
   float q = 0.f;
-  for (int i = tid; i < H; i += 256) { const float d = row[i] - mean; q += d * d; }
-  q = warp_sum(q);
-  if (lane == 0) red[wid] = q;
-  __syncthreads();
-  float var = 0.f;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) var += red[w];
-  var /= H;
-  const float rstd = rsqrtf(var + 1e-5f);
+  for (int c = 0; c < NCH; ++c) {
+    const int col = (c * NT + tid) * 8;
+    if (col < H)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { const float d = v[c][i] - mean; q += d * d; }
+  }
+  const float rstd = rsqrtf(block_sum<NT>(q, red[1]) / H + 1e-5f);
   if (tid == 0) { mean_out[r] = mean; rstd_out[r] = rstd; }
   T* yr = y + (int64_t)r * H;
-  for (int i = tid * 8; i < H; i += 2048) {
-    float v[8], g[8], b[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = row[i + j];
-    load8<float>(gam + i, g);
-    load8<float>(bet + i, b);
+  for (int c = 0; c < NCH; ++c) {
+    const int col = (c * NT + tid) * 8;
+    if (col < H) {
+      float g[8], b[8], o[8];
+      load8<float>(gam + col, g);
+      load8<float>(bet + col, b);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = (v[j] - mean) * rstd * g[j] + b[j];
-    store8<T>(yr + i, v);
+      for (int i = 0; i < 8; ++i) o[i] = (v[c][i] - mean) * rstd * g[i] + b[i];
+      store8<T>(yr + col, o);
+    }
   }
 }
 
-// dx = resid + rstd * (dxhat - mean(dxhat) - xhat * mean(dxhat * xhat)),  dxhat = dy * gamma;
-// dgamma += dy * xhat, dbeta += dy (fp32 atomics).
-template <typename T>
-__global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
-                                                     const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
-                                                     const float* __restrict__ gam, const float* __restrict__ resid,
-                                                     float* __restrict__ dx_out, T* __restrict__ dx_copy,
-                                                     float* __restrict__ dgam, float* __restrict__ dbet, int H) {
-  __shared__ float red[2][8];
-  const int r = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const float mean = mean_in[r], rstd = rstd_in[r];
-  const float* dyr = dy + (int64_t)r * H;
-  const float* xr = x + (int64_t)r * H;
-  float s1 = 0.f, s2 = 0.f;
-  for (int i = tid; i < H; i += 256) {
-    const float xh = (xr[i] - mean) * rstd;
-    const float dxh = dyr[i] * gam[i];
-    s1 += dxh;
-    s2 += dxh * xh;
-  }
-  s1 = warp_sum(s1);
-  s2 = warp_sum(s2);
-  if (lane == 0) { red[0][wid] = s1; red[1][wid] = s2; }
-  __syncthreads();
-  float m1 = 0.f, m2 = 0.f;
+// dx = resid + rstd * (dxhat - mean(dxhat) - xhat * mean(dxhat * xhat)),  dxhat = dy * gamma.
+// A CTA handles `rpb` consecutive rows and keeps its dgamma/dbeta partial sums in registers, so the
+// fp32 atomics are one per column per CTA (not per row).
+template <typename T, int NT, int NCH>
+__global__ void __launch_bounds__(NT) ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
+                                                    const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
+                                                    const float* __restrict__ gam, const float* __restrict__ resid,
+                                                    float* __restrict__ dx_out, T* __restrict__ dx_copy,
+                                                    float* __restrict__ dgam, float* __restrict__ dbet, int rows, int H,
+                                                    int rpb) {
+  __shared__ float red[2][2][NT / 32];
+  const int tid = threadIdx.x;
+  float g[NCH][8], pg[NCH][8], pb[NCH][8];
 #pragma unroll
-  for (int w = 0; w < 8; ++w) { m1 += red[0][w]; m2 += red[1][w]; }
-  m1 /= H;
-  m2 /= H;
-  for (int i = tid; i < H; i += 256) {
-    const float xh = (xr[i] - mean) * rstd;
-    const float d = dyr[i];
-    float dx = rstd * (d * gam[i] - m1 - xh * m2);
-    if (resid) dx += resid[(int64_t)r * H + i];
-    dx_out[(int64_t)r * H + i] = dx;
-    if (dx_copy) dx_copy[(int64_t)r * H + i] = from_f<T>(dx);
-    atomicAdd(dgam + i, d * xh);
-    atomicAdd(dbet + i, d);
+  for (int c = 0; c < NCH; ++c) {
+    const int col = (c * NT + tid) * 8;
+    if (col < H) load8<float>(gam + col, g[c]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { pg[c][i] = 0.f; pb[c][i] = 0.f; if (col >= H) g[c][i] = 0.f; }
+  }
+  const int r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
+  for (int r = r0; r < r1; ++r) {
+    const float mean = mean_in[r], rstd = rstd_in[r];
+    float d[NCH][8], xh[NCH][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const int col = (c * NT + tid) * 8;
+      if (col < H) {
+        load8<float>(dy + (int64_t)r * H + col, d[c]);
+        load8<float>(x + (int64_t)r * H + col, xh[c]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { d[c][i] = 0.f; xh[c][i] = 0.f; }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        xh[c][i] = (xh[c][i] - mean) * rstd;
+        const float dxh = d[c][i] * g[c][i];
+        s1 += dxh;
+        s2 += dxh * xh[c][i];
+        pg[c][i] += d[c][i] * xh[c][i];
+        pb[c][i] += d[c][i];
+      }
+    }
+    // two block reductions sharing one barrier; buffers alternate with the row parity
+    float (*rd)[NT / 32] = red[r & 1];
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if ((tid & 31) == 0) { rd[0][tid >> 5] = s1; rd[1][tid >> 5] = s2; }
+    __syncthreads();
+    float m1 = 0.f, m2 = 0.f;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) { m1 += rd[0][w]; m2 += rd[1][w]; }
+    m1 /= H;
+    m2 /= H;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const int col = (c * NT + tid) * 8;
+      if (col < H) {
+        float o[8], rs[8];
+        if (resid) load8<float>(resid + (int64_t)r * H + col, rs);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = rstd * (d[c][i] * g[c][i] - m1 - xh[c][i] * m2) + (resid ? rs[i] : 0.f);
+        store8<float>(dx_out + (int64_t)r * H + col, o);
+        if (dx_copy) store8<T>(dx_copy + (int64_t)r * H + col, o);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int col = (c * NT + tid) * 8;
+    if (col < H && r0 < r1)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { atomicAdd(dgam + col + i, pg[c][i]); atomicAdd(dbet + col + i, pb[c][i]); }
   }
 }
 
@@ -220,7 +269,11 @@ template <typename T>
 cudaError_t layernorm_fwd(const float* x, const float* gam, const float* bet, T* y, float* mean, float* rstd,
                           int rows, int H, cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
-  ln_fwd_kernel<T><<<rows, 256, H * sizeof(float), st>>>(x, gam, bet, y, mean, rstd, H);
+  if (H <= 2048) ln_fwd_kernel<T, 256, 1><<<rows, 256, 0, st>>>(x, gam, bet, y, mean, rstd, H);
+  else if (H <= 4096) ln_fwd_kernel<T, 256, 2><<<rows, 256, 0, st>>>(x, gam, bet, y, mean, rstd, H);
+  else if (H <= 6144) ln_fwd_kernel<T, 256, 3><<<rows, 256, 0, st>>>(x, gam, bet, y, mean, rstd, H);
+  else if (H <= 12288) ln_fwd_kernel<T, 512, 3><<<rows, 512, 0, st>>>(x, gam, bet, y, mean, rstd, H);
+  else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 template <typename T>
@@ -228,7 +281,15 @@ cudaError_t layernorm_bwd(const float* dy, const float* x, const float* mean, co
                           const float* resid, float* dx_out, T* dx_copy, float* dgam, float* dbet, int rows, int H,
                           cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
-  ln_bwd_kernel<T><<<rows, 256, 0, st>>>(dy, x, mean, rstd, gam, resid, dx_out, dx_copy, dgam, dbet, H);
+  const int rpb = std::max(1, std::min(32, (rows + 295) / 296));
+  const int grid = (rows + rpb - 1) / rpb;
+#define LNB(NT, NCH) ln_bwd_kernel<T, NT, NCH><<<grid, NT, 0, st>>>(dy, x, mean, rstd, gam, resid, dx_out, dx_copy, dgam, dbet, rows, H, rpb)
+  if (H <= 2048) LNB(256, 1);
+  else if (H <= 4096) LNB(256, 2);
+  else if (H <= 6144) LNB(256, 3);
+  else if (H <= 12288) LNB(512, 3);
+  else return cudaErrorInvalidValue;
+#undef LNB
   return cudaGetLastError();
 }
 cudaError_t embed_fwd(const int32_t* tok, const float* wte, const float* wpe, float* h, int c, int l, int H, int V,
