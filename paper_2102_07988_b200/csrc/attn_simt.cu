@@ -136,16 +136,20 @@ __global__ void __launch_bounds__(WARPS * 32) attn_bwd_dkv_kernel(const T* __res
   }
 }
 
+// dQKV[r][H + i] = dK_acc[head][c + r][e], dQKV[r][2H + i] = dV_acc[...] (i = head*d + e), 8-wide.
 template <typename T>
 __global__ void dkv_finalize_kernel(const float* __restrict__ dk_acc, const float* __restrict__ dv_acc,
                                     T* __restrict__ dqkv, int64_t ld, int a, int s, int d, int c) {
   const int r = blockIdx.x;
   const int H = a * d;
-  for (int i = threadIdx.x; i < H; i += blockDim.x) {
+  for (int i = threadIdx.x * 8; i < H; i += blockDim.x * 8) {
     const int head = i / d, e = i - head * d;
     const int64_t src = ((int64_t)head * s + c + r) * d + e;
-    dqkv[(int64_t)r * ld + H + i] = from_f<T>(dk_acc[src]);
-    dqkv[(int64_t)r * ld + 2 * H + i] = from_f<T>(dv_acc[src]);
+    float v[8];
+    load8<float>(dk_acc + src, v);
+    store8<T>(dqkv + (int64_t)r * ld + H + i, v);
+    load8<float>(dv_acc + src, v);
+    store8<T>(dqkv + (int64_t)r * ld + 2 * H + i, v);
   }
 }
 }  // namespace

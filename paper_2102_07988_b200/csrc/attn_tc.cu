@@ -220,18 +220,29 @@ __global__ void __launch_bounds__(NWARP * 32) attn_fwd_tc_kernel(const bf16* __r
 }
 
 // ======================================================================== backward
-// D[head][r] = rowsum(dO * O) (warp per (row, head)).
+// D[head][r] = rowsum(dO * O): one warp per row, lanes take 8-element chunks of all heads.
 template <int D>
 __global__ void attn_bwd_prep_kernel(const bf16* __restrict__ dO, int64_t ld_do, const bf16* __restrict__ o,
-                                     int64_t ldo, float* __restrict__ Dvec, int l) {
+                                     int64_t ldo, float* __restrict__ Dvec, int a, int l) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int r = blockIdx.x * 4 + w, head = blockIdx.y;
+  const int r = blockIdx.x * 4 + w;
   if (r >= l) return;
-  float acc = 0.f;
-  for (int e = lane; e < D; e += 32)
-    acc += __bfloat162float(dO[(int64_t)r * ld_do + head * D + e]) * __bfloat162float(o[(int64_t)r * ldo + head * D + e]);
-  acc = warp_sum(acc);
-  if (lane == 0) Dvec[(int64_t)head * l + r] = acc;
+  constexpr int CPH = D / 8;  // chunks per head (2..16)
+  for (int base = 0; base < a * CPH; base += 32) {
+    const int ch = base + lane;
+    float acc = 0.f;
+    if (ch < a * CPH) {
+      float x[8], y[8];
+      load8<bf16>(dO + (int64_t)r * ld_do + ch * 8, x);
+      load8<bf16>(o + (int64_t)r * ldo + ch * 8, y);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc += x[i] * y[i];
+    }
+    // reduce groups of CPH consecutive lanes (one head each)
+#pragma unroll
+    for (int off = 1; off < CPH && off < 32; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (CPH <= 32 && ch < a * CPH && (lane % CPH) == 0) Dvec[(int64_t)(ch / CPH) * l + r] = acc;
+  }
 }
 
 // dQ: per (64-row query tile, head).
@@ -520,7 +531,7 @@ cudaError_t bwd_d(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ldo, con
     attr = true;
   }
   const float scale = rsqrtf((float)D);
-  attn_bwd_prep_kernel<D><<<dim3((l + 3) / 4, a), 128, 0, st>>>(dO, ld_do, o, ldo, Dvec, l);
+  attn_bwd_prep_kernel<D><<<dim3((l + 3) / 4), 128, 0, st>>>(dO, ld_do, o, ldo, Dvec, a, l);
   attn_bwd_dq_kernel<D><<<dim3((l + BQ - 1) / BQ, a), NWARP * 32, smem_q, st>>>(dO, ld_do, q, k, v, lse, Dvec, dq, ldq, s,
                                                                                 c, l, scale, scale * LOG2E);
   attn_bwd_dkv_kernel<D><<<dim3((c + l + BKEY - 1) / BKEY, a), NWARP * 32, smem_kv, st>>>(

@@ -253,14 +253,33 @@ __global__ void transpose_kernel(const float* __restrict__ src, T* __restrict__ 
   }
 }
 
+// out[n] += sum_r src[r][n]: a CTA covers 256 columns (32 lanes x 8, 16-byte loads) and 256 rows
+// (8 warps striding the rows), reduces across warps in shared memory, one atomic per column.
 template <typename T>
-__global__ void colsum_kernel(const T* __restrict__ src, int64_t ld, float* __restrict__ out, int rows, int N) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
-  const int r0 = blockIdx.y * 128, r1 = min(rows, r0 + 128);
-  float s = 0.f;
-  for (int r = r0; r < r1; ++r) s += to_f<T>(src[(int64_t)r * ld + n]);
-  atomicAdd(out + n, s);
+__global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ src, int64_t ld, float* __restrict__ out,
+                                                     int rows, int N) {
+  __shared__ float red[8][256 + 8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int n0 = blockIdx.x * 256 + lane * 8;
+  const int r0 = blockIdx.y * 256, r1 = min(rows, r0 + 256);
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (n0 < N)
+    for (int r = r0 + w; r < r1; r += 8) {
+      float v[8];
+      load8<T>(src + (int64_t)r * ld + n0, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += v[i];
+    }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) red[w][lane * 8 + i] = acc[i];
+  __syncthreads();
+  const int n = blockIdx.x * 256 + threadIdx.x;
+  if (n < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k][threadIdx.x];
+    atomicAdd(out + n, t);
+  }
 }
 
 }  // namespace
@@ -281,7 +300,7 @@ cudaError_t layernorm_bwd(const float* dy, const float* x, const float* mean, co
                           const float* resid, float* dx_out, T* dx_copy, float* dgam, float* dbet, int rows, int H,
                           cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
-  const int rpb = std::max(1, std::min(32, (rows + 295) / 296));
+  const int rpb = std::max(1, std::min(16, (rows + 4 * 148 - 1) / (4 * 148)));
   const int grid = (rows + rpb - 1) / rpb;
 #define LNB(NT, NCH) ln_bwd_kernel<T, NT, NCH><<<grid, NT, 0, st>>>(dy, x, mean, rstd, gam, resid, dx_out, dx_copy, dgam, dbet, rows, H, rpb)
   if (H <= 2048) LNB(256, 1);
@@ -331,7 +350,7 @@ cudaError_t transpose_convert(const float* src, T* dst, int R, int C, cudaStream
 template <typename T>
 cudaError_t colsum_accum(const T* src, int64_t ld, float* out, int rows, int N, cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
-  dim3 grid((N + 255) / 256, (rows + 127) / 128);
+  dim3 grid((N + 255) / 256, (rows + 255) / 256);
   colsum_kernel<T><<<grid, 256, 0, st>>>(src, ld, out, rows, N);
   return cudaGetLastError();
 }
