@@ -1,0 +1,281 @@
+// attn_sm100.cu — slice-vs-prefix causal attention on 5th-generation tensor cores (head_dim 128).
+//
+// Same contract as attn_tc.cu (Eq. 2; one job = one sequence's slice rows
+// [c, c+l) attending keys [0, c+r] of the per-layer prefix K/V cache [a][s][d]), for d = 128.
+//
+// Forward, per (128-query tile, head), 6 warps:
+//   warp 0  TMA producer: Q once, then K_j / V_j 128-key blocks (3-D maps [a][c+l][d], rows past
+//           the prefix zero-filled) into a 2-deep ring;
+//   warp 1  MMA issuer (one thread): S_j = Q K_j^T -> TMEM (2 buffers x 128 fp32 columns), and
+//           O_j = P_j V_j -> TMEM (2 buffers) with P_j read from shared memory (K-major) and V_j as
+//           an MN-major operand (no transpose pass);
+//   warps 2-5 softmax: thread t owns query row t (its TMEM lane), so row max / sum need no
+//           shuffles: pass 1 reads S_j for the max, pass 2 writes P_j = exp2(S_j*scale - m) as bf16
+//           into the 128B-swizzled P tile; O is accumulated in registers, o = o*exp2(m_old-m_j) + O_j.
+// Key blocks are aligned to absolute multiples of 128; only blocks crossing a query's position are
+// masked element-wise.
+#include "kernels.h"
+#include "tc5.cuh"
+
+namespace tp {
+
+namespace {
+
+using namespace tc5;
+
+constexpr int AT = 128;                   // query rows per CTA, keys per block, head dim
+constexpr uint32_t TILE = AT * AT * 2;    // one 128 x 128 bf16 tile (two 64-column swizzle atoms)
+constexpr uint32_t HALF = TILE / 2;       // 16 KiB: second 64-column atom
+constexpr float LOG2E_F = 1.4426950408889634f;
+
+struct FwdSmem {
+  static constexpr uint32_t Q = 0, K0 = TILE, V0 = 2 * TILE, K1 = 3 * TILE, V1 = 4 * TILE, P = 5 * TILE;
+  static constexpr uint32_t BAR = 6 * TILE;
+  static constexpr uint32_t BYTES = BAR + 256 + 1024;
+};
+
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// byte offset of 16-byte chunk `cc` (0..7) of row `row` inside a 128B-swizzled K-major atom region
+__device__ __forceinline__ uint32_t swz(int row, int cc) {
+  return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((cc ^ (row & 7)) << 4));
+}
+
+__global__ void __launch_bounds__(192, 1)
+    attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                          const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ o, int64_t ldo,
+                          float* __restrict__ lse, int s, int c, int l, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + FwdSmem::BAR);
+  uint64_t* qfull = bars + 0;
+  uint64_t* kvfull = bars + 1;   // [2]
+  uint64_t* kvfree = bars + 3;   // [2]
+  uint64_t* sfull = bars + 5;    // [2]
+  uint64_t* sfree = bars + 7;    // [2]
+  uint64_t* pfull = bars + 9;
+  uint64_t* pfree = bars + 10;
+  uint64_t* ofull = bars + 11;   // [2]
+  uint64_t* ofree = bars + 13;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int head = blockIdx.y, r0 = blockIdx.x * AT;
+  const int qlast = c + min(l, r0 + AT) - 1;
+  const int nkb = qlast / AT + 1;
+
+  if (threadIdx.x == 0) {
+    mbar_init(qfull, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(kvfull + i, 1); mbar_init(kvfree + i, 1);
+      mbar_init(sfull + i, 1); mbar_init(sfree + i, 4);
+      mbar_init(ofull + i, 1); mbar_init(ofree + i, 4);
+    }
+    mbar_init(pfull, 4);
+    mbar_init(pfree, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    mbar_expect_tx(qfull, TILE);
+    tma_load_3d(sm + FwdSmem::Q, &tmQ, 0, c + r0, head, qfull);
+    tma_load_3d(sm + FwdSmem::Q + HALF, &tmQ, 64, c + r0, head, qfull);
+    for (int j = 0; j < nkb; ++j) {
+      const int b = j & 1;
+      if (j >= 2) mbar_wait(kvfree + b, ((j >> 1) - 1) & 1);
+      uint8_t* kd = sm + (b ? FwdSmem::K1 : FwdSmem::K0);
+      uint8_t* vd = sm + (b ? FwdSmem::V1 : FwdSmem::V0);
+      mbar_expect_tx(kvfull + b, 2 * TILE);
+      tma_load_3d(kd, &tmK, 0, j * AT, head, kvfull + b);
+      tma_load_3d(kd + HALF, &tmK, 64, j * AT, head, kvfull + b);
+      tma_load_3d(vd, &tmV, 0, j * AT, head, kvfull + b);
+      tma_load_3d(vd + HALF, &tmV, 64, j * AT, head, kvfull + b);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idS = idesc_bf16(128, 128, false, false);
+    constexpr uint32_t idO = idesc_bf16(128, 128, false, true);
+    const uint32_t q_base = smem_u32(sm + FwdSmem::Q), p_base = smem_u32(sm + FwdSmem::P);
+    auto pv = [&](int i) {
+      const int bi = i & 1;
+      mbar_wait(pfull, i & 1);
+      if (i >= 2) mbar_wait(ofree + bi, ((i >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t v_base = smem_u32(sm + (bi ? FwdSmem::V1 : FwdSmem::V0));
+#pragma unroll
+      for (int kk = 0; kk < AT / 16; ++kk) {
+        const uint64_t ad = make_desc(p_base + (kk >> 2) * HALF + (kk & 3) * 32, 16, 1024);
+        const uint64_t bd = make_desc(v_base + kk * 2048, HALF, 1024);
+        mma_bf16(tmem + 256 + bi * 128, ad, bd, idO, kk > 0);
+      }
+      mma_commit(ofull + bi);
+      mma_commit(pfree);
+      mma_commit(kvfree + bi);
+    };
+    mbar_wait(qfull, 0);
+    for (int j = 0; j < nkb; ++j) {
+      const int b = j & 1;
+      mbar_wait(kvfull + b, (j >> 1) & 1);
+      if (j >= 2) mbar_wait(sfree + b, ((j >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t k_base = smem_u32(sm + (b ? FwdSmem::K1 : FwdSmem::K0));
+#pragma unroll
+      for (int kk = 0; kk < AT / 16; ++kk) {
+        const uint32_t off = (kk >> 2) * HALF + (kk & 3) * 32;
+        mma_bf16(tmem + b * 128, make_desc(q_base + off, 16, 1024), make_desc(k_base + off, 16, 1024), idS, kk > 0);
+      }
+      mma_commit(sfull + b);
+      if (j >= 1) pv(j - 1);
+    }
+    pv(nkb - 1);
+  } else if (warp >= 2) {
+    // ---------------- softmax / output: thread owns query row `row`
+    const int q = warp & 3, row = q * 32 + lane;
+    const int qabs = c + r0 + row;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    uint8_t* P = sm + FwdSmem::P;
+    float m = -INFINITY, lsum = 0.f, m_acc = -INFINITY, m_last = -INFINITY;
+    float acc[AT];
+#pragma unroll
+    for (int i = 0; i < AT; ++i) acc[i] = 0.f;
+    auto add_o = [&](int i, float m_i) {
+      const int bi = i & 1;
+      mbar_wait(ofull + bi, (i >> 1) & 1);
+      tc_fence_after();
+      const float sc = exp2f(m_acc - m_i);
+#pragma unroll
+      for (int ch = 0; ch < AT / 32; ++ch) {
+        uint32_t r[32];
+        tmem_ld32_nowait(lane_base + 256 + bi * 128 + ch * 32, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int t = 0; t < 32; ++t) acc[ch * 32 + t] = acc[ch * 32 + t] * sc + __uint_as_float(r[t]);
+      }
+      m_acc = m_i;
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ofree + bi);
+    };
+    for (int j = 0; j < nkb; ++j) {
+      const int b = j & 1;
+      mbar_wait(sfull + b, (j >> 1) & 1);
+      tc_fence_after();
+      const int key0 = j * AT;
+      const bool diag = key0 + AT - 1 > qabs;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int ch = 0; ch < AT / 32; ++ch) {
+        uint32_t r[32];
+        tmem_ld32_nowait(lane_base + b * 128 + ch * 32, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const float x = (diag && key0 + ch * 32 + t > qabs) ? -INFINITY : __uint_as_float(r[t]) * scale_log2;
+          mx = fmaxf(mx, x);
+        }
+      }
+      const float m_new = fmaxf(m, mx);
+      if (j >= 1) mbar_wait(pfree, (j - 1) & 1);  // PV_{j-1} has finished reading the P tile
+      float rs = 0.f;
+#pragma unroll
+      for (int ch = 0; ch < AT / 32; ++ch) {
+        uint32_t r[32];
+        tmem_ld32_nowait(lane_base + b * 128 + ch * 32, r);
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int t = 0; t < 32; t += 2) {
+          const int k0i = key0 + ch * 32 + t;
+          const float x0 = (diag && k0i > qabs) ? -INFINITY : __uint_as_float(r[t]) * scale_log2;
+          const float x1 = (diag && k0i + 1 > qabs) ? -INFINITY : __uint_as_float(r[t + 1]) * scale_log2;
+          const float p0 = exp2f(x0 - m_new), p1 = exp2f(x1 - m_new);
+          rs += p0 + p1;
+          __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+          pk[t >> 1] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        uint8_t* region = P + (ch >> 1) * HALF;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int cc = (ch & 1) * 4 + u;
+          *reinterpret_cast<uint4*>(region + swz(row, cc)) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+      }
+      tc_fence_before();
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) { mbar_arrive(sfree + b); mbar_arrive(pfull); }
+      lsum = lsum * exp2f(m - m_new) + rs;
+      m_last = m;
+      m = m_new;
+      if (j >= 1) add_o(j - 1, m_last);
+    }
+    add_o(nkb - 1, m);
+    const int r = r0 + row;
+    if (r < l) {
+      const float inv = 1.f / lsum;
+      bf16* orow = o + (int64_t)r * ldo + head * AT;
+#pragma unroll
+      for (int i = 0; i < AT; i += 8) {
+        float v8[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v8[t] = acc[i + t] * inv;
+        store8<bf16>(orow + i, v8);
+      }
+      lse[(int64_t)head * s + c + r] = (m + log2f(lsum)) / LOG2E_F;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace
+
+bool attn_sm100_supported(int d) { return d == AT; }
+
+cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o, int64_t ldo, float* lse, int a, int s,
+                           int d, int c, int l, cudaStream_t st) {
+  if (l == 0) return cudaSuccess;
+  if (d != AT) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)FwdSmem::BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  // [a][s][d] viewed as 3-D {d, rows = c + l (prefix), a}: rows past the prefix are zero-filled
+  const uint64_t dims[3] = {(uint64_t)d, (uint64_t)(c + l), (uint64_t)a};
+  const uint64_t strides[2] = {(uint64_t)d * 2, (uint64_t)s * d * 2};
+  const uint32_t box[3] = {64, AT, 1};
+  CUtensorMap mq, mk, mv;
+  if (!encode_bf16_map(&mq, q, 3, dims, strides, box) || !encode_bf16_map(&mk, k, 3, dims, strides, box) ||
+      !encode_bf16_map(&mv, v, 3, dims, strides, box))
+    return cudaErrorInvalidValue;
+  dim3 grid((l + AT - 1) / AT, a);
+  attn_fwd_sm100_kernel<<<grid, 192, FwdSmem::BYTES, st>>>(mq, mk, mv, o, ldo, lse, s, c, l,
+                                                           rsqrtf((float)d) * LOG2E_F);
+  return cudaGetLastError();
+}
+
+}  // namespace tp

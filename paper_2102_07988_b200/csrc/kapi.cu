@@ -37,7 +37,9 @@ extern "C" tp_status tpk_attention_fwd(const void* q, const void* k, const void*
   TP_CHECK_ARG(a >= 1 && d % 16 == 0 && d <= 128 && c >= 0 && l >= 0 && c + l <= s, "tpk_attention_fwd: bad shape");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bf16 *Q = (const bf16*)q, *Kp = (const bf16*)k, *Vp = (const bf16*)v;
-  if (impl == 0) return cu(attn_fwd_tc(Q, Kp, Vp, (bf16*)o, (int64_t)a * d, lse, a, s, d, c, l, st), "attn_fwd_tc");
+  if (impl == 0 && attn_sm100_supported(d))
+    return cu(attn_fwd_sm100(Q, Kp, Vp, (bf16*)o, (int64_t)a * d, lse, a, s, d, c, l, st), "attn_fwd_sm100");
+  if (impl == 0 || impl == 2) return cu(attn_fwd_tc(Q, Kp, Vp, (bf16*)o, (int64_t)a * d, lse, a, s, d, c, l, st), "attn_fwd_tc");
   return cu(attn_fwd_simt<bf16>(Q, Kp, Vp, (bf16*)o, (int64_t)a * d, lse, a, s, d, c, l, st), "attn_fwd_simt");
 }
 
@@ -52,7 +54,7 @@ extern "C" tp_status tpk_attention_bwd(const void* dO, const void* o, const void
   tp_status r = cu(cudaMallocAsync(&Dvec, sizeof(float) * a * l, st), "cudaMallocAsync");
   if (r != TP_OK) return r;
   const int64_t H = (int64_t)a * d;
-  if (impl == 0)
+  if (impl == 0 || impl == 2)
     r = cu(attn_bwd_tc((const bf16*)dO, H, (const bf16*)o, H, (const bf16*)q, (const bf16*)k, (const bf16*)v, lse, Dvec,
                        (bf16*)dq, ldq, dk_acc, dv_acc, a, s, d, c, l, accumulate, st), "attn_bwd_tc");
   else

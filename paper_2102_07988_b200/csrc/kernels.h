@@ -33,7 +33,8 @@ cudaError_t layernorm_fwd(const float* x, const float* gam, const float* bet, T*
 template <typename T>
 cudaError_t layernorm_bwd(const float* dy, const float* x, const float* mean, const float* rstd,
                           const float* gam, const float* resid, float* dx_out, T* dx_copy,
-                          float* dgam, float* dbet, int rows, int H, cudaStream_t st);
+                          float* dgam, float* dbet, float* ws /* >= 2*H*ceil(rows/4) floats */, int rows, int H,
+                          cudaStream_t st);
 
 cudaError_t embed_fwd(const int32_t* tok, const float* wte, const float* wpe, float* h, int c, int l,
                       int H, int V, cudaStream_t st);
@@ -58,6 +59,10 @@ cudaError_t attn_fwd_tc(const bf16* q, const bf16* k, const bf16* v, bf16* o, in
 cudaError_t attn_bwd_tc(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ldo, const bf16* q, const bf16* k,
                         const bf16* v, const float* lse, float* Dvec, bf16* dq, int64_t ldq, float* dk_acc,
                         float* dv_acc, int a, int s, int d, int c, int l, int accumulate, cudaStream_t st);
+// tcgen05/TMEM attention (attn_sm100.cu), head_dim 128 only.
+bool attn_sm100_supported(int d);
+cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o, int64_t ldo, float* lse, int a, int s,
+                           int d, int c, int l, cudaStream_t st);
 template <typename T>
 cudaError_t attn_dkv_finalize(const float* dk_acc, const float* dv_acc, T* dqkv, int64_t ld, int a,
                               int s, int d, int c, int l, cudaStream_t st);

@@ -77,8 +77,7 @@ __global__ void __launch_bounds__(NT) ln_bwd_kernel(const float* __restrict__ dy
                                                     const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
                                                     const float* __restrict__ gam, const float* __restrict__ resid,
                                                     float* __restrict__ dx_out, T* __restrict__ dx_copy,
-                                                    float* __restrict__ dgam, float* __restrict__ dbet, int rows, int H,
-                                                    int rpb) {
+                                                    float* __restrict__ ws, int rows, int H, int rpb) {
   __shared__ float red[2][2][NT / 32];
   const int tid = threadIdx.x;
   float g[NCH][8], pg[NCH][8], pb[NCH][8];
@@ -138,13 +137,23 @@ __global__ void __launch_bounds__(NT) ln_bwd_kernel(const float* __restrict__ dy
       }
     }
   }
+  // per-CTA partial sums to the workspace [gridDim.x][2][H] (reduced by ln_bwd_reduce_kernel)
+  float* wg = ws + (int64_t)blockIdx.x * 2 * H;
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     const int col = (c * NT + tid) * 8;
-    if (col < H && r0 < r1)
-#pragma unroll
-      for (int i = 0; i < 8; ++i) { atomicAdd(dgam + col + i, pg[c][i]); atomicAdd(dbet + col + i, pb[c][i]); }
+    if (col < H) { store8<float>(wg + col, pg[c]); store8<float>(wg + H + col, pb[c]); }
   }
+}
+
+// dgamma[n] += sum_b ws[b][0][n], dbeta[n] += sum_b ws[b][1][n] (one writer per column).
+__global__ void ln_bwd_reduce_kernel(const float* __restrict__ ws, int nb, float* __restrict__ dgam,
+                                     float* __restrict__ dbet, int H) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= 2 * H) return;
+  float t = 0.f;
+  for (int b = 0; b < nb; ++b) t += ws[(int64_t)b * 2 * H + n];
+  if (n < H) dgam[n] += t; else dbet[n - H] += t;
 }
 
 // ---------------------------------------------------------------- embedding
@@ -297,18 +306,19 @@ cudaError_t layernorm_fwd(const float* x, const float* gam, const float* bet, T*
 }
 template <typename T>
 cudaError_t layernorm_bwd(const float* dy, const float* x, const float* mean, const float* rstd, const float* gam,
-                          const float* resid, float* dx_out, T* dx_copy, float* dgam, float* dbet, int rows, int H,
-                          cudaStream_t st) {
+                          const float* resid, float* dx_out, T* dx_copy, float* dgam, float* dbet, float* ws, int rows,
+                          int H, cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
-  const int rpb = std::max(1, std::min(16, (rows + 4 * 148 - 1) / (4 * 148)));
+  const int rpb = std::max(4, (rows + 4 * 148 - 1) / (4 * 148));
   const int grid = (rows + rpb - 1) / rpb;
-#define LNB(NT, NCH) ln_bwd_kernel<T, NT, NCH><<<grid, NT, 0, st>>>(dy, x, mean, rstd, gam, resid, dx_out, dx_copy, dgam, dbet, rows, H, rpb)
+#define LNB(NT, NCH) ln_bwd_kernel<T, NT, NCH><<<grid, NT, 0, st>>>(dy, x, mean, rstd, gam, resid, dx_out, dx_copy, ws, rows, H, rpb)
   if (H <= 2048) LNB(256, 1);
   else if (H <= 4096) LNB(256, 2);
   else if (H <= 6144) LNB(256, 3);
   else if (H <= 12288) LNB(512, 3);
   else return cudaErrorInvalidValue;
 #undef LNB
+  ln_bwd_reduce_kernel<<<(2 * H + 255) / 256, 256, 0, st>>>(ws, grid, dgam, dbet, H);
   return cudaGetLastError();
 }
 cudaError_t embed_fwd(const int32_t* tok, const float* wte, const float* wpe, float* h, int c, int l, int H, int V,
@@ -359,7 +369,7 @@ cudaError_t colsum_accum(const T* src, int64_t ld, float* out, int rows, int N, 
   template cudaError_t layernorm_fwd<T>(const float*, const float*, const float*, T*, float*, float*, int, int, \
                                         cudaStream_t);                                                      \
   template cudaError_t layernorm_bwd<T>(const float*, const float*, const float*, const float*, const float*,   \
-                                        const float*, float*, T*, float*, float*, int, int, cudaStream_t);  \
+                                        const float*, float*, T*, float*, float*, float*, int, int, cudaStream_t); \
   template cudaError_t ce_fwd_bwd<T>(T*, const int32_t*, float*, float*, int, int, float, cudaStream_t);   \
   template cudaError_t convert_f32<T>(const float*, T*, int64_t, cudaStream_t);                            \
   template cudaError_t transpose_convert<T>(const float*, T*, int, int, cudaStream_t);                     \

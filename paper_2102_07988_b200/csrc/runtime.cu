@@ -18,6 +18,7 @@
 #include <array>
 #include <type_traits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -181,7 +182,7 @@ struct Stage {
   // backward stash of ONE sequence (deferred dW)
   std::vector<T*> dQKV, dhmid_b, dU, dhout_b;
   std::vector<float*> dk_acc, dv_acc;  // [a][s][d]
-  float *gA = nullptr, *gB = nullptr, *gm = nullptr, *dA = nullptr, *Dvec = nullptr;
+  float *gA = nullptr, *gB = nullptr, *gm = nullptr, *dA = nullptr, *Dvec = nullptr, *lnws = nullptr;
   T* dO = nullptr;
 };
 
@@ -191,6 +192,7 @@ class Engine final : public EngineBase {
   ModelShape m;
   int rank, world, k0, k1, precision, flags, max_batch, device;
   bool force_simt;
+  bool legacy_attn = false;  // env TP_LEGACY_ATTN=1: mma.sync attention instead of tcgen05 (cross-checks)
   std::vector<Stage<T>> stages;
   std::vector<void*> allocs;
   int32_t* d_tokens = nullptr;
@@ -247,6 +249,7 @@ class Engine final : public EngineBase {
     rank = rank_; world = world_; precision = precision_; flags = flags_; max_batch = max_batch_; device = device_;
     force_simt = (flags & TP_FLAG_FORCE_SIMT) != 0 || precision == TP_FP32;
     instr.on = (flags & TP_FLAG_KERNEL_STATS) != 0;
+    if (const char* e = std::getenv("TP_LEGACY_ATTN")) legacy_attn = std::atoi(e) != 0;
     if (world == 1) { k0 = 0; k1 = m.K; } else { k0 = rank; k1 = rank + 1; }
     CU(cudaSetDevice(device));
     int major = 0;
@@ -327,6 +330,7 @@ class Engine final : public EngineBase {
     TRY(vec(S.dk_acc, nl, s * H)); TRY(vec(S.dv_acc, nl, s * H));
     TRY(alloc(&S.gA, s * H)); TRY(alloc(&S.gB, s * H)); TRY(alloc(&S.gm, s * H)); TRY(alloc(&S.dA, s * H));
     TRY(alloc(&S.Dvec, a * s)); TRY(alloc(&S.dO, s * H));
+    TRY(alloc(&S.lnws, 2 * H * ((s + 3) / 4)));
     return TP_OK;
   }
 
@@ -412,7 +416,10 @@ class Engine final : public EngineBase {
       TRY(launch(KC_ATTN_FWD, attn_flops, ebytes * (2.0 * H * (c + l) + 2.0 * H * l), [&] {
         const T *q = S.Q[j] + (size_t)d * s * H, *kk = S.Kc[j] + (size_t)d * s * H, *vv = S.Vc[j] + (size_t)d * s * H;
         if constexpr (std::is_same<T, bf16>::value)
-          if (!force_simt) return attn_fwd_tc(q, kk, vv, o, H, lse, a, s, dh, c, l, stream);
+          if (!force_simt) {
+            if (attn_sm100_supported(dh) && !legacy_attn) return attn_fwd_sm100(q, kk, vv, o, H, lse, a, s, dh, c, l, stream);
+            return attn_fwd_tc(q, kk, vv, o, H, lse, a, s, dh, c, l, stream);
+          }
         return attn_fwd_simt<T>(q, kk, vv, o, H, lse, a, s, dh, c, l, stream);
       }));
       Epi er; er.kind = EPI_RESID; er.bias = P + f.b_o; er.out = S.hmid[j] + row * H; er.ldo = H; er.resid = x; er.ldr = H;
@@ -455,7 +462,7 @@ class Engine final : public EngineBase {
       TRY(gemm(KC_GEMM_DX, gd(l, H, V, S.Z + row * V, V, false, S.wout_io, V, false), e));
       TRY(launch(KC_LN, 0, (12.0 + ebytes) * l * H, [&] {
         return layernorm_bwd<T>(S.dA, S.hs[S.nl] + row * H, S.stf + row, S.stf + (size_t)batch * s + row, P + S.L.lnf_g, nullptr, g,
-                                S.dhout_b[S.nl - 1] + (size_t)c * H, S.gflat + S.L.lnf_g, S.gflat + S.L.lnf_b, l, H, stream);
+                                S.dhout_b[S.nl - 1] + (size_t)c * H, S.gflat + S.L.lnf_g, S.gflat + S.L.lnf_b, S.lnws, l, H, stream);
       }));
     } else {
       TRY(launch(KC_MISC, 0, (4.0 + ebytes) * l * H, [&] {
@@ -474,7 +481,7 @@ class Engine final : public EngineBase {
       float* st2 = S.st2[j];
       TRY(launch(KC_LN, 0, (16.0 + ebytes) * l * H, [&] {
         return layernorm_bwd<T>(S.dA, S.hmid[j] + row * H, st2 + row, st2 + (size_t)batch * s + row, P + f.ln2_g, g, S.gm,
-                                S.dhmid_b[j] + (size_t)c * H, GR + f.ln2_g, GR + f.ln2_b, l, H, stream);
+                                S.dhmid_b[j] + (size_t)c * H, GR + f.ln2_g, GR + f.ln2_b, S.lnws, l, H, stream);
       }));
       // attention: dO = dh_mid W_o^T, then slice-vs-prefix attention backward with dK/dV push
       Epi e3; e3.kind = EPI_STORE; e3.out = S.dO; e3.ldo = H;
@@ -501,7 +508,7 @@ class Engine final : public EngineBase {
       float* st1 = S.st1[j];
       TRY(launch(KC_LN, 0, (16.0 + ebytes) * l * H, [&] {
         return layernorm_bwd<T>(S.dA, S.hs[j] + row * H, st1 + row, st1 + (size_t)batch * s + row, P + f.ln1_g, S.gm, gnext, copy,
-                                GR + f.ln1_g, GR + f.ln1_b, l, H, stream);
+                                GR + f.ln1_g, GR + f.ln1_b, S.lnws, l, H, stream);
       }));
       g = gnext;
     }

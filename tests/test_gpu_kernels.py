@@ -58,7 +58,7 @@ def attn_ref(q, k, v, c, l):
 
 @pytest.mark.parametrize("a,s,d,c,l", [(2, 200, 128, 72, 96), (3, 64, 16, 0, 64), (2, 512, 128, 448, 64),
                                        (1, 300, 64, 0, 300), (4, 256, 32, 100, 37), (2, 2048, 128, 1536, 512)])
-@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("impl", [0, 1, 2])
 def test_attention_fwd_bwd(a, s, d, c, l, impl):
     g = torch.Generator(device="cpu").manual_seed(a * 1000 + s + c + l)
     q, k, v = (torch.randn(a, s, d, generator=g).to(dev, torch.bfloat16) for _ in range(3))
