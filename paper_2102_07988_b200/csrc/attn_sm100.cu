@@ -249,6 +249,252 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// ======================================================================== backward
+// Per (128-key block of the prefix [0, c+l), head); loop over the slice's 64-query tiles that can
+// see the block. TMEM: S^T [128 keys x 64 q] (cols 0-63), dP^T (64-127), dV (128-255),
+// dK (256-383), dQ^T [128 d x 64 q] (384-447).
+//   S^T = K Q^T, dP^T = V dO^T                                  (M=128 keys, N=64, K=d)
+//   softmax warps (thread = key row): P^T = exp2(S^T scale - lse), dS^T = P^T (dP^T - D) -> smem
+//   dV += P^T dO, dK += dS^T Q                                  (M=128 keys, N=d, K=64; Q/dO as MN-major B)
+//   dQ^T = K^T dS^T                                             (M=d, N=64 q, K=128 keys; K as MN-major A)
+//   dQ^T is drained by the softmax warps with coalesced fp32 reductions into dq_acc[l][H];
+//   dK (x scale) / dV are written or added to the fp32 prefix accumulators once per key row.
+constexpr int BQB = 64;                          // query rows per tile (backward)
+constexpr uint32_t QT = BQB * AT * 2;            // 16 KiB: [64 q][128 d]
+constexpr uint32_t QHALF = QT / 2;               // 8 KiB: second 64-column atom
+constexpr uint32_t PT = AT * BQB * 2;            // 16 KiB: [128 keys][64 q] (one atom wide)
+
+struct BwdSmem {
+  static constexpr uint32_t K = 0, V = TILE, Q0 = 2 * TILE, Q1 = Q0 + QT, O0 = Q1 + QT, O1 = O0 + QT;
+  static constexpr uint32_t P = O1 + QT, DS = P + PT, BAR = DS + PT;
+  static constexpr uint32_t BYTES = BAR + 256 + 1024;
+};
+
+__global__ void __launch_bounds__(192, 1)
+    attn_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                          const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
+                          const float* __restrict__ lse, const float* __restrict__ Dvec, float* __restrict__ dq_acc,
+                          int64_t ldq, float* __restrict__ dk_acc, float* __restrict__ dv_acc, int s, int c, int l,
+                          float scale, float scale_log2, int accumulate) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + BwdSmem::BAR);
+  uint64_t* kvfull = bars + 0;
+  uint64_t* qfull = bars + 1;    // [2]
+  uint64_t* qfree = bars + 3;    // [2]
+  uint64_t* sfull = bars + 5;
+  uint64_t* sfree = bars + 6;
+  uint64_t* pfull = bars + 7;
+  uint64_t* pfree = bars + 8;
+  uint64_t* dqfull = bars + 9;
+  uint64_t* dqfree = bars + 10;
+  uint64_t* done = bars + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int head = blockIdx.y, key0 = blockIdx.x * AT;
+  const int nkeys = c + l;
+  const int qt0 = max(0, key0 - c) / BQB, nqt = (l + BQB - 1) / BQB;
+  const int ntile = nqt - qt0;  // >= 1 because key0 < c + l
+
+  if (threadIdx.x == 0) {
+    mbar_init(kvfull, 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(qfull + i, 1); mbar_init(qfree + i, 1); }
+    mbar_init(sfull, 1); mbar_init(sfree, 4);
+    mbar_init(pfull, 4); mbar_init(pfree, 1);
+    mbar_init(dqfull, 1); mbar_init(dqfree, 4);
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t T_S = 0, T_DP = 64, T_DV = 128, T_DK = 256, T_DQ = 384;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer: K, V once; Q_i, dO_i double-buffered
+    mbar_expect_tx(kvfull, 2 * TILE);
+    tma_load_3d(sm + BwdSmem::K, &tmK, 0, key0, head, kvfull);
+    tma_load_3d(sm + BwdSmem::K + HALF, &tmK, 64, key0, head, kvfull);
+    tma_load_3d(sm + BwdSmem::V, &tmV, 0, key0, head, kvfull);
+    tma_load_3d(sm + BwdSmem::V + HALF, &tmV, 64, key0, head, kvfull);
+    for (int i = 0; i < ntile; ++i) {
+      const int b = i & 1, qt = qt0 + i;
+      if (i >= 2) mbar_wait(qfree + b, ((i >> 1) - 1) & 1);
+      uint8_t* qd = sm + (b ? BwdSmem::Q1 : BwdSmem::Q0);
+      uint8_t* od = sm + (b ? BwdSmem::O1 : BwdSmem::O0);
+      mbar_expect_tx(qfull + b, 2 * QT);
+      tma_load_3d(qd, &tmQ, 0, c + qt * BQB, head, qfull + b);
+      tma_load_3d(qd + QHALF, &tmQ, 64, c + qt * BQB, head, qfull + b);
+      tma_load_2d(od, &tmdO, head * AT, qt * BQB, qfull + b);
+      tma_load_2d(od + QHALF, &tmdO, head * AT + 64, qt * BQB, qfull + b);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idS = idesc_bf16(128, BQB, false, false);   // S^T, dP^T
+    constexpr uint32_t idKV = idesc_bf16(128, 128, false, true);   // dV, dK (B = dO / Q, MN-major)
+    constexpr uint32_t idQ = idesc_bf16(128, BQB, true, true);     // dQ^T (A = K MN-major, B = dS^T MN-major)
+    const uint32_t k_base = smem_u32(sm + BwdSmem::K), v_base = smem_u32(sm + BwdSmem::V);
+    const uint32_t p_base = smem_u32(sm + BwdSmem::P), ds_base = smem_u32(sm + BwdSmem::DS);
+    mbar_wait(kvfull, 0);
+    for (int i = 0; i < ntile; ++i) {
+      const int b = i & 1;
+      const uint32_t q_base = smem_u32(sm + (b ? BwdSmem::Q1 : BwdSmem::Q0));
+      const uint32_t o_base = smem_u32(sm + (b ? BwdSmem::O1 : BwdSmem::O0));
+      mbar_wait(qfull + b, (i >> 1) & 1);
+      if (i >= 1) mbar_wait(sfree, (i - 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < AT / 16; ++kk) {
+        const uint32_t ok = (kk >> 2) * HALF + (kk & 3) * 32, oq = (kk >> 2) * QHALF + (kk & 3) * 32;
+        mma_bf16(tmem + T_S, make_desc(k_base + ok, 16, 1024), make_desc(q_base + oq, 16, 1024), idS, kk > 0);
+        mma_bf16(tmem + T_DP, make_desc(v_base + ok, 16, 1024), make_desc(o_base + oq, 16, 1024), idS, kk > 0);
+      }
+      mma_commit(sfull);
+      mbar_wait(pfull, i & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < BQB / 16; ++kk) {
+        mma_bf16(tmem + T_DV, make_desc(p_base + kk * 32, 16, 1024), make_desc(o_base + kk * 2048, QHALF, 1024), idKV,
+                 (i | kk) != 0);
+        mma_bf16(tmem + T_DK, make_desc(ds_base + kk * 32, 16, 1024), make_desc(q_base + kk * 2048, QHALF, 1024), idKV,
+                 (i | kk) != 0);
+      }
+      if (i >= 1) mbar_wait(dqfree, (i - 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < AT / 16; ++kk)
+        mma_bf16(tmem + T_DQ, make_desc(k_base + kk * 2048, HALF, 1024), make_desc(ds_base + kk * 2048, 8192, 1024), idQ,
+                 kk > 0);
+      mma_commit(dqfull);
+      mma_commit(pfree);
+      mma_commit(qfree + b);
+    }
+    mma_commit(done);
+  } else if (warp >= 2) {
+    // ---------------- softmax-gradient warps: thread owns key row `row` (TMEM lane)
+    const int q = warp & 3, row = q * 32 + lane;
+    const int kabs = key0 + row;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    uint8_t* Pt = sm + BwdSmem::P;
+    uint8_t* dSt = sm + BwdSmem::DS;
+    const float* lse_h = lse + (int64_t)head * s + c;
+    const float* D_h = Dvec + (int64_t)head * l;
+    auto drain_dq = [&](int i) {  // dQ^T of tile i: thread = head-dim index `row`, 64 query columns
+      mbar_wait(dqfull, i & 1);
+      tc_fence_after();
+      const int qrow0 = (qt0 + i) * BQB;
+      float* dst = dq_acc + (int64_t)head * AT + row;
+#pragma unroll
+      for (int ch = 0; ch < BQB / 32; ++ch) {
+        uint32_t r[32];
+        tmem_ld32_nowait(lane_base + T_DQ + ch * 32, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const int qr = qrow0 + ch * 32 + t;
+          if (qr < l) atomicAdd(dst + (int64_t)qr * ldq, __uint_as_float(r[t]) * scale);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dqfree);
+    };
+    for (int i = 0; i < ntile; ++i) {
+      const int qrow0 = (qt0 + i) * BQB;
+      mbar_wait(sfull, i & 1);
+      tc_fence_after();
+      if (i >= 1) mbar_wait(pfree, (i - 1) & 1);  // MMAs of tile i-1 have read P^T / dS^T
+#pragma unroll
+      for (int ch = 0; ch < BQB / 32; ++ch) {
+        uint32_t rs[32], rp[32];
+        tmem_ld32_nowait(lane_base + T_S + ch * 32, rs);
+        tmem_ld32_nowait(lane_base + T_DP + ch * 32, rp);
+        tmem_wait_ld();
+        uint32_t pk[16], dk[16];
+#pragma unroll
+        for (int t = 0; t < 32; t += 2) {
+          float pv[2], dv[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int qr = qrow0 + ch * 32 + t + e;
+            const bool ok = qr < l && c + qr >= kabs;
+            const float L2 = ok ? __ldg(lse_h + qr) * LOG2E_F : 0.f;
+            const float Dq = ok ? __ldg(D_h + qr) : 0.f;
+            const float p = ok ? exp2f(__uint_as_float(rs[t + e]) * scale_log2 - L2) : 0.f;
+            pv[e] = p;
+            dv[e] = p * (__uint_as_float(rp[t + e]) - Dq);
+          }
+          __nv_bfloat162 hp = __floats2bfloat162_rn(pv[0], pv[1]);
+          __nv_bfloat162 hd = __floats2bfloat162_rn(dv[0], dv[1]);
+          pk[t >> 1] = *reinterpret_cast<uint32_t*>(&hp);
+          dk[t >> 1] = *reinterpret_cast<uint32_t*>(&hd);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int cc = ch * 4 + u;
+          *reinterpret_cast<uint4*>(Pt + swz(row, cc)) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          *reinterpret_cast<uint4*>(dSt + swz(row, cc)) = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+        }
+      }
+      tc_fence_before();
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) { mbar_arrive(sfree); mbar_arrive(pfull); }
+      if (i >= 1) drain_dq(i - 1);
+    }
+    drain_dq(ntile - 1);
+    // dK (x scale) and dV rows of this key block -> fp32 prefix accumulators
+    mbar_wait(done, 0);
+    tc_fence_after();
+    if (kabs < nkeys) {
+      float* dkr = dk_acc + ((int64_t)head * s + kabs) * AT;
+      float* dvr = dv_acc + ((int64_t)head * s + kabs) * AT;
+#pragma unroll
+      for (int ch = 0; ch < AT / 32; ++ch) {
+        uint32_t rk[32], rv[32];
+        tmem_ld32_nowait(lane_base + T_DK + ch * 32, rk);
+        tmem_ld32_nowait(lane_base + T_DV + ch * 32, rv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int t = 0; t < 32; t += 4) {
+          float4 nk = make_float4(__uint_as_float(rk[t]) * scale, __uint_as_float(rk[t + 1]) * scale,
+                                  __uint_as_float(rk[t + 2]) * scale, __uint_as_float(rk[t + 3]) * scale);
+          float4 nv = make_float4(__uint_as_float(rv[t]), __uint_as_float(rv[t + 1]), __uint_as_float(rv[t + 2]),
+                                  __uint_as_float(rv[t + 3]));
+          float4* pk = reinterpret_cast<float4*>(dkr + ch * 32 + t);
+          float4* pv = reinterpret_cast<float4*>(dvr + ch * 32 + t);
+          if (accumulate) {
+            const float4 ok = *pk, ov = *pv;
+            nk.x += ok.x; nk.y += ok.y; nk.z += ok.z; nk.w += ok.w;
+            nv.x += ov.x; nv.y += ov.y; nv.z += ov.z; nv.w += ov.w;
+          }
+          *pk = nk;
+          *pv = nv;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+__global__ void dq_convert_kernel(const float* __restrict__ dq_acc, int64_t ld_acc, bf16* __restrict__ dq, int64_t ldq,
+                                  int H) {
+  const int r = blockIdx.x;
+  for (int i = threadIdx.x * 8; i < H; i += blockDim.x * 8) {
+    float v[8];
+    load8<float>(dq_acc + (int64_t)r * ld_acc + i, v);
+    store8<bf16>(dq + (int64_t)r * ldq + i, v);
+  }
+}
+
 }  // namespace
 
 bool attn_sm100_supported(int d) { return d == AT; }
@@ -275,6 +521,43 @@ cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o,
   dim3 grid((l + AT - 1) / AT, a);
   attn_fwd_sm100_kernel<<<grid, 192, FwdSmem::BYTES, st>>>(mq, mk, mv, o, ldo, lse, s, c, l,
                                                            rsqrtf((float)d) * LOG2E_F);
+  return cudaGetLastError();
+}
+
+cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ldo, const bf16* q, const bf16* k,
+                           const bf16* v, const float* lse, float* Dvec, float* dq_acc, bf16* dq, int64_t ldq,
+                           float* dk_acc, float* dv_acc, int a, int s, int d, int c, int l, int accumulate,
+                           cudaStream_t st) {
+  if (l == 0) return cudaSuccess;
+  if (d != AT) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)BwdSmem::BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int H = a * d;
+  cudaError_t e = cudaMemsetAsync(dq_acc, 0, sizeof(float) * (size_t)l * H, st);
+  if (e == cudaSuccess) e = attn_bwd_prep(dO, ld_do, o, ldo, Dvec, a, d, l, st);
+  if (e != cudaSuccess) return e;
+  const uint64_t kdims[3] = {(uint64_t)d, (uint64_t)(c + l), (uint64_t)a};
+  const uint64_t kstr[2] = {(uint64_t)d * 2, (uint64_t)s * d * 2};
+  const uint32_t kbox[3] = {64, AT, 1}, qbox[3] = {64, BQB, 1};
+  const uint64_t odims[2] = {(uint64_t)H, (uint64_t)l};
+  const uint64_t ostr[1] = {(uint64_t)ld_do * 2};
+  const uint32_t obox[2] = {64, BQB};
+  CUtensorMap mk, mv, mq, mo;
+  if (!encode_bf16_map(&mk, k, 3, kdims, kstr, kbox) || !encode_bf16_map(&mv, v, 3, kdims, kstr, kbox) ||
+      !encode_bf16_map(&mq, q, 3, kdims, kstr, qbox) || !encode_bf16_map(&mo, dO, 2, odims, ostr, obox))
+    return cudaErrorInvalidValue;
+  const float scale = rsqrtf((float)d);
+  dim3 grid((c + l + AT - 1) / AT, a);
+  attn_bwd_sm100_kernel<<<grid, 192, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, lse, Dvec, dq_acc, H, dk_acc, dv_acc, s, c, l,
+                                                           scale, scale * LOG2E_F, accumulate);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dq_convert_kernel<<<l, 128, 0, st>>>(dq_acc, H, dq, ldq, H);
   return cudaGetLastError();
 }
 

@@ -541,6 +541,20 @@ cudaError_t bwd_d(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ldo, con
 
 }  // namespace
 
+cudaError_t attn_bwd_prep(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ldo, float* Dvec, int a, int d, int l,
+                          cudaStream_t st) {
+  if (l == 0) return cudaSuccess;
+  dim3 grid((l + 3) / 4);
+  switch (d) {
+    case 16: attn_bwd_prep_kernel<16><<<grid, 128, 0, st>>>(dO, ld_do, o, ldo, Dvec, a, l); break;
+    case 32: attn_bwd_prep_kernel<32><<<grid, 128, 0, st>>>(dO, ld_do, o, ldo, Dvec, a, l); break;
+    case 64: attn_bwd_prep_kernel<64><<<grid, 128, 0, st>>>(dO, ld_do, o, ldo, Dvec, a, l); break;
+    case 128: attn_bwd_prep_kernel<128><<<grid, 128, 0, st>>>(dO, ld_do, o, ldo, Dvec, a, l); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t attn_fwd_tc(const bf16* q, const bf16* k, const bf16* v, bf16* o, int64_t ldo, float* lse, int a, int s,
                         int d, int c, int l, cudaStream_t st) {
   if (l == 0) return cudaSuccess;

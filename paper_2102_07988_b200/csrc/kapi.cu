@@ -54,7 +54,14 @@ extern "C" tp_status tpk_attention_bwd(const void* dO, const void* o, const void
   tp_status r = cu(cudaMallocAsync(&Dvec, sizeof(float) * a * l, st), "cudaMallocAsync");
   if (r != TP_OK) return r;
   const int64_t H = (int64_t)a * d;
-  if (impl == 0 || impl == 2)
+  if (impl == 0 && attn_sm100_supported(d)) {
+    float* dq_acc = nullptr;
+    r = cu(cudaMallocAsync(&dq_acc, sizeof(float) * H * l, st), "cudaMallocAsync");
+    if (r != TP_OK) return r;
+    r = cu(attn_bwd_sm100((const bf16*)dO, H, (const bf16*)o, H, (const bf16*)q, (const bf16*)k, (const bf16*)v, lse, Dvec,
+                          dq_acc, (bf16*)dq, ldq, dk_acc, dv_acc, a, s, d, c, l, accumulate, st), "attn_bwd_sm100");
+    cudaFreeAsync(dq_acc, st);
+  } else if (impl == 0 || impl == 2)
     r = cu(attn_bwd_tc((const bf16*)dO, H, (const bf16*)o, H, (const bf16*)q, (const bf16*)k, (const bf16*)v, lse, Dvec,
                        (bf16*)dq, ldq, dk_acc, dv_acc, a, s, d, c, l, accumulate, st), "attn_bwd_tc");
   else

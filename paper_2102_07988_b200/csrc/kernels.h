@@ -63,6 +63,14 @@ cudaError_t attn_bwd_tc(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ld
 bool attn_sm100_supported(int d);
 cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o, int64_t ldo, float* lse, int a, int s,
                            int d, int c, int l, cudaStream_t st);
+// D[head][r] = rowsum(dO * O) per head (attn_tc.cu)
+cudaError_t attn_bwd_prep(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ldo, float* Dvec, int a, int d, int l,
+                          cudaStream_t st);
+// dq_acc: fp32 scratch [l][a*d] (zeroed inside); dq: bf16 output rows (ld ldq)
+cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ldo, const bf16* q, const bf16* k,
+                           const bf16* v, const float* lse, float* Dvec, float* dq_acc, bf16* dq, int64_t ldq,
+                           float* dk_acc, float* dv_acc, int a, int s, int d, int c, int l, int accumulate,
+                           cudaStream_t st);
 template <typename T>
 cudaError_t attn_dkv_finalize(const float* dk_acc, const float* dv_acc, T* dqkv, int64_t ld, int a,
                               int s, int d, int c, int l, cudaStream_t st);

@@ -182,7 +182,7 @@ struct Stage {
   // backward stash of ONE sequence (deferred dW)
   std::vector<T*> dQKV, dhmid_b, dU, dhout_b;
   std::vector<float*> dk_acc, dv_acc;  // [a][s][d]
-  float *gA = nullptr, *gB = nullptr, *gm = nullptr, *dA = nullptr, *Dvec = nullptr, *lnws = nullptr;
+  float *gA = nullptr, *gB = nullptr, *gm = nullptr, *dA = nullptr, *Dvec = nullptr, *lnws = nullptr, *dqacc = nullptr;
   T* dO = nullptr;
 };
 
@@ -331,6 +331,7 @@ class Engine final : public EngineBase {
     TRY(alloc(&S.gA, s * H)); TRY(alloc(&S.gB, s * H)); TRY(alloc(&S.gm, s * H)); TRY(alloc(&S.dA, s * H));
     TRY(alloc(&S.Dvec, a * s)); TRY(alloc(&S.dO, s * H));
     TRY(alloc(&S.lnws, 2 * H * ((s + 3) / 4)));
+    TRY(alloc(&S.dqacc, s * H));
     return TP_OK;
   }
 
@@ -491,6 +492,10 @@ class Engine final : public EngineBase {
       TRY(launch(KC_ATTN_BWD, attn_flops, ebytes * 4.0 * H * (c + l) + 16.0 * H * (c + l), [&] {
         const T *q = S.Q[j] + (size_t)d * s * H, *kk = S.Kc[j] + (size_t)d * s * H, *vv = S.Vc[j] + (size_t)d * s * H;
         const int accum = first_bwd_slice ? 0 : 1;
+        if constexpr (std::is_same<T, bf16>::value)
+          if (!force_simt && attn_sm100_supported(dh) && !legacy_attn)
+            return attn_bwd_sm100(S.dO, H, S.O[j] + row * H, H, q, kk, vv, S.LSE[j] + (size_t)d * a * s, S.Dvec, S.dqacc,
+                                  dq, 3 * H, S.dk_acc[j], S.dv_acc[j], a, s, dh, c, l, accum, stream);
         if constexpr (std::is_same<T, bf16>::value)
           if (!force_simt)
             return attn_bwd_tc(S.dO, H, S.O[j] + row * H, H, q, kk, vv, S.LSE[j] + (size_t)d * a * s, S.Dvec, dq, 3 * H,
