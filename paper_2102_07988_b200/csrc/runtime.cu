@@ -55,9 +55,16 @@ struct ModelShape {
 struct LayerOff {
   size_t ln1_g, ln1_b, w_qkv, b_qkv, w_o, b_o, ln2_g, ln2_b, w_1, b_1, w_2, b_2;
 };
+// Offsets of the fp32 parameters kept on the device as fp32 (LayerNorm, biases, embeddings) inside
+// the compact `psmall` array; weight matrices live only as bf16 (or fp32-mode) GEMM operands.
+struct SmallOff {
+  size_t ln1_g, ln1_b, b_qkv, b_o, ln2_g, ln2_b, b_1, b_2;
+};
 struct StageLayout {
   size_t wte = 0, wpe = 0, lnf_g = 0, lnf_b = 0, w_out = 0, total = 0;
   std::vector<LayerOff> layers;
+  size_t s_wte = 0, s_wpe = 0, s_lnf_g = 0, s_lnf_b = 0, small_total = 0;
+  std::vector<SmallOff> small;
 };
 
 static StageLayout stage_layout(const ModelShape& m, int k) {
@@ -78,6 +85,16 @@ static StageLayout stage_layout(const ModelShape& m, int k) {
   }
   if (k == m.K - 1) { L.lnf_g = o; o += H; L.lnf_b = o; o += H; L.w_out = o; o += H * (size_t)m.V; }
   L.total = o;
+  size_t q = 0;
+  if (k == 0) { L.s_wte = q; q += (size_t)m.V * H; L.s_wpe = q; q += (size_t)m.s * H; }
+  for (int j = 0; j < nl; ++j) {
+    SmallOff f;
+    f.ln1_g = q; q += H; f.ln1_b = q; q += H; f.b_qkv = q; q += 3 * H; f.b_o = q; q += H;
+    f.ln2_g = q; q += H; f.ln2_b = q; q += H; f.b_1 = q; q += 4 * H; f.b_2 = q; q += H;
+    L.small.push_back(f);
+  }
+  if (k == m.K - 1) { L.s_lnf_g = q; q += H; L.s_lnf_b = q; q += H; }
+  L.small_total = q;
   return L;
 }
 
@@ -160,7 +177,7 @@ template <typename T>
 struct Stage {
   int k = 0, nl = 0;
   StageLayout L;
-  float* pflat = nullptr;  // fp32 params (flat layout)
+  float* psmall = nullptr;  // fp32 LayerNorm / bias / embedding parameters (StageLayout::small offsets)
   float* gflat = nullptr;  // fp32 grads (flat layout)
   // GEMM operands in T: *_t = [out][in] (K-major B for fwd), *_io = [in][out] (K-major B for dX)
   std::vector<T*> wqkv_t, wqkv_io, wo_t, wo_io, w1_t, w1_io, w2_t, w2_io;
@@ -287,7 +304,7 @@ class Engine final : public EngineBase {
     S.nl = m.n_layer / m.K;
     S.L = stage_layout(m, k);
     const size_t B = max_batch, s = m.s, H = m.H, a = m.a, nl = S.nl;
-    TRY(alloc(&S.pflat, S.L.total));
+    TRY(alloc(&S.psmall, S.L.small_total));
     TRY(alloc(&S.gflat, S.L.total));
     auto vec = [&](auto& v, size_t n, size_t count) -> tp_status {
       v.resize(n);
@@ -338,29 +355,55 @@ class Engine final : public EngineBase {
   // ------------------------------------------------------------ parameter load
   tp_status load(const float* host, size_t n) override {
     if (n != param_count()) return fail(TP_EINVAL, "tp_load_params: n=%zu, expected %zu", n, param_count());
+    // weight matrices go through one fp32 staging buffer into their two GEMM-operand copies
+    size_t big = (size_t)4 * m.H * m.H;
+    for (auto& S : stages) if (S.k == m.K - 1) big = std::max(big, (size_t)m.H * m.V);
+    float* stage_buf = nullptr;
+    CU(cudaMalloc(&stage_buf, big * sizeof(float)));
+    auto put = [&](float* dst, const float* src, size_t cnt) -> tp_status {
+      CU(cudaMemcpyAsync(dst, src, cnt * sizeof(float), cudaMemcpyHostToDevice, stream));
+      return TP_OK;
+    };
+    auto mat = [&](const float* src, int R, int Cc, T* t_copy, T* io_copy) -> tp_status {
+      CU(cudaMemcpyAsync(stage_buf, src, (size_t)R * Cc * sizeof(float), cudaMemcpyHostToDevice, stream));
+      CU(transpose_convert<T>(stage_buf, t_copy, R, Cc, stream));
+      CU(convert_f32<T>(stage_buf, io_copy, (int64_t)R * Cc, stream));
+      CU(cudaStreamSynchronize(stream));
+      return TP_OK;
+    };
+    tp_status st = TP_OK;
     size_t off = 0;
+    const size_t H = m.H;
     for (auto& S : stages) {
-      CU(cudaMemcpyAsync(S.pflat, host + off, S.L.total * sizeof(float), cudaMemcpyHostToDevice, stream));
-      off += S.L.total;
-      const int H = m.H;
-      for (int j = 0; j < S.nl; ++j) {
-        const LayerOff& f = S.L.layers[j];
-        CU(transpose_convert<T>(S.pflat + f.w_qkv, S.wqkv_t[j], H, 3 * H, stream));
-        CU(convert_f32<T>(S.pflat + f.w_qkv, S.wqkv_io[j], (int64_t)H * 3 * H, stream));
-        CU(transpose_convert<T>(S.pflat + f.w_o, S.wo_t[j], H, H, stream));
-        CU(convert_f32<T>(S.pflat + f.w_o, S.wo_io[j], (int64_t)H * H, stream));
-        CU(transpose_convert<T>(S.pflat + f.w_1, S.w1_t[j], H, 4 * H, stream));
-        CU(convert_f32<T>(S.pflat + f.w_1, S.w1_io[j], (int64_t)H * 4 * H, stream));
-        CU(transpose_convert<T>(S.pflat + f.w_2, S.w2_t[j], 4 * H, H, stream));
-        CU(convert_f32<T>(S.pflat + f.w_2, S.w2_io[j], (int64_t)4 * H * H, stream));
+      const float* h = host + off;
+      const StageLayout& L = S.L;
+      if (S.k == 0) {
+        if ((st = put(S.psmall + L.s_wte, h + L.wte, (size_t)m.V * H)) != TP_OK) break;
+        if ((st = put(S.psmall + L.s_wpe, h + L.wpe, (size_t)m.s * H)) != TP_OK) break;
       }
-      if (S.k == m.K - 1) {
-        CU(transpose_convert<T>(S.pflat + S.L.w_out, S.wout_t, H, m.V, stream));
-        CU(convert_f32<T>(S.pflat + S.L.w_out, S.wout_io, (int64_t)H * m.V, stream));
+      for (int j = 0; j < S.nl && st == TP_OK; ++j) {
+        const LayerOff& f = L.layers[j];
+        const SmallOff& g = L.small[j];
+        const size_t srcs[8] = {f.ln1_g, f.ln1_b, f.b_qkv, f.b_o, f.ln2_g, f.ln2_b, f.b_1, f.b_2};
+        const size_t dsts[8] = {g.ln1_g, g.ln1_b, g.b_qkv, g.b_o, g.ln2_g, g.ln2_b, g.b_1, g.b_2};
+        const size_t cnts[8] = {H, H, 3 * H, H, H, H, 4 * H, H};
+        for (int i = 0; i < 8 && st == TP_OK; ++i) st = put(S.psmall + dsts[i], h + srcs[i], cnts[i]);
+        if (st == TP_OK) st = mat(h + f.w_qkv, (int)H, 3 * (int)H, S.wqkv_t[j], S.wqkv_io[j]);
+        if (st == TP_OK) st = mat(h + f.w_o, (int)H, (int)H, S.wo_t[j], S.wo_io[j]);
+        if (st == TP_OK) st = mat(h + f.w_1, (int)H, 4 * (int)H, S.w1_t[j], S.w1_io[j]);
+        if (st == TP_OK) st = mat(h + f.w_2, 4 * (int)H, (int)H, S.w2_t[j], S.w2_io[j]);
       }
+      if (st == TP_OK && S.k == m.K - 1) {
+        st = put(S.psmall + L.s_lnf_g, h + L.lnf_g, H);
+        if (st == TP_OK) st = put(S.psmall + L.s_lnf_b, h + L.lnf_b, H);
+        if (st == TP_OK) st = mat(h + L.w_out, (int)H, m.V, S.wout_t, S.wout_io);
+      }
+      if (st != TP_OK) break;
+      off += L.total;
     }
-    CU(cudaStreamSynchronize(stream));
-    return TP_OK;
+    cudaStreamSynchronize(stream);
+    cudaFree(stage_buf);
+    return st;
   }
 
   // ------------------------------------------------------------ launch helpers
@@ -396,12 +439,12 @@ class Engine final : public EngineBase {
     const double ebytes = sizeof(T);
     if (S.k == 0) {
       TRY(launch(KC_EMBED, 0, 8.0 * l * H, [&] {
-        return embed_fwd(d_tokens + (size_t)d * (s + 1), S.pflat + S.L.wte, S.pflat + S.L.wpe, S.hs[0] + row * H, c, l, H, V, stream);
+        return embed_fwd(d_tokens + (size_t)d * (s + 1), S.psmall + S.L.s_wte, S.psmall + S.L.s_wpe, S.hs[0] + row * H, c, l, H, V, stream);
       }));
     }
     for (int j = 0; j < S.nl; ++j) {
-      const LayerOff& f = S.L.layers[j];
-      const float* P = S.pflat;
+      const SmallOff& f = S.L.small[j];
+      const float* P = S.psmall;
       float* x = S.hs[j] + row * H;
       float* st1 = S.st1[j];
       TRY(launch(KC_LN, 0, (4.0 + ebytes) * l * H, [&] {
@@ -435,10 +478,10 @@ class Engine final : public EngineBase {
       TRY(gemm(KC_GEMM_FWD, gd(l, H, 4 * H, S.G[j] + row * 4 * H, 4 * H, false, S.w2_t[j], 4 * H, false), e2));
     }
     if (S.k == m.K - 1) {
-      const float* P = S.pflat;
+      const float* P = S.psmall;
       float* x = S.hs[S.nl] + row * H;
       TRY(launch(KC_LN, 0, (4.0 + ebytes) * l * H, [&] {
-        return layernorm_fwd<T>(x, P + S.L.lnf_g, P + S.L.lnf_b, S.Af + row * H, S.stf + row, S.stf + (size_t)batch * s + row, l, H, stream);
+        return layernorm_fwd<T>(x, P + S.L.s_lnf_g, P + S.L.s_lnf_b, S.Af + row * H, S.stf + row, S.stf + (size_t)batch * s + row, l, H, stream);
       }));
       Epi ez; ez.kind = EPI_STORE; ez.out = S.Z + row * V; ez.ldo = V;
       TRY(gemm(KC_GEMM_FWD, gd(l, V, H, S.Af + row * H, H, false, S.wout_t, H, false), ez));
@@ -458,11 +501,11 @@ class Engine final : public EngineBase {
     const double ebytes = sizeof(T);
     float* g = S.grad_out + row * H;  // fp32 gradient at the stage output, rows of this job
     if (S.k == m.K - 1) {
-      const float* P = S.pflat;
+      const float* P = S.psmall;
       Epi e; e.kind = EPI_STORE; e.out = S.dA; e.ldo = H; e.out_f32 = 1;
       TRY(gemm(KC_GEMM_DX, gd(l, H, V, S.Z + row * V, V, false, S.wout_io, V, false), e));
       TRY(launch(KC_LN, 0, (12.0 + ebytes) * l * H, [&] {
-        return layernorm_bwd<T>(S.dA, S.hs[S.nl] + row * H, S.stf + row, S.stf + (size_t)batch * s + row, P + S.L.lnf_g, nullptr, g,
+        return layernorm_bwd<T>(S.dA, S.hs[S.nl] + row * H, S.stf + row, S.stf + (size_t)batch * s + row, P + S.L.s_lnf_g, nullptr, g,
                                 S.dhout_b[S.nl - 1] + (size_t)c * H, S.gflat + S.L.lnf_g, S.gflat + S.L.lnf_b, S.lnws, l, H, stream);
       }));
     } else {
@@ -472,7 +515,8 @@ class Engine final : public EngineBase {
     }
     for (int j = S.nl - 1; j >= 0; --j) {
       const LayerOff& f = S.L.layers[j];
-      const float* P = S.pflat;
+      const SmallOff& fs = S.L.small[j];
+      const float* P = S.psmall;
       float* GR = S.gflat;
       // FFN: dU = (dh W_2^T) * gelu'(U)
       Epi e1; e1.kind = EPI_DGELU; e1.out = S.dU[j] + (size_t)c * 4 * H; e1.ldo = 4 * H; e1.aux = S.U[j] + row * 4 * H; e1.ld_aux = 4 * H;
@@ -481,7 +525,7 @@ class Engine final : public EngineBase {
       TRY(gemm(KC_GEMM_DX, gd(l, H, 4 * H, S.dU[j] + (size_t)c * 4 * H, 4 * H, false, S.w1_io[j], 4 * H, false), e2));
       float* st2 = S.st2[j];
       TRY(launch(KC_LN, 0, (16.0 + ebytes) * l * H, [&] {
-        return layernorm_bwd<T>(S.dA, S.hmid[j] + row * H, st2 + row, st2 + (size_t)batch * s + row, P + f.ln2_g, g, S.gm,
+        return layernorm_bwd<T>(S.dA, S.hmid[j] + row * H, st2 + row, st2 + (size_t)batch * s + row, P + fs.ln2_g, g, S.gm,
                                 S.dhmid_b[j] + (size_t)c * H, GR + f.ln2_g, GR + f.ln2_b, S.lnws, l, H, stream);
       }));
       // attention: dO = dh_mid W_o^T, then slice-vs-prefix attention backward with dK/dV push
@@ -512,7 +556,7 @@ class Engine final : public EngineBase {
       T* copy = j == 0 ? nullptr : S.dhout_b[j - 1] + (size_t)c * H;
       float* st1 = S.st1[j];
       TRY(launch(KC_LN, 0, (16.0 + ebytes) * l * H, [&] {
-        return layernorm_bwd<T>(S.dA, S.hs[j] + row * H, st1 + row, st1 + (size_t)batch * s + row, P + f.ln1_g, S.gm, gnext, copy,
+        return layernorm_bwd<T>(S.dA, S.hs[j] + row * H, st1 + row, st1 + (size_t)batch * s + row, P + fs.ln1_g, S.gm, gnext, copy,
                                 GR + f.ln1_g, GR + f.ln1_b, S.lnws, l, H, stream);
       }));
       g = gnext;
