@@ -32,19 +32,27 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 // Waits for the phase with the given parity. A watchdog turns a protocol deadlock into a trap
-// (a CUDA error on the host) instead of a hung GPU: ~2^26 suspended try_waits is seconds.
+// (a CUDA error on the host) instead of a hung GPU: after 4 s of waiting it prints the barrier and
+// traps.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try(bar, parity)) return;
+  const uint64_t t0 = global_ns();
   uint32_t n = 0;
   while (!mbar_try(bar, parity)) {
-    if (++n == (1u << 26)) {
+    if ((++n & 1023u) == 0 && global_ns() - t0 > 4000000000ull) {
       printf("tp: mbarrier watchdog: block (%d,%d) thread %d bar smem+%u parity %u\n", blockIdx.x, blockIdx.y,
              threadIdx.x, smem_u32(bar), parity);
       __trap();
     }
   }
 }
+
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
