@@ -14,6 +14,12 @@
 //           into the 128B-swizzled P tile; O is accumulated in registers, o = o*exp2(m_old-m_j) + O_j.
 // Key blocks are aligned to absolute multiples of 128; only blocks crossing a query's position are
 // masked element-wise.
+#include <unistd.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
 #include "kernels.h"
 #include "tc5.cuh"
 
@@ -275,8 +281,12 @@ __global__ void __launch_bounds__(192, 1)
                           const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                           const float* __restrict__ lse, const float* __restrict__ Dvec, float* __restrict__ dq_acc,
                           int64_t ldq, float* __restrict__ dk_acc, float* __restrict__ dv_acc, int s, int c, int l,
-                          float scale, float scale_log2, int accumulate) {
+                          float scale, float scale_log2, int accumulate, volatile int* dbg) {
   extern __shared__ uint8_t smem_raw[];
+#define DBG(role, v)                                                                    \
+  do {                                                                                  \
+    if (dbg) { dbg[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + (role)] = (v); __threadfence_system(); } \
+  } while (0)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + BwdSmem::BAR);
   uint64_t* kvfull = bars + 0;
@@ -306,11 +316,14 @@ __global__ void __launch_bounds__(192, 1)
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (threadIdx.x == 0) DBG(7, 1);
   if (warp == 0) tmem_alloc(tmem_slot, 512);
+  if (threadIdx.x == 0) DBG(7, 2);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) DBG(6, ntile);
   constexpr uint32_t T_S = 0, T_DP = 64, T_DV = 128, T_DK = 256, T_DQ = 384;
 
   if (warp == 0 && lane == 0) {
@@ -322,6 +335,7 @@ __global__ void __launch_bounds__(192, 1)
     tma_load_3d(sm + BwdSmem::V + HALF, &tmV, 64, key0, head, kvfull);
     for (int i = 0; i < ntile; ++i) {
       const int b = i & 1, qt = qt0 + i;
+      DBG(0, 100 + i);
       if (i >= 2) mbar_wait(qfree + b, ((i >> 1) - 1) & 1);
       uint8_t* qd = sm + (b ? BwdSmem::Q1 : BwdSmem::Q0);
       uint8_t* od = sm + (b ? BwdSmem::O1 : BwdSmem::O0);
@@ -343,8 +357,11 @@ __global__ void __launch_bounds__(192, 1)
       const int b = i & 1;
       const uint32_t q_base = smem_u32(sm + (b ? BwdSmem::Q1 : BwdSmem::Q0));
       const uint32_t o_base = smem_u32(sm + (b ? BwdSmem::O1 : BwdSmem::O0));
+      DBG(1, 100 + 10 * i);
       mbar_wait(qfull + b, (i >> 1) & 1);
+      DBG(1, 101 + 10 * i);
       if (i >= 1) mbar_wait(sfree, (i - 1) & 1);
+      DBG(1, 102 + 10 * i);
       tc_fence_after();
 #pragma unroll
       for (int kk = 0; kk < AT / 16; ++kk) {
@@ -353,7 +370,9 @@ __global__ void __launch_bounds__(192, 1)
         mma_bf16(tmem + T_DP, make_desc(v_base + ok, 16, 1024), make_desc(o_base + oq, 16, 1024), idS, kk > 0);
       }
       mma_commit(sfull);
+      DBG(1, 103 + 10 * i);
       mbar_wait(pfull, i & 1);
+      DBG(1, 104 + 10 * i);
       tc_fence_after();
 #pragma unroll
       for (int kk = 0; kk < BQB / 16; ++kk) {
@@ -371,8 +390,10 @@ __global__ void __launch_bounds__(192, 1)
       mma_commit(dqfull);
       mma_commit(pfree);
       mma_commit(qfree + b);
+      DBG(1, 105 + 10 * i);
     }
     mma_commit(done);
+    DBG(1, 999);
   } else if (warp >= 2) {
     // ---------------- softmax-gradient warps: thread owns key row `row` (TMEM lane)
     const int q = warp & 3, row = q * 32 + lane;
@@ -404,7 +425,9 @@ __global__ void __launch_bounds__(192, 1)
     };
     for (int i = 0; i < ntile; ++i) {
       const int qrow0 = (qt0 + i) * BQB;
+      if (lane == 0) DBG(2 + q, 100 + 10 * i);
       mbar_wait(sfull, i & 1);
+      if (lane == 0) DBG(2 + q, 101 + 10 * i);
       tc_fence_after();
       if (i >= 1) mbar_wait(pfree, (i - 1) & 1);  // MMAs of tile i-1 have read P^T / dS^T
 #pragma unroll
@@ -446,18 +469,21 @@ __global__ void __launch_bounds__(192, 1)
       if (i >= 1) drain_dq(i - 1);
     }
     drain_dq(ntile - 1);
+    if (lane == 0) DBG(2 + q, 900);
     // dK (x scale) and dV rows of this key block -> fp32 prefix accumulators
     mbar_wait(done, 0);
     tc_fence_after();
-    if (kabs < nkeys) {
-      float* dkr = dk_acc + ((int64_t)head * s + kabs) * AT;
-      float* dvr = dv_acc + ((int64_t)head * s + kabs) * AT;
+    // (tcgen05.ld is warp-collective: every lane loads, only rows inside the prefix store)
+    const bool store = kabs < nkeys;
+    float* dkr = dk_acc + ((int64_t)head * s + kabs) * AT;
+    float* dvr = dv_acc + ((int64_t)head * s + kabs) * AT;
 #pragma unroll
-      for (int ch = 0; ch < AT / 32; ++ch) {
-        uint32_t rk[32], rv[32];
-        tmem_ld32_nowait(lane_base + T_DK + ch * 32, rk);
-        tmem_ld32_nowait(lane_base + T_DV + ch * 32, rv);
-        tmem_wait_ld();
+    for (int ch = 0; ch < AT / 32; ++ch) {
+      uint32_t rk[32], rv[32];
+      tmem_ld32_nowait(lane_base + T_DK + ch * 32, rk);
+      tmem_ld32_nowait(lane_base + T_DV + ch * 32, rv);
+      tmem_wait_ld();
+      if (store) {
 #pragma unroll
         for (int t = 0; t < 32; t += 4) {
           float4 nk = make_float4(__uint_as_float(rk[t]) * scale, __uint_as_float(rk[t + 1]) * scale,
@@ -553,9 +579,29 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
     return cudaErrorInvalidValue;
   const float scale = rsqrtf((float)d);
   dim3 grid((c + l + AT - 1) / AT, a);
+  static int* dbg = nullptr;
+  static bool dbg_on = getenv("TP_ATTN_DEBUG") != nullptr;
+  if (dbg_on && !dbg) {
+    cudaHostAlloc(&dbg, 4096 * sizeof(int), cudaHostAllocMapped);
+  }
+  int* dbg_dev = nullptr;
+  if (dbg_on) { memset(dbg, 0, 4096 * sizeof(int)); cudaHostGetDevicePointer(&dbg_dev, dbg, 0); }
   attn_bwd_sm100_kernel<<<grid, 192, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, lse, Dvec, dq_acc, H, dk_acc, dv_acc, s, c, l,
-                                                           scale, scale * LOG2E_F, accumulate);
+                                                           scale, scale * LOG2E_F, accumulate, dbg_dev);
   e = cudaGetLastError();
+  if (dbg_on) {
+    for (int it = 0; it < 50 && cudaStreamQuery(st) == cudaErrorNotReady; ++it) usleep(100000);
+    if (cudaStreamQuery(st) == cudaErrorNotReady) {
+      fprintf(stderr, "attn_bwd_sm100 HUNG: grid %d x %d, c=%d l=%d\n", grid.x, grid.y, c, l);
+      for (unsigned b = 0; b < grid.x * grid.y; ++b) {
+        fprintf(stderr, " cta %u:", b);
+        for (int r = 0; r < 8; ++r) fprintf(stderr, " %d", ((volatile int*)dbg)[b * 8 + r]);
+        fprintf(stderr, "\n");
+      }
+      fflush(stderr);
+      abort();
+    }
+  }
   if (e != cudaSuccess) return e;
   dq_convert_kernel<<<l, 128, 0, st>>>(dq_acc, H, dq, ldq, H);
   return cudaGetLastError();

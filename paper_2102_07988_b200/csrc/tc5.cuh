@@ -43,9 +43,8 @@ __device__ __forceinline__ uint64_t global_ns() {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try(bar, parity)) return;
   const uint64_t t0 = global_ns();
-  uint32_t n = 0;
   while (!mbar_try(bar, parity)) {
-    if ((++n & 1023u) == 0 && global_ns() - t0 > 4000000000ull) {
+    if (global_ns() - t0 > 4000000000ull) {
       printf("tp: mbarrier watchdog: block (%d,%d) thread %d bar smem+%u parity %u\n", blockIdx.x, blockIdx.y,
              threadIdx.x, smem_u32(bar), parity);
       __trap();
