@@ -272,15 +272,15 @@ constexpr uint32_t PT = AT * BQB * 2;            // 16 KiB: [128 keys][64 q] (on
 
 struct BwdSmem {
   static constexpr uint32_t K = 0, V = TILE, Q0 = 2 * TILE, Q1 = Q0 + QT, O0 = Q1 + QT, O1 = O0 + QT;
-  static constexpr uint32_t P = O1 + QT, DS = P + PT, BAR = DS + PT;
+  static constexpr uint32_t P = O1 + QT, DS = P + PT, DQ = DS + PT /* fp32 [64 q][128 d] */, BAR = DQ + 32768;
   static constexpr uint32_t BYTES = BAR + 256 + 1024;
 };
 
 __global__ void __launch_bounds__(192, 1)
     attn_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                           const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
-                          const float* __restrict__ lse, const float* __restrict__ Dvec, float* __restrict__ dq_acc,
-                          int64_t ldq, float* __restrict__ dk_acc, float* __restrict__ dv_acc, int s, int c, int l,
+                          const __grid_constant__ CUtensorMap tmdQ, const float* __restrict__ lse,
+                          const float* __restrict__ Dvec, float* __restrict__ dk_acc, float* __restrict__ dv_acc, int s, int c, int l,
                           float scale, float scale_log2, int accumulate, volatile int* dbg) {
   extern __shared__ uint8_t smem_raw[];
 #define DBG(role, v)                                                                    \
@@ -403,25 +403,27 @@ __global__ void __launch_bounds__(192, 1)
     uint8_t* dSt = sm + BwdSmem::DS;
     const float* lse_h = lse + (int64_t)head * s + c;
     const float* D_h = Dvec + (int64_t)head * l;
-    auto drain_dq = [&](int i) {  // dQ^T of tile i: thread = head-dim index `row`, 64 query columns
+    float* dqs = reinterpret_cast<float*>(sm + BwdSmem::DQ);
+    // dQ^T of tile i (thread = head-dim index `row`) -> smem [64 q][128 d] -> one TMA reduce-add
+    auto drain_dq = [&](int i) {
       mbar_wait(dqfull, i & 1);
       tc_fence_after();
-      const int qrow0 = (qt0 + i) * BQB;
-      float* dst = dq_acc + (int64_t)head * AT + row;
+      if (threadIdx.x == 64) tma_wait_reads();  // previous reduce has finished reading the buffer
+      named_bar(1, 128);
 #pragma unroll
       for (int ch = 0; ch < BQB / 32; ++ch) {
         uint32_t r[32];
         tmem_ld32_nowait(lane_base + T_DQ + ch * 32, r);
         tmem_wait_ld();
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const int qr = qrow0 + ch * 32 + t;
-          if (qr < l) atomicAdd(dst + (int64_t)qr * ldq, __uint_as_float(r[t]) * scale);
-        }
+        for (int t = 0; t < 32; ++t) dqs[(ch * 32 + t) * AT + row] = __uint_as_float(r[t]) * scale;
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(dqfree);
+      fence_proxy_async();
+      named_bar(1, 128);
+      if (threadIdx.x == 64) tma_reduce_add_2d(&tmdQ, dqs, head * AT, (qt0 + i) * BQB);
     };
     for (int i = 0; i < ntile; ++i) {
       const int qrow0 = (qt0 + i) * BQB;
@@ -469,6 +471,7 @@ __global__ void __launch_bounds__(192, 1)
       if (i >= 1) drain_dq(i - 1);
     }
     drain_dq(ntile - 1);
+    if (threadIdx.x == 64) tma_wait_all();
     if (lane == 0) DBG(2 + q, 900);
     // dK (x scale) and dV rows of this key block -> fp32 prefix accumulators
     mbar_wait(done, 0);
@@ -573,9 +576,13 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
   const uint64_t odims[2] = {(uint64_t)H, (uint64_t)l};
   const uint64_t ostr[1] = {(uint64_t)ld_do * 2};
   const uint32_t obox[2] = {64, BQB};
-  CUtensorMap mk, mv, mq, mo;
+  const uint64_t qdims[2] = {(uint64_t)H, (uint64_t)l};
+  const uint64_t qstr[1] = {(uint64_t)H * 4};
+  const uint32_t qrbox[2] = {AT, BQB};
+  CUtensorMap mk, mv, mq, mo, mdq;
   if (!encode_bf16_map(&mk, k, 3, kdims, kstr, kbox) || !encode_bf16_map(&mv, v, 3, kdims, kstr, kbox) ||
-      !encode_bf16_map(&mq, q, 3, kdims, kstr, qbox) || !encode_bf16_map(&mo, dO, 2, odims, ostr, obox))
+      !encode_bf16_map(&mq, q, 3, kdims, kstr, qbox) || !encode_bf16_map(&mo, dO, 2, odims, ostr, obox) ||
+      !encode_f32_map_noswizzle(&mdq, dq_acc, 2, qdims, qstr, qrbox))
     return cudaErrorInvalidValue;
   const float scale = rsqrtf((float)d);
   dim3 grid((c + l + AT - 1) / AT, a);
@@ -586,7 +593,7 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
   }
   int* dbg_dev = nullptr;
   if (dbg_on) { memset(dbg, 0, 4096 * sizeof(int)); cudaHostGetDevicePointer(&dbg_dev, dbg, 0); }
-  attn_bwd_sm100_kernel<<<grid, 192, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, lse, Dvec, dq_acc, H, dk_acc, dv_acc, s, c, l,
+  attn_bwd_sm100_kernel<<<grid, 192, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, mdq, lse, Dvec, dk_acc, dv_acc, s, c, l,
                                                            scale, scale * LOG2E_F, accumulate, dbg_dev);
   e = cudaGetLastError();
   if (dbg_on) {
