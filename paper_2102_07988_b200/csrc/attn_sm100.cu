@@ -53,6 +53,12 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[3
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // byte offset of 16-byte chunk `cc` (0..7) of row `row` inside a 128B-swizzled K-major atom region
 __device__ __forceinline__ uint32_t swz(int row, int cc) {
   return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((cc ^ (row & 7)) << 4));
@@ -165,14 +171,14 @@ __global__ void __launch_bounds__(192, 1)
       const int bi = i & 1;
       mbar_wait(ofull + bi, (i >> 1) & 1);
       tc_fence_after();
-      const float sc = exp2f(m_acc - m_i);
+      const float sc = ex2(m_acc - m_i);
 #pragma unroll
       for (int ch = 0; ch < AT / 32; ++ch) {
         uint32_t r[32];
         tmem_ld32_nowait(lane_base + 256 + bi * 128 + ch * 32, r);
         tmem_wait_ld();
 #pragma unroll
-        for (int t = 0; t < 32; ++t) acc[ch * 32 + t] = acc[ch * 32 + t] * sc + __uint_as_float(r[t]);
+        for (int t = 0; t < 32; ++t) acc[ch * 32 + t] = fmaf(acc[ch * 32 + t], sc, __uint_as_float(r[t]));
       }
       m_acc = m_i;
       tc_fence_before();
@@ -184,21 +190,26 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(sfull + b, (j >> 1) & 1);
       tc_fence_after();
       const int key0 = j * AT;
-      const bool diag = key0 + AT - 1 > qabs;
+      const bool diag = key0 + AT - 1 > qabs;  // only the diagonal block needs the causal mask
+      const int nvis = qabs - key0 + 1;        // keys key0 .. qabs are visible (diag blocks)
+      // pass 1: row max of the raw scores (scale > 0 commutes with max)
       float mx = -INFINITY;
 #pragma unroll
       for (int ch = 0; ch < AT / 32; ++ch) {
         uint32_t r[32];
         tmem_ld32_nowait(lane_base + b * 128 + ch * 32, r);
         tmem_wait_ld();
+        if (!diag) {
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const float x = (diag && key0 + ch * 32 + t > qabs) ? -INFINITY : __uint_as_float(r[t]) * scale_log2;
-          mx = fmaxf(mx, x);
+          for (int t = 0; t < 32; ++t) mx = fmaxf(mx, __uint_as_float(r[t]));
+        } else {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) mx = fmaxf(mx, ch * 32 + t < nvis ? __uint_as_float(r[t]) : -INFINITY);
         }
       }
-      const float m_new = fmaxf(m, mx);
+      const float m_new = fmaxf(m, mx * scale_log2);
       if (j >= 1) mbar_wait(pfree, (j - 1) & 1);  // PV_{j-1} has finished reading the P tile
+      // pass 2: P = exp2(S * scale_log2 - m_new) -> bf16, 128B-swizzled K-major tile
       float rs = 0.f;
 #pragma unroll
       for (int ch = 0; ch < AT / 32; ++ch) {
@@ -208,10 +219,12 @@ __global__ void __launch_bounds__(192, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int t = 0; t < 32; t += 2) {
-          const int k0i = key0 + ch * 32 + t;
-          const float x0 = (diag && k0i > qabs) ? -INFINITY : __uint_as_float(r[t]) * scale_log2;
-          const float x1 = (diag && k0i + 1 > qabs) ? -INFINITY : __uint_as_float(r[t + 1]) * scale_log2;
-          const float p0 = exp2f(x0 - m_new), p1 = exp2f(x1 - m_new);
+          float p0 = ex2(fmaf(__uint_as_float(r[t]), scale_log2, -m_new));
+          float p1 = ex2(fmaf(__uint_as_float(r[t + 1]), scale_log2, -m_new));
+          if (diag) {
+            p0 = ch * 32 + t < nvis ? p0 : 0.f;
+            p1 = ch * 32 + t + 1 < nvis ? p1 : 0.f;
+          }
           rs += p0 + p1;
           __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
           pk[t >> 1] = *reinterpret_cast<uint32_t*>(&h);
@@ -227,7 +240,7 @@ __global__ void __launch_bounds__(192, 1)
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) { mbar_arrive(sfree + b); mbar_arrive(pfull); }
-      lsum = lsum * exp2f(m - m_new) + rs;
+      lsum = lsum * ex2(m - m_new) + rs;
       m_last = m;
       m = m_new;
       if (j >= 1) add_o(j - 1, m_last);
@@ -272,7 +285,9 @@ constexpr uint32_t PT = AT * BQB * 2;            // 16 KiB: [128 keys][64 q] (on
 
 struct BwdSmem {
   static constexpr uint32_t K = 0, V = TILE, Q0 = 2 * TILE, Q1 = Q0 + QT, O0 = Q1 + QT, O1 = O0 + QT;
-  static constexpr uint32_t P = O1 + QT, DS = P + PT, DQ = DS + PT /* fp32 [64 q][128 d] */, BAR = DQ + 32768;
+  static constexpr uint32_t P = O1 + QT, DS = P + PT, DQ = DS + PT /* fp32 [64 q][128 d] */;
+  static constexpr uint32_t LD = DQ + 32768; /* fp32 [2 tiles][lse*log2e[64], D[64]] */
+  static constexpr uint32_t BAR = LD + 1024;
   static constexpr uint32_t BYTES = BAR + 256 + 1024;
 };
 
@@ -427,11 +442,21 @@ __global__ void __launch_bounds__(192, 1)
     };
     for (int i = 0; i < ntile; ++i) {
       const int qrow0 = (qt0 + i) * BQB;
+      float* Ls = reinterpret_cast<float*>(sm + BwdSmem::LD) + (i & 1) * 2 * BQB;  // double-buffered by tile
+      float* Ds = Ls + BQB;
       if (lane == 0) DBG(2 + q, 100 + 10 * i);
+      {  // stage lse*log2e and D of this tile's 64 queries (rows past the slice: +inf / 0)
+        const int t = threadIdx.x - 64, qr = qrow0 + (t & 63);
+        if (t < 64) Ls[t] = qr < l ? __ldg(lse_h + qr) * LOG2E_F : INFINITY;
+        else Ds[t - 64] = qr < l ? __ldg(D_h + qr) : 0.f;
+      }
+      named_bar(1, 128);
       mbar_wait(sfull, i & 1);
       if (lane == 0) DBG(2 + q, 101 + 10 * i);
       tc_fence_after();
       if (i >= 1) mbar_wait(pfree, (i - 1) & 1);  // MMAs of tile i-1 have read P^T / dS^T
+      // visible iff c + qr >= kabs (and qr < l, which Ls = +inf enforces)
+      const int vis0 = kabs - c - qrow0;  // first visible column of this key row
 #pragma unroll
       for (int ch = 0; ch < BQB / 32; ++ch) {
         uint32_t rs[32], rp[32];
@@ -444,13 +469,11 @@ __global__ void __launch_bounds__(192, 1)
           float pv[2], dv[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int qr = qrow0 + ch * 32 + t + e;
-            const bool ok = qr < l && c + qr >= kabs;
-            const float L2 = ok ? __ldg(lse_h + qr) * LOG2E_F : 0.f;
-            const float Dq = ok ? __ldg(D_h + qr) : 0.f;
-            const float p = ok ? exp2f(__uint_as_float(rs[t + e]) * scale_log2 - L2) : 0.f;
+            const int col = ch * 32 + t + e;
+            float p = ex2(fmaf(__uint_as_float(rs[t + e]), scale_log2, -Ls[col]));
+            p = col >= vis0 ? p : 0.f;
             pv[e] = p;
-            dv[e] = p * (__uint_as_float(rp[t + e]) - Dq);
+            dv[e] = p * (__uint_as_float(rp[t + e]) - Ds[col]);
           }
           __nv_bfloat162 hp = __floats2bfloat162_rn(pv[0], pv[1]);
           __nv_bfloat162 hd = __floats2bfloat162_rn(dv[0], dv[1]);

@@ -8,6 +8,19 @@
 using namespace tp;
 
 namespace {
+// grow-only device scratch (kernel-level entry points are test/benchmark plumbing; per-call
+// cudaMallocAsync would put pool growth/trim inside the timed region)
+float* scratch(int which, size_t n) {
+  static float* buf[2] = {nullptr, nullptr};
+  static size_t cap[2] = {0, 0};
+  if (n > cap[which]) {
+    if (buf[which]) cudaFree(buf[which]);
+    buf[which] = nullptr;
+    if (cudaMalloc(&buf[which], n * sizeof(float)) != cudaSuccess) { cap[which] = 0; return nullptr; }
+    cap[which] = n;
+  }
+  return buf[which];
+}
 tp_status cu(cudaError_t e, const char* what) {
   if (e != cudaSuccess) return fail(TP_ECUDA, "%s: %s", what, cudaGetErrorString(e));
   return TP_OK;
@@ -50,17 +63,15 @@ extern "C" tp_status tpk_attention_bwd(const void* dO, const void* o, const void
   TP_CHECK_ARG(dO && o && q && k && v && lse && dq && dk_acc && dv_acc, "tpk_attention_bwd: null pointer");
   TP_CHECK_ARG(a >= 1 && d % 16 == 0 && d <= 128 && c >= 0 && l >= 1 && c + l <= s, "tpk_attention_bwd: bad shape");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  float* Dvec = nullptr;
-  tp_status r = cu(cudaMallocAsync(&Dvec, sizeof(float) * a * l, st), "cudaMallocAsync");
-  if (r != TP_OK) return r;
+  float* Dvec = scratch(0, (size_t)a * l);
+  if (!Dvec) return fail(TP_ENOMEM, "tpk_attention_bwd: scratch");
+  tp_status r = TP_OK;
   const int64_t H = (int64_t)a * d;
   if (impl == 0 && attn_sm100_supported(d)) {
-    float* dq_acc = nullptr;
-    r = cu(cudaMallocAsync(&dq_acc, sizeof(float) * H * l, st), "cudaMallocAsync");
-    if (r != TP_OK) return r;
+    float* dq_acc = scratch(1, (size_t)H * l);
+    if (!dq_acc) return fail(TP_ENOMEM, "tpk_attention_bwd: scratch");
     r = cu(attn_bwd_sm100((const bf16*)dO, H, (const bf16*)o, H, (const bf16*)q, (const bf16*)k, (const bf16*)v, lse, Dvec,
                           dq_acc, (bf16*)dq, ldq, dk_acc, dv_acc, a, s, d, c, l, accumulate, st), "attn_bwd_sm100");
-    cudaFreeAsync(dq_acc, st);
   } else if (impl == 0 || impl == 2)
     r = cu(attn_bwd_tc((const bf16*)dO, H, (const bf16*)o, H, (const bf16*)q, (const bf16*)k, (const bf16*)v, lse, Dvec,
                        (bf16*)dq, ldq, dk_acc, dv_acc, a, s, d, c, l, accumulate, st), "attn_bwd_tc");
@@ -68,6 +79,5 @@ extern "C" tp_status tpk_attention_bwd(const void* dO, const void* o, const void
     r = cu(attn_bwd_simt<bf16>((const bf16*)dO, H, (const bf16*)o, H, (const bf16*)q, (const bf16*)k, (const bf16*)v,
                                lse, Dvec, (bf16*)dq, ldq, dk_acc, dv_acc, a, s, d, c, l, accumulate, st),
            "attn_bwd_simt");
-  cudaFreeAsync(Dvec, st);
   return r;
 }
