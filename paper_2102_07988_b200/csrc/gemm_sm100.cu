@@ -44,7 +44,8 @@ struct Cfg {
   static constexpr uint32_t B_BYTES = (BN / CG) * BK * 2;
   static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
   static constexpr int NS = (196608 / STAGE) > 8 ? 8 : (196608 / STAGE);  // pipeline depth
-  static constexpr uint32_t SMEM = NS * STAGE + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr uint32_t EPI_SCRATCH = 4 * 32 * 33 * 4;  // per epilogue warp: 32 x 32 fp32 (+1 pad)
+  static constexpr uint32_t SMEM = NS * STAGE + EPI_SCRATCH + 1024 /*align slack*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = 2 * BN;  // double-buffered fp32 accumulator
   static constexpr int TILE_M = BM * CG;
 };
@@ -56,7 +57,8 @@ __global__ void __launch_bounds__(192, 1)
   using C = Cfg<CG, BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::NS * C::STAGE);
+  float* epi_scratch = reinterpret_cast<float*>(smem + C::NS * C::STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::NS * C::STAGE + C::EPI_SCRATCH);
   uint64_t* empty = full + C::NS;
   uint64_t* tfull = empty + C::NS;
   uint64_t* tempty = tfull + 2;
@@ -169,23 +171,27 @@ __global__ void __launch_bounds__(192, 1)
       const int m0 = (tile % m_tiles) * C::TILE_M + crank * BM, n0 = (tile / m_tiles) * BN;
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
-      const int row = m0 + q * 32 + lane;
+      // TMEM (thread = row) -> padded smem transpose -> 4 lanes per row, 8 columns each: every
+      // global access of the fused epilogue is a 64/128-byte contiguous row segment.
+      float* scr = epi_scratch + (warp - 2) * 32 * 33;
 #pragma unroll 1
       for (int ch = 0; ch < BN / 32; ++ch) {
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 32, r);
-        if (row < M) {
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const int n = n0 + ch * 32 + g * 8;
-            if (n < N) {
-              float v[8];
+        for (int i = 0; i < 32; ++i) scr[lane * 33 + i] = __uint_as_float(r[i]);
+        __syncwarp();
+        const int n = n0 + ch * 32 + (lane & 3) * 8;
 #pragma unroll
-              for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[g * 8 + i]);
-              epi_apply8<bf16>(epi, row, n, v);
-            }
-          }
+        for (int it = 0; it < 4; ++it) {
+          const int rr = it * 8 + (lane >> 2);
+          const int row = m0 + q * 32 + rr;
+          float v[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = scr[rr * 33 + (lane & 3) * 8 + i];
+          if (row < M && n < N) epi_apply8<bf16>(epi, row, n, v);
         }
+        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();

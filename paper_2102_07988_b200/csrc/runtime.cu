@@ -196,7 +196,7 @@ struct Stage {
   float* logits_keep = nullptr;   // [B][s][V] (TP_FLAG_KEEP_LOGITS)
   float* grad_out = nullptr;      // [B][s][H] dloss/d(stage output)
   float* grad_in = nullptr;       // [B][s][H] dloss/d(stage input)
-  // backward stash of ONE sequence (deferred dW)
+  // backward stash over [B][s] rows: the operands of the deferred weight-gradient GEMMs
   std::vector<T*> dQKV, dhmid_b, dU, dhout_b;
   std::vector<float*> dk_acc, dv_acc;  // [a][s][d]
   float *gA = nullptr, *gB = nullptr, *gm = nullptr, *dA = nullptr, *Dvec = nullptr, *lnws = nullptr, *dqacc = nullptr;
@@ -342,8 +342,8 @@ class Engine final : public EngineBase {
       TRY(alloc(&S.grad_in, B * s * H));
     }
     (void)first;
-    TRY(vec(S.dQKV, nl, s * 3 * H)); TRY(vec(S.dhmid_b, nl, s * H));
-    TRY(vec(S.dU, nl, s * 4 * H)); TRY(vec(S.dhout_b, nl, s * H));
+    TRY(vec(S.dQKV, nl, B * s * 3 * H)); TRY(vec(S.dhmid_b, nl, B * s * H));
+    TRY(vec(S.dU, nl, B * s * 4 * H)); TRY(vec(S.dhout_b, nl, B * s * H));
     TRY(vec(S.dk_acc, nl, s * H)); TRY(vec(S.dv_acc, nl, s * H));
     TRY(alloc(&S.gA, s * H)); TRY(alloc(&S.gB, s * H)); TRY(alloc(&S.gm, s * H)); TRY(alloc(&S.dA, s * H));
     TRY(alloc(&S.Dvec, a * s)); TRY(alloc(&S.dO, s * H));
@@ -506,11 +506,11 @@ class Engine final : public EngineBase {
       TRY(gemm(KC_GEMM_DX, gd(l, H, V, S.Z + row * V, V, false, S.wout_io, V, false), e));
       TRY(launch(KC_LN, 0, (12.0 + ebytes) * l * H, [&] {
         return layernorm_bwd<T>(S.dA, S.hs[S.nl] + row * H, S.stf + row, S.stf + (size_t)batch * s + row, P + S.L.s_lnf_g, nullptr, g,
-                                S.dhout_b[S.nl - 1] + (size_t)c * H, S.gflat + S.L.lnf_g, S.gflat + S.L.lnf_b, S.lnws, l, H, stream);
+                                S.dhout_b[S.nl - 1] + row * H, S.gflat + S.L.lnf_g, S.gflat + S.L.lnf_b, S.lnws, l, H, stream);
       }));
     } else {
       TRY(launch(KC_MISC, 0, (4.0 + ebytes) * l * H, [&] {
-        return convert_f32<T>(g, S.dhout_b[S.nl - 1] + (size_t)c * H, (int64_t)l * H, stream);
+        return convert_f32<T>(g, S.dhout_b[S.nl - 1] + row * H, (int64_t)l * H, stream);
       }));
     }
     for (int j = S.nl - 1; j >= 0; --j) {
@@ -519,20 +519,20 @@ class Engine final : public EngineBase {
       const float* P = S.psmall;
       float* GR = S.gflat;
       // FFN: dU = (dh W_2^T) * gelu'(U)
-      Epi e1; e1.kind = EPI_DGELU; e1.out = S.dU[j] + (size_t)c * 4 * H; e1.ldo = 4 * H; e1.aux = S.U[j] + row * 4 * H; e1.ld_aux = 4 * H;
-      TRY(gemm(KC_GEMM_DX, gd(l, 4 * H, H, S.dhout_b[j] + (size_t)c * H, H, false, S.w2_io[j], H, false), e1));
+      Epi e1; e1.kind = EPI_DGELU; e1.out = S.dU[j] + row * 4 * H; e1.ldo = 4 * H; e1.aux = S.U[j] + row * 4 * H; e1.ld_aux = 4 * H;
+      TRY(gemm(KC_GEMM_DX, gd(l, 4 * H, H, S.dhout_b[j] + row * H, H, false, S.w2_io[j], H, false), e1));
       Epi e2; e2.kind = EPI_STORE; e2.out = S.dA; e2.ldo = H; e2.out_f32 = 1;
-      TRY(gemm(KC_GEMM_DX, gd(l, H, 4 * H, S.dU[j] + (size_t)c * 4 * H, 4 * H, false, S.w1_io[j], 4 * H, false), e2));
+      TRY(gemm(KC_GEMM_DX, gd(l, H, 4 * H, S.dU[j] + row * 4 * H, 4 * H, false, S.w1_io[j], 4 * H, false), e2));
       float* st2 = S.st2[j];
       TRY(launch(KC_LN, 0, (16.0 + ebytes) * l * H, [&] {
         return layernorm_bwd<T>(S.dA, S.hmid[j] + row * H, st2 + row, st2 + (size_t)batch * s + row, P + fs.ln2_g, g, S.gm,
-                                S.dhmid_b[j] + (size_t)c * H, GR + f.ln2_g, GR + f.ln2_b, S.lnws, l, H, stream);
+                                S.dhmid_b[j] + row * H, GR + f.ln2_g, GR + f.ln2_b, S.lnws, l, H, stream);
       }));
       // attention: dO = dh_mid W_o^T, then slice-vs-prefix attention backward with dK/dV push
       Epi e3; e3.kind = EPI_STORE; e3.out = S.dO; e3.ldo = H;
-      TRY(gemm(KC_GEMM_DX, gd(l, H, H, S.dhmid_b[j] + (size_t)c * H, H, false, S.wo_io[j], H, false), e3));
+      TRY(gemm(KC_GEMM_DX, gd(l, H, H, S.dhmid_b[j] + row * H, H, false, S.wo_io[j], H, false), e3));
       const double attn_flops = 8.0 * H * ((double)l * c + 0.5 * l * (l + 1.0));
-      T* dq = S.dQKV[j] + (size_t)c * 3 * H;
+      T* dq = S.dQKV[j] + row * 3 * H;
       TRY(launch(KC_ATTN_BWD, attn_flops, ebytes * 4.0 * H * (c + l) + 16.0 * H * (c + l), [&] {
         const T *q = S.Q[j] + (size_t)d * s * H, *kk = S.Kc[j] + (size_t)d * s * H, *vv = S.Vc[j] + (size_t)d * s * H;
         const int accum = first_bwd_slice ? 0 : 1;
@@ -553,7 +553,7 @@ class Engine final : public EngineBase {
       Epi e4; e4.kind = EPI_STORE; e4.out = S.dA; e4.ldo = H; e4.out_f32 = 1;
       TRY(gemm(KC_GEMM_DX, gd(l, H, 3 * H, dq, 3 * H, false, S.wqkv_io[j], 3 * H, false), e4));
       float* gnext = j == 0 ? S.grad_in + row * H : (g == S.gA ? S.gB : S.gA);
-      T* copy = j == 0 ? nullptr : S.dhout_b[j - 1] + (size_t)c * H;
+      T* copy = j == 0 ? nullptr : S.dhout_b[j - 1] + row * H;
       float* st1 = S.st1[j];
       TRY(launch(KC_LN, 0, (16.0 + ebytes) * l * H, [&] {
         return layernorm_bwd<T>(S.dA, S.hs[j] + row * H, st1 + row, st1 + (size_t)batch * s + row, P + fs.ln1_g, S.gm, gnext, copy,
@@ -569,33 +569,36 @@ class Engine final : public EngineBase {
     return TP_OK;
   }
 
-  // ------------------------------------------------------------ deferred weight gradients of sequence d
-  tp_status wgrad(Stage<T>& S, int d) {
-    const int H = m.H, s = m.s, V = m.V;
-    const size_t row = (size_t)d * s;
+  // ------------------------------------------------------------ deferred weight gradients
+  // One GEMM per weight over all B*s tokens of the step (K = B*s, both operands MN-major), written
+  // once (the gradients start at zero), plus the bias column sums: off the per-job critical path and
+  // with no fp32 read-modify-write.
+  tp_status wgrad(Stage<T>& S, int batch) {
+    const int H = m.H, V = m.V;
+    const int K = batch * m.s;
     float* GR = S.gflat;
     for (int j = 0; j < S.nl; ++j) {
       const LayerOff& f = S.L.layers[j];
-      Epi e; e.kind = EPI_ACCUM;
+      Epi e; e.kind = EPI_STORE; e.out_f32 = 1;
       e.out = GR + f.w_qkv; e.ldo = 3 * H;
-      TRY(gemm(KC_GEMM_DW, gd(H, 3 * H, s, S.A1[j] + row * H, H, true, S.dQKV[j], 3 * H, true), e));
+      TRY(gemm(KC_GEMM_DW, gd(H, 3 * H, K, S.A1[j], H, true, S.dQKV[j], 3 * H, true), e));
       e.out = GR + f.w_o; e.ldo = H;
-      TRY(gemm(KC_GEMM_DW, gd(H, H, s, S.O[j] + row * H, H, true, S.dhmid_b[j], H, true), e));
+      TRY(gemm(KC_GEMM_DW, gd(H, H, K, S.O[j], H, true, S.dhmid_b[j], H, true), e));
       e.out = GR + f.w_1; e.ldo = 4 * H;
-      TRY(gemm(KC_GEMM_DW, gd(H, 4 * H, s, S.A2[j] + row * H, H, true, S.dU[j], 4 * H, true), e));
+      TRY(gemm(KC_GEMM_DW, gd(H, 4 * H, K, S.A2[j], H, true, S.dU[j], 4 * H, true), e));
       e.out = GR + f.w_2; e.ldo = H;
-      TRY(gemm(KC_GEMM_DW, gd(4 * H, H, s, S.G[j] + row * 4 * H, 4 * H, true, S.dhout_b[j], H, true), e));
-      TRY(launch(KC_MISC, 0, sizeof(T) * 9.0 * s * H, [&] {
-        cudaError_t r = colsum_accum<T>(S.dQKV[j], 3 * H, GR + f.b_qkv, s, 3 * H, stream);
-        if (r == cudaSuccess) r = colsum_accum<T>(S.dhmid_b[j], H, GR + f.b_o, s, H, stream);
-        if (r == cudaSuccess) r = colsum_accum<T>(S.dU[j], 4 * H, GR + f.b_1, s, 4 * H, stream);
-        if (r == cudaSuccess) r = colsum_accum<T>(S.dhout_b[j], H, GR + f.b_2, s, H, stream);
+      TRY(gemm(KC_GEMM_DW, gd(4 * H, H, K, S.G[j], 4 * H, true, S.dhout_b[j], H, true), e));
+      TRY(launch(KC_MISC, 0, sizeof(T) * 9.0 * K * H, [&] {
+        cudaError_t r = colsum_accum<T>(S.dQKV[j], 3 * H, GR + f.b_qkv, K, 3 * H, stream);
+        if (r == cudaSuccess) r = colsum_accum<T>(S.dhmid_b[j], H, GR + f.b_o, K, H, stream);
+        if (r == cudaSuccess) r = colsum_accum<T>(S.dU[j], 4 * H, GR + f.b_1, K, 4 * H, stream);
+        if (r == cudaSuccess) r = colsum_accum<T>(S.dhout_b[j], H, GR + f.b_2, K, H, stream);
         return r;
       }));
     }
     if (S.k == m.K - 1) {
-      Epi e; e.kind = EPI_ACCUM; e.out = GR + S.L.w_out; e.ldo = V;
-      TRY(gemm(KC_GEMM_DW, gd(H, V, s, S.Af + row * H, H, true, S.Z + row * V, V, true), e));
+      Epi e; e.kind = EPI_STORE; e.out_f32 = 1; e.out = GR + S.L.w_out; e.ldo = V;
+      TRY(gemm(KC_GEMM_DW, gd(H, V, K, S.Af, H, true, S.Z, V, true), e));
     }
     return TP_OK;
   }
@@ -674,8 +677,8 @@ class Engine final : public EngineBase {
           TRY(bwd(S, d, off[i], sl->lengths[i], batch, i == M - 1));
           if (multi && S.k > 0) TRY(send_bwd(S, row, sl->lengths[i]));
         }
-      for (auto& S : stages) TRY(wgrad(S, d));
     }
+    for (auto& S : stages) TRY(wgrad(S, batch));
     // loss: sum of per-token NLL on the last stage, mean over batch*seq_len (A-9)
     Stage<T>* last = nullptr;
     for (auto& S : stages) if (S.k == m.K - 1) last = &S;
