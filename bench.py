@@ -139,6 +139,7 @@ def main():
     ap.add_argument("--no-gpipe", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slicing", default="dp", help="dp | gpipe | comma-separated lengths")
+    ap.add_argument("--batch-slices", default="auto", help="auto | comma-separated batch-slice sizes b to plan over")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -198,26 +199,41 @@ def main():
     tok_pin = torch.from_numpy(tokens).pin_memory()
     stream = torch.cuda.ExternalStream(ctx.stream())
 
-    # --- cost table (this stage; max over stages = bottleneck table, A-16) and the DP plan
+    # --- cost tables (this stage; max over stages = bottleneck table, A-16) and the DP plan.
+    # Joint batch x token slicing with a uniform batch slice b: one table per b,
+    # tp_plan with D = B/b jobs per slice index, keep the b with the smallest predicted T (A-20).
     g = args.granularity
+    bsl = [int(x) for x in args.batch_slices.split(",")] if args.batch_slices != "auto" else \
+        [x for x in (1, 2, 4, 8, 16) if B % x == 0 and x <= B]
+    dp, fit, t_prof, t_plan, plans = None, None, 0.0, 0.0, []
     gpipe = tp.Slicing([cfg.seq_len])
-    dp, fit, t_prof, t_plan = None, None, 0.0, 0.0
-    if args.slicing == "dp":
-        t_prof = time.time()
-        ticks, fit = ctx.profile(g, reps=3)
-        if world > 1:
-            ticks = tdist.bottleneck_table(ticks)
-        t_prof = time.time() - t_prof
-        t_plan = time.time()
-        dp = tp.plan(ticks, g, cfg.n_layer, cfg.hidden, cfg.seq_len, K, n_micro=B, eps_ticks=0)
-        t_plan = time.time() - t_plan
-        if world > 1 and not tdist.agreed(dp.lengths):
+    if args.slicing in ("dp", "gpipe") and (args.slicing == "dp" or len(bsl) > 1):
+        t0 = time.time()
+        for b in bsl:
+            ticks, f = ctx.profile(g, reps=3, batch_slice=b)
+            if world > 1:
+                ticks = tdist.bottleneck_table(ticks)
+            t1 = time.time()
+            sl = tp.plan(ticks, g, cfg.n_layer, cfg.hidden, cfg.seq_len, K, n_micro=B // b, eps_ticks=0)
+            t_plan += time.time() - t1
+            sl = tp.Slicing(sl.lengths, b, sl.t_max, sl.predicted)
+            n = cfg.seq_len // g
+            gp_pred = (B // b + K - 1) * int(ticks[n - 1, 0])   # unsliced [(b, [s])] * (B/b)
+            plans.append({"b": b, "slicing": sl, "fit": f, "gpipe_pred": gp_pred})
+        t_prof = time.time() - t0 - t_plan
+        best = min(plans, key=lambda p: (p["slicing"].predicted, -p["b"]))
+        dp, fit = best["slicing"], best["fit"]
+        gbest = min(plans, key=lambda p: (p["gpipe_pred"], -p["b"]))
+        gpipe = tp.Slicing([cfg.seq_len], gbest["b"])
+        if world > 1 and not tdist.agreed(dp.lengths + [dp.batch_slice, gpipe.batch_slice]):
             raise RuntimeError("ranks planned different slicings")
+    if args.slicing == "dp":
         main_sl = dp
     elif args.slicing == "gpipe":
         main_sl = gpipe
     else:
-        main_sl = tp.Slicing([int(x) for x in args.slicing.split(",")])
+        main_sl = tp.Slicing([int(x) for x in args.slicing.split(",")], int(args.batch_slices.split(",")[0])
+                             if args.batch_slices != "auto" else 1)
 
     def timed(sl, steps, device_tokens=True):
         barrier()
@@ -245,11 +261,12 @@ def main():
     ms_e2e, _ = timed(main_sl, args.steps, device_tokens=False)
     # unsliced GPipe on the same kernels
     ms_gpipe = None
-    if not args.no_gpipe and main_sl.lengths != gpipe.lengths:
+    same = main_sl.lengths == gpipe.lengths and main_sl.batch_slice == gpipe.batch_slice
+    if not args.no_gpipe and not same:
         for _ in range(1):
             ctx.step_device(gpipe, tok_dev.data_ptr(), B)
         ms_gpipe, _ = timed(gpipe, args.steps)
-    elif main_sl.lengths == gpipe.lengths:
+    elif same:
         ms_gpipe = ms
     # kernel statistics: a second timed region with CUDA events around every launch (on the
     # library's stream, which every kernel is launched on)
@@ -278,7 +295,9 @@ def main():
             "speedup_of_dp": ms_gpipe / ms},
         "plan": None if dp is None else {
             "predicted_ms": dp.predicted / 1e6, "t_max_ms": dp.t_max / 1e6, "profile_s": t_prof, "plan_s": t_plan,
-            "fit": {"a": [float(x) for x in fit[:4]], "max_rel_err": float(fit[4])}},
+            "fit": {"a": [float(x) for x in fit[:4]], "max_rel_err": float(fit[4])},
+            "candidates": [{"b": p["b"], "slicing": p["slicing"].notation(B), "predicted_ms": p["slicing"].predicted / 1e6,
+                            "gpipe_predicted_ms": p["gpipe_pred"] / 1e6} for p in plans]},
         "loss": loss,
         "clocks": clk,
         "e2e": {"value": tokens_per_step / (ms_e2e / 1e3), "unit": "tokens/s",

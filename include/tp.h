@@ -80,7 +80,8 @@ typedef struct {
 
 /* A slicing scheme [(b, [l_1..l_M])] * (B/b) in the paper's notation.
  * lengths: caller-owned array of `capacity` int32 (tokens; multiples of g, sum = seq_len).
- * batch_slice b: sequences per job (this build runs b = 1; other values -> TP_EINVAL in tp_step). */
+ * batch_slice b: sequences per job (b | batch): every job is b sequences x one token slice, so
+ * D = batch / b jobs share each slice index (joint batch x token slicing). */
 typedef struct {
   int32_t batch_slice;
   int32_t n_slices;          /* M                                          */
@@ -152,14 +153,14 @@ tp_status tp_get_grads(tp_ctx* ctx, float* host_out, size_t n);
  * TP_FLAG_KEEP_LOGITS and a context owning the last stage (else TP_ESTATE). */
 tp_status tp_get_logits(tp_ctx* ctx, float* host_out, size_t n);
 
-/* Measures this context's (first owned) stage: t_{fwd+bwd}(l, c) of one job of l tokens with c
- * tokens of context, in ns (median of `reps` after 2 warm-ups). The base curve t(l, 0) is measured
+/* Measures this context's (first owned) stage: t_{fwd+bwd}(l, c) of one job of batch_slice
+ * sequences x l tokens with c tokens of context, in ns (median of `reps` after 2 warm-ups). The base curve t(l, 0) is measured
  * for every l = g, 2g, .., s and t_ctx(l, c) = a0 + a1 l + a2 c + a3 l c is least-squares fitted on
  * a subset of (l, c); ticks_out[(l/g-1)*(n+1) + c/g] = t(l,0) + t_ctx(l,c)
  * (n = s/g; caller-owned, n*(n+1) int64). fit_out (may be NULL): a0..a3 (ns, ns/token, ns/token,
  * ns/token^2) and the max relative error of the fit on the samples. Parameters must be loaded. */
-tp_status tp_profile(tp_ctx* ctx, int32_t granularity, int32_t reps, int64_t* ticks_out,
-                     double* fit_out /* [5] */);
+tp_status tp_profile(tp_ctx* ctx, int32_t granularity, int32_t batch_slice, int32_t reps,
+                     int64_t* ticks_out, double* fit_out /* [5] */);
 
 /* The CUDA stream (cudaStream_t) all compute of this context is issued on. */
 tp_status tp_get_stream(tp_ctx* ctx, void** stream_out);

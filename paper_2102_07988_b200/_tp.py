@@ -65,7 +65,7 @@ def _load() -> C.CDLL:
         "tp_step_device": (C.c_int, [P, C.POINTER(SlicingC), P, C.c_int32, C.POINTER(C.c_float)]),
         "tp_get_grads": (C.c_int, [P, P, C.c_size_t]),
         "tp_get_logits": (C.c_int, [P, P, C.c_size_t]),
-        "tp_profile": (C.c_int, [P, C.c_int32, C.c_int32, P, P]),
+        "tp_profile": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, P, P]),
         "tp_get_stream": (C.c_int, [P, C.POINTER(P)]),
         "tp_kernel_stats": (C.c_int, [P, C.c_int32, C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                       C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
@@ -206,11 +206,11 @@ class Context:
         _check(_lib.tp_get_logits(self._h, out.ctypes.data, out.size))
         return out
 
-    def profile(self, granularity: int, reps: int = 5) -> Tuple[np.ndarray, np.ndarray]:
+    def profile(self, granularity: int, reps: int = 5, batch_slice: int = 1) -> Tuple[np.ndarray, np.ndarray]:
         n = self.cfg.seq_len // granularity
         ticks = np.zeros((n, n + 1), dtype=np.int64)
         fit = np.zeros(5, dtype=np.float64)
-        _check(_lib.tp_profile(self._h, granularity, reps, ticks.ctypes.data, fit.ctypes.data))
+        _check(_lib.tp_profile(self._h, granularity, batch_slice, reps, ticks.ctypes.data, fit.ctypes.data))
         return ticks, fit
 
     def stream(self) -> int:

@@ -6,7 +6,7 @@
 //   EPI_GELU  : U = acc + bias;  out = U (T);  out2 = gelu(U) (T)     (Eq. 3; A-2)
 //   EPI_DGELU : out[m][n] = acc * gelu'(aux[m][n])               (dU from dG and stored U)
 //   EPI_QKV   : v = acc + bias; column n -> (part = n / H, head = (n % H) / d, e = n % d);
-//               part 0 -> q, 1 -> k, 2 -> v, each [a][s][d] at row (row0 + m): the slice's
+//               part 0 -> q, 1 -> k, 2 -> v, each [seq][a][s][d] at (m % bs, row0 + m / bs): the slice's
 //               queries and its K/V appended to the per-layer prefix cache
 //   EPI_ACCUM : out[m][n] += acc                                (fp32 weight-gradient accumulate)
 #pragma once
@@ -32,6 +32,7 @@ struct Epi {
   void* k = nullptr;
   void* v = nullptr;
   int s_len = 0, head_dim = 0, hidden = 0, row0 = 0;
+  int bs = 1;                 // QKV: rows m -> (sequence m % bs, position row0 + m / bs); sequences s_len*hidden apart
 };
 
 __device__ __forceinline__ float gelu_f(float u) {
@@ -92,7 +93,8 @@ __device__ __forceinline__ void epi_apply8(const Epi& e, int m, int n0, float (&
       const int head = within / e.head_dim;
       const int dd = within - head * e.head_dim;
       T* base = reinterpret_cast<T*>(part == 0 ? e.q : (part == 1 ? e.k : e.v));
-      store8<T>(base + ((int64_t)head * e.s_len + e.row0 + m) * e.head_dim + dd, v);
+      const int sq = m % e.bs, pos = e.row0 + m / e.bs;
+      store8<T>(base + (int64_t)sq * e.s_len * e.hidden + ((int64_t)head * e.s_len + pos) * e.head_dim + dd, v);
       break;
     }
     case EPI_ACCUM: {

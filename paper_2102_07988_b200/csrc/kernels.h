@@ -36,14 +36,16 @@ cudaError_t layernorm_bwd(const float* dy, const float* x, const float* mean, co
                           float* dgam, float* dbet, float* ws /* >= 2*H*ceil(rows/4) floats */, int rows, int H,
                           cudaStream_t st);
 
-cudaError_t embed_fwd(const int32_t* tok, const float* wte, const float* wpe, float* h, int c, int l,
-                      int H, int V, cudaStream_t st);
-cudaError_t embed_bwd(const int32_t* tok, const float* dh, float* gwte, float* gwpe, int c, int l,
-                      int H, cudaStream_t st);
+// Job rows m = 0..b*l-1 map to (sequence j = m % b, position p = c + m / b); tok points at the job's
+// first sequence row of tokens[B][s+1].
+cudaError_t embed_fwd(const int32_t* tok, const float* wte, const float* wpe, float* h, int c, int l, int b,
+                      int s, int H, int V, cudaStream_t st);
+cudaError_t embed_bwd(const int32_t* tok, const float* dh, float* gwte, float* gwpe, int c, int l, int b,
+                      int s, int H, cudaStream_t st);
 
 template <typename T>
-cudaError_t ce_fwd_bwd(T* logits_inout, const int32_t* targets, float* loss_rows, float* logits_copy,
-                       int rows, int V, float scale, cudaStream_t st);
+cudaError_t ce_fwd_bwd(T* logits_inout, const int32_t* tok, int c, int b, int s, float* loss_rows,
+                       float* logits_copy, int rows, int V, float scale, cudaStream_t st);
 cudaError_t sum_rows(const float* x, int n, float* out, cudaStream_t st);
 
 template <typename T>

@@ -158,12 +158,14 @@ __global__ void ln_bwd_reduce_kernel(const float* __restrict__ ws, int nb, float
 
 // ---------------------------------------------------------------- embedding
 __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const float* __restrict__ wte,
-                                 const float* __restrict__ wpe, float* __restrict__ h, int c, int H, int V) {
+                                 const float* __restrict__ wpe, float* __restrict__ h, int c, int b, int s, int H,
+                                 int V) {
   const int r = blockIdx.x;
-  int id = tok[c + r];
+  const int j = r % b, pos = c + r / b;
+  int id = tok[(int64_t)j * (s + 1) + pos];
   id = min(max(id, 0), V - 1);
   const float* e = wte + (int64_t)id * H;
-  const float* p = wpe + (int64_t)(c + r) * H;
+  const float* p = wpe + (int64_t)pos * H;
   float* o = h + (int64_t)r * H;
   for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
     float4 a = *reinterpret_cast<const float4*>(e + i), b = *reinterpret_cast<const float4*>(p + i);
@@ -172,24 +174,26 @@ __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const float* _
 }
 
 __global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const float* __restrict__ dh,
-                                 float* __restrict__ gwte, float* __restrict__ gwpe, int c, int H) {
+                                 float* __restrict__ gwte, float* __restrict__ gwpe, int c, int b, int s, int H) {
   const int r = blockIdx.x;
-  const int id = tok[c + r];
+  const int j = r % b, pos = c + r / b;
+  const int id = tok[(int64_t)j * (s + 1) + pos];
   const float* g = dh + (int64_t)r * H;
   float* e = gwte + (int64_t)id * H;
-  float* p = gwpe + (int64_t)(c + r) * H;  // rows c..c+l are owned by this job alone
+  float* p = gwpe + (int64_t)pos * H;  // positions c..c+l are shared by the job's b sequences
   for (int i = threadIdx.x; i < H; i += blockDim.x) {
     const float v = g[i];
     atomicAdd(e + i, v);
-    p[i] += v;
+    if (b == 1) p[i] += v;
+    else atomicAdd(p + i, v);
   }
 }
 
 // ---------------------------------------------------------------- cross-entropy
 // per row: lse = log sum exp z; loss_row = lse - z_y; z <- (softmax(z) - onehot(y)) * scale.
 template <typename T>
-__global__ void __launch_bounds__(512) ce_kernel(T* __restrict__ z, const int32_t* __restrict__ tgt,
-                                                 float* __restrict__ loss_rows, float* __restrict__ zcopy,
+__global__ void __launch_bounds__(512) ce_kernel(T* __restrict__ z, const int32_t* __restrict__ tok, int c, int b,
+                                                 int seq_len, float* __restrict__ loss_rows, float* __restrict__ zcopy,
                                                  int V, float scale) {
   __shared__ float rm[16], rs[16];
   const int r = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -216,7 +220,7 @@ __global__ void __launch_bounds__(512) ce_kernel(T* __restrict__ z, const int32_
   float S = 0.f;
   for (int w = 0; w < 16; ++w) S += rs[w] * __expf(rm[w] - M);
   const float lse = M + logf(S);
-  const int y = tgt[r];
+  const int y = tok[(int64_t)(r % b) * (seq_len + 1) + c + r / b + 1];  // target = next token (A-8)
   if (tid == 0) loss_rows[r] = lse - to_f<T>(zr[y]);
   __syncthreads();  // every thread has read z[y] (via tid 0) before it is overwritten
   for (int i = tid; i < V; i += 512) {
@@ -321,23 +325,23 @@ cudaError_t layernorm_bwd(const float* dy, const float* x, const float* mean, co
   ln_bwd_reduce_kernel<<<(2 * H + 255) / 256, 256, 0, st>>>(ws, grid, dgam, dbet, H);
   return cudaGetLastError();
 }
-cudaError_t embed_fwd(const int32_t* tok, const float* wte, const float* wpe, float* h, int c, int l, int H, int V,
-                      cudaStream_t st) {
+cudaError_t embed_fwd(const int32_t* tok, const float* wte, const float* wpe, float* h, int c, int l, int b, int s,
+                      int H, int V, cudaStream_t st) {
   if (l == 0) return cudaSuccess;
-  embed_fwd_kernel<<<l, 256, 0, st>>>(tok, wte, wpe, h, c, H, V);
+  embed_fwd_kernel<<<l * b, 256, 0, st>>>(tok, wte, wpe, h, c, b, s, H, V);
   return cudaGetLastError();
 }
-cudaError_t embed_bwd(const int32_t* tok, const float* dh, float* gwte, float* gwpe, int c, int l, int H,
-                      cudaStream_t st) {
+cudaError_t embed_bwd(const int32_t* tok, const float* dh, float* gwte, float* gwpe, int c, int l, int b, int s,
+                      int H, cudaStream_t st) {
   if (l == 0) return cudaSuccess;
-  embed_bwd_kernel<<<l, 256, 0, st>>>(tok, dh, gwte, gwpe, c, H);
+  embed_bwd_kernel<<<l * b, 256, 0, st>>>(tok, dh, gwte, gwpe, c, b, s, H);
   return cudaGetLastError();
 }
 template <typename T>
-cudaError_t ce_fwd_bwd(T* logits, const int32_t* targets, float* loss_rows, float* logits_copy, int rows, int V,
-                       float scale, cudaStream_t st) {
+cudaError_t ce_fwd_bwd(T* logits, const int32_t* tok, int c, int b, int s, float* loss_rows, float* logits_copy,
+                       int rows, int V, float scale, cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
-  ce_kernel<T><<<rows, 512, 0, st>>>(logits, targets, loss_rows, logits_copy, V, scale);
+  ce_kernel<T><<<rows, 512, 0, st>>>(logits, tok, c, b, s, loss_rows, logits_copy, V, scale);
   return cudaGetLastError();
 }
 cudaError_t sum_rows(const float* x, int n, float* out, cudaStream_t st) {
@@ -370,7 +374,8 @@ cudaError_t colsum_accum(const T* src, int64_t ld, float* out, int rows, int N, 
                                         cudaStream_t);                                                      \
   template cudaError_t layernorm_bwd<T>(const float*, const float*, const float*, const float*, const float*,   \
                                         const float*, float*, T*, float*, float*, float*, int, int, cudaStream_t); \
-  template cudaError_t ce_fwd_bwd<T>(T*, const int32_t*, float*, float*, int, int, float, cudaStream_t);   \
+  template cudaError_t ce_fwd_bwd<T>(T*, const int32_t*, int, int, int, float*, float*, int, int, float,    \
+                                     cudaStream_t);                                                        \
   template cudaError_t convert_f32<T>(const float*, T*, int64_t, cudaStream_t);                            \
   template cudaError_t transpose_convert<T>(const float*, T*, int, int, cudaStream_t);                     \
   template cudaError_t colsum_accum<T>(const T*, int64_t, float*, int, int, cudaStream_t);

@@ -167,7 +167,7 @@ struct EngineBase {
   virtual tp_status step(const tp_slicing* sl, const int32_t* tokens, bool host_tokens, int batch, float* loss) = 0;
   virtual tp_status grads(float* host, size_t n) = 0;
   virtual tp_status logits(float* host, size_t n) = 0;
-  virtual tp_status profile(int g, int reps, int64_t* ticks, double* fit) = 0;
+  virtual tp_status profile(int g, int b, int reps, int64_t* ticks, double* fit) = 0;
   virtual size_t param_count() const = 0;
   Instr instr;
   cudaStream_t stream = nullptr;
@@ -215,7 +215,7 @@ class Engine final : public EngineBase {
   int32_t* d_tokens = nullptr;
   float* d_loss = nullptr;
   float* h_loss = nullptr;  // pinned
-  int last_batch = 0;
+  int last_batch = 0, last_b = 1;
   // NCCL (multi-rank)
   ncclComm_t base = nullptr, commF[2] = {nullptr, nullptr}, commB[2] = {nullptr, nullptr};
   cudaStream_t s_recv_f = nullptr, s_send_f = nullptr, s_recv_b = nullptr, s_send_b = nullptr;
@@ -344,10 +344,11 @@ class Engine final : public EngineBase {
     (void)first;
     TRY(vec(S.dQKV, nl, B * s * 3 * H)); TRY(vec(S.dhmid_b, nl, B * s * H));
     TRY(vec(S.dU, nl, B * s * 4 * H)); TRY(vec(S.dhout_b, nl, B * s * H));
-    TRY(vec(S.dk_acc, nl, s * H)); TRY(vec(S.dv_acc, nl, s * H));
-    TRY(alloc(&S.gA, s * H)); TRY(alloc(&S.gB, s * H)); TRY(alloc(&S.gm, s * H)); TRY(alloc(&S.dA, s * H));
-    TRY(alloc(&S.Dvec, a * s)); TRY(alloc(&S.dO, s * H));
-    TRY(alloc(&S.lnws, 2 * H * ((s + 3) / 4)));
+    // per job: up to b = max_batch sequences of one slice
+    TRY(vec(S.dk_acc, nl, B * s * H)); TRY(vec(S.dv_acc, nl, B * s * H));
+    TRY(alloc(&S.gA, B * s * H)); TRY(alloc(&S.gB, B * s * H)); TRY(alloc(&S.gm, B * s * H)); TRY(alloc(&S.dA, B * s * H));
+    TRY(alloc(&S.Dvec, a * s)); TRY(alloc(&S.dO, B * s * H));
+    TRY(alloc(&S.lnws, 2 * H * ((B * s + 3) / 4)));
     TRY(alloc(&S.dqacc, s * H));
     return TP_OK;
   }
@@ -433,13 +434,20 @@ class Engine final : public EngineBase {
   }
 
   // ------------------------------------------------------------ forward of one job on one stage
-  tp_status fwd(Stage<T>& S, int d, int c, int l, int batch) {
+  // Internal row order of every [B][s] activation buffer for a step with batch slice b:
+  // row((group g, position p, member j)) = (g*s + p)*b + j, so the job (g, slice [c, c+l)) is the
+  // contiguous row range [(g*s + c)*b, (g*s + c + l)*b) of T = b*l tokens (PAPER.md:362-364 joint
+  // batch x token slicing; b = 1 is the plain token slicing of §3.2).
+  tp_status fwd(Stage<T>& S, int g, int c, int l, int b, int batch) {
     const int H = m.H, s = m.s, a = m.a, dh = m.d, V = m.V;
-    const size_t row = (size_t)d * s + c;  // first row of this job in [B][s] buffers
+    const int Tn = b * l;
+    const size_t row = ((size_t)g * s + c) * b;  // first row of this job
+    const size_t seq0 = (size_t)g * b;          // first sequence of this job
+    const int32_t* tok0 = d_tokens + seq0 * (s + 1);
     const double ebytes = sizeof(T);
     if (S.k == 0) {
-      TRY(launch(KC_EMBED, 0, 8.0 * l * H, [&] {
-        return embed_fwd(d_tokens + (size_t)d * (s + 1), S.psmall + S.L.s_wte, S.psmall + S.L.s_wpe, S.hs[0] + row * H, c, l, H, V, stream);
+      TRY(launch(KC_EMBED, 0, 8.0 * Tn * H, [&] {
+        return embed_fwd(tok0, S.psmall + S.L.s_wte, S.psmall + S.L.s_wpe, S.hs[0] + row * H, c, l, b, s, H, V, stream);
       }));
     }
     for (int j = 0; j < S.nl; ++j) {
@@ -447,70 +455,84 @@ class Engine final : public EngineBase {
       const float* P = S.psmall;
       float* x = S.hs[j] + row * H;
       float* st1 = S.st1[j];
-      TRY(launch(KC_LN, 0, (4.0 + ebytes) * l * H, [&] {
-        return layernorm_fwd<T>(x, P + f.ln1_g, P + f.ln1_b, S.A1[j] + row * H, st1 + row, st1 + (size_t)batch * s + row, l, H, stream);
+      TRY(launch(KC_LN, 0, (4.0 + ebytes) * Tn * H, [&] {
+        return layernorm_fwd<T>(x, P + f.ln1_g, P + f.ln1_b, S.A1[j] + row * H, st1 + row, st1 + (size_t)batch * s + row, Tn, H, stream);
       }));
       Epi eq; eq.kind = EPI_QKV; eq.bias = P + f.b_qkv;
-      eq.q = S.Q[j] + (size_t)d * s * H; eq.k = S.Kc[j] + (size_t)d * s * H; eq.v = S.Vc[j] + (size_t)d * s * H;
-      eq.s_len = s; eq.head_dim = dh; eq.hidden = H; eq.row0 = c;
-      TRY(gemm(KC_GEMM_FWD, gd(l, 3 * H, H, S.A1[j] + row * H, H, false, S.wqkv_t[j], H, false), eq));
+      eq.q = S.Q[j] + seq0 * s * H; eq.k = S.Kc[j] + seq0 * s * H; eq.v = S.Vc[j] + seq0 * s * H;
+      eq.s_len = s; eq.head_dim = dh; eq.hidden = H; eq.row0 = c; eq.bs = b;
+      TRY(gemm(KC_GEMM_FWD, gd(Tn, 3 * H, H, S.A1[j] + row * H, H, false, S.wqkv_t[j], H, false), eq));
       T* o = S.O[j] + row * H;
-      float* lse = S.LSE[j] + (size_t)d * a * s;
-      const double attn_flops = 4.0 * H * ((double)l * c + 0.5 * l * (l + 1.0));
-      TRY(launch(KC_ATTN_FWD, attn_flops, ebytes * (2.0 * H * (c + l) + 2.0 * H * l), [&] {
-        const T *q = S.Q[j] + (size_t)d * s * H, *kk = S.Kc[j] + (size_t)d * s * H, *vv = S.Vc[j] + (size_t)d * s * H;
-        if constexpr (std::is_same<T, bf16>::value)
-          if (!force_simt) {
-            if (attn_sm100_supported(dh) && !legacy_attn) return attn_fwd_sm100(q, kk, vv, o, H, lse, a, s, dh, c, l, stream);
-            return attn_fwd_tc(q, kk, vv, o, H, lse, a, s, dh, c, l, stream);
+      const double attn_flops = 4.0 * H * b * ((double)l * c + 0.5 * l * (l + 1.0));
+      TRY(launch(KC_ATTN_FWD, attn_flops, ebytes * b * (2.0 * H * (c + l) + 2.0 * H * l), [&] {
+        for (int jj = 0; jj < b; ++jj) {
+          const size_t sq = seq0 + jj;
+          const T *q = S.Q[j] + sq * s * H, *kk = S.Kc[j] + sq * s * H, *vv = S.Vc[j] + sq * s * H;
+          T* oj = o + (size_t)jj * H;
+          float* lse = S.LSE[j] + sq * a * s;
+          cudaError_t e;
+          if constexpr (std::is_same<T, bf16>::value) {
+            if (!force_simt && attn_sm100_supported(dh) && !legacy_attn)
+              e = attn_fwd_sm100(q, kk, vv, oj, (int64_t)b * H, lse, a, s, dh, c, l, stream);
+            else if (!force_simt)
+              e = attn_fwd_tc(q, kk, vv, oj, (int64_t)b * H, lse, a, s, dh, c, l, stream);
+            else
+              e = attn_fwd_simt<T>(q, kk, vv, oj, (int64_t)b * H, lse, a, s, dh, c, l, stream);
+          } else {
+            e = attn_fwd_simt<T>(q, kk, vv, oj, (int64_t)b * H, lse, a, s, dh, c, l, stream);
           }
-        return attn_fwd_simt<T>(q, kk, vv, o, H, lse, a, s, dh, c, l, stream);
+          if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
       }));
       Epi er; er.kind = EPI_RESID; er.bias = P + f.b_o; er.out = S.hmid[j] + row * H; er.ldo = H; er.resid = x; er.ldr = H;
-      TRY(gemm(KC_GEMM_FWD, gd(l, H, H, o, H, false, S.wo_t[j], H, false), er));
+      TRY(gemm(KC_GEMM_FWD, gd(Tn, H, H, o, H, false, S.wo_t[j], H, false), er));
       float* st2 = S.st2[j];
-      TRY(launch(KC_LN, 0, (4.0 + ebytes) * l * H, [&] {
-        return layernorm_fwd<T>(S.hmid[j] + row * H, P + f.ln2_g, P + f.ln2_b, S.A2[j] + row * H, st2 + row, st2 + (size_t)batch * s + row, l, H, stream);
+      TRY(launch(KC_LN, 0, (4.0 + ebytes) * Tn * H, [&] {
+        return layernorm_fwd<T>(S.hmid[j] + row * H, P + f.ln2_g, P + f.ln2_b, S.A2[j] + row * H, st2 + row, st2 + (size_t)batch * s + row, Tn, H, stream);
       }));
       Epi eg; eg.kind = EPI_GELU; eg.bias = P + f.b_1; eg.out = S.U[j] + row * 4 * H; eg.ldo = 4 * H; eg.out2 = S.G[j] + row * 4 * H; eg.ldo2 = 4 * H;
-      TRY(gemm(KC_GEMM_FWD, gd(l, 4 * H, H, S.A2[j] + row * H, H, false, S.w1_t[j], H, false), eg));
+      TRY(gemm(KC_GEMM_FWD, gd(Tn, 4 * H, H, S.A2[j] + row * H, H, false, S.w1_t[j], H, false), eg));
       Epi e2; e2.kind = EPI_RESID; e2.bias = P + f.b_2; e2.out = S.hs[j + 1] + row * H; e2.ldo = H; e2.resid = S.hmid[j] + row * H; e2.ldr = H;
-      TRY(gemm(KC_GEMM_FWD, gd(l, H, 4 * H, S.G[j] + row * 4 * H, 4 * H, false, S.w2_t[j], 4 * H, false), e2));
+      TRY(gemm(KC_GEMM_FWD, gd(Tn, H, 4 * H, S.G[j] + row * 4 * H, 4 * H, false, S.w2_t[j], 4 * H, false), e2));
     }
     if (S.k == m.K - 1) {
       const float* P = S.psmall;
       float* x = S.hs[S.nl] + row * H;
-      TRY(launch(KC_LN, 0, (4.0 + ebytes) * l * H, [&] {
-        return layernorm_fwd<T>(x, P + S.L.s_lnf_g, P + S.L.s_lnf_b, S.Af + row * H, S.stf + row, S.stf + (size_t)batch * s + row, l, H, stream);
+      TRY(launch(KC_LN, 0, (4.0 + ebytes) * Tn * H, [&] {
+        return layernorm_fwd<T>(x, P + S.L.s_lnf_g, P + S.L.s_lnf_b, S.Af + row * H, S.stf + row, S.stf + (size_t)batch * s + row, Tn, H, stream);
       }));
       Epi ez; ez.kind = EPI_STORE; ez.out = S.Z + row * V; ez.ldo = V;
-      TRY(gemm(KC_GEMM_FWD, gd(l, V, H, S.Af + row * H, H, false, S.wout_t, H, false), ez));
+      TRY(gemm(KC_GEMM_FWD, gd(Tn, V, H, S.Af + row * H, H, false, S.wout_t, H, false), ez));
       const float scale = 1.0f / (float)((double)batch * s);
       float* keep = S.logits_keep ? S.logits_keep + row * V : nullptr;
-      TRY(launch(KC_CE, 0, 2.0 * ebytes * l * V, [&] {
-        return ce_fwd_bwd<T>(S.Z + row * V, d_tokens + (size_t)d * (s + 1) + c + 1, S.loss_rows + row, keep, l, V, scale, stream);
+      TRY(launch(KC_CE, 0, 2.0 * ebytes * Tn * V, [&] {
+        return ce_fwd_bwd<T>(S.Z + row * V, tok0, c, b, s, S.loss_rows + row, keep, Tn, V, scale, stream);
       }));
     }
     return TP_OK;
   }
 
   // ------------------------------------------------------------ backward of one job on one stage
-  tp_status bwd(Stage<T>& S, int d, int c, int l, int batch, bool first_bwd_slice) {
+  tp_status bwd(Stage<T>& S, int g, int c, int l, int b, int batch, bool first_bwd_slice) {
     const int H = m.H, s = m.s, a = m.a, dh = m.d, V = m.V;
-    const size_t row = (size_t)d * s + c;
+    const int Tn = b * l;
+    const size_t row = ((size_t)g * s + c) * b;
+    const size_t seq0 = (size_t)g * b;
+    const int32_t* tok0 = d_tokens + seq0 * (s + 1);
     const double ebytes = sizeof(T);
-    float* g = S.grad_out + row * H;  // fp32 gradient at the stage output, rows of this job
+    float* gr = S.grad_out + row * H;  // fp32 gradient at the stage output, rows of this job
     if (S.k == m.K - 1) {
       const float* P = S.psmall;
       Epi e; e.kind = EPI_STORE; e.out = S.dA; e.ldo = H; e.out_f32 = 1;
-      TRY(gemm(KC_GEMM_DX, gd(l, H, V, S.Z + row * V, V, false, S.wout_io, V, false), e));
-      TRY(launch(KC_LN, 0, (12.0 + ebytes) * l * H, [&] {
-        return layernorm_bwd<T>(S.dA, S.hs[S.nl] + row * H, S.stf + row, S.stf + (size_t)batch * s + row, P + S.L.s_lnf_g, nullptr, g,
-                                S.dhout_b[S.nl - 1] + row * H, S.gflat + S.L.lnf_g, S.gflat + S.L.lnf_b, S.lnws, l, H, stream);
+      TRY(gemm(KC_GEMM_DX, gd(Tn, H, V, S.Z + row * V, V, false, S.wout_io, V, false), e));
+      TRY(launch(KC_LN, 0, (12.0 + ebytes) * Tn * H, [&] {
+        return layernorm_bwd<T>(S.dA, S.hs[S.nl] + row * H, S.stf + row, S.stf + (size_t)batch * s + row, P + S.L.s_lnf_g, nullptr, gr,
+                                S.dhout_b[S.nl - 1] + row * H, S.gflat + S.L.lnf_g, S.gflat + S.L.lnf_b, S.lnws, Tn, H, stream);
       }));
     } else {
-      TRY(launch(KC_MISC, 0, (4.0 + ebytes) * l * H, [&] {
-        return convert_f32<T>(g, S.dhout_b[S.nl - 1] + row * H, (int64_t)l * H, stream);
+      TRY(launch(KC_MISC, 0, (4.0 + ebytes) * Tn * H, [&] {
+        return convert_f32<T>(gr, S.dhout_b[S.nl - 1] + row * H, (int64_t)Tn * H, stream);
       }));
     }
     for (int j = S.nl - 1; j >= 0; --j) {
@@ -520,50 +542,61 @@ class Engine final : public EngineBase {
       float* GR = S.gflat;
       // FFN: dU = (dh W_2^T) * gelu'(U)
       Epi e1; e1.kind = EPI_DGELU; e1.out = S.dU[j] + row * 4 * H; e1.ldo = 4 * H; e1.aux = S.U[j] + row * 4 * H; e1.ld_aux = 4 * H;
-      TRY(gemm(KC_GEMM_DX, gd(l, 4 * H, H, S.dhout_b[j] + row * H, H, false, S.w2_io[j], H, false), e1));
+      TRY(gemm(KC_GEMM_DX, gd(Tn, 4 * H, H, S.dhout_b[j] + row * H, H, false, S.w2_io[j], H, false), e1));
       Epi e2; e2.kind = EPI_STORE; e2.out = S.dA; e2.ldo = H; e2.out_f32 = 1;
-      TRY(gemm(KC_GEMM_DX, gd(l, H, 4 * H, S.dU[j] + row * 4 * H, 4 * H, false, S.w1_io[j], 4 * H, false), e2));
+      TRY(gemm(KC_GEMM_DX, gd(Tn, H, 4 * H, S.dU[j] + row * 4 * H, 4 * H, false, S.w1_io[j], 4 * H, false), e2));
       float* st2 = S.st2[j];
-      TRY(launch(KC_LN, 0, (16.0 + ebytes) * l * H, [&] {
-        return layernorm_bwd<T>(S.dA, S.hmid[j] + row * H, st2 + row, st2 + (size_t)batch * s + row, P + fs.ln2_g, g, S.gm,
-                                S.dhmid_b[j] + row * H, GR + f.ln2_g, GR + f.ln2_b, S.lnws, l, H, stream);
+      TRY(launch(KC_LN, 0, (16.0 + ebytes) * Tn * H, [&] {
+        return layernorm_bwd<T>(S.dA, S.hmid[j] + row * H, st2 + row, st2 + (size_t)batch * s + row, P + fs.ln2_g, gr, S.gm,
+                                S.dhmid_b[j] + row * H, GR + f.ln2_g, GR + f.ln2_b, S.lnws, Tn, H, stream);
       }));
       // attention: dO = dh_mid W_o^T, then slice-vs-prefix attention backward with dK/dV push
       Epi e3; e3.kind = EPI_STORE; e3.out = S.dO; e3.ldo = H;
-      TRY(gemm(KC_GEMM_DX, gd(l, H, H, S.dhmid_b[j] + row * H, H, false, S.wo_io[j], H, false), e3));
-      const double attn_flops = 8.0 * H * ((double)l * c + 0.5 * l * (l + 1.0));
+      TRY(gemm(KC_GEMM_DX, gd(Tn, H, H, S.dhmid_b[j] + row * H, H, false, S.wo_io[j], H, false), e3));
+      const double attn_flops = 8.0 * H * b * ((double)l * c + 0.5 * l * (l + 1.0));
       T* dq = S.dQKV[j] + row * 3 * H;
-      TRY(launch(KC_ATTN_BWD, attn_flops, ebytes * 4.0 * H * (c + l) + 16.0 * H * (c + l), [&] {
-        const T *q = S.Q[j] + (size_t)d * s * H, *kk = S.Kc[j] + (size_t)d * s * H, *vv = S.Vc[j] + (size_t)d * s * H;
-        const int accum = first_bwd_slice ? 0 : 1;
-        if constexpr (std::is_same<T, bf16>::value)
-          if (!force_simt && attn_sm100_supported(dh) && !legacy_attn)
-            return attn_bwd_sm100(S.dO, H, S.O[j] + row * H, H, q, kk, vv, S.LSE[j] + (size_t)d * a * s, S.Dvec, S.dqacc,
-                                  dq, 3 * H, S.dk_acc[j], S.dv_acc[j], a, s, dh, c, l, accum, stream);
-        if constexpr (std::is_same<T, bf16>::value)
-          if (!force_simt)
-            return attn_bwd_tc(S.dO, H, S.O[j] + row * H, H, q, kk, vv, S.LSE[j] + (size_t)d * a * s, S.Dvec, dq, 3 * H,
-                               S.dk_acc[j], S.dv_acc[j], a, s, dh, c, l, accum, stream);
-        return attn_bwd_simt<T>(S.dO, H, S.O[j] + row * H, H, q, kk, vv, S.LSE[j] + (size_t)d * a * s, S.Dvec, dq, 3 * H,
-                                S.dk_acc[j], S.dv_acc[j], a, s, dh, c, l, accum, stream);
-      }));
-      TRY(launch(KC_MISC, 0, (8.0 + 2 * ebytes) * l * H, [&] {
-        return attn_dkv_finalize<T>(S.dk_acc[j], S.dv_acc[j], dq, 3 * H, a, s, dh, c, l, stream);
+      const int accum = first_bwd_slice ? 0 : 1;
+      TRY(launch(KC_ATTN_BWD, attn_flops, b * (ebytes * 4.0 * H * (c + l) + 16.0 * H * (c + l)), [&] {
+        for (int jj = 0; jj < b; ++jj) {
+          const size_t sq = seq0 + jj;
+          const T *q = S.Q[j] + sq * s * H, *kk = S.Kc[j] + sq * s * H, *vv = S.Vc[j] + sq * s * H;
+          const T* dOj = S.dO + (size_t)jj * H;
+          const T* Oj = S.O[j] + (row + jj) * H;
+          const float* lse = S.LSE[j] + sq * a * s;
+          T* dqj = dq + (size_t)jj * 3 * H;
+          float* dka = S.dk_acc[j] + (size_t)jj * s * H;
+          float* dva = S.dv_acc[j] + (size_t)jj * s * H;
+          const int64_t ldb = (int64_t)b * H, ldq = (int64_t)b * 3 * H;
+          cudaError_t e;
+          if constexpr (std::is_same<T, bf16>::value) {
+            if (!force_simt && attn_sm100_supported(dh) && !legacy_attn)
+              e = attn_bwd_sm100(dOj, ldb, Oj, ldb, q, kk, vv, lse, S.Dvec, S.dqacc, dqj, ldq, dka, dva, a, s, dh, c, l, accum, stream);
+            else if (!force_simt)
+              e = attn_bwd_tc(dOj, ldb, Oj, ldb, q, kk, vv, lse, S.Dvec, dqj, ldq, dka, dva, a, s, dh, c, l, accum, stream);
+            else
+              e = attn_bwd_simt<T>(dOj, ldb, Oj, ldb, q, kk, vv, lse, S.Dvec, dqj, ldq, dka, dva, a, s, dh, c, l, accum, stream);
+          } else {
+            e = attn_bwd_simt<T>(dOj, ldb, Oj, ldb, q, kk, vv, lse, S.Dvec, dqj, ldq, dka, dva, a, s, dh, c, l, accum, stream);
+          }
+          if (e == cudaSuccess) e = attn_dkv_finalize<T>(dka, dva, dqj, ldq, a, s, dh, c, l, stream);
+          if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
       }));
       Epi e4; e4.kind = EPI_STORE; e4.out = S.dA; e4.ldo = H; e4.out_f32 = 1;
-      TRY(gemm(KC_GEMM_DX, gd(l, H, 3 * H, dq, 3 * H, false, S.wqkv_io[j], 3 * H, false), e4));
-      float* gnext = j == 0 ? S.grad_in + row * H : (g == S.gA ? S.gB : S.gA);
+      TRY(gemm(KC_GEMM_DX, gd(Tn, H, 3 * H, dq, 3 * H, false, S.wqkv_io[j], 3 * H, false), e4));
+      float* gnext = j == 0 ? S.grad_in + row * H : (gr == S.gA ? S.gB : S.gA);
       T* copy = j == 0 ? nullptr : S.dhout_b[j - 1] + row * H;
       float* st1 = S.st1[j];
-      TRY(launch(KC_LN, 0, (16.0 + ebytes) * l * H, [&] {
+      TRY(launch(KC_LN, 0, (16.0 + ebytes) * Tn * H, [&] {
         return layernorm_bwd<T>(S.dA, S.hs[j] + row * H, st1 + row, st1 + (size_t)batch * s + row, P + fs.ln1_g, S.gm, gnext, copy,
-                                GR + f.ln1_g, GR + f.ln1_b, S.lnws, l, H, stream);
+                                GR + f.ln1_g, GR + f.ln1_b, S.lnws, Tn, H, stream);
       }));
-      g = gnext;
+      gr = gnext;
     }
     if (S.k == 0) {
-      TRY(launch(KC_EMBED, 0, 12.0 * l * H, [&] {
-        return embed_bwd(d_tokens + (size_t)d * (s + 1), S.grad_in + row * H, S.gflat + S.L.wte, S.gflat + S.L.wpe, c, l, H, stream);
+      TRY(launch(KC_EMBED, 0, 12.0 * Tn * H, [&] {
+        return embed_bwd(tok0, S.grad_in + row * H, S.gflat + S.L.wte, S.gflat + S.L.wpe, c, l, b, s, H, stream);
       }));
     }
     return TP_OK;
@@ -640,7 +673,9 @@ class Engine final : public EngineBase {
   tp_status step(const tp_slicing* sl, const int32_t* tokens, bool host_tokens, int batch, float* loss_out) override {
     if (!sl || !sl->lengths) return fail(TP_EINVAL, "tp_step: null slicing");
     if (batch < 1 || batch > max_batch) return fail(TP_EINVAL, "tp_step: batch %d not in [1, max_batch=%d]", batch, max_batch);
-    if (sl->batch_slice != 1) return fail(TP_EINVAL, "tp_step: batch_slice %d unsupported (this build runs b = 1)", sl->batch_slice);
+    const int b = sl->batch_slice;
+    if (b < 1 || batch % b != 0)
+      return fail(TP_EINVAL, "tp_step: batch_slice %d must be >= 1 and divide batch %d", b, batch);
     const int M = sl->n_slices;
     if (M < 1 || M > m.s) return fail(TP_EINVAL, "tp_step: n_slices %d", M);
     std::vector<int> off(M + 1, 0);
@@ -654,28 +689,33 @@ class Engine final : public EngineBase {
     instr.launches = 0;
     ev_next = 0;
     last_batch = batch;
+    last_b = b;
+    const int D = batch / b;
     const size_t ntok = (size_t)batch * (m.s + 1);
     CU(cudaMemcpyAsync(d_tokens, tokens, ntok * sizeof(int32_t), host_tokens ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, stream));
     for (auto& S : stages) CU(cudaMemsetAsync(S.gflat, 0, S.L.total * sizeof(float), stream));
     const bool multi = world > 1;
-    // forward: F(d, i) for d = 0..B-1, i = 1..M (stage order inside a job in loopback)
-    for (int d = 0; d < batch; ++d)
+    // forward: F(g, i) for groups g = 0..D-1 of b sequences, slices i = 1..M (stage order inside a
+    // job in loopback); a job is b*l_i tokens, contiguous rows (see fwd())
+    for (int d = 0; d < D; ++d)
       for (int i = 0; i < M; ++i)
         for (auto& S : stages) {
-          const size_t row = (size_t)d * m.s + off[i];
-          if (multi && S.k > 0) TRY(recv_fwd(S, row, sl->lengths[i]));
-          TRY(fwd(S, d, off[i], sl->lengths[i], batch));
-          if (multi && S.k < m.K - 1) TRY(send_fwd(S, row, sl->lengths[i]));
+          const size_t row = ((size_t)d * m.s + off[i]) * b;
+          const int Tn = b * sl->lengths[i];
+          if (multi && S.k > 0) TRY(recv_fwd(S, row, Tn));
+          TRY(fwd(S, d, off[i], sl->lengths[i], b, batch));
+          if (multi && S.k < m.K - 1) TRY(send_fwd(S, row, Tn));
         }
-    // backward: exact reverse order; deferred dW of sequence d after its slice 1
-    for (int d = batch - 1; d >= 0; --d) {
+    // backward: exact reverse order (GPipe order, A-21)
+    for (int d = D - 1; d >= 0; --d) {
       for (int i = M - 1; i >= 0; --i)
         for (int si = (int)stages.size() - 1; si >= 0; --si) {
           Stage<T>& S = stages[si];
-          const size_t row = (size_t)d * m.s + off[i];
-          if (multi && S.k < m.K - 1) TRY(recv_bwd(S, row, sl->lengths[i]));
-          TRY(bwd(S, d, off[i], sl->lengths[i], batch, i == M - 1));
-          if (multi && S.k > 0) TRY(send_bwd(S, row, sl->lengths[i]));
+          const size_t row = ((size_t)d * m.s + off[i]) * b;
+          const int Tn = b * sl->lengths[i];
+          if (multi && S.k < m.K - 1) TRY(recv_bwd(S, row, Tn));
+          TRY(bwd(S, d, off[i], sl->lengths[i], b, batch, i == M - 1));
+          if (multi && S.k > 0) TRY(send_bwd(S, row, Tn));
         }
     }
     for (auto& S : stages) TRY(wgrad(S, batch));
@@ -719,19 +759,27 @@ class Engine final : public EngineBase {
     if (!last || !last->logits_keep) return fail(TP_ESTATE, "tp_get_logits: needs TP_FLAG_KEEP_LOGITS and the last stage");
     const size_t need = (size_t)last_batch * m.s * m.V;
     if (n != need) return fail(TP_EINVAL, "tp_get_logits: n=%zu, expected %zu", n, need);
-    CU(cudaMemcpy(host, last->logits_keep, need * sizeof(float), cudaMemcpyDeviceToHost));
+    std::vector<float> tmp(need);
+    CU(cudaMemcpy(tmp.data(), last->logits_keep, need * sizeof(float), cudaMemcpyDeviceToHost));
+    // internal row (g*s + p)*b + j  ->  [sequence g*b + j][position p]
+    const size_t b = last_b, s = m.s, V = m.V;
+    for (size_t r = 0; r < (size_t)last_batch * s; ++r) {
+      const size_t g = r / (s * b), rem = r % (s * b), p = rem / b, j = rem % b;
+      std::memcpy(host + ((g * b + j) * s + p) * V, tmp.data() + r * V, V * sizeof(float));
+    }
     return TP_OK;
   }
-  tp_status profile(int g, int reps, int64_t* ticks, double* fit) override;
+  tp_status profile(int g, int b, int reps, int64_t* ticks, double* fit) override;
 };
 
 // ---------------------------------------------------------------- tp_profile
 // measure t(l, 0) for every l, fit t_ctx(l, c) = a0 + a1 l + a2 c + a3 l c on a
 // subset of (l, c) by least squares, fill the table with t(l, 0) + t_ctx(l, c).
 template <typename T>
-tp_status Engine<T>::profile(int g, int reps, int64_t* ticks, double* fit) {
+tp_status Engine<T>::profile(int g, int bsl, int reps, int64_t* ticks, double* fit) {
   if (g < 1 || m.s % g != 0) return fail(TP_EINVAL, "tp_profile: granularity %d must divide seq_len %d", g, m.s);
   if (reps < 1) return fail(TP_EINVAL, "tp_profile: reps must be >= 1");
+  if (bsl < 1 || bsl > max_batch) return fail(TP_EINVAL, "tp_profile: batch_slice %d not in [1, max_batch]", bsl);
   if (!ticks) return fail(TP_EINVAL, "tp_profile: null ticks_out");
   const int n = m.s / g;
   Stage<T>& S = stages[0];
@@ -739,13 +787,13 @@ tp_status Engine<T>::profile(int g, int reps, int64_t* ticks, double* fit) {
   CU(cudaEventCreate(&e0));
   CU(cudaEventCreate(&e1));
   // tokens for sequence 0 (values do not affect dense cost)
-  CU(cudaMemsetAsync(d_tokens, 0, sizeof(int32_t) * (m.s + 1), stream));
+  CU(cudaMemsetAsync(d_tokens, 0, sizeof(int32_t) * (m.s + 1) * bsl, stream));
   auto time_job = [&](int l, int c, double* out_ns) -> tp_status {
     std::vector<float> v;
     for (int r = 0; r < reps + 2; ++r) {
       CU(cudaEventRecord(e0, stream));
-      TRY(fwd(S, 0, c, l, 1));
-      TRY(bwd(S, 0, c, l, 1, true));
+      TRY(fwd(S, 0, c, l, bsl, bsl));
+      TRY(bwd(S, 0, c, l, bsl, bsl, true));
       CU(cudaEventRecord(e1, stream));
       CU(cudaEventSynchronize(e1));
       float ms = 0;
@@ -908,9 +956,10 @@ extern "C" tp_status tp_get_logits(tp_ctx* ctx, float* host, size_t n) {
   TP_CHECK_ARG(ctx && host, "tp_get_logits: null argument");
   return ctx->eng->logits(host, n);
 }
-extern "C" tp_status tp_profile(tp_ctx* ctx, int32_t g, int32_t reps, int64_t* ticks, double* fit) {
+extern "C" tp_status tp_profile(tp_ctx* ctx, int32_t g, int32_t batch_slice, int32_t reps, int64_t* ticks,
+                                double* fit) {
   TP_CHECK_ARG(ctx, "tp_profile: null ctx");
-  return ctx->eng->profile(g, reps, ticks, fit);
+  return ctx->eng->profile(g, batch_slice, reps, ticks, fit);
 }
 extern "C" tp_status tp_get_stream(tp_ctx* ctx, void** out) {
   TP_CHECK_ARG(ctx && out, "tp_get_stream: null argument");

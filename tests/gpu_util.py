@@ -23,11 +23,11 @@ def oracle_run(cfg, B, seed, bf16):
     return params, tokens, ref
 
 
-def gpu_run(cfg, B, params, tokens, lengths, precision, flags=tp.TP_FLAG_KEEP_LOGITS):
+def gpu_run(cfg, B, params, tokens, lengths, precision, flags=tp.TP_FLAG_KEEP_LOGITS, batch_slice=1):
     ctx = tp.Context(cfg, precision=precision, max_batch=B, device=0, flags=flags)
     try:
         ctx.load_params(pack_all_stages(params, cfg))
-        loss = ctx.step(tp.Slicing(lengths), tokens)
+        loss = ctx.step(tp.Slicing(lengths, batch_slice), tokens)
         grads = unpack_all_stages(ctx.grads(), cfg)
         logits = ctx.logits(B) if flags & tp.TP_FLAG_KEEP_LOGITS else None
         launches = ctx.last_step_launches()

@@ -78,8 +78,22 @@ def test_parity_mid_13b_width():
     check(worst_errors(loss, logits, grads, ref), 2e-2)
 
 
+@pytest.mark.parametrize("precision,tol", [(tp.TP_BF16, 2e-2), (tp.TP_FP32, 1e-4)])
+@pytest.mark.parametrize("K,b,lengths", [(2, 2, [40, 24, 64]), (1, 4, [128]), (2, 2, [8] * 16), (4, 4, [56, 72])])
+def test_joint_batch_token_slicing(K, b, lengths, precision, tol):
+    """Jobs of b sequences x one token slice: same result as the unsliced oracle."""
+    cfg = SMALL.with_(n_stages=K)
+    B = 4
+    params, tokens, ref = oracle_run(cfg, B, 8, precision == tp.TP_BF16)
+    loss, logits, grads, _ = gpu_run(cfg, B, params, tokens, lengths, precision, batch_slice=b)
+    check(worst_errors(loss, logits, grads, ref), tol)
+
+
 def test_rejects_bad_slicing():
     params, tokens, _ = oracle_run(TINY, 1, 0, True)
     with pytest.raises(tp.TpError) as e:
         gpu_run(TINY, 1, params, tokens, [16, 8], tp.TP_BF16)
+    assert e.value.status == tp.TP_EINVAL
+    with pytest.raises(tp.TpError) as e:                        # batch_slice must divide batch
+        gpu_run(TINY, 1, params, tokens, [32], tp.TP_BF16, batch_slice=2)
     assert e.value.status == tp.TP_EINVAL
