@@ -67,7 +67,8 @@ __device__ __forceinline__ uint32_t swz(int row, int cc) {
 __global__ void __launch_bounds__(192, 1)
     attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                           const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ o, int64_t ldo,
-                          float* __restrict__ lse, int s, int c, int l, float scale_log2) {
+                          float* __restrict__ lse, int s, int c, int l, float scale_log2, int64_t o_sstride,
+                          int64_t lse_sstride) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + FwdSmem::BAR);
@@ -83,7 +84,9 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int head = blockIdx.y, r0 = blockIdx.x * AT;
+  const int head = blockIdx.y, r0 = blockIdx.x * AT, sq = blockIdx.z;  // sequence of the job
+  o += sq * o_sstride;
+  lse += sq * lse_sstride;
   const int qlast = c + min(l, r0 + AT) - 1;
   const int nkb = qlast / AT + 1;
 
@@ -107,18 +110,18 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
     mbar_expect_tx(qfull, TILE);
-    tma_load_3d(sm + FwdSmem::Q, &tmQ, 0, c + r0, head, qfull);
-    tma_load_3d(sm + FwdSmem::Q + HALF, &tmQ, 64, c + r0, head, qfull);
+    tma_load_4d(sm + FwdSmem::Q, &tmQ, 0, c + r0, head, sq, qfull);
+    tma_load_4d(sm + FwdSmem::Q + HALF, &tmQ, 64, c + r0, head, sq, qfull);
     for (int j = 0; j < nkb; ++j) {
       const int b = j & 1;
       if (j >= 2) mbar_wait(kvfree + b, ((j >> 1) - 1) & 1);
       uint8_t* kd = sm + (b ? FwdSmem::K1 : FwdSmem::K0);
       uint8_t* vd = sm + (b ? FwdSmem::V1 : FwdSmem::V0);
       mbar_expect_tx(kvfull + b, 2 * TILE);
-      tma_load_3d(kd, &tmK, 0, j * AT, head, kvfull + b);
-      tma_load_3d(kd + HALF, &tmK, 64, j * AT, head, kvfull + b);
-      tma_load_3d(vd, &tmV, 0, j * AT, head, kvfull + b);
-      tma_load_3d(vd + HALF, &tmV, 64, j * AT, head, kvfull + b);
+      tma_load_4d(kd, &tmK, 0, j * AT, head, sq, kvfull + b);
+      tma_load_4d(kd + HALF, &tmK, 64, j * AT, head, sq, kvfull + b);
+      tma_load_4d(vd, &tmV, 0, j * AT, head, sq, kvfull + b);
+      tma_load_4d(vd + HALF, &tmV, 64, j * AT, head, sq, kvfull + b);
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer
@@ -295,12 +298,12 @@ __global__ void __launch_bounds__(192, 1)
     attn_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                           const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                           const __grid_constant__ CUtensorMap tmdQ, const float* __restrict__ lse,
-                          const float* __restrict__ Dvec, float* __restrict__ dk_acc, float* __restrict__ dv_acc, int s, int c, int l,
+                          const float* __restrict__ Dvec, int64_t lse_sstride, int64_t dkv_sstride, float* __restrict__ dk_acc, float* __restrict__ dv_acc, int s, int c, int l,
                           float scale, float scale_log2, int accumulate, volatile int* dbg) {
   extern __shared__ uint8_t smem_raw[];
 #define DBG(role, v)                                                                    \
   do {                                                                                  \
-    if (dbg) { dbg[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + (role)] = (v); __threadfence_system(); } \
+    if (dbg) { dbg[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 8 + (role)] = (v); __threadfence_system(); } \
   } while (0)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + BwdSmem::BAR);
@@ -317,7 +320,11 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int head = blockIdx.y, key0 = blockIdx.x * AT;
+  const int head = blockIdx.y, key0 = blockIdx.x * AT, sq = blockIdx.z;  // sequence of the job
+  lse += sq * lse_sstride;
+  Dvec += (int64_t)sq * gridDim.y * l;
+  dk_acc += sq * dkv_sstride;
+  dv_acc += sq * dkv_sstride;
   const int nkeys = c + l;
   const int qt0 = max(0, key0 - c) / BQB, nqt = (l + BQB - 1) / BQB;
   const int ntile = nqt - qt0;  // >= 1 because key0 < c + l
@@ -344,10 +351,10 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer: K, V once; Q_i, dO_i double-buffered
     mbar_expect_tx(kvfull, 2 * TILE);
-    tma_load_3d(sm + BwdSmem::K, &tmK, 0, key0, head, kvfull);
-    tma_load_3d(sm + BwdSmem::K + HALF, &tmK, 64, key0, head, kvfull);
-    tma_load_3d(sm + BwdSmem::V, &tmV, 0, key0, head, kvfull);
-    tma_load_3d(sm + BwdSmem::V + HALF, &tmV, 64, key0, head, kvfull);
+    tma_load_4d(sm + BwdSmem::K, &tmK, 0, key0, head, sq, kvfull);
+    tma_load_4d(sm + BwdSmem::K + HALF, &tmK, 64, key0, head, sq, kvfull);
+    tma_load_4d(sm + BwdSmem::V, &tmV, 0, key0, head, sq, kvfull);
+    tma_load_4d(sm + BwdSmem::V + HALF, &tmV, 64, key0, head, sq, kvfull);
     for (int i = 0; i < ntile; ++i) {
       const int b = i & 1, qt = qt0 + i;
       DBG(0, 100 + i);
@@ -355,10 +362,10 @@ __global__ void __launch_bounds__(192, 1)
       uint8_t* qd = sm + (b ? BwdSmem::Q1 : BwdSmem::Q0);
       uint8_t* od = sm + (b ? BwdSmem::O1 : BwdSmem::O0);
       mbar_expect_tx(qfull + b, 2 * QT);
-      tma_load_3d(qd, &tmQ, 0, c + qt * BQB, head, qfull + b);
-      tma_load_3d(qd + QHALF, &tmQ, 64, c + qt * BQB, head, qfull + b);
-      tma_load_2d(od, &tmdO, head * AT, qt * BQB, qfull + b);
-      tma_load_2d(od + QHALF, &tmdO, head * AT + 64, qt * BQB, qfull + b);
+      tma_load_4d(qd, &tmQ, 0, c + qt * BQB, head, sq, qfull + b);
+      tma_load_4d(qd + QHALF, &tmQ, 64, c + qt * BQB, head, sq, qfull + b);
+      tma_load_3d(od, &tmdO, head * AT, qt * BQB, sq, qfull + b);
+      tma_load_3d(od + QHALF, &tmdO, head * AT + 64, qt * BQB, sq, qfull + b);
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer
@@ -438,7 +445,7 @@ __global__ void __launch_bounds__(192, 1)
       if (lane == 0) mbar_arrive(dqfree);
       fence_proxy_async();
       named_bar(1, 128);
-      if (threadIdx.x == 64) tma_reduce_add_2d(&tmdQ, dqs, head * AT, (qt0 + i) * BQB);
+      if (threadIdx.x == 64) tma_reduce_add_3d(&tmdQ, dqs, head * AT, (qt0 + i) * BQB, sq);
     };
     for (int i = 0; i < ntile; ++i) {
       const int qrow0 = (qt0 + i) * BQB;
@@ -538,8 +545,10 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 __global__ void dq_convert_kernel(const float* __restrict__ dq_acc, int64_t ld_acc, bf16* __restrict__ dq, int64_t ldq,
-                                  int H) {
-  const int r = blockIdx.x;
+                                  int H, int l, int64_t dq_sstride) {
+  const int r = blockIdx.x, sq = blockIdx.y;
+  dq_acc += (int64_t)sq * l * ld_acc;
+  dq += sq * dq_sstride;
   for (int i = threadIdx.x * 8; i < H; i += blockDim.x * 8) {
     float v[8];
     load8<float>(dq_acc + (int64_t)r * ld_acc + i, v);
@@ -552,8 +561,9 @@ __global__ void dq_convert_kernel(const float* __restrict__ dq_acc, int64_t ld_a
 bool attn_sm100_supported(int d) { return d == AT; }
 
 cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o, int64_t ldo, float* lse, int a, int s,
-                           int d, int c, int l, cudaStream_t st) {
-  if (l == 0) return cudaSuccess;
+                           int d, int c, int l, cudaStream_t st, int nseq, int64_t qkv_sstride, int64_t o_sstride,
+                           int64_t lse_sstride) {
+  if (l == 0 || nseq == 0) return cudaSuccess;
   if (d != AT) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
@@ -562,25 +572,26 @@ cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o,
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  // [a][s][d] viewed as 3-D {d, rows = c + l (prefix), a}: rows past the prefix are zero-filled
-  const uint64_t dims[3] = {(uint64_t)d, (uint64_t)(c + l), (uint64_t)a};
-  const uint64_t strides[2] = {(uint64_t)d * 2, (uint64_t)s * d * 2};
-  const uint32_t box[3] = {64, AT, 1};
+  // [seq][a][s][d] viewed as 4-D {d, rows = c + l (prefix), a, seq}: rows past the prefix zero-filled
+  const uint64_t dims[4] = {(uint64_t)d, (uint64_t)(c + l), (uint64_t)a, (uint64_t)nseq};
+  const uint64_t strides[3] = {(uint64_t)d * 2, (uint64_t)s * d * 2, (uint64_t)(nseq > 1 ? qkv_sstride : (int64_t)a * s * d) * 2};
+  const uint32_t box[4] = {64, AT, 1, 1};
   CUtensorMap mq, mk, mv;
-  if (!encode_bf16_map(&mq, q, 3, dims, strides, box) || !encode_bf16_map(&mk, k, 3, dims, strides, box) ||
-      !encode_bf16_map(&mv, v, 3, dims, strides, box))
+  if (!encode_bf16_map(&mq, q, 4, dims, strides, box) || !encode_bf16_map(&mk, k, 4, dims, strides, box) ||
+      !encode_bf16_map(&mv, v, 4, dims, strides, box))
     return cudaErrorInvalidValue;
-  dim3 grid((l + AT - 1) / AT, a);
-  attn_fwd_sm100_kernel<<<grid, 192, FwdSmem::BYTES, st>>>(mq, mk, mv, o, ldo, lse, s, c, l,
-                                                           rsqrtf((float)d) * LOG2E_F);
+  dim3 grid((l + AT - 1) / AT, a, nseq);
+  attn_fwd_sm100_kernel<<<grid, 192, FwdSmem::BYTES, st>>>(mq, mk, mv, o, ldo, lse, s, c, l, rsqrtf((float)d) * LOG2E_F,
+                                                           o_sstride, lse_sstride);
   return cudaGetLastError();
 }
 
 cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ldo, const bf16* q, const bf16* k,
                            const bf16* v, const float* lse, float* Dvec, float* dq_acc, bf16* dq, int64_t ldq,
                            float* dk_acc, float* dv_acc, int a, int s, int d, int c, int l, int accumulate,
-                           cudaStream_t st) {
-  if (l == 0) return cudaSuccess;
+                           cudaStream_t st, int nseq, int64_t qkv_sstride, int64_t o_sstride, int64_t lse_sstride,
+                           int64_t dq_sstride, int64_t dkv_sstride) {
+  if (l == 0 || nseq == 0) return cudaSuccess;
   if (d != AT) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
@@ -590,25 +601,28 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
     attr = true;
   }
   const int H = a * d;
-  cudaError_t e = cudaMemsetAsync(dq_acc, 0, sizeof(float) * (size_t)l * H, st);
-  if (e == cudaSuccess) e = attn_bwd_prep(dO, ld_do, o, ldo, Dvec, a, d, l, st);
+  cudaError_t e = cudaMemsetAsync(dq_acc, 0, sizeof(float) * (size_t)l * H * nseq, st);
+  if (e == cudaSuccess) e = attn_bwd_prep(dO, ld_do, o, ldo, Dvec, a, d, l, st, nseq, o_sstride);
   if (e != cudaSuccess) return e;
-  const uint64_t kdims[3] = {(uint64_t)d, (uint64_t)(c + l), (uint64_t)a};
-  const uint64_t kstr[2] = {(uint64_t)d * 2, (uint64_t)s * d * 2};
-  const uint32_t kbox[3] = {64, AT, 1}, qbox[3] = {64, BQB, 1};
-  const uint64_t odims[2] = {(uint64_t)H, (uint64_t)l};
-  const uint64_t ostr[1] = {(uint64_t)ld_do * 2};
-  const uint32_t obox[2] = {64, BQB};
-  const uint64_t qdims[2] = {(uint64_t)H, (uint64_t)l};
-  const uint64_t qstr[1] = {(uint64_t)H * 4};
-  const uint32_t qrbox[2] = {AT, BQB};
+  const int64_t qs = nseq > 1 ? qkv_sstride : (int64_t)a * s * d;
+  const uint64_t kdims[4] = {(uint64_t)d, (uint64_t)(c + l), (uint64_t)a, (uint64_t)nseq};
+  const uint64_t kstr[3] = {(uint64_t)d * 2, (uint64_t)s * d * 2, (uint64_t)qs * 2};
+  const uint32_t kbox[4] = {64, AT, 1, 1}, qbox[4] = {64, BQB, 1, 1};
+  // dO rows of sequence j: dO + j*o_sstride + r*ld_do
+  const uint64_t odims[3] = {(uint64_t)H, (uint64_t)l, (uint64_t)nseq};
+  const uint64_t ostr[2] = {(uint64_t)ld_do * 2, (uint64_t)(nseq > 1 ? o_sstride : (int64_t)l * ld_do) * 2};
+  const uint32_t obox[3] = {64, BQB, 1};
+  // dq_acc: [nseq][l][H] fp32
+  const uint64_t qdims[3] = {(uint64_t)H, (uint64_t)l, (uint64_t)nseq};
+  const uint64_t qstr[2] = {(uint64_t)H * 4, (uint64_t)l * H * 4};
+  const uint32_t qrbox[3] = {AT, BQB, 1};
   CUtensorMap mk, mv, mq, mo, mdq;
-  if (!encode_bf16_map(&mk, k, 3, kdims, kstr, kbox) || !encode_bf16_map(&mv, v, 3, kdims, kstr, kbox) ||
-      !encode_bf16_map(&mq, q, 3, kdims, kstr, qbox) || !encode_bf16_map(&mo, dO, 2, odims, ostr, obox) ||
-      !encode_f32_map_noswizzle(&mdq, dq_acc, 2, qdims, qstr, qrbox))
+  if (!encode_bf16_map(&mk, k, 4, kdims, kstr, kbox) || !encode_bf16_map(&mv, v, 4, kdims, kstr, kbox) ||
+      !encode_bf16_map(&mq, q, 4, kdims, kstr, qbox) || !encode_bf16_map(&mo, dO, 3, odims, ostr, obox) ||
+      !encode_f32_map_noswizzle(&mdq, dq_acc, 3, qdims, qstr, qrbox))
     return cudaErrorInvalidValue;
   const float scale = rsqrtf((float)d);
-  dim3 grid((c + l + AT - 1) / AT, a);
+  dim3 grid((c + l + AT - 1) / AT, a, nseq);
   static int* dbg = nullptr;
   static bool dbg_on = getenv("TP_ATTN_DEBUG") != nullptr;
   if (dbg_on && !dbg) {
@@ -616,14 +630,15 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
   }
   int* dbg_dev = nullptr;
   if (dbg_on) { memset(dbg, 0, 4096 * sizeof(int)); cudaHostGetDevicePointer(&dbg_dev, dbg, 0); }
-  attn_bwd_sm100_kernel<<<grid, 192, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, mdq, lse, Dvec, dk_acc, dv_acc, s, c, l,
-                                                           scale, scale * LOG2E_F, accumulate, dbg_dev);
+  attn_bwd_sm100_kernel<<<grid, 192, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, mdq, lse, Dvec, lse_sstride, dkv_sstride,
+                                                           dk_acc, dv_acc, s, c, l, scale, scale * LOG2E_F, accumulate,
+                                                           dbg_dev);
   e = cudaGetLastError();
   if (dbg_on) {
     for (int it = 0; it < 50 && cudaStreamQuery(st) == cudaErrorNotReady; ++it) usleep(100000);
     if (cudaStreamQuery(st) == cudaErrorNotReady) {
       fprintf(stderr, "attn_bwd_sm100 HUNG: grid %d x %d, c=%d l=%d\n", grid.x, grid.y, c, l);
-      for (unsigned b = 0; b < grid.x * grid.y; ++b) {
+      for (unsigned b = 0; b < grid.x * grid.y * grid.z && b < 500; ++b) {
         fprintf(stderr, " cta %u:", b);
         for (int r = 0; r < 8; ++r) fprintf(stderr, " %d", ((volatile int*)dbg)[b * 8 + r]);
         fprintf(stderr, "\n");
@@ -633,7 +648,7 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
     }
   }
   if (e != cudaSuccess) return e;
-  dq_convert_kernel<<<l, 128, 0, st>>>(dq_acc, H, dq, ldq, H);
+  dq_convert_kernel<<<dim3(l, nseq), 128, 0, st>>>(dq_acc, H, dq, ldq, H, l, dq_sstride);
   return cudaGetLastError();
 }
 

@@ -223,9 +223,12 @@ __global__ void __launch_bounds__(NWARP * 32) attn_fwd_tc_kernel(const bf16* __r
 // D[head][r] = rowsum(dO * O): one warp per row, lanes take 8-element chunks of all heads.
 template <int D>
 __global__ void attn_bwd_prep_kernel(const bf16* __restrict__ dO, int64_t ld_do, const bf16* __restrict__ o,
-                                     int64_t ldo, float* __restrict__ Dvec, int a, int l) {
+                                     int64_t ldo, float* __restrict__ Dvec, int a, int l, int64_t o_sstride) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int r = blockIdx.x * 4 + w;
+  dO += blockIdx.y * o_sstride;
+  o += blockIdx.y * o_sstride;
+  Dvec += (int64_t)blockIdx.y * a * l;
   if (r >= l) return;
   constexpr int CPH = D / 8;  // chunks per head (2..16)
   for (int base = 0; base < a * CPH; base += 32) {
@@ -531,7 +534,7 @@ cudaError_t bwd_d(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ldo, con
     attr = true;
   }
   const float scale = rsqrtf((float)D);
-  attn_bwd_prep_kernel<D><<<dim3((l + 3) / 4), 128, 0, st>>>(dO, ld_do, o, ldo, Dvec, a, l);
+  attn_bwd_prep_kernel<D><<<dim3((l + 3) / 4), 128, 0, st>>>(dO, ld_do, o, ldo, Dvec, a, l, 0);
   attn_bwd_dq_kernel<D><<<dim3((l + BQ - 1) / BQ, a), NWARP * 32, smem_q, st>>>(dO, ld_do, q, k, v, lse, Dvec, dq, ldq, s,
                                                                                 c, l, scale, scale * LOG2E);
   attn_bwd_dkv_kernel<D><<<dim3((c + l + BKEY - 1) / BKEY, a), NWARP * 32, smem_kv, st>>>(
@@ -542,14 +545,14 @@ cudaError_t bwd_d(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ldo, con
 }  // namespace
 
 cudaError_t attn_bwd_prep(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ldo, float* Dvec, int a, int d, int l,
-                          cudaStream_t st) {
+                          cudaStream_t st, int nseq, int64_t o_sstride) {
   if (l == 0) return cudaSuccess;
-  dim3 grid((l + 3) / 4);
+  dim3 grid((l + 3) / 4, nseq);
   switch (d) {
-    case 16: attn_bwd_prep_kernel<16><<<grid, 128, 0, st>>>(dO, ld_do, o, ldo, Dvec, a, l); break;
-    case 32: attn_bwd_prep_kernel<32><<<grid, 128, 0, st>>>(dO, ld_do, o, ldo, Dvec, a, l); break;
-    case 64: attn_bwd_prep_kernel<64><<<grid, 128, 0, st>>>(dO, ld_do, o, ldo, Dvec, a, l); break;
-    case 128: attn_bwd_prep_kernel<128><<<grid, 128, 0, st>>>(dO, ld_do, o, ldo, Dvec, a, l); break;
+    case 16: attn_bwd_prep_kernel<16><<<grid, 128, 0, st>>>(dO, ld_do, o, ldo, Dvec, a, l, o_sstride); break;
+    case 32: attn_bwd_prep_kernel<32><<<grid, 128, 0, st>>>(dO, ld_do, o, ldo, Dvec, a, l, o_sstride); break;
+    case 64: attn_bwd_prep_kernel<64><<<grid, 128, 0, st>>>(dO, ld_do, o, ldo, Dvec, a, l, o_sstride); break;
+    case 128: attn_bwd_prep_kernel<128><<<grid, 128, 0, st>>>(dO, ld_do, o, ldo, Dvec, a, l, o_sstride); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -63,16 +63,20 @@ cudaError_t attn_bwd_tc(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ld
                         float* dv_acc, int a, int s, int d, int c, int l, int accumulate, cudaStream_t st);
 // tcgen05/TMEM attention (attn_sm100.cu), head_dim 128 only.
 bool attn_sm100_supported(int d);
+// nseq sequences per launch (grid.z): sequence j uses q/k/v + j*qkv_sstride, o + j*o_sstride (row r at
+// + r*ldo), lse + j*lse_sstride.
 cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o, int64_t ldo, float* lse, int a, int s,
-                           int d, int c, int l, cudaStream_t st);
+                           int d, int c, int l, cudaStream_t st, int nseq = 1, int64_t qkv_sstride = 0,
+                           int64_t o_sstride = 0, int64_t lse_sstride = 0);
 // D[head][r] = rowsum(dO * O) per head (attn_tc.cu)
 cudaError_t attn_bwd_prep(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ldo, float* Dvec, int a, int d, int l,
-                          cudaStream_t st);
+                          cudaStream_t st, int nseq = 1, int64_t o_sstride = 0);
 // dq_acc: fp32 scratch [l][a*d] (zeroed inside); dq: bf16 output rows (ld ldq)
 cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ldo, const bf16* q, const bf16* k,
                            const bf16* v, const float* lse, float* Dvec, float* dq_acc, bf16* dq, int64_t ldq,
                            float* dk_acc, float* dv_acc, int a, int s, int d, int c, int l, int accumulate,
-                           cudaStream_t st);
+                           cudaStream_t st, int nseq = 1, int64_t qkv_sstride = 0, int64_t o_sstride = 0,
+                           int64_t lse_sstride = 0, int64_t dq_sstride = 0, int64_t dkv_sstride = 0);
 template <typename T>
 cudaError_t attn_dkv_finalize(const float* dk_acc, const float* dv_acc, T* dqkv, int64_t ld, int a,
                               int s, int d, int c, int l, cudaStream_t st);

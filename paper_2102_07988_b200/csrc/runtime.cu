@@ -347,9 +347,9 @@ class Engine final : public EngineBase {
     // per job: up to b = max_batch sequences of one slice
     TRY(vec(S.dk_acc, nl, B * s * H)); TRY(vec(S.dv_acc, nl, B * s * H));
     TRY(alloc(&S.gA, B * s * H)); TRY(alloc(&S.gB, B * s * H)); TRY(alloc(&S.gm, B * s * H)); TRY(alloc(&S.dA, B * s * H));
-    TRY(alloc(&S.Dvec, a * s)); TRY(alloc(&S.dO, B * s * H));
+    TRY(alloc(&S.Dvec, B * a * s)); TRY(alloc(&S.dO, B * s * H));
     TRY(alloc(&S.lnws, 2 * H * ((B * s + 3) / 4)));
-    TRY(alloc(&S.dqacc, s * H));
+    TRY(alloc(&S.dqacc, B * s * H));
     return TP_OK;
   }
 
@@ -465,6 +465,10 @@ class Engine final : public EngineBase {
       T* o = S.O[j] + row * H;
       const double attn_flops = 4.0 * H * b * ((double)l * c + 0.5 * l * (l + 1.0));
       TRY(launch(KC_ATTN_FWD, attn_flops, ebytes * b * (2.0 * H * (c + l) + 2.0 * H * l), [&] {
+        if constexpr (std::is_same<T, bf16>::value)
+          if (!force_simt && attn_sm100_supported(dh) && !legacy_attn)  // all b sequences in one launch
+            return attn_fwd_sm100(S.Q[j] + seq0 * s * H, S.Kc[j] + seq0 * s * H, S.Vc[j] + seq0 * s * H, o, (int64_t)b * H,
+                                  S.LSE[j] + seq0 * a * s, a, s, dh, c, l, stream, b, (int64_t)s * H, H, (int64_t)a * s);
         for (int jj = 0; jj < b; ++jj) {
           const size_t sq = seq0 + jj;
           const T *q = S.Q[j] + sq * s * H, *kk = S.Kc[j] + sq * s * H, *vv = S.Vc[j] + sq * s * H;
@@ -557,6 +561,17 @@ class Engine final : public EngineBase {
       T* dq = S.dQKV[j] + row * 3 * H;
       const int accum = first_bwd_slice ? 0 : 1;
       TRY(launch(KC_ATTN_BWD, attn_flops, b * (ebytes * 4.0 * H * (c + l) + 16.0 * H * (c + l)), [&] {
+        if constexpr (std::is_same<T, bf16>::value)
+          if (!force_simt && attn_sm100_supported(dh) && !legacy_attn) {  // all b sequences in one launch
+            cudaError_t e = attn_bwd_sm100(S.dO, (int64_t)b * H, S.O[j] + row * H, (int64_t)b * H, S.Q[j] + seq0 * s * H,
+                                           S.Kc[j] + seq0 * s * H, S.Vc[j] + seq0 * s * H, S.LSE[j] + seq0 * a * s, S.Dvec,
+                                           S.dqacc, dq, (int64_t)b * 3 * H, S.dk_acc[j], S.dv_acc[j], a, s, dh, c, l, accum,
+                                           stream, b, (int64_t)s * H, H, (int64_t)a * s, 3 * H, (int64_t)s * H);
+            for (int jj = 0; jj < b && e == cudaSuccess; ++jj)
+              e = attn_dkv_finalize<T>(S.dk_acc[j] + (size_t)jj * s * H, S.dv_acc[j] + (size_t)jj * s * H,
+                                       dq + (size_t)jj * 3 * H, (int64_t)b * 3 * H, a, s, dh, c, l, stream);
+            return e;
+          }
         for (int jj = 0; jj < b; ++jj) {
           const size_t sq = seq0 + jj;
           const T *q = S.Q[j] + sq * s * H, *kk = S.Kc[j] + sq * s * H, *vv = S.Vc[j] + sq * s * H;
