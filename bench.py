@@ -210,7 +210,7 @@ def main():
     if args.slicing in ("dp", "gpipe") and (args.slicing == "dp" or len(bsl) > 1):
         t0 = time.time()
         for b in bsl:
-            ticks, f = ctx.profile(g, reps=3, batch_slice=b)
+            ticks, f = ctx.profile(g, reps=5, batch_slice=b)
             if world > 1:
                 ticks = tdist.bottleneck_table(ticks)
             t1 = time.time()
