@@ -35,13 +35,23 @@ struct Epi {
   int bs = 1;                 // QKV: rows m -> (sequence m % bs, position row0 + m / bs); sequences s_len*hidden apart
 };
 
+// tanh: exact libm form in fp32 mode; the MUFU tanh.approx (rel. err ~2^-11, below the bf16 output
+// rounding of 2^-9) in bf16 mode, where the GeLU epilogue would otherwise pace the GEMM.
+template <typename T> __device__ __forceinline__ float tanh_t(float x) { return tanhf(x); }
+template <> __device__ __forceinline__ float tanh_t<bf16>(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+template <typename T>
 __device__ __forceinline__ float gelu_f(float u) {
   const float c = 0.7978845608028654f;  // sqrt(2/pi)
-  return 0.5f * u * (1.f + tanhf(c * (u + 0.044715f * u * u * u)));
+  return 0.5f * u * (1.f + tanh_t<T>(c * (u + 0.044715f * u * u * u)));
 }
+template <typename T>
 __device__ __forceinline__ float gelu_grad_f(float u) {
   const float c = 0.7978845608028654f;
-  const float t = tanhf(c * (u + 0.044715f * u * u * u));
+  const float t = tanh_t<T>(c * (u + 0.044715f * u * u * u));
   return 0.5f * (1.f + t) + 0.5f * u * (1.f - t * t) * c * (1.f + 3.f * 0.044715f * u * u);
 }
 
@@ -74,7 +84,7 @@ __device__ __forceinline__ void epi_apply8(const Epi& e, int m, int n0, float (&
 #pragma unroll
       for (int i = 0; i < 8; ++i) u[i] = to_f<T>(from_f<T>(v[i]));
 #pragma unroll
-      for (int i = 0; i < 8; ++i) g[i] = gelu_f(u[i]);
+      for (int i = 0; i < 8; ++i) g[i] = gelu_f<T>(u[i]);
       store8<T>(reinterpret_cast<T*>(e.out) + (int64_t)m * e.ldo + n0, u);
       store8<T>(reinterpret_cast<T*>(e.out2) + (int64_t)m * e.ldo2 + n0, g);
       break;
@@ -83,7 +93,7 @@ __device__ __forceinline__ void epi_apply8(const Epi& e, int m, int n0, float (&
       float u[8];
       load8<T>(reinterpret_cast<const T*>(e.aux) + (int64_t)m * e.ld_aux + n0, u);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] *= gelu_grad_f(u[i]);
+      for (int i = 0; i < 8; ++i) v[i] *= gelu_grad_f<T>(u[i]);
       store8<T>(reinterpret_cast<T*>(e.out) + (int64_t)m * e.ldo + n0, v);
       break;
     }

@@ -97,3 +97,32 @@ def test_rejects_bad_slicing():
     with pytest.raises(tp.TpError) as e:                        # batch_slice must divide batch
         gpu_run(TINY, 1, params, tokens, [32], tp.TP_BF16, batch_slice=2)
     assert e.value.status == tp.TP_EINVAL
+
+
+def test_profile_plan_step_end_to_end():
+    """a1 -> a2 -> tp_step: the measured cost table feeds the DP
+    and the chosen slicing runs with parity against the oracle; the DP result equals the oracle's
+    Algorithm 1 on the same table."""
+    from oracle import plan as op
+    cfg = SMALL.with_(n_stages=2)
+    B = 2
+    params, tokens, ref = oracle_run(cfg, B, 9, True)
+    ctx = tp.Context(cfg, precision=tp.TP_BF16, max_batch=B, device=0, flags=tp.TP_FLAG_KEEP_LOGITS)
+    try:
+        from synth import pack_all_stages, unpack_all_stages
+        ctx.load_params(pack_all_stages(params, cfg))
+        g = 16
+        for b in (1, 2):
+            ticks, fit = ctx.profile(g, reps=3, batch_slice=b)
+            n = cfg.seq_len // g
+            assert ticks.shape == (n, n + 1)
+            assert all(ticks[l - 1, c] > 0 for l in range(1, n + 1) for c in range(0, n - l + 1))
+            assert fit.shape == (5,) and np.isfinite(fit).all()
+            sl = tp.plan(ticks, g, cfg.n_layer, cfg.hidden, cfg.seq_len, 2, n_micro=B // b)
+            T, m, lens = op.optimize(ticks, n, 2, B // b)
+            assert sl.lengths == [g * x for x in lens] and sl.predicted == T
+            loss = ctx.step(tp.Slicing(sl.lengths, b), tokens)
+            grads = unpack_all_stages(ctx.grads(), cfg)
+            check(worst_errors(loss, ctx.logits(B), grads, ref), 2e-2)
+    finally:
+        ctx.close()
