@@ -216,6 +216,12 @@ class Engine final : public EngineBase {
   float* d_loss = nullptr;
   float* h_loss = nullptr;  // pinned
   int last_batch = 0, last_b = 1;
+  int32_t* h_tokens = nullptr;  // pinned staging of the step's tokens
+  // CUDA graph of the last (slicing, batch) op list
+  bool use_graphs = true;
+  std::vector<int64_t> g_key;
+  cudaGraphExec_t g_exec = nullptr;
+  int64_t g_launches = 0;
   // NCCL (multi-rank)
   ncclComm_t base = nullptr, commF[2] = {nullptr, nullptr}, commB[2] = {nullptr, nullptr};
   cudaStream_t s_recv_f = nullptr, s_send_f = nullptr, s_recv_b = nullptr, s_send_b = nullptr;
@@ -224,6 +230,8 @@ class Engine final : public EngineBase {
 
   ~Engine() override {
     if (stream) cudaStreamSynchronize(stream);
+    if (g_exec) cudaGraphExecDestroy(g_exec);
+    if (h_tokens) cudaFreeHost(h_tokens);
     for (ncclComm_t c : {commF[0], commF[1], commB[0], commB[1], base})
       if (c) ncclCommDestroy(c);
     for (void* p : allocs) cudaFree(p);
@@ -276,6 +284,8 @@ class Engine final : public EngineBase {
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CU(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, hi));
     CU(cudaHostAlloc(&h_loss, sizeof(float), cudaHostAllocDefault));
+    CU(cudaHostAlloc(&h_tokens, sizeof(int32_t) * (size_t)max_batch * (m.s + 1), cudaHostAllocDefault));
+    use_graphs = std::getenv("TP_NO_GRAPHS") == nullptr && std::getenv("TP_ATTN_DEBUG") == nullptr;
     TRY(alloc(&d_tokens, (size_t)max_batch * (m.s + 1)));
     TRY(alloc(&d_loss, 4));
     stages.resize(k1 - k0);
@@ -685,40 +695,26 @@ class Engine final : public EngineBase {
   }
 
   // ------------------------------------------------------------ one step
-  tp_status step(const tp_slicing* sl, const int32_t* tokens, bool host_tokens, int batch, float* loss_out) override {
-    if (!sl || !sl->lengths) return fail(TP_EINVAL, "tp_step: null slicing");
-    if (batch < 1 || batch > max_batch) return fail(TP_EINVAL, "tp_step: batch %d not in [1, max_batch=%d]", batch, max_batch);
-    const int b = sl->batch_slice;
-    if (b < 1 || batch % b != 0)
-      return fail(TP_EINVAL, "tp_step: batch_slice %d must be >= 1 and divide batch %d", b, batch);
-    const int M = sl->n_slices;
-    if (M < 1 || M > m.s) return fail(TP_EINVAL, "tp_step: n_slices %d", M);
-    std::vector<int> off(M + 1, 0);
-    for (int i = 0; i < M; ++i) {
-      if (sl->lengths[i] <= 0) return fail(TP_EINVAL, "tp_step: slice %d has length %d", i, sl->lengths[i]);
-      off[i + 1] = off[i] + sl->lengths[i];
-    }
-    if (off[M] != m.s) return fail(TP_EINVAL, "tp_step: slice lengths sum to %d, seq_len is %d", off[M], m.s);
-    if (!tokens) return fail(TP_EINVAL, "tp_step: null tokens");
-    CU(cudaSetDevice(device));
-    instr.launches = 0;
-    ev_next = 0;
-    last_batch = batch;
-    last_b = b;
+  // Everything one step puts on the device after the tokens are in d_tokens: zero the gradients, the
+  // forward and backward op lists of every owned stage, the deferred weight gradients, the loss.
+  tp_status enqueue_step(const std::vector<int>& off, const int32_t* lengths, int M, int b, int batch) {
     const int D = batch / b;
-    const size_t ntok = (size_t)batch * (m.s + 1);
-    CU(cudaMemcpyAsync(d_tokens, tokens, ntok * sizeof(int32_t), host_tokens ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, stream));
-    for (auto& S : stages) CU(cudaMemsetAsync(S.gflat, 0, S.L.total * sizeof(float), stream));
     const bool multi = world > 1;
+    if (multi) {  // fork: the comm streams join this step's stream order (and any graph capture)
+      cudaEvent_t e = event();
+      CU(cudaEventRecord(e, stream));
+      for (cudaStream_t cs : {s_send_f, s_recv_f, s_send_b, s_recv_b}) CU(cudaStreamWaitEvent(cs, e, 0));
+    }
+    for (auto& S : stages) CU(cudaMemsetAsync(S.gflat, 0, S.L.total * sizeof(float), stream));
     // forward: F(g, i) for groups g = 0..D-1 of b sequences, slices i = 1..M (stage order inside a
     // job in loopback); a job is b*l_i tokens, contiguous rows (see fwd())
     for (int d = 0; d < D; ++d)
       for (int i = 0; i < M; ++i)
         for (auto& S : stages) {
           const size_t row = ((size_t)d * m.s + off[i]) * b;
-          const int Tn = b * sl->lengths[i];
+          const int Tn = b * lengths[i];
           if (multi && S.k > 0) TRY(recv_fwd(S, row, Tn));
-          TRY(fwd(S, d, off[i], sl->lengths[i], b, batch));
+          TRY(fwd(S, d, off[i], lengths[i], b, batch));
           if (multi && S.k < m.K - 1) TRY(send_fwd(S, row, Tn));
         }
     // backward: exact reverse order (GPipe order, A-21)
@@ -727,9 +723,9 @@ class Engine final : public EngineBase {
         for (int si = (int)stages.size() - 1; si >= 0; --si) {
           Stage<T>& S = stages[si];
           const size_t row = ((size_t)d * m.s + off[i]) * b;
-          const int Tn = b * sl->lengths[i];
+          const int Tn = b * lengths[i];
           if (multi && S.k < m.K - 1) TRY(recv_bwd(S, row, Tn));
-          TRY(bwd(S, d, off[i], sl->lengths[i], b, batch, i == M - 1));
+          TRY(bwd(S, d, off[i], lengths[i], b, batch, i == M - 1));
           if (multi && S.k > 0) TRY(send_bwd(S, row, Tn));
         }
     }
@@ -752,6 +748,64 @@ class Engine final : public EngineBase {
       NC(ncclAllReduce(d_loss, d_loss, 1, ncclFloat32, ncclSum, base, stream));
     }
     CU(cudaMemcpyAsync(h_loss, d_loss, sizeof(float), cudaMemcpyDeviceToHost, stream));
+    return TP_OK;
+  }
+
+  tp_status step(const tp_slicing* sl, const int32_t* tokens, bool host_tokens, int batch, float* loss_out) override {
+    if (!sl || !sl->lengths) return fail(TP_EINVAL, "tp_step: null slicing");
+    if (batch < 1 || batch > max_batch) return fail(TP_EINVAL, "tp_step: batch %d not in [1, max_batch=%d]", batch, max_batch);
+    const int b = sl->batch_slice;
+    if (b < 1 || batch % b != 0)
+      return fail(TP_EINVAL, "tp_step: batch_slice %d must be >= 1 and divide batch %d", b, batch);
+    const int M = sl->n_slices;
+    if (M < 1 || M > m.s) return fail(TP_EINVAL, "tp_step: n_slices %d", M);
+    std::vector<int> off(M + 1, 0);
+    for (int i = 0; i < M; ++i) {
+      if (sl->lengths[i] <= 0) return fail(TP_EINVAL, "tp_step: slice %d has length %d", i, sl->lengths[i]);
+      off[i + 1] = off[i] + sl->lengths[i];
+    }
+    if (off[M] != m.s) return fail(TP_EINVAL, "tp_step: slice lengths sum to %d, seq_len is %d", off[M], m.s);
+    if (!tokens) return fail(TP_EINVAL, "tp_step: null tokens");
+    CU(cudaSetDevice(device));
+    last_batch = batch;
+    last_b = b;
+    // tokens -> d_tokens, outside any graph (the caller's pointer may change between calls)
+    const size_t ntok = (size_t)batch * (m.s + 1);
+    if (host_tokens) {
+      std::memcpy(h_tokens, tokens, ntok * sizeof(int32_t));
+      CU(cudaMemcpyAsync(d_tokens, h_tokens, ntok * sizeof(int32_t), cudaMemcpyHostToDevice, stream));
+    } else {
+      CU(cudaMemcpyAsync(d_tokens, tokens, ntok * sizeof(int32_t), cudaMemcpyDeviceToDevice, stream));
+    }
+    // The op list of a (slicing, batch) pair is static: the first step with a new key runs eagerly,
+    // the second is captured into a CUDA graph, later ones replay it (no per-kernel host launch cost).
+    std::vector<int64_t> key = {b, batch, M};
+    for (int i = 0; i < M; ++i) key.push_back(sl->lengths[i]);
+    const bool graphs = use_graphs && !instr.on;
+    if (graphs && g_exec && key == g_key) {
+      CU(cudaGraphLaunch(g_exec, stream));
+      instr.launches = g_launches;
+    } else if (graphs && key == g_key) {
+      instr.launches = 0;
+      ev_next = 0;
+      CU(cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed));
+      tp_status st = enqueue_step(off, sl->lengths, M, b, batch);
+      cudaGraph_t graph = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(stream, &graph);
+      if (st != TP_OK) { if (graph) cudaGraphDestroy(graph); return st; }
+      if (ce != cudaSuccess) return fail(TP_ECUDA, "graph capture: %s", cudaGetErrorString(ce));
+      ce = cudaGraphInstantiate(&g_exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ce != cudaSuccess) { g_exec = nullptr; return fail(TP_ECUDA, "graph instantiate: %s", cudaGetErrorString(ce)); }
+      g_launches = instr.launches;
+      CU(cudaGraphLaunch(g_exec, stream));
+    } else {
+      if (g_exec) { cudaGraphExecDestroy(g_exec); g_exec = nullptr; }
+      g_key = key;
+      instr.launches = 0;
+      ev_next = 0;
+      TRY(enqueue_step(off, sl->lengths, M, b, batch));
+    }
     CU(cudaStreamSynchronize(stream));
     CU(cudaGetLastError());
     instr.resolve();

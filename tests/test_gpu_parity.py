@@ -126,3 +126,29 @@ def test_profile_plan_step_end_to_end():
             check(worst_errors(loss, ctx.logits(B), grads, ref), 2e-2)
     finally:
         ctx.close()
+
+
+def test_graph_replay_identical():
+    """tp_step runs a new (slicing, batch) eagerly, captures it into a CUDA graph on the second call
+    and replays the graph afterwards: all three give identical results, and a different slicing in
+    between invalidates the graph."""
+    cfg = SMALL.with_(n_stages=2)
+    B = 2
+    params, tokens, ref = oracle_run(cfg, B, 10, True)
+    from synth import pack_all_stages
+    ctx = tp.Context(cfg, precision=tp.TP_BF16, max_batch=B, device=0)
+    try:
+        ctx.load_params(pack_all_stages(params, cfg))
+        sl = tp.Slicing([40, 24, 64])
+        outs = []
+        for _ in range(3):
+            loss = ctx.step(sl, tokens)
+            outs.append((loss, ctx.grads(), ctx.last_step_launches()))
+        ctx.step(tp.Slicing([64, 64], 2), tokens)
+        outs.append((ctx.step(sl, tokens), ctx.grads(), ctx.last_step_launches()))
+        for loss, g, n in outs[1:]:
+            assert abs(loss - outs[0][0]) <= 1e-6 * abs(outs[0][0])
+            assert rel(g, outs[0][1]) < 1e-6 and n == outs[0][2] > 0
+        assert abs(outs[0][0] - ref["loss"]) < 2e-2 * abs(ref["loss"])
+    finally:
+        ctx.close()
