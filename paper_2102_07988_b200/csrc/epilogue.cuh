@@ -55,10 +55,18 @@ __device__ __forceinline__ float gelu_grad_f(float u) {
   return 0.5f * (1.f + t) + 0.5f * u * (1.f - t * t) * c * (1.f + 3.f * 0.044715f * u * u);
 }
 
-// Applies the epilogue to columns [n0, n0+8) of row m; n0 % 8 == 0, caller guarantees m < M and
-// n0 + 8 <= N.
+// The per-element input an epilogue reads besides the accumulator (RESID: the fp32 residual row,
+// DGELU: the stored U), fetched ahead of time so its latency overlaps other work.
 template <typename T>
-__device__ __forceinline__ void epi_apply8(const Epi& e, int m, int n0, float (&v)[8]) {
+__device__ __forceinline__ void epi_prefetch8(const Epi& e, int m, int n0, float (&aux)[8]) {
+  if (e.kind == EPI_RESID) load8<float>(e.resid + (int64_t)m * e.ldr + n0, aux);
+  else if (e.kind == EPI_DGELU) load8<T>(reinterpret_cast<const T*>(e.aux) + (int64_t)m * e.ld_aux + n0, aux);
+}
+
+// Applies the epilogue to columns [n0, n0+8) of row m; n0 % 8 == 0, caller guarantees m < M and
+// n0 + 8 <= N. `aux` holds epi_prefetch8's result for the same (m, n0).
+template <typename T>
+__device__ __forceinline__ void epi_apply8(const Epi& e, int m, int n0, float (&v)[8], const float (&aux)[8]) {
   if (e.kind != EPI_DGELU && e.kind != EPI_ACCUM && e.bias) {
     float b[8];
     load8<float>(e.bias + n0, b);
@@ -71,10 +79,8 @@ __device__ __forceinline__ void epi_apply8(const Epi& e, int m, int n0, float (&
       else store8<T>(reinterpret_cast<T*>(e.out) + (int64_t)m * e.ldo + n0, v);
       break;
     case EPI_RESID: {
-      float r[8];
-      load8<float>(e.resid + (int64_t)m * e.ldr + n0, r);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] += r[i];
+      for (int i = 0; i < 8; ++i) v[i] += aux[i];
       store8<float>(reinterpret_cast<float*>(e.out) + (int64_t)m * e.ldo + n0, v);
       break;
     }
@@ -90,10 +96,8 @@ __device__ __forceinline__ void epi_apply8(const Epi& e, int m, int n0, float (&
       break;
     }
     case EPI_DGELU: {
-      float u[8];
-      load8<T>(reinterpret_cast<const T*>(e.aux) + (int64_t)m * e.ld_aux + n0, u);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] *= gelu_grad_f<T>(u[i]);
+      for (int i = 0; i < 8; ++i) v[i] *= gelu_grad_f<T>(aux[i]);
       store8<T>(reinterpret_cast<T*>(e.out) + (int64_t)m * e.ldo + n0, v);
       break;
     }
@@ -117,6 +121,13 @@ __device__ __forceinline__ void epi_apply8(const Epi& e, int m, int n0, float (&
       break;
     }
   }
+}
+
+template <typename T>
+__device__ __forceinline__ void epi_apply8(const Epi& e, int m, int n0, float (&v)[8]) {
+  float aux[8];
+  epi_prefetch8<T>(e, m, n0, aux);
+  epi_apply8<T>(e, m, n0, v, aux);
 }
 
 }  // namespace tp

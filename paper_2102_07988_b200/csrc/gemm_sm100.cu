@@ -174,14 +174,24 @@ __global__ void __launch_bounds__(192, 1)
       // TMEM (thread = row) -> padded smem transpose -> 4 lanes per row, 8 columns each: every
       // global access of the fused epilogue is a 64/128-byte contiguous row segment.
       float* scr = epi_scratch + (warp - 2) * 32 * 33;
+      const bool has_aux = epi.kind == EPI_RESID || epi.kind == EPI_DGELU;
 #pragma unroll 1
       for (int ch = 0; ch < BN / 32; ++ch) {
+        const int n = n0 + ch * 32 + (lane & 3) * 8;
+        // issue this chunk's residual / U loads first: 4 independent 32-byte loads in flight per thread
+        float aux[4][8];
+        if (has_aux) {
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const int row = m0 + q * 32 + it * 8 + (lane >> 2);
+            if (row < M && n < N) epi_prefetch8<bf16>(epi, row, n, aux[it]);
+          }
+        }
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 32, r);
 #pragma unroll
         for (int i = 0; i < 32; ++i) scr[lane * 33 + i] = __uint_as_float(r[i]);
         __syncwarp();
-        const int n = n0 + ch * 32 + (lane & 3) * 8;
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
           const int rr = it * 8 + (lane >> 2);
@@ -189,7 +199,7 @@ __global__ void __launch_bounds__(192, 1)
           float v[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) v[i] = scr[rr * 33 + (lane & 3) * 8 + i];
-          if (row < M && n < N) epi_apply8<bf16>(epi, row, n, v);
+          if (row < M && n < N) epi_apply8<bf16>(epi, row, n, v, aux[it]);
         }
         __syncwarp();
       }

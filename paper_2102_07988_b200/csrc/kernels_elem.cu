@@ -8,6 +8,9 @@
 
 namespace tp {
 
+template <typename T>
+cudaError_t colsum_accum(const T* src, int64_t ld, float* out, int rows, int N, cudaStream_t st);
+
 namespace {
 
 // ---------------------------------------------------------------- LayerNorm
@@ -322,8 +325,11 @@ cudaError_t layernorm_bwd(const float* dy, const float* x, const float* mean, co
   else if (H <= 12288) LNB(512, 3);
   else return cudaErrorInvalidValue;
 #undef LNB
-  ln_bwd_reduce_kernel<<<(2 * H + 255) / 256, 256, 0, st>>>(ws, grid, dgam, dbet, H);
-  return cudaGetLastError();
+  // dgamma += column sums of the per-CTA partials ws[grid][0][H], dbeta of ws[grid][1][H]
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = colsum_accum<float>(ws, 2 * (int64_t)H, dgam, grid, H, st);
+  if (e == cudaSuccess) e = colsum_accum<float>(ws + H, 2 * (int64_t)H, dbet, grid, H, st);
+  return e;
 }
 cudaError_t embed_fwd(const int32_t* tok, const float* wte, const float* wpe, float* h, int c, int l, int b, int s,
                       int H, int V, cudaStream_t st) {

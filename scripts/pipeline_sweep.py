@@ -1,0 +1,92 @@
+"""DP vs uniform slicing on the same kernels (the B200 analogue of PAPER.md Table 3 / Fig. 7,
+PAPER.md:388-418). One process per GPU (torchrun), K = world stages.
+
+  torchrun --nproc-per-node 4 scripts/pipeline_sweep.py --config gpt3-175b-24l --uniform 1,2,4,8,16
+
+Prints one JSON line per scheme (rank 0): slicing, max-over-ranks ms per step, MFU, and the DP's
+predicted T for the DP row. The DP row uses the same profile -> plan path as bench.py.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2102_07988_b200 as tp  # noqa: E402
+from paper_2102_07988_b200 import dist as tdist  # noqa: E402
+from bench import model_flops, load_peaks  # noqa: E402
+from synth import CONFIGS, make_stage_flat, make_tokens  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="gpt3-175b-24l")
+    ap.add_argument("--uniform", default="1,2,4,8,16")
+    ap.add_argument("--batch-slice", type=int, default=1)
+    ap.add_argument("--granularity", type=int, default=64)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=2)
+    args = ap.parse_args()
+    world, rank, local = int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    base, B = CONFIGS[args.config]
+    cfg = base.with_(n_stages=world)
+    b = args.batch_slice
+    nid = tdist.share_nccl_id(rank) if world > 1 else None
+    ctx = tp.Context(cfg, rank=rank, world=world, nccl_id=nid, max_batch=B, device=local)
+    ctx.load_params(make_stage_flat(cfg, rank, seed=0) if world > 1 else make_stage_flat(cfg, 0, seed=0))
+    tok = torch.from_numpy(make_tokens(cfg, B, seed=1)).cuda()
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    peak = load_peaks()[0]
+    flops = model_flops(cfg, B)
+
+    ticks, fit = ctx.profile(args.granularity, reps=5, batch_slice=b)
+    if world > 1:
+        ticks = tdist.bottleneck_table(ticks)
+    dp = tp.plan(ticks, args.granularity, cfg.n_layer, cfg.hidden, cfg.seq_len, world, n_micro=B // b)
+    schemes = [("dp", tp.Slicing(dp.lengths, b, dp.t_max, dp.predicted))]
+    for m in [int(x) for x in args.uniform.split(",")]:
+        if cfg.seq_len % m == 0:
+            schemes.append((f"uniform{m}", tp.Slicing([cfg.seq_len // m] * m, b)))
+
+    def timed(sl):
+        for _ in range(args.warmup):
+            ctx.step_device(sl, tok.data_ptr(), B)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            ctx.step_device(sl, tok.data_ptr(), B)
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        return tdist.max_over_ranks(ms) if world > 1 else ms
+
+    for name, sl in schemes:
+        ms = timed(sl)
+        # predicted T of this scheme from the same table (Eq. 5 with D = B/b)
+        n, g, c, ts = cfg.seq_len // args.granularity, args.granularity, 0, []
+        for l in sl.lengths:
+            ts.append(int(ticks[l // g - 1, c // g]))
+            c += l
+        pred = (B // b) * sum(ts) + (world - 1) * max(ts)
+        if rank == 0:
+            print(json.dumps({"config": args.config, "stages": world, "scheme": name, "slicing": sl.notation(B),
+                              "ms_per_step": ms, "mfu": flops / (ms / 1e3) / (world * peak * 1e12),
+                              "predicted_ms": pred / 1e6}), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
