@@ -37,8 +37,10 @@ constexpr float LOG2E_F = 1.4426950408889634f;
 struct FwdSmem {
   static constexpr uint32_t Q = 0, K0 = TILE, V0 = 2 * TILE, K1 = 3 * TILE, V1 = 4 * TILE, P = 5 * TILE;
   static constexpr uint32_t BAR = 6 * TILE;
-  static constexpr uint32_t BYTES = BAR + 256 + 1024;
+  static constexpr uint32_t XCH = BAR + 256;  // fp32 [2 parity][2 halves][128 rows]: partial row maxima / sums
+  static constexpr uint32_t BYTES = XCH + 3072 + 1024;  // + [2][128] partial sums
 };
+constexpr int FWD_THREADS = 320;  // TMA warp, MMA warp, 8 softmax warps (2 per TMEM lane quarter)
 
 __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -64,7 +66,7 @@ __device__ __forceinline__ uint32_t swz(int row, int cc) {
   return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((cc ^ (row & 7)) << 4));
 }
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(FWD_THREADS, 1)
     attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                           const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ o, int64_t ldo,
                           float* __restrict__ lse, int s, int c, int l, float scale_log2, int64_t o_sstride,
@@ -94,10 +96,10 @@ __global__ void __launch_bounds__(192, 1)
     mbar_init(qfull, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(kvfull + i, 1); mbar_init(kvfree + i, 1);
-      mbar_init(sfull + i, 1); mbar_init(sfree + i, 4);
-      mbar_init(ofull + i, 1); mbar_init(ofree + i, 4);
+      mbar_init(sfull + i, 1); mbar_init(sfree + i, 8);
+      mbar_init(ofull + i, 1); mbar_init(ofree + i, 8);
     }
-    mbar_init(pfull, 4);
+    mbar_init(pfull, 8);
     mbar_init(pfree, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -161,24 +163,28 @@ __global__ void __launch_bounds__(192, 1)
     }
     pv(nkb - 1);
   } else if (warp >= 2) {
-    // ---------------- softmax / output: thread owns query row `row`
-    const int q = warp & 3, row = q * 32 + lane;
+    // ---------------- softmax / output: two warps per TMEM lane quarter; thread owns query row
+    // `row` and the key / head-dim columns [half*64, half*64+64); the two halves exchange row maxima
+    // through shared memory once per key block (named barrier 1, 256 threads).
+    const int q = warp & 3, row = q * 32 + lane, half = (warp - 2) >> 2;
     const int qabs = c + r0 + row;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     uint8_t* P = sm + FwdSmem::P;
+    float* xch = reinterpret_cast<float*>(sm + FwdSmem::XCH);
     float m = -INFINITY, lsum = 0.f, m_acc = -INFINITY, m_last = -INFINITY;
-    float acc[AT];
+    constexpr int HC = AT / 2;  // columns per half
+    float acc[HC];
 #pragma unroll
-    for (int i = 0; i < AT; ++i) acc[i] = 0.f;
+    for (int i = 0; i < HC; ++i) acc[i] = 0.f;
     auto add_o = [&](int i, float m_i) {
       const int bi = i & 1;
       mbar_wait(ofull + bi, (i >> 1) & 1);
       tc_fence_after();
       const float sc = ex2(m_acc - m_i);
 #pragma unroll
-      for (int ch = 0; ch < AT / 32; ++ch) {
+      for (int ch = 0; ch < HC / 32; ++ch) {
         uint32_t r[32];
-        tmem_ld32_nowait(lane_base + 256 + bi * 128 + ch * 32, r);
+        tmem_ld32_nowait(lane_base + 256 + bi * 128 + half * HC + ch * 32, r);
         tmem_wait_ld();
 #pragma unroll
         for (int t = 0; t < 32; ++t) acc[ch * 32 + t] = fmaf(acc[ch * 32 + t], sc, __uint_as_float(r[t]));
@@ -192,15 +198,15 @@ __global__ void __launch_bounds__(192, 1)
       const int b = j & 1;
       mbar_wait(sfull + b, (j >> 1) & 1);
       tc_fence_after();
-      const int key0 = j * AT;
-      const bool diag = key0 + AT - 1 > qabs;  // only the diagonal block needs the causal mask
-      const int nvis = qabs - key0 + 1;        // keys key0 .. qabs are visible (diag blocks)
-      // pass 1: row max of the raw scores (scale > 0 commutes with max)
+      const int key0 = j * AT + half * HC;       // first key of this half
+      const bool diag = key0 + HC - 1 > qabs;    // only blocks crossing the diagonal need the mask
+      const int nvis = qabs - key0 + 1;          // keys key0 .. qabs are visible
+      // pass 1: partial row max of the raw scores (scale > 0 commutes with max), exchanged
       float mx = -INFINITY;
 #pragma unroll
-      for (int ch = 0; ch < AT / 32; ++ch) {
+      for (int ch = 0; ch < HC / 32; ++ch) {
         uint32_t r[32];
-        tmem_ld32_nowait(lane_base + b * 128 + ch * 32, r);
+        tmem_ld32_nowait(lane_base + b * 128 + half * HC + ch * 32, r);
         tmem_wait_ld();
         if (!diag) {
 #pragma unroll
@@ -210,14 +216,18 @@ __global__ void __launch_bounds__(192, 1)
           for (int t = 0; t < 32; ++t) mx = fmaxf(mx, ch * 32 + t < nvis ? __uint_as_float(r[t]) : -INFINITY);
         }
       }
+      float* xm = xch + (j & 1) * 256;
+      xm[half * 128 + row] = mx;
+      named_bar(1, 256);
+      mx = fmaxf(mx, xm[(half ^ 1) * 128 + row]);
       const float m_new = fmaxf(m, mx * scale_log2);
       if (j >= 1) mbar_wait(pfree, (j - 1) & 1);  // PV_{j-1} has finished reading the P tile
-      // pass 2: P = exp2(S * scale_log2 - m_new) -> bf16, 128B-swizzled K-major tile
+      // pass 2: P = exp2(S * scale_log2 - m_new) -> bf16, this half's 64 keys of the swizzled P tile
       float rs = 0.f;
 #pragma unroll
-      for (int ch = 0; ch < AT / 32; ++ch) {
+      for (int ch = 0; ch < HC / 32; ++ch) {
         uint32_t r[32];
-        tmem_ld32_nowait(lane_base + b * 128 + ch * 32, r);
+        tmem_ld32_nowait(lane_base + b * 128 + half * HC + ch * 32, r);
         tmem_wait_ld();
         uint32_t pk[16];
 #pragma unroll
@@ -232,10 +242,10 @@ __global__ void __launch_bounds__(192, 1)
           __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
           pk[t >> 1] = *reinterpret_cast<uint32_t*>(&h);
         }
-        uint8_t* region = P + (ch >> 1) * HALF;
+        uint8_t* region = P + half * HALF;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int cc = (ch & 1) * 4 + u;
+          const int cc = ch * 4 + u;
           *reinterpret_cast<uint4*>(region + swz(row, cc)) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
       }
@@ -243,24 +253,28 @@ __global__ void __launch_bounds__(192, 1)
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) { mbar_arrive(sfree + b); mbar_arrive(pfull); }
-      lsum = lsum * ex2(m - m_new) + rs;
+      lsum = lsum * ex2(m - m_new) + rs;  // partial (this half's keys), same m in both halves
       m_last = m;
       m = m_new;
       if (j >= 1) add_o(j - 1, m_last);
     }
     add_o(nkb - 1, m);
+    float* xl = xch + 512;  // after the two max buffers
+    xl[half * 128 + row] = lsum;
+    named_bar(1, 256);
+    const float ltot = lsum + xl[(half ^ 1) * 128 + row];
     const int r = r0 + row;
     if (r < l) {
-      const float inv = 1.f / lsum;
-      bf16* orow = o + (int64_t)r * ldo + head * AT;
+      const float inv = 1.f / ltot;
+      bf16* orow = o + (int64_t)r * ldo + head * AT + half * HC;
 #pragma unroll
-      for (int i = 0; i < AT; i += 8) {
+      for (int i = 0; i < HC; i += 8) {
         float v8[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) v8[t] = acc[i + t] * inv;
         store8<bf16>(orow + i, v8);
       }
-      lse[(int64_t)head * s + c + r] = (m + log2f(lsum)) / LOG2E_F;
+      if (half == 0) lse[(int64_t)head * s + c + r] = (m + log2f(ltot)) / LOG2E_F;
     }
   }
   tc_fence_before();
@@ -581,7 +595,7 @@ cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o,
       !encode_bf16_map(&mv, v, 4, dims, strides, box))
     return cudaErrorInvalidValue;
   dim3 grid((l + AT - 1) / AT, a, nseq);
-  attn_fwd_sm100_kernel<<<grid, 192, FwdSmem::BYTES, st>>>(mq, mk, mv, o, ldo, lse, s, c, l, rsqrtf((float)d) * LOG2E_F,
+  attn_fwd_sm100_kernel<<<grid, FWD_THREADS, FwdSmem::BYTES, st>>>(mq, mk, mv, o, ldo, lse, s, c, l, rsqrtf((float)d) * LOG2E_F,
                                                            o_sstride, lse_sstride);
   return cudaGetLastError();
 }
