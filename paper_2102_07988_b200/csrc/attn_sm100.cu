@@ -308,7 +308,7 @@ struct BwdSmem {
   static constexpr uint32_t BYTES = BAR + 256 + 1024;
 };
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(FWD_THREADS, 1)
     attn_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                           const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                           const __grid_constant__ CUtensorMap tmdQ, const float* __restrict__ lse,
@@ -346,9 +346,9 @@ __global__ void __launch_bounds__(192, 1)
   if (threadIdx.x == 0) {
     mbar_init(kvfull, 1);
     for (int i = 0; i < 2; ++i) { mbar_init(qfull + i, 1); mbar_init(qfree + i, 1); }
-    mbar_init(sfull, 1); mbar_init(sfree, 4);
-    mbar_init(pfull, 4); mbar_init(pfree, 1);
-    mbar_init(dqfull, 1); mbar_init(dqfree, 4);
+    mbar_init(sfull, 1); mbar_init(sfree, 8);
+    mbar_init(pfull, 8); mbar_init(pfree, 1);
+    mbar_init(dqfull, 1); mbar_init(dqfree, 8);
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -431,8 +431,9 @@ __global__ void __launch_bounds__(192, 1)
     mma_commit(done);
     DBG(1, 999);
   } else if (warp >= 2) {
-    // ---------------- softmax-gradient warps: thread owns key row `row` (TMEM lane)
-    const int q = warp & 3, row = q * 32 + lane;
+    // ---------------- softmax-gradient warps: two per TMEM lane quarter; thread owns key row `row`
+    // and query columns [half*32, half*32+32) of the tile (head-dim columns for dQ^T / dK / dV)
+    const int q = warp & 3, row = q * 32 + lane, half = (warp - 2) >> 2;
     const int kabs = key0 + row;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     uint8_t* Pt = sm + BwdSmem::P;
@@ -440,25 +441,25 @@ __global__ void __launch_bounds__(192, 1)
     const float* lse_h = lse + (int64_t)head * s + c;
     const float* D_h = Dvec + (int64_t)head * l;
     float* dqs = reinterpret_cast<float*>(sm + BwdSmem::DQ);
+    constexpr int HQ = BQB / 2;  // query columns per half
     // dQ^T of tile i (thread = head-dim index `row`) -> smem [64 q][128 d] -> one TMA reduce-add
     auto drain_dq = [&](int i) {
       mbar_wait(dqfull, i & 1);
       tc_fence_after();
       if (threadIdx.x == 64) tma_wait_reads();  // previous reduce has finished reading the buffer
-      named_bar(1, 128);
-#pragma unroll
-      for (int ch = 0; ch < BQB / 32; ++ch) {
+      named_bar(1, 256);
+      {
         uint32_t r[32];
-        tmem_ld32_nowait(lane_base + T_DQ + ch * 32, r);
+        tmem_ld32_nowait(lane_base + T_DQ + half * HQ, r);
         tmem_wait_ld();
 #pragma unroll
-        for (int t = 0; t < 32; ++t) dqs[(ch * 32 + t) * AT + row] = __uint_as_float(r[t]) * scale;
+        for (int t = 0; t < 32; ++t) dqs[(half * HQ + t) * AT + row] = __uint_as_float(r[t]) * scale;
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(dqfree);
       fence_proxy_async();
-      named_bar(1, 128);
+      named_bar(1, 256);
       if (threadIdx.x == 64) tma_reduce_add_3d(&tmdQ, dqs, head * AT, (qt0 + i) * BQB, sq);
     };
     for (int i = 0; i < ntile; ++i) {
@@ -469,17 +470,17 @@ __global__ void __launch_bounds__(192, 1)
       {  // stage lse*log2e and D of this tile's 64 queries (rows past the slice: +inf / 0)
         const int t = threadIdx.x - 64, qr = qrow0 + (t & 63);
         if (t < 64) Ls[t] = qr < l ? __ldg(lse_h + qr) * LOG2E_F : INFINITY;
-        else Ds[t - 64] = qr < l ? __ldg(D_h + qr) : 0.f;
+        else if (t < 128) Ds[t - 64] = qr < l ? __ldg(D_h + qr) : 0.f;
       }
-      named_bar(1, 128);
+      named_bar(1, 256);
       mbar_wait(sfull, i & 1);
       if (lane == 0) DBG(2 + q, 101 + 10 * i);
       tc_fence_after();
       if (i >= 1) mbar_wait(pfree, (i - 1) & 1);  // MMAs of tile i-1 have read P^T / dS^T
       // visible iff c + qr >= kabs (and qr < l, which Ls = +inf enforces)
       const int vis0 = kabs - c - qrow0;  // first visible column of this key row
-#pragma unroll
-      for (int ch = 0; ch < BQB / 32; ++ch) {
+      {
+        const int ch = half;
         uint32_t rs[32], rp[32];
         tmem_ld32_nowait(lane_base + T_S + ch * 32, rs);
         tmem_ld32_nowait(lane_base + T_DP + ch * 32, rp);
@@ -517,7 +518,7 @@ __global__ void __launch_bounds__(192, 1)
     drain_dq(ntile - 1);
     if (threadIdx.x == 64) tma_wait_all();
     if (lane == 0) DBG(2 + q, 900);
-    // dK (x scale) and dV rows of this key block -> fp32 prefix accumulators
+    // dK (x scale) and dV rows of this key block, head-dim half -> fp32 prefix accumulators
     mbar_wait(done, 0);
     tc_fence_after();
     // (tcgen05.ld is warp-collective: every lane loads, only rows inside the prefix store)
@@ -525,7 +526,8 @@ __global__ void __launch_bounds__(192, 1)
     float* dkr = dk_acc + ((int64_t)head * s + kabs) * AT;
     float* dvr = dv_acc + ((int64_t)head * s + kabs) * AT;
 #pragma unroll
-    for (int ch = 0; ch < AT / 32; ++ch) {
+    for (int cq = 0; cq < 2; ++cq) {
+      const int ch = half * 2 + cq;
       uint32_t rk[32], rv[32];
       tmem_ld32_nowait(lane_base + T_DK + ch * 32, rk);
       tmem_ld32_nowait(lane_base + T_DV + ch * 32, rv);
@@ -644,7 +646,7 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
   }
   int* dbg_dev = nullptr;
   if (dbg_on) { memset(dbg, 0, 4096 * sizeof(int)); cudaHostGetDevicePointer(&dbg_dev, dbg, 0); }
-  attn_bwd_sm100_kernel<<<grid, 192, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, mdq, lse, Dvec, lse_sstride, dkv_sstride,
+  attn_bwd_sm100_kernel<<<grid, FWD_THREADS, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, mdq, lse, Dvec, lse_sstride, dkv_sstride,
                                                            dk_acc, dv_acc, s, c, l, scale, scale * LOG2E_F, accumulate,
                                                            dbg_dev);
   e = cudaGetLastError();
