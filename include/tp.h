@@ -154,11 +154,14 @@ tp_status tp_get_grads(tp_ctx* ctx, float* host_out, size_t n);
 tp_status tp_get_logits(tp_ctx* ctx, float* host_out, size_t n);
 
 /* Measures this context's (first owned) stage: t_{fwd+bwd}(l, c) of one job of batch_slice
- * sequences x l tokens with c tokens of context, in ns (median of `reps` after 2 warm-ups). The base curve t(l, 0) is measured
- * for every l = g, 2g, .., s and t_ctx(l, c) = a0 + a1 l + a2 c + a3 l c is least-squares fitted on
- * a subset of (l, c); ticks_out[(l/g-1)*(n+1) + c/g] = t(l,0) + t_ctx(l,c)
- * (n = s/g; caller-owned, n*(n+1) int64). fit_out (may be NULL): a0..a3 (ns, ns/token, ns/token,
- * ns/token^2) and the max relative error of the fit on the samples. Parameters must be loaded. */
+ * sequences x l tokens with c tokens of context, in ns (median of `reps` after 2 warm-ups). The base
+ * curve t(l, 0) is measured for every l = g, 2g, .., s; the context term t_ctx(l, c)
+ * is measured on a grid (l in {g 2^k} U {s}, c in multiples of s/8 U {s - l}) and
+ * ticks_out[(l/g-1)*(n+1) + c/g] = t(l,0) + t_ctx(l,c) with t_ctx interpolated from the grid
+ * (env TP_CTX_FIT=linear: the paper's least-squares t_ctx = a0 + a1 l + a2 c + a3 l c instead,
+ * PAPER.md:292-296). n = s/g; caller-owned, n*(n+1) int64. fit_out (may be NULL): the linear fit's
+ * a0..a3 (ns, ns/token, ns/token, ns/token^2) and its max relative error on the grid samples (the
+ * paper reports < 2%). Parameters must be loaded. */
 tp_status tp_profile(tp_ctx* ctx, int32_t granularity, int32_t batch_slice, int32_t reps,
                      int64_t* ticks_out, double* fit_out /* [5] */);
 

@@ -877,17 +877,23 @@ tp_status Engine<T>::profile(int g, int bsl, int reps, int64_t* ticks, double* f
   instr.on = false;
   std::vector<double> base(n + 1, 0.0);
   for (int u = 1; u <= n; ++u) TRY(time_job(u * g, 0, &base[u]));
-  // context samples: l in {g * 2^k}, c in {0, s/8, s/4, s/2, s - l}
-  std::vector<std::array<double, 3>> samp;  // (l, c, t_ctx)
-  for (int lu = 1; lu <= n; lu *= 2) {
-    const int l = lu * g;
-    int cs[5] = {0, m.s / 8, m.s / 4, m.s / 2, m.s - l};
-    for (int c : cs) {
-      c = (c / g) * g;
-      if (c < 0 || c + l > m.s) continue;
-      double t;
-      TRY(time_job(l, c, &t));
-      samp.push_back({(double)l, (double)c, t - base[lu]});
+  // context samples on a grid: l in {g * 2^k} U {s}, c in {0, s/8, 2s/8, ...} U {s - l}
+  std::vector<int> lgrid;
+  for (int lu = 1; lu < n; lu *= 2) lgrid.push_back(lu);
+  lgrid.push_back(n);
+  const int cstep = std::max(1, n / 8);
+  std::vector<std::array<double, 3>> samp;                  // (l, c, t_ctx) in tokens / ns
+  std::vector<std::vector<std::pair<int, double>>> cs_of(lgrid.size());  // per grid l: (cu, t_ctx)
+  for (size_t li = 0; li < lgrid.size(); ++li) {
+    const int lu = lgrid[li];
+    std::vector<int> cus;
+    for (int cu = 0; cu + lu <= n; cu += cstep) cus.push_back(cu);
+    if (cus.back() != n - lu) cus.push_back(n - lu);
+    for (int cu : cus) {
+      double t = base[lu];
+      if (cu > 0) TRY(time_job(lu * g, cu * g, &t));
+      cs_of[li].push_back({cu, t - base[lu]});
+      samp.push_back({(double)lu * g, (double)cu * g, t - base[lu]});
     }
   }
   instr.on = saved;
@@ -927,12 +933,39 @@ tp_status Engine<T>::profile(int g, int bsl, int reps, int64_t* ticks, double* f
     const double full = base[lu] + sp[2];
     if (full > 0) maxrel = std::max(maxrel, std::fabs(base[lu] + pred - full) / full);
   }
+  // Table fill. Default: t(l, c) = t(l, 0) + t_ctx(l, c) with t_ctx interpolated from the measured
+  // grid (piecewise-linear in c at each grid l, then linear in l) — on B200 small-slice attention is
+  // latency-bound, so t_ctx is not the bilinear a0 + a1 l + a2 c + a3 l c of PAPER.md:294 (the fit
+  // above is still reported). TP_CTX_FIT=linear fills the table from the paper's linear fit.
+  const bool linear = std::getenv("TP_CTX_FIT") && std::string(std::getenv("TP_CTX_FIT")) == "linear";
+  auto ctx_at = [&](size_t li, int cu) -> double {  // t_ctx at grid l index li, any cu >= 0
+    const auto& v = cs_of[li];
+    if (v.size() == 1) return v[0].second;
+    size_t k = 1;
+    while (k + 1 < v.size() && v[k].first < cu) ++k;
+    const double x0 = v[k - 1].first, x1 = v[k].first, y0 = v[k - 1].second, y1 = v[k].second;
+    return y0 + (y1 - y0) * (cu - x0) / (x1 - x0);  // extrapolates past the last point
+  };
   for (int lu = 1; lu <= n; ++lu)
     for (int cu = 0; cu + lu <= n; ++cu) {
       const double l = lu * g, c = cu * g;
-      double t = base[lu] + coef[0] + coef[1] * l + coef[2] * c + coef[3] * l * c;
-      if (cu == 0) t = base[lu];
-      ticks[(size_t)(lu - 1) * (n + 1) + cu] = std::max<int64_t>(1, (int64_t)std::llround(t));
+      double tc;
+      if (cu == 0) {
+        tc = 0.0;
+      } else if (linear) {
+        tc = coef[0] + coef[1] * l + coef[2] * c + coef[3] * l * c;
+      } else {
+        size_t hi = 0;
+        while (lgrid[hi] < lu) ++hi;
+        if (lgrid[hi] == lu || hi == 0) {
+          tc = ctx_at(hi, cu);
+        } else {
+          const double w = (double)(lu - lgrid[hi - 1]) / (lgrid[hi] - lgrid[hi - 1]);
+          tc = (1.0 - w) * ctx_at(hi - 1, cu) + w * ctx_at(hi, cu);
+        }
+        tc = std::max(0.0, tc);  // more context never costs less
+      }
+      ticks[(size_t)(lu - 1) * (n + 1) + cu] = std::max<int64_t>(1, (int64_t)std::llround(base[lu] + tc));
     }
   if (fit) { for (int i = 0; i < 4; ++i) fit[i] = coef[i]; fit[4] = maxrel; }
   return TP_OK;
