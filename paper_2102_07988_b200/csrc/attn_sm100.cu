@@ -54,6 +54,24 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[3
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// D[tmem] (+)= A[tmem] * B[smem]: the A operand (bf16, K packed two per 32-bit column) read from TMEM
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accum)
+      : "memory");
+}
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -79,8 +97,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   uint64_t* kvfree = bars + 3;   // [2]
   uint64_t* sfull = bars + 5;    // [2]
   uint64_t* sfree = bars + 7;    // [2]
-  uint64_t* pfull = bars + 9;
-  uint64_t* pfree = bars + 10;
+  uint64_t* pfull = bars + 9;    // [2] P_j written into S buffer j%2
   uint64_t* ofull = bars + 11;   // [2]
   uint64_t* ofree = bars + 13;   // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
@@ -96,11 +113,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     mbar_init(qfull, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(kvfull + i, 1); mbar_init(kvfree + i, 1);
-      mbar_init(sfull + i, 1); mbar_init(sfree + i, 8);
+      mbar_init(sfull + i, 1); mbar_init(sfree + i, 1);
       mbar_init(ofull + i, 1); mbar_init(ofree + i, 8);
+      mbar_init(pfull + i, 8);
     }
-    mbar_init(pfull, 8);
-    mbar_init(pfree, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tmem_alloc(tmem_slot, 512);
@@ -129,21 +145,22 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     // ---------------- MMA issuer
     constexpr uint32_t idS = idesc_bf16(128, 128, false, false);
     constexpr uint32_t idO = idesc_bf16(128, 128, false, true);
-    const uint32_t q_base = smem_u32(sm + FwdSmem::Q), p_base = smem_u32(sm + FwdSmem::P);
+    const uint32_t q_base = smem_u32(sm + FwdSmem::Q);
+    // O_i = P_i V_i with P_i (bf16) read from TMEM, where the softmax warps wrote it over the
+    // consumed S_i columns (S buffer bi, 64 packed columns); the commit then frees that S buffer.
     auto pv = [&](int i) {
       const int bi = i & 1;
-      mbar_wait(pfull, i & 1);
+      mbar_wait(pfull + bi, (i >> 1) & 1);
       if (i >= 2) mbar_wait(ofree + bi, ((i >> 1) - 1) & 1);
       tc_fence_after();
       const uint32_t v_base = smem_u32(sm + (bi ? FwdSmem::V1 : FwdSmem::V0));
 #pragma unroll
       for (int kk = 0; kk < AT / 16; ++kk) {
-        const uint64_t ad = make_desc(p_base + (kk >> 2) * HALF + (kk & 3) * 32, 16, 1024);
         const uint64_t bd = make_desc(v_base + kk * 2048, HALF, 1024);
-        mma_bf16(tmem + 256 + bi * 128, ad, bd, idO, kk > 0);
+        mma_bf16_ts(tmem + 256 + bi * 128, tmem + bi * 128 + kk * 8, bd, idO, kk > 0);
       }
       mma_commit(ofull + bi);
-      mma_commit(pfree);
+      mma_commit(sfree + bi);
       mma_commit(kvfree + bi);
     };
     mbar_wait(qfull, 0);
@@ -169,7 +186,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     const int q = warp & 3, row = q * 32 + lane, half = (warp - 2) >> 2;
     const int qabs = c + r0 + row;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    uint8_t* P = sm + FwdSmem::P;
     float* xch = reinterpret_cast<float*>(sm + FwdSmem::XCH);
     float m = -INFINITY, lsum = 0.f, m_acc = -INFINITY, m_last = -INFINITY;
     constexpr int HC = AT / 2;  // columns per half
@@ -201,19 +217,22 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       const int key0 = j * AT + half * HC;       // first key of this half
       const bool diag = key0 + HC - 1 > qabs;    // only blocks crossing the diagonal need the mask
       const int nvis = qabs - key0 + 1;          // keys key0 .. qabs are visible
-      // pass 1: partial row max of the raw scores (scale > 0 commutes with max), exchanged
+      // pass 1: this half's 64 scores -> registers, partial row max (scale > 0 commutes with max),
+      // exchanged with the other half. After the exchange barrier nobody reads S_j from TMEM again,
+      // so P_j may overwrite any of its columns.
+      float sv[HC];
       float mx = -INFINITY;
 #pragma unroll
       for (int ch = 0; ch < HC / 32; ++ch) {
         uint32_t r[32];
         tmem_ld32_nowait(lane_base + b * 128 + half * HC + ch * 32, r);
         tmem_wait_ld();
-        if (!diag) {
 #pragma unroll
-          for (int t = 0; t < 32; ++t) mx = fmaxf(mx, __uint_as_float(r[t]));
-        } else {
-#pragma unroll
-          for (int t = 0; t < 32; ++t) mx = fmaxf(mx, ch * 32 + t < nvis ? __uint_as_float(r[t]) : -INFINITY);
+        for (int t = 0; t < 32; ++t) {
+          float x = __uint_as_float(r[t]);
+          if (diag && ch * 32 + t >= nvis) x = -INFINITY;
+          sv[ch * 32 + t] = x;
+          mx = fmaxf(mx, x);
         }
       }
       float* xm = xch + (j & 1) * 256;
@@ -221,38 +240,26 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       named_bar(1, 256);
       mx = fmaxf(mx, xm[(half ^ 1) * 128 + row]);
       const float m_new = fmaxf(m, mx * scale_log2);
-      if (j >= 1) mbar_wait(pfree, (j - 1) & 1);  // PV_{j-1} has finished reading the P tile
-      // pass 2: P = exp2(S * scale_log2 - m_new) -> bf16, this half's 64 keys of the swizzled P tile
+      // pass 2: P = exp2(S * scale_log2 - m_new) -> bf16, packed two per TMEM column in key order
       float rs = 0.f;
 #pragma unroll
       for (int ch = 0; ch < HC / 32; ++ch) {
-        uint32_t r[32];
-        tmem_ld32_nowait(lane_base + b * 128 + half * HC + ch * 32, r);
-        tmem_wait_ld();
         uint32_t pk[16];
 #pragma unroll
         for (int t = 0; t < 32; t += 2) {
-          float p0 = ex2(fmaf(__uint_as_float(r[t]), scale_log2, -m_new));
-          float p1 = ex2(fmaf(__uint_as_float(r[t + 1]), scale_log2, -m_new));
-          if (diag) {
-            p0 = ch * 32 + t < nvis ? p0 : 0.f;
-            p1 = ch * 32 + t + 1 < nvis ? p1 : 0.f;
-          }
+          const float p0 = ex2(fmaf(sv[ch * 32 + t], scale_log2, -m_new));
+          const float p1 = ex2(fmaf(sv[ch * 32 + t + 1], scale_log2, -m_new));
           rs += p0 + p1;
           __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
           pk[t >> 1] = *reinterpret_cast<uint32_t*>(&h);
         }
-        uint8_t* region = P + half * HALF;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int cc = ch * 4 + u;
-          *reinterpret_cast<uint4*>(region + swz(row, cc)) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-        }
+        // keys [half*64 + ch*32, +32) -> packed TMEM columns half*32 + ch*16 .. +16 of S buffer b
+        tmem_st16(lane_base + b * 128 + half * (HC / 2) + ch * 16, pk);
       }
+      tmem_wait_st();
       tc_fence_before();
-      fence_proxy_async();
       __syncwarp();
-      if (lane == 0) { mbar_arrive(sfree + b); mbar_arrive(pfull); }
+      if (lane == 0) mbar_arrive(pfull + b);
       lsum = lsum * ex2(m - m_new) + rs;  // partial (this half's keys), same m in both halves
       m_last = m;
       m = m_new;
