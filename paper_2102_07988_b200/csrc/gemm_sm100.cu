@@ -273,7 +273,7 @@ cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   ok = ok && (B_MN ? make_map(&tb, g.B, g.N, g.K, g.ldb, 64, 64) : make_map(&tb, g.B, g.K, g.N, g.ldb, 64, BN / CG));
   if (!ok) return cudaErrorInvalidValue;
   const int tiles = ((g.M + C::TILE_M - 1) / C::TILE_M) * ((g.N + BN - 1) / BN);
-  const int units = std::min(tiles, g_num_sms / CG);
+  const int units = g.persistent ? std::min(tiles, g_num_sms / CG) : tiles;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * CG);
   cfg.blockDim = dim3(192);

@@ -20,6 +20,7 @@ struct GemmDesc {
   const void* B = nullptr;
   int64_t ldb = 0;
   bool b_mn = false;  // false: B[n*ldb + k];  true: B[k*ldb + n]
+  bool persistent = true;  // false: one tile per CTA (lets higher-priority streams interleave)
 };
 
 template <typename T> cudaError_t gemm_simt(const GemmDesc& g, const Epi& e, cudaStream_t st);

@@ -225,6 +225,7 @@ class Engine final : public EngineBase {
   // NCCL (multi-rank)
   ncclComm_t base = nullptr, commF[2] = {nullptr, nullptr}, commB[2] = {nullptr, nullptr};
   cudaStream_t s_recv_f = nullptr, s_send_f = nullptr, s_recv_b = nullptr, s_send_b = nullptr;
+  cudaStream_t s_wgrad = nullptr;  // low priority: deferred weight gradients (multi-rank)
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_next = 0;
 
@@ -237,7 +238,7 @@ class Engine final : public EngineBase {
     for (void* p : allocs) cudaFree(p);
     if (h_loss) cudaFreeHost(h_loss);
     for (auto e : ev_pool) cudaEventDestroy(e);
-    for (cudaStream_t s : {s_recv_f, s_send_f, s_recv_b, s_send_b, stream})
+    for (cudaStream_t s : {s_recv_f, s_send_f, s_recv_b, s_send_b, s_wgrad, stream})
       if (s) cudaStreamDestroy(s);
   }
 
@@ -304,6 +305,7 @@ class Engine final : public EngineBase {
       CU(cudaStreamCreateWithPriority(&s_send_f, cudaStreamNonBlocking, hi));
       CU(cudaStreamCreateWithPriority(&s_recv_b, cudaStreamNonBlocking, hi));
       CU(cudaStreamCreateWithPriority(&s_send_b, cudaStreamNonBlocking, hi));
+      if (std::getenv("TP_NO_SIDE_DW") == nullptr) CU(cudaStreamCreateWithPriority(&s_wgrad, cudaStreamNonBlocking, lo));
     }
     CU(cudaStreamSynchronize(stream));
     return TP_OK;
@@ -418,13 +420,14 @@ class Engine final : public EngineBase {
   }
 
   // ------------------------------------------------------------ launch helpers
-  tp_status gemm(int cls, const GemmDesc& g, const Epi& e) {
+  tp_status gemm(int cls, const GemmDesc& g, const Epi& e, cudaStream_t st = nullptr) {
+    if (!st) st = stream;
     Pending p;
-    instr.begin(stream, cls, 2.0 * g.M * g.N * g.K, 0, p);
+    instr.begin(st, cls, 2.0 * g.M * g.N * g.K, 0, p);
     cudaError_t err;
-    if (!force_simt && std::is_same<T, bf16>::value && gemm_sm100_supported(g)) err = gemm_sm100(g, e, stream);
-    else err = gemm_simt<T>(g, e, stream);
-    instr.end(stream, p);
+    if (!force_simt && std::is_same<T, bf16>::value && gemm_sm100_supported(g)) err = gemm_sm100(g, e, st);
+    else err = gemm_simt<T>(g, e, st);
+    instr.end(st, p);
     if (err != cudaSuccess) return fail(TP_ECUDA, "gemm M=%d N=%d K=%d: %s", g.M, g.N, g.K, cudaGetErrorString(err));
     return TP_OK;
   }
@@ -631,32 +634,41 @@ class Engine final : public EngineBase {
   // One GEMM per weight over all B*s tokens of the step (K = B*s, both operands MN-major), written
   // once (the gradients start at zero), plus the bias column sums: off the per-job critical path and
   // with no fp32 read-modify-write.
-  tp_status wgrad(Stage<T>& S, int batch) {
+  tp_status wgrad(Stage<T>& S, int batch) { return wgrad_rows(S, 0, batch * m.s, false, stream, true); }
+
+  // Weight gradients over rows [row0, row0 + K) of the step (K = tokens), written (accum = false) or
+  // added; `persistent` = false launches one tile per CTA so a higher-priority stream interleaves.
+  tp_status wgrad_rows(Stage<T>& S, size_t row0, int K, bool accum, cudaStream_t st, bool persistent) {
     const int H = m.H, V = m.V;
-    const int K = batch * m.s;
     float* GR = S.gflat;
+    auto G = [&](int M_, int N_, const void* A_, int64_t lda, const void* B_, int64_t ldb) {
+      GemmDesc g = gd(M_, N_, K, A_, lda, true, B_, ldb, true);
+      g.persistent = persistent;
+      return g;
+    };
     for (int j = 0; j < S.nl; ++j) {
       const LayerOff& f = S.L.layers[j];
-      Epi e; e.kind = EPI_STORE; e.out_f32 = 1;
+      Epi e; e.kind = accum ? EPI_ACCUM : EPI_STORE; e.out_f32 = 1;
       e.out = GR + f.w_qkv; e.ldo = 3 * H;
-      TRY(gemm(KC_GEMM_DW, gd(H, 3 * H, K, S.A1[j], H, true, S.dQKV[j], 3 * H, true), e));
+      TRY(gemm(KC_GEMM_DW, G(H, 3 * H, S.A1[j] + row0 * H, H, S.dQKV[j] + row0 * 3 * H, 3 * H), e, st));
       e.out = GR + f.w_o; e.ldo = H;
-      TRY(gemm(KC_GEMM_DW, gd(H, H, K, S.O[j], H, true, S.dhmid_b[j], H, true), e));
+      TRY(gemm(KC_GEMM_DW, G(H, H, S.O[j] + row0 * H, H, S.dhmid_b[j] + row0 * H, H), e, st));
       e.out = GR + f.w_1; e.ldo = 4 * H;
-      TRY(gemm(KC_GEMM_DW, gd(H, 4 * H, K, S.A2[j], H, true, S.dU[j], 4 * H, true), e));
+      TRY(gemm(KC_GEMM_DW, G(H, 4 * H, S.A2[j] + row0 * H, H, S.dU[j] + row0 * 4 * H, 4 * H), e, st));
       e.out = GR + f.w_2; e.ldo = H;
-      TRY(gemm(KC_GEMM_DW, gd(4 * H, H, K, S.G[j], 4 * H, true, S.dhout_b[j], H, true), e));
-      TRY(launch(KC_MISC, 0, sizeof(T) * 9.0 * K * H, [&] {
-        cudaError_t r = colsum_accum<T>(S.dQKV[j], 3 * H, GR + f.b_qkv, K, 3 * H, stream);
-        if (r == cudaSuccess) r = colsum_accum<T>(S.dhmid_b[j], H, GR + f.b_o, K, H, stream);
-        if (r == cudaSuccess) r = colsum_accum<T>(S.dU[j], 4 * H, GR + f.b_1, K, 4 * H, stream);
-        if (r == cudaSuccess) r = colsum_accum<T>(S.dhout_b[j], H, GR + f.b_2, K, H, stream);
-        return r;
-      }));
+      TRY(gemm(KC_GEMM_DW, G(4 * H, H, S.G[j] + row0 * 4 * H, 4 * H, S.dhout_b[j] + row0 * H, H), e, st));
+      Pending p;
+      instr.begin(st, KC_MISC, 0, sizeof(T) * 9.0 * K * H, p);
+      cudaError_t r = colsum_accum<T>(S.dQKV[j] + row0 * 3 * H, 3 * H, GR + f.b_qkv, K, 3 * H, st);
+      if (r == cudaSuccess) r = colsum_accum<T>(S.dhmid_b[j] + row0 * H, H, GR + f.b_o, K, H, st);
+      if (r == cudaSuccess) r = colsum_accum<T>(S.dU[j] + row0 * 4 * H, 4 * H, GR + f.b_1, K, 4 * H, st);
+      if (r == cudaSuccess) r = colsum_accum<T>(S.dhout_b[j] + row0 * H, H, GR + f.b_2, K, H, st);
+      instr.end(st, p);
+      if (r != cudaSuccess) return fail(TP_ECUDA, "bias grads: %s", cudaGetErrorString(r));
     }
     if (S.k == m.K - 1) {
-      Epi e; e.kind = EPI_STORE; e.out_f32 = 1; e.out = GR + S.L.w_out; e.ldo = V;
-      TRY(gemm(KC_GEMM_DW, gd(H, V, K, S.Af, H, true, S.Z, V, true), e));
+      Epi e; e.kind = accum ? EPI_ACCUM : EPI_STORE; e.out_f32 = 1; e.out = GR + S.L.w_out; e.ldo = V;
+      TRY(gemm(KC_GEMM_DW, G(H, V, S.Af + row0 * H, H, S.Z + row0 * V, V), e, st));
     }
     return TP_OK;
   }
@@ -717,7 +729,11 @@ class Engine final : public EngineBase {
           TRY(fwd(S, d, off[i], lengths[i], b, batch));
           if (multi && S.k < m.K - 1) TRY(send_fwd(S, row, Tn));
         }
-    // backward: exact reverse order (GPipe order, A-21)
+    // backward: exact reverse order (GPipe order, A-21). With one stage per GPU and D >= 2 groups,
+    // group d's weight gradients go to a low-priority stream as soon as its last backward job is
+    // done (one tile per CTA, so the critical-path kernels interleave and the dW fills the pipeline
+    // bubbles); otherwise one K = B*s GEMM per weight at the end.
+    const bool side_dw = multi && D >= 2 && s_wgrad;
     for (int d = D - 1; d >= 0; --d) {
       for (int i = M - 1; i >= 0; --i)
         for (int si = (int)stages.size() - 1; si >= 0; --si) {
@@ -728,8 +744,20 @@ class Engine final : public EngineBase {
           TRY(bwd(S, d, off[i], lengths[i], b, batch, i == M - 1));
           if (multi && S.k > 0) TRY(send_bwd(S, row, Tn));
         }
+      if (side_dw) {
+        cudaEvent_t e = event();
+        CU(cudaEventRecord(e, stream));
+        CU(cudaStreamWaitEvent(s_wgrad, e, 0));
+        for (auto& S : stages) TRY(wgrad_rows(S, (size_t)d * b * m.s, b * m.s, d != D - 1, s_wgrad, false));
+      }
     }
-    for (auto& S : stages) TRY(wgrad(S, batch));
+    if (side_dw) {
+      cudaEvent_t e = event();
+      CU(cudaEventRecord(e, s_wgrad));
+      CU(cudaStreamWaitEvent(stream, e, 0));
+    } else {
+      for (auto& S : stages) TRY(wgrad(S, batch));
+    }
     // loss: sum of per-token NLL on the last stage, mean over batch*seq_len (A-9)
     Stage<T>* last = nullptr;
     for (auto& S : stages) if (S.k == m.K - 1) last = &S;

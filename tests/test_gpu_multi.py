@@ -29,6 +29,12 @@ def test_tiny_two_stages_nccl(precision, tol, tmp_path):
         assert max(errs.values()) < tol, errs
 
 
+def test_small_two_stages_nccl_side_stream_dw(tmp_path):
+    """D = B/b = 2 groups: the weight gradients of the first group run on the low-priority stream."""
+    for errs in run(2, "small", "bf16", "40,24,64", tmp_path):
+        assert max(errs.values()) < 2e-2, errs
+
+
 def test_small_four_stages_nccl(tmp_path):
     for errs in run(4, "small", "bf16", "40,24,64", tmp_path):
         assert max(errs.values()) < 2e-2, errs
