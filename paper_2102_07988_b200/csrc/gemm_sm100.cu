@@ -38,20 +38,26 @@ constexpr int BM = 128, BK = 64;
 //         tcgen05.mma.cta_group::2 (M = 256): each CTA stages its own 128 rows of A and half of
 //         the BN rows of B, the leader issues the MMAs over both CTAs' shared memory, and each
 //         CTA's TMEM receives its 128 rows — halving the per-SM L2->SMEM operand traffic.
+// 2 + 8 warps: TMA producer, MMA issuer, and 8 epilogue warps — two per TMEM lane quarter, each
+// draining half of the tile's columns (the fused epilogues are instruction-bound, 4 warps cannot
+// keep up with a 256-wide tile at K = 2048).
+constexpr int GEMM_THREADS = 320;
+
 template <int CG, int BN>
 struct Cfg {
   static constexpr uint32_t A_BYTES = BM * BK * 2;
   static constexpr uint32_t B_BYTES = (BN / CG) * BK * 2;
   static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
   static constexpr int NS = (196608 / STAGE) > 8 ? 8 : (196608 / STAGE);  // pipeline depth
-  static constexpr uint32_t EPI_SCRATCH = 4 * 32 * 33 * 4;  // per epilogue warp: 32 x 32 fp32 (+1 pad)
+  static constexpr uint32_t EPI_SCRATCH = 8 * 32 * 33 * 4;  // per epilogue warp: 32 x 32 fp32 (+1 pad)
   static constexpr uint32_t SMEM = NS * STAGE + EPI_SCRATCH + 1024 /*align slack*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = 2 * BN;  // double-buffered fp32 accumulator
   static constexpr int TILE_M = BM * CG;
+  static_assert(SMEM <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
 template <int CG, int BN, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                       int K, Epi epi) {
   using C = Cfg<CG, BN>;
@@ -73,7 +79,7 @@ __global__ void __launch_bounds__(192, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::NS; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, 4 * CG); }
+    for (int i = 0; i < 2; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, 8 * CG); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
@@ -176,7 +182,7 @@ __global__ void __launch_bounds__(192, 1)
       float* scr = epi_scratch + (warp - 2) * 32 * 33;
       const bool has_aux = epi.kind == EPI_RESID || epi.kind == EPI_DGELU;
 #pragma unroll 1
-      for (int ch = 0; ch < BN / 32; ++ch) {
+      for (int ch = ((warp - 2) >> 2) * (BN / 64); ch < (((warp - 2) >> 2) + 1) * (BN / 64); ++ch) {
         const int n = n0 + ch * 32 + (lane & 3) * 8;
         // issue this chunk's residual / U loads first: 4 independent 32-byte loads in flight per thread
         float aux[4][8];
@@ -276,7 +282,7 @@ cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   const int units = g.persistent ? std::min(tiles, g_num_sms / CG) : tiles;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * CG);
-  cfg.blockDim = dim3(192);
+  cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
