@@ -254,7 +254,13 @@ def main():
         ctx.step_device(main_sl, tok_dev.data_ptr(), B)
     clocks = ClockSampler(local_rank)
     clocks.start()
+    # TP_PROFILE_RANGE=1 limits an `ncu --profile-from-start off` capture to the timed device region
+    prof_range = os.environ.get("TP_PROFILE_RANGE") == "1"
+    if prof_range:
+        torch.cuda.profiler.start()
     ms, loss = timed(main_sl, args.steps)
+    if prof_range:
+        torch.cuda.profiler.stop()
     clk = clocks.stop()
     launches = allsum(ctx.last_step_launches()) * args.steps
     # e2e through the public API with host tokens (pinned) and the loss read back every step

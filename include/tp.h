@@ -177,7 +177,9 @@ tp_status tp_kernel_stats_reset(tp_ctx* ctx);
 /* Turns the per-launch CUDA-event bracketing of TP_FLAG_KERNEL_STATS on (1) or off (0). */
 tp_status tp_kernel_stats_enable(tp_ctx* ctx, int32_t on);
 
-/* Number of kernel launches issued by the last tp_step (device work only, this context). */
+/* Number of kernel launches issued by the last tp_step on this context. For a step replayed from
+ * the CUDA graph this is the number of kernel nodes in the captured graph (every launch, NCCL p2p
+ * kernels included); for an eager step it counts the instrumented launches only. */
 tp_status tp_last_step_launches(tp_ctx* ctx, int64_t* out);
 
 void tp_destroy(tp_ctx* ctx);

@@ -822,10 +822,21 @@ class Engine final : public EngineBase {
       cudaError_t ce = cudaStreamEndCapture(stream, &graph);
       if (st != TP_OK) { if (graph) cudaGraphDestroy(graph); return st; }
       if (ce != cudaSuccess) return fail(TP_ECUDA, "graph capture: %s", cudaGetErrorString(ce));
+      // launch count of a replayed step = the kernel nodes of the captured graph (includes the
+      // launches made inside helpers that bypass the instrumentation, e.g. colsum / dkv_finalize)
+      size_t nn = 0;
+      cudaGraphGetNodes(graph, nullptr, &nn);
+      std::vector<cudaGraphNode_t> nodes(nn);
+      int64_t kn = 0;
+      if (nn && cudaGraphGetNodes(graph, nodes.data(), &nn) == cudaSuccess)
+        for (auto nd : nodes) {
+          cudaGraphNodeType t;
+          if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++kn;
+        }
       ce = cudaGraphInstantiate(&g_exec, graph, 0);
       cudaGraphDestroy(graph);
       if (ce != cudaSuccess) { g_exec = nullptr; return fail(TP_ECUDA, "graph instantiate: %s", cudaGetErrorString(ce)); }
-      g_launches = instr.launches;
+      g_launches = kn;
       CU(cudaGraphLaunch(g_exec, stream));
     } else {
       if (g_exec) { cudaGraphExecDestroy(g_exec); g_exec = nullptr; }
