@@ -139,8 +139,12 @@ __global__ void __launch_bounds__(WARPS * 32) attn_bwd_dkv_kernel(const T* __res
 // dQKV[r][H + i] = dK_acc[head][c + r][e], dQKV[r][2H + i] = dV_acc[...] (i = head*d + e), 8-wide.
 template <typename T>
 __global__ void dkv_finalize_kernel(const float* __restrict__ dk_acc, const float* __restrict__ dv_acc,
-                                    T* __restrict__ dqkv, int64_t ld, int a, int s, int d, int c) {
+                                    T* __restrict__ dqkv, int64_t ld, int a, int s, int d, int c,
+                                    int64_t acc_sstride, int64_t out_sstride) {
   const int r = blockIdx.x;
+  dk_acc += blockIdx.y * acc_sstride;
+  dv_acc += blockIdx.y * acc_sstride;
+  dqkv += blockIdx.y * out_sstride;
   const int H = a * d;
   for (int i = threadIdx.x * 8; i < H; i += blockDim.x * 8) {
     const int head = i / d, e = i - head * d;
@@ -177,9 +181,9 @@ cudaError_t attn_bwd_simt(const T* dO, int64_t ld_do, const T* o, int64_t ldo, c
 
 template <typename T>
 cudaError_t attn_dkv_finalize(const float* dk_acc, const float* dv_acc, T* dqkv, int64_t ld, int a, int s, int d,
-                              int c, int l, cudaStream_t st) {
-  if (l == 0) return cudaSuccess;
-  dkv_finalize_kernel<T><<<l, 256, 0, st>>>(dk_acc, dv_acc, dqkv, ld, a, s, d, c);
+                              int c, int l, cudaStream_t st, int nseq, int64_t acc_sstride, int64_t out_sstride) {
+  if (l == 0 || nseq == 0) return cudaSuccess;
+  dkv_finalize_kernel<T><<<dim3(l, nseq), 256, 0, st>>>(dk_acc, dv_acc, dqkv, ld, a, s, d, c, acc_sstride, out_sstride);
   return cudaGetLastError();
 }
 
@@ -190,7 +194,7 @@ cudaError_t attn_dkv_finalize(const float* dk_acc, const float* dv_acc, T* dqkv,
                                         const float*, float*, T*, int64_t, float*, float*, int, int, int, int, int, int, \
                                         cudaStream_t);                                                          \
   template cudaError_t attn_dkv_finalize<T>(const float*, const float*, T*, int64_t, int, int, int, int, int,       \
-                                            cudaStream_t);
+                                            cudaStream_t, int, int64_t, int64_t);
 TP_INST(float)
 TP_INST(bf16)
 #undef TP_INST

@@ -293,26 +293,34 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 }
 
 // ======================================================================== backward
-// Per (128-key block of the prefix [0, c+l), head); loop over the slice's 64-query tiles that can
-// see the block. TMEM: S^T [128 keys x 64 q] (cols 0-63), dP^T (64-127), dV (128-255),
-// dK (256-383), dQ^T [128 d x 64 q] (384-447).
+// Per (128-key block of the prefix [0, c+l), head, sequence); loop over the slice's 64-query tiles
+// that can see the block. The tile loop is software-pipelined so the tensor pipe never waits for
+// the softmax-gradient warps: S^T / dP^T of tile i+1 are computed while tile i is in the softmax.
+// TMEM (512 columns):
+//   buffer b = i & 1 at b*128: S^T [128 keys x 64 q] (cols 0-63) then P^T (bf16, packed over the S
+//   columns), dP^T (cols 64-127) then dQ^T [128 d x 64 q] of the same tile;
+//   dV at 256, dK at 384 (fp32 [128 keys x 128 d], accumulated over the tiles).
 //   S^T = K Q^T, dP^T = V dO^T                                  (M=128 keys, N=64, K=d)
-//   softmax warps (thread = key row): P^T = exp2(S^T scale - lse), dS^T = P^T (dP^T - D) -> smem
-//   dV += P^T dO, dK += dS^T Q                                  (M=128 keys, N=d, K=64; Q/dO as MN-major B)
+//   softmax warps (thread = key row): P^T = exp2(S^T scale - lse) -> TMEM, dS^T = P^T (dP^T - D) -> smem
+//   dV += P^T dO  (A = P^T from TMEM), dK += dS^T Q             (M=128 keys, N=d, K=64; Q/dO MN-major B)
 //   dQ^T = K^T dS^T                                             (M=d, N=64 q, K=128 keys; K as MN-major A)
-//   dQ^T is drained by the softmax warps with coalesced fp32 reductions into dq_acc[l][H];
-//   dK (x scale) / dV are written or added to the fp32 prefix accumulators once per key row.
+//   dQ^T is drained by the softmax warps into shared memory and added to dq_acc[l][H] by one TMA
+//   reduce-add per tile; dK (x scale) / dV are written or added to the fp32 prefix accumulators once.
+// Shared memory: K, V (32 KiB each), a 3-deep Q / dO ring (16 KiB tiles), dS^T double-buffered,
+// the fp32 dQ staging tile.
 constexpr int BQB = 64;                          // query rows per tile (backward)
 constexpr uint32_t QT = BQB * AT * 2;            // 16 KiB: [64 q][128 d]
 constexpr uint32_t QHALF = QT / 2;               // 8 KiB: second 64-column atom
 constexpr uint32_t PT = AT * BQB * 2;            // 16 KiB: [128 keys][64 q] (one atom wide)
+constexpr int NQB = 3;                           // Q / dO ring depth
 
 struct BwdSmem {
-  static constexpr uint32_t K = 0, V = TILE, Q0 = 2 * TILE, Q1 = Q0 + QT, O0 = Q1 + QT, O1 = O0 + QT;
-  static constexpr uint32_t P = O1 + QT, DS = P + PT, DQ = DS + PT /* fp32 [64 q][128 d] */;
-  static constexpr uint32_t LD = DQ + 32768; /* fp32 [2 tiles][lse*log2e[64], D[64]] */
+  static constexpr uint32_t K = 0, V = TILE, Q = 2 * TILE, O = Q + NQB * QT, DS = O + NQB * QT;
+  static constexpr uint32_t DQ = DS + 2 * PT;  // fp32 [64 q][128 d]
+  static constexpr uint32_t LD = DQ + 32768;   // fp32 [2 tiles][lse*log2e[64], D[64]]
   static constexpr uint32_t BAR = LD + 1024;
   static constexpr uint32_t BYTES = BAR + 256 + 1024;
+  static_assert(BYTES <= 232448, "backward tile set exceeds 227 KB of shared memory");
 };
 
 __global__ void __launch_bounds__(FWD_THREADS, 1)
@@ -320,30 +328,30 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
                           const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                           const __grid_constant__ CUtensorMap tmdQ, const float* __restrict__ lse,
                           const float* __restrict__ Dvec, int64_t lse_sstride, int64_t dkv_sstride, float* __restrict__ dk_acc, float* __restrict__ dv_acc, int s, int c, int l,
-                          float scale, float scale_log2, int accumulate, volatile int* dbg) {
+                          float scale, float scale_log2, int accumulate, int nheads, volatile int* dbg) {
   extern __shared__ uint8_t smem_raw[];
 #define DBG(role, v)                                                                    \
   do {                                                                                  \
-    if (dbg) { dbg[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 8 + (role)] = (v); __threadfence_system(); } \
+    if (dbg) { dbg[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + (role)] = (v); __threadfence_system(); } \
   } while (0)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + BwdSmem::BAR);
   uint64_t* kvfull = bars + 0;
-  uint64_t* qfull = bars + 1;    // [2]
-  uint64_t* qfree = bars + 3;    // [2]
-  uint64_t* sfull = bars + 5;
-  uint64_t* sfree = bars + 6;
-  uint64_t* pfull = bars + 7;
-  uint64_t* pfree = bars + 8;
-  uint64_t* dqfull = bars + 9;
-  uint64_t* dqfree = bars + 10;
-  uint64_t* done = bars + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* qfull = bars + 1;    // [3] Q / dO tile landed
+  uint64_t* qfree = bars + 4;    // [3] dV / dK MMAs of the tile done (Q, dO, P^T consumed)
+  uint64_t* sfull = bars + 7;    // [2] S^T, dP^T in TMEM buffer
+  uint64_t* pfull = bars + 9;    // [2] P^T in TMEM, dS^T in smem (8 warps)
+  uint64_t* dsfree = bars + 11;  // [2] dK / dQ MMAs done reading dS^T
+  uint64_t* dqfull = bars + 13;  // [2] dQ^T in TMEM
+  uint64_t* dqfree = bars + 15;  // [2] dQ^T drained (8 warps)
+  uint64_t* done = bars + 17;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int head = blockIdx.y, key0 = blockIdx.x * AT, sq = blockIdx.z;  // sequence of the job
+  // heaviest key blocks (the most query tiles) first: blockIdx.y is the key block
+  const int head = blockIdx.x % nheads, sq = blockIdx.x / nheads, key0 = blockIdx.y * AT;
   lse += sq * lse_sstride;
-  Dvec += (int64_t)sq * gridDim.y * l;
+  Dvec += (int64_t)sq * nheads * l;
   dk_acc += sq * dkv_sstride;
   dv_acc += sq * dkv_sstride;
   const int nkeys = c + l;
@@ -352,36 +360,35 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(kvfull, 1);
-    for (int i = 0; i < 2; ++i) { mbar_init(qfull + i, 1); mbar_init(qfree + i, 1); }
-    mbar_init(sfull, 1); mbar_init(sfree, 8);
-    mbar_init(pfull, 8); mbar_init(pfree, 1);
-    mbar_init(dqfull, 1); mbar_init(dqfree, 8);
+    for (int i = 0; i < NQB; ++i) { mbar_init(qfull + i, 1); mbar_init(qfree + i, 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(sfull + i, 1); mbar_init(pfull + i, 8); mbar_init(dsfree + i, 1);
+      mbar_init(dqfull + i, 1); mbar_init(dqfree + i, 8);
+    }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (threadIdx.x == 0) DBG(7, 1);
   if (warp == 0) tmem_alloc(tmem_slot, 512);
-  if (threadIdx.x == 0) DBG(7, 2);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) DBG(6, ntile);
-  constexpr uint32_t T_S = 0, T_DP = 64, T_DV = 128, T_DK = 256, T_DQ = 384;
+  constexpr uint32_t T_DV = 256, T_DK = 384;
 
   if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer: K, V once; Q_i, dO_i double-buffered
+    // ---------------- TMA producer: K, V once; Q_i, dO_i through the 3-deep ring
     mbar_expect_tx(kvfull, 2 * TILE);
     tma_load_4d(sm + BwdSmem::K, &tmK, 0, key0, head, sq, kvfull);
     tma_load_4d(sm + BwdSmem::K + HALF, &tmK, 64, key0, head, sq, kvfull);
     tma_load_4d(sm + BwdSmem::V, &tmV, 0, key0, head, sq, kvfull);
     tma_load_4d(sm + BwdSmem::V + HALF, &tmV, 64, key0, head, sq, kvfull);
     for (int i = 0; i < ntile; ++i) {
-      const int b = i & 1, qt = qt0 + i;
+      const int b = i % NQB, qt = qt0 + i;
       DBG(0, 100 + i);
-      if (i >= 2) mbar_wait(qfree + b, ((i >> 1) - 1) & 1);
-      uint8_t* qd = sm + (b ? BwdSmem::Q1 : BwdSmem::Q0);
-      uint8_t* od = sm + (b ? BwdSmem::O1 : BwdSmem::O0);
+      if (i >= NQB) mbar_wait(qfree + b, ((i / NQB) - 1) & 1);
+      uint8_t* qd = sm + BwdSmem::Q + b * QT;
+      uint8_t* od = sm + BwdSmem::O + b * QT;
       mbar_expect_tx(qfull + b, 2 * QT);
       tma_load_4d(qd, &tmQ, 0, c + qt * BQB, head, sq, qfull + b);
       tma_load_4d(qd + QHALF, &tmQ, 64, c + qt * BQB, head, sq, qfull + b);
@@ -391,48 +398,60 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer
     constexpr uint32_t idS = idesc_bf16(128, BQB, false, false);   // S^T, dP^T
-    constexpr uint32_t idKV = idesc_bf16(128, 128, false, true);   // dV, dK (B = dO / Q, MN-major)
+    constexpr uint32_t idKV = idesc_bf16(128, 128, false, true);   // dV (A = P^T in TMEM), dK (B = dO / Q, MN-major)
     constexpr uint32_t idQ = idesc_bf16(128, BQB, true, true);     // dQ^T (A = K MN-major, B = dS^T MN-major)
     const uint32_t k_base = smem_u32(sm + BwdSmem::K), v_base = smem_u32(sm + BwdSmem::V);
-    const uint32_t p_base = smem_u32(sm + BwdSmem::P), ds_base = smem_u32(sm + BwdSmem::DS);
     mbar_wait(kvfull, 0);
-    for (int i = 0; i < ntile; ++i) {
-      const int b = i & 1;
-      const uint32_t q_base = smem_u32(sm + (b ? BwdSmem::Q1 : BwdSmem::Q0));
-      const uint32_t o_base = smem_u32(sm + (b ? BwdSmem::O1 : BwdSmem::O0));
-      DBG(1, 100 + 10 * i);
-      mbar_wait(qfull + b, (i >> 1) & 1);
-      DBG(1, 101 + 10 * i);
-      if (i >= 1) mbar_wait(sfree, (i - 1) & 1);
-      DBG(1, 102 + 10 * i);
+    // S^T / dP^T of tile j into TMEM buffer j & 1
+    auto issue_sdp = [&](int j) {
+      const int bq = j % NQB, bb = j & 1;
+      const uint32_t q_base = smem_u32(sm + BwdSmem::Q + bq * QT), o_base = smem_u32(sm + BwdSmem::O + bq * QT);
+      const uint32_t tb = tmem + bb * 128;
+      mbar_wait(qfull + bq, (j / NQB) & 1);
+      // buffer bb last held tile j-2: its S^T was read by the softmax (pfull(j-2), waited before
+      // the MMAs of j-2), its P^T by dV(j-2) (qfree(j-2)), its dQ^T by the drain (dqfree(j-2))
+      if (j >= 2) mbar_wait(qfree + (j - 2) % NQB, ((j - 2) / NQB) & 1);
       tc_fence_after();
 #pragma unroll
       for (int kk = 0; kk < AT / 16; ++kk) {
         const uint32_t ok = (kk >> 2) * HALF + (kk & 3) * 32, oq = (kk >> 2) * QHALF + (kk & 3) * 32;
-        mma_bf16(tmem + T_S, make_desc(k_base + ok, 16, 1024), make_desc(q_base + oq, 16, 1024), idS, kk > 0);
-        mma_bf16(tmem + T_DP, make_desc(v_base + ok, 16, 1024), make_desc(o_base + oq, 16, 1024), idS, kk > 0);
+        mma_bf16(tb, make_desc(k_base + ok, 16, 1024), make_desc(q_base + oq, 16, 1024), idS, kk > 0);
       }
-      mma_commit(sfull);
-      DBG(1, 103 + 10 * i);
-      mbar_wait(pfull, i & 1);
-      DBG(1, 104 + 10 * i);
+      if (j >= 2) mbar_wait(dqfree + bb, ((j >> 1) - 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < AT / 16; ++kk) {
+        const uint32_t ok = (kk >> 2) * HALF + (kk & 3) * 32, oq = (kk >> 2) * QHALF + (kk & 3) * 32;
+        mma_bf16(tb + 64, make_desc(v_base + ok, 16, 1024), make_desc(o_base + oq, 16, 1024), idS, kk > 0);
+      }
+      mma_commit(sfull + bb);
+    };
+    issue_sdp(0);
+    for (int i = 0; i < ntile; ++i) {
+      const int bq = i % NQB, bb = i & 1;
+      const uint32_t q_base = smem_u32(sm + BwdSmem::Q + bq * QT), o_base = smem_u32(sm + BwdSmem::O + bq * QT);
+      const uint32_t ds_base = smem_u32(sm + BwdSmem::DS + bb * PT);
+      const uint32_t tb = tmem + bb * 128;
+      DBG(1, 100 + 10 * i);
+      if (i + 1 < ntile) issue_sdp(i + 1);
+      DBG(1, 101 + 10 * i);
+      mbar_wait(pfull + bb, (i >> 1) & 1);
       tc_fence_after();
 #pragma unroll
       for (int kk = 0; kk < BQB / 16; ++kk) {
-        mma_bf16(tmem + T_DV, make_desc(p_base + kk * 32, 16, 1024), make_desc(o_base + kk * 2048, QHALF, 1024), idKV,
-                 (i | kk) != 0);
+        // P^T columns: query half h = kk >> 1 was packed at h*32 .. h*32+15 of the S^T columns
+        mma_bf16_ts(tmem + T_DV, tb + (kk >> 1) * 32 + (kk & 1) * 8, make_desc(o_base + kk * 2048, QHALF, 1024), idKV,
+                    (i | kk) != 0);
         mma_bf16(tmem + T_DK, make_desc(ds_base + kk * 32, 16, 1024), make_desc(q_base + kk * 2048, QHALF, 1024), idKV,
                  (i | kk) != 0);
       }
-      if (i >= 1) mbar_wait(dqfree, (i - 1) & 1);
-      tc_fence_after();
+      mma_commit(qfree + bq);
 #pragma unroll
       for (int kk = 0; kk < AT / 16; ++kk)
-        mma_bf16(tmem + T_DQ, make_desc(k_base + kk * 2048, HALF, 1024), make_desc(ds_base + kk * 2048, 8192, 1024), idQ,
+        mma_bf16(tb + 64, make_desc(k_base + kk * 2048, HALF, 1024), make_desc(ds_base + kk * 2048, 8192, 1024), idQ,
                  kk > 0);
-      mma_commit(dqfull);
-      mma_commit(pfree);
-      mma_commit(qfree + b);
+      mma_commit(dqfull + bb);
+      mma_commit(dsfree + bb);
       DBG(1, 105 + 10 * i);
     }
     mma_commit(done);
@@ -443,35 +462,35 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     const int q = warp & 3, row = q * 32 + lane, half = (warp - 2) >> 2;
     const int kabs = key0 + row;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    uint8_t* Pt = sm + BwdSmem::P;
-    uint8_t* dSt = sm + BwdSmem::DS;
     const float* lse_h = lse + (int64_t)head * s + c;
     const float* D_h = Dvec + (int64_t)head * l;
     float* dqs = reinterpret_cast<float*>(sm + BwdSmem::DQ);
     constexpr int HQ = BQB / 2;  // query columns per half
-    // dQ^T of tile i (thread = head-dim index `row`) -> smem [64 q][128 d] -> one TMA reduce-add
-    auto drain_dq = [&](int i) {
-      mbar_wait(dqfull, i & 1);
+    // dQ^T of tile j (thread = head-dim index `row`) -> smem [64 q][128 d] -> one TMA reduce-add
+    auto drain_dq = [&](int j) {
+      const int bb = j & 1;
+      mbar_wait(dqfull + bb, (j >> 1) & 1);
       tc_fence_after();
       if (threadIdx.x == 64) tma_wait_reads();  // previous reduce has finished reading the buffer
       named_bar(1, 256);
       {
         uint32_t r[32];
-        tmem_ld32_nowait(lane_base + T_DQ + half * HQ, r);
+        tmem_ld32_nowait(lane_base + bb * 128 + 64 + half * HQ, r);
         tmem_wait_ld();
 #pragma unroll
         for (int t = 0; t < 32; ++t) dqs[(half * HQ + t) * AT + row] = __uint_as_float(r[t]) * scale;
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(dqfree);
+      if (lane == 0) mbar_arrive(dqfree + bb);
       fence_proxy_async();
       named_bar(1, 256);
-      if (threadIdx.x == 64) tma_reduce_add_3d(&tmdQ, dqs, head * AT, (qt0 + i) * BQB, sq);
+      if (threadIdx.x == 64) tma_reduce_add_3d(&tmdQ, dqs, head * AT, (qt0 + j) * BQB, sq);
     };
     for (int i = 0; i < ntile; ++i) {
+      const int bb = i & 1;
       const int qrow0 = (qt0 + i) * BQB;
-      float* Ls = reinterpret_cast<float*>(sm + BwdSmem::LD) + (i & 1) * 2 * BQB;  // double-buffered by tile
+      float* Ls = reinterpret_cast<float*>(sm + BwdSmem::LD) + bb * 2 * BQB;  // double-buffered by tile
       float* Ds = Ls + BQB;
       if (lane == 0) DBG(2 + q, 100 + 10 * i);
       {  // stage lse*log2e and D of this tile's 64 queries (rows past the slice: +inf / 0)
@@ -480,17 +499,15 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         else if (t < 128) Ds[t - 64] = qr < l ? __ldg(D_h + qr) : 0.f;
       }
       named_bar(1, 256);
-      mbar_wait(sfull, i & 1);
-      if (lane == 0) DBG(2 + q, 101 + 10 * i);
+      mbar_wait(sfull + bb, (i >> 1) & 1);
+      if (i >= 2) mbar_wait(dsfree + bb, ((i >> 1) - 1) & 1);  // dK / dQ MMAs of tile i-2 read dS^T buffer bb
       tc_fence_after();
-      if (i >= 1) mbar_wait(pfree, (i - 1) & 1);  // MMAs of tile i-1 have read P^T / dS^T
       // visible iff c + qr >= kabs (and qr < l, which Ls = +inf enforces)
       const int vis0 = kabs - c - qrow0;  // first visible column of this key row
       {
-        const int ch = half;
         uint32_t rs[32], rp[32];
-        tmem_ld32_nowait(lane_base + T_S + ch * 32, rs);
-        tmem_ld32_nowait(lane_base + T_DP + ch * 32, rp);
+        tmem_ld32_nowait(lane_base + bb * 128 + half * HQ, rs);
+        tmem_ld32_nowait(lane_base + bb * 128 + 64 + half * HQ, rp);
         tmem_wait_ld();
         uint32_t pk[16], dk[16];
 #pragma unroll
@@ -498,7 +515,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           float pv[2], dv[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int col = ch * 32 + t + e;
+            const int col = half * HQ + t + e;
             float p = ex2(fmaf(__uint_as_float(rs[t + e]), scale_log2, -Ls[col]));
             p = col >= vis0 ? p : 0.f;
             pv[e] = p;
@@ -509,17 +526,20 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           pk[t >> 1] = *reinterpret_cast<uint32_t*>(&hp);
           dk[t >> 1] = *reinterpret_cast<uint32_t*>(&hd);
         }
+        // P^T (this half's 32 queries) packed into the first 16 of this half's own S^T columns
+        tmem_st16(lane_base + bb * 128 + half * HQ, pk);
+        uint8_t* dSt = sm + BwdSmem::DS + bb * PT;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int cc = ch * 4 + u;
-          *reinterpret_cast<uint4*>(Pt + swz(row, cc)) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          const int cc = half * 4 + u;
           *reinterpret_cast<uint4*>(dSt + swz(row, cc)) = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
         }
       }
+      tmem_wait_st();
       tc_fence_before();
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) { mbar_arrive(sfree); mbar_arrive(pfull); }
+      if (lane == 0) mbar_arrive(pfull + bb);
       if (i >= 1) drain_dq(i - 1);
     }
     drain_dq(ntile - 1);
@@ -645,7 +665,7 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
       !encode_f32_map_noswizzle(&mdq, dq_acc, 3, qdims, qstr, qrbox))
     return cudaErrorInvalidValue;
   const float scale = rsqrtf((float)d);
-  dim3 grid((c + l + AT - 1) / AT, a, nseq);
+  dim3 grid(a * nseq, (c + l + AT - 1) / AT);
   static int* dbg = nullptr;
   static bool dbg_on = getenv("TP_ATTN_DEBUG") != nullptr;
   if (dbg_on && !dbg) {
@@ -655,13 +675,13 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
   if (dbg_on) { memset(dbg, 0, 4096 * sizeof(int)); cudaHostGetDevicePointer(&dbg_dev, dbg, 0); }
   attn_bwd_sm100_kernel<<<grid, FWD_THREADS, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, mdq, lse, Dvec, lse_sstride, dkv_sstride,
                                                            dk_acc, dv_acc, s, c, l, scale, scale * LOG2E_F, accumulate,
-                                                           dbg_dev);
+                                                           a, dbg_dev);
   e = cudaGetLastError();
   if (dbg_on) {
     for (int it = 0; it < 50 && cudaStreamQuery(st) == cudaErrorNotReady; ++it) usleep(100000);
     if (cudaStreamQuery(st) == cudaErrorNotReady) {
       fprintf(stderr, "attn_bwd_sm100 HUNG: grid %d x %d, c=%d l=%d\n", grid.x, grid.y, c, l);
-      for (unsigned b = 0; b < grid.x * grid.y * grid.z && b < 500; ++b) {
+      for (unsigned b = 0; b < grid.x * grid.y && b < 500; ++b) {
         fprintf(stderr, " cta %u:", b);
         for (int r = 0; r < 8; ++r) fprintf(stderr, " %d", ((volatile int*)dbg)[b * 8 + r]);
         fprintf(stderr, "\n");

@@ -80,7 +80,8 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
                            int64_t lse_sstride = 0, int64_t dq_sstride = 0, int64_t dkv_sstride = 0);
 template <typename T>
 cudaError_t attn_dkv_finalize(const float* dk_acc, const float* dv_acc, T* dqkv, int64_t ld, int a,
-                              int s, int d, int c, int l, cudaStream_t st);
+                              int s, int d, int c, int l, cudaStream_t st, int nseq = 1, int64_t acc_sstride = 0,
+                              int64_t out_sstride = 0);
 
 template <typename T> cudaError_t convert_f32(const float* src, T* dst, int64_t n, cudaStream_t st);
 template <typename T>

@@ -580,9 +580,9 @@ class Engine final : public EngineBase {
                                            S.Kc[j] + seq0 * s * H, S.Vc[j] + seq0 * s * H, S.LSE[j] + seq0 * a * s, S.Dvec,
                                            S.dqacc, dq, (int64_t)b * 3 * H, S.dk_acc[j], S.dv_acc[j], a, s, dh, c, l, accum,
                                            stream, b, (int64_t)s * H, H, (int64_t)a * s, 3 * H, (int64_t)s * H);
-            for (int jj = 0; jj < b && e == cudaSuccess; ++jj)
-              e = attn_dkv_finalize<T>(S.dk_acc[j] + (size_t)jj * s * H, S.dv_acc[j] + (size_t)jj * s * H,
-                                       dq + (size_t)jj * 3 * H, (int64_t)b * 3 * H, a, s, dh, c, l, stream);
+            if (e == cudaSuccess)
+              e = attn_dkv_finalize<T>(S.dk_acc[j], S.dv_acc[j], dq, (int64_t)b * 3 * H, a, s, dh, c, l, stream, b,
+                                       (int64_t)s * H, 3 * H);
             return e;
           }
         for (int jj = 0; jj < b; ++jj) {

@@ -148,7 +148,10 @@ def test_graph_replay_identical():
         outs.append((ctx.step(sl, tokens), ctx.grads(), ctx.last_step_launches()))
         for loss, g, n in outs[1:]:
             assert abs(loss - outs[0][0]) <= 1e-6 * abs(outs[0][0])
-            assert rel(g, outs[0][1]) < 1e-6 and n == outs[0][2] > 0
+            assert rel(g, outs[0][1]) < 1e-6
+        # eager steps count the instrumented launches, captured / replayed steps the graph's kernel
+        # nodes (every launch): the replays agree, and the eager count is a lower bound
+        assert outs[1][2] == outs[2][2] and 0 < outs[0][2] <= outs[1][2]
         assert abs(outs[0][0] - ref["loss"]) < 2e-2 * abs(ref["loss"])
     finally:
         ctx.close()
