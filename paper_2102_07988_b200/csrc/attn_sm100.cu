@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int head = blockIdx.y, r0 = blockIdx.x * AT, sq = blockIdx.z;  // sequence of the job
+  // heaviest query tiles (the most key blocks) first: LPT order over the whole grid
+  const int head = blockIdx.x, sq = blockIdx.y, r0 = (gridDim.z - 1 - blockIdx.z) * AT;
   o += sq * o_sstride;
   lse += sq * lse_sstride;
   const int qlast = c + min(l, r0 + AT) - 1;
@@ -326,8 +327,9 @@ struct BwdSmem {
 __global__ void __launch_bounds__(FWD_THREADS, 1)
     attn_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                           const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
-                          const __grid_constant__ CUtensorMap tmdQ, const float* __restrict__ lse,
-                          const float* __restrict__ Dvec, int64_t lse_sstride, int64_t dkv_sstride, float* __restrict__ dk_acc, float* __restrict__ dv_acc, int s, int c, int l,
+                          const __grid_constant__ CUtensorMap tmdQ, const __grid_constant__ CUtensorMap tmdK,
+                          const __grid_constant__ CUtensorMap tmdV, const float* __restrict__ lse,
+                          const float* __restrict__ Dvec, int64_t lse_sstride, int s, int c, int l,
                           float scale, float scale_log2, int accumulate, int nheads, volatile int* dbg) {
   extern __shared__ uint8_t smem_raw[];
 #define DBG(role, v)                                                                    \
@@ -352,9 +354,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   const int head = blockIdx.x % nheads, sq = blockIdx.x / nheads, key0 = blockIdx.y * AT;
   lse += sq * lse_sstride;
   Dvec += (int64_t)sq * nheads * l;
-  dk_acc += sq * dkv_sstride;
-  dv_acc += sq * dkv_sstride;
-  const int nkeys = c + l;
   const int qt0 = max(0, key0 - c) / BQB, nqt = (l + BQB - 1) / BQB;
   const int ntile = nqt - qt0;  // >= 1 because key0 < c + l
 
@@ -545,13 +544,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     drain_dq(ntile - 1);
     if (threadIdx.x == 64) tma_wait_all();
     if (lane == 0) DBG(2 + q, 900);
-    // dK (x scale) and dV rows of this key block, head-dim half -> fp32 prefix accumulators
+    // dK (x scale) and dV of this key block -> 128B-swizzled fp32 staging over the (now idle) Q / dO
+    // ring and dS^T buffers: [dK | dV][4 column chunks of 32 d][128 keys][32] -> 8 TMA stores (first
+    // slice) or reduce-adds (later slices) into the prefix accumulators; key rows past the prefix
+    // are clipped by the tensor map.
     mbar_wait(done, 0);
     tc_fence_after();
-    // (tcgen05.ld is warp-collective: every lane loads, only rows inside the prefix store)
-    const bool store = kabs < nkeys;
-    float* dkr = dk_acc + ((int64_t)head * s + kabs) * AT;
-    float* dvr = dv_acc + ((int64_t)head * s + kabs) * AT;
+    float* stg = reinterpret_cast<float*>(sm + BwdSmem::Q);
 #pragma unroll
     for (int cq = 0; cq < 2; ++cq) {
       const int ch = half * 2 + cq;
@@ -559,24 +558,33 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       tmem_ld32_nowait(lane_base + T_DK + ch * 32, rk);
       tmem_ld32_nowait(lane_base + T_DV + ch * 32, rv);
       tmem_wait_ld();
-      if (store) {
+      uint8_t* bk = reinterpret_cast<uint8_t*>(stg + ch * 4096) + row * 128;
+      uint8_t* bv = reinterpret_cast<uint8_t*>(stg + 16384 + ch * 4096) + row * 128;
 #pragma unroll
-        for (int t = 0; t < 32; t += 4) {
-          float4 nk = make_float4(__uint_as_float(rk[t]) * scale, __uint_as_float(rk[t + 1]) * scale,
-                                  __uint_as_float(rk[t + 2]) * scale, __uint_as_float(rk[t + 3]) * scale);
-          float4 nv = make_float4(__uint_as_float(rv[t]), __uint_as_float(rv[t + 1]), __uint_as_float(rv[t + 2]),
-                                  __uint_as_float(rv[t + 3]));
-          float4* pk = reinterpret_cast<float4*>(dkr + ch * 32 + t);
-          float4* pv = reinterpret_cast<float4*>(dvr + ch * 32 + t);
-          if (accumulate) {
-            const float4 ok = *pk, ov = *pv;
-            nk.x += ok.x; nk.y += ok.y; nk.z += ok.z; nk.w += ok.w;
-            nv.x += ov.x; nv.y += ov.y; nv.z += ov.z; nv.w += ov.w;
-          }
-          *pk = nk;
-          *pv = nv;
+      for (int u = 0; u < 8; ++u) {
+        const int off = (u ^ (row & 7)) * 16;
+        *reinterpret_cast<float4*>(bk + off) =
+            make_float4(__uint_as_float(rk[4 * u]) * scale, __uint_as_float(rk[4 * u + 1]) * scale,
+                        __uint_as_float(rk[4 * u + 2]) * scale, __uint_as_float(rk[4 * u + 3]) * scale);
+        *reinterpret_cast<float4*>(bv + off) = make_float4(__uint_as_float(rv[4 * u]), __uint_as_float(rv[4 * u + 1]),
+                                                           __uint_as_float(rv[4 * u + 2]), __uint_as_float(rv[4 * u + 3]));
+      }
+    }
+    fence_proxy_async();
+    named_bar(1, 256);
+    if (threadIdx.x == 64) {
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        if (accumulate) {
+          tma_reduce_add_4d(&tmdK, stg + ch * 4096, ch * 32, key0, head, sq);
+          tma_reduce_add_4d(&tmdV, stg + 16384 + ch * 4096, ch * 32, key0, head, sq);
+        } else {
+          tma_store_4d(&tmdK, stg + ch * 4096, ch * 32, key0, head, sq);
+          tma_store_4d(&tmdV, stg + 16384 + ch * 4096, ch * 32, key0, head, sq);
         }
       }
+      tma_commit_group();
+      tma_wait_all();
     }
   }
   tc_fence_before();
@@ -623,7 +631,7 @@ cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o,
   if (!encode_bf16_map(&mq, q, 4, dims, strides, box) || !encode_bf16_map(&mk, k, 4, dims, strides, box) ||
       !encode_bf16_map(&mv, v, 4, dims, strides, box))
     return cudaErrorInvalidValue;
-  dim3 grid((l + AT - 1) / AT, a, nseq);
+  dim3 grid(a, nseq, (l + AT - 1) / AT);
   attn_fwd_sm100_kernel<<<grid, FWD_THREADS, FwdSmem::BYTES, st>>>(mq, mk, mv, o, ldo, lse, s, c, l, rsqrtf((float)d) * LOG2E_F,
                                                            o_sstride, lse_sstride);
   return cudaGetLastError();
@@ -664,6 +672,14 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
       !encode_bf16_map(&mq, q, 4, kdims, kstr, qbox) || !encode_bf16_map(&mo, dO, 3, odims, ostr, obox) ||
       !encode_f32_map_noswizzle(&mdq, dq_acc, 3, qdims, qstr, qrbox))
     return cudaErrorInvalidValue;
+  // dk_acc / dv_acc: [nseq][a][s][d] fp32, viewed as {d, rows = c + l (prefix), a, seq}
+  const uint64_t adims[4] = {(uint64_t)d, (uint64_t)(c + l), (uint64_t)a, (uint64_t)nseq};
+  const uint64_t astr[3] = {(uint64_t)d * 4, (uint64_t)s * d * 4,
+                            (uint64_t)(nseq > 1 ? dkv_sstride : (int64_t)a * s * d) * 4};
+  const uint32_t abox[4] = {32, AT, 1, 1};
+  CUtensorMap mdk, mdv;
+  if (!encode_f32_map_sw128(&mdk, dk_acc, 4, adims, astr, abox) || !encode_f32_map_sw128(&mdv, dv_acc, 4, adims, astr, abox))
+    return cudaErrorInvalidValue;
   const float scale = rsqrtf((float)d);
   dim3 grid(a * nseq, (c + l + AT - 1) / AT);
   static int* dbg = nullptr;
@@ -673,8 +689,8 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
   }
   int* dbg_dev = nullptr;
   if (dbg_on) { memset(dbg, 0, 4096 * sizeof(int)); cudaHostGetDevicePointer(&dbg_dev, dbg, 0); }
-  attn_bwd_sm100_kernel<<<grid, FWD_THREADS, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, mdq, lse, Dvec, lse_sstride, dkv_sstride,
-                                                           dk_acc, dv_acc, s, c, l, scale, scale * LOG2E_F, accumulate,
+  attn_bwd_sm100_kernel<<<grid, FWD_THREADS, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, mdq, mdk, mdv, lse, Dvec, lse_sstride,
+                                                           s, c, l, scale, scale * LOG2E_F, accumulate,
                                                            a, dbg_dev);
   e = cudaGetLastError();
   if (dbg_on) {

@@ -837,6 +837,7 @@ class Engine final : public EngineBase {
       cudaGraphDestroy(graph);
       if (ce != cudaSuccess) { g_exec = nullptr; return fail(TP_ECUDA, "graph instantiate: %s", cudaGetErrorString(ce)); }
       g_launches = kn;
+      instr.launches = kn;
       CU(cudaGraphLaunch(g_exec, stream));
     } else {
       if (g_exec) { cudaGraphExecDestroy(g_exec); g_exec = nullptr; }

@@ -173,6 +173,20 @@ __device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, const 
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+// TMA store / reduce-add of a 4-D smem tile (rows outside the tensor bounds are clipped)
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2,
+                                                  int c3) {
+  asm volatile("cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+__device__ __forceinline__ void tma_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // shared-memory writes by threads -> visible to the async proxy (tcgen05.mma / TMA reads)
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -198,6 +212,9 @@ bool encode_bf16_map(CUtensorMap* map, const void* ptr, int rank, const uint64_t
 // host: plain (unswizzled) fp32 tensor map, e.g. the target of a TMA reduce-add
 bool encode_f32_map_noswizzle(CUtensorMap* map, const void* ptr, int rank, const uint64_t* dims,
                               const uint64_t* strides_bytes, const uint32_t* box);
+// host: 128-byte-swizzled fp32 tensor map (inner box = 32 floats = one 128-byte line)
+bool encode_f32_map_sw128(CUtensorMap* map, const void* ptr, int rank, const uint64_t* dims,
+                          const uint64_t* strides_bytes, const uint32_t* box);
 int num_sms();
 
 }  // namespace tp
