@@ -53,6 +53,19 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[3
         "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
@@ -69,6 +82,17 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accum)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_bf16_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                              uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(accum)
       : "memory");
 }
@@ -90,7 +114,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
                           float* __restrict__ lse, int s, int c, int l, float scale_log2, int64_t o_sstride,
                           int64_t lse_sstride) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned base derived by pointer arithmetic on the __shared__ array (not through an
+  // integer cast), so the compiler keeps the shared state space: LDS/STS instead of generic LD/ST
+  uint8_t* sm = smem_raw + ((1024u - (tc5::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + FwdSmem::BAR);
   uint64_t* qfull = bars + 0;
   uint64_t* kvfull = bars + 1;   // [2]
@@ -142,8 +168,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       tma_load_4d(vd, &tmV, 0, j * AT, head, sq, kvfull + b);
       tma_load_4d(vd + HALF, &tmV, 64, j * AT, head, sq, kvfull + b);
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (whole warp; one elected lane issues)
     constexpr uint32_t idS = idesc_bf16(128, 128, false, false);
     constexpr uint32_t idO = idesc_bf16(128, 128, false, true);
     const uint32_t q_base = smem_u32(sm + FwdSmem::Q);
@@ -158,11 +184,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 #pragma unroll
       for (int kk = 0; kk < AT / 16; ++kk) {
         const uint64_t bd = make_desc(v_base + kk * 2048, HALF, 1024);
-        mma_bf16_ts(tmem + 256 + bi * 128, tmem + bi * 128 + kk * 8, bd, idO, kk > 0);
+        mma_bf16_ts_w(tmem + 256 + bi * 128, tmem + bi * 128 + kk * 8, bd, idO, kk > 0);
       }
-      mma_commit(ofull + bi);
-      mma_commit(sfree + bi);
-      mma_commit(kvfree + bi);
+      mma_commit_w(ofull + bi);
+      mma_commit_w(sfree + bi);
+      mma_commit_w(kvfree + bi);
     };
     mbar_wait(qfull, 0);
     for (int j = 0; j < nkb; ++j) {
@@ -174,9 +200,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 #pragma unroll
       for (int kk = 0; kk < AT / 16; ++kk) {
         const uint32_t off = (kk >> 2) * HALF + (kk & 3) * 32;
-        mma_bf16(tmem + b * 128, make_desc(q_base + off, 16, 1024), make_desc(k_base + off, 16, 1024), idS, kk > 0);
+        mma_bf16_w(tmem + b * 128, make_desc(q_base + off, 16, 1024), make_desc(k_base + off, 16, 1024), idS, kk > 0);
       }
-      mma_commit(sfull + b);
+      mma_commit_w(sfull + b);
       if (j >= 1) pv(j - 1);
     }
     pv(nkb - 1);
@@ -314,29 +340,37 @@ constexpr uint32_t QT = BQB * AT * 2;            // 16 KiB: [64 q][128 d]
 constexpr uint32_t QHALF = QT / 2;               // 8 KiB: second 64-column atom
 constexpr uint32_t PT = AT * BQB * 2;            // 16 KiB: [128 keys][64 q] (one atom wide)
 constexpr int NQB = 3;                           // Q / dO ring depth
+constexpr int BWD_THREADS = 448;                 // TMA, MMA, 8 softmax-gradient warps, 4 dQ drain warps
 
 struct BwdSmem {
   static constexpr uint32_t K = 0, V = TILE, Q = 2 * TILE, O = Q + NQB * QT, DS = O + NQB * QT;
   static constexpr uint32_t DQ = DS + 2 * PT;  // fp32 [64 q][128 d]
-  static constexpr uint32_t LD = DQ + 32768;   // fp32 [2 tiles][lse*log2e[64], D[64]]
-  static constexpr uint32_t BAR = LD + 1024;
+  static constexpr uint32_t LD = DQ + 32768;   // fp32 [3 ring slots][lse*log2e[64], D[64]]
+  static constexpr uint32_t BAR = LD + NQB * 512;
   static constexpr uint32_t BYTES = BAR + 256 + 1024;
   static_assert(BYTES <= 232448, "backward tile set exceeds 227 KB of shared memory");
 };
 
-__global__ void __launch_bounds__(FWD_THREADS, 1)
+__global__ void __launch_bounds__(BWD_THREADS, 1)
     attn_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                           const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                           const __grid_constant__ CUtensorMap tmdQ, const __grid_constant__ CUtensorMap tmdK,
-                          const __grid_constant__ CUtensorMap tmdV, const float* __restrict__ lse,
-                          const float* __restrict__ Dvec, int64_t lse_sstride, int s, int c, int l,
-                          float scale, float scale_log2, int accumulate, int nheads, volatile int* dbg) {
+                          const __grid_constant__ CUtensorMap tmdV, const float* __restrict__ ldg, int s, int c, int l,
+                          float scale, float scale_log2, int accumulate, int nheads, volatile int* dbg,
+                          long long* trace) {
   extern __shared__ uint8_t smem_raw[];
 #define DBG(role, v)                                                                    \
   do {                                                                                  \
     if (dbg) { dbg[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + (role)] = (v); __threadfence_system(); } \
   } while (0)
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // TP_ATTN_TRACE: clock64 timeline of CTA (0, 0), slot (role * 8 + event) * 64 + tile
+#define TRC(role, ev, i)                                                                  \
+  do {                                                                                    \
+    if (trace && blockIdx.x == 0 && blockIdx.y == 0 && (i) < 64) trace[((role) * 8 + (ev)) * 64 + (i)] = clock64(); \
+  } while (0)
+  // 1024-aligned base derived by pointer arithmetic on the __shared__ array (not through an
+  // integer cast), so the compiler keeps the shared state space: LDS/STS instead of generic LD/ST
+  uint8_t* sm = smem_raw + ((1024u - (tc5::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + BwdSmem::BAR);
   uint64_t* kvfull = bars + 0;
   uint64_t* qfull = bars + 1;    // [3] Q / dO tile landed
@@ -345,15 +379,14 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   uint64_t* pfull = bars + 9;    // [2] P^T in TMEM, dS^T in smem (8 warps)
   uint64_t* dsfree = bars + 11;  // [2] dK / dQ MMAs done reading dS^T
   uint64_t* dqfull = bars + 13;  // [2] dQ^T in TMEM
-  uint64_t* dqfree = bars + 15;  // [2] dQ^T drained (8 warps)
+  uint64_t* dqfree = bars + 15;  // [2] dQ^T drained (4 warps)
   uint64_t* done = bars + 17;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // heaviest key blocks (the most query tiles) first: blockIdx.y is the key block
   const int head = blockIdx.x % nheads, sq = blockIdx.x / nheads, key0 = blockIdx.y * AT;
-  lse += sq * lse_sstride;
-  Dvec += (int64_t)sq * nheads * l;
+  ldg += ((int64_t)sq * nheads + head) * ((l + BQB - 1) / BQB) * (2 * BQB);
   const int qt0 = max(0, key0 - c) / BQB, nqt = (l + BQB - 1) / BQB;
   const int ntile = nqt - qt0;  // >= 1 because key0 < c + l
 
@@ -362,7 +395,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     for (int i = 0; i < NQB; ++i) { mbar_init(qfull + i, 1); mbar_init(qfree + i, 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(sfull + i, 1); mbar_init(pfull + i, 8); mbar_init(dsfree + i, 1);
-      mbar_init(dqfull + i, 1); mbar_init(dqfree + i, 8);
+      mbar_init(dqfull + i, 1); mbar_init(dqfree + i, 4);
     }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -386,16 +419,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       const int b = i % NQB, qt = qt0 + i;
       DBG(0, 100 + i);
       if (i >= NQB) mbar_wait(qfree + b, ((i / NQB) - 1) & 1);
+      TRC(0, 0, i);
       uint8_t* qd = sm + BwdSmem::Q + b * QT;
       uint8_t* od = sm + BwdSmem::O + b * QT;
-      mbar_expect_tx(qfull + b, 2 * QT);
+      mbar_expect_tx(qfull + b, 2 * QT + 2 * BQB * 4);
+      bulk_load(sm + BwdSmem::LD + b * 512, ldg + qt * (2 * BQB), 2 * BQB * 4, qfull + b);
       tma_load_4d(qd, &tmQ, 0, c + qt * BQB, head, sq, qfull + b);
       tma_load_4d(qd + QHALF, &tmQ, 64, c + qt * BQB, head, sq, qfull + b);
       tma_load_3d(od, &tmdO, head * AT, qt * BQB, sq, qfull + b);
       tma_load_3d(od + QHALF, &tmdO, head * AT + 64, qt * BQB, sq, qfull + b);
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (whole warp, warp-uniform control flow; one elected lane issues)
     constexpr uint32_t idS = idesc_bf16(128, BQB, false, false);   // S^T, dP^T
     constexpr uint32_t idKV = idesc_bf16(128, 128, false, true);   // dV (A = P^T in TMEM), dK (B = dO / Q, MN-major)
     constexpr uint32_t idQ = idesc_bf16(128, BQB, true, true);     // dQ^T (A = K MN-major, B = dS^T MN-major)
@@ -407,23 +442,26 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       const uint32_t q_base = smem_u32(sm + BwdSmem::Q + bq * QT), o_base = smem_u32(sm + BwdSmem::O + bq * QT);
       const uint32_t tb = tmem + bb * 128;
       mbar_wait(qfull + bq, (j / NQB) & 1);
+      if (lane == 0) TRC(1, 0, j);
       // buffer bb last held tile j-2: its S^T was read by the softmax (pfull(j-2), waited before
       // the MMAs of j-2), its P^T by dV(j-2) (qfree(j-2)), its dQ^T by the drain (dqfree(j-2))
       if (j >= 2) mbar_wait(qfree + (j - 2) % NQB, ((j - 2) / NQB) & 1);
+      if (lane == 0) TRC(1, 1, j);
       tc_fence_after();
 #pragma unroll
       for (int kk = 0; kk < AT / 16; ++kk) {
         const uint32_t ok = (kk >> 2) * HALF + (kk & 3) * 32, oq = (kk >> 2) * QHALF + (kk & 3) * 32;
-        mma_bf16(tb, make_desc(k_base + ok, 16, 1024), make_desc(q_base + oq, 16, 1024), idS, kk > 0);
+        mma_bf16_w(tb, make_desc(k_base + ok, 16, 1024), make_desc(q_base + oq, 16, 1024), idS, kk > 0);
       }
       if (j >= 2) mbar_wait(dqfree + bb, ((j >> 1) - 1) & 1);
+      if (lane == 0) TRC(1, 2, j);
       tc_fence_after();
 #pragma unroll
       for (int kk = 0; kk < AT / 16; ++kk) {
         const uint32_t ok = (kk >> 2) * HALF + (kk & 3) * 32, oq = (kk >> 2) * QHALF + (kk & 3) * 32;
-        mma_bf16(tb + 64, make_desc(v_base + ok, 16, 1024), make_desc(o_base + oq, 16, 1024), idS, kk > 0);
+        mma_bf16_w(tb + 64, make_desc(v_base + ok, 16, 1024), make_desc(o_base + oq, 16, 1024), idS, kk > 0);
       }
-      mma_commit(sfull + bb);
+      mma_commit_w(sfull + bb);
     };
     issue_sdp(0);
     for (int i = 0; i < ntile; ++i) {
@@ -431,106 +469,123 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       const uint32_t q_base = smem_u32(sm + BwdSmem::Q + bq * QT), o_base = smem_u32(sm + BwdSmem::O + bq * QT);
       const uint32_t ds_base = smem_u32(sm + BwdSmem::DS + bb * PT);
       const uint32_t tb = tmem + bb * 128;
-      DBG(1, 100 + 10 * i);
+      if (lane == 0) DBG(1, 100 + 10 * i);
       if (i + 1 < ntile) issue_sdp(i + 1);
-      DBG(1, 101 + 10 * i);
+      if (lane == 0) DBG(1, 101 + 10 * i);
       mbar_wait(pfull + bb, (i >> 1) & 1);
+      if (lane == 0) TRC(1, 3, i);
       tc_fence_after();
 #pragma unroll
       for (int kk = 0; kk < BQB / 16; ++kk) {
         // P^T columns: query half h = kk >> 1 was packed at h*32 .. h*32+15 of the S^T columns
-        mma_bf16_ts(tmem + T_DV, tb + (kk >> 1) * 32 + (kk & 1) * 8, make_desc(o_base + kk * 2048, QHALF, 1024), idKV,
+        mma_bf16_ts_w(tmem + T_DV, tb + (kk >> 1) * 32 + (kk & 1) * 8, make_desc(o_base + kk * 2048, QHALF, 1024), idKV,
                     (i | kk) != 0);
-        mma_bf16(tmem + T_DK, make_desc(ds_base + kk * 32, 16, 1024), make_desc(q_base + kk * 2048, QHALF, 1024), idKV,
+        mma_bf16_w(tmem + T_DK, make_desc(ds_base + kk * 32, 16, 1024), make_desc(q_base + kk * 2048, QHALF, 1024), idKV,
                  (i | kk) != 0);
       }
-      mma_commit(qfree + bq);
+      mma_commit_w(qfree + bq);
 #pragma unroll
       for (int kk = 0; kk < AT / 16; ++kk)
-        mma_bf16(tb + 64, make_desc(k_base + kk * 2048, HALF, 1024), make_desc(ds_base + kk * 2048, 8192, 1024), idQ,
+        mma_bf16_w(tb + 64, make_desc(k_base + kk * 2048, HALF, 1024), make_desc(ds_base + kk * 2048, 8192, 1024), idQ,
                  kk > 0);
-      mma_commit(dqfull + bb);
-      mma_commit(dsfree + bb);
-      DBG(1, 105 + 10 * i);
+      mma_commit_w(dqfull + bb);
+      mma_commit_w(dsfree + bb);
+      if (lane == 0) TRC(1, 4, i);
+      if (lane == 0) DBG(1, 105 + 10 * i);
     }
-    mma_commit(done);
-    DBG(1, 999);
-  } else if (warp >= 2) {
-    // ---------------- softmax-gradient warps: two per TMEM lane quarter; thread owns key row `row`
-    // and query columns [half*32, half*32+32) of the tile (head-dim columns for dQ^T / dK / dV)
-    const int q = warp & 3, row = q * 32 + lane, half = (warp - 2) >> 2;
-    const int kabs = key0 + row;
+    mma_commit_w(done);
+    if (lane == 0) DBG(1, 999);
+  } else if (warp >= 10) {
+    // ---------------- dQ drain warps (one per TMEM lane quarter; thread = head-dim index `row`):
+    // dQ^T of tile j -> smem [64 q][128 d] -> one TMA reduce-add into dq_acc
+    const int q = warp & 3, row = q * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    const float* lse_h = lse + (int64_t)head * s + c;
-    const float* D_h = Dvec + (int64_t)head * l;
     float* dqs = reinterpret_cast<float*>(sm + BwdSmem::DQ);
-    constexpr int HQ = BQB / 2;  // query columns per half
-    // dQ^T of tile j (thread = head-dim index `row`) -> smem [64 q][128 d] -> one TMA reduce-add
-    auto drain_dq = [&](int j) {
+    const bool leader = threadIdx.x == 320;
+    for (int j = 0; j < ntile; ++j) {
       const int bb = j & 1;
+      if (leader) tma_wait_reads();  // the previous reduce has finished reading the staging tile
+      named_bar(2, 128);
       mbar_wait(dqfull + bb, (j >> 1) & 1);
+      if (leader) TRC(2, 4, j);
       tc_fence_after();
-      if (threadIdx.x == 64) tma_wait_reads();  // previous reduce has finished reading the buffer
-      named_bar(1, 256);
-      {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
         uint32_t r[32];
-        tmem_ld32_nowait(lane_base + bb * 128 + 64 + half * HQ, r);
+        tmem_ld32_nowait(lane_base + bb * 128 + 64 + h * 32, r);
         tmem_wait_ld();
 #pragma unroll
-        for (int t = 0; t < 32; ++t) dqs[(half * HQ + t) * AT + row] = __uint_as_float(r[t]) * scale;
+        for (int t = 0; t < 32; ++t) dqs[(h * 32 + t) * AT + row] = __uint_as_float(r[t]) * scale;
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(dqfree + bb);
       fence_proxy_async();
-      named_bar(1, 256);
-      if (threadIdx.x == 64) tma_reduce_add_3d(&tmdQ, dqs, head * AT, (qt0 + j) * BQB, sq);
-    };
+      named_bar(2, 128);
+      if (leader) { tma_reduce_add_3d(&tmdQ, dqs, head * AT, (qt0 + j) * BQB, sq); TRC(2, 5, j); }
+    }
+    if (leader) tma_wait_all();
+  } else if (warp >= 2) {
+    // ---------------- softmax-gradient warps: two per TMEM lane quarter; thread owns key row `row`
+    // and query columns [half*32, half*32+32) of the tile (head-dim columns for dK / dV)
+    const int q = warp & 3, row = q * 32 + lane, half = (warp - 2) >> 2;
+    const int kabs = key0 + row;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    constexpr int HQ = BQB / 2;  // query columns per half
     for (int i = 0; i < ntile; ++i) {
       const int bb = i & 1;
       const int qrow0 = (qt0 + i) * BQB;
-      float* Ls = reinterpret_cast<float*>(sm + BwdSmem::LD) + bb * 2 * BQB;  // double-buffered by tile
-      float* Ds = Ls + BQB;
-      if (lane == 0) DBG(2 + q, 100 + 10 * i);
-      {  // stage lse*log2e and D of this tile's 64 queries (rows past the slice: +inf / 0)
-        const int t = threadIdx.x - 64, qr = qrow0 + (t & 63);
-        if (t < 64) Ls[t] = qr < l ? __ldg(lse_h + qr) * LOG2E_F : INFINITY;
-        else if (t < 128) Ds[t - 64] = qr < l ? __ldg(D_h + qr) : 0.f;
-      }
-      named_bar(1, 256);
+      // lse*log2e / D of the tile's queries (rows past the slice: +inf / 0), bulk-loaded with Q / dO
+      const float* Ls = reinterpret_cast<const float*>(sm + BwdSmem::LD + (i % NQB) * 512);
+      const float* Ds = Ls + BQB;
+      if (threadIdx.x == 64) TRC(2, 0, i);
+      mbar_wait(qfull + i % NQB, (i / NQB) & 1);
+      if (threadIdx.x == 64) TRC(2, 1, i);
       mbar_wait(sfull + bb, (i >> 1) & 1);
+      if (threadIdx.x == 64) TRC(2, 2, i);
       if (i >= 2) mbar_wait(dsfree + bb, ((i >> 1) - 1) & 1);  // dK / dQ MMAs of tile i-2 read dS^T buffer bb
       tc_fence_after();
       // visible iff c + qr >= kabs (and qr < l, which Ls = +inf enforces)
-      const int vis0 = kabs - c - qrow0;  // first visible column of this key row
-      {
-        uint32_t rs[32], rp[32];
-        tmem_ld32_nowait(lane_base + bb * 128 + half * HQ, rs);
-        tmem_ld32_nowait(lane_base + bb * 128 + 64 + half * HQ, rp);
-        tmem_wait_ld();
-        uint32_t pk[16], dk[16];
+      const int vis0 = kabs - c - qrow0 - half * HQ;  // first visible column of this key row, in this half
+      uint8_t* dSt = sm + BwdSmem::DS + bb * PT;
 #pragma unroll
-        for (int t = 0; t < 32; t += 2) {
+      for (int ch = 0; ch < 2; ++ch) {  // 16 query columns at a time
+        uint32_t rs[16], rp[16];
+        tmem_ld16_nowait(lane_base + bb * 128 + half * HQ + ch * 16, rs);
+        tmem_ld16_nowait(lane_base + bb * 128 + 64 + half * HQ + ch * 16, rp);
+        const float4* L4 = reinterpret_cast<const float4*>(Ls + half * HQ + ch * 16);
+        const float4* D4 = reinterpret_cast<const float4*>(Ds + half * HQ + ch * 16);
+        float Lv[16], Dv[16];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 a4 = L4[u], d4 = D4[u];
+          Lv[4 * u] = a4.x; Lv[4 * u + 1] = a4.y; Lv[4 * u + 2] = a4.z; Lv[4 * u + 3] = a4.w;
+          Dv[4 * u] = d4.x; Dv[4 * u + 1] = d4.y; Dv[4 * u + 2] = d4.z; Dv[4 * u + 3] = d4.w;
+        }
+        tmem_wait_ld();
+        uint32_t pk[8], dk[8];
+#pragma unroll
+        for (int t = 0; t < 16; t += 2) {
           float pv[2], dv[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int col = half * HQ + t + e;
-            float p = ex2(fmaf(__uint_as_float(rs[t + e]), scale_log2, -Ls[col]));
+            const int col = ch * 16 + t + e;
+            float p = ex2(fmaf(__uint_as_float(rs[t + e]), scale_log2, -Lv[t + e]));
             p = col >= vis0 ? p : 0.f;
             pv[e] = p;
-            dv[e] = p * (__uint_as_float(rp[t + e]) - Ds[col]);
+            dv[e] = p * (__uint_as_float(rp[t + e]) - Dv[t + e]);
           }
           __nv_bfloat162 hp = __floats2bfloat162_rn(pv[0], pv[1]);
           __nv_bfloat162 hd = __floats2bfloat162_rn(dv[0], dv[1]);
           pk[t >> 1] = *reinterpret_cast<uint32_t*>(&hp);
           dk[t >> 1] = *reinterpret_cast<uint32_t*>(&hd);
         }
-        // P^T (this half's 32 queries) packed into the first 16 of this half's own S^T columns
-        tmem_st16(lane_base + bb * 128 + half * HQ, pk);
-        uint8_t* dSt = sm + BwdSmem::DS + bb * PT;
+        // P^T (this half's 32 queries) packed into the first 16 of this half's own S^T columns;
+        // this chunk's S^T columns were consumed above (the second chunk's lie at +16 .. +31)
+        tmem_st8(lane_base + bb * 128 + half * HQ + ch * 8, pk);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int cc = half * 4 + u;
+        for (int u = 0; u < 2; ++u) {
+          const int cc = half * 4 + ch * 2 + u;
           *reinterpret_cast<uint4*>(dSt + swz(row, cc)) = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
         }
       }
@@ -539,16 +594,15 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(pfull + bb);
-      if (i >= 1) drain_dq(i - 1);
+      if (threadIdx.x == 64) TRC(2, 3, i);
     }
-    drain_dq(ntile - 1);
-    if (threadIdx.x == 64) tma_wait_all();
     if (lane == 0) DBG(2 + q, 900);
     // dK (x scale) and dV of this key block -> 128B-swizzled fp32 staging over the (now idle) Q / dO
     // ring and dS^T buffers: [dK | dV][4 column chunks of 32 d][128 keys][32] -> 8 TMA stores (first
     // slice) or reduce-adds (later slices) into the prefix accumulators; key rows past the prefix
     // are clipped by the tensor map.
     mbar_wait(done, 0);
+    if (threadIdx.x == 64) TRC(2, 6, 0);
     tc_fence_after();
     float* stg = reinterpret_cast<float*>(sm + BwdSmem::Q);
 #pragma unroll
@@ -585,6 +639,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       }
       tma_commit_group();
       tma_wait_all();
+      TRC(2, 7, 0);
     }
   }
   tc_fence_before();
@@ -592,6 +647,41 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
+  }
+}
+
+// Per 64-query tile of every (sequence, head): lse*log2e (+inf past the slice) and D = rowsum(dO * O)
+// (0 past the slice) as [nseq][a][ntq][lse 64 | D 64] fp32, one 512-byte bulk copy per tile for the
+// backward kernel. One warp per query row, lanes over 8-element chunks of all heads.
+__global__ void bwd_stage_kernel(const bf16* __restrict__ dO, int64_t ld_do, const bf16* __restrict__ o, int64_t ldo,
+                                 const float* __restrict__ lse, int64_t lse_sstride, float* __restrict__ out, int a,
+                                 int s, int c, int l, int ntq, int64_t o_sstride) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r = blockIdx.x * 4 + w, sq = blockIdx.y;
+  if (r >= ntq * BQB) return;
+  dO += sq * o_sstride;
+  o += sq * o_sstride;
+  lse += sq * lse_sstride;
+  float* base = out + (int64_t)sq * a * ntq * (2 * BQB) + (r / BQB) * (2 * BQB) + (r % BQB);
+  constexpr int CPH = AT / 8;  // 16 chunks per head: two heads per pass of the warp
+  for (int hb = 0; hb < a * CPH; hb += 32) {
+    const int ch = hb + lane;
+    float acc = 0.f;
+    if (r < l && ch < a * CPH) {
+      float x[8], y[8];
+      load8<bf16>(dO + (int64_t)r * ld_do + ch * 8, x);
+      load8<bf16>(o + (int64_t)r * ldo + ch * 8, y);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc += x[i] * y[i];
+    }
+#pragma unroll
+    for (int off = 1; off < CPH; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (ch < a * CPH && (lane % CPH) == 0) {
+      const int head = ch / CPH;
+      float* p = base + (int64_t)head * ntq * (2 * BQB);
+      p[0] = r < l ? __ldg(lse + (int64_t)head * s + c + r) * LOG2E_F : INFINITY;
+      p[BQB] = r < l ? acc : 0.f;
+    }
   }
 }
 
@@ -652,9 +742,11 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
     attr = true;
   }
   const int H = a * d;
+  const int ntq = (l + BQB - 1) / BQB;
   cudaError_t e = cudaMemsetAsync(dq_acc, 0, sizeof(float) * (size_t)l * H * nseq, st);
-  if (e == cudaSuccess) e = attn_bwd_prep(dO, ld_do, o, ldo, Dvec, a, d, l, st, nseq, o_sstride);
   if (e != cudaSuccess) return e;
+  bwd_stage_kernel<<<dim3((ntq * BQB + 3) / 4, nseq), 128, 0, st>>>(dO, ld_do, o, ldo, lse, lse_sstride, Dvec, a, s, c,
+                                                                     l, ntq, o_sstride);
   const int64_t qs = nseq > 1 ? qkv_sstride : (int64_t)a * s * d;
   const uint64_t kdims[4] = {(uint64_t)d, (uint64_t)(c + l), (uint64_t)a, (uint64_t)nseq};
   const uint64_t kstr[3] = {(uint64_t)d * 2, (uint64_t)s * d * 2, (uint64_t)qs * 2};
@@ -689,10 +781,30 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
   }
   int* dbg_dev = nullptr;
   if (dbg_on) { memset(dbg, 0, 4096 * sizeof(int)); cudaHostGetDevicePointer(&dbg_dev, dbg, 0); }
-  attn_bwd_sm100_kernel<<<grid, FWD_THREADS, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, mdq, mdk, mdv, lse, Dvec, lse_sstride,
+  static int trace_left = getenv("TP_ATTN_TRACE") ? atoi(getenv("TP_ATTN_TRACE")) : 0;
+  static long long* trace = nullptr;
+  if (trace_left > 0 && !trace) cudaMalloc(&trace, 3 * 8 * 64 * sizeof(long long));
+  if (trace_left > 0) cudaMemsetAsync(trace, 0, 3 * 8 * 64 * sizeof(long long), st);
+  attn_bwd_sm100_kernel<<<grid, BWD_THREADS, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, mdq, mdk, mdv, Dvec,
                                                            s, c, l, scale, scale * LOG2E_F, accumulate,
-                                                           a, dbg_dev);
+                                                           a, dbg_dev, trace_left > 0 ? trace : nullptr);
   e = cudaGetLastError();
+  if (trace_left > 0) {
+    --trace_left;
+    long long h[3 * 8 * 64];
+    cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    long long t0 = h[(1 * 8 + 0) * 64];
+    for (int i = 0; i < 3 * 8 * 64; ++i) if (h[i] && h[i] < t0) t0 = h[i];
+    fprintf(stderr, "attn_bwd trace c=%d l=%d: tile | P:qfree-ok | M:qfull M:bufS M:bufdP M:pfull M:issued | S:stage S:bar S:sfull S:pfull S:dqfull S:dqred\n", c, l);
+    for (int i = 0; i < 64; ++i) {
+      auto g = [&](int r, int e) { long long v = h[(r * 8 + e) * 64 + i]; return v ? (long long)(v - t0) : -1LL; };
+      if (g(1, 0) < 0 && g(2, 0) < 0) break;
+      fprintf(stderr, "%3d | %7lld | %7lld %7lld %7lld %7lld %7lld | %7lld %7lld %7lld %7lld %7lld %7lld\n", i, g(0, 0), g(1, 0),
+              g(1, 1), g(1, 2), g(1, 3), g(1, 4), g(2, 0), g(2, 1), g(2, 2), g(2, 3), g(2, 4), g(2, 5));
+    }
+    fprintf(stderr, "done-seen %lld  dkv-stored %lld\n", h[(2 * 8 + 6) * 64] - t0, h[(2 * 8 + 7) * 64] - t0);
+  }
   if (dbg_on) {
     for (int it = 0; it < 50 && cudaStreamQuery(st) == cudaErrorNotReady; ++it) usleep(100000);
     if (cudaStreamQuery(st) == cudaErrorNotReady) {

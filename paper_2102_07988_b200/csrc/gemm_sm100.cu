@@ -62,7 +62,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                       int K, Epi epi) {
   using C = Cfg<CG, BN>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned base derived by pointer arithmetic on the __shared__ array (not through an
+  // integer cast), so the compiler keeps the shared state space: LDS/STS instead of generic LD/ST
+  uint8_t* smem = smem_raw + ((1024u - (tc5::smem_u32(smem_raw) & 1023u)) & 1023u);
   float* epi_scratch = reinterpret_cast<float*>(smem + C::NS * C::STAGE);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::NS * C::STAGE + C::EPI_SCRATCH);
   uint64_t* empty = full + C::NS;

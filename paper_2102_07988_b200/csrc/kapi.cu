@@ -63,7 +63,7 @@ extern "C" tp_status tpk_attention_bwd(const void* dO, const void* o, const void
   TP_CHECK_ARG(dO && o && q && k && v && lse && dq && dk_acc && dv_acc, "tpk_attention_bwd: null pointer");
   TP_CHECK_ARG(a >= 1 && d % 16 == 0 && d <= 128 && c >= 0 && l >= 1 && c + l <= s, "tpk_attention_bwd: bad shape");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  float* Dvec = scratch(0, (size_t)a * l);
+  float* Dvec = scratch(0, (size_t)2 * a * (l + 64));
   if (!Dvec) return fail(TP_ENOMEM, "tpk_attention_bwd: scratch");
   tp_status r = TP_OK;
   const int64_t H = (int64_t)a * d;

@@ -72,7 +72,8 @@ cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o,
 // D[head][r] = rowsum(dO * O) per head (attn_tc.cu)
 cudaError_t attn_bwd_prep(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ldo, float* Dvec, int a, int d, int l,
                           cudaStream_t st, int nseq = 1, int64_t o_sstride = 0);
-// dq_acc: fp32 scratch [l][a*d] (zeroed inside); dq: bf16 output rows (ld ldq)
+// dq_acc: fp32 scratch [l][a*d] per sequence (zeroed inside); dq: bf16 output rows (ld ldq);
+// Dvec: fp32 scratch of at least nseq * a * 128 * ceil(l/64) floats (per-tile lse / D staging)
 cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ldo, const bf16* q, const bf16* k,
                            const bf16* v, const float* lse, float* Dvec, float* dq_acc, bf16* dq, int64_t ldq,
                            float* dk_acc, float* dv_acc, int a, int s, int d, int c, int l, int accumulate,

@@ -359,7 +359,8 @@ class Engine final : public EngineBase {
     // per job: up to b = max_batch sequences of one slice
     TRY(vec(S.dk_acc, nl, B * s * H)); TRY(vec(S.dv_acc, nl, B * s * H));
     TRY(alloc(&S.gA, B * s * H)); TRY(alloc(&S.gB, B * s * H)); TRY(alloc(&S.gm, B * s * H)); TRY(alloc(&S.dA, B * s * H));
-    TRY(alloc(&S.Dvec, B * a * s)); TRY(alloc(&S.dO, B * s * H));
+    // Dvec: the sm100 backward's per-tile lse / D staging, [b][a][ceil(l/64)][128]
+    TRY(alloc(&S.Dvec, 2 * B * a * (s + 64))); TRY(alloc(&S.dO, B * s * H));
     TRY(alloc(&S.lnws, 2 * H * ((B * s + 3) / 4)));
     TRY(alloc(&S.dqacc, B * s * H));
     return TP_OK;
