@@ -127,7 +127,28 @@ def cpu_oracle_sample(cfg, B, reps=1, warmup=0):
                       f"(t_seq = {t_seq:.0f} s)"}
 
 
+# The JSON result line is the only thing on stdout: keep a private handle on the original stdout and
+# point fd 1 at stderr, so banners printed by native libraries (e.g. NCCL's version line at
+# communicator init) cannot interleave with it.
+_RESULT_OUT = None
+
+
+def emit(line):
+    global _RESULT_OUT
+    out = _RESULT_OUT if _RESULT_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
+def _isolate_stdout():
+    global _RESULT_OUT
+    sys.stdout.flush()
+    _RESULT_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
 def main():
+    _isolate_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -163,7 +184,7 @@ def main():
                 "config": {"workload": args.config, "batch": B, "stages": K},
                 "cpu_baseline": cpu, "e2e": {"value": cpu["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                                              "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
+        emit(line)
         return 0
 
     import torch
@@ -319,7 +340,7 @@ def main():
         line["ms_per_step_instrumented"] = ms_instr
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_oracle_sample(cfg, B)
-        print(json.dumps(line), flush=True)
+        emit(line)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()

@@ -112,7 +112,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                           const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ o, int64_t ldo,
                           float* __restrict__ lse, int s, int c, int l, float scale_log2, int64_t o_sstride,
-                          int64_t lse_sstride) {
+                          int64_t lse_sstride, long long* trace) {
+#define TRF(role, ev, i)                                                                  \
+  do {                                                                                    \
+    if (trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (i) < 64) trace[((role) * 8 + (ev)) * 64 + (i)] = clock64(); \
+  } while (0)
   extern __shared__ uint8_t smem_raw[];
   // 1024-aligned base derived by pointer arithmetic on the __shared__ array (not through an
   // integer cast), so the compiler keeps the shared state space: LDS/STS instead of generic LD/ST
@@ -160,6 +164,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     for (int j = 0; j < nkb; ++j) {
       const int b = j & 1;
       if (j >= 2) mbar_wait(kvfree + b, ((j >> 1) - 1) & 1);
+      TRF(0, 0, j);
       uint8_t* kd = sm + (b ? FwdSmem::K1 : FwdSmem::K0);
       uint8_t* vd = sm + (b ? FwdSmem::V1 : FwdSmem::V0);
       mbar_expect_tx(kvfull + b, 2 * TILE);
@@ -178,7 +183,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     auto pv = [&](int i) {
       const int bi = i & 1;
       mbar_wait(pfull + bi, (i >> 1) & 1);
+      if (lane == 0) TRF(1, 3, i);
       if (i >= 2) mbar_wait(ofree + bi, ((i >> 1) - 1) & 1);
+      if (lane == 0) TRF(1, 4, i);
       tc_fence_after();
       const uint32_t v_base = smem_u32(sm + (bi ? FwdSmem::V1 : FwdSmem::V0));
 #pragma unroll
@@ -189,12 +196,15 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       mma_commit_w(ofull + bi);
       mma_commit_w(sfree + bi);
       mma_commit_w(kvfree + bi);
+      if (lane == 0) TRF(1, 5, i);
     };
     mbar_wait(qfull, 0);
     for (int j = 0; j < nkb; ++j) {
       const int b = j & 1;
       mbar_wait(kvfull + b, (j >> 1) & 1);
+      if (lane == 0) TRF(1, 0, j);
       if (j >= 2) mbar_wait(sfree + b, ((j >> 1) - 1) & 1);
+      if (lane == 0) TRF(1, 1, j);
       tc_fence_after();
       const uint32_t k_base = smem_u32(sm + (b ? FwdSmem::K1 : FwdSmem::K0));
 #pragma unroll
@@ -203,6 +213,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         mma_bf16_w(tmem + b * 128, make_desc(q_base + off, 16, 1024), make_desc(k_base + off, 16, 1024), idS, kk > 0);
       }
       mma_commit_w(sfull + b);
+      if (lane == 0) TRF(1, 2, j);
       if (j >= 1) pv(j - 1);
     }
     pv(nkb - 1);
@@ -222,6 +233,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     auto add_o = [&](int i, float m_i) {
       const int bi = i & 1;
       mbar_wait(ofull + bi, (i >> 1) & 1);
+      if (threadIdx.x == 64) TRF(2, 3, i);
       tc_fence_after();
       const float sc = ex2(m_acc - m_i);
 #pragma unroll
@@ -236,10 +248,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ofree + bi);
+      if (threadIdx.x == 64) TRF(2, 4, i);
     };
     for (int j = 0; j < nkb; ++j) {
       const int b = j & 1;
       mbar_wait(sfull + b, (j >> 1) & 1);
+      if (threadIdx.x == 64) TRF(2, 0, j);
       tc_fence_after();
       const int key0 = j * AT + half * HC;       // first key of this half
       const bool diag = key0 + HC - 1 > qabs;    // only blocks crossing the diagonal need the mask
@@ -265,6 +279,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       float* xm = xch + (j & 1) * 256;
       xm[half * 128 + row] = mx;
       named_bar(1, 256);
+      if (threadIdx.x == 64) TRF(2, 1, j);
       mx = fmaxf(mx, xm[(half ^ 1) * 128 + row]);
       const float m_new = fmaxf(m, mx * scale_log2);
       // pass 2: P = exp2(S * scale_log2 - m_new) -> bf16, packed two per TMEM column in key order
@@ -287,6 +302,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(pfull + b);
+      if (threadIdx.x == 64) TRF(2, 2, j);
       lsum = lsum * ex2(m - m_new) + rs;  // partial (this half's keys), same m in both halves
       m_last = m;
       m = m_new;
@@ -722,8 +738,27 @@ cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o,
       !encode_bf16_map(&mv, v, 4, dims, strides, box))
     return cudaErrorInvalidValue;
   dim3 grid(a, nseq, (l + AT - 1) / AT);
+  static int trace_left = getenv("TP_ATTN_TRACE") ? atoi(getenv("TP_ATTN_TRACE")) : 0;
+  static long long* trace = nullptr;
+  if (trace_left > 0 && !trace) cudaMalloc(&trace, 3 * 8 * 64 * sizeof(long long));
+  if (trace_left > 0) cudaMemsetAsync(trace, 0, 3 * 8 * 64 * sizeof(long long), st);
   attn_fwd_sm100_kernel<<<grid, FWD_THREADS, FwdSmem::BYTES, st>>>(mq, mk, mv, o, ldo, lse, s, c, l, rsqrtf((float)d) * LOG2E_F,
-                                                           o_sstride, lse_sstride);
+                                                           o_sstride, lse_sstride, trace_left > 0 ? trace : nullptr);
+  if (trace_left > 0) {
+    --trace_left;
+    long long h[3 * 8 * 64];
+    cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    long long t0 = 0;
+    for (int i = 0; i < 3 * 8 * 64; ++i) if (h[i] && (!t0 || h[i] < t0)) t0 = h[i];
+    fprintf(stderr, "attn_fwd trace c=%d l=%d: kb | P:kvfree | M:kvfull M:sfree M:Scommit M:pfull M:ofree M:PVcommit | S:sfull S:maxbar S:pfull S:ofull S:addO\n", c, l);
+    for (int i = 0; i < 64; ++i) {
+      auto g = [&](int r, int e) { long long v = h[(r * 8 + e) * 64 + i]; return v ? (long long)(v - t0) : -1LL; };
+      if (g(1, 0) < 0) break;
+      fprintf(stderr, "%3d | %7lld | %7lld %7lld %7lld %7lld %7lld %7lld | %7lld %7lld %7lld %7lld %7lld\n", i, g(0, 0), g(1, 0),
+              g(1, 1), g(1, 2), g(1, 3), g(1, 4), g(1, 5), g(2, 0), g(2, 1), g(2, 2), g(2, 3), g(2, 4));
+    }
+  }
   return cudaGetLastError();
 }
 

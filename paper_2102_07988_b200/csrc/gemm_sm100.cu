@@ -10,8 +10,9 @@
 // Design (sm_100a):
 //   * persistent CTAs (grid = min(tiles, #SMs)), 128 x BN output tiles (BN = 256 or 128),
 //     tile order m-fastest so the weight tile is reused from L2 by consecutive CTAs;
-//   * warp-specialised: warp 0 = TMA producer (one thread), warp 1 = tcgen05.mma issuer (one
-//     thread), warps 2..5 = epilogue (TMEM -> registers -> fused epilogue -> global);
+//   * warp-specialised: warp 0 = TMA producer (one thread), warp 1 = tcgen05.mma issuer (whole
+//     warp, one elected lane), warps 2..9 = epilogue (two per TMEM lane quarter, each draining
+//     half of the tile's columns: TMEM -> registers -> smem transpose -> fused epilogue -> global);
 //   * operands staged by TMA (cp.async.bulk.tensor, 128-byte swizzle) into an NS-deep mbarrier
 //     ring; K-major operands are one box per stage, MN-major operands (dW) are 64-wide boxes placed
 //     at LBO = 8 KiB steps, described to the tensor core with the canonical SW128 layouts;
@@ -139,8 +140,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (++stage == C::NS) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 1 && lane == 0 && leader) {
-    // ---------------- MMA issuer (one thread issues for the CTA / CTA pair)
+  } else if (warp == 1 && leader) {
+    // ---------------- MMA issuer (whole warp, one elected lane issues for the CTA / CTA pair)
     const uint32_t idesc = (1u << 4)                       // D = fp32
                            | (1u << 7) | (1u << 10)        // A, B = bf16
                            | ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16)
@@ -160,13 +161,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int k = 0; k < BK / 16; ++k) {
           const uint64_t ad = A_MN ? make_desc(a_base + k * 2048, 8192, 1024) : make_desc(a_base + k * 32, 16, 1024);
           const uint64_t bd = B_MN ? make_desc(b_base + k * 2048, 8192, 1024) : make_desc(b_base + k * 32, 16, 1024);
-          if (CG == 1) mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
-          else mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          if (CG == 1) mma_bf16_w(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          else mma_bf16_pair_w(d_tmem, ad, bd, idesc, (kb | k) != 0);
         }
-        if (CG == 1) mma_commit(empty + stage); else mma_commit_pair(empty + stage);  // frees the smem slot(s)
+        if (CG == 1) mma_commit_w(empty + stage); else mma_commit_pair_w(empty + stage);  // frees the smem slot(s)
         if (++stage == C::NS) { stage = 0; phase ^= 1; }
       }
-      if (CG == 1) mma_commit(tfull + acc); else mma_commit_pair(tfull + acc);        // accumulator ready
+      if (CG == 1) mma_commit_w(tfull + acc); else mma_commit_pair_w(tfull + acc);        // accumulator ready
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 2) {
@@ -359,15 +360,28 @@ bool gemm_sm100_supported(const GemmDesc& g) {
 
 cudaError_t gemm_sm100(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   init_once();
-  // Pair tiles (256 x BN, cta_group::2) whenever M spans more than one 128-row tile; BN = 256 when
-  // that still gives at least one wave of work units, else 128.
-  int cg = g.M > BM ? 2 : 1;
-  if (g_force_cg) cg = g_force_cg;
-  const int units = g_num_sms / cg;
-  const int t256 = ((g.M + BM * cg - 1) / (BM * cg)) * ((g.N + 255) / 256);
-  const bool bn256 = g.N >= 256 && t256 >= units;
-  if (cg == 2) return bn256 ? launch_major<2, 256>(g, e, st) : launch_major<2, 128>(g, e, st);
-  return bn256 ? launch_major<1, 256>(g, e, st) : launch_major<1, 128>(g, e, st);
+  // Tile shape by a wave-quantisation cost model: every SM gets ceil(tiles / units) tiles of
+  // 128 x BN rows-per-SM work, divided by a per-shape efficiency (smaller tiles re-read more
+  // operand bytes per FLOP from L2 and issue smaller MMAs). Pair tiles (256 x BN, cta_group::2)
+  // need M > 128.
+  struct Cand { int cg, bn; double eff; };
+  static const Cand cands[4] = {{2, 256, 1.0}, {2, 128, 0.9}, {1, 256, 0.85}, {1, 128, 0.75}};
+  int best = -1;
+  double best_cost = 0;
+  for (int i = 0; i < 4; ++i) {
+    const Cand& c = cands[i];
+    if ((c.cg == 2 && g.M <= BM) || (g_force_cg && c.cg != g_force_cg)) continue;
+    const long units = g_num_sms / c.cg;
+    const long tiles = (long)((g.M + BM * c.cg - 1) / (BM * c.cg)) * ((g.N + c.bn - 1) / c.bn);
+    const double cost = (double)((tiles + units - 1) / units) * c.bn / c.eff;
+    if (best < 0 || cost < best_cost * 0.999) { best = i; best_cost = cost; }
+  }
+  switch (best) {
+    case 0: return launch_major<2, 256>(g, e, st);
+    case 1: return launch_major<2, 128>(g, e, st);
+    case 2: return launch_major<1, 256>(g, e, st);
+    default: return launch_major<1, 128>(g, e, st);
+  }
 }
 
 }  // namespace tp

@@ -15,7 +15,7 @@ for cfg in $CONFIGS; do
 import json, sys
 cfg, n = sys.argv[1], sys.argv[2]
 try:
-    d = json.load(open(f"gpurun_out/pipe_{cfg}_n{n}.json"))
+    d = json.loads([l for l in open(f"gpurun_out/pipe_{cfg}_n{n}.json") if l.startswith("{")][-1])
     g = d.get("gpipe") or {}
     print(cfg, "DP", d["config"]["slicing"], f'{d["ms_per_step"]:.1f} ms', f'mfu {d["mfu"]:.3f}',
           "| GPipe", f'{g.get("ms_per_step", float("nan")):.1f} ms', f'mfu {g.get("mfu", float("nan")):.3f}',
