@@ -34,9 +34,12 @@ constexpr uint32_t TILE = AT * AT * 2;    // one 128 x 128 bf16 tile (two 64-col
 constexpr uint32_t HALF = TILE / 2;       // 16 KiB: second 64-column atom
 constexpr float LOG2E_F = 1.4426950408889634f;
 
+// K and V in separate rings: K_j is released as soon as S_j is computed (3 stages), V_j after
+// O_j = P_j V_j (2 stages), so the loads run two key blocks ahead of the MMAs that need them.
+constexpr int NKS = 3, NVS = 2;
 struct FwdSmem {
-  static constexpr uint32_t Q = 0, K0 = TILE, V0 = 2 * TILE, K1 = 3 * TILE, V1 = 4 * TILE, P = 5 * TILE;
-  static constexpr uint32_t BAR = 6 * TILE;
+  static constexpr uint32_t Q = 0, K = TILE, V = K + NKS * TILE;
+  static constexpr uint32_t BAR = V + NVS * TILE;
   static constexpr uint32_t XCH = BAR + 256;  // fp32 [2 parity][2 halves][128 rows]: partial row maxima / sums
   static constexpr uint32_t BYTES = XCH + 3072 + 1024;  // + [2][128] partial sums
 };
@@ -123,14 +126,16 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   uint8_t* sm = smem_raw + ((1024u - (tc5::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + FwdSmem::BAR);
   uint64_t* qfull = bars + 0;
-  uint64_t* kvfull = bars + 1;   // [2]
-  uint64_t* kvfree = bars + 3;   // [2]
-  uint64_t* sfull = bars + 5;    // [2]
-  uint64_t* sfree = bars + 7;    // [2]
-  uint64_t* pfull = bars + 9;    // [2] P_j written into S buffer j%2
-  uint64_t* ofull = bars + 11;   // [2]
-  uint64_t* ofree = bars + 13;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  uint64_t* kfull = bars + 1;    // [3]
+  uint64_t* kfree = bars + 4;    // [3]
+  uint64_t* vfull = bars + 7;    // [2]
+  uint64_t* vfree = bars + 9;    // [2]
+  uint64_t* sfull = bars + 11;   // [2]
+  uint64_t* sfree = bars + 13;   // [2]
+  uint64_t* pfull = bars + 15;   // [2] P_j written into S buffer j%2
+  uint64_t* ofull = bars + 17;   // [2]
+  uint64_t* ofree = bars + 19;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // heaviest query tiles (the most key blocks) first: LPT order over the whole grid
@@ -142,8 +147,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(qfull, 1);
+    for (int i = 0; i < NKS; ++i) { mbar_init(kfull + i, 1); mbar_init(kfree + i, 1); }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(kvfull + i, 1); mbar_init(kvfree + i, 1);
+      mbar_init(vfull + i, 1); mbar_init(vfree + i, 1);
       mbar_init(sfull + i, 1); mbar_init(sfree + i, 1);
       mbar_init(ofull + i, 1); mbar_init(ofree + i, 8);
       mbar_init(pfull + i, 8);
@@ -162,16 +168,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     tma_load_4d(sm + FwdSmem::Q, &tmQ, 0, c + r0, head, sq, qfull);
     tma_load_4d(sm + FwdSmem::Q + HALF, &tmQ, 64, c + r0, head, sq, qfull);
     for (int j = 0; j < nkb; ++j) {
-      const int b = j & 1;
-      if (j >= 2) mbar_wait(kvfree + b, ((j >> 1) - 1) & 1);
+      const int bk = j % NKS, bv = j & 1;
+      if (j >= NKS) mbar_wait(kfree + bk, ((j / NKS) - 1) & 1);
       TRF(0, 0, j);
-      uint8_t* kd = sm + (b ? FwdSmem::K1 : FwdSmem::K0);
-      uint8_t* vd = sm + (b ? FwdSmem::V1 : FwdSmem::V0);
-      mbar_expect_tx(kvfull + b, 2 * TILE);
-      tma_load_4d(kd, &tmK, 0, j * AT, head, sq, kvfull + b);
-      tma_load_4d(kd + HALF, &tmK, 64, j * AT, head, sq, kvfull + b);
-      tma_load_4d(vd, &tmV, 0, j * AT, head, sq, kvfull + b);
-      tma_load_4d(vd + HALF, &tmV, 64, j * AT, head, sq, kvfull + b);
+      uint8_t* kd = sm + FwdSmem::K + bk * TILE;
+      mbar_expect_tx(kfull + bk, TILE);
+      tma_load_4d(kd, &tmK, 0, j * AT, head, sq, kfull + bk);
+      tma_load_4d(kd + HALF, &tmK, 64, j * AT, head, sq, kfull + bk);
+      if (j >= NVS) mbar_wait(vfree + bv, ((j >> 1) - 1) & 1);
+      uint8_t* vd = sm + FwdSmem::V + bv * TILE;
+      mbar_expect_tx(vfull + bv, TILE);
+      tma_load_4d(vd, &tmV, 0, j * AT, head, sq, vfull + bv);
+      tma_load_4d(vd + HALF, &tmV, 64, j * AT, head, sq, vfull + bv);
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (whole warp; one elected lane issues)
@@ -185,9 +193,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       mbar_wait(pfull + bi, (i >> 1) & 1);
       if (lane == 0) TRF(1, 3, i);
       if (i >= 2) mbar_wait(ofree + bi, ((i >> 1) - 1) & 1);
+      mbar_wait(vfull + bi, (i >> 1) & 1);
       if (lane == 0) TRF(1, 4, i);
       tc_fence_after();
-      const uint32_t v_base = smem_u32(sm + (bi ? FwdSmem::V1 : FwdSmem::V0));
+      const uint32_t v_base = smem_u32(sm + FwdSmem::V + bi * TILE);
 #pragma unroll
       for (int kk = 0; kk < AT / 16; ++kk) {
         const uint64_t bd = make_desc(v_base + kk * 2048, HALF, 1024);
@@ -195,24 +204,26 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       }
       mma_commit_w(ofull + bi);
       mma_commit_w(sfree + bi);
-      mma_commit_w(kvfree + bi);
+      mma_commit_w(vfree + bi);
       if (lane == 0) TRF(1, 5, i);
     };
     mbar_wait(qfull, 0);
     for (int j = 0; j < nkb; ++j) {
       const int b = j & 1;
-      mbar_wait(kvfull + b, (j >> 1) & 1);
+      const int bk = j % NKS;
+      mbar_wait(kfull + bk, (j / NKS) & 1);
       if (lane == 0) TRF(1, 0, j);
       if (j >= 2) mbar_wait(sfree + b, ((j >> 1) - 1) & 1);
       if (lane == 0) TRF(1, 1, j);
       tc_fence_after();
-      const uint32_t k_base = smem_u32(sm + (b ? FwdSmem::K1 : FwdSmem::K0));
+      const uint32_t k_base = smem_u32(sm + FwdSmem::K + bk * TILE);
 #pragma unroll
       for (int kk = 0; kk < AT / 16; ++kk) {
         const uint32_t off = (kk >> 2) * HALF + (kk & 3) * 32;
         mma_bf16_w(tmem + b * 128, make_desc(q_base + off, 16, 1024), make_desc(k_base + off, 16, 1024), idS, kk > 0);
       }
       mma_commit_w(sfull + b);
+      mma_commit_w(kfree + bk);
       if (lane == 0) TRF(1, 2, j);
       if (j >= 1) pv(j - 1);
     }
@@ -397,7 +408,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint64_t* dqfull = bars + 13;  // [2] dQ^T in TMEM
   uint64_t* dqfree = bars + 15;  // [2] dQ^T drained (4 warps)
   uint64_t* done = bars + 17;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* dpfull = bars + 18;  // [2] dP^T in TMEM buffer (sfull: S^T)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // heaviest key blocks (the most query tiles) first: blockIdx.y is the key block
@@ -410,7 +422,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     mbar_init(kvfull, 1);
     for (int i = 0; i < NQB; ++i) { mbar_init(qfull + i, 1); mbar_init(qfree + i, 1); }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(sfull + i, 1); mbar_init(pfull + i, 8); mbar_init(dsfree + i, 1);
+      mbar_init(sfull + i, 1); mbar_init(dpfull + i, 1); mbar_init(pfull + i, 8); mbar_init(dsfree + i, 1);
       mbar_init(dqfull + i, 1); mbar_init(dqfree + i, 4);
     }
     mbar_init(done, 1);
@@ -452,41 +464,50 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     constexpr uint32_t idQ = idesc_bf16(128, BQB, true, true);     // dQ^T (A = K MN-major, B = dS^T MN-major)
     const uint32_t k_base = smem_u32(sm + BwdSmem::K), v_base = smem_u32(sm + BwdSmem::V);
     mbar_wait(kvfull, 0);
-    // S^T / dP^T of tile j into TMEM buffer j & 1
-    auto issue_sdp = [&](int j) {
+    // Per tile j (TMEM buffer j & 1): S^T is issued as early as possible (the softmax warps start the
+    // exp2 work on it while dV / dK of the previous tile run), dP^T after dV / dK of j-1 (its
+    // columns held dQ^T of j-2, which the drain warps must have read).
+    auto issue_s = [&](int j) {
       const int bq = j % NQB, bb = j & 1;
-      const uint32_t q_base = smem_u32(sm + BwdSmem::Q + bq * QT), o_base = smem_u32(sm + BwdSmem::O + bq * QT);
-      const uint32_t tb = tmem + bb * 128;
+      const uint32_t q_base = smem_u32(sm + BwdSmem::Q + bq * QT);
       mbar_wait(qfull + bq, (j / NQB) & 1);
       if (lane == 0) TRC(1, 0, j);
       // buffer bb last held tile j-2: its S^T was read by the softmax (pfull(j-2), waited before
-      // the MMAs of j-2), its P^T by dV(j-2) (qfree(j-2)), its dQ^T by the drain (dqfree(j-2))
+      // the MMAs of j-2), its P^T by dV(j-2) (qfree(j-2))
       if (j >= 2) mbar_wait(qfree + (j - 2) % NQB, ((j - 2) / NQB) & 1);
       if (lane == 0) TRC(1, 1, j);
       tc_fence_after();
 #pragma unroll
       for (int kk = 0; kk < AT / 16; ++kk) {
         const uint32_t ok = (kk >> 2) * HALF + (kk & 3) * 32, oq = (kk >> 2) * QHALF + (kk & 3) * 32;
-        mma_bf16_w(tb, make_desc(k_base + ok, 16, 1024), make_desc(q_base + oq, 16, 1024), idS, kk > 0);
+        mma_bf16_w(tmem + bb * 128, make_desc(k_base + ok, 16, 1024), make_desc(q_base + oq, 16, 1024), idS, kk > 0);
       }
+      mma_commit_w(sfull + bb);
+      if (lane == 0) TRC(1, 5, j);
+    };
+    auto issue_dp = [&](int j) {
+      const int bq = j % NQB, bb = j & 1;
+      const uint32_t o_base = smem_u32(sm + BwdSmem::O + bq * QT);
       if (j >= 2) mbar_wait(dqfree + bb, ((j >> 1) - 1) & 1);
       if (lane == 0) TRC(1, 2, j);
       tc_fence_after();
 #pragma unroll
       for (int kk = 0; kk < AT / 16; ++kk) {
         const uint32_t ok = (kk >> 2) * HALF + (kk & 3) * 32, oq = (kk >> 2) * QHALF + (kk & 3) * 32;
-        mma_bf16_w(tb + 64, make_desc(v_base + ok, 16, 1024), make_desc(o_base + oq, 16, 1024), idS, kk > 0);
+        mma_bf16_w(tmem + bb * 128 + 64, make_desc(v_base + ok, 16, 1024), make_desc(o_base + oq, 16, 1024), idS,
+                   kk > 0);
       }
-      mma_commit_w(sfull + bb);
+      mma_commit_w(dpfull + bb);
     };
-    issue_sdp(0);
+    issue_s(0);
+    issue_dp(0);
     for (int i = 0; i < ntile; ++i) {
       const int bq = i % NQB, bb = i & 1;
       const uint32_t q_base = smem_u32(sm + BwdSmem::Q + bq * QT), o_base = smem_u32(sm + BwdSmem::O + bq * QT);
       const uint32_t ds_base = smem_u32(sm + BwdSmem::DS + bb * PT);
       const uint32_t tb = tmem + bb * 128;
       if (lane == 0) DBG(1, 100 + 10 * i);
-      if (i + 1 < ntile) issue_sdp(i + 1);
+      if (i + 1 < ntile) issue_s(i + 1);
       if (lane == 0) DBG(1, 101 + 10 * i);
       mbar_wait(pfull + bb, (i >> 1) & 1);
       if (lane == 0) TRC(1, 3, i);
@@ -500,6 +521,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                  (i | kk) != 0);
       }
       mma_commit_w(qfree + bq);
+      if (i + 1 < ntile) issue_dp(i + 1);
 #pragma unroll
       for (int kk = 0; kk < AT / 16; ++kk)
         mma_bf16_w(tb + 64, make_desc(k_base + kk * 2048, HALF, 1024), make_desc(ds_base + kk * 2048, 8192, 1024), idQ,
@@ -559,46 +581,64 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       if (threadIdx.x == 64) TRC(2, 1, i);
       mbar_wait(sfull + bb, (i >> 1) & 1);
       if (threadIdx.x == 64) TRC(2, 2, i);
-      if (i >= 2) mbar_wait(dsfree + bb, ((i >> 1) - 1) & 1);  // dK / dQ MMAs of tile i-2 read dS^T buffer bb
       tc_fence_after();
       // visible iff c + qr >= kabs (and qr < l, which Ls = +inf enforces)
       const int vis0 = kabs - c - qrow0 - half * HQ;  // first visible column of this key row, in this half
-      uint8_t* dSt = sm + BwdSmem::DS + bb * PT;
+      // phase 1 (needs S^T only): P^T = exp2(S^T scale - lse) -> registers and, packed, into TMEM
+      float pv[HQ];
 #pragma unroll
       for (int ch = 0; ch < 2; ++ch) {  // 16 query columns at a time
-        uint32_t rs[16], rp[16];
+        uint32_t rs[16];
         tmem_ld16_nowait(lane_base + bb * 128 + half * HQ + ch * 16, rs);
-        tmem_ld16_nowait(lane_base + bb * 128 + 64 + half * HQ + ch * 16, rp);
         const float4* L4 = reinterpret_cast<const float4*>(Ls + half * HQ + ch * 16);
-        const float4* D4 = reinterpret_cast<const float4*>(Ds + half * HQ + ch * 16);
-        float Lv[16], Dv[16];
+        float Lv[16];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const float4 a4 = L4[u], d4 = D4[u];
+          const float4 a4 = L4[u];
           Lv[4 * u] = a4.x; Lv[4 * u + 1] = a4.y; Lv[4 * u + 2] = a4.z; Lv[4 * u + 3] = a4.w;
-          Dv[4 * u] = d4.x; Dv[4 * u + 1] = d4.y; Dv[4 * u + 2] = d4.z; Dv[4 * u + 3] = d4.w;
         }
         tmem_wait_ld();
-        uint32_t pk[8], dk[8];
+        uint32_t pk[8];
 #pragma unroll
         for (int t = 0; t < 16; t += 2) {
-          float pv[2], dv[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int col = ch * 16 + t + e;
-            float p = ex2(fmaf(__uint_as_float(rs[t + e]), scale_log2, -Lv[t + e]));
-            p = col >= vis0 ? p : 0.f;
-            pv[e] = p;
-            dv[e] = p * (__uint_as_float(rp[t + e]) - Dv[t + e]);
+            const float p = ex2(fmaf(__uint_as_float(rs[t + e]), scale_log2, -Lv[t + e]));
+            pv[col] = col >= vis0 ? p : 0.f;
           }
-          __nv_bfloat162 hp = __floats2bfloat162_rn(pv[0], pv[1]);
-          __nv_bfloat162 hd = __floats2bfloat162_rn(dv[0], dv[1]);
+          __nv_bfloat162 hp = __floats2bfloat162_rn(pv[ch * 16 + t], pv[ch * 16 + t + 1]);
           pk[t >> 1] = *reinterpret_cast<uint32_t*>(&hp);
-          dk[t >> 1] = *reinterpret_cast<uint32_t*>(&hd);
         }
         // P^T (this half's 32 queries) packed into the first 16 of this half's own S^T columns;
         // this chunk's S^T columns were consumed above (the second chunk's lie at +16 .. +31)
         tmem_st8(lane_base + bb * 128 + half * HQ + ch * 8, pk);
+      }
+      // phase 2 (needs dP^T): dS^T = P^T (dP^T - D) -> bf16 -> smem (K-major swizzled)
+      mbar_wait(dpfull + bb, (i >> 1) & 1);
+      if (i >= 2) mbar_wait(dsfree + bb, ((i >> 1) - 1) & 1);  // dK / dQ MMAs of tile i-2 read dS^T buffer bb
+      tc_fence_after();
+      uint8_t* dSt = sm + BwdSmem::DS + bb * PT;
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        uint32_t rp[16];
+        tmem_ld16_nowait(lane_base + bb * 128 + 64 + half * HQ + ch * 16, rp);
+        const float4* D4 = reinterpret_cast<const float4*>(Ds + half * HQ + ch * 16);
+        float Dv[16];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 d4 = D4[u];
+          Dv[4 * u] = d4.x; Dv[4 * u + 1] = d4.y; Dv[4 * u + 2] = d4.z; Dv[4 * u + 3] = d4.w;
+        }
+        tmem_wait_ld();
+        uint32_t dk[8];
+#pragma unroll
+        for (int t = 0; t < 16; t += 2) {
+          const float d0 = pv[ch * 16 + t] * (__uint_as_float(rp[t]) - Dv[t]);
+          const float d1 = pv[ch * 16 + t + 1] * (__uint_as_float(rp[t + 1]) - Dv[t + 1]);
+          __nv_bfloat162 hd = __floats2bfloat162_rn(d0, d1);
+          dk[t >> 1] = *reinterpret_cast<uint32_t*>(&hd);
+        }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int cc = half * 4 + ch * 2 + u;
@@ -609,7 +649,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       tc_fence_before();
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive(pfull + bb);
+      if (lane == 0) { mbar_arrive(pfull + bb); TRC(3, warp - 2, i); }
       if (threadIdx.x == 64) TRC(2, 3, i);
     }
     if (lane == 0) DBG(2 + q, 900);
@@ -818,25 +858,27 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
   if (dbg_on) { memset(dbg, 0, 4096 * sizeof(int)); cudaHostGetDevicePointer(&dbg_dev, dbg, 0); }
   static int trace_left = getenv("TP_ATTN_TRACE") ? atoi(getenv("TP_ATTN_TRACE")) : 0;
   static long long* trace = nullptr;
-  if (trace_left > 0 && !trace) cudaMalloc(&trace, 3 * 8 * 64 * sizeof(long long));
-  if (trace_left > 0) cudaMemsetAsync(trace, 0, 3 * 8 * 64 * sizeof(long long), st);
+  if (trace_left > 0 && !trace) cudaMalloc(&trace, 4 * 8 * 64 * sizeof(long long));
+  if (trace_left > 0) cudaMemsetAsync(trace, 0, 4 * 8 * 64 * sizeof(long long), st);
   attn_bwd_sm100_kernel<<<grid, BWD_THREADS, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, mdq, mdk, mdv, Dvec,
                                                            s, c, l, scale, scale * LOG2E_F, accumulate,
                                                            a, dbg_dev, trace_left > 0 ? trace : nullptr);
   e = cudaGetLastError();
   if (trace_left > 0) {
     --trace_left;
-    long long h[3 * 8 * 64];
+    long long h[4 * 8 * 64];
     cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     long long t0 = h[(1 * 8 + 0) * 64];
-    for (int i = 0; i < 3 * 8 * 64; ++i) if (h[i] && h[i] < t0) t0 = h[i];
-    fprintf(stderr, "attn_bwd trace c=%d l=%d: tile | P:qfree-ok | M:qfull M:bufS M:bufdP M:pfull M:issued | S:stage S:bar S:sfull S:pfull S:dqfull S:dqred\n", c, l);
+    for (int i = 0; i < 4 * 8 * 64; ++i) if (h[i] && h[i] < t0) t0 = h[i];
+    fprintf(stderr, "attn_bwd trace c=%d l=%d: tile | P:qfree-ok | M:qfull M:bufS M:Sissued M:bufdP M:pfull M:issued | S:stage S:bar S:sfull S:pfull S:dqfull S:dqred\n", c, l);
     for (int i = 0; i < 64; ++i) {
       auto g = [&](int r, int e) { long long v = h[(r * 8 + e) * 64 + i]; return v ? (long long)(v - t0) : -1LL; };
       if (g(1, 0) < 0 && g(2, 0) < 0) break;
-      fprintf(stderr, "%3d | %7lld | %7lld %7lld %7lld %7lld %7lld | %7lld %7lld %7lld %7lld %7lld %7lld\n", i, g(0, 0), g(1, 0),
-              g(1, 1), g(1, 2), g(1, 3), g(1, 4), g(2, 0), g(2, 1), g(2, 2), g(2, 3), g(2, 4), g(2, 5));
+      fprintf(stderr, "%3d | %7lld | %7lld %7lld %7lld %7lld %7lld %7lld | %7lld %7lld %7lld %7lld %7lld %7lld | warps", i, g(0, 0), g(1, 0),
+              g(1, 1), g(1, 5), g(1, 2), g(1, 3), g(1, 4), g(2, 0), g(2, 1), g(2, 2), g(2, 3), g(2, 4), g(2, 5));
+      for (int w = 0; w < 8; ++w) fprintf(stderr, " %lld", g(3, w));
+      fprintf(stderr, "\n");
     }
     fprintf(stderr, "done-seen %lld  dkv-stored %lld\n", h[(2 * 8 + 6) * 64] - t0, h[(2 * 8 + 7) * 64] - t0);
   }

@@ -365,7 +365,9 @@ cudaError_t gemm_sm100(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   // operand bytes per FLOP from L2 and issue smaller MMAs). Pair tiles (256 x BN, cta_group::2)
   // need M > 128.
   struct Cand { int cg, bn; double eff; };
-  static const Cand cands[4] = {{2, 256, 1.0}, {2, 128, 0.9}, {1, 256, 0.85}, {1, 128, 0.75}};
+  // (efficiencies: per-SM operand bytes per MMA cycle are 64 / 96 / 96 / 128 B for the four shapes
+  // against the ~42 B/clk L2 share; calibrated with scripts/bench_kernels.py)
+  static const Cand cands[4] = {{2, 256, 1.0}, {2, 128, 0.8}, {1, 256, 0.8}, {1, 128, 0.65}};
   int best = -1;
   double best_cost = 0;
   for (int i = 0; i < 4; ++i) {
