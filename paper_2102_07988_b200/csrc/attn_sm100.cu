@@ -64,6 +64,17 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[1
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
                "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
@@ -336,6 +347,269 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         store8<bf16>(orow + i, v8);
       }
       if (half == 0) lse[(int64_t)head * s + c + r] = (m + log2f(ltot)) / LOG2E_F;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------ forward, two query tiles
+// Per (256 query rows = two 128-row tiles, head, sequence), LPT order. Each K_j / V_j block loaded
+// once serves both tiles. TMEM: S_0 (cols 0-127), S_1 (128-255), O_0 (256-383), O_1 (384-511).
+//   warp 0      TMA: Q_0, Q_1 once; K_j into a 3-deep ring, V_j into a 2-deep ring;
+//   warp 1      MMA (whole warp, one elected lane): per block j, S_t = Q_t K_j^T for both tiles, then
+//               O_t += P_t V_j (P_t read from TMEM where the softmax wrote it over S_t);
+//   warps 2-5   softmax of tile 0, warps 6-9 of tile 1: thread = query row (its TMEM lane), all 128
+//               scores of the block in registers, so the row max needs no exchange; P = exp2(S*scale
+//               - m_ref) packed as bf16 into TMEM. O stays in TMEM: it is rescaled (by the owning
+//               thread, warp-uniform decision) only when a row's max grows past m_ref + 8 (log2
+//               units), so P <= 256 and the common case has no O traffic at all.
+constexpr int F2_THREADS = 320;
+struct Fwd2Smem {
+  static constexpr uint32_t Q = 0, K = 2 * TILE, V = K + NKS * TILE;
+  static constexpr uint32_t BAR = V + NVS * TILE;
+  static constexpr uint32_t BYTES = BAR + 256 + 1024;
+  static_assert(BYTES <= 232448, "forward tile set exceeds 227 KB of shared memory");
+};
+constexpr float RESCALE_LOG2 = 8.f;
+
+__global__ void __launch_bounds__(F2_THREADS, 1)
+    attn_fwd2_sm100_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                           const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ o, int64_t ldo,
+                           float* __restrict__ lse, int s, int c, int l, float scale_log2, int64_t o_sstride,
+                           int64_t lse_sstride, long long* trace) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (tc5::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Fwd2Smem::BAR);
+  uint64_t* qfull = bars + 0;
+  uint64_t* kfull = bars + 1;    // [3]
+  uint64_t* kfree = bars + 4;    // [3]
+  uint64_t* vfull = bars + 7;    // [2]
+  uint64_t* vfree = bars + 9;    // [2]
+  uint64_t* sfull = bars + 11;   // [2 tiles]
+  uint64_t* pfull = bars + 13;   // [2 tiles] (4 warps each)
+  uint64_t* ofull = bars + 15;   // [2 tiles] O_t += P_t V_j complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int head = blockIdx.x, sq = blockIdx.y, r0 = (gridDim.z - 1 - blockIdx.z) * 2 * AT;
+  o += sq * o_sstride;
+  lse += sq * lse_sstride;
+  // key blocks of each tile: tile t covers rows [r0 + t*128, +128) of the slice (absolute c + ...)
+  const int ntiles = r0 + AT < l ? 2 : 1;
+  int nkb[2];
+  for (int t = 0; t < 2; ++t) nkb[t] = (c + min(l, r0 + (t + 1) * AT) - 1) / AT + 1;
+  const int nkbmax = nkb[ntiles - 1];
+
+  if (threadIdx.x == 0) {
+    mbar_init(qfull, 1);
+    for (int i = 0; i < NKS; ++i) { mbar_init(kfull + i, 1); mbar_init(kfree + i, 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(vfull + i, 1); mbar_init(vfree + i, 1);
+      mbar_init(sfull + i, 1); mbar_init(pfull + i, 4); mbar_init(ofull + i, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    mbar_expect_tx(qfull, 2 * TILE);
+    for (int t = 0; t < 2; ++t) {
+      tma_load_4d(sm + Fwd2Smem::Q + t * TILE, &tmQ, 0, c + r0 + t * AT, head, sq, qfull);
+      tma_load_4d(sm + Fwd2Smem::Q + t * TILE + HALF, &tmQ, 64, c + r0 + t * AT, head, sq, qfull);
+    }
+    for (int j = 0; j < nkbmax; ++j) {
+      const int bk = j % NKS, bv = j & 1;
+      if (j >= NKS) mbar_wait(kfree + bk, ((j / NKS) - 1) & 1);
+      uint8_t* kd = sm + Fwd2Smem::K + bk * TILE;
+      mbar_expect_tx(kfull + bk, TILE);
+      tma_load_4d(kd, &tmK, 0, j * AT, head, sq, kfull + bk);
+      tma_load_4d(kd + HALF, &tmK, 64, j * AT, head, sq, kfull + bk);
+      if (j >= NVS) mbar_wait(vfree + bv, ((j >> 1) - 1) & 1);
+      uint8_t* vd = sm + Fwd2Smem::V + bv * TILE;
+      mbar_expect_tx(vfull + bv, TILE);
+      tma_load_4d(vd, &tmV, 0, j * AT, head, sq, vfull + bv);
+      tma_load_4d(vd + HALF, &tmV, 64, j * AT, head, sq, vfull + bv);
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idS = idesc_bf16(128, 128, false, false);
+    constexpr uint32_t idO = idesc_bf16(128, 128, false, true);
+    // Issue order O_0 += P_0 V_j, S_0 = Q_0 K_{j+1}^T, O_1 += P_1 V_j, S_1 = Q_1 K_{j+1}^T: the two
+    // tiles' softmaxes alternate (ping-pong), each running while the tensor pipe works on the other
+    // tile's MMAs.
+    auto issue_s = [&](int t, int j) {  // S_t = Q_t K_j^T (K_j resident)
+      const uint32_t k_base = smem_u32(sm + Fwd2Smem::K + (j % NKS) * TILE);
+      const uint32_t q_base = smem_u32(sm + Fwd2Smem::Q + t * TILE);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < AT / 16; ++kk) {
+        const uint32_t off = (kk >> 2) * HALF + (kk & 3) * 32;
+        mma_bf16_w(tmem + t * 128, make_desc(q_base + off, 16, 1024), make_desc(k_base + off, 16, 1024), idS, kk > 0);
+      }
+      mma_commit_w(sfull + t);
+      if (lane == 0) TRF(1, 1 + t, j);
+    };
+    mbar_wait(qfull, 0);
+    mbar_wait(kfull, 0);
+    if (lane == 0) TRF(1, 0, 0);
+    for (int t = 0; t < ntiles; ++t) issue_s(t, 0);
+    mma_commit_w(kfree);
+    for (int j = 0; j < nkbmax; ++j) {
+      const int bv = j & 1;
+      const bool next_k = j + 1 < nkbmax;
+      bool k_waited = false;
+      mbar_wait(vfull + bv, (j >> 1) & 1);
+      const uint32_t v_base = smem_u32(sm + Fwd2Smem::V + bv * TILE);
+      for (int t = 0; t < ntiles; ++t) {
+        if (j >= nkb[t]) continue;
+        mbar_wait(pfull + t, j & 1);
+        if (lane == 0) TRF(1, 3 + t, j);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < AT / 16; ++kk)
+          mma_bf16_ts_w(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, make_desc(v_base + kk * 2048, HALF, 1024), idO,
+                        (j | kk) != 0);
+        mma_commit_w(ofull + t);
+        if (lane == 0) TRF(1, 5 + t, j);
+        if (j + 1 < nkb[t]) {
+          if (!k_waited) { mbar_wait(kfull + (j + 1) % NKS, ((j + 1) / NKS) & 1); k_waited = true; }
+          if (lane == 0) TRF(1, 0, j + 1);
+          // S_t's columns hold P_t until O_t += P_t V_j has completed
+          mbar_wait(ofull + t, j & 1);
+          issue_s(t, j + 1);
+        }
+      }
+      mma_commit_w(vfree + bv);
+      if (next_k) mma_commit_w(kfree + (j + 1) % NKS);
+    }
+  } else if (warp >= 2) {
+    // ---------------- softmax: tile t = (warp - 2) / 4, thread = query row of the tile
+    const int t = (warp - 2) >> 2, q = warp & 3, row = q * 32 + lane;
+    if (t < ntiles) {
+      const int qabs = c + r0 + t * AT + row;
+      const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+      const uint32_t s_col = t * 128, o_col = 256 + t * 128;
+      float m_ref = -INFINITY, lsum = 0.f;
+      for (int j = 0; j < nkb[t]; ++j) {
+        mbar_wait(sfull + t, j & 1);
+        if (row == 0) TRF(2 + t, 0, j);
+        tc_fence_after();
+        const int nvis = qabs - j * AT + 1;  // keys j*128 .. qabs of this block are visible
+        // only blocks crossing some row's diagonal need the element mask (warp-uniform branch)
+        const bool diag = __any_sync(0xffffffffu, nvis < AT);
+        // pass 1: row max over the block's 128 scores, two 32-column TMEM loads in flight, four
+        // independent max chains
+        float mx;
+        {
+          float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int ch = 0; ch < AT / 32; ch += 2) {
+            uint32_t r[2][32];
+            tmem_ld32_nowait(lane_base + s_col + ch * 32, r[0]);
+            tmem_ld32_nowait(lane_base + s_col + ch * 32 + 32, r[1]);
+            tmem_wait_ld();
+            if (diag) {
+#pragma unroll
+              for (int u = 0; u < 64; ++u)
+                m4[u & 3] = fmaxf(m4[u & 3], ch * 32 + u < nvis ? __uint_as_float(r[u >> 5][u & 31]) : -INFINITY);
+            } else {
+#pragma unroll
+              for (int u = 0; u < 64; ++u) m4[u & 3] = fmaxf(m4[u & 3], __uint_as_float(r[u >> 5][u & 31]));
+            }
+          }
+          mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        }
+        if (row == 0) TRF(2 + t, 1, j);
+        const float m_blk = mx * scale_log2;  // scale > 0 commutes with max
+        // lazy rescale: move the reference max only when it grew by more than 2^8
+        const bool grow = m_blk > m_ref + RESCALE_LOG2;
+        if (__any_sync(0xffffffffu, grow)) {
+          const float m_new = grow ? m_blk : m_ref;
+          const float f = ex2(m_ref - m_new);  // 0 on the first block (m_ref = -inf), 1 if unchanged
+          if (j >= 1) {
+            // O_t += P_t V_{j-1} must be complete before O is rewritten
+            mbar_wait(ofull + t, (j - 1) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int ch = 0; ch < AT / 32; ++ch) {
+              uint32_t r[32];
+              tmem_ld32_nowait(lane_base + o_col + ch * 32, r);
+              tmem_wait_ld();
+#pragma unroll
+              for (int u = 0; u < 32; ++u) r[u] = __float_as_uint(__uint_as_float(r[u]) * f);
+              tmem_st32(lane_base + o_col + ch * 32, r);
+            }
+            tmem_wait_st();
+          }
+          lsum *= f;
+          m_ref = m_new;
+        }
+        // pass 2: P = exp2(S * scale_log2 - m_ref) -> bf16, packed two per TMEM column over S_t
+        // (chunk pair ch's packed columns [ch*16, ch*16+32) lie inside S columns already re-read);
+        // four independent partial row sums
+        float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+        const float nm = -m_ref;
+#pragma unroll
+        for (int ch = 0; ch < AT / 32; ch += 2) {
+          uint32_t r[2][32], pk[32];
+          tmem_ld32_nowait(lane_base + s_col + ch * 32, r[0]);
+          tmem_ld32_nowait(lane_base + s_col + ch * 32 + 32, r[1]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int u = 0; u < 64; u += 2) {
+            float x0 = __uint_as_float(r[u >> 5][u & 31]), x1 = __uint_as_float(r[u >> 5][(u & 31) + 1]);
+            if (diag) {
+              x0 = ch * 32 + u < nvis ? x0 : -INFINITY;
+              x1 = ch * 32 + u + 1 < nvis ? x1 : -INFINITY;
+            }
+            const float p0 = ex2(fmaf(x0, scale_log2, nm));
+            const float p1 = ex2(fmaf(x1, scale_log2, nm));
+            rs4[(u >> 1) & 3] += p0 + p1;
+            __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+            pk[u >> 1] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          tmem_st32(lane_base + s_col + ch * 16, pk);
+        }
+        const float rs = (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+        lsum += rs;
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(pfull + t);
+        if (row == 0) TRF(2 + t, 2, j);
+      }
+      // epilogue: O / lsum -> bf16 rows, lse
+      mbar_wait(ofull + t, (nkb[t] - 1) & 1);
+      tc_fence_after();
+      const int r = r0 + t * AT + row;
+      const float inv = 1.f / lsum;
+      bf16* orow = o + (int64_t)r * ldo + head * AT;
+#pragma unroll 1
+      for (int ch = 0; ch < AT / 32; ++ch) {
+        uint32_t rr[32];
+        tmem_ld32_nowait(lane_base + o_col + ch * 32, rr);
+        tmem_wait_ld();
+        if (r < l) {
+#pragma unroll
+          for (int u = 0; u < 32; u += 8) {
+            float v8[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v8[e] = __uint_as_float(rr[u + e]) * inv;
+            store8<bf16>(orow + ch * 32 + u, v8);
+          }
+        }
+      }
+      if (r < l) lse[(int64_t)head * s + c + r] = (m_ref + log2f(lsum)) / LOG2E_F;
     }
   }
   tc_fence_before();
@@ -777,6 +1051,40 @@ cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o,
   if (!encode_bf16_map(&mq, q, 4, dims, strides, box) || !encode_bf16_map(&mk, k, 4, dims, strides, box) ||
       !encode_bf16_map(&mv, v, 4, dims, strides, box))
     return cudaErrorInvalidValue;
+  static const bool v1 = getenv("TP_ATTN_FWD_V1") != nullptr;
+  if (!v1) {
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaError_t e = cudaFuncSetAttribute(attn_fwd2_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)Fwd2Smem::BYTES);
+      if (e != cudaSuccess) return e;
+      attr2 = true;
+    }
+    dim3 grid2(a, nseq, (l + 2 * AT - 1) / (2 * AT));
+    static int trace2_left = getenv("TP_ATTN_TRACE") ? atoi(getenv("TP_ATTN_TRACE")) : 0;
+    static long long* trace2 = nullptr;
+    if (trace2_left > 0 && !trace2) cudaMalloc(&trace2, 4 * 8 * 64 * sizeof(long long));
+    if (trace2_left > 0) cudaMemsetAsync(trace2, 0, 4 * 8 * 64 * sizeof(long long), st);
+    attn_fwd2_sm100_kernel<<<grid2, F2_THREADS, Fwd2Smem::BYTES, st>>>(mq, mk, mv, o, ldo, lse, s, c, l,
+                                                                      rsqrtf((float)d) * LOG2E_F, o_sstride, lse_sstride,
+                                                                      trace2_left > 0 ? trace2 : nullptr);
+    if (trace2_left > 0) {
+      --trace2_left;
+      long long h[4 * 8 * 64];
+      cudaMemcpyAsync(h, trace2, sizeof(h), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      long long t0 = 0;
+      for (int i = 0; i < 4 * 8 * 64; ++i) if (h[i] && (!t0 || h[i] < t0)) t0 = h[i];
+      fprintf(stderr, "attn_fwd2 trace c=%d l=%d: kb | M:kfull M:S0 M:S1 M:pfull0 M:pfull1 M:PV0 M:PV1 | T0:sfull T0:max T0:pfull | T1:sfull T1:max T1:pfull\n", c, l);
+      for (int i = 0; i < 64; ++i) {
+        auto g = [&](int r, int e) { long long v = h[(r * 8 + e) * 64 + i]; return v ? (long long)(v - t0) : -1LL; };
+        if (g(1, 0) < 0) break;
+        fprintf(stderr, "%3d | %7lld %7lld %7lld %7lld %7lld %7lld %7lld | %7lld %7lld %7lld | %7lld %7lld %7lld\n", i,
+                g(1, 0), g(1, 1), g(1, 2), g(1, 3), g(1, 4), g(1, 5), g(1, 6), g(2, 0), g(2, 1), g(2, 2), g(3, 0), g(3, 1), g(3, 2));
+      }
+    }
+    return cudaGetLastError();
+  }
   dim3 grid(a, nseq, (l + AT - 1) / AT);
   static int trace_left = getenv("TP_ATTN_TRACE") ? atoi(getenv("TP_ATTN_TRACE")) : 0;
   static long long* trace = nullptr;
