@@ -111,6 +111,21 @@ __device__ __forceinline__ void mma_bf16_ts_w(uint32_t d_tmem, uint32_t a_tmem, 
       : "memory");
 }
 
+// 2^x on the FMA/ALU pipes (no MUFU): round-to-nearest split x = j + f (|f| <= 1/2) with the 1.5*2^23
+// magic constant, degree-3 minimax polynomial for 2^f (max relative error 1.03e-4, well below the
+// bf16 rounding P goes through), 2^j added to the exponent field (j >= -125 keeps the result a
+// normal number: 2^f >= 2^-1/2); exactly 0 below 2^-125 (masked scores are -inf). Used for a quarter
+// of the softmax elements to offload the 16/clk/SM MUFU pipe.
+__device__ __forceinline__ float ex2_poly(float x) {
+  const float xc = fmaxf(x, -125.f);
+  const float t = xc + 12582912.f;
+  const float j = t - 12582912.f;
+  const float f = xc - j;
+  const float p = fmaf(fmaf(fmaf(0.05592203564723278f, f, 0.24264008283277078f), f, 0.6931210339915522f), f,
+                       0.9999244814555215f);
+  const float r = __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+  return x < -125.f ? 0.f : r;
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -368,6 +383,69 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 //               - m_ref) packed as bf16 into TMEM. O stays in TMEM: it is rescaled (by the owning
 //               thread, warp-uniform decision) only when a row's max grows past m_ref + 8 (log2
 //               units), so P <= 256 and the common case has no O traffic at all.
+// Softmax inner loops, specialised on whether the block crosses the causal diagonal (the mask test
+// costs two instructions per element, so the common unmasked case gets its own loop).
+template <bool MASK>
+__device__ __forceinline__ void row_max_chunk(const uint32_t (&r)[2][32], int col0, int nvis, float (&m4)[4]) {
+#pragma unroll
+  for (int u = 0; u < 64; ++u) {
+    const float x = __uint_as_float(r[u >> 5][u & 31]);
+    m4[u & 3] = fmaxf(m4[u & 3], MASK && col0 + u >= nvis ? -INFINITY : x);
+  }
+}
+template <bool MASK>
+__device__ __forceinline__ void exp_max_chunk(const uint32_t (&r)[32], int col0, int nvis, float scale_log2, float nm,
+                                              float (&rs4)[4], float (&m4)[4], uint32_t (&pk)[64], int pk0) {
+#pragma unroll
+  for (int u = 0; u < 32; u += 2) {
+    float x0 = __uint_as_float(r[u]), x1 = __uint_as_float(r[u + 1]);
+    if (MASK) {
+      x0 = col0 + u < nvis ? x0 : -INFINITY;
+      x1 = col0 + u + 1 < nvis ? x1 : -INFINITY;
+    }
+    m4[(u >> 1) & 3] = fmaxf(m4[(u >> 1) & 3], fmaxf(x0, x1));
+    const float p0 = ex2(fmaf(x0, scale_log2, nm));
+    const float p1 = ex2(fmaf(x1, scale_log2, nm));
+    rs4[(u >> 1) & 3] += p0 + p1;
+    __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+    pk[pk0 + (u >> 1)] = *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+template <bool MASK>
+__device__ __forceinline__ void exp_max_chunk16(const uint32_t (&r)[32], int col0, int nvis, float scale_log2,
+                                                float nm, float (&rs4)[4], float (&m4)[4], uint32_t (&pk)[16]) {
+#pragma unroll
+  for (int u = 0; u < 32; u += 2) {
+    float x0 = __uint_as_float(r[u]), x1 = __uint_as_float(r[u + 1]);
+    if (MASK) {
+      x0 = col0 + u < nvis ? x0 : -INFINITY;
+      x1 = col0 + u + 1 < nvis ? x1 : -INFINITY;
+    }
+    const float p0 = ex2(fmaf(x0, scale_log2, nm));
+    const float p1 = ex2(fmaf(x1, scale_log2, nm));
+    rs4[(u >> 1) & 3] += p0 + p1;
+    __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+    pk[u >> 1] = *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+template <bool MASK>
+__device__ __forceinline__ void exp_chunk(const uint32_t (&r)[32], int col0, int nvis, float scale_log2, float nm,
+                                          float (&rs4)[4], uint32_t (&pk)[16]) {
+#pragma unroll
+  for (int u = 0; u < 32; u += 2) {
+    float x0 = __uint_as_float(r[u]), x1 = __uint_as_float(r[u + 1]);
+    if (MASK) {
+      x0 = col0 + u < nvis ? x0 : -INFINITY;
+      x1 = col0 + u + 1 < nvis ? x1 : -INFINITY;
+    }
+    const float p0 = ex2(fmaf(x0, scale_log2, nm));
+    const float p1 = ex2(fmaf(x1, scale_log2, nm));
+    rs4[(u >> 1) & 3] += p0 + p1;
+    __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+    pk[u >> 1] = *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+
 constexpr int F2_THREADS = 320;
 struct Fwd2Smem {
   static constexpr uint32_t Q = 0, K = 2 * TILE, V = K + NKS * TILE;
@@ -484,7 +562,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
         if (j + 1 < nkb[t]) {
           if (!k_waited) { mbar_wait(kfull + (j + 1) % NKS, ((j + 1) / NKS) & 1); k_waited = true; }
           if (lane == 0) TRF(1, 0, j + 1);
-          // S_t's columns hold P_t until O_t += P_t V_j has completed
+          // S_t's columns hold P_t, read by O_t += P_t V_j just issued; S_{j+1} overwrites them only
+          // after that MMA has completed (measured: the wait is off the critical path)
           mbar_wait(ofull + t, j & 1);
           issue_s(t, j + 1);
         }
@@ -507,30 +586,36 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
         const int nvis = qabs - j * AT + 1;  // keys j*128 .. qabs of this block are visible
         // only blocks crossing some row's diagonal need the element mask (warp-uniform branch)
         const bool diag = __any_sync(0xffffffffu, nvis < AT);
-        // pass 1: row max over the block's 128 scores, two 32-column TMEM loads in flight, four
-        // independent max chains
-        float mx;
-        {
-          float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        // One pass over the block's 128 scores: P = exp2(S * scale_log2 - m_ref) into registers (packed
+        // bf16) while tracking the row max. P is written to TMEM (over S) only after the whole row is
+        // read, so the rare case where the max outgrew m_ref + 8 (and always the first block) can
+        // rescale O and recompute P from the intact S.
+        float rs4[4] = {0.f, 0.f, 0.f, 0.f}, m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        uint32_t pk[64];
+        const float nm = -m_ref;
+        if (j > 0) {
+#pragma unroll
+          for (int ch = 0; ch < AT / 32; ++ch) {
+            uint32_t r[32];
+            tmem_ld32_nowait(lane_base + s_col + ch * 32, r);
+            tmem_wait_ld();
+            if (diag) exp_max_chunk<true>(r, ch * 32, nvis, scale_log2, nm, rs4, m4, pk, ch * 16);
+            else exp_max_chunk<false>(r, ch * 32, nvis, scale_log2, nm, rs4, m4, pk, ch * 16);
+          }
+        } else {
+          // first block: only the max (m_ref = -inf would make every P infinite)
 #pragma unroll
           for (int ch = 0; ch < AT / 32; ch += 2) {
             uint32_t r[2][32];
             tmem_ld32_nowait(lane_base + s_col + ch * 32, r[0]);
             tmem_ld32_nowait(lane_base + s_col + ch * 32 + 32, r[1]);
             tmem_wait_ld();
-            if (diag) {
-#pragma unroll
-              for (int u = 0; u < 64; ++u)
-                m4[u & 3] = fmaxf(m4[u & 3], ch * 32 + u < nvis ? __uint_as_float(r[u >> 5][u & 31]) : -INFINITY);
-            } else {
-#pragma unroll
-              for (int u = 0; u < 64; ++u) m4[u & 3] = fmaxf(m4[u & 3], __uint_as_float(r[u >> 5][u & 31]));
-            }
+            if (diag) row_max_chunk<true>(r, ch * 32, nvis, m4);
+            else row_max_chunk<false>(r, ch * 32, nvis, m4);
           }
-          mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
         }
         if (row == 0) TRF(2 + t, 1, j);
-        const float m_blk = mx * scale_log2;  // scale > 0 commutes with max
+        const float m_blk = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;  // scale > 0
         // lazy rescale: move the reference max only when it grew by more than 2^8
         const bool grow = m_blk > m_ref + RESCALE_LOG2;
         if (__any_sync(0xffffffffu, grow)) {
@@ -553,34 +638,31 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
           }
           lsum *= f;
           m_ref = m_new;
-        }
-        // pass 2: P = exp2(S * scale_log2 - m_ref) -> bf16, packed two per TMEM column over S_t
-        // (chunk pair ch's packed columns [ch*16, ch*16+32) lie inside S columns already re-read);
-        // four independent partial row sums
-        float rs4[4] = {0.f, 0.f, 0.f, 0.f};
-        const float nm = -m_ref;
+          // recompute P with the new reference
+          const float nm2 = -m_ref;
 #pragma unroll
-        for (int ch = 0; ch < AT / 32; ch += 2) {
-          uint32_t r[2][32], pk[32];
-          tmem_ld32_nowait(lane_base + s_col + ch * 32, r[0]);
-          tmem_ld32_nowait(lane_base + s_col + ch * 32 + 32, r[1]);
-          tmem_wait_ld();
+          for (int i = 0; i < 4; ++i) rs4[i] = 0.f;
 #pragma unroll
-          for (int u = 0; u < 64; u += 2) {
-            float x0 = __uint_as_float(r[u >> 5][u & 31]), x1 = __uint_as_float(r[u >> 5][(u & 31) + 1]);
-            if (diag) {
-              x0 = ch * 32 + u < nvis ? x0 : -INFINITY;
-              x1 = ch * 32 + u + 1 < nvis ? x1 : -INFINITY;
-            }
-            const float p0 = ex2(fmaf(x0, scale_log2, nm));
-            const float p1 = ex2(fmaf(x1, scale_log2, nm));
-            rs4[(u >> 1) & 3] += p0 + p1;
-            __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
-            pk[u >> 1] = *reinterpret_cast<uint32_t*>(&h);
+          for (int ch = 0; ch < AT / 32; ++ch) {
+            uint32_t r[32];
+            tmem_ld32_nowait(lane_base + s_col + ch * 32, r);
+            tmem_wait_ld();
+            uint32_t pk16[16];
+            float mm[4];
+            exp_max_chunk16<true>(r, ch * 32, nvis, scale_log2, nm2, rs4, mm, pk16);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) pk[ch * 16 + u] = pk16[u];
           }
-          tmem_st32(lane_base + s_col + ch * 16, pk);
         }
         const float rs = (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+        // P (bf16, two per column) over S_t's first 64 columns
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t pk16[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) pk16[u] = pk[ch * 16 + u];
+          tmem_st16(lane_base + s_col + ch * 16, pk16);
+        }
         lsum += rs;
         tmem_wait_st();
         tc_fence_before();
