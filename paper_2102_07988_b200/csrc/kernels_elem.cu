@@ -72,15 +72,22 @@ __global__ void __launch_bounds__(NT) ln_fwd_kernel(const float* __restrict__ x,
   }
 }
 
+// out[0..3] += (a, b, c, d) as one 16-byte L2 reduction (sm_90+ vector red)
+__device__ __forceinline__ void red_add4(float* out, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(out), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
 // dx = resid + rstd * (dxhat - mean(dxhat) - xhat * mean(dxhat * xhat)),  dxhat = dy * gamma.
 // A CTA handles `rpb` consecutive rows and keeps its dgamma/dbeta partial sums in registers, so the
-// fp32 atomics are one per column per CTA (not per row).
+// fp32 reductions are one per column per CTA (not per row). The next row's dy / x / stats are
+// loaded before the current row's block reduction, so the HBM latency overlaps the barrier.
 template <typename T, int NT, int NCH>
 __global__ void __launch_bounds__(NT) ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
                                                     const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
                                                     const float* __restrict__ gam, const float* __restrict__ resid,
                                                     float* __restrict__ dx_out, T* __restrict__ dx_copy,
-                                                    float* __restrict__ ws, int rows, int H, int rpb) {
+                                                    float* __restrict__ dgam, float* __restrict__ dbet, int rows,
+                                                    int H, int rpb) {
   __shared__ float red[2][2][NT / 32];
   const int tid = threadIdx.x;
   float g[NCH][8], pg[NCH][8], pb[NCH][8];
@@ -92,20 +99,36 @@ __global__ void __launch_bounds__(NT) ln_bwd_kernel(const float* __restrict__ dy
     for (int i = 0; i < 8; ++i) { pg[c][i] = 0.f; pb[c][i] = 0.f; if (col >= H) g[c][i] = 0.f; }
   }
   const int r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
-  for (int r = r0; r < r1; ++r) {
-    const float mean = mean_in[r], rstd = rstd_in[r];
-    float d[NCH][8], xh[NCH][8];
-    float s1 = 0.f, s2 = 0.f;
+  float nd[NCH][8], nx[NCH][8], nres[NCH][8], nmean = 0.f, nrstd = 0.f;  // row r+1, prefetched
+  auto fetch = [&](int r) {
+    if (r >= r1) return;
+    nmean = mean_in[r];
+    nrstd = rstd_in[r];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
       const int col = (c * NT + tid) * 8;
       if (col < H) {
-        load8<float>(dy + (int64_t)r * H + col, d[c]);
-        load8<float>(x + (int64_t)r * H + col, xh[c]);
+        load8<float>(dy + (int64_t)r * H + col, nd[c]);
+        load8<float>(x + (int64_t)r * H + col, nx[c]);
+        if (resid) load8<float>(resid + (int64_t)r * H + col, nres[c]);
       } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) { d[c][i] = 0.f; xh[c][i] = 0.f; }
+        for (int i = 0; i < 8; ++i) { nd[c][i] = 0.f; nx[c][i] = 0.f; }
       }
+    }
+  };
+  fetch(r0);
+  for (int r = r0; r < r1; ++r) {
+    const float mean = nmean, rstd = nrstd;
+    float d[NCH][8], xh[NCH][8], rs[NCH][8];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { d[c][i] = nd[c][i]; xh[c][i] = nx[c][i]; rs[c][i] = resid ? nres[c][i] : 0.f; }
+    fetch(r + 1);
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         xh[c][i] = (xh[c][i] - mean) * rstd;
@@ -131,32 +154,25 @@ __global__ void __launch_bounds__(NT) ln_bwd_kernel(const float* __restrict__ dy
     for (int c = 0; c < NCH; ++c) {
       const int col = (c * NT + tid) * 8;
       if (col < H) {
-        float o[8], rs[8];
-        if (resid) load8<float>(resid + (int64_t)r * H + col, rs);
+        float o[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = rstd * (d[c][i] * g[c][i] - m1 - xh[c][i] * m2) + (resid ? rs[i] : 0.f);
+        for (int i = 0; i < 8; ++i) o[i] = rstd * (d[c][i] * g[c][i] - m1 - xh[c][i] * m2) + rs[c][i];
         store8<float>(dx_out + (int64_t)r * H + col, o);
         if (dx_copy) store8<T>(dx_copy + (int64_t)r * H + col, o);
       }
     }
   }
-  // per-CTA partial sums to the workspace [gridDim.x][2][H] (reduced by ln_bwd_reduce_kernel)
-  float* wg = ws + (int64_t)blockIdx.x * 2 * H;
+  // per-CTA partial dgamma / dbeta added in L2 (16-byte vector reductions; no workspace pass)
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     const int col = (c * NT + tid) * 8;
-    if (col < H) { store8<float>(wg + col, pg[c]); store8<float>(wg + H + col, pb[c]); }
+    if (col < H) {
+      red_add4(dgam + col, pg[c][0], pg[c][1], pg[c][2], pg[c][3]);
+      red_add4(dgam + col + 4, pg[c][4], pg[c][5], pg[c][6], pg[c][7]);
+      red_add4(dbet + col, pb[c][0], pb[c][1], pb[c][2], pb[c][3]);
+      red_add4(dbet + col + 4, pb[c][4], pb[c][5], pb[c][6], pb[c][7]);
+    }
   }
-}
-
-// dgamma[n] += sum_b ws[b][0][n], dbeta[n] += sum_b ws[b][1][n] (one writer per column).
-__global__ void ln_bwd_reduce_kernel(const float* __restrict__ ws, int nb, float* __restrict__ dgam,
-                                     float* __restrict__ dbet, int H) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= 2 * H) return;
-  float t = 0.f;
-  for (int b = 0; b < nb; ++b) t += ws[(int64_t)b * 2 * H + n];
-  if (n < H) dgam[n] += t; else dbet[n - H] += t;
 }
 
 // ---------------------------------------------------------------- embedding
@@ -318,18 +334,15 @@ cudaError_t layernorm_bwd(const float* dy, const float* x, const float* mean, co
   if (rows == 0) return cudaSuccess;
   const int rpb = std::max(4, (rows + 4 * 148 - 1) / (4 * 148));
   const int grid = (rows + rpb - 1) / rpb;
-#define LNB(NT, NCH) ln_bwd_kernel<T, NT, NCH><<<grid, NT, 0, st>>>(dy, x, mean, rstd, gam, resid, dx_out, dx_copy, ws, rows, H, rpb)
+  (void)ws;
+#define LNB(NT, NCH) ln_bwd_kernel<T, NT, NCH><<<grid, NT, 0, st>>>(dy, x, mean, rstd, gam, resid, dx_out, dx_copy, dgam, dbet, rows, H, rpb)
   if (H <= 2048) LNB(256, 1);
   else if (H <= 4096) LNB(256, 2);
   else if (H <= 6144) LNB(256, 3);
   else if (H <= 12288) LNB(512, 3);
   else return cudaErrorInvalidValue;
 #undef LNB
-  // dgamma += column sums of the per-CTA partials ws[grid][0][H], dbeta of ws[grid][1][H]
-  cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess) e = colsum_accum<float>(ws, 2 * (int64_t)H, dgam, grid, H, st);
-  if (e == cudaSuccess) e = colsum_accum<float>(ws + H, 2 * (int64_t)H, dbet, grid, H, st);
-  return e;
+  return cudaGetLastError();
 }
 cudaError_t embed_fwd(const int32_t* tok, const float* wte, const float* wpe, float* h, int c, int l, int b, int s,
                       int H, int V, cudaStream_t st) {
