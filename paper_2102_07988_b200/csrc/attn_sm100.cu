@@ -738,8 +738,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     attn_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                           const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                           const __grid_constant__ CUtensorMap tmdQ, const __grid_constant__ CUtensorMap tmdK,
-                          const __grid_constant__ CUtensorMap tmdV, const float* __restrict__ ldg,
-                          float* __restrict__ dq_red, int s, int c, int l,
+                          const __grid_constant__ CUtensorMap tmdV, const float* __restrict__ ldg, int s, int c, int l,
                           float scale, float scale_log2, int accumulate, int nheads, volatile int* dbg,
                           long long* trace) {
   extern __shared__ uint8_t smem_raw[];
@@ -897,30 +896,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     float* dqs = reinterpret_cast<float*>(sm + BwdSmem::DQ);
     const bool leader = threadIdx.x == 320;
-    if (dq_red) {
-      // variant (TP_ATTN_DQ_RED=1): coalesced fp32 L2 reductions straight from registers, no staging
-      // (for a fixed query the 32 lanes of a warp add 32 consecutive floats of one dq_acc row)
-      const int H = nheads * AT;
-      float* base = dq_red + (int64_t)sq * l * H + head * AT + row;
-      for (int j = 0; j < ntile; ++j) {
-        const int bb = j & 1, q0 = (qt0 + j) * BQB;
-        mbar_wait(dqfull + bb, (j >> 1) & 1);
-        tc_fence_after();
-        uint32_t r[2][32];
-        tmem_ld32_nowait(lane_base + bb * 128 + 64, r[0]);
-        tmem_ld32_nowait(lane_base + bb * 128 + 96, r[1]);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(dqfree + bb);
-#pragma unroll
-        for (int t = 0; t < BQB; ++t)
-          if (q0 + t < l)
-            asm volatile("red.global.add.f32 [%0], %1;" ::"l"(base + (int64_t)(q0 + t) * H),
-                         "f"(__uint_as_float(r[t >> 5][t & 31]) * scale)
-                         : "memory");
-      }
-    } else
     for (int j = 0; j < ntile; ++j) {
       const int bb = j & 1;
       if (leader) tma_wait_reads();  // the previous reduce has finished reading the staging tile
@@ -1271,13 +1246,12 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
   }
   int* dbg_dev = nullptr;
   if (dbg_on) { memset(dbg, 0, 4096 * sizeof(int)); cudaHostGetDevicePointer(&dbg_dev, dbg, 0); }
-  static const bool dq_red_on = getenv("TP_ATTN_DQ_RED") != nullptr;
   static int trace_left = getenv("TP_ATTN_TRACE") ? atoi(getenv("TP_ATTN_TRACE")) : 0;
   static long long* trace = nullptr;
   if (trace_left > 0 && !trace) cudaMalloc(&trace, 4 * 8 * 64 * sizeof(long long));
   if (trace_left > 0) cudaMemsetAsync(trace, 0, 4 * 8 * 64 * sizeof(long long), st);
   attn_bwd_sm100_kernel<<<grid, BWD_THREADS, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, mdq, mdk, mdv, Dvec,
-                                                           dq_red_on ? dq_acc : nullptr, s, c, l, scale, scale * LOG2E_F, accumulate,
+                                                           s, c, l, scale, scale * LOG2E_F, accumulate,
                                                            a, dbg_dev, trace_left > 0 ? trace : nullptr);
   e = cudaGetLastError();
   if (trace_left > 0) {

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 import paper_2102_07988_b200 as tp
-from gpu_util import rel
+from tests.gpu_util import rel
 from oracle.model import gpt_forward_backward
 from synth import CONFIGS, make_stage_flat, make_tokens, round_bf16, unpack_all_stages
 
