@@ -248,84 +248,56 @@ __global__ void __launch_bounds__(512) ce_kernel(T* __restrict__ z, const int32_
   }
 }
 
-// Same contract, one CTA (512 threads) per row with the row held in registers as packed bf16
-// (16-byte loads / stores, <= 16 chunks of 8 per thread: V <= 65536): one HBM read and one write
-// of the logits instead of three scalar passes.
-template <int NCHK>
+// Same contract for bf16 logits with 16-byte accesses (V % 8 == 0): pass 1 reads the row once from
+// HBM with an online (max, sum) per thread, pass 2 re-reads it (L2-resident: one 100 KB row per CTA)
+// and writes the gradient in place.
 __global__ void __launch_bounds__(512) ce_vec_kernel(bf16* __restrict__ z, const int32_t* __restrict__ tok, int c,
                                                      int b, int seq_len, float* __restrict__ loss_rows,
                                                      float* __restrict__ zcopy, int V, float scale) {
-  __shared__ float red[16];
+  __shared__ float rm[16], rs[16];
   const int r = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   bf16* zr = z + (int64_t)r * V;
-  const int nch = V / 8;  // V % 8 == 0
-  uint4 raw[NCHK];
-  float m = -INFINITY;
+  const int nch = V / 8;
+  float m = -INFINITY, s = 0.f;
+  for (int ch = tid; ch < nch; ch += 512) {
+    float v[8];
+    load8<bf16>(zr + ch * 8, v);
+    if (zcopy) store8<float>(zcopy + (int64_t)r * V + ch * 8, v);
+    float cm = v[0];
 #pragma unroll
-  for (int k = 0; k < NCHK; ++k) {
-    const int ch = k * 512 + tid;
-    if (ch < nch) {
-      raw[k] = *reinterpret_cast<const uint4*>(zr + ch * 8);
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[k]);
-      float v[8];
+    for (int i = 1; i < 8; ++i) cm = fmaxf(cm, v[i]);
+    const float mn = fmaxf(m, cm);
+    float cs = 0.f;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) { const float2 f = __bfloat1622float2(h[i]); v[2 * i] = f.x; v[2 * i + 1] = f.y; }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) m = fmaxf(m, v[i]);
-      if (zcopy) {
-        float4* zc = reinterpret_cast<float4*>(zcopy + (int64_t)r * V + ch * 8);
-        zc[0] = make_float4(v[0], v[1], v[2], v[3]);
-        zc[1] = make_float4(v[4], v[5], v[6], v[7]);
-      }
-    }
+    for (int i = 0; i < 8; ++i) cs += __expf(v[i] - mn);
+    s = s * __expf(m - mn) + cs;  // m = -inf on the first chunk: exp(-inf) = 0
+    m = mn;
   }
-  m = warp_max(m);
-  if (lane == 0) red[wid] = m;
-  __syncthreads();
-  float M = red[0];
 #pragma unroll
-  for (int w = 1; w < 16; ++w) M = fmaxf(M, red[w]);
-  __syncthreads();
-  float sacc = 0.f;
-#pragma unroll
-  for (int k = 0; k < NCHK; ++k) {
-    const int ch = k * 512 + tid;
-    if (ch < nch) {
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[k]);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 f = __bfloat1622float2(h[i]);
-        sacc += __expf(f.x - M) + __expf(f.y - M);
-      }
-    }
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const float mn = fmaxf(m, m2);
+    s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mn));
+    m = mn;
   }
-  sacc = warp_sum(sacc);
-  if (lane == 0) red[wid] = sacc;
+  if (lane == 0) { rm[wid] = m; rs[wid] = s; }
   __syncthreads();
+  float M = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < 16; ++w) M = fmaxf(M, rm[w]);
   float S = 0.f;
 #pragma unroll
-  for (int w = 0; w < 16; ++w) S += red[w];
+  for (int w = 0; w < 16; ++w) S += rs[w] * __expf(rm[w] - M);
   const float lse = M + logf(S);
   const int y = tok[(int64_t)(r % b) * (seq_len + 1) + c + r / b + 1];  // target = next token (A-8)
   if (tid == 0) loss_rows[r] = lse - __bfloat162float(zr[y]);
   __syncthreads();  // z[y] read before the row is overwritten
+  for (int ch = tid; ch < nch; ch += 512) {
+    float v[8];
+    load8<bf16>(zr + ch * 8, v);
 #pragma unroll
-  for (int k = 0; k < NCHK; ++k) {
-    const int ch = k * 512 + tid;
-    if (ch < nch) {
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[k]);
-      uint4 outv;
-      __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(&outv);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 f = __bfloat1622float2(h[i]);
-        const int col = ch * 8 + 2 * i;
-        const float g0 = (__expf(f.x - lse) - (col == y ? 1.f : 0.f)) * scale;
-        const float g1 = (__expf(f.y - lse) - (col + 1 == y ? 1.f : 0.f)) * scale;
-        o[i] = __floats2bfloat162_rn(g0, g1);
-      }
-      *reinterpret_cast<uint4*>(zr + ch * 8) = outv;
-    }
+    for (int i = 0; i < 8; ++i) v[i] = (__expf(v[i] - lse) - (ch * 8 + i == y ? 1.f : 0.f)) * scale;
+    store8<bf16>(zr + ch * 8, v);
   }
 }
 
@@ -442,8 +414,8 @@ cudaError_t ce_fwd_bwd(T* logits, const int32_t* tok, int c, int b, int s, float
                        int rows, int V, float scale, cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
   if constexpr (std::is_same<T, bf16>::value) {
-    if (V % 8 == 0 && V <= 512 * 8 * 16 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0) {
-      ce_vec_kernel<16><<<rows, 512, 0, st>>>(logits, tok, c, b, s, loss_rows, logits_copy, V, scale);
+    if (V % 8 == 0 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0) {
+      ce_vec_kernel<<<rows, 512, 0, st>>>(logits, tok, c, b, s, loss_rows, logits_copy, V, scale);
       return cudaGetLastError();
     }
   }
