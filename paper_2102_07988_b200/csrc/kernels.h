@@ -34,8 +34,8 @@ cudaError_t layernorm_fwd(const float* x, const float* gam, const float* bet, T*
 template <typename T>
 cudaError_t layernorm_bwd(const float* dy, const float* x, const float* mean, const float* rstd,
                           const float* gam, const float* resid, float* dx_out, T* dx_copy,
-                          float* dgam, float* dbet, float* ws /* >= 2*H*ceil(rows/4) floats */, int rows, int H,
-                          cudaStream_t st);
+                          float* dgam, float* dbet, float* ws /* unused */, int rows, int H, cudaStream_t st,
+                          float* dbias = nullptr /* += column sums of dx_out (the upstream bias gradient) */);
 
 // Job rows m = 0..b*l-1 map to (sequence j = m % b, position p = c + m / b); tok points at the job's
 // first sequence row of tokens[B][s+1].

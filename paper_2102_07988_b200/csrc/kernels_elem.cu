@@ -86,17 +86,17 @@ __global__ void __launch_bounds__(NT) ln_bwd_kernel(const float* __restrict__ dy
                                                     const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
                                                     const float* __restrict__ gam, const float* __restrict__ resid,
                                                     float* __restrict__ dx_out, T* __restrict__ dx_copy,
-                                                    float* __restrict__ dgam, float* __restrict__ dbet, int rows,
-                                                    int H, int rpb) {
+                                                    float* __restrict__ dgam, float* __restrict__ dbet,
+                                                    float* __restrict__ dbias, int rows, int H, int rpb) {
   __shared__ float red[2][2][NT / 32];
   const int tid = threadIdx.x;
-  float g[NCH][8], pg[NCH][8], pb[NCH][8];
+  float g[NCH][8], pg[NCH][8], pb[NCH][8], pd[NCH][8];
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     const int col = (c * NT + tid) * 8;
     if (col < H) load8<float>(gam + col, g[c]);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) { pg[c][i] = 0.f; pb[c][i] = 0.f; if (col >= H) g[c][i] = 0.f; }
+    for (int i = 0; i < 8; ++i) { pg[c][i] = 0.f; pb[c][i] = 0.f; pd[c][i] = 0.f; if (col >= H) g[c][i] = 0.f; }
   }
   const int r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
   float nd[NCH][8], nx[NCH][8], nres[NCH][8], nmean = 0.f, nrstd = 0.f;  // row r+1, prefetched
@@ -156,7 +156,10 @@ __global__ void __launch_bounds__(NT) ln_bwd_kernel(const float* __restrict__ dy
       if (col < H) {
         float o[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = rstd * (d[c][i] * g[c][i] - m1 - xh[c][i] * m2) + rs[c][i];
+        for (int i = 0; i < 8; ++i) {
+          o[i] = rstd * (d[c][i] * g[c][i] - m1 - xh[c][i] * m2) + rs[c][i];
+          pd[c][i] += o[i];
+        }
         store8<float>(dx_out + (int64_t)r * H + col, o);
         if (dx_copy) store8<T>(dx_copy + (int64_t)r * H + col, o);
       }
@@ -171,6 +174,10 @@ __global__ void __launch_bounds__(NT) ln_bwd_kernel(const float* __restrict__ dy
       red_add4(dgam + col + 4, pg[c][4], pg[c][5], pg[c][6], pg[c][7]);
       red_add4(dbet + col, pb[c][0], pb[c][1], pb[c][2], pb[c][3]);
       red_add4(dbet + col + 4, pb[c][4], pb[c][5], pb[c][6], pb[c][7]);
+      if (dbias) {
+        red_add4(dbias + col, pd[c][0], pd[c][1], pd[c][2], pd[c][3]);
+        red_add4(dbias + col + 4, pd[c][4], pd[c][5], pd[c][6], pd[c][7]);
+      }
     }
   }
 }
@@ -383,12 +390,12 @@ cudaError_t layernorm_fwd(const float* x, const float* gam, const float* bet, T*
 template <typename T>
 cudaError_t layernorm_bwd(const float* dy, const float* x, const float* mean, const float* rstd, const float* gam,
                           const float* resid, float* dx_out, T* dx_copy, float* dgam, float* dbet, float* ws, int rows,
-                          int H, cudaStream_t st) {
+                          int H, cudaStream_t st, float* dbias) {
   if (rows == 0) return cudaSuccess;
   const int rpb = std::max(4, (rows + 4 * 148 - 1) / (4 * 148));
   const int grid = (rows + rpb - 1) / rpb;
   (void)ws;
-#define LNB(NT, NCH) ln_bwd_kernel<T, NT, NCH><<<grid, NT, 0, st>>>(dy, x, mean, rstd, gam, resid, dx_out, dx_copy, dgam, dbet, rows, H, rpb)
+#define LNB(NT, NCH) ln_bwd_kernel<T, NT, NCH><<<grid, NT, 0, st>>>(dy, x, mean, rstd, gam, resid, dx_out, dx_copy, dgam, dbet, dbias, rows, H, rpb)
   if (H <= 2048) LNB(256, 1);
   else if (H <= 4096) LNB(256, 2);
   else if (H <= 6144) LNB(256, 3);
@@ -451,7 +458,8 @@ cudaError_t colsum_accum(const T* src, int64_t ld, float* out, int rows, int N, 
   template cudaError_t layernorm_fwd<T>(const float*, const float*, const float*, T*, float*, float*, int, int, \
                                         cudaStream_t);                                                      \
   template cudaError_t layernorm_bwd<T>(const float*, const float*, const float*, const float*, const float*,   \
-                                        const float*, float*, T*, float*, float*, float*, int, int, cudaStream_t); \
+                                        const float*, float*, T*, float*, float*, float*, int, int, cudaStream_t,  \
+                                        float*);                                                                \
   template cudaError_t ce_fwd_bwd<T>(T*, const int32_t*, int, int, int, float*, float*, int, int, float,    \
                                      cudaStream_t);                                                        \
   template cudaError_t convert_f32<T>(const float*, T*, int64_t, cudaStream_t);                            \

@@ -546,7 +546,8 @@ class Engine final : public EngineBase {
       TRY(gemm(KC_GEMM_DX, gd(Tn, H, V, S.Z + row * V, V, false, S.wout_io, V, false), e));
       TRY(launch(KC_LN, 0, (12.0 + ebytes) * Tn * H, [&] {
         return layernorm_bwd<T>(S.dA, S.hs[S.nl] + row * H, S.stf + row, S.stf + (size_t)batch * s + row, P + S.L.s_lnf_g, nullptr, gr,
-                                S.dhout_b[S.nl - 1] + row * H, S.gflat + S.L.lnf_g, S.gflat + S.L.lnf_b, S.lnws, Tn, H, stream);
+                                S.dhout_b[S.nl - 1] + row * H, S.gflat + S.L.lnf_g, S.gflat + S.L.lnf_b, S.lnws, Tn, H, stream,
+                                S.gflat + S.L.layers[S.nl - 1].b_2);
       }));
     } else {
       TRY(launch(KC_MISC, 0, (4.0 + ebytes) * Tn * H, [&] {
@@ -566,7 +567,7 @@ class Engine final : public EngineBase {
       float* st2 = S.st2[j];
       TRY(launch(KC_LN, 0, (16.0 + ebytes) * Tn * H, [&] {
         return layernorm_bwd<T>(S.dA, S.hmid[j] + row * H, st2 + row, st2 + (size_t)batch * s + row, P + fs.ln2_g, gr, S.gm,
-                                S.dhmid_b[j] + row * H, GR + f.ln2_g, GR + f.ln2_b, S.lnws, Tn, H, stream);
+                                S.dhmid_b[j] + row * H, GR + f.ln2_g, GR + f.ln2_b, S.lnws, Tn, H, stream, GR + f.b_o);
       }));
       // attention: dO = dh_mid W_o^T, then slice-vs-prefix attention backward with dK/dV push
       Epi e3; e3.kind = EPI_STORE; e3.out = S.dO; e3.ldo = H;
@@ -619,7 +620,8 @@ class Engine final : public EngineBase {
       float* st1 = S.st1[j];
       TRY(launch(KC_LN, 0, (16.0 + ebytes) * Tn * H, [&] {
         return layernorm_bwd<T>(S.dA, S.hs[j] + row * H, st1 + row, st1 + (size_t)batch * s + row, P + fs.ln1_g, S.gm, gnext, copy,
-                                GR + f.ln1_g, GR + f.ln1_b, S.lnws, Tn, H, stream);
+                                GR + f.ln1_g, GR + f.ln1_b, S.lnws, Tn, H, stream,
+                                j == 0 ? nullptr : GR + S.L.layers[j - 1].b_2);
       }));
       gr = gnext;
     }
@@ -659,11 +661,13 @@ class Engine final : public EngineBase {
       e.out = GR + f.w_2; e.ldo = H;
       TRY(gemm(KC_GEMM_DW, G(4 * H, H, S.G[j] + row0 * 4 * H, 4 * H, S.dhout_b[j] + row0 * H, H), e, st));
       Pending p;
-      instr.begin(st, KC_MISC, 0, sizeof(T) * 9.0 * K * H, p);
+      instr.begin(st, KC_MISC, 0, sizeof(T) * 7.0 * K * H, p);
+      // b_o and b_2 are summed by the LayerNorm backward that produces their dY (fused column sums),
+      // except b_2 of a non-last stage's last layer, whose dY arrives from the next stage
       cudaError_t r = colsum_accum<T>(S.dQKV[j] + row0 * 3 * H, 3 * H, GR + f.b_qkv, K, 3 * H, st);
-      if (r == cudaSuccess) r = colsum_accum<T>(S.dhmid_b[j] + row0 * H, H, GR + f.b_o, K, H, st);
       if (r == cudaSuccess) r = colsum_accum<T>(S.dU[j] + row0 * 4 * H, 4 * H, GR + f.b_1, K, 4 * H, st);
-      if (r == cudaSuccess) r = colsum_accum<T>(S.dhout_b[j] + row0 * H, H, GR + f.b_2, K, H, st);
+      if (r == cudaSuccess && j == S.nl - 1 && S.k != m.K - 1)
+        r = colsum_accum<T>(S.dhout_b[j] + row0 * H, H, GR + f.b_2, K, H, st);
       instr.end(st, p);
       if (r != cudaSuccess) return fail(TP_ECUDA, "bias grads: %s", cudaGetErrorString(r));
     }
