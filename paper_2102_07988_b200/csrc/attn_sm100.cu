@@ -111,21 +111,6 @@ __device__ __forceinline__ void mma_bf16_ts_w(uint32_t d_tmem, uint32_t a_tmem, 
       : "memory");
 }
 
-// 2^x on the FMA/ALU pipes (no MUFU): round-to-nearest split x = j + f (|f| <= 1/2) with the 1.5*2^23
-// magic constant, degree-3 minimax polynomial for 2^f (max relative error 1.03e-4, well below the
-// bf16 rounding P goes through), 2^j added to the exponent field (j >= -125 keeps the result a
-// normal number: 2^f >= 2^-1/2); exactly 0 below 2^-125 (masked scores are -inf). Used for a quarter
-// of the softmax elements to offload the 16/clk/SM MUFU pipe.
-__device__ __forceinline__ float ex2_poly(float x) {
-  const float xc = fmaxf(x, -125.f);
-  const float t = xc + 12582912.f;
-  const float j = t - 12582912.f;
-  const float f = xc - j;
-  const float p = fmaf(fmaf(fmaf(0.05592203564723278f, f, 0.24264008283277078f), f, 0.6931210339915522f), f,
-                       0.9999244814555215f);
-  const float r = __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-  return x < -125.f ? 0.f : r;
-}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -428,24 +413,6 @@ __device__ __forceinline__ void exp_max_chunk16(const uint32_t (&r)[32], int col
     pk[u >> 1] = *reinterpret_cast<uint32_t*>(&h);
   }
 }
-template <bool MASK>
-__device__ __forceinline__ void exp_chunk(const uint32_t (&r)[32], int col0, int nvis, float scale_log2, float nm,
-                                          float (&rs4)[4], uint32_t (&pk)[16]) {
-#pragma unroll
-  for (int u = 0; u < 32; u += 2) {
-    float x0 = __uint_as_float(r[u]), x1 = __uint_as_float(r[u + 1]);
-    if (MASK) {
-      x0 = col0 + u < nvis ? x0 : -INFINITY;
-      x1 = col0 + u + 1 < nvis ? x1 : -INFINITY;
-    }
-    const float p0 = ex2(fmaf(x0, scale_log2, nm));
-    const float p1 = ex2(fmaf(x1, scale_log2, nm));
-    rs4[(u >> 1) & 3] += p0 + p1;
-    __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
-    pk[u >> 1] = *reinterpret_cast<uint32_t*>(&h);
-  }
-}
-
 constexpr int F2_THREADS = 320;
 struct Fwd2Smem {
   static constexpr uint32_t Q = 0, K = 2 * TILE, V = K + NKS * TILE;
