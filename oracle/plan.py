@@ -13,6 +13,9 @@ Objective (Eq. 5, generalised by reading A-20 to D jobs per sl
     T(l_1..l_M) = D * sum_i t_i + (K - 1) * max_i t_i,   t_i = t(l_i, sum_{j<i} l_j).
 D = 1 is exactly the paper's Eq. 5.
 
+Joint batch x token plan (reading A-20b): joint_optimize == joint_brute_force on
+random integer instances (tests/test_oracle_plan.py).
+
 Parity status: pinned (tests/test_oracle_plan.py) — optimize() == brute_force() exactly on
 random integer instances; SPEC.md:146-147 worked examples (T = 4, T = 10); closed form ==
 flow-shop simulation (SPEC.md:253-264 examples and random vectors); epsilon gap <= K*eps
@@ -139,6 +142,106 @@ def brute_force(t: np.ndarray, n: int, K: int, D: int = 1) -> Tuple[int, int, Li
             best = key
     T, m, rev = best
     return T, m, list(reversed(rev))
+
+
+# ---------------------------------------------------------------- joint batch x token plan
+# PAPER.md:362-364 (§3.4): run the DP for every batch-slice size b, then choose b_1 + .. + b_D = B
+# (a 1-D knapsack). Reading A-20b: all D groups' jobs are pipelined back to back, so the objective
+# of a batch plan {(b_d, l^d)} is  sum_d sum_i t_{b_d}(l^d_i, c^d_i) + (K - 1) * max over all jobs,
+# i.e. the fill/drain bubble is paid once for the whole batch (A-20 with heterogeneous groups; a
+# uniform plan [(b, l)] * D is exactly tp_plan's D * sum + (K - 1) * max).
+
+def joint_objective(tables, plan: Sequence[Tuple[int, Sequence[int]]], K: int) -> int:
+    ts = [x for b, lengths in plan for x in slice_costs(tables[b], lengths)]
+    return sum(ts) + (K - 1) * max(ts)
+
+
+def joint_candidates(tables, n: int, eps: int = 0) -> List[int]:
+    """Union over b of the per-table candidates, thinned as in candidates()."""
+    vals = sorted({v for t in tables.values() for v in candidates(t, n, 0)})
+    if eps <= 0:
+        return vals
+    out: List[int] = []
+    for v in vals:
+        if not out or v >= out[-1] + eps:
+            out.append(v)
+    if out[-1] != vals[-1]:
+        out.append(vals[-1])
+    return out
+
+
+def knapsack(costs, B: int):
+    """C(0) = 0, C(m) = min_{b <= m, costs[b] finite} C(m - b) + costs[b] (PAPER.md:364 '1D
+    knapsack'); ties keep the smallest b. Returns (C(B), [b_1, b_2, ..]) by backtracking from B, or
+    None if B cannot be composed."""
+    C: List[Optional[int]] = [None] * (B + 1)
+    choice = [0] * (B + 1)
+    C[0] = 0
+    for m in range(1, B + 1):
+        for b in sorted(costs):
+            if b > m or costs[b] is None or C[m - b] is None:
+                continue
+            v = C[m - b] + costs[b]
+            if C[m] is None or v < C[m]:
+                C[m], choice[m] = v, b
+    if C[B] is None:
+        return None
+    parts, m = [], B
+    while m > 0:
+        parts.append(choice[m])
+        m -= choice[m]
+    return C[B], parts
+
+
+def joint_optimize(tables, n: int, B: int, K: int, eps: int = 0):
+    """For each t_max candidate (ascending): Algorithm 1 per batch-slice size b (the smallest sum
+    S*_b with every slice <= t_max), the knapsack over b, and the exact objective of the resulting
+    plan; keep strict improvements; stop once K * t_max >= best (any plan whose largest job is
+    >= t_max costs at least max + (K - 1) * max). Returns (T, [(b_d, lengths_d), ..])."""
+    best = None
+    for tau in joint_candidates(tables, n, eps):
+        if best is not None and K * tau >= best[0]:
+            break
+        per_b, schemes = {}, {}
+        for b, t in tables.items():
+            r = dp_fixed_tmax(t, n, tau)
+            per_b[b] = None if r is None else r[0]
+            if r is not None:
+                schemes[b] = r[1]
+        ks = knapsack(per_b, B)
+        if ks is None:
+            continue
+        plan = [(b, schemes[b]) for b in ks[1]]
+        T = joint_objective(tables, plan, K)
+        if best is None or T < best[0]:
+            best = (T, plan)
+    if best is None:
+        raise ValueError("infeasible: no batch plan")
+    return best
+
+
+def partitions(B: int, parts: Sequence[int], max_part: Optional[int] = None) -> Iterable[Tuple[int, ...]]:
+    """Non-increasing partitions of B into the allowed part sizes."""
+    if B == 0:
+        yield ()
+        return
+    for p in sorted(parts, reverse=True):
+        if p <= B and (max_part is None or p <= max_part):
+            for rest in partitions(B - p, parts, p):
+                yield (p,) + rest
+
+
+def joint_brute_force(tables, n: int, B: int, K: int) -> int:
+    """The definition of the joint optimum: every partition of B into the available batch-slice
+    sizes, every slicing of every group, scored with the A-20b objective. Returns the minimum T."""
+    comps = list(compositions(n))
+    best = None
+    for parts in partitions(B, list(tables)):
+        for choice in itertools.product(comps, repeat=len(parts)):
+            T = joint_objective(tables, list(zip(parts, choice)), K)
+            if best is None or T < best:
+                best = T
+    return best
 
 
 def uniform_schemes(n: int) -> List[List[int]]:

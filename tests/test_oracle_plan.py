@@ -128,3 +128,55 @@ def test_tiny_config_dp_equals_c_brute_force_2pow31(c_brute):
     rng = np.random.default_rng(32)
     t = gpu_like_table(32, rng, knee=4, base_ns=10_000, per_unit_ns=900, ctx_ns=300)
     assert c_brute(t, 32, 2, 1) == op.optimize(t, 32, 2, 1)
+
+
+# ---------------------------------------------------------------- joint batch x token plan
+from oracle.plan import (joint_brute_force, joint_objective, joint_optimize, knapsack,  # noqa: E402
+                         partitions)
+
+
+def test_knapsack_spec_example():
+    # T_1 = 5, T_2 = 8 -> C(2) = min(T_2, 2 T_1) = 8, partition [2]
+    assert knapsack({1: 5, 2: 8}, 2) == (8, [2])
+    # ties keep the smallest b: T_2 = 2 T_1 exactly -> all ones
+    assert knapsack({1: 4, 2: 8}, 2) == (8, [1, 1])
+    assert knapsack({2: 3}, 3) is None
+
+
+def test_partitions_count():
+    # p(6) over parts {1..6} = 11; parts {1, 2} of 6: 4 (2+2+2, 2+2+1+1, 2+1*4, 1*6)
+    assert len(list(partitions(6, [1, 2, 3, 4, 5, 6]))) == 11
+    assert len(list(partitions(6, [1, 2]))) == 4
+
+
+def _monotone_tables(rng, n, bs):
+    # per-b tables: larger b costs more per job (b sequences), context makes later slices dearer
+    base = rng.integers(1, 20, size=(n, n + 1)).astype(np.int64)
+    return {b: base * b + rng.integers(0, 5 * b, size=(n, n + 1)) for b in bs}
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_joint_optimize_equals_brute_force(seed):
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(1, 5))
+    B = int(rng.integers(1, 5))
+    K = int(rng.integers(1, 5))
+    bs = sorted(set(int(x) for x in rng.integers(1, B + 1, size=rng.integers(1, 3)))) or [1]
+    if 1 not in bs:
+        bs = [1] + bs  # every B is composable
+    tables = _monotone_tables(rng, n, bs)
+    T, plan = joint_optimize(tables, n, B, K)
+    assert sum(b for b, _ in plan) == B and all(sum(l) == n for _, l in plan)
+    assert T == joint_objective(tables, plan, K)
+    assert T == joint_brute_force(tables, n, B, K)
+
+
+def test_joint_reduces_to_uniform_objective():
+    # a single allowed batch-slice size b: the joint plan is [(b, l)] * (B / b) with the tp_plan
+    # objective D * sum + (K - 1) * max (reading A-20)
+    rng = np.random.default_rng(7)
+    n, K, B, b = 5, 3, 4, 2
+    t = rng.integers(1, 30, size=(n, n + 1)).astype(np.int64)
+    T, plan = joint_optimize({b: t}, n, B, K)
+    T_u, _, lengths = op.optimize(t, n, K, D=B // b)
+    assert T == T_u and [x for x, _ in plan] == [b, b]
