@@ -106,6 +106,39 @@ typedef struct {
 tp_status tp_plan(int32_t n_layer, int32_t hidden, int32_t seq_len, int32_t n_stages,
                   const tp_cost_table* cost, int32_t n_micro, int64_t eps_ticks, tp_slicing* out);
 
+/* A batch plan [(b_1, l^1), (b_2, l^2), ..]: group d is b_d consecutive
+ * sequences x its own token slicing l^d (multiples of g, sum = seq_len); sum_d b_d = batch. Groups
+ * run in order d = 1..D, each group's jobs in slice order (GPipe order, A-21). All arrays
+ * caller-owned: batch_slice[] / n_slices[] hold `capacity_groups` entries, lengths[] (the groups'
+ * slicings concatenated) holds `capacity_lengths`. A uniform tp_slicing is the plan with D = batch/b
+ * identical groups. */
+typedef struct {
+  int32_t n_groups;          /* D                                                      */
+  int32_t capacity_groups;   /* size of batch_slice[] and n_slices[]                   */
+  int32_t* batch_slice;      /* b_1..b_D                                               */
+  int32_t* n_slices;         /* M_1..M_D                                               */
+  int32_t capacity_lengths;  /* size of lengths[]                                      */
+  int32_t* lengths;          /* l^1_1..l^1_{M_1}, l^2_1.., in tokens                    */
+  int64_t t_max_ticks;       /* max over all jobs of the plan (tp_plan_joint output)   */
+  int64_t predicted_ticks;   /* sum over all jobs + (K-1) * max (A-20b)      */
+} tp_batch_plan;
+
+/* Joint batch x token planning: cost tables costs[i] of jobs of b_values[i]
+ * sequences (tp_profile with batch_slice = b_values[i], all with the same granularity); chooses
+ * b_1 + .. + b_D = batch and a slicing per group minimising the exact pipelined makespan
+ * sum_jobs t + (K-1) * max_jobs t (A-20b: the bubble is paid once for the whole batch).
+ * For each t_max candidate (the union of the tables' distinct values, ascending, eps-thinned, the
+ * largest always kept): Algorithm 1 per table, then the 1-D knapsack C(m) = min_b C(m-b) + S*_b
+ * (smallest b wins ties), then the exact objective of the plan; strict improvements only; stop
+ * once K * t_max >= best. eps_ticks = 0 is the exact optimum (pinned to brute force over all
+ * partitions x slicings). Groups are returned in knapsack backtrack order from m = batch. Output:
+ * out->capacity_groups >= batch, out->capacity_lengths >= batch * seq_len / g.
+ * Errors: TP_EINVAL (shapes, tables, capacities, duplicate b), TP_EINFEASIBLE (batch not a sum of
+ * the available b). Pure, deterministic, thread-safe. */
+tp_status tp_plan_joint(int32_t n_layer, int32_t hidden, int32_t seq_len, int32_t n_stages, int32_t n_b,
+                        const int32_t* b_values, const tp_cost_table* const* costs, int32_t batch,
+                        int64_t eps_ticks, tp_batch_plan* out);
+
 /* Number of float32 parameters of stage `stage` (see "Parameter layout"). */
 tp_status tp_stage_param_count(const tp_model_cfg* cfg, int32_t stage, size_t* out);
 
@@ -145,6 +178,17 @@ tp_status tp_step(tp_ctx* ctx, const tp_slicing* slicing, const int32_t* tokens,
 /* Same as tp_step with DEVICE tokens (already resident in HBM on this context's device). */
 tp_status tp_step_device(tp_ctx* ctx, const tp_slicing* slicing, const int32_t* dev_tokens,
                          int32_t batch, float* loss_out);
+
+/* tp_step with a heterogeneous batch plan (tp_plan_joint's output): group d is
+ * sequences [b_1+..+b_{d-1}, +b_d) with its own token slicing; forward jobs run group by group,
+ * each in slice order, backward in exact reverse. sum b_d must equal batch <= max_batch; every
+ * group's lengths must be positive and sum to seq_len (TP_EINVAL otherwise). Same tokens / loss /
+ * gradient contract as tp_step (a uniform tp_slicing is the plan of batch/b identical groups). */
+tp_status tp_step_plan(tp_ctx* ctx, const tp_batch_plan* plan, const int32_t* tokens, int32_t batch,
+                       float* loss_out);
+/* Same with DEVICE tokens. */
+tp_status tp_step_plan_device(tp_ctx* ctx, const tp_batch_plan* plan, const int32_t* dev_tokens, int32_t batch,
+                              float* loss_out);
 
 /* Copies the last step's gradients (same layout as tp_load_params) to host_out[n]. */
 tp_status tp_get_grads(tp_ctx* ctx, float* host_out, size_t n);

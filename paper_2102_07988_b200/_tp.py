@@ -17,7 +17,7 @@ TP_OK, TP_EINVAL, TP_EINFEASIBLE, TP_ETOOBIG, TP_ECUDA, TP_ENCCL, TP_ENOMEM, TP_
 TP_BF16, TP_FP32 = 0, 1
 TP_FLAG_KEEP_LOGITS, TP_FLAG_KERNEL_STATS, TP_FLAG_FORCE_SIMT = 1, 2, 4
 
-EXPORTED = ["tp_plan", "tp_stage_param_count", "tp_nccl_unique_id", "tp_init", "tp_param_count",
+EXPORTED = ["tp_plan", "tp_plan_joint", "tp_step_plan", "tp_step_plan_device", "tp_stage_param_count", "tp_nccl_unique_id", "tp_init", "tp_param_count",
             "tp_load_params", "tp_step", "tp_step_device", "tp_get_grads", "tp_get_logits",
             "tp_profile", "tp_get_stream", "tp_kernel_stats", "tp_kernel_stats_reset", "tp_kernel_stats_enable",
             "tp_last_step_launches", "tp_destroy", "tp_last_error"]
@@ -46,6 +46,12 @@ class SlicingC(C.Structure):
                 ("predicted_ticks", C.c_int64)]
 
 
+class BatchPlanC(C.Structure):
+    _fields_ = [("n_groups", C.c_int32), ("capacity_groups", C.c_int32), ("batch_slice", C.POINTER(C.c_int32)),
+                ("n_slices", C.POINTER(C.c_int32)), ("capacity_lengths", C.c_int32),
+                ("lengths", C.POINTER(C.c_int32)), ("t_max_ticks", C.c_int64), ("predicted_ticks", C.c_int64)]
+
+
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} not built — run `python -c 'import __graft_entry__ as g; g.build()'` "
@@ -55,6 +61,10 @@ def _load() -> C.CDLL:
     sigs = {
         "tp_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(CostTableC), C.c_int32,
                               C.c_int64, C.POINTER(SlicingC)]),
+        "tp_plan_joint": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                                    C.POINTER(C.POINTER(CostTableC)), C.c_int32, C.c_int64, C.POINTER(BatchPlanC)]),
+        "tp_step_plan": (C.c_int, [P, C.POINTER(BatchPlanC), P, C.c_int32, C.POINTER(C.c_float)]),
+        "tp_step_plan_device": (C.c_int, [P, C.POINTER(BatchPlanC), P, C.c_int32, C.POINTER(C.c_float)]),
         "tp_stage_param_count": (C.c_int, [C.POINTER(ModelCfgC), C.c_int32, C.POINTER(C.c_size_t)]),
         "tp_nccl_unique_id": (C.c_int, [P]),
         "tp_init": (C.c_int, [C.POINTER(ModelCfgC), C.c_int32, C.c_int32, P, C.c_int32, C.c_int32, C.c_int32,
@@ -140,6 +150,72 @@ def plan(ticks: np.ndarray, granularity: int, n_layer: int, hidden: int, seq_len
     return Slicing([buf[i] for i in range(out.n_slices)], out.batch_slice, out.t_max_ticks, out.predicted_ticks)
 
 
+class BatchPlan:
+    """A batch plan [(b_1, l^1), (b_2, l^2), ..]: group d = b_d consecutive
+    sequences with its own token slicing. Uniform slicings are the special case of identical groups."""
+
+    def __init__(self, groups: Sequence[Tuple[int, Sequence[int]]], t_max: int = 0, predicted: int = 0):
+        self.groups = [(int(b), [int(x) for x in ls]) for b, ls in groups]
+        self.t_max = int(t_max)
+        self.predicted = int(predicted)
+        D = len(self.groups)
+        flat = [x for _, ls in self.groups for x in ls]
+        self._b = (C.c_int32 * max(1, D))(*[b for b, _ in self.groups])
+        self._m = (C.c_int32 * max(1, D))(*[len(ls) for _, ls in self.groups])
+        self._l = (C.c_int32 * max(1, len(flat)))(*flat)
+        self._c = BatchPlanC(D, D, self._b, self._m, len(flat), self._l, self.t_max, self.predicted)
+
+    @classmethod
+    def uniform(cls, slicing: "Slicing", batch: int) -> "BatchPlan":
+        return cls([(slicing.batch_slice, slicing.lengths)] * (batch // slicing.batch_slice), slicing.t_max,
+                   slicing.predicted)
+
+    @property
+    def c(self) -> BatchPlanC:
+        return self._c
+
+    def batch(self) -> int:
+        return sum(b for b, _ in self.groups)
+
+    def notation(self) -> str:
+        """The paper's notation, runs of identical groups collapsed: [(b, [l..])] * k + ..."""
+        runs: List[List] = []
+        for g in self.groups:
+            if runs and runs[-1][0] == g:
+                runs[-1][1] += 1
+            else:
+                runs.append([g, 1])
+        return " + ".join(f"[({b}, {ls})] * {k}" for (b, ls), k in runs)
+
+    def __repr__(self):
+        return f"BatchPlan({self.groups})"
+
+
+def plan_joint(tables: Dict[int, np.ndarray], granularity: int, n_layer: int, hidden: int, seq_len: int,
+               n_stages: int, batch: int, eps_ticks: int = 0, ticks_per_ms: int = 1_000_000) -> BatchPlan:
+    """tp_plan_joint (include/tp.h): per-b tables t_b[l-1][c] -> the batch plan minimising the
+    pipelined makespan (A-20b)."""
+    n = seq_len // granularity if granularity > 0 else 0
+    bs = sorted(int(b) for b in tables)
+    arrs = [np.ascontiguousarray(tables[b], dtype=np.int64) for b in bs]
+    for b, t in zip(bs, arrs):
+        if t.shape != (n, n + 1):
+            raise TpError(TP_EINVAL, f"table for b={b}: shape {t.shape} != ({n}, {n + 1})")
+    cts = [CostTableC(granularity, n, t.ctypes.data_as(C.POINTER(C.c_int64)), ticks_per_ms) for t in arrs]
+    ptrs = (C.POINTER(CostTableC) * len(cts))(*[C.pointer(ct) for ct in cts])
+    bvals = (C.c_int32 * len(bs))(*bs)
+    gb, gm = (C.c_int32 * batch)(), (C.c_int32 * batch)()
+    lens = (C.c_int32 * max(1, batch * n))()
+    out = BatchPlanC(0, batch, gb, gm, batch * n, lens, 0, 0)
+    _check(_lib.tp_plan_joint(n_layer, hidden, seq_len, n_stages, len(bs), bvals, ptrs, batch, eps_ticks,
+                              C.byref(out)))
+    groups, pos = [], 0
+    for d in range(out.n_groups):
+        groups.append((gb[d], [lens[pos + i] for i in range(gm[d])]))
+        pos += gm[d]
+    return BatchPlan(groups, out.t_max_ticks, out.predicted_ticks)
+
+
 def stage_param_count(cfg, stage: int) -> int:
     n = C.c_size_t()
     _check(_lib.tp_stage_param_count(C.byref(_cfg(cfg)), stage, C.byref(n)))
@@ -193,6 +269,18 @@ class Context:
     def step_device(self, slicing: Slicing, dev_tokens_ptr: int, batch: int) -> float:
         loss = C.c_float()
         _check(_lib.tp_step_device(self._h, C.byref(slicing.c), C.c_void_p(dev_tokens_ptr), batch, C.byref(loss)))
+        return loss.value
+
+    def step_plan(self, plan: BatchPlan, tokens: np.ndarray) -> float:
+        tok = np.ascontiguousarray(tokens, dtype=np.int32)
+        loss = C.c_float()
+        _check(_lib.tp_step_plan(self._h, C.byref(plan.c), tok.ctypes.data, tok.shape[0], C.byref(loss)))
+        return loss.value
+
+    def step_plan_device(self, plan: BatchPlan, dev_tokens_ptr: int, batch: int) -> float:
+        loss = C.c_float()
+        _check(_lib.tp_step_plan_device(self._h, C.byref(plan.c), C.c_void_p(dev_tokens_ptr), batch,
+                                        C.byref(loss)))
         return loss.value
 
     def grads(self) -> np.ndarray:

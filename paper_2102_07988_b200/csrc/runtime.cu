@@ -165,6 +165,8 @@ struct EngineBase {
   virtual ~EngineBase() = default;
   virtual tp_status load(const float* host, size_t n) = 0;
   virtual tp_status step(const tp_slicing* sl, const int32_t* tokens, bool host_tokens, int batch, float* loss) = 0;
+  virtual tp_status step_plan(const tp_batch_plan* pl, const int32_t* tokens, bool host_tokens, int batch,
+                              float* loss) = 0;
   virtual tp_status grads(float* host, size_t n) = 0;
   virtual tp_status logits(float* host, size_t n) = 0;
   virtual tp_status profile(int g, int b, int reps, int64_t* ticks, double* fit) = 0;
@@ -215,7 +217,8 @@ class Engine final : public EngineBase {
   int32_t* d_tokens = nullptr;
   float* d_loss = nullptr;
   float* h_loss = nullptr;  // pinned
-  int last_batch = 0, last_b = 1;
+  int last_batch = 0;
+  std::vector<std::pair<size_t, int>> last_groups;  // (seq0, b) of the last step's groups
   int32_t* h_tokens = nullptr;  // pinned staging of the step's tokens
   // CUDA graph of the last (slicing, batch) op list
   bool use_graphs = true;
@@ -449,14 +452,14 @@ class Engine final : public EngineBase {
 
   // ------------------------------------------------------------ forward of one job on one stage
   // Internal row order of every [B][s] activation buffer for a step with batch slice b:
-  // row((group g, position p, member j)) = (g*s + p)*b + j, so the job (g, slice [c, c+l)) is the
-  // contiguous row range [(g*s + c)*b, (g*s + c + l)*b) of T = b*l tokens (PAPER.md:362-364 joint
-  // batch x token slicing; b = 1 is the plain token slicing of §3.2).
-  tp_status fwd(Stage<T>& S, int g, int c, int l, int b, int batch) {
+  // A group of b sequences starting at sequence seq0 owns rows [seq0*s, (seq0+b)*s), member j at
+  // position p in row seq0*s + p*b + j, so the job (group, slice [c, c+l)) is the contiguous row
+  // range [seq0*s + c*b, seq0*s + (c+l)*b) of T = b*l tokens (PAPER.md:362-364 joint batch x token
+  // slicing; b = 1 is the plain token slicing of §3.2; groups may differ in b).
+  tp_status fwd(Stage<T>& S, size_t seq0, int c, int l, int b, int batch) {
     const int H = m.H, s = m.s, a = m.a, dh = m.d, V = m.V;
     const int Tn = b * l;
-    const size_t row = ((size_t)g * s + c) * b;  // first row of this job
-    const size_t seq0 = (size_t)g * b;          // first sequence of this job
+    const size_t row = seq0 * s + (size_t)c * b;  // first row of this job
     const int32_t* tok0 = d_tokens + seq0 * (s + 1);
     const double ebytes = sizeof(T);
     if (S.k == 0) {
@@ -532,11 +535,10 @@ class Engine final : public EngineBase {
   }
 
   // ------------------------------------------------------------ backward of one job on one stage
-  tp_status bwd(Stage<T>& S, int g, int c, int l, int b, int batch, bool first_bwd_slice) {
+  tp_status bwd(Stage<T>& S, size_t seq0, int c, int l, int b, int batch, bool first_bwd_slice) {
     const int H = m.H, s = m.s, a = m.a, dh = m.d, V = m.V;
     const int Tn = b * l;
-    const size_t row = ((size_t)g * s + c) * b;
-    const size_t seq0 = (size_t)g * b;
+    const size_t row = seq0 * s + (size_t)c * b;
     const int32_t* tok0 = d_tokens + seq0 * (s + 1);
     const double ebytes = sizeof(T);
     float* gr = S.grad_out + row * H;  // fp32 gradient at the stage output, rows of this job
@@ -714,8 +716,13 @@ class Engine final : public EngineBase {
   // ------------------------------------------------------------ one step
   // Everything one step puts on the device after the tokens are in d_tokens: zero the gradients, the
   // forward and backward op lists of every owned stage, the deferred weight gradients, the loss.
-  tp_status enqueue_step(const std::vector<int>& off, const int32_t* lengths, int M, int b, int batch) {
-    const int D = batch / b;
+  struct Group {
+    size_t seq0;
+    int b;
+    std::vector<int> off, len;  // slice offsets (M + 1) and lengths (M), tokens
+  };
+  tp_status enqueue_step(const std::vector<Group>& G, int batch) {
+    const int D = (int)G.size();
     const bool multi = world > 1;
     if (multi) {  // fork: the comm streams join this step's stream order (and any graph capture)
       cudaEvent_t e = event();
@@ -723,15 +730,16 @@ class Engine final : public EngineBase {
       for (cudaStream_t cs : {s_send_f, s_recv_f, s_send_b, s_recv_b}) CU(cudaStreamWaitEvent(cs, e, 0));
     }
     for (auto& S : stages) CU(cudaMemsetAsync(S.gflat, 0, S.L.total * sizeof(float), stream));
-    // forward: F(g, i) for groups g = 0..D-1 of b sequences, slices i = 1..M (stage order inside a
-    // job in loopback); a job is b*l_i tokens, contiguous rows (see fwd())
+    // forward: F(d, i) for groups d = 0..D-1 (b_d sequences each), slices i = 1..M_d (stage order
+    // inside a job in loopback); a job is b_d*l_i tokens, contiguous rows (see fwd())
     for (int d = 0; d < D; ++d)
-      for (int i = 0; i < M; ++i)
+      for (size_t i = 0; i < G[d].len.size(); ++i)
         for (auto& S : stages) {
-          const size_t row = ((size_t)d * m.s + off[i]) * b;
-          const int Tn = b * lengths[i];
+          const int b = G[d].b;
+          const size_t row = G[d].seq0 * m.s + (size_t)G[d].off[i] * b;
+          const int Tn = b * G[d].len[i];
           if (multi && S.k > 0) TRY(recv_fwd(S, row, Tn));
-          TRY(fwd(S, d, off[i], lengths[i], b, batch));
+          TRY(fwd(S, G[d].seq0, G[d].off[i], G[d].len[i], b, batch));
           if (multi && S.k < m.K - 1) TRY(send_fwd(S, row, Tn));
         }
     // backward: exact reverse order (GPipe order, A-21). With one stage per GPU and D >= 2 groups,
@@ -740,20 +748,21 @@ class Engine final : public EngineBase {
     // bubbles); otherwise one K = B*s GEMM per weight at the end.
     const bool side_dw = multi && D >= 2 && s_wgrad;
     for (int d = D - 1; d >= 0; --d) {
+      const int M = (int)G[d].len.size(), b = G[d].b;
       for (int i = M - 1; i >= 0; --i)
         for (int si = (int)stages.size() - 1; si >= 0; --si) {
           Stage<T>& S = stages[si];
-          const size_t row = ((size_t)d * m.s + off[i]) * b;
-          const int Tn = b * lengths[i];
+          const size_t row = G[d].seq0 * m.s + (size_t)G[d].off[i] * b;
+          const int Tn = b * G[d].len[i];
           if (multi && S.k < m.K - 1) TRY(recv_bwd(S, row, Tn));
-          TRY(bwd(S, d, off[i], lengths[i], b, batch, i == M - 1));
+          TRY(bwd(S, G[d].seq0, G[d].off[i], G[d].len[i], b, batch, i == M - 1));
           if (multi && S.k > 0) TRY(send_bwd(S, row, Tn));
         }
       if (side_dw) {
         cudaEvent_t e = event();
         CU(cudaEventRecord(e, stream));
         CU(cudaStreamWaitEvent(s_wgrad, e, 0));
-        for (auto& S : stages) TRY(wgrad_rows(S, (size_t)d * b * m.s, b * m.s, d != D - 1, s_wgrad, false));
+        for (auto& S : stages) TRY(wgrad_rows(S, G[d].seq0 * m.s, b * m.s, d != D - 1, s_wgrad, false));
       }
     }
     if (side_dw) {
@@ -792,16 +801,58 @@ class Engine final : public EngineBase {
       return fail(TP_EINVAL, "tp_step: batch_slice %d must be >= 1 and divide batch %d", b, batch);
     const int M = sl->n_slices;
     if (M < 1 || M > m.s) return fail(TP_EINVAL, "tp_step: n_slices %d", M);
-    std::vector<int> off(M + 1, 0);
+    Group g0;
+    g0.b = b;
+    g0.off.assign(M + 1, 0);
     for (int i = 0; i < M; ++i) {
       if (sl->lengths[i] <= 0) return fail(TP_EINVAL, "tp_step: slice %d has length %d", i, sl->lengths[i]);
-      off[i + 1] = off[i] + sl->lengths[i];
+      g0.off[i + 1] = g0.off[i] + sl->lengths[i];
+      g0.len.push_back(sl->lengths[i]);
     }
-    if (off[M] != m.s) return fail(TP_EINVAL, "tp_step: slice lengths sum to %d, seq_len is %d", off[M], m.s);
+    if (g0.off[M] != m.s) return fail(TP_EINVAL, "tp_step: slice lengths sum to %d, seq_len is %d", g0.off[M], m.s);
+    std::vector<Group> G(batch / b, g0);
+    for (int d = 0; d < batch / b; ++d) G[d].seq0 = (size_t)d * b;
+    return run_step(G, tokens, host_tokens, batch, loss_out);
+  }
+
+  tp_status step_plan(const tp_batch_plan* pl, const int32_t* tokens, bool host_tokens, int batch,
+                      float* loss_out) override {
+    if (!pl || !pl->batch_slice || !pl->n_slices || !pl->lengths) return fail(TP_EINVAL, "tp_step_plan: null plan");
+    if (batch < 1 || batch > max_batch)
+      return fail(TP_EINVAL, "tp_step_plan: batch %d not in [1, max_batch=%d]", batch, max_batch);
+    if (pl->n_groups < 1 || pl->n_groups > batch) return fail(TP_EINVAL, "tp_step_plan: n_groups %d", pl->n_groups);
+    std::vector<Group> G(pl->n_groups);
+    size_t seq0 = 0, pos = 0;
+    for (int d = 0; d < pl->n_groups; ++d) {
+      const int b = pl->batch_slice[d], M = pl->n_slices[d];
+      if (b < 1) return fail(TP_EINVAL, "tp_step_plan: group %d has batch_slice %d", d, b);
+      if (M < 1 || M > m.s) return fail(TP_EINVAL, "tp_step_plan: group %d has n_slices %d", d, M);
+      if (pos + M > (size_t)pl->capacity_lengths) return fail(TP_EINVAL, "tp_step_plan: lengths[] overrun at group %d", d);
+      G[d].seq0 = seq0;
+      G[d].b = b;
+      G[d].off.assign(M + 1, 0);
+      for (int i = 0; i < M; ++i) {
+        const int l = pl->lengths[pos + i];
+        if (l <= 0) return fail(TP_EINVAL, "tp_step_plan: group %d slice %d has length %d", d, i, l);
+        G[d].off[i + 1] = G[d].off[i] + l;
+        G[d].len.push_back(l);
+      }
+      if (G[d].off[M] != m.s)
+        return fail(TP_EINVAL, "tp_step_plan: group %d slice lengths sum to %d, seq_len is %d", d, G[d].off[M], m.s);
+      seq0 += b;
+      pos += M;
+    }
+    if ((int)seq0 != batch) return fail(TP_EINVAL, "tp_step_plan: batch slices sum to %zu, batch is %d", seq0, batch);
+    return run_step(G, tokens, host_tokens, batch, loss_out);
+  }
+
+  tp_status run_step(const std::vector<Group>& G, const int32_t* tokens, bool host_tokens, int batch,
+                     float* loss_out) {
     if (!tokens) return fail(TP_EINVAL, "tp_step: null tokens");
     CU(cudaSetDevice(device));
     last_batch = batch;
-    last_b = b;
+    last_groups.clear();
+    for (const Group& g : G) last_groups.push_back({g.seq0, g.b});
     // tokens -> d_tokens, outside any graph (the caller's pointer may change between calls)
     const size_t ntok = (size_t)batch * (m.s + 1);
     if (host_tokens) {
@@ -810,10 +861,14 @@ class Engine final : public EngineBase {
     } else {
       CU(cudaMemcpyAsync(d_tokens, tokens, ntok * sizeof(int32_t), cudaMemcpyDeviceToDevice, stream));
     }
-    // The op list of a (slicing, batch) pair is static: the first step with a new key runs eagerly,
-    // the second is captured into a CUDA graph, later ones replay it (no per-kernel host launch cost).
-    std::vector<int64_t> key = {b, batch, M};
-    for (int i = 0; i < M; ++i) key.push_back(sl->lengths[i]);
+    // The op list of a plan is static: the first step with a new key runs eagerly, the second is
+    // captured into a CUDA graph, later ones replay it (no per-kernel host launch cost).
+    std::vector<int64_t> key = {batch, (int64_t)G.size()};
+    for (const Group& g : G) {
+      key.push_back(g.b);
+      key.push_back((int64_t)g.len.size());
+      for (int l : g.len) key.push_back(l);
+    }
     const bool graphs = use_graphs && !instr.on;
     if (graphs && g_exec && key == g_key) {
       CU(cudaGraphLaunch(g_exec, stream));
@@ -822,7 +877,7 @@ class Engine final : public EngineBase {
       instr.launches = 0;
       ev_next = 0;
       CU(cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed));
-      tp_status st = enqueue_step(off, sl->lengths, M, b, batch);
+      tp_status st = enqueue_step(G, batch);
       cudaGraph_t graph = nullptr;
       cudaError_t ce = cudaStreamEndCapture(stream, &graph);
       if (st != TP_OK) { if (graph) cudaGraphDestroy(graph); return st; }
@@ -849,7 +904,7 @@ class Engine final : public EngineBase {
       g_key = key;
       instr.launches = 0;
       ev_next = 0;
-      TRY(enqueue_step(off, sl->lengths, M, b, batch));
+      TRY(enqueue_step(G, batch));
     }
     CU(cudaStreamSynchronize(stream));
     CU(cudaGetLastError());
@@ -875,11 +930,13 @@ class Engine final : public EngineBase {
     if (n != need) return fail(TP_EINVAL, "tp_get_logits: n=%zu, expected %zu", n, need);
     std::vector<float> tmp(need);
     CU(cudaMemcpy(tmp.data(), last->logits_keep, need * sizeof(float), cudaMemcpyDeviceToHost));
-    // internal row (g*s + p)*b + j  ->  [sequence g*b + j][position p]
-    const size_t b = last_b, s = m.s, V = m.V;
-    for (size_t r = 0; r < (size_t)last_batch * s; ++r) {
-      const size_t g = r / (s * b), rem = r % (s * b), p = rem / b, j = rem % b;
-      std::memcpy(host + ((g * b + j) * s + p) * V, tmp.data() + r * V, V * sizeof(float));
+    // internal row seq0*s + p*b + j of a group (seq0, b)  ->  [sequence seq0 + j][position p]
+    const size_t s = m.s, V = m.V;
+    for (const auto& gr : last_groups) {
+      const size_t seq0 = gr.first, b = (size_t)gr.second;
+      for (size_t p = 0; p < s; ++p)
+        for (size_t j = 0; j < b; ++j)
+          std::memcpy(host + ((seq0 + j) * s + p) * V, tmp.data() + (seq0 * s + p * b + j) * V, V * sizeof(float));
     }
     return TP_OK;
   }
@@ -1094,6 +1151,16 @@ extern "C" tp_status tp_step(tp_ctx* ctx, const tp_slicing* sl, const int32_t* t
 extern "C" tp_status tp_step_device(tp_ctx* ctx, const tp_slicing* sl, const int32_t* tokens, int32_t batch, float* loss) {
   TP_CHECK_ARG(ctx, "tp_step_device: null ctx");
   return ctx->eng->step(sl, tokens, false, batch, loss);
+}
+extern "C" tp_status tp_step_plan(tp_ctx* ctx, const tp_batch_plan* pl, const int32_t* tokens, int32_t batch,
+                                  float* loss) {
+  TP_CHECK_ARG(ctx, "tp_step_plan: null ctx");
+  return ctx->eng->step_plan(pl, tokens, true, batch, loss);
+}
+extern "C" tp_status tp_step_plan_device(tp_ctx* ctx, const tp_batch_plan* pl, const int32_t* tokens, int32_t batch,
+                                         float* loss) {
+  TP_CHECK_ARG(ctx, "tp_step_plan_device: null ctx");
+  return ctx->eng->step_plan(pl, tokens, false, batch, loss);
 }
 extern "C" tp_status tp_get_grads(tp_ctx* ctx, float* host, size_t n) {
   TP_CHECK_ARG(ctx && host, "tp_get_grads: null argument");

@@ -135,3 +135,65 @@ def test_plan_tiny_config_vs_2pow31_brute_force():
         out = [int(x) for x in subprocess.run([bf], input=inp, capture_output=True, text=True, check=True).stdout.split()]
         s = _plan(t, 32, 2)
         assert (s.predicted, s.t_max, s.lengths) == (out[0], out[1], out[3:3 + out[2]])
+
+
+# ---------------------------------------------------------------- tp_plan_joint
+def _joint_tables(rng, n, bs):
+    base = rng.integers(1, 20, size=(n, n + 1)).astype(np.int64)
+    return {b: base * b + rng.integers(0, 5 * b, size=(n, n + 1)).astype(np.int64) for b in bs}
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_plan_joint_bit_exact_vs_oracle(seed):
+    rng = np.random.default_rng(5000 + seed)
+    n = int(rng.integers(1, 9))
+    B = int(rng.integers(1, 9))
+    K = int(rng.integers(1, 6))
+    bs = sorted({1} | {int(x) for x in rng.integers(1, B + 1, size=int(rng.integers(0, 3)))})
+    tables = _joint_tables(rng, n, bs)
+    g = 8
+    T, plan = op.joint_optimize(tables, n, B, K)
+    got = tp.plan_joint(tables, g, K, 64, n * g, K, B)
+    assert got.predicted == T
+    assert got.groups == [(b, [x * g for x in ls]) for b, ls in plan]
+    assert got.t_max == max(x for b, ls in plan for x in op.slice_costs(tables[b], ls))
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_plan_joint_vs_brute_force(seed):
+    rng = np.random.default_rng(7000 + seed)
+    n, B, K = int(rng.integers(1, 5)), int(rng.integers(1, 5)), int(rng.integers(1, 5))
+    bs = sorted({1} | {int(rng.integers(1, B + 1))})
+    tables = _joint_tables(rng, n, bs)
+    got = tp.plan_joint(tables, 1, K, 64, n, K, B)
+    assert got.predicted == op.joint_brute_force(tables, n, B, K)
+    assert sum(b for b, _ in got.groups) == B
+
+
+def test_plan_joint_single_b_equals_plan():
+    # one batch-slice size: the joint plan is tp_plan with n_micro = B / b (reading A-20)
+    rng = np.random.default_rng(11)
+    n, K, B, b, g = 16, 4, 8, 2, 64
+    t = random_int_table(n, rng, 1, 1000)
+    j = tp.plan_joint({b: t}, g, K, 64, n * g, K, B)
+    u = tp.plan(t, g, K, 64, n * g, K, n_micro=B // b)
+    assert j.predicted == u.predicted and j.groups == [(b, u.lengths)] * (B // b)
+
+
+def test_plan_joint_rejects_bad_input():
+    t = np.ones((2, 3), dtype=np.int64)
+    with pytest.raises(tp.TpError) as e:
+        tp.plan_joint({2: t}, 1, 1, 64, 2, 1, 3)  # 3 is not a sum of 2s
+    assert e.value.status == tp.TP_EINFEASIBLE
+    with pytest.raises(tp.TpError) as e:
+        tp.plan_joint({1: t, 2: np.ones((3, 4), dtype=np.int64)}, 1, 1, 64, 2, 1, 2)
+    assert e.value.status == tp.TP_EINVAL
+    bad = t.copy()
+    bad[0, 0] = 0
+    with pytest.raises(tp.TpError):
+        tp.plan_joint({1: bad}, 1, 1, 64, 2, 1, 1)
+
+
+def test_batch_plan_notation():
+    p = tp.BatchPlan([(2, [384, 384]), (2, [384, 384]), (1, [768])])
+    assert p.notation() == "[(2, [384, 384])] * 2 + [(1, [768])] * 1" and p.batch() == 5
