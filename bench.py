@@ -221,19 +221,22 @@ def main():
     stream = torch.cuda.ExternalStream(ctx.stream())
 
     # --- cost tables (this stage; max over stages = bottleneck table, A-16) and the DP plan.
-    # Joint batch x token slicing with a uniform batch slice b: one table per b,
-    # tp_plan with D = B/b jobs per slice index, keep the b with the smallest predicted T (A-20).
+    # Joint batch x token slicing: one table per batch-slice size b, then
+    # tp_plan_joint (per-b Algorithm 1 + 1-D knapsack over the batch under a shared t_max, A-20b);
+    # the per-b uniform plans (tp_plan with D = B/b, A-20) are reported as candidates.
     g = args.granularity
     bsl = [int(x) for x in args.batch_slices.split(",")] if args.batch_slices != "auto" else \
         [x for x in (1, 2, 4, 8, 16) if B % x == 0 and x <= B]
     dp, fit, t_prof, t_plan, plans = None, None, 0.0, 0.0, []
-    gpipe = tp.Slicing([cfg.seq_len])
+    gpipe = tp.BatchPlan.uniform(tp.Slicing([cfg.seq_len]), B)
     if args.slicing in ("dp", "gpipe") and (args.slicing == "dp" or len(bsl) > 1):
         t0 = time.time()
+        tables = {}
         for b in bsl:
             ticks, f = ctx.profile(g, reps=5, batch_slice=b)
             if world > 1:
                 ticks = tdist.bottleneck_table(ticks)
+            tables[b] = ticks
             t1 = time.time()
             sl = tp.plan(ticks, g, cfg.n_layer, cfg.hidden, cfg.seq_len, K, n_micro=B // b, eps_ticks=0)
             t_plan += time.time() - t1
@@ -241,20 +244,24 @@ def main():
             n = cfg.seq_len // g
             gp_pred = (B // b + K - 1) * int(ticks[n - 1, 0])   # unsliced [(b, [s])] * (B/b)
             plans.append({"b": b, "slicing": sl, "fit": f, "gpipe_pred": gp_pred})
+        t1 = time.time()
+        dp = tp.plan_joint(tables, g, cfg.n_layer, cfg.hidden, cfg.seq_len, K, B, eps_ticks=0)
+        t_plan += time.time() - t1
         t_prof = time.time() - t0 - t_plan
-        best = min(plans, key=lambda p: (p["slicing"].predicted, -p["b"]))
-        dp, fit = best["slicing"], best["fit"]
+        fit = min(plans, key=lambda p: (p["slicing"].predicted, -p["b"]))["fit"]
         gbest = min(plans, key=lambda p: (p["gpipe_pred"], -p["b"]))
-        gpipe = tp.Slicing([cfg.seq_len], gbest["b"])
-        if world > 1 and not tdist.agreed(dp.lengths + [dp.batch_slice, gpipe.batch_slice]):
+        gpipe = tp.BatchPlan.uniform(tp.Slicing([cfg.seq_len], gbest["b"]), B)
+        flat_plan = [x for bb, ls in dp.groups for x in [bb] + ls] + [gbest["b"]]
+        if world > 1 and not tdist.agreed(flat_plan):
             raise RuntimeError("ranks planned different slicings")
     if args.slicing == "dp":
         main_sl = dp
     elif args.slicing == "gpipe":
         main_sl = gpipe
     else:
-        main_sl = tp.Slicing([int(x) for x in args.slicing.split(",")], int(args.batch_slices.split(",")[0])
-                             if args.batch_slices != "auto" else 1)
+        main_sl = tp.BatchPlan.uniform(tp.Slicing([int(x) for x in args.slicing.split(",")],
+                                                  int(args.batch_slices.split(",")[0])
+                                                  if args.batch_slices != "auto" else 1), B)
 
     def timed(sl, steps, device_tokens=True):
         barrier()
@@ -263,16 +270,16 @@ def main():
         loss = None
         for _ in range(steps):
             if device_tokens:
-                loss = ctx.step_device(sl, tok_dev.data_ptr(), B)
+                loss = ctx.step_plan_device(sl, tok_dev.data_ptr(), B)
             else:
-                    loss = ctx.step(sl, tok_pin.numpy())
+                loss = ctx.step_plan(sl, tok_pin.numpy())
         e1.record(stream)
         e1.synchronize()
         barrier()
         return allmax(e0.elapsed_time(e1) / steps), loss
 
     for _ in range(args.warmup):
-        ctx.step_device(main_sl, tok_dev.data_ptr(), B)
+        ctx.step_plan_device(main_sl, tok_dev.data_ptr(), B)
     clocks = ClockSampler(local_rank)
     clocks.start()
     # TP_PROFILE_RANGE=1 limits an `ncu --profile-from-start off` capture to the timed device region
@@ -288,10 +295,10 @@ def main():
     ms_e2e, _ = timed(main_sl, args.steps, device_tokens=False)
     # unsliced GPipe on the same kernels
     ms_gpipe = None
-    same = main_sl.lengths == gpipe.lengths and main_sl.batch_slice == gpipe.batch_slice
+    same = main_sl.groups == gpipe.groups
     if not args.no_gpipe and not same:
         for _ in range(1):
-            ctx.step_device(gpipe, tok_dev.data_ptr(), B)
+            ctx.step_plan_device(gpipe, tok_dev.data_ptr(), B)
         ms_gpipe, _ = timed(gpipe, args.steps)
     elif same:
         ms_gpipe = ms
@@ -313,16 +320,17 @@ def main():
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": args.config, "n_layer": cfg.n_layer, "hidden": cfg.hidden, "heads": cfg.n_head,
                    "seq_len": cfg.seq_len, "batch": B, "vocab": cfg.vocab, "stages": K,
-                   "parallelism": f"pipeline{K}", "slicing": main_sl.notation(B), "granularity": g,
+                   "parallelism": f"pipeline{K}", "slicing": main_sl.notation(), "granularity": g,
                    "l2": "working set > L2 (bf16 weights alone exceed 126 MB); no flush"},
         "mfu": mfu, "mfu_sustained_peak": flops / (ms / 1e3) / (args.gpus * peak_sust * 1e12),
         "gpipe": None if ms_gpipe is None else {
-            "slicing": gpipe.notation(B), "ms_per_step": ms_gpipe, "tokens_per_s": tokens_per_step / (ms_gpipe / 1e3),
+            "slicing": gpipe.notation(), "ms_per_step": ms_gpipe, "tokens_per_s": tokens_per_step / (ms_gpipe / 1e3),
             "mfu": flops / (ms_gpipe / 1e3) / (args.gpus * peak_burst * 1e12),
             "speedup_of_dp": ms_gpipe / ms},
         "plan": None if dp is None else {
             "predicted_ms": dp.predicted / 1e6, "t_max_ms": dp.t_max / 1e6, "profile_s": t_prof, "plan_s": t_plan,
             "fit": {"a": [float(x) for x in fit[:4]], "max_rel_err": float(fit[4])},
+            "joint": "tp_plan_joint over b in " + str(bsl),
             "candidates": [{"b": p["b"], "slicing": p["slicing"].notation(B), "predicted_ms": p["slicing"].predicted / 1e6,
                             "gpipe_predicted_ms": p["gpipe_pred"] / 1e6} for p in plans]},
         "loss": loss,

@@ -43,3 +43,16 @@ def worst_errors(loss, logits, grads, ref):
     for k, g in ref["grads"].items():
         errs[k] = rel(grads[k], g)
     return errs
+
+
+def gpu_run_plan(cfg, B, params, tokens, groups, precision, flags=tp.TP_FLAG_KEEP_LOGITS):
+    """One step with a heterogeneous batch plan [(b_d, lengths_d), ..] (tp_step_plan)."""
+    ctx = tp.Context(cfg, precision=precision, max_batch=B, device=0, flags=flags)
+    try:
+        ctx.load_params(pack_all_stages(params, cfg))
+        loss = ctx.step_plan(tp.BatchPlan(groups), tokens)
+        grads = unpack_all_stages(ctx.grads(), cfg)
+        logits = ctx.logits(B) if flags & tp.TP_FLAG_KEEP_LOGITS else None
+    finally:
+        ctx.close()
+    return loss, logits, grads

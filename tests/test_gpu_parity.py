@@ -7,7 +7,7 @@ import pytest
 
 import paper_2102_07988_b200 as tp
 from synth import CONFIGS, ModelCfg
-from tests.gpu_util import gpu_run, oracle_run, rel, worst_errors
+from tests.gpu_util import gpu_run, gpu_run_plan, oracle_run, rel, worst_errors
 
 pytestmark = pytest.mark.gpu
 
@@ -87,6 +87,30 @@ def test_joint_batch_token_slicing(K, b, lengths, precision, tol):
     params, tokens, ref = oracle_run(cfg, B, 8, precision == tp.TP_BF16)
     loss, logits, grads, _ = gpu_run(cfg, B, params, tokens, lengths, precision, batch_slice=b)
     check(worst_errors(loss, logits, grads, ref), tol)
+
+
+@pytest.mark.parametrize("precision,tol", [(tp.TP_BF16, 2e-2), (tp.TP_FP32, 1e-4)])
+@pytest.mark.parametrize("K,groups", [
+    (2, [(2, [40, 24, 64]), (1, [128]), (1, [8] * 16)]),      # three groups, three slicings
+    (1, [(1, [64, 64]), (3, [16, 112])]),
+    (4, [(3, [128]), (1, [32, 32, 32, 32])]),
+])
+def test_heterogeneous_batch_plan(K, groups, precision, tol):
+    """Groups of different batch-slice sizes, each with its own token slicing (PAPER.md:362-364,
+    tp_plan_joint's output): the same function as the unsliced oracle."""
+    cfg = SMALL.with_(n_stages=K)
+    B = 4
+    params, tokens, ref = oracle_run(cfg, B, 9, precision == tp.TP_BF16)
+    loss, logits, grads = gpu_run_plan(cfg, B, params, tokens, groups, precision)
+    check(worst_errors(loss, logits, grads, ref), tol)
+
+
+def test_heterogeneous_plan_rejects_bad_plans():
+    params, tokens, _ = oracle_run(TINY, 2, 0, True)
+    for groups in ([(1, [32])], [(1, [32]), (2, [32])], [(1, [16, 8]), (1, [32])], [(0, [32]), (2, [32])]):
+        with pytest.raises(tp.TpError) as e:
+            gpu_run_plan(TINY, 2, params, tokens, groups, tp.TP_BF16)
+        assert e.value.status == tp.TP_EINVAL
 
 
 def test_rejects_bad_slicing():
