@@ -308,7 +308,10 @@ class Engine final : public EngineBase {
       CU(cudaStreamCreateWithPriority(&s_send_f, cudaStreamNonBlocking, hi));
       CU(cudaStreamCreateWithPriority(&s_recv_b, cudaStreamNonBlocking, hi));
       CU(cudaStreamCreateWithPriority(&s_send_b, cudaStreamNonBlocking, hi));
-      if (std::getenv("TP_NO_SIDE_DW") == nullptr) CU(cudaStreamCreateWithPriority(&s_wgrad, cudaStreamNonBlocking, lo));
+      // opt-in (TP_SIDE_DW=1): per-group weight gradients on a low-priority stream. Measured on 4 x B200
+      // it slows the step (1B 64.2 vs 56.1 ms, 13B 435 vs 418 ms): its one-tile-per-CTA GEMMs hold SMs
+      // the critical path needs and the per-group fp32 gradient RMW adds HBM traffic.
+      if (std::getenv("TP_SIDE_DW") != nullptr) CU(cudaStreamCreateWithPriority(&s_wgrad, cudaStreamNonBlocking, lo));
     }
     CU(cudaStreamSynchronize(stream));
     return TP_OK;
@@ -742,10 +745,10 @@ class Engine final : public EngineBase {
           TRY(fwd(S, G[d].seq0, G[d].off[i], G[d].len[i], b, batch));
           if (multi && S.k < m.K - 1) TRY(send_fwd(S, row, Tn));
         }
-    // backward: exact reverse order (GPipe order, A-21). With one stage per GPU and D >= 2 groups,
-    // group d's weight gradients go to a low-priority stream as soon as its last backward job is
-    // done (one tile per CTA, so the critical-path kernels interleave and the dW fills the pipeline
-    // bubbles); otherwise one K = B*s GEMM per weight at the end.
+    // backward: exact reverse order (GPipe order, A-21). Weight gradients: one K = B*s GEMM per
+    // weight at the end (the last stage's overlaps the other stages' remaining backward); with
+    // TP_SIDE_DW=1, one stage per GPU and D >= 2 groups, group d's go to a low-priority stream as
+    // soon as its last backward job is done.
     const bool side_dw = multi && D >= 2 && s_wgrad;
     for (int d = D - 1; d >= 0; --d) {
       const int M = (int)G[d].len.size(), b = G[d].b;
