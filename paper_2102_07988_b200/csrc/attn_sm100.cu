@@ -840,8 +840,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         // P^T columns: query half h = kk >> 1 was packed at h*32 .. h*32+15 of the S^T columns
         mma_bf16_ts_w(tmem + T_DV, tb + (kk >> 1) * 32 + (kk & 1) * 8, make_desc(o_base + kk * 2048, QHALF, 1024), idKV,
                     (i | kk) != 0);
-        mma_bf16_w(tmem + T_DK, make_desc(ds_base + kk * 32, 16, 1024), make_desc(q_base + kk * 2048, QHALF, 1024), idKV,
-                 (i | kk) != 0);
+        // dS^T columns: the softmax warps also wrote it packed into h*32+16 .. h*32+31 (TS-MMA:
+        // only Q is read from shared memory)
+        mma_bf16_ts_w(tmem + T_DK, tb + (kk >> 1) * 32 + 16 + (kk & 1) * 8, make_desc(q_base + kk * 2048, QHALF, 1024),
+                      idKV, (i | kk) != 0);
       }
       mma_commit_w(qfree + bq);
       if (i + 1 < ntile) issue_dp(i + 1);
@@ -967,6 +969,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           const int cc = half * 4 + ch * 2 + u;
           *reinterpret_cast<uint4*>(dSt + swz(row, cc)) = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
         }
+        // and packed into TMEM (second 16 of this half's S^T columns) as dK's A operand
+        tmem_st8(lane_base + bb * 128 + half * HQ + 16 + ch * 8, dk);
       }
       tmem_wait_st();
       tc_fence_before();
