@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
           for (int it = 0; it < 4; ++it) {
             const int row = m0 + q * 32 + it * 8 + (lane >> 2);
-            if (row < M && n < N) epi_prefetch8<bf16>(epi, row, n, aux[it]);
+            if (row < M && n < N) epi_prefetch8<bf16>(epi, row, n + epi.n_off, aux[it]);
           }
         }
         uint32_t r[32];
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           float v[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) v[i] = scr[rr * 33 + (lane & 3) * 8 + i];
-          if (row < M && n < N) epi_apply8<bf16>(epi, row, n, v, aux[it]);
+          if (row < M && n < N) epi_apply8<bf16>(epi, row, n + epi.n_off, v, aux[it]);
         }
         __syncwarp();
       }
@@ -378,12 +378,45 @@ cudaError_t gemm_sm100(const GemmDesc& g, const Epi& e, cudaStream_t st) {
     const double cost = (double)((tiles + units - 1) / units) * c.bn / c.eff;
     if (best < 0 || cost < best_cost * 0.999) { best = i; best_cost = cost; }
   }
-  switch (best) {
-    case 0: return launch_major<2, 256>(g, e, st);
-    case 1: return launch_major<2, 128>(g, e, st);
-    case 2: return launch_major<1, 256>(g, e, st);
-    default: return launch_major<1, 128>(g, e, st);
+  auto launch = [&](int which, const GemmDesc& gg, const Epi& ee) -> cudaError_t {
+    switch (which) {
+      case 0: return launch_major<2, 256>(gg, ee, st);
+      case 1: return launch_major<2, 128>(gg, ee, st);
+      case 2: return launch_major<1, 256>(gg, ee, st);
+      default: return launch_major<1, 128>(gg, ee, st);
+    }
+  };
+  // Tail split: when the chosen shape leaves a partial last wave, run the n-tile columns that fill
+  // whole waves with it and the remaining columns as a second launch with half-width tiles (twice
+  // the tiles, half the time each), if the model says that is cheaper: the partial wave then costs
+  // half a wave. The second launch sees its columns through Epi::n_off.
+  if (g.persistent && !g_force_cg && (best == 0 || best == 2)) {
+    const Cand& c = cands[best];
+    const Cand& h = cands[best + 1];  // same CTA group, BN / 2
+    const long units = g_num_sms / c.cg;
+    const long mt = (g.M + BM * c.cg - 1) / (BM * c.cg), nt = (g.N + c.bn - 1) / c.bn;
+    const long full = (mt * nt) / units;
+    const long n1 = full * units / mt;  // n-tile columns covered by whole waves
+    if (full >= 1 && n1 >= 1 && n1 < nt) {
+      const long t1 = n1 * mt, t2 = mt * ((g.N - n1 * c.bn + h.bn - 1) / h.bn);
+      const double split = (double)((t1 + units - 1) / units) * c.bn / c.eff +
+                           (double)((t2 + units - 1) / units) * h.bn / h.eff + 8.0 /* second launch */;
+      if (split < best_cost * 0.95) {
+        const int N1 = (int)(n1 * c.bn);
+        GemmDesc g1 = g, g2 = g;
+        g1.N = N1;
+        g2.N = g.N - N1;
+        const size_t off = g.b_mn ? (size_t)N1 : (size_t)N1 * g.ldb;
+        g2.B = reinterpret_cast<const bf16*>(g.B) + off;
+        Epi e2 = e;
+        e2.n_off = e.n_off + N1;
+        cudaError_t r = launch(best, g1, e);
+        if (r != cudaSuccess) return r;
+        return launch(best + 1, g2, e2);
+      }
+    }
   }
+  return launch(best, g, e);
 }
 
 }  // namespace tp

@@ -22,7 +22,10 @@ def rel(a, b):
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (200, 384, 320), (37, 136, 72), (512, 5120, 2048),
-                                   (1000, 1536, 512), (2048, 2048, 2048), (8, 64, 32)])
+                                   (1000, 1536, 512), (2048, 2048, 2048), (8, 64, 32),
+                                   # partial last wave -> the tail columns run as a second launch
+                                   # with half-width tiles (gemm_sm100 tail split), incl. a ragged N
+                                   (768, 15360, 256), (768, 15296, 192), (200, 20480, 128)])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 1), (1, 0), (0, 1)])
 @pytest.mark.parametrize("impl", [0, 1])
 def test_gemm(M, N, K, a_mn, b_mn, impl):

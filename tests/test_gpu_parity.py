@@ -78,6 +78,16 @@ def test_parity_mid_13b_width():
     check(worst_errors(loss, logits, grads, ref), 2e-2)
 
 
+def test_parity_mid_batch2_tail_split():
+    """13B width, b = 2 unsliced: 1024-row GEMMs whose partial last wave is split into a second
+    half-width-tile launch (QKV scatter, GeLU, residual and dX epilogues through Epi::n_off)."""
+    cfg, _ = CONFIGS["parity-mid"]
+    B = 2
+    params, tokens, ref = oracle_run(cfg, B, 13, True)
+    loss, logits, grads, _ = gpu_run(cfg, B, params, tokens, [512], tp.TP_BF16, batch_slice=2)
+    check(worst_errors(loss, logits, grads, ref), 2e-2)
+
+
 @pytest.mark.parametrize("precision,tol", [(tp.TP_BF16, 2e-2), (tp.TP_FP32, 1e-4)])
 @pytest.mark.parametrize("K,b,lengths", [(2, 2, [40, 24, 64]), (1, 4, [128]), (2, 2, [8] * 16), (4, 4, [56, 72])])
 def test_joint_batch_token_slicing(K, b, lengths, precision, tol):
