@@ -32,7 +32,8 @@ template <typename T>
 cudaError_t layernorm_fwd(const float* x, const float* gam, const float* bet, T* y, float* mean,
                           float* rstd, int rows, int H, cudaStream_t st);
 template <typename T>
-cudaError_t layernorm_bwd(const float* dy, const float* x, const float* mean, const float* rstd,
+cudaError_t layernorm_bwd(const T* dy /* compute precision: bf16 in bf16 mode */, const float* x, const float* mean,
+                          const float* rstd,
                           const float* gam, const float* resid, float* dx_out, T* dx_copy,
                           float* dgam, float* dbet, float* ws /* unused */, int rows, int H, cudaStream_t st,
                           float* dbias = nullptr /* += column sums of dx_out (the upstream bias gradient) */);

@@ -82,7 +82,7 @@ __device__ __forceinline__ void red_add4(float* out, float a, float b, float c, 
 // fp32 reductions are one per column per CTA (not per row). The next row's dy / x / stats are
 // loaded before the current row's block reduction, so the HBM latency overlaps the barrier.
 template <typename T, int NT, int NCH>
-__global__ void __launch_bounds__(NT) ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
+__global__ void __launch_bounds__(NT) ln_bwd_kernel(const T* __restrict__ dy, const float* __restrict__ x,
                                                     const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
                                                     const float* __restrict__ gam, const float* __restrict__ resid,
                                                     float* __restrict__ dx_out, T* __restrict__ dx_copy,
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(NT) ln_bwd_kernel(const float* __restrict__ dy
     for (int c = 0; c < NCH; ++c) {
       const int col = (c * NT + tid) * 8;
       if (col < H) {
-        load8<float>(dy + (int64_t)r * H + col, nd[c]);
+        load8<T>(dy + (int64_t)r * H + col, nd[c]);
         load8<float>(x + (int64_t)r * H + col, nx[c]);
         if (resid) load8<float>(resid + (int64_t)r * H + col, nres[c]);
       } else {
@@ -388,7 +388,7 @@ cudaError_t layernorm_fwd(const float* x, const float* gam, const float* bet, T*
   return cudaGetLastError();
 }
 template <typename T>
-cudaError_t layernorm_bwd(const float* dy, const float* x, const float* mean, const float* rstd, const float* gam,
+cudaError_t layernorm_bwd(const T* dy, const float* x, const float* mean, const float* rstd, const float* gam,
                           const float* resid, float* dx_out, T* dx_copy, float* dgam, float* dbet, float* ws, int rows,
                           int H, cudaStream_t st, float* dbias) {
   if (rows == 0) return cudaSuccess;
@@ -457,7 +457,7 @@ cudaError_t colsum_accum(const T* src, int64_t ld, float* out, int rows, int N, 
 #define TP_INST(T)                                                                                          \
   template cudaError_t layernorm_fwd<T>(const float*, const float*, const float*, T*, float*, float*, int, int, \
                                         cudaStream_t);                                                      \
-  template cudaError_t layernorm_bwd<T>(const float*, const float*, const float*, const float*, const float*,   \
+  template cudaError_t layernorm_bwd<T>(const T*, const float*, const float*, const float*, const float*,       \
                                         const float*, float*, T*, float*, float*, float*, int, int, cudaStream_t,  \
                                         float*);                                                                \
   template cudaError_t ce_fwd_bwd<T>(T*, const int32_t*, int, int, int, float*, float*, int, int, float,    \

@@ -547,10 +547,10 @@ class Engine final : public EngineBase {
     float* gr = S.grad_out + row * H;  // fp32 gradient at the stage output, rows of this job
     if (S.k == m.K - 1) {
       const float* P = S.psmall;
-      Epi e; e.kind = EPI_STORE; e.out = S.dA; e.ldo = H; e.out_f32 = 1;
+      Epi e; e.kind = EPI_STORE; e.out = S.dA; e.ldo = H; e.out_f32 = std::is_same<T, float>::value;
       TRY(gemm(KC_GEMM_DX, gd(Tn, H, V, S.Z + row * V, V, false, S.wout_io, V, false), e));
       TRY(launch(KC_LN, 0, (12.0 + ebytes) * Tn * H, [&] {
-        return layernorm_bwd<T>(S.dA, S.hs[S.nl] + row * H, S.stf + row, S.stf + (size_t)batch * s + row, P + S.L.s_lnf_g, nullptr, gr,
+        return layernorm_bwd<T>(reinterpret_cast<const T*>(S.dA), S.hs[S.nl] + row * H, S.stf + row, S.stf + (size_t)batch * s + row, P + S.L.s_lnf_g, nullptr, gr,
                                 S.dhout_b[S.nl - 1] + row * H, S.gflat + S.L.lnf_g, S.gflat + S.L.lnf_b, S.lnws, Tn, H, stream,
                                 S.gflat + S.L.layers[S.nl - 1].b_2);
       }));
@@ -567,11 +567,11 @@ class Engine final : public EngineBase {
       // FFN: dU = (dh W_2^T) * gelu'(U)
       Epi e1; e1.kind = EPI_DGELU; e1.out = S.dU[j] + row * 4 * H; e1.ldo = 4 * H; e1.aux = S.U[j] + row * 4 * H; e1.ld_aux = 4 * H;
       TRY(gemm(KC_GEMM_DX, gd(Tn, 4 * H, H, S.dhout_b[j] + row * H, H, false, S.w2_io[j], H, false), e1));
-      Epi e2; e2.kind = EPI_STORE; e2.out = S.dA; e2.ldo = H; e2.out_f32 = 1;
+      Epi e2; e2.kind = EPI_STORE; e2.out = S.dA; e2.ldo = H; e2.out_f32 = std::is_same<T, float>::value;
       TRY(gemm(KC_GEMM_DX, gd(Tn, H, 4 * H, S.dU[j] + row * 4 * H, 4 * H, false, S.w1_io[j], 4 * H, false), e2));
       float* st2 = S.st2[j];
       TRY(launch(KC_LN, 0, (16.0 + ebytes) * Tn * H, [&] {
-        return layernorm_bwd<T>(S.dA, S.hmid[j] + row * H, st2 + row, st2 + (size_t)batch * s + row, P + fs.ln2_g, gr, S.gm,
+        return layernorm_bwd<T>(reinterpret_cast<const T*>(S.dA), S.hmid[j] + row * H, st2 + row, st2 + (size_t)batch * s + row, P + fs.ln2_g, gr, S.gm,
                                 S.dhmid_b[j] + row * H, GR + f.ln2_g, GR + f.ln2_b, S.lnws, Tn, H, stream, GR + f.b_o);
       }));
       // attention: dO = dh_mid W_o^T, then slice-vs-prefix attention backward with dK/dV push
@@ -618,13 +618,13 @@ class Engine final : public EngineBase {
         }
         return cudaSuccess;
       }));
-      Epi e4; e4.kind = EPI_STORE; e4.out = S.dA; e4.ldo = H; e4.out_f32 = 1;
+      Epi e4; e4.kind = EPI_STORE; e4.out = S.dA; e4.ldo = H; e4.out_f32 = std::is_same<T, float>::value;
       TRY(gemm(KC_GEMM_DX, gd(Tn, H, 3 * H, dq, 3 * H, false, S.wqkv_io[j], 3 * H, false), e4));
       float* gnext = j == 0 ? S.grad_in + row * H : (gr == S.gA ? S.gB : S.gA);
       T* copy = j == 0 ? nullptr : S.dhout_b[j - 1] + row * H;
       float* st1 = S.st1[j];
       TRY(launch(KC_LN, 0, (16.0 + ebytes) * Tn * H, [&] {
-        return layernorm_bwd<T>(S.dA, S.hs[j] + row * H, st1 + row, st1 + (size_t)batch * s + row, P + fs.ln1_g, S.gm, gnext, copy,
+        return layernorm_bwd<T>(reinterpret_cast<const T*>(S.dA), S.hs[j] + row * H, st1 + row, st1 + (size_t)batch * s + row, P + fs.ln1_g, S.gm, gnext, copy,
                                 GR + f.ln1_g, GR + f.ln1_b, S.lnws, Tn, H, stream,
                                 j == 0 ? nullptr : GR + S.L.layers[j - 1].b_2);
       }));
