@@ -34,6 +34,8 @@ struct Epi {
   int s_len = 0, head_dim = 0, hidden = 0, row0 = 0;
   int bs = 1;                 // QKV: rows m -> (sequence m % bs, position row0 + m / bs); sequences s_len*hidden apart
   int n_off = 0;              // column offset of this GEMM in the epilogue's column space (N-split launches)
+  float* dbias = nullptr;     // DGELU (tcgen05 GEMM): += column sums of the output (the bias gradient of
+                              // the layer whose dY this is), one 16-byte L2 reduction per warp and 8 columns
 };
 
 // tanh: exact libm form in fp32 mode; the MUFU tanh.approx (rel. err ~2^-11, below the bf16 output

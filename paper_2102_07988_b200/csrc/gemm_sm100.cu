@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // global access of the fused epilogue is a 64/128-byte contiguous row segment.
       float* scr = epi_scratch + (warp - 2) * 32 * 33;
       const bool has_aux = epi.kind == EPI_RESID || epi.kind == EPI_DGELU;
+      const bool has_dbias = epi.kind == EPI_DGELU && epi.dbias != nullptr;
 #pragma unroll 1
       for (int ch = ((warp - 2) >> 2) * (BN / 64); ch < (((warp - 2) >> 2) + 1) * (BN / 64); ++ch) {
         const int n = n0 + ch * 32 + (lane & 3) * 8;
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) scr[lane * 33 + i] = __uint_as_float(r[i]);
         __syncwarp();
+        float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // column sums (Epi::dbias)
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
           const int rr = it * 8 + (lane >> 2);
@@ -208,7 +210,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           float v[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) v[i] = scr[rr * 33 + (lane & 3) * 8 + i];
-          if (row < M && n < N) epi_apply8<bf16>(epi, row, n + epi.n_off, v, aux[it]);
+          if (row < M && n < N) {
+            epi_apply8<bf16>(epi, row, n + epi.n_off, v, aux[it]);
+            if (has_dbias)
+#pragma unroll
+              for (int i = 0; i < 8; ++i) cs[i] += v[i];
+          }
+        }
+        if (has_dbias) {  // the 8 lanes holding the same 8 columns (lane bits 2-4) reduce the warp's 32 rows
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 4);
+            cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 8);
+            cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 16);
+          }
+          if (lane < 4 && n < N) {
+            float* d = epi.dbias + n + epi.n_off;
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d), "f"(cs[0]), "f"(cs[1]), "f"(cs[2]),
+                         "f"(cs[3]) : "memory");
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d + 4), "f"(cs[4]), "f"(cs[5]),
+                         "f"(cs[6]), "f"(cs[7]) : "memory");
+          }
         }
         __syncwarp();
       }

@@ -432,8 +432,15 @@ class Engine final : public EngineBase {
     Pending p;
     instr.begin(st, cls, 2.0 * g.M * g.N * g.K, 0, p);
     cudaError_t err;
-    if (!force_simt && std::is_same<T, bf16>::value && gemm_sm100_supported(g)) err = gemm_sm100(g, e, st);
-    else err = gemm_simt<T>(g, e, st);
+    if (!force_simt && std::is_same<T, bf16>::value && gemm_sm100_supported(g)) {
+      err = gemm_sm100(g, e, st);
+    } else {
+      Epi e0 = e;
+      e0.dbias = nullptr;  // the SIMT epilogue has no fused column sums: a separate pass
+      err = gemm_simt<T>(g, e0, st);
+      if (err == cudaSuccess && e.dbias)
+        err = colsum_accum<T>(reinterpret_cast<const T*>(e.out), e.ldo, e.dbias, g.M, g.N, st);
+    }
     instr.end(st, p);
     if (err != cudaSuccess) return fail(TP_ECUDA, "gemm M=%d N=%d K=%d: %s", g.M, g.N, g.K, cudaGetErrorString(err));
     return TP_OK;
@@ -566,6 +573,7 @@ class Engine final : public EngineBase {
       float* GR = S.gflat;
       // FFN: dU = (dh W_2^T) * gelu'(U)
       Epi e1; e1.kind = EPI_DGELU; e1.out = S.dU[j] + row * 4 * H; e1.ldo = 4 * H; e1.aux = S.U[j] + row * 4 * H; e1.ld_aux = 4 * H;
+      e1.dbias = GR + f.b_1;  // FC1's bias gradient = column sums of dU, fused into this GEMM's epilogue
       TRY(gemm(KC_GEMM_DX, gd(Tn, 4 * H, H, S.dhout_b[j] + row * H, H, false, S.w2_io[j], H, false), e1));
       Epi e2; e2.kind = EPI_STORE; e2.out = S.dA; e2.ldo = H; e2.out_f32 = std::is_same<T, float>::value;
       TRY(gemm(KC_GEMM_DX, gd(Tn, H, 4 * H, S.dU[j] + row * 4 * H, 4 * H, false, S.w1_io[j], 4 * H, false), e2));
@@ -666,11 +674,11 @@ class Engine final : public EngineBase {
       e.out = GR + f.w_2; e.ldo = H;
       TRY(gemm(KC_GEMM_DW, G(4 * H, H, S.G[j] + row0 * 4 * H, 4 * H, S.dhout_b[j] + row0 * H, H), e, st));
       Pending p;
-      instr.begin(st, KC_MISC, 0, sizeof(T) * 7.0 * K * H, p);
-      // b_o and b_2 are summed by the LayerNorm backward that produces their dY (fused column sums),
-      // except b_2 of a non-last stage's last layer, whose dY arrives from the next stage
+      instr.begin(st, KC_MISC, 0, sizeof(T) * 3.0 * K * H, p);
+      // b_o and b_2 are summed by the LayerNorm backward that produces their dY, b_1 by the GeLU'
+      // epilogue of the FC2 dX GEMM (fused column sums), except b_2 of a non-last stage's last layer,
+      // whose dY arrives from the next stage
       cudaError_t r = colsum_accum<T>(S.dQKV[j] + row0 * 3 * H, 3 * H, GR + f.b_qkv, K, 3 * H, st);
-      if (r == cudaSuccess) r = colsum_accum<T>(S.dU[j] + row0 * 4 * H, 4 * H, GR + f.b_1, K, 4 * H, st);
       if (r == cudaSuccess && j == S.nl - 1 && S.k != m.K - 1)
         r = colsum_accum<T>(S.dhout_b[j] + row0 * H, H, GR + f.b_2, K, H, st);
       instr.end(st, p);
