@@ -27,6 +27,55 @@ __device__ __forceinline__ float block_sum(float v, float* red /*[NT/32]*/) {
   return t;
 }
 
+// One warp per row for H <= 32 * 8 * NCW (the row in registers, shuffle reductions, no block
+// barrier): 8 rows per 256-thread CTA, so many rows' loads are in flight per SM.
+template <typename T, int NCW>
+__global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const float* __restrict__ x, const float* __restrict__ gam,
+                                                          const float* __restrict__ bet, T* __restrict__ y,
+                                                          float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                                                          int rows, int H) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const float* xr = x + (int64_t)r * H;
+  float v[NCW][8];
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < NCW; ++c) {
+    const int col = (c * 32 + lane) * 8;
+    if (col < H) load8<float>(xr + col, v[c]);
+    else
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[c][i] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += v[c][i];
+  }
+  const float mean = warp_sum(s) / H;
+  float q = 0.f;
+#pragma unroll
+  for (int c = 0; c < NCW; ++c) {
+    const int col = (c * 32 + lane) * 8;
+    if (col < H)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { const float d = v[c][i] - mean; q += d * d; }
+  }
+  const float rstd = rsqrtf(warp_sum(q) / H + 1e-5f);
+  if (lane == 0) { mean_out[r] = mean; rstd_out[r] = rstd; }
+  T* yr = y + (int64_t)r * H;
+#pragma unroll
+  for (int c = 0; c < NCW; ++c) {
+    const int col = (c * 32 + lane) * 8;
+    if (col < H) {
+      float g[8], b[8], o[8];
+      load8<float>(gam + col, g);
+      load8<float>(bet + col, b);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = (v[c][i] - mean) * rstd * g[i] + b[i];
+      store8<T>(yr + col, o);
+    }
+  }
+}
+
 template <typename T, int NT, int NCH>
 __global__ void __launch_bounds__(NT) ln_fwd_kernel(const float* __restrict__ x, const float* __restrict__ gam,
                                                     const float* __restrict__ bet, T* __restrict__ y,
@@ -380,7 +429,7 @@ template <typename T>
 cudaError_t layernorm_fwd(const float* x, const float* gam, const float* bet, T* y, float* mean, float* rstd,
                           int rows, int H, cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
-  if (H <= 2048) ln_fwd_kernel<T, 256, 1><<<rows, 256, 0, st>>>(x, gam, bet, y, mean, rstd, H);
+  if (H <= 2048) ln_fwd_warp_kernel<T, 8><<<(rows + 7) / 8, 256, 0, st>>>(x, gam, bet, y, mean, rstd, rows, H);
   else if (H <= 4096) ln_fwd_kernel<T, 256, 2><<<rows, 256, 0, st>>>(x, gam, bet, y, mean, rstd, H);
   else if (H <= 6144) ln_fwd_kernel<T, 256, 3><<<rows, 256, 0, st>>>(x, gam, bet, y, mean, rstd, H);
   else if (H <= 12288) ln_fwd_kernel<T, 512, 3><<<rows, 512, 0, st>>>(x, gam, bet, y, mean, rstd, H);
