@@ -3,15 +3,13 @@
 // Same contract as attn_tc.cu (Eq. 2; one job = one sequence's slice rows
 // [c, c+l) attending keys [0, c+r] of the per-layer prefix K/V cache [a][s][d]), for d = 128.
 //
-// Forward, per (128-query tile, head), 6 warps:
-//   warp 0  TMA producer: Q once, then K_j / V_j 128-key blocks (3-D maps [a][c+l][d], rows past
-//           the prefix zero-filled) into a 2-deep ring;
-//   warp 1  MMA issuer (one thread): S_j = Q K_j^T -> TMEM (2 buffers x 128 fp32 columns), and
-//           O_j = P_j V_j -> TMEM (2 buffers) with P_j read from shared memory (K-major) and V_j as
-//           an MN-major operand (no transpose pass);
-//   warps 2-5 softmax: thread t owns query row t (its TMEM lane), so row max / sum need no
-//           shuffles: pass 1 reads S_j for the max, pass 2 writes P_j = exp2(S_j*scale - m) as bf16
-//           into the 128B-swizzled P tile; O is accumulated in registers, o = o*exp2(m_old-m_j) + O_j.
+// Forward (attn_fwd2_sm100_kernel): per 256 query rows (two 128-row tiles) x head x sequence,
+// heaviest tiles first; K_j / V_j 128-key blocks are TMA-loaded once per CTA for both tiles (4-D maps
+// {d, c+l, a, seq}, rows past the prefix zero-filled); S_t = Q_t K_j^T and O_t += P_t V_j on tcgen05
+// with P_t written back over S_t in TMEM (TS-MMA), O kept in TMEM and rescaled lazily; one thread
+// per query row for the softmax (see the kernel's comment).
+// Backward (attn_bwd_sm100_kernel): per 128-key block x head x sequence, software-pipelined over
+// the 64-query tiles that see the block (see the kernel's comment).
 // Key blocks are aligned to absolute multiples of 128; only blocks crossing a query's position are
 // masked element-wise.
 #include <unistd.h>
@@ -37,13 +35,7 @@ constexpr float LOG2E_F = 1.4426950408889634f;
 // K and V in separate rings: K_j is released as soon as S_j is computed (3 stages), V_j after
 // O_j = P_j V_j (2 stages), so the loads run two key blocks ahead of the MMAs that need them.
 constexpr int NKS = 3, NVS = 2;
-struct FwdSmem {
-  static constexpr uint32_t Q = 0, K = TILE, V = K + NKS * TILE;
-  static constexpr uint32_t BAR = V + NVS * TILE;
-  static constexpr uint32_t XCH = BAR + 256;  // fp32 [2 parity][2 halves][128 rows]: partial row maxima / sums
-  static constexpr uint32_t BYTES = XCH + 3072 + 1024;  // + [2][128] partial sums
-};
-constexpr int FWD_THREADS = 320;  // TMA warp, MMA warp, 8 softmax warps (2 per TMEM lane quarter)
+
 
 __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -122,240 +114,6 @@ __device__ __forceinline__ uint32_t swz(int row, int cc) {
   return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((cc ^ (row & 7)) << 4));
 }
 
-__global__ void __launch_bounds__(FWD_THREADS, 1)
-    attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                          const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ o, int64_t ldo,
-                          float* __restrict__ lse, int s, int c, int l, float scale_log2, int64_t o_sstride,
-                          int64_t lse_sstride, long long* trace) {
-#define TRF(role, ev, i)                                                                  \
-  do {                                                                                    \
-    if (trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (i) < 64) trace[((role) * 8 + (ev)) * 64 + (i)] = clock64(); \
-  } while (0)
-  extern __shared__ uint8_t smem_raw[];
-  // 1024-aligned base derived by pointer arithmetic on the __shared__ array (not through an
-  // integer cast), so the compiler keeps the shared state space: LDS/STS instead of generic LD/ST
-  uint8_t* sm = smem_raw + ((1024u - (tc5::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + FwdSmem::BAR);
-  uint64_t* qfull = bars + 0;
-  uint64_t* kfull = bars + 1;    // [3]
-  uint64_t* kfree = bars + 4;    // [3]
-  uint64_t* vfull = bars + 7;    // [2]
-  uint64_t* vfree = bars + 9;    // [2]
-  uint64_t* sfull = bars + 11;   // [2]
-  uint64_t* sfree = bars + 13;   // [2]
-  uint64_t* pfull = bars + 15;   // [2] P_j written into S buffer j%2
-  uint64_t* ofull = bars + 17;   // [2]
-  uint64_t* ofree = bars + 19;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // heaviest query tiles (the most key blocks) first: LPT order over the whole grid
-  const int head = blockIdx.x, sq = blockIdx.y, r0 = (gridDim.z - 1 - blockIdx.z) * AT;
-  o += sq * o_sstride;
-  lse += sq * lse_sstride;
-  const int qlast = c + min(l, r0 + AT) - 1;
-  const int nkb = qlast / AT + 1;
-
-  if (threadIdx.x == 0) {
-    mbar_init(qfull, 1);
-    for (int i = 0; i < NKS; ++i) { mbar_init(kfull + i, 1); mbar_init(kfree + i, 1); }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(vfull + i, 1); mbar_init(vfree + i, 1);
-      mbar_init(sfull + i, 1); mbar_init(sfree + i, 1);
-      mbar_init(ofull + i, 1); mbar_init(ofree + i, 8);
-      mbar_init(pfull + i, 8);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer
-    mbar_expect_tx(qfull, TILE);
-    tma_load_4d(sm + FwdSmem::Q, &tmQ, 0, c + r0, head, sq, qfull);
-    tma_load_4d(sm + FwdSmem::Q + HALF, &tmQ, 64, c + r0, head, sq, qfull);
-    for (int j = 0; j < nkb; ++j) {
-      const int bk = j % NKS, bv = j & 1;
-      if (j >= NKS) mbar_wait(kfree + bk, ((j / NKS) - 1) & 1);
-      TRF(0, 0, j);
-      uint8_t* kd = sm + FwdSmem::K + bk * TILE;
-      mbar_expect_tx(kfull + bk, TILE);
-      tma_load_4d(kd, &tmK, 0, j * AT, head, sq, kfull + bk);
-      tma_load_4d(kd + HALF, &tmK, 64, j * AT, head, sq, kfull + bk);
-      if (j >= NVS) mbar_wait(vfree + bv, ((j >> 1) - 1) & 1);
-      uint8_t* vd = sm + FwdSmem::V + bv * TILE;
-      mbar_expect_tx(vfull + bv, TILE);
-      tma_load_4d(vd, &tmV, 0, j * AT, head, sq, vfull + bv);
-      tma_load_4d(vd + HALF, &tmV, 64, j * AT, head, sq, vfull + bv);
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer (whole warp; one elected lane issues)
-    constexpr uint32_t idS = idesc_bf16(128, 128, false, false);
-    constexpr uint32_t idO = idesc_bf16(128, 128, false, true);
-    const uint32_t q_base = smem_u32(sm + FwdSmem::Q);
-    // O_i = P_i V_i with P_i (bf16) read from TMEM, where the softmax warps wrote it over the
-    // consumed S_i columns (S buffer bi, 64 packed columns); the commit then frees that S buffer.
-    auto pv = [&](int i) {
-      const int bi = i & 1;
-      mbar_wait(pfull + bi, (i >> 1) & 1);
-      if (lane == 0) TRF(1, 3, i);
-      if (i >= 2) mbar_wait(ofree + bi, ((i >> 1) - 1) & 1);
-      mbar_wait(vfull + bi, (i >> 1) & 1);
-      if (lane == 0) TRF(1, 4, i);
-      tc_fence_after();
-      const uint32_t v_base = smem_u32(sm + FwdSmem::V + bi * TILE);
-#pragma unroll
-      for (int kk = 0; kk < AT / 16; ++kk) {
-        const uint64_t bd = make_desc(v_base + kk * 2048, HALF, 1024);
-        mma_bf16_ts_w(tmem + 256 + bi * 128, tmem + bi * 128 + kk * 8, bd, idO, kk > 0);
-      }
-      mma_commit_w(ofull + bi);
-      mma_commit_w(sfree + bi);
-      mma_commit_w(vfree + bi);
-      if (lane == 0) TRF(1, 5, i);
-    };
-    mbar_wait(qfull, 0);
-    for (int j = 0; j < nkb; ++j) {
-      const int b = j & 1;
-      const int bk = j % NKS;
-      mbar_wait(kfull + bk, (j / NKS) & 1);
-      if (lane == 0) TRF(1, 0, j);
-      if (j >= 2) mbar_wait(sfree + b, ((j >> 1) - 1) & 1);
-      if (lane == 0) TRF(1, 1, j);
-      tc_fence_after();
-      const uint32_t k_base = smem_u32(sm + FwdSmem::K + bk * TILE);
-#pragma unroll
-      for (int kk = 0; kk < AT / 16; ++kk) {
-        const uint32_t off = (kk >> 2) * HALF + (kk & 3) * 32;
-        mma_bf16_w(tmem + b * 128, make_desc(q_base + off, 16, 1024), make_desc(k_base + off, 16, 1024), idS, kk > 0);
-      }
-      mma_commit_w(sfull + b);
-      mma_commit_w(kfree + bk);
-      if (lane == 0) TRF(1, 2, j);
-      if (j >= 1) pv(j - 1);
-    }
-    pv(nkb - 1);
-  } else if (warp >= 2) {
-    // ---------------- softmax / output: two warps per TMEM lane quarter; thread owns query row
-    // `row` and the key / head-dim columns [half*64, half*64+64); the two halves exchange row maxima
-    // through shared memory once per key block (named barrier 1, 256 threads).
-    const int q = warp & 3, row = q * 32 + lane, half = (warp - 2) >> 2;
-    const int qabs = c + r0 + row;
-    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    float* xch = reinterpret_cast<float*>(sm + FwdSmem::XCH);
-    float m = -INFINITY, lsum = 0.f, m_acc = -INFINITY, m_last = -INFINITY;
-    constexpr int HC = AT / 2;  // columns per half
-    float acc[HC];
-#pragma unroll
-    for (int i = 0; i < HC; ++i) acc[i] = 0.f;
-    auto add_o = [&](int i, float m_i) {
-      const int bi = i & 1;
-      mbar_wait(ofull + bi, (i >> 1) & 1);
-      if (threadIdx.x == 64) TRF(2, 3, i);
-      tc_fence_after();
-      const float sc = ex2(m_acc - m_i);
-#pragma unroll
-      for (int ch = 0; ch < HC / 32; ++ch) {
-        uint32_t r[32];
-        tmem_ld32_nowait(lane_base + 256 + bi * 128 + half * HC + ch * 32, r);
-        tmem_wait_ld();
-#pragma unroll
-        for (int t = 0; t < 32; ++t) acc[ch * 32 + t] = fmaf(acc[ch * 32 + t], sc, __uint_as_float(r[t]));
-      }
-      m_acc = m_i;
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(ofree + bi);
-      if (threadIdx.x == 64) TRF(2, 4, i);
-    };
-    for (int j = 0; j < nkb; ++j) {
-      const int b = j & 1;
-      mbar_wait(sfull + b, (j >> 1) & 1);
-      if (threadIdx.x == 64) TRF(2, 0, j);
-      tc_fence_after();
-      const int key0 = j * AT + half * HC;       // first key of this half
-      const bool diag = key0 + HC - 1 > qabs;    // only blocks crossing the diagonal need the mask
-      const int nvis = qabs - key0 + 1;          // keys key0 .. qabs are visible
-      // pass 1: this half's 64 scores -> registers, partial row max (scale > 0 commutes with max),
-      // exchanged with the other half. After the exchange barrier nobody reads S_j from TMEM again,
-      // so P_j may overwrite any of its columns.
-      float sv[HC];
-      float mx = -INFINITY;
-#pragma unroll
-      for (int ch = 0; ch < HC / 32; ++ch) {
-        uint32_t r[32];
-        tmem_ld32_nowait(lane_base + b * 128 + half * HC + ch * 32, r);
-        tmem_wait_ld();
-#pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          float x = __uint_as_float(r[t]);
-          if (diag && ch * 32 + t >= nvis) x = -INFINITY;
-          sv[ch * 32 + t] = x;
-          mx = fmaxf(mx, x);
-        }
-      }
-      float* xm = xch + (j & 1) * 256;
-      xm[half * 128 + row] = mx;
-      named_bar(1, 256);
-      if (threadIdx.x == 64) TRF(2, 1, j);
-      mx = fmaxf(mx, xm[(half ^ 1) * 128 + row]);
-      const float m_new = fmaxf(m, mx * scale_log2);
-      // pass 2: P = exp2(S * scale_log2 - m_new) -> bf16, packed two per TMEM column in key order
-      float rs = 0.f;
-#pragma unroll
-      for (int ch = 0; ch < HC / 32; ++ch) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int t = 0; t < 32; t += 2) {
-          const float p0 = ex2(fmaf(sv[ch * 32 + t], scale_log2, -m_new));
-          const float p1 = ex2(fmaf(sv[ch * 32 + t + 1], scale_log2, -m_new));
-          rs += p0 + p1;
-          __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
-          pk[t >> 1] = *reinterpret_cast<uint32_t*>(&h);
-        }
-        // keys [half*64 + ch*32, +32) -> packed TMEM columns half*32 + ch*16 .. +16 of S buffer b
-        tmem_st16(lane_base + b * 128 + half * (HC / 2) + ch * 16, pk);
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(pfull + b);
-      if (threadIdx.x == 64) TRF(2, 2, j);
-      lsum = lsum * ex2(m - m_new) + rs;  // partial (this half's keys), same m in both halves
-      m_last = m;
-      m = m_new;
-      if (j >= 1) add_o(j - 1, m_last);
-    }
-    add_o(nkb - 1, m);
-    float* xl = xch + 512;  // after the two max buffers
-    xl[half * 128 + row] = lsum;
-    named_bar(1, 256);
-    const float ltot = lsum + xl[(half ^ 1) * 128 + row];
-    const int r = r0 + row;
-    if (r < l) {
-      const float inv = 1.f / ltot;
-      bf16* orow = o + (int64_t)r * ldo + head * AT + half * HC;
-#pragma unroll
-      for (int i = 0; i < HC; i += 8) {
-        float v8[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) v8[t] = acc[i + t] * inv;
-        store8<bf16>(orow + i, v8);
-      }
-      if (half == 0) lse[(int64_t)head * s + c + r] = (m + log2f(ltot)) / LOG2E_F;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
 
 // ------------------------------------------------------------------ forward, two query tiles
 // Per (256 query rows = two 128-row tiles, head, sequence), LPT order. Each K_j / V_j block loaded
@@ -422,6 +180,11 @@ struct Fwd2Smem {
 };
 constexpr float RESCALE_LOG2 = 8.f;
 
+// TP_ATTN_TRACE: clock64 timeline of CTA (0, 0, 0), slot (role * 8 + event) * 64 + key block
+#define TRF(role, ev, i)                                                                  \
+  do {                                                                                    \
+    if (trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (i) < 64) trace[((role) * 8 + (ev)) * 64 + (i)] = clock64(); \
+  } while (0)
 __global__ void __launch_bounds__(F2_THREADS, 1)
     attn_fwd2_sm100_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                            const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ o, int64_t ldo,
@@ -1089,13 +852,6 @@ cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o,
                            int64_t lse_sstride) {
   if (l == 0 || nseq == 0) return cudaSuccess;
   if (d != AT) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)FwdSmem::BYTES);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
   // [seq][a][s][d] viewed as 4-D {d, rows = c + l (prefix), a, seq}: rows past the prefix zero-filled
   const uint64_t dims[4] = {(uint64_t)d, (uint64_t)(c + l), (uint64_t)a, (uint64_t)nseq};
   const uint64_t strides[3] = {(uint64_t)d * 2, (uint64_t)s * d * 2, (uint64_t)(nseq > 1 ? qkv_sstride : (int64_t)a * s * d) * 2};
@@ -1104,8 +860,7 @@ cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o,
   if (!encode_bf16_map(&mq, q, 4, dims, strides, box) || !encode_bf16_map(&mk, k, 4, dims, strides, box) ||
       !encode_bf16_map(&mv, v, 4, dims, strides, box))
     return cudaErrorInvalidValue;
-  static const bool v1 = getenv("TP_ATTN_FWD_V1") != nullptr;
-  if (!v1) {
+  {
     static bool attr2 = false;
     if (!attr2) {
       cudaError_t e = cudaFuncSetAttribute(attn_fwd2_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1138,29 +893,6 @@ cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o,
     }
     return cudaGetLastError();
   }
-  dim3 grid(a, nseq, (l + AT - 1) / AT);
-  static int trace_left = getenv("TP_ATTN_TRACE") ? atoi(getenv("TP_ATTN_TRACE")) : 0;
-  static long long* trace = nullptr;
-  if (trace_left > 0 && !trace) cudaMalloc(&trace, 3 * 8 * 64 * sizeof(long long));
-  if (trace_left > 0) cudaMemsetAsync(trace, 0, 3 * 8 * 64 * sizeof(long long), st);
-  attn_fwd_sm100_kernel<<<grid, FWD_THREADS, FwdSmem::BYTES, st>>>(mq, mk, mv, o, ldo, lse, s, c, l, rsqrtf((float)d) * LOG2E_F,
-                                                           o_sstride, lse_sstride, trace_left > 0 ? trace : nullptr);
-  if (trace_left > 0) {
-    --trace_left;
-    long long h[3 * 8 * 64];
-    cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    long long t0 = 0;
-    for (int i = 0; i < 3 * 8 * 64; ++i) if (h[i] && (!t0 || h[i] < t0)) t0 = h[i];
-    fprintf(stderr, "attn_fwd trace c=%d l=%d: kb | P:kvfree | M:kvfull M:sfree M:Scommit M:pfull M:ofree M:PVcommit | S:sfull S:maxbar S:pfull S:ofull S:addO\n", c, l);
-    for (int i = 0; i < 64; ++i) {
-      auto g = [&](int r, int e) { long long v = h[(r * 8 + e) * 64 + i]; return v ? (long long)(v - t0) : -1LL; };
-      if (g(1, 0) < 0) break;
-      fprintf(stderr, "%3d | %7lld | %7lld %7lld %7lld %7lld %7lld %7lld | %7lld %7lld %7lld %7lld %7lld\n", i, g(0, 0), g(1, 0),
-              g(1, 1), g(1, 2), g(1, 3), g(1, 4), g(1, 5), g(2, 0), g(2, 1), g(2, 2), g(2, 3), g(2, 4));
-    }
-  }
-  return cudaGetLastError();
 }
 
 cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t ldo, const bf16* q, const bf16* k,
