@@ -44,10 +44,17 @@ constexpr int BM = 128, BK = 64;
 // keep up with a 256-wide tile at K = 2048).
 constexpr int GEMM_THREADS = 320;
 
-template <int CG, int BN>
+// WN = 1: tile N = BN with a double-buffered accumulator (epilogue of tile t overlaps the MMAs of
+// tile t+1). WN = 2: tile N = 2 * BN as two side-by-side accumulators, single-buffered — 25 % fewer
+// operand bytes per FLOP (A is shared by twice the columns) at the price of an un-overlapped
+// epilogue; used for long-K GEMMs (dW with K = B*s, FC2 / FC1-dX with K = 4H).
+template <int CG, int BN, int WN = 1>
 struct Cfg {
   static constexpr uint32_t A_BYTES = BM * BK * 2;
-  static constexpr uint32_t B_BYTES = (BN / CG) * BK * 2;
+  static constexpr uint32_t B_HALF = (BN / CG) * BK * 2;   // one accumulator's B rows of this CTA
+  static constexpr uint32_t B_BYTES = WN * B_HALF;
+  static constexpr int TILE_N = WN * BN;
+  static constexpr int NACC = WN == 1 ? 2 : 1;             // accumulator buffers in flight
   static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
   static constexpr int NS = (196608 / STAGE) > 8 ? 8 : (196608 / STAGE);  // pipeline depth
   static constexpr uint32_t EPI_SCRATCH = 8 * 32 * 33 * 4;  // per epilogue warp: 32 x 32 fp32 (+1 pad)
@@ -57,11 +64,11 @@ struct Cfg {
   static_assert(SMEM <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
-template <int CG, int BN, bool A_MN, bool B_MN>
+template <int CG, int BN, bool A_MN, bool B_MN, int WN = 1>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                       int K, Epi epi) {
-  using C = Cfg<CG, BN>;
+  using C = Cfg<CG, BN, WN>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-aligned base derived by pointer arithmetic on the __shared__ array (not through an
   // integer cast), so the compiler keeps the shared state space: LDS/STS instead of generic LD/ST
@@ -76,7 +83,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = CG == 2 ? cluster_rank() : 0;
   const bool leader = crank == 0;
-  const int m_tiles = (M + C::TILE_M - 1) / C::TILE_M, n_tiles = (N + BN - 1) / BN;
+  const int m_tiles = (M + C::TILE_M - 1) / C::TILE_M, n_tiles = (N + C::TILE_N - 1) / C::TILE_N;
   const int tiles = m_tiles * n_tiles, kbs = (K + BK - 1) / BK;
   const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;
 
@@ -111,31 +118,40 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint32_t phase = 0;
     for (int tile = unit; tile < tiles; tile += nunits) {
       const int m0 = (tile % m_tiles) * C::TILE_M + crank * BM;
-      const int nb0 = (tile / m_tiles) * BN + crank * (BN / CG);
+      const int nt0 = (tile / m_tiles) * C::TILE_N + crank * (BN / CG);
       for (int kb = 0; kb < kbs; ++kb) {
         mbar_wait(empty + stage, phase ^ 1);
         if (leader) mbar_expect_tx(full + stage, C::STAGE * CG);
         uint8_t* a_dst = smem + stage * C::STAGE;
-        uint8_t* b_dst = a_dst + C::A_BYTES;
         if (CG == 1) {
           if (!A_MN) tma_load_2d(a_dst, &tmA, kb * BK, m0, full + stage);
           else
 #pragma unroll
             for (int i = 0; i < BM / 64; ++i) tma_load_2d(a_dst + i * 8192, &tmA, m0 + i * 64, kb * BK, full + stage);
-          if (!B_MN) tma_load_2d(b_dst, &tmB, kb * BK, nb0, full + stage);
-          else
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i) tma_load_2d(b_dst + i * 8192, &tmB, nb0 + i * 64, kb * BK, full + stage);
+          for (int h = 0; h < WN; ++h) {
+            uint8_t* b_dst = a_dst + C::A_BYTES + h * C::B_HALF;
+            const int nb0 = nt0 + h * BN;
+            if (!B_MN) tma_load_2d(b_dst, &tmB, kb * BK, nb0, full + stage);
+            else
+#pragma unroll
+              for (int i = 0; i < BN / 64; ++i) tma_load_2d(b_dst + i * 8192, &tmB, nb0 + i * 64, kb * BK, full + stage);
+          }
         } else {
           const uint32_t bar = map_to_rank(smem_u32(full + stage), 0);
           if (!A_MN) tma_load_2d_pair(a_dst, &tmA, kb * BK, m0, bar);
           else
 #pragma unroll
             for (int i = 0; i < BM / 64; ++i) tma_load_2d_pair(a_dst + i * 8192, &tmA, m0 + i * 64, kb * BK, bar);
-          if (!B_MN) tma_load_2d_pair(b_dst, &tmB, kb * BK, nb0, bar);
-          else
 #pragma unroll
-            for (int i = 0; i < BN / CG / 64; ++i) tma_load_2d_pair(b_dst + i * 8192, &tmB, nb0 + i * 64, kb * BK, bar);
+          for (int h = 0; h < WN; ++h) {
+            uint8_t* b_dst = a_dst + C::A_BYTES + h * C::B_HALF;
+            const int nb0 = nt0 + h * BN;
+            if (!B_MN) tma_load_2d_pair(b_dst, &tmB, kb * BK, nb0, bar);
+            else
+#pragma unroll
+              for (int i = 0; i < BN / CG / 64; ++i) tma_load_2d_pair(b_dst + i * 8192, &tmB, nb0 + i * 64, kb * BK, bar);
+          }
         }
         if (++stage == C::NS) { stage = 0; phase ^= 1; }
       }
@@ -151,24 +167,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int tile = unit; tile < tiles; tile += nunits) {
       mbar_wait(tempty + acc, acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
+      const uint32_t d_tmem = tmem_base + acc * BN;  // WN = 2: acc = 0, halves at +0 and +BN
       for (int kb = 0; kb < kbs; ++kb) {
         mbar_wait(full + stage, phase);
         tc_fence_after();
         const uint32_t a_base = smem_u32(smem + stage * C::STAGE);
-        const uint32_t b_base = a_base + C::A_BYTES;
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k) {
           const uint64_t ad = A_MN ? make_desc(a_base + k * 2048, 8192, 1024) : make_desc(a_base + k * 32, 16, 1024);
-          const uint64_t bd = B_MN ? make_desc(b_base + k * 2048, 8192, 1024) : make_desc(b_base + k * 32, 16, 1024);
-          if (CG == 1) mma_bf16_w(d_tmem, ad, bd, idesc, (kb | k) != 0);
-          else mma_bf16_pair_w(d_tmem, ad, bd, idesc, (kb | k) != 0);
+#pragma unroll
+          for (int h = 0; h < WN; ++h) {
+            const uint32_t b_base = a_base + C::A_BYTES + h * C::B_HALF;
+            const uint64_t bd = B_MN ? make_desc(b_base + k * 2048, 8192, 1024) : make_desc(b_base + k * 32, 16, 1024);
+            if (CG == 1) mma_bf16_w(d_tmem + h * BN, ad, bd, idesc, (kb | k) != 0);
+            else mma_bf16_pair_w(d_tmem + h * BN, ad, bd, idesc, (kb | k) != 0);
+          }
         }
         if (CG == 1) mma_commit_w(empty + stage); else mma_commit_pair_w(empty + stage);  // frees the smem slot(s)
         if (++stage == C::NS) { stage = 0; phase ^= 1; }
       }
       if (CG == 1) mma_commit_w(tfull + acc); else mma_commit_pair_w(tfull + acc);        // accumulator ready
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == C::NACC) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 2) {
     // ---------------- epilogue: TMEM lanes (warp % 4) * 32 .. +31 = rows of this CTA's 128
@@ -177,7 +196,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = unit; tile < tiles; tile += nunits) {
-      const int m0 = (tile % m_tiles) * C::TILE_M + crank * BM, n0 = (tile / m_tiles) * BN;
+      const int m0 = (tile % m_tiles) * C::TILE_M + crank * BM, n0 = (tile / m_tiles) * C::TILE_N;
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
       // TMEM (thread = row) -> padded smem transpose -> 4 lanes per row, 8 columns each: every
@@ -186,7 +205,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const bool has_aux = epi.kind == EPI_RESID || epi.kind == EPI_DGELU;
       const bool has_dbias = epi.kind == EPI_DGELU && epi.dbias != nullptr;
 #pragma unroll 1
-      for (int ch = ((warp - 2) >> 2) * (BN / 64); ch < (((warp - 2) >> 2) + 1) * (BN / 64); ++ch) {
+      for (int ch = ((warp - 2) >> 2) * (C::TILE_N / 64); ch < (((warp - 2) >> 2) + 1) * (C::TILE_N / 64); ++ch) {
         const int n = n0 + ch * 32 + (lane & 3) * 8;
         // issue this chunk's residual / U loads first: 4 independent 32-byte loads in flight per thread
         float aux[4][8];
@@ -240,7 +259,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (CG == 1) mbar_arrive(tempty + acc);
         else mbar_arrive_cluster(tempty_leader + acc * 8);
       }
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == C::NACC) { acc = 0; acc_phase ^= 1; }
     }
   }
   tc_fence_before();
@@ -289,10 +308,10 @@ bool make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
   return r == CUDA_SUCCESS;
 }
 
-template <int CG, int BN, bool A_MN, bool B_MN>
+template <int CG, int BN, bool A_MN, bool B_MN, int WN = 1>
 cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
-  using C = Cfg<CG, BN>;
-  auto kern = gemm_sm100_kernel<CG, BN, A_MN, B_MN>;
+  using C = Cfg<CG, BN, WN>;
+  auto kern = gemm_sm100_kernel<CG, BN, A_MN, B_MN, WN>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -303,7 +322,7 @@ cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   bool ok = A_MN ? make_map(&ta, g.A, g.M, g.K, g.lda, 64, 64) : make_map(&ta, g.A, g.K, g.M, g.lda, 64, BM);
   ok = ok && (B_MN ? make_map(&tb, g.B, g.N, g.K, g.ldb, 64, 64) : make_map(&tb, g.B, g.K, g.N, g.ldb, 64, BN / CG));
   if (!ok) return cudaErrorInvalidValue;
-  const int tiles = ((g.M + C::TILE_M - 1) / C::TILE_M) * ((g.N + BN - 1) / BN);
+  const int tiles = ((g.M + C::TILE_M - 1) / C::TILE_M) * ((g.N + C::TILE_N - 1) / C::TILE_N);
   const int units = g.persistent ? std::min(tiles, g_num_sms / CG) : tiles;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * CG);
@@ -320,12 +339,12 @@ cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   return cudaLaunchKernelEx(&cfg, kern, ta, tb, g.M, g.N, g.K, e);
 }
 
-template <int CG, int BN>
+template <int CG, int BN, int WN = 1>
 cudaError_t launch_major(const GemmDesc& g, const Epi& e, cudaStream_t st) {
-  if (!g.a_mn && !g.b_mn) return launch_bn<CG, BN, false, false>(g, e, st);
-  if (g.a_mn && g.b_mn) return launch_bn<CG, BN, true, true>(g, e, st);
-  if (g.a_mn) return launch_bn<CG, BN, true, false>(g, e, st);
-  return launch_bn<CG, BN, false, true>(g, e, st);
+  if (!g.a_mn && !g.b_mn) return launch_bn<CG, BN, false, false, WN>(g, e, st);
+  if (g.a_mn && g.b_mn) return launch_bn<CG, BN, true, true, WN>(g, e, st);
+  if (g.a_mn) return launch_bn<CG, BN, true, false, WN>(g, e, st);
+  return launch_bn<CG, BN, false, true, WN>(g, e, st);
 }
 
 }  // namespace
@@ -390,6 +409,19 @@ cudaError_t gemm_sm100(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   // (efficiencies: per-SM operand bytes per MMA cycle are 64 / 96 / 96 / 128 B for the four shapes
   // against the ~42 B/clk L2 share; calibrated with scripts/bench_kernels.py)
   static const Cand cands[4] = {{2, 256, 1.0}, {2, 128, 0.8}, {1, 256, 0.8}, {1, 128, 0.65}};
+  // Wide pair tiles (256 x 512, WN = 2) for long K: 48 instead of 64 B/clk/SM of operands, with the
+  // epilogue no longer hidden behind the next tile's MMAs (relative cost ~ 1 + 4 / (K/64) k-blocks).
+  // TP_GEMM_WIDE=0 disables, =1 forces (when the shape allows).
+  const int wide_env = getenv("TP_GEMM_WIDE") ? atoi(getenv("TP_GEMM_WIDE")) : -1;
+  if (wide_env != 0 && !g_force_cg && g.persistent && g.M > BM && g.N >= 512 && (g.K >= 4096 || wide_env == 1)) {
+    const long units = g_num_sms / 2;
+    const long tw = (long)((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + 511) / 512);
+    const long t2 = (long)((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + 255) / 256);
+    const double kbs = (g.K + BK - 1) / BK;
+    const double cost_wide = (double)((tw + units - 1) / units) * 512 / 1.25 * (1.0 + 4.0 / kbs);
+    const double cost_256 = (double)((t2 + units - 1) / units) * 256;
+    if (wide_env == 1 || cost_wide < cost_256 * 0.97) return launch_major<2, 256, 2>(g, e, st);
+  }
   int best = -1;
   double best_cost = 0;
   for (int i = 0; i < 4; ++i) {
