@@ -64,10 +64,34 @@ struct Cfg {
   static_assert(SMEM <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
+// Stream-K tail: the tiles that would form a partial last wave are split along K into `S` parts
+// processed by different work units; each part writes its fp32 partial tile to a workspace, and
+// the last part to finish (atomic ticket per tile and CTA) sums them and runs the fused epilogue.
+struct SplitK {
+  int dp_tiles = 0;    // tiles [0, dp_tiles) run whole; [dp_tiles, tiles) run as S K-parts each
+  int S = 1;
+  float* ws = nullptr;  // [(tile - dp_tiles) * S + part][CG][128][TILE_N] fp32
+  int* cnt = nullptr;   // [(tile - dp_tiles) * CG + crank], zero between launches (the last part resets)
+};
+// Work item `it` of unit `unit`: first its whole tiles (round robin), then its tail K-parts.
+__device__ __forceinline__ bool gemm_item(int it, int unit, int nunits, int tiles, int kbs, const SplitK& sk,
+                                          int& tile, int& k0, int& k1, int& part) {
+  const int ndp = unit < sk.dp_tiles ? (sk.dp_tiles - unit + nunits - 1) / nunits : 0;
+  if (it < ndp) { tile = unit + it * nunits; k0 = 0; k1 = kbs; part = -1; return true; }
+  if (sk.S <= 1) return false;  // no split: dp_tiles == tiles
+  const int w = unit + (it - ndp) * nunits;
+  if (w >= (tiles - sk.dp_tiles) * sk.S) return false;
+  tile = sk.dp_tiles + w / sk.S;
+  part = w % sk.S;
+  k0 = (int)((int64_t)part * kbs / sk.S);
+  k1 = (int)((int64_t)(part + 1) * kbs / sk.S);
+  return true;
+}
+
 template <int CG, int BN, bool A_MN, bool B_MN, int WN = 1>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                      int K, Epi epi) {
+                      int K, Epi epi, SplitK sk) {
   using C = Cfg<CG, BN, WN>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-aligned base derived by pointer arithmetic on the __shared__ array (not through an
@@ -79,6 +103,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* tfull = empty + C::NS;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  volatile int* sk_ticket = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = CG == 2 ? cluster_rank() : 0;
@@ -116,10 +141,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // ---------------- TMA producer (both CTAs of a pair; bytes land on the leader's barrier)
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = unit; tile < tiles; tile += nunits) {
+    int tile, k0, k1, part;
+    for (int item = 0; gemm_item(item, unit, nunits, tiles, kbs, sk, tile, k0, k1, part); ++item) {
       const int m0 = (tile % m_tiles) * C::TILE_M + crank * BM;
       const int nt0 = (tile / m_tiles) * C::TILE_N + crank * (BN / CG);
-      for (int kb = 0; kb < kbs; ++kb) {
+      for (int kb = k0; kb < k1; ++kb) {
         mbar_wait(empty + stage, phase ^ 1);
         if (leader) mbar_expect_tx(full + stage, C::STAGE * CG);
         uint8_t* a_dst = smem + stage * C::STAGE;
@@ -164,11 +190,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                            | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(C::TILE_M >> 4) << 24);
     int stage = 0, acc = 0;
     uint32_t phase = 0, acc_phase = 0;
-    for (int tile = unit; tile < tiles; tile += nunits) {
+    int tile, k0, k1, part;
+    for (int item = 0; gemm_item(item, unit, nunits, tiles, kbs, sk, tile, k0, k1, part); ++item) {
       mbar_wait(tempty + acc, acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;  // WN = 2: acc = 0, halves at +0 and +BN
-      for (int kb = 0; kb < kbs; ++kb) {
+      for (int kb = k0; kb < k1; ++kb) {
         mbar_wait(full + stage, phase);
         tc_fence_after();
         const uint32_t a_base = smem_u32(smem + stage * C::STAGE);
@@ -179,8 +206,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int h = 0; h < WN; ++h) {
             const uint32_t b_base = a_base + C::A_BYTES + h * C::B_HALF;
             const uint64_t bd = B_MN ? make_desc(b_base + k * 2048, 8192, 1024) : make_desc(b_base + k * 32, 16, 1024);
-            if (CG == 1) mma_bf16_w(d_tmem + h * BN, ad, bd, idesc, (kb | k) != 0);
-            else mma_bf16_pair_w(d_tmem + h * BN, ad, bd, idesc, (kb | k) != 0);
+            if (CG == 1) mma_bf16_w(d_tmem + h * BN, ad, bd, idesc, (kb != k0) | (k != 0));
+            else mma_bf16_pair_w(d_tmem + h * BN, ad, bd, idesc, (kb != k0) | (k != 0));
           }
         }
         if (CG == 1) mma_commit_w(empty + stage); else mma_commit_pair_w(empty + stage);  // frees the smem slot(s)
@@ -195,64 +222,89 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const uint32_t tempty_leader = CG == 2 ? map_to_rank(smem_u32(tempty), 0) : 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = unit; tile < tiles; tile += nunits) {
-      const int m0 = (tile % m_tiles) * C::TILE_M + crank * BM, n0 = (tile / m_tiles) * C::TILE_N;
-      mbar_wait(tfull + acc, acc_phase);
-      tc_fence_after();
-      // TMEM (thread = row) -> padded smem transpose -> 4 lanes per row, 8 columns each: every
-      // global access of the fused epilogue is a 64/128-byte contiguous row segment.
-      float* scr = epi_scratch + (warp - 2) * 32 * 33;
-      const bool has_aux = epi.kind == EPI_RESID || epi.kind == EPI_DGELU;
-      const bool has_dbias = epi.kind == EPI_DGELU && epi.dbias != nullptr;
-#pragma unroll 1
-      for (int ch = ((warp - 2) >> 2) * (C::TILE_N / 64); ch < (((warp - 2) >> 2) + 1) * (C::TILE_N / 64); ++ch) {
-        const int n = n0 + ch * 32 + (lane & 3) * 8;
-        // issue this chunk's residual / U loads first: 4 independent 32-byte loads in flight per thread
-        float aux[4][8];
-        if (has_aux) {
+    // TMEM (thread = row) -> padded smem transpose -> 4 lanes per row, 8 columns each: every
+    // global access of the fused epilogue is a 64/128-byte contiguous row segment.
+    float* scr = epi_scratch + (warp - 2) * 32 * 33;
+    const bool has_aux = epi.kind == EPI_RESID || epi.kind == EPI_DGELU;
+    const bool has_dbias = epi.kind == EPI_DGELU && epi.dbias != nullptr;
+    const int ch0 = ((warp - 2) >> 2) * (C::TILE_N / 64), ch1 = ch0 + C::TILE_N / 64;
+    // mode 0: TMEM -> fused epilogue; 1: TMEM -> raw fp32 partial to `wsp`; 2: sum of the S partials
+    // at `wsp` (stride 128 * TILE_N * CG per part) -> fused epilogue
+    auto chunk = [&](int ch, int mode, int m0, int n0, float* wsp) {
+      const int n = n0 + ch * 32 + (lane & 3) * 8;
+      // issue this chunk's residual / U loads first: 4 independent 32-byte loads in flight per thread
+      float aux[4][8];
+      if (mode != 1 && has_aux) {
 #pragma unroll
-          for (int it = 0; it < 4; ++it) {
-            const int row = m0 + q * 32 + it * 8 + (lane >> 2);
-            if (row < M && n < N) epi_prefetch8<bf16>(epi, row, n + epi.n_off, aux[it]);
-          }
+        for (int it = 0; it < 4; ++it) {
+          const int row = m0 + q * 32 + it * 8 + (lane >> 2);
+          if (row < M && n < N) epi_prefetch8<bf16>(epi, row, n + epi.n_off, aux[it]);
         }
+      }
+      if (mode != 2) {
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 32, r);
 #pragma unroll
         for (int i = 0; i < 32; ++i) scr[lane * 33 + i] = __uint_as_float(r[i]);
         __syncwarp();
-        float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // column sums (Epi::dbias)
+      }
+      float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // column sums (Epi::dbias)
 #pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          const int rr = it * 8 + (lane >> 2);
-          const int row = m0 + q * 32 + rr;
-          float v[8];
+      for (int it = 0; it < 4; ++it) {
+        const int rr = it * 8 + (lane >> 2);
+        const int row = m0 + q * 32 + rr;
+        const int64_t woff = (int64_t)(q * 32 + rr) * C::TILE_N + (ch * 32 + (lane & 3) * 8);
+        float v[8];
+        if (mode != 2) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) v[i] = scr[rr * 33 + (lane & 3) * 8 + i];
-          if (row < M && n < N) {
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = 0.f;
+          for (int p = 0; p < sk.S; ++p) {
+            float w[8];
+            load8<float>(wsp + (int64_t)p * CG * 128 * C::TILE_N + woff, w);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] += w[i];
+          }
+        }
+        if (row < M && n < N) {
+          if (mode == 1) {
+            store8<float>(wsp + woff, v);
+          } else {
             epi_apply8<bf16>(epi, row, n + epi.n_off, v, aux[it]);
             if (has_dbias)
 #pragma unroll
               for (int i = 0; i < 8; ++i) cs[i] += v[i];
           }
         }
-        if (has_dbias) {  // the 8 lanes holding the same 8 columns (lane bits 2-4) reduce the warp's 32 rows
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 4);
-            cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 8);
-            cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 16);
-          }
-          if (lane < 4 && n < N) {
-            float* d = epi.dbias + n + epi.n_off;
-            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d), "f"(cs[0]), "f"(cs[1]), "f"(cs[2]),
-                         "f"(cs[3]) : "memory");
-            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d + 4), "f"(cs[4]), "f"(cs[5]),
-                         "f"(cs[6]), "f"(cs[7]) : "memory");
-          }
-        }
-        __syncwarp();
       }
+      if (mode != 1 && has_dbias) {  // the 8 lanes holding the same 8 columns (lane bits 2-4) reduce the warp's 32 rows
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 4);
+          cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 8);
+          cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 16);
+        }
+        if (lane < 4 && n < N) {
+          float* d = epi.dbias + n + epi.n_off;
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d), "f"(cs[0]), "f"(cs[1]), "f"(cs[2]),
+                       "f"(cs[3]) : "memory");
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d + 4), "f"(cs[4]), "f"(cs[5]),
+                       "f"(cs[6]), "f"(cs[7]) : "memory");
+        }
+      }
+      __syncwarp();
+    };
+    int tile, k0, k1, part;
+    for (int item = 0; gemm_item(item, unit, nunits, tiles, kbs, sk, tile, k0, k1, part); ++item) {
+      const int m0 = (tile % m_tiles) * C::TILE_M + crank * BM, n0 = (tile / m_tiles) * C::TILE_N;
+      mbar_wait(tfull + acc, acc_phase);
+      tc_fence_after();
+      float* wst = part < 0 ? nullptr : sk.ws + ((int64_t)(tile - sk.dp_tiles) * sk.S * CG + crank) * 128 * C::TILE_N;
+#pragma unroll 1
+      for (int ch = ch0; ch < ch1; ++ch)
+        chunk(ch, part < 0 ? 0 : 1, m0, n0, part < 0 ? nullptr : wst + (int64_t)part * CG * 128 * C::TILE_N);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -260,6 +312,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         else mbar_arrive_cluster(tempty_leader + acc * 8);
       }
       if (++acc == C::NACC) { acc = 0; acc_phase ^= 1; }
+      if (part >= 0) {
+        // stream-K: the last of the S parts (per tile and CTA) reduces the partials and runs the epilogue
+        __threadfence();
+        named_bar(1, 256);
+        int* cnt = sk.cnt + (tile - sk.dp_tiles) * CG + crank;
+        if (threadIdx.x == 64) *sk_ticket = atomicAdd(cnt, 1);
+        named_bar(1, 256);
+        if (*sk_ticket == sk.S - 1) {
+          __threadfence();
+#pragma unroll 1
+          for (int ch = ch0; ch < ch1; ++ch) chunk(ch, 2, m0, n0, wst);
+          if (threadIdx.x == 64) *cnt = 0;
+        }
+        named_bar(1, 256);  // nobody overwrites sk_ticket before every thread has read it
+      }
     }
   }
   tc_fence_before();
@@ -278,6 +345,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 int g_force_cg = 0;  // test hook: TP_GEMM_CG=1|2 forces the CTA-group size
+// Stream-K tail (TP_GEMM_STREAMK=1, read per launch): correct and tested, but measured neutral on
+// the hot path's partial-wave shapes (scripts/bench_kernels.py), so off by default.
+int g_stream_k = 0;
+// stream-K workspace (grow-only, one GEMM at a time uses it: all persistent GEMMs of a context run on
+// its main stream)
+float* g_sk_ws = nullptr;
+int* g_sk_cnt = nullptr;
+size_t g_sk_ws_n = 0, g_sk_cnt_n = 0;
 int g_num_sms = 0;
 std::once_flag g_once;
 
@@ -291,6 +366,7 @@ void init_once() {
     int dev = 0;
     cudaGetDevice(&dev);
     if (const char* e = getenv("TP_GEMM_CG")) g_force_cg = atoi(e);
+
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   });
 }
@@ -323,7 +399,45 @@ cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   ok = ok && (B_MN ? make_map(&tb, g.B, g.N, g.K, g.ldb, 64, 64) : make_map(&tb, g.B, g.K, g.N, g.ldb, 64, BN / CG));
   if (!ok) return cudaErrorInvalidValue;
   const int tiles = ((g.M + C::TILE_M - 1) / C::TILE_M) * ((g.N + C::TILE_N - 1) / C::TILE_N);
-  const int units = g.persistent ? std::min(tiles, g_num_sms / CG) : tiles;
+  int units = g.persistent ? std::min(tiles, g_num_sms / CG) : tiles;
+  SplitK sk;
+  sk.dp_tiles = tiles;
+  const int kbs = (g.K + BK - 1) / BK;
+  {
+    const char* e = getenv("TP_GEMM_STREAMK");
+    g_stream_k = e ? atoi(e) : 0;
+  }
+  if (g.persistent && WN == 1 && g_stream_k) {
+    const int full_units = g_num_sms / CG;
+    const int tail = tiles % full_units;
+    const int S = tail > 0 ? std::min(4, full_units / tail) : 1;
+    if (S >= 2 && kbs >= 2 * S) {
+      const size_t ws_need = (size_t)tail * S * CG * 128 * C::TILE_N, cnt_need = (size_t)tail * CG;
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(st, &cap);
+      if (ws_need > g_sk_ws_n || cnt_need > g_sk_cnt_n) {
+        if (cap == cudaStreamCaptureStatusNone) {  // grow (never inside a graph capture)
+          cudaStreamSynchronize(st);
+          if (g_sk_ws) cudaFree(g_sk_ws);
+          if (g_sk_cnt) cudaFree(g_sk_cnt);
+          g_sk_ws = nullptr; g_sk_cnt = nullptr; g_sk_ws_n = g_sk_cnt_n = 0;
+          if (cudaMalloc(&g_sk_ws, ws_need * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&g_sk_cnt, cnt_need * sizeof(int)) == cudaSuccess &&
+              cudaMemset(g_sk_cnt, 0, cnt_need * sizeof(int)) == cudaSuccess) {
+            g_sk_ws_n = ws_need;
+            g_sk_cnt_n = cnt_need;
+          }
+        }
+      }
+      if (ws_need <= g_sk_ws_n && cnt_need <= g_sk_cnt_n) {
+        sk.dp_tiles = tiles - tail;
+        sk.S = S;
+        sk.ws = g_sk_ws;
+        sk.cnt = g_sk_cnt;
+        units = full_units;
+      }
+    }
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * CG);
   cfg.blockDim = dim3(GEMM_THREADS);
@@ -336,7 +450,7 @@ cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ta, tb, g.M, g.N, g.K, e);
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, g.M, g.N, g.K, e, sk);
 }
 
 template <int CG, int BN, int WN = 1>
@@ -444,7 +558,8 @@ cudaError_t gemm_sm100(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   // whole waves with it and the remaining columns as a second launch with half-width tiles (twice
   // the tiles, half the time each), if the model says that is cheaper: the partial wave then costs
   // half a wave. The second launch sees its columns through Epi::n_off.
-  if (g.persistent && !g_force_cg && (best == 0 || best == 2)) {
+  const bool sk_on = getenv("TP_GEMM_STREAMK") && atoi(getenv("TP_GEMM_STREAMK")) != 0;
+  if (!sk_on && g.persistent && !g_force_cg && (best == 0 || best == 2)) {  // stream-K supersedes this
     const Cand& c = cands[best];
     const Cand& h = cands[best + 1];  // same CTA group, BN / 2
     const long units = g_num_sms / c.cg;

@@ -76,7 +76,12 @@ if __name__ == "__main__":
                                        (512, 15360, 5120, 0, 0, "13b qkv fwd l=512"),
                                        (512, 5120, 20480, 0, 0, "13b fc2 fwd l=512"),
                                        (5120, 15360, 2048, 1, 1, "13b qkv dW"),
-                                       (256, 20480, 5120, 0, 0, "13b fc1 l=256"), (8192, 8192, 8192, 0, 0, "square")]:
+                                       (256, 20480, 5120, 0, 0, "13b fc1 l=256"), (8192, 8192, 8192, 0, 0, "square"),
+                                       # partial last waves (stream-K tail / tail split)
+                                       (8192, H, H, 0, 0, "1b o-proj b=4 (3.46 waves)"),
+                                       (8192, H, 4 * H, 0, 0, "1b fc2 b=4 (3.46 waves)"),
+                                       (768, 15360, 5120, 0, 0, "13b qkv b=2 l=384 (2.43 waves)"),
+                                       (1536, 5120, 20480, 0, 0, "13b fc2 b=2 l=768 (1.62 waves)")]:
             gemm(M, N, K, am, bm, 0, tag)
     if args.which in ("all", "attn"):
         for (a, s, d, c, l, tag) in [(16, 2048, 128, 0, 2048, "1b full"), (40, 2048, 128, 1536, 512, "13b last slice"),
