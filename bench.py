@@ -1,10 +1,11 @@
 #!/usr/bin/env python
 """bench.py — one JSON line for the driver.
 
-A step = one synchronous tp_step: token-sliced, pipelined forward+backward of one batch of a GPT-3
-shaped model (BASELINE.json:5, metric BASELINE.json:2) with the slicing chosen by tp_plan from a
-cost table that tp_profile measured on this box (the max over stages, A-16). The unsliced GPipe
-schedule [(1, [s])] * B on the same kernels is timed beside it.
+A step = one synchronous tp_step_plan: token-sliced, pipelined forward+backward of one batch of a
+GPT-3 shaped model (BASELINE.json:5, metric BASELINE.json:2) with the batch x token plan chosen by
+tp_plan_joint from the cost tables tp_profile measured on this box for every batch-slice size b
+(the max over stages, A-16, A-20b). The unsliced GPipe schedule [(b, [s])] * B/b
+(best predicted b) on the same kernels is timed beside it.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config gpt3-1b] [--impl reference]
 
