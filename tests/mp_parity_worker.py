@@ -18,11 +18,15 @@ from tests.gpu_util import rel
 
 
 def main():
+    # lengths: "l1,l2,.." (uniform slicing, b = 1) or a batch plan "b:l1,l2;b:l1,.." (tp_step_plan);
+    # optional argv[5]: batch size override
     cfg_name, precision, lengths, out_dir = sys.argv[1], sys.argv[2], sys.argv[3], sys.argv[4]
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     base, B = CONFIGS[cfg_name]
+    if len(sys.argv) > 5:
+        B = int(sys.argv[5])
     cfg = base.with_(n_stages=world)
     prec = tp.TP_BF16 if precision == "bf16" else tp.TP_FP32
     params = make_params(cfg, seed=11, bf16=(prec == tp.TP_BF16))
@@ -31,8 +35,13 @@ def main():
     ctx = tp.Context(cfg, rank=rank, world=world, nccl_id=nid, precision=prec, max_batch=B, device=local,
                      flags=tp.TP_FLAG_KEEP_LOGITS if rank == world - 1 else 0)
     ctx.load_params(pack_stage(params, cfg, rank))
-    sl = tp.Slicing([int(x) for x in lengths.split(",")])
-    losses = [ctx.step(sl, tokens) for _ in range(2)]          # twice: grads are re-zeroed per step
+    if ":" in lengths:
+        plan = tp.BatchPlan([(int(g.split(":")[0]), [int(x) for x in g.split(":")[1].split(",")])
+                             for g in lengths.split(";")])
+        losses = [ctx.step_plan(plan, tokens) for _ in range(2)]  # twice: grads are re-zeroed per step
+    else:
+        sl = tp.Slicing([int(x) for x in lengths.split(",")])
+        losses = [ctx.step(sl, tokens) for _ in range(2)]          # twice: grads are re-zeroed per step
     grads = unpack_stage(ctx.grads(), cfg, rank)
     ref = gpt_forward_backward(params, tokens, cfg.n_layer, cfg.n_head)
     errs = {k: rel(v, ref["grads"][k]) for k, v in grads.items()}

@@ -12,12 +12,12 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def run(world, cfg, precision, lengths, tmp_path, env=None):
+def run(world, cfg, precision, lengths, tmp_path, env=None, batch=None):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29531", os.path.join(ROOT, "tests", "mp_parity_worker.py"),
-           cfg, precision, lengths, str(tmp_path)]
+           cfg, precision, lengths, str(tmp_path)] + ([str(batch)] if batch else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env={**os.environ, **(env or {})})
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return [json.load(open(tmp_path / f"rank{k}.json")) for k in range(world)]
@@ -38,4 +38,11 @@ def test_small_two_stages_nccl_side_stream_dw(tmp_path):
 
 def test_small_four_stages_nccl(tmp_path):
     for errs in run(4, "small", "bf16", "40,24,64", tmp_path):
+        assert max(errs.values()) < 2e-2, errs
+
+
+def test_small_two_stages_heterogeneous_batch_plan(tmp_path):
+    """tp_step_plan over NCCL: groups of different batch-slice sizes with their own slicings (jobs
+    of different row counts and message sizes on the p2p edges)."""
+    for errs in run(2, "small", "bf16", "2:40,24,64;1:128", tmp_path, batch=3):
         assert max(errs.values()) < 2e-2, errs
