@@ -345,9 +345,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 int g_force_cg = 0;  // test hook: TP_GEMM_CG=1|2 forces the CTA-group size
-// Stream-K tail (TP_GEMM_STREAMK=1, read per launch): correct and tested, but measured neutral on
-// the hot path's partial-wave shapes (scripts/bench_kernels.py), so off by default.
-int g_stream_k = 0;
+// Stream-K tail (TP_GEMM_STREAMK=0 disables, read per launch): ~2 % on the 13B 4-stage pipeline
+// step (its slice GEMMs leave partial waves), neutral at N = 1.
+int g_stream_k = 1;
 // stream-K workspace (grow-only, one GEMM at a time uses it: all persistent GEMMs of a context run on
 // its main stream)
 float* g_sk_ws = nullptr;
@@ -405,7 +405,7 @@ cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   const int kbs = (g.K + BK - 1) / BK;
   {
     const char* e = getenv("TP_GEMM_STREAMK");
-    g_stream_k = e ? atoi(e) : 0;
+    g_stream_k = e ? atoi(e) : 1;
   }
   if (g.persistent && WN == 1 && g_stream_k) {
     const int full_units = g_num_sms / CG;
@@ -558,7 +558,7 @@ cudaError_t gemm_sm100(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   // whole waves with it and the remaining columns as a second launch with half-width tiles (twice
   // the tiles, half the time each), if the model says that is cheaper: the partial wave then costs
   // half a wave. The second launch sees its columns through Epi::n_off.
-  const bool sk_on = getenv("TP_GEMM_STREAMK") && atoi(getenv("TP_GEMM_STREAMK")) != 0;
+  const bool sk_on = !getenv("TP_GEMM_STREAMK") || atoi(getenv("TP_GEMM_STREAMK")) != 0;
   if (!sk_on && g.persistent && !g_force_cg && (best == 0 || best == 2)) {  // stream-K supersedes this
     const Cand& c = cands[best];
     const Cand& h = cands[best + 1];  // same CTA group, BN / 2
