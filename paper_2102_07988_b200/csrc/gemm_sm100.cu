@@ -410,8 +410,10 @@ cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   if (g.persistent && WN == 1 && g_stream_k) {
     const int full_units = g_num_sms / CG;
     const int tail = tiles % full_units;
-    const int S = tail > 0 ? std::min(4, full_units / tail) : 1;
-    if (S >= 2 && kbs >= 2 * S) {
+    // each part must keep >= 32 k-blocks of MMA work to amortise its fp32 partial write and the
+    // last part's S-way read (e.g. K = 2048 -> no split, K = 5120 -> S <= 2)
+    const int S = tail > 0 ? std::min(std::min(4, full_units / tail), kbs / 32) : 1;
+    if (S >= 2) {
       const size_t ws_need = (size_t)tail * S * CG * 128 * C::TILE_N, cnt_need = (size_t)tail * CG;
       cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
       cudaStreamIsCapturing(st, &cap);
