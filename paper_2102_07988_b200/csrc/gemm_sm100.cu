@@ -560,8 +560,10 @@ cudaError_t gemm_sm100(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   // whole waves with it and the remaining columns as a second launch with half-width tiles (twice
   // the tiles, half the time each), if the model says that is cheaper: the partial wave then costs
   // half a wave. The second launch sees its columns through Epi::n_off.
-  const bool sk_on = !getenv("TP_GEMM_STREAMK") || atoi(getenv("TP_GEMM_STREAMK")) != 0;
-  if (!sk_on && g.persistent && !g_force_cg && (best == 0 || best == 2)) {  // stream-K supersedes this
+  // stream-K (launch_bn) supersedes this split where it can apply: K long enough for >= 2 parts of
+  // >= 32 k-blocks each
+  const bool sk_on = (!getenv("TP_GEMM_STREAMK") || atoi(getenv("TP_GEMM_STREAMK")) != 0) && (g.K + BK - 1) / BK >= 64;
+  if (!sk_on && g.persistent && !g_force_cg && (best == 0 || best == 2)) {
     const Cand& c = cands[best];
     const Cand& h = cands[best + 1];  // same CTA group, BN / 2
     const long units = g_num_sms / c.cg;
