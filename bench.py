@@ -159,6 +159,7 @@ def main():
     ap.add_argument("--granularity", type=int, default=64)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-gpipe", action="store_true")
+    ap.add_argument("--profile-reps", type=int, default=7, help="tp_profile repetitions per (l, c) point (median)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slicing", default="dp", help="dp | gpipe | comma-separated lengths")
     ap.add_argument("--batch-slices", default="auto", help="auto | comma-separated batch-slice sizes b to plan over")
@@ -234,7 +235,7 @@ def main():
         t0 = time.time()
         tables = {}
         for b in bsl:
-            ticks, f = ctx.profile(g, reps=5, batch_slice=b)
+            ticks, f = ctx.profile(g, reps=args.profile_reps, batch_slice=b)
             if world > 1:
                 ticks = tdist.bottleneck_table(ticks)
             tables[b] = ticks
