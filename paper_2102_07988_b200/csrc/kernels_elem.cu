@@ -231,6 +231,95 @@ __global__ void __launch_bounds__(NT) ln_bwd_kernel(const T* __restrict__ dy, co
   }
 }
 
+// Wide rows (H > 2048, e.g. 13B / 175B): the same math with more threads per row and the dgamma /
+// dbeta / dbias partial sums in shared memory (thread t owns its columns' slots, no conflicts) instead
+// of registers, and no prefetch buffers, so the CTA keeps <= 64-80 registers per thread and 16-24
+// warps per SM are in flight (the register-resident version spilled or ran one 8-warp CTA per SM).
+template <typename T, int NT, int NCH>
+__global__ void __launch_bounds__(NT, 1) ln_bwd_wide_kernel(const T* __restrict__ dy, const float* __restrict__ x,
+                                                            const float* __restrict__ mean_in,
+                                                            const float* __restrict__ rstd_in,
+                                                            const float* __restrict__ gam, const float* __restrict__ resid,
+                                                            float* __restrict__ dx_out, T* __restrict__ dx_copy,
+                                                            float* __restrict__ dgam, float* __restrict__ dbet,
+                                                            float* __restrict__ dbias, int rows, int H, int rpb) {
+  extern __shared__ float acc_s[];  // [3][NCH * NT * 8]: dgamma, dbeta, dbias partials
+  __shared__ float red[2][2][NT / 32];
+  const int tid = threadIdx.x;
+  constexpr int W = NCH * NT * 8;
+  for (int i = tid; i < 3 * W; i += NT) acc_s[i] = 0.f;
+  __syncthreads();
+  const int r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
+  for (int r = r0; r < r1; ++r) {
+    const float mean = mean_in[r], rstd = rstd_in[r];
+    float d[NCH][8], xh[NCH][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const int col = (c * NT + tid) * 8;
+      if (col < H) {
+        float g[8];
+        load8<T>(dy + (int64_t)r * H + col, d[c]);
+        load8<float>(x + (int64_t)r * H + col, xh[c]);
+        load8<float>(gam + col, g);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          xh[c][i] = (xh[c][i] - mean) * rstd;
+          const float dxh = d[c][i] * g[i];
+          s1 += dxh;
+          s2 += dxh * xh[c][i];
+          acc_s[col + i] += d[c][i] * xh[c][i];
+          acc_s[W + col + i] += d[c][i];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { d[c][i] = 0.f; xh[c][i] = 0.f; }
+      }
+    }
+    float (*rd)[NT / 32] = red[r & 1];
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if ((tid & 31) == 0) { rd[0][tid >> 5] = s1; rd[1][tid >> 5] = s2; }
+    __syncthreads();
+    float m1 = 0.f, m2 = 0.f;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) { m1 += rd[0][w]; m2 += rd[1][w]; }
+    m1 /= H;
+    m2 /= H;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const int col = (c * NT + tid) * 8;
+      if (col < H) {
+        float g[8], o[8], rs[8];
+        load8<float>(gam + col, g);
+        if (resid) load8<float>(resid + (int64_t)r * H + col, rs);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          o[i] = rstd * (d[c][i] * g[i] - m1 - xh[c][i] * m2) + (resid ? rs[i] : 0.f);
+          acc_s[2 * W + col + i] += o[i];
+        }
+        store8<float>(dx_out + (int64_t)r * H + col, o);
+        if (dx_copy) store8<T>(dx_copy + (int64_t)r * H + col, o);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int col = (c * NT + tid) * 8;
+    if (col < H) {
+      const float* a = acc_s + col;
+      red_add4(dgam + col, a[0], a[1], a[2], a[3]);
+      red_add4(dgam + col + 4, a[4], a[5], a[6], a[7]);
+      red_add4(dbet + col, a[W], a[W + 1], a[W + 2], a[W + 3]);
+      red_add4(dbet + col + 4, a[W + 4], a[W + 5], a[W + 6], a[W + 7]);
+      if (dbias) {
+        red_add4(dbias + col, a[2 * W], a[2 * W + 1], a[2 * W + 2], a[2 * W + 3]);
+        red_add4(dbias + col + 4, a[2 * W + 4], a[2 * W + 5], a[2 * W + 6], a[2 * W + 7]);
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- embedding
 __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const float* __restrict__ wte,
                                  const float* __restrict__ wpe, float* __restrict__ h, int c, int b, int s, int H,
@@ -445,12 +534,26 @@ cudaError_t layernorm_bwd(const T* dy, const float* x, const float* mean, const 
   const int grid = (rows + rpb - 1) / rpb;
   (void)ws;
 #define LNB(NT, NCH) ln_bwd_kernel<T, NT, NCH><<<grid, NT, 0, st>>>(dy, x, mean, rstd, gam, resid, dx_out, dx_copy, dgam, dbet, dbias, rows, H, rpb)
+#define LNBW(NT, NCH)                                                                                     \
+  do {                                                                                                    \
+    const int smem = 3 * NCH * NT * 8 * (int)sizeof(float);                                               \
+    static bool attr = false;                                                                             \
+    if (!attr) {                                                                                          \
+      cudaError_t e = cudaFuncSetAttribute(ln_bwd_wide_kernel<T, NT, NCH>,                                \
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);            \
+      if (e != cudaSuccess) return e;                                                                     \
+      attr = true;                                                                                        \
+    }                                                                                                     \
+    ln_bwd_wide_kernel<T, NT, NCH><<<grid, NT, smem, st>>>(dy, x, mean, rstd, gam, resid, dx_out, dx_copy, \
+                                                          dgam, dbet, dbias, rows, H, rpb);               \
+  } while (0)
   if (H <= 2048) LNB(256, 1);
-  else if (H <= 4096) LNB(256, 2);
-  else if (H <= 6144) LNB(256, 3);
-  else if (H <= 12288) LNB(512, 3);
+  else if (H <= 4096) LNBW(512, 1);
+  else if (H <= 6144) LNBW(768, 1);
+  else if (H <= 12288) LNBW(768, 2);
   else return cudaErrorInvalidValue;
 #undef LNB
+#undef LNBW
   return cudaGetLastError();
 }
 cudaError_t embed_fwd(const int32_t* tok, const float* wte, const float* wpe, float* h, int c, int l, int b, int s,

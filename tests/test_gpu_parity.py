@@ -78,6 +78,15 @@ def test_parity_mid_13b_width():
     check(worst_errors(loss, logits, grads, ref), 2e-2)
 
 
+def test_wide_hidden_175b_width():
+    """GPT-3 175B width (H = 12288, 96 heads of 128) on one layer: the wide-row LayerNorm backward
+    (768 threads x 2 chunks, shared-memory gradient partials) and the GEMMs at that width."""
+    cfg = ModelCfg(1, 12288, 96, 256, 64, 1)
+    params, tokens, ref = oracle_run(cfg, 1, 17, True)
+    loss, logits, grads, _ = gpu_run(cfg, 1, params, tokens, [40, 24], tp.TP_BF16)
+    check(worst_errors(loss, logits, grads, ref), 2e-2)
+
+
 def test_parity_mid_batch2_tail_split():
     """13B width, b = 2 unsliced: 1024-row GEMMs whose partial last wave is split into a second
     half-width-tile launch (QKV scatter, GeLU, residual and dX epilogues through Epi::n_off)."""
