@@ -35,7 +35,7 @@ def load(path):
 def cls(i, k, last_ce):
     n = k["name"]
     if "gemm_sm100" in n:
-        if re.search(r"1, 1>|true, true", n):
+        if re.search(r"<\d+, \d+, (1|true), (1|true)\b", n):
             return "gemm_dw"
         return "gemm_fwd" if i < last_ce else "gemm_dx"
     if "attn_fwd" in n:
