@@ -36,6 +36,14 @@ def test_small_two_stages_nccl_side_stream_dw(tmp_path):
         assert max(errs.values()) < 2e-2, errs
 
 
+@pytest.mark.parametrize("g", ["1", "2"])
+def test_small_two_stages_group_dw(g, tmp_path):
+    """TP_GROUP_DW=g: the first stage computes the weight gradients of every run of g finished groups
+    in order (three groups of different b: flushes of one or two groups, then the rest at the end)."""
+    for errs in run(2, "small", "bf16", "1:40,24,64;1:128;2:64,64", tmp_path, batch=4, env={"TP_GROUP_DW": g}):
+        assert max(errs.values()) < 2e-2, errs
+
+
 def test_small_four_stages_nccl(tmp_path):
     for errs in run(4, "small", "bf16", "40,24,64", tmp_path):
         assert max(errs.values()) < 2e-2, errs
