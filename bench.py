@@ -345,8 +345,10 @@ def main():
     if rank == 0:
         line["roofline"] = roofline(kstats, ms_instr, args.steps, peak_sust, hbm, peak_kind)
         line["kernel_classes"] = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
-                                      "tflops": (v["flops"] / (v["ms"] * 1e9)) if v["ms"] > 0 and v["flops"] > 0 else None}
+                                      "tflops": (v["flops"] / (v["ms"] * 1e9)) if v["ms"] > 0 and v["flops"] > 0 else None,
+                                      "gbs": (v["bytes"] / (v["ms"] * 1e6)) if v["ms"] > 0 and v["bytes"] > 0 else None}
                                   for k, v in kstats.items() if v["launches"]}
+        line["roofline_hbm"] = roofline_hbm(kstats, ms_instr, args.steps, hbm, peak_kind)
         line["ms_per_step_instrumented"] = ms_instr
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_oracle_sample(cfg, B)
@@ -381,6 +383,23 @@ def roofline(kstats, ms_step, steps, peak_tflops, hbm_gbs, peak_kind):
     ach = v["bytes"] / v["launches"] / (per_launch_ms * 1e-3) / 1e9
     return {"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm_gbs, "unit": "GB/s", "frac": ach / hbm_gbs,
             "traffic": traffic, "peak_kind": peak_kind, "share_of_step": v["ms"] / steps / ms_step}
+
+
+def roofline_hbm(kstats, ms_step, steps, hbm_gbs, peak_kind):
+    """The HBM-bound kernel classes (no FLOPs counted: LayerNorm fwd/bwd, embedding, cross-entropy,
+    the dK/dV finalise / dQ convert / column-sum passes in "misc"): ALGORITHMIC bytes per launch (the
+    per-unit figures of DESIGN.md §6 x the tokens of one job) / mean CUDA-event launch duration,
+    against the measured HBM copy bandwidth. The dominant one (largest summed time) leads."""
+    live = {k: v for k, v in kstats.items() if v["launches"] and v["ms"] > 0 and v["bytes"] > 0 and v["flops"] == 0}
+    if not live:
+        return None
+    out = []
+    for name, v in sorted(live.items(), key=lambda kv: -kv[1]["ms"]):
+        ach = v["bytes"] / (v["ms"] * 1e-3) / 1e9
+        out.append({"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm_gbs, "unit": "GB/s",
+                    "frac": ach / hbm_gbs, "peak_kind": peak_kind, "share_of_step": v["ms"] / steps / ms_step,
+                    "launches_per_step": v["launches"] / steps, "bytes_per_launch": v["bytes"] / v["launches"]})
+    return out
 
 
 if __name__ == "__main__":
