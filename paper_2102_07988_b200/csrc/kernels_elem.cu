@@ -533,7 +533,8 @@ cudaError_t layernorm_bwd(const T* dy, const float* x, const float* mean, const 
   // Row groups sized for `ctas` CTAs per SM. The 112-register H <= 2048 kernel keeps 2 CTAs of 256
   // threads resident per SM, so 2 x 148 groups run as one wave (measured: LayerNorm class 10.2 -> 9.6
   // ms per step vs 4 x 148; an 80-register 3-CTA variant spilled and was slower). The wide kernels
-  // keep 4 x 148. TP_LNB_CTAS overrides (A/B knob, scripts/ln_ab.sh).
+  // keep 4 x 148 (at H = 5120, 4 vs 2 per SM measured within noise, profiles/r01_lnb_ab_13b_n4.txt).
+  // TP_LNB_CTAS overrides (A/B knob, scripts/ln_ab.sh, scripts/ln_ab_13b.sh).
   static const int ctas_env = getenv("TP_LNB_CTAS") ? std::max(1, atoi(getenv("TP_LNB_CTAS"))) : 0;
   const int ctas = ctas_env ? ctas_env : (H <= 2048 ? 2 : 4);
   const int rpb = std::max(4, (rows + ctas * 148 - 1) / (ctas * 148));
