@@ -58,7 +58,12 @@ enum { TP_BF16 = 0, /* bf16 GEMM/attention operands, fp32 accumulation, fp32 res
 
 enum { TP_FLAG_KEEP_LOGITS = 1,   /* keep fp32 logits of the last step for tp_get_logits     */
        TP_FLAG_KERNEL_STATS = 2,  /* bracket launches with CUDA events (tp_kernel_stats)      */
-       TP_FLAG_FORCE_SIMT = 4     /* bf16 mode: use SIMT GEMM/attention (kernel cross-checks)  */ };
+       TP_FLAG_FORCE_SIMT = 4,    /* bf16 mode: use SIMT GEMM/attention (kernel cross-checks)  */
+       TP_FLAG_NCCL_LOOPBACK = 8  /* world == 1, n_stages > 1: send every stage message through
+                                     ncclSend/ncclRecv to self on a one-rank communicator (grouped
+                                     per message, on the same per-direction comm streams, NCCL
+                                     communicators and events as world == n_stages) instead of
+                                     aliasing the buffers; lets the p2p path run on one GPU        */ };
 
 /* Model shape. n_layer % n_stages == 0; hidden % n_head == 0; head_dim = hidden / n_head must be
  * a multiple of 16 and <= 128; hidden % 64 == 0; seq_len >= 1. */
@@ -149,8 +154,9 @@ typedef struct tp_ctx tp_ctx;
 tp_status tp_nccl_unique_id(void* out128);
 
 /* Creates a context on CUDA device `device`.
- *  world == 1: this context owns ALL cfg->n_stages stages on one GPU ("loopback": stage messages
- *              are device copies; no NCCL; nccl_id may be NULL).
+ *  world == 1: this context owns ALL cfg->n_stages stages on one GPU ("loopback": stage k's input
+ *              buffer is stage k-1's output buffer, no copy and no NCCL; with TP_FLAG_NCCL_LOOPBACK
+ *              every message is an NCCL send/recv to self instead; nccl_id may be NULL).
  *  world == cfg->n_stages > 1: this context owns stage `rank`; neighbours exchange slice
  *              activations / gradients with ncclSend/ncclRecv over NVLink.
  * precision: TP_BF16 or TP_FP32. max_batch: largest `batch` tp_step will be called with (sizes the
@@ -170,12 +176,15 @@ tp_status tp_load_params(tp_ctx* ctx, const float* host_params, size_t n);
  * entry, every stage runs F(d,i) for d = 0..B-1, i = 1..M, then B(d,i) in exact reverse order
  * (GPipe order, store-all, A-21); weight gradients are accumulated per sequence.
  * tokens: HOST int32 [batch][seq_len+1] (input = [:, :s], target = [:, 1:], A-8); read by the
- * first and last stage. loss_out (may be NULL): mean cross-entropy over batch*seq_len targets,
- * identical on every rank. Returns after all local device work has completed. */
+ * first and last stage; every id must lie in [0, vocab): an id outside it is rejected with
+ * TP_EINVAL before any device work (never clamped). loss_out (may be NULL): mean cross-entropy over
+ * batch*seq_len targets, identical on every rank. Returns after all local device work has completed. */
 tp_status tp_step(tp_ctx* ctx, const tp_slicing* slicing, const int32_t* tokens, int32_t batch,
                   float* loss_out);
 
-/* Same as tp_step with DEVICE tokens (already resident in HBM on this context's device). */
+/* Same as tp_step with DEVICE tokens (already resident in HBM on this context's device). Ids outside
+ * [0, vocab) are counted on the device (the kernels never read or scatter out of range with them)
+ * and the call returns TP_EINVAL after the step; its loss, logits and gradients are then invalid. */
 tp_status tp_step_device(tp_ctx* ctx, const tp_slicing* slicing, const int32_t* dev_tokens,
                          int32_t batch, float* loss_out);
 

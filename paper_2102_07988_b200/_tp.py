@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libtp.so")
 
 TP_OK, TP_EINVAL, TP_EINFEASIBLE, TP_ETOOBIG, TP_ECUDA, TP_ENCCL, TP_ENOMEM, TP_ESTATE = 0, -1, -2, -3, -4, -5, -6, -7
 TP_BF16, TP_FP32 = 0, 1
-TP_FLAG_KEEP_LOGITS, TP_FLAG_KERNEL_STATS, TP_FLAG_FORCE_SIMT = 1, 2, 4
+TP_FLAG_KEEP_LOGITS, TP_FLAG_KERNEL_STATS, TP_FLAG_FORCE_SIMT, TP_FLAG_NCCL_LOOPBACK = 1, 2, 4, 8
 
 EXPORTED = ["tp_plan", "tp_plan_joint", "tp_step_plan", "tp_step_plan_device", "tp_stage_param_count", "tp_nccl_unique_id", "tp_init", "tp_param_count",
             "tp_load_params", "tp_step", "tp_step_device", "tp_get_grads", "tp_get_logits",
@@ -260,8 +260,14 @@ class Context:
         a = np.ascontiguousarray(flat, dtype=np.float32)
         _check(_lib.tp_load_params(self._h, a.ctypes.data, a.size))
 
-    def step(self, slicing: Slicing, tokens: np.ndarray) -> float:
+    def _tokens(self, tokens: np.ndarray) -> np.ndarray:
         tok = np.ascontiguousarray(tokens, dtype=np.int32)
+        if tok.ndim != 2 or tok.shape[1] != self.cfg.seq_len + 1:
+            raise TpError(TP_EINVAL, f"tokens shape {tok.shape} != (batch, seq_len + 1 = {self.cfg.seq_len + 1})")
+        return tok
+
+    def step(self, slicing: Slicing, tokens: np.ndarray) -> float:
+        tok = self._tokens(tokens)
         loss = C.c_float()
         _check(_lib.tp_step(self._h, C.byref(slicing.c), tok.ctypes.data, tok.shape[0], C.byref(loss)))
         return loss.value
@@ -272,7 +278,7 @@ class Context:
         return loss.value
 
     def step_plan(self, plan: BatchPlan, tokens: np.ndarray) -> float:
-        tok = np.ascontiguousarray(tokens, dtype=np.int32)
+        tok = self._tokens(tokens)
         loss = C.c_float()
         _check(_lib.tp_step_plan(self._h, C.byref(plan.c), tok.ctypes.data, tok.shape[0], C.byref(loss)))
         return loss.value

@@ -204,7 +204,9 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int head = blockIdx.x, sq = blockIdx.y, r0 = (gridDim.z - 1 - blockIdx.z) * 2 * AT;
+  // raster: the query-tile pairs of one (head, sequence) are consecutive CTAs (heaviest first), so
+  // they run concurrently and read that head's K / V blocks from L2 instead of DRAM
+  const int head = blockIdx.y, sq = blockIdx.z, r0 = (gridDim.x - 1 - blockIdx.x) * 2 * AT;
   o += sq * o_sstride;
   lse += sq * lse_sstride;
   // key blocks of each tile: tile t covers rows [r0 + t*128, +128) of the slice (absolute c + ...)
@@ -498,8 +500,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // heaviest key blocks (the most query tiles) first: blockIdx.y is the key block
-  const int head = blockIdx.x % nheads, sq = blockIdx.x / nheads, key0 = blockIdx.y * AT;
+  // raster: the key blocks of one (sequence, head) are consecutive CTAs (heaviest, key block 0,
+  // first), so they run concurrently: that head's Q / dO tiles are read from DRAM once and shared
+  // through L2, and the fp32 dQ reduce-adds of all its key blocks meet in L2
+  const int head = blockIdx.y % nheads, sq = blockIdx.y / nheads, key0 = blockIdx.x * AT;
   ldg += ((int64_t)sq * nheads + head) * ((l + BQB - 1) / BQB) * (2 * BQB);
   const int qt0 = max(0, key0 - c) / BQB, nqt = (l + BQB - 1) / BQB;
   const int ntile = nqt - qt0;  // >= 1 because key0 < c + l
@@ -868,7 +872,7 @@ cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o,
       if (e != cudaSuccess) return e;
       attr2 = true;
     }
-    dim3 grid2(a, nseq, (l + 2 * AT - 1) / (2 * AT));
+    dim3 grid2((l + 2 * AT - 1) / (2 * AT), a, nseq);
     static int trace2_left = getenv("TP_ATTN_TRACE") ? atoi(getenv("TP_ATTN_TRACE")) : 0;
     static long long* trace2 = nullptr;
     if (trace2_left > 0 && !trace2) cudaMalloc(&trace2, 4 * 8 * 64 * sizeof(long long));
@@ -941,7 +945,7 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
   if (!encode_f32_map_sw128(&mdk, dk_acc, 4, adims, astr, abox) || !encode_f32_map_sw128(&mdv, dv_acc, 4, adims, astr, abox))
     return cudaErrorInvalidValue;
   const float scale = rsqrtf((float)d);
-  dim3 grid(a * nseq, (c + l + AT - 1) / AT);
+  dim3 grid((c + l + AT - 1) / AT, a * nseq);
   static int* dbg = nullptr;
   static bool dbg_on = getenv("TP_ATTN_DEBUG") != nullptr;
   if (dbg_on && !dbg) {

@@ -9,7 +9,8 @@
 //
 // Design (sm_100a):
 //   * persistent CTAs (grid = min(tiles, #SMs)), 128 x BN output tiles (BN = 256 or 128),
-//     tile order m-fastest so the weight tile is reused from L2 by consecutive CTAs;
+//     grouped tile raster (tile_mn: blocks of 2048 rows, m fastest inside a block) so one wave's
+//     operand blocks are fetched from DRAM about once and reused from L2;
 //   * warp-specialised: warp 0 = TMA producer (one thread), warp 1 = tcgen05.mma issuer (whole
 //     warp, one elected lane), warps 2..9 = epilogue (two per TMEM lane quarter, each draining
 //     half of the tile's columns: TMEM -> registers -> smem transpose -> fused epilogue -> global);
@@ -88,10 +89,22 @@ __device__ __forceinline__ bool gemm_item(int it, int unit, int nunits, int tile
   return true;
 }
 
+// Tile raster: groups of `gm` m-tiles; inside a group m is fastest and n slower, so a wave of
+// persistent CTAs covers a compact gm x (units / gm) block of the output — each A row block and
+// each B column block is fetched from DRAM about once per group instead of once per n column
+// (m-fastest over all of M re-streams A for every column).
+__device__ __forceinline__ void tile_mn(int tile, int m_tiles, int n_tiles, int gm, int& mt, int& nt) {
+  const int per_group = gm * n_tiles;
+  const int g = tile / per_group, w = tile - g * per_group;
+  const int first = g * gm;
+  const int rows = min(gm, m_tiles - first);
+  mt = first + w % rows;
+  nt = w / rows;
+}
 template <int CG, int BN, bool A_MN, bool B_MN, int WN = 1>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                      int K, Epi epi, SplitK sk) {
+                      int K, Epi epi, SplitK sk, int group_m) {
   using C = Cfg<CG, BN, WN>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-aligned base derived by pointer arithmetic on the __shared__ array (not through an
@@ -143,8 +156,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint32_t phase = 0;
     int tile, k0, k1, part;
     for (int item = 0; gemm_item(item, unit, nunits, tiles, kbs, sk, tile, k0, k1, part); ++item) {
-      const int m0 = (tile % m_tiles) * C::TILE_M + crank * BM;
-      const int nt0 = (tile / m_tiles) * C::TILE_N + crank * (BN / CG);
+      int mt, nt;
+      tile_mn(tile, m_tiles, n_tiles, group_m, mt, nt);
+      const int m0 = mt * C::TILE_M + crank * BM;
+      const int nt0 = nt * C::TILE_N + crank * (BN / CG);
       for (int kb = k0; kb < k1; ++kb) {
         mbar_wait(empty + stage, phase ^ 1);
         if (leader) mbar_expect_tx(full + stage, C::STAGE * CG);
@@ -298,7 +313,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     };
     int tile, k0, k1, part;
     for (int item = 0; gemm_item(item, unit, nunits, tiles, kbs, sk, tile, k0, k1, part); ++item) {
-      const int m0 = (tile % m_tiles) * C::TILE_M + crank * BM, n0 = (tile / m_tiles) * C::TILE_N;
+      int mt, nt;
+      tile_mn(tile, m_tiles, n_tiles, group_m, mt, nt);
+      const int m0 = mt * C::TILE_M + crank * BM, n0 = nt * C::TILE_N;
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
       float* wst = part < 0 ? nullptr : sk.ws + ((int64_t)(tile - sk.dp_tiles) * sk.S * CG + crank) * 128 * C::TILE_N;
@@ -348,11 +365,6 @@ int g_force_cg = 0;  // test hook: TP_GEMM_CG=1|2 forces the CTA-group size
 // Stream-K tail (TP_GEMM_STREAMK=0 disables, read per launch): ~2 % on the 13B 4-stage pipeline
 // step (its slice GEMMs leave partial waves), neutral at N = 1.
 int g_stream_k = 1;
-// stream-K workspace (grow-only, one GEMM at a time uses it: all persistent GEMMs of a context run on
-// its main stream)
-float* g_sk_ws = nullptr;
-int* g_sk_cnt = nullptr;
-size_t g_sk_ws_n = 0, g_sk_cnt_n = 0;
 int g_num_sms = 0;
 std::once_flag g_once;
 
@@ -413,31 +425,14 @@ cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
     // each part must keep >= 32 k-blocks of MMA work to amortise its fp32 partial write and the
     // last part's S-way read (e.g. K = 2048 -> no split, K = 5120 -> S <= 2)
     const int S = tail > 0 ? std::min(std::min(4, full_units / tail), kbs / 32) : 1;
-    if (S >= 2) {
-      const size_t ws_need = (size_t)tail * S * CG * 128 * C::TILE_N, cnt_need = (size_t)tail * CG;
-      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-      cudaStreamIsCapturing(st, &cap);
-      if (ws_need > g_sk_ws_n || cnt_need > g_sk_cnt_n) {
-        if (cap == cudaStreamCaptureStatusNone) {  // grow (never inside a graph capture)
-          cudaStreamSynchronize(st);
-          if (g_sk_ws) cudaFree(g_sk_ws);
-          if (g_sk_cnt) cudaFree(g_sk_cnt);
-          g_sk_ws = nullptr; g_sk_cnt = nullptr; g_sk_ws_n = g_sk_cnt_n = 0;
-          if (cudaMalloc(&g_sk_ws, ws_need * sizeof(float)) == cudaSuccess &&
-              cudaMalloc(&g_sk_cnt, cnt_need * sizeof(int)) == cudaSuccess &&
-              cudaMemset(g_sk_cnt, 0, cnt_need * sizeof(int)) == cudaSuccess) {
-            g_sk_ws_n = ws_need;
-            g_sk_cnt_n = cnt_need;
-          }
-        }
-      }
-      if (ws_need <= g_sk_ws_n && cnt_need <= g_sk_cnt_n) {
-        sk.dp_tiles = tiles - tail;
-        sk.S = S;
-        sk.ws = g_sk_ws;
-        sk.cnt = g_sk_cnt;
-        units = full_units;
-      }
+    if (S >= 2 && g.sk_ws && g.sk_cnt) {
+      // tail * S * CG <= #SMs partial tiles of 128 x TILE_N <= 128 x 256 fp32: the fixed workspace
+      // of gemm_sm100_workspace always fits
+      sk.dp_tiles = tiles - tail;
+      sk.S = S;
+      sk.ws = g.sk_ws;
+      sk.cnt = g.sk_cnt;
+      units = full_units;
     }
   }
   cudaLaunchConfig_t cfg = {};
@@ -452,7 +447,10 @@ cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ta, tb, g.M, g.N, g.K, e, sk);
+  // raster group: TP_GEMM_GROUP rows of M per group (default 2048; >= M gives the plain m-fastest order)
+  const int group_rows = getenv("TP_GEMM_GROUP") ? std::max(1, atoi(getenv("TP_GEMM_GROUP"))) : 2048;
+  const int group_m = std::max(1, group_rows / C::TILE_M);
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, g.M, g.N, g.K, e, sk, group_m);
 }
 
 template <int CG, int BN, int WN = 1>
@@ -500,6 +498,15 @@ bool encode_f32_map_sw128(CUtensorMap* map, const void* ptr, int rank, const uin
   return g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(ptr), d, st, b, e,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+void gemm_sm100_workspace(size_t* ws_floats, size_t* cnt_ints) {
+  init_once();
+  *ws_floats = (size_t)g_num_sms * 128 * 256;
+  *cnt_ints = (size_t)g_num_sms;
+}
+bool tensor_maps_available() {
+  init_once();
+  return g_encode != nullptr;
 }
 int num_sms() {
   init_once();

@@ -38,6 +38,19 @@ extern "C" tp_status tpk_gemm(int32_t M, int32_t N, int32_t K, const void* A, in
   e.kind = EPI_STORE; e.out = out; e.ldo = ldo; e.out_f32 = 1;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (impl == 0) {
+    // fixed-size stream-K workspace of the kernel-level API (allocated once, never reallocated, so a
+    // captured launch never sees a freed pointer); tickets start at zero and the last part resets them
+    static float* ws = nullptr;
+    static int* cnt = nullptr;
+    if (!ws) {
+      size_t nw = 0, nc = 0;
+      gemm_sm100_workspace(&nw, &nc);
+      if (cudaMalloc(&ws, nw * sizeof(float)) != cudaSuccess || cudaMalloc(&cnt, nc * sizeof(int)) != cudaSuccess ||
+          cudaMemset(cnt, 0, nc * sizeof(int)) != cudaSuccess)
+        return fail(TP_ENOMEM, "tpk_gemm: stream-K workspace");
+    }
+    g.sk_ws = ws;
+    g.sk_cnt = cnt;
     if (!gemm_sm100_supported(g)) return fail(TP_EINVAL, "tpk_gemm: shape/alignment not supported by the sm100 kernel");
     return cu(gemm_sm100(g, e, st), "gemm_sm100");
   }

@@ -21,12 +21,21 @@ struct GemmDesc {
   int64_t ldb = 0;
   bool b_mn = false;  // false: B[n*ldb + k];  true: B[k*ldb + n]
   bool persistent = true;  // false: one tile per CTA (lets higher-priority streams interleave)
+  // stream-K workspace of the caller (gemm_sm100_workspace sizes): fp32 partial tiles + per-tile
+  // tickets (zero between launches). Null: no stream-K split. One GEMM at a time may use a workspace.
+  float* sk_ws = nullptr;
+  int* sk_cnt = nullptr;
 };
 
 template <typename T> cudaError_t gemm_simt(const GemmDesc& g, const Epi& e, cudaStream_t st);
 // tcgen05 / TMEM / TMA GEMM for sm_100a, bf16 operands, fp32 accumulation (gemm_sm100.cu).
 cudaError_t gemm_sm100(const GemmDesc& g, const Epi& e, cudaStream_t st);
 bool gemm_sm100_supported(const GemmDesc& g);
+// Fixed stream-K workspace size that covers every launch on this device: tail tiles x parts x CTAs
+// per tile <= #SMs, each a 128 x 256 fp32 partial (floats), plus one int ticket per SM.
+void gemm_sm100_workspace(size_t* ws_floats, size_t* cnt_ints);
+// false when the driver's cuTensorMapEncodeTiled entry point is unavailable (no TMA descriptors)
+bool tensor_maps_available();
 
 template <typename T>
 cudaError_t layernorm_fwd(const float* x, const float* gam, const float* bet, T* y, float* mean,
@@ -43,7 +52,9 @@ cudaError_t layernorm_bwd(const T* dy /* compute precision: bf16 in bf16 mode */
 cudaError_t embed_fwd(const int32_t* tok, const float* wte, const float* wpe, float* h, int c, int l, int b,
                       int s, int H, int V, cudaStream_t st);
 cudaError_t embed_bwd(const int32_t* tok, const float* dh, float* gwte, float* gwpe, int c, int l, int b,
-                      int s, int H, cudaStream_t st);
+                      int s, int H, int V, cudaStream_t st);
+// *bad = number of token ids outside [0, V) among tok[0..n) (device-side check of device tokens)
+cudaError_t count_bad_tokens(const int32_t* tok, int64_t n, int V, int* bad, cudaStream_t st);
 
 template <typename T>
 cudaError_t ce_fwd_bwd(T* logits_inout, const int32_t* tok, int c, int b, int s, float* loss_rows,

@@ -326,22 +326,26 @@ __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const float* _
                                  int V) {
   const int r = blockIdx.x;
   const int j = r % b, pos = c + r / b;
-  int id = tok[(int64_t)j * (s + 1) + pos];
-  id = min(max(id, 0), V - 1);
-  const float* e = wte + (int64_t)id * H;
+  const int id = tok[(int64_t)j * (s + 1) + pos];
+  // ids outside [0, V) are rejected by the step (host check, or the device count of
+  // count_bad_tokens); the row is then NaN, never an out-of-range read
+  const bool ok = id >= 0 && id < V;
+  const float* e = wte + (int64_t)(ok ? id : 0) * H;
   const float* p = wpe + (int64_t)pos * H;
   float* o = h + (int64_t)r * H;
   for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
-    float4 a = *reinterpret_cast<const float4*>(e + i), b = *reinterpret_cast<const float4*>(p + i);
+    float4 a = ok ? *reinterpret_cast<const float4*>(e + i) : make_float4(NAN, NAN, NAN, NAN);
+    float4 b = *reinterpret_cast<const float4*>(p + i);
     *reinterpret_cast<float4*>(o + i) = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
   }
 }
 
 __global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const float* __restrict__ dh,
-                                 float* __restrict__ gwte, float* __restrict__ gwpe, int c, int b, int s, int H) {
+                                 float* __restrict__ gwte, float* __restrict__ gwpe, int c, int b, int s, int H, int V) {
   const int r = blockIdx.x;
   const int j = r % b, pos = c + r / b;
   const int id = tok[(int64_t)j * (s + 1) + pos];
+  if (id < 0 || id >= V) return;  // rejected by the step; never scatter outside wte's gradient
   const float* g = dh + (int64_t)r * H;
   float* e = gwte + (int64_t)id * H;
   float* p = gwpe + (int64_t)pos * H;  // positions c..c+l are shared by the job's b sequences
@@ -384,8 +388,10 @@ __global__ void __launch_bounds__(512) ce_kernel(T* __restrict__ z, const int32_
   float S = 0.f;
   for (int w = 0; w < 16; ++w) S += rs[w] * __expf(rm[w] - M);
   const float lse = M + logf(S);
-  const int y = tok[(int64_t)(r % b) * (seq_len + 1) + c + r / b + 1];  // target = next token (A-8)
-  if (tid == 0) loss_rows[r] = lse - to_f<T>(zr[y]);
+  int y = tok[(int64_t)(r % b) * (seq_len + 1) + c + r / b + 1];  // target = next token (A-8)
+  const bool yok = y >= 0 && y < V;  // else rejected by the step: NaN loss, no read outside the row
+  if (tid == 0) loss_rows[r] = yok ? lse - to_f<T>(zr[y]) : NAN;
+  if (!yok) y = -1;
   __syncthreads();  // every thread has read z[y] (via tid 0) before it is overwritten
   for (int i = tid; i < V; i += 512) {
     const float p = __expf(to_f<T>(zr[i]) - lse);
@@ -434,8 +440,10 @@ __global__ void __launch_bounds__(512) ce_vec_kernel(bf16* __restrict__ z, const
 #pragma unroll
   for (int w = 0; w < 16; ++w) S += rs[w] * __expf(rm[w] - M);
   const float lse = M + logf(S);
-  const int y = tok[(int64_t)(r % b) * (seq_len + 1) + c + r / b + 1];  // target = next token (A-8)
-  if (tid == 0) loss_rows[r] = lse - __bfloat162float(zr[y]);
+  int y = tok[(int64_t)(r % b) * (seq_len + 1) + c + r / b + 1];  // target = next token (A-8)
+  const bool yok = y >= 0 && y < V;  // else rejected by the step: NaN loss, no read outside the row
+  if (tid == 0) loss_rows[r] = yok ? lse - __bfloat162float(zr[y]) : NAN;
+  if (!yok) y = -1;
   __syncthreads();  // z[y] read before the row is overwritten
   for (int ch = tid; ch < nch; ch += 512) {
     float v[8];
@@ -569,10 +577,25 @@ cudaError_t embed_fwd(const int32_t* tok, const float* wte, const float* wpe, fl
   embed_fwd_kernel<<<l * b, 256, 0, st>>>(tok, wte, wpe, h, c, b, s, H, V);
   return cudaGetLastError();
 }
+__global__ void count_bad_tokens_kernel(const int32_t* __restrict__ tok, int64_t n, int V, int* __restrict__ bad) {
+  int cnt = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    cnt += (tok[i] < 0 || tok[i] >= V) ? 1 : 0;
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(bad, cnt);
+}
+cudaError_t count_bad_tokens(const int32_t* tok, int64_t n, int V, int* bad, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(int), st);
+  if (e != cudaSuccess || n == 0) return e;
+  const int blocks = (int)std::min<int64_t>(1024, (n + 255) / 256);
+  count_bad_tokens_kernel<<<blocks, 256, 0, st>>>(tok, n, V, bad);
+  return cudaGetLastError();
+}
+
 cudaError_t embed_bwd(const int32_t* tok, const float* dh, float* gwte, float* gwpe, int c, int l, int b, int s,
-                      int H, cudaStream_t st) {
+                      int H, int V, cudaStream_t st) {
   if (l == 0) return cudaSuccess;
-  embed_bwd_kernel<<<l * b, 256, 0, st>>>(tok, dh, gwte, gwpe, c, b, s, H);
+  embed_bwd_kernel<<<l * b, 256, 0, st>>>(tok, dh, gwte, gwpe, c, b, s, H, V);
   return cudaGetLastError();
 }
 template <typename T>

@@ -216,6 +216,10 @@ class Engine final : public EngineBase {
   std::vector<void*> allocs;
   int32_t* d_tokens = nullptr;
   float* d_loss = nullptr;
+  float* sk_ws = nullptr;  // stream-K workspace of the persistent GEMMs on `stream` (fixed size)
+  int* sk_cnt = nullptr;
+  int* d_bad_tok = nullptr;  // device token check of the *_device steps: count of ids outside [0, V)
+  int* h_bad_tok = nullptr;  // pinned
   float* h_loss = nullptr;  // pinned
   int last_batch = 0;
   std::vector<std::pair<size_t, int>> last_groups;  // (seq0, b) of the last step's groups
@@ -225,7 +229,8 @@ class Engine final : public EngineBase {
   std::vector<int64_t> g_key;
   cudaGraphExec_t g_exec = nullptr;
   int64_t g_launches = 0;
-  // NCCL (multi-rank)
+  // NCCL (multi-rank, or the single-GPU NCCL loopback of TP_FLAG_NCCL_LOOPBACK)
+  bool nccl_lb = false;  // world == 1, K > 1: stage messages through ncclSend/ncclRecv to self
   ncclComm_t base = nullptr, commF[2] = {nullptr, nullptr}, commB[2] = {nullptr, nullptr};
   cudaStream_t s_recv_f = nullptr, s_send_f = nullptr, s_recv_b = nullptr, s_send_b = nullptr;
   cudaStream_t s_wgrad = nullptr;  // low priority: deferred weight gradients (multi-rank)
@@ -240,6 +245,7 @@ class Engine final : public EngineBase {
       if (c) ncclCommDestroy(c);
     for (void* p : allocs) cudaFree(p);
     if (h_loss) cudaFreeHost(h_loss);
+    if (h_bad_tok) cudaFreeHost(h_bad_tok);
     for (auto e : ev_pool) cudaEventDestroy(e);
     for (cudaStream_t s : {s_recv_f, s_send_f, s_recv_b, s_send_b, s_wgrad, stream})
       if (s) cudaStreamDestroy(s);
@@ -280,6 +286,7 @@ class Engine final : public EngineBase {
     instr.on = (flags & TP_FLAG_KERNEL_STATS) != 0;
     if (const char* e = std::getenv("TP_LEGACY_ATTN")) legacy_attn = std::atoi(e) != 0;
     if (world == 1) { k0 = 0; k1 = m.K; } else { k0 = rank; k1 = rank + 1; }
+    nccl_lb = world == 1 && m.K > 1 && (flags & TP_FLAG_NCCL_LOOPBACK) != 0;
     CU(cudaSetDevice(device));
     int major = 0;
     CU(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
@@ -292,12 +299,31 @@ class Engine final : public EngineBase {
     use_graphs = std::getenv("TP_NO_GRAPHS") == nullptr && std::getenv("TP_ATTN_DEBUG") == nullptr;
     TRY(alloc(&d_tokens, (size_t)max_batch * (m.s + 1)));
     TRY(alloc(&d_loss, 4));
+    CU(cudaHostAlloc(&h_bad_tok, sizeof(int), cudaHostAllocDefault));
+    TRY(alloc(&d_bad_tok, 1));
+    if (std::is_same<T, bf16>::value && !force_simt) {
+      // bf16 mode runs every GEMM on the tcgen05 kernel: no silent SIMT fallback
+      if (!tensor_maps_available())
+        return fail(TP_ECUDA, "tp_init: cuTensorMapEncodeTiled is unavailable (driver too old?); the bf16 path needs TMA");
+      size_t nw = 0, nc = 0;
+      gemm_sm100_workspace(&nw, &nc);
+      TRY(alloc(&sk_ws, nw));
+      TRY(alloc(&sk_cnt, nc));
+      CU(cudaMemset(sk_cnt, 0, nc * sizeof(int)));
+    }
     stages.resize(k1 - k0);
     for (int k = k0; k < k1; ++k) TRY(alloc_stage(stages[k - k0], k));
-    if (world > 1) {
-      ncclUniqueId id;
-      std::memcpy(&id, nccl_id, sizeof id);
-      NC(ncclCommInitRank(&base, world, id, rank));
+    if (world > 1 || nccl_lb) {
+      if (world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof id);
+        NC(ncclCommInitRank(&base, world, id, rank));
+      } else {
+        // one-rank communicator: stage k -> k+1 messages are ncclSend/ncclRecv to self (the same
+        // NCCL p2p kernels, streams and events as world == K; runnable on a one-GPU box)
+        int dev = device;
+        NC(ncclCommInitAll(&base, 1, &dev));
+      }
       // one communicator per (direction, edge parity): each rank uses each communicator from
       // exactly one stream, so p2p ops on a communicator are issued in one order on both ends.
       for (int i = 0; i < 2; ++i) {
@@ -337,7 +363,7 @@ class Engine final : public EngineBase {
     if (last) { TRY(alloc(&S.wout_t, H * m.V)); TRY(alloc(&S.wout_io, H * m.V)); }
     S.hs.assign(nl + 1, nullptr);
     // loopback: stage k's input buffer IS stage k-1's output buffer (the "send" is free)
-    const bool alias = world == 1 && k > k0;
+    const bool alias = world == 1 && k > k0 && !nccl_lb;
     if (alias) S.hs[0] = stages[k - 1 - k0].hs[stages[k - 1 - k0].nl];
     for (size_t j = alias ? 1 : 0; j <= nl; ++j) TRY(alloc(&S.hs[j], B * s * H));
     TRY(vec(S.hmid, nl, B * s * H));
@@ -427,12 +453,18 @@ class Engine final : public EngineBase {
   }
 
   // ------------------------------------------------------------ launch helpers
-  tp_status gemm(int cls, const GemmDesc& g, const Epi& e, cudaStream_t st = nullptr) {
+  tp_status gemm(int cls, const GemmDesc& g0, const Epi& e, cudaStream_t st = nullptr) {
     if (!st) st = stream;
+    GemmDesc g = g0;
+    if (st == stream) { g.sk_ws = sk_ws; g.sk_cnt = sk_cnt; }  // one persistent GEMM at a time on `stream`
     Pending p;
     instr.begin(st, cls, 2.0 * g.M * g.N * g.K, 0, p);
     cudaError_t err;
-    if (!force_simt && std::is_same<T, bf16>::value && gemm_sm100_supported(g)) {
+    if (!force_simt && std::is_same<T, bf16>::value) {
+      // bf16 mode: the tcgen05 kernel or an error, never a silent ~10x slower SIMT fallback
+      if (!gemm_sm100_supported(g))
+        return fail(TP_ECUDA, "gemm M=%d N=%d K=%d lda=%lld ldb=%lld: not supported by the sm100 kernel (alignment)",
+                    g.M, g.N, g.K, (long long)g.lda, (long long)g.ldb);
       err = gemm_sm100(g, e, st);
     } else {
       Epi e0 = e;
@@ -640,7 +672,7 @@ class Engine final : public EngineBase {
     }
     if (S.k == 0) {
       TRY(launch(KC_EMBED, 0, 12.0 * Tn * H, [&] {
-        return embed_bwd(tok0, S.grad_in + row * H, S.gflat + S.L.wte, S.gflat + S.L.wpe, c, l, b, s, H, stream);
+        return embed_bwd(tok0, S.grad_in + row * H, S.gflat + S.L.wte, S.gflat + S.L.wpe, c, l, b, s, H, V, stream);
       }));
     }
     return TP_OK;
@@ -724,6 +756,27 @@ class Engine final : public EngineBase {
     return TP_OK;
   }
 
+  // NCCL loopback (world == 1): the message of one job from stage S to its neighbour T (both owned
+  // by this context) as a grouped ncclSend + ncclRecv to self on the direction's comm stream, gated
+  // by events exactly like the multi-rank path (sender's compute -> comm stream -> receiver's compute)
+  tp_status p2p_self(const float* src, float* dst, size_t count, bool fwd, int edge) {
+    cudaStream_t cs = fwd ? s_send_f : s_send_b;
+    ncclComm_t comm = fwd ? commF[edge & 1] : commB[edge & 1];
+    cudaEvent_t e0 = event(), e1 = event();
+    CU(cudaEventRecord(e0, stream));
+    CU(cudaStreamWaitEvent(cs, e0, 0));
+    Pending p;
+    instr.begin(cs, KC_COMM, 0, 4.0 * count, p);
+    NC(ncclGroupStart());
+    NC(ncclSend(src, count, ncclFloat32, 0, comm, cs));
+    NC(ncclRecv(dst, count, ncclFloat32, 0, comm, cs));
+    NC(ncclGroupEnd());
+    instr.end(cs, p);
+    CU(cudaEventRecord(e1, cs));
+    CU(cudaStreamWaitEvent(stream, e1, 0));
+    return TP_OK;
+  }
+
   // ------------------------------------------------------------ one step
   // Everything one step puts on the device after the tokens are in d_tokens: zero the gradients, the
   // forward and backward op lists of every owned stage, the deferred weight gradients, the loss.
@@ -735,7 +788,7 @@ class Engine final : public EngineBase {
   tp_status enqueue_step(const std::vector<Group>& G, int batch) {
     const int D = (int)G.size();
     const bool multi = world > 1;
-    if (multi) {  // fork: the comm streams join this step's stream order (and any graph capture)
+    if (multi || nccl_lb) {  // fork: the comm streams join this step's stream order (and any graph capture)
       cudaEvent_t e = event();
       CU(cudaEventRecord(e, stream));
       for (cudaStream_t cs : {s_send_f, s_recv_f, s_send_b, s_recv_b}) CU(cudaStreamWaitEvent(cs, e, 0));
@@ -745,13 +798,16 @@ class Engine final : public EngineBase {
     // inside a job in loopback); a job is b_d*l_i tokens, contiguous rows (see fwd())
     for (int d = 0; d < D; ++d)
       for (size_t i = 0; i < G[d].len.size(); ++i)
-        for (auto& S : stages) {
+        for (size_t si = 0; si < stages.size(); ++si) {
+          Stage<T>& S = stages[si];
           const int b = G[d].b;
           const size_t row = G[d].seq0 * m.s + (size_t)G[d].off[i] * b;
           const int Tn = b * G[d].len[i];
           if (multi && S.k > 0) TRY(recv_fwd(S, row, Tn));
           TRY(fwd(S, G[d].seq0, G[d].off[i], G[d].len[i], b, batch));
           if (multi && S.k < m.K - 1) TRY(send_fwd(S, row, Tn));
+          if (nccl_lb && si + 1 < stages.size())
+            TRY(p2p_self(S.hs[S.nl] + row * m.H, stages[si + 1].hs[0] + row * m.H, (size_t)Tn * m.H, true, S.k));
         }
     // backward: exact reverse order (GPipe order, A-21). Weight gradients: one K = B*s GEMM per
     // weight at the end (the last stage's overlaps the other stages' remaining backward); with
@@ -768,6 +824,8 @@ class Engine final : public EngineBase {
           if (multi && S.k < m.K - 1) TRY(recv_bwd(S, row, Tn));
           TRY(bwd(S, G[d].seq0, G[d].off[i], G[d].len[i], b, batch, i == M - 1));
           if (multi && S.k > 0) TRY(send_bwd(S, row, Tn));
+          if (nccl_lb && si > 0)
+            TRY(p2p_self(S.grad_in + row * m.H, stages[si - 1].grad_out + row * m.H, (size_t)Tn * m.H, false, S.k - 1));
         }
       if (side_dw) {
         cudaEvent_t e = event();
@@ -791,14 +849,14 @@ class Engine final : public EngineBase {
     } else {
       CU(cudaMemsetAsync(d_loss, 0, sizeof(float), stream));
     }
-    if (multi) {
+    if (multi || nccl_lb) {
       // the comm streams must have drained before the step ends
       for (cudaStream_t cs : {s_send_f, s_recv_f, s_send_b, s_recv_b}) {
         cudaEvent_t e = event();
         CU(cudaEventRecord(e, cs));
         CU(cudaStreamWaitEvent(stream, e, 0));
       }
-      NC(ncclAllReduce(d_loss, d_loss, 1, ncclFloat32, ncclSum, base, stream));
+      if (multi) NC(ncclAllReduce(d_loss, d_loss, 1, ncclFloat32, ncclSum, base, stream));
     }
     CU(cudaMemcpyAsync(h_loss, d_loss, sizeof(float), cudaMemcpyDeviceToHost, stream));
     return TP_OK;
@@ -832,6 +890,8 @@ class Engine final : public EngineBase {
     if (batch < 1 || batch > max_batch)
       return fail(TP_EINVAL, "tp_step_plan: batch %d not in [1, max_batch=%d]", batch, max_batch);
     if (pl->n_groups < 1 || pl->n_groups > batch) return fail(TP_EINVAL, "tp_step_plan: n_groups %d", pl->n_groups);
+    if (pl->n_groups > pl->capacity_groups)
+      return fail(TP_EINVAL, "tp_step_plan: n_groups %d exceeds capacity_groups %d", pl->n_groups, pl->capacity_groups);
     std::vector<Group> G(pl->n_groups);
     size_t seq0 = 0, pos = 0;
     for (int d = 0; d < pl->n_groups; ++d) {
@@ -866,11 +926,20 @@ class Engine final : public EngineBase {
     for (const Group& g : G) last_groups.push_back({g.seq0, g.b});
     // tokens -> d_tokens, outside any graph (the caller's pointer may change between calls)
     const size_t ntok = (size_t)batch * (m.s + 1);
+    // token ids outside [0, V) are rejected (TP_EINVAL), never clamped: host tokens before anything
+    // runs, device tokens by a device count read back with the loss
     if (host_tokens) {
+      for (size_t i = 0; i < ntok; ++i)
+        if (tokens[i] < 0 || tokens[i] >= m.V)
+          return fail(TP_EINVAL, "tp_step: token id %d at [%zu][%zu] outside [0, %d)", tokens[i], i / (m.s + 1),
+                      i % (m.s + 1), m.V);
       std::memcpy(h_tokens, tokens, ntok * sizeof(int32_t));
       CU(cudaMemcpyAsync(d_tokens, h_tokens, ntok * sizeof(int32_t), cudaMemcpyHostToDevice, stream));
+      *h_bad_tok = 0;
     } else {
       CU(cudaMemcpyAsync(d_tokens, tokens, ntok * sizeof(int32_t), cudaMemcpyDeviceToDevice, stream));
+      CU(count_bad_tokens(d_tokens, (int64_t)ntok, m.V, d_bad_tok, stream));
+      CU(cudaMemcpyAsync(h_bad_tok, d_bad_tok, sizeof(int), cudaMemcpyDeviceToHost, stream));
     }
     // The op list of a plan is static: the first step with a new key runs eagerly, the second is
     // captured into a CUDA graph, later ones replay it (no per-kernel host launch cost).
@@ -920,6 +989,8 @@ class Engine final : public EngineBase {
     CU(cudaStreamSynchronize(stream));
     CU(cudaGetLastError());
     instr.resolve();
+    if (*h_bad_tok)
+      return fail(TP_EINVAL, "tp_step_device: %d token ids outside [0, %d); the step's results are invalid", *h_bad_tok, m.V);
     if (loss_out) *loss_out = (float)(*h_loss / ((double)batch * m.s));
     return TP_OK;
   }
@@ -968,14 +1039,21 @@ tp_status Engine<T>::profile(int g, int bsl, int reps, int64_t* ticks, double* f
   cudaEvent_t e0, e1;
   CU(cudaEventCreate(&e0));
   CU(cudaEventCreate(&e1));
-  // tokens for sequence 0 (values do not affect dense cost)
+  // tokens for sequence 0 (values do not affect dense cost); finite dK/dV accumulators for the
+  // reduce-add path of non-final slices
   CU(cudaMemsetAsync(d_tokens, 0, sizeof(int32_t) * (m.s + 1) * bsl, stream));
+  for (int j = 0; j < S.nl; ++j) {
+    CU(cudaMemsetAsync(S.dk_acc[j], 0, sizeof(float) * (size_t)bsl * m.s * m.H, stream));
+    CU(cudaMemsetAsync(S.dv_acc[j], 0, sizeof(float) * (size_t)bsl * m.s * m.H, stream));
+  }
   auto time_job = [&](int l, int c, double* out_ns) -> tp_status {
     std::vector<float> v;
     for (int r = 0; r < reps + 2; ++r) {
       CU(cudaEventRecord(e0, stream));
       TRY(fwd(S, 0, c, l, bsl, bsl));
-      TRY(bwd(S, 0, c, l, bsl, bsl, true));
+      // as the step runs it: the slice ending at s (the first in backward) stores dK/dV, every other
+      // slice reduce-adds into the c + l prefix rows
+      TRY(bwd(S, 0, c, l, bsl, bsl, c + l == m.s));
       CU(cudaEventRecord(e1, stream));
       CU(cudaEventSynchronize(e1));
       float ms = 0;

@@ -47,8 +47,8 @@ def test_gemm(M, N, K, a_mn, b_mn, impl):
 
 @pytest.mark.parametrize("M,N,K", [(8192, 2048, 4096), (768, 15360, 5120), (1024, 5120, 8192), (300, 4096, 8192)])
 def test_gemm_stream_k(M, N, K, monkeypatch):
-    """Opt-in stream-K tail (TP_GEMM_STREAMK=1): the partial last wave's tiles split along K, partial
-    fp32 tiles reduced by the last part before the epilogue."""
+    """Stream-K tail (on by default; TP_GEMM_STREAMK=0 disables): the partial last wave's tiles split
+    along K, partial fp32 tiles reduced by the last part before the epilogue. K-major operands."""
     monkeypatch.setenv("TP_GEMM_STREAMK", "1")
     g = torch.Generator(device="cpu").manual_seed(M + N + K)
     A = torch.randn(M, K, generator=g).to(dev, torch.bfloat16)
@@ -59,6 +59,30 @@ def test_gemm_stream_k(M, N, K, monkeypatch):
         tp.k_gemm(M, N, K, ptr(A), K, 0, ptr(B), K, 0, ptr(out), N, 0)
         torch.cuda.synchronize()
         assert rel(out, ref) < 1e-5, rel(out, ref)
+
+
+@pytest.mark.parametrize("M,N,K", [(2048, 6144, 8192), (2048, 2048, 16384), (8192, 2048, 4096),
+                                   (2048, 8192, 16384), (2048, 1024, 8192), (1000, 2048, 4096)])
+@pytest.mark.parametrize("wide", [None, "1", "0"])
+def test_gemm_weight_grad_shapes(M, N, K, wide, monkeypatch):
+    """The deferred weight-gradient GEMMs the bench times (dW = X^T dY, K = B*s, both operands
+    MN-major): the 256 x 512 pair tile (<2,256,MN,MN,WN=2>, chosen by the wave model for K >= 4096,
+    TP_GEMM_WIDE=1 forces it, =0 disables it) and the MN-major stream-K tail, at the bench's K."""
+    if wide is not None:
+        monkeypatch.setenv("TP_GEMM_WIDE", wide)
+    g = torch.Generator(device="cpu").manual_seed(M + 3 * N + K)
+    A = torch.randn(M, K, generator=g).to(dev, torch.bfloat16)
+    B = torch.randn(N, K, generator=g).to(dev, torch.bfloat16)
+    ref = A.float() @ B.float().T
+    Ast, Bst = A.T.contiguous(), B.T.contiguous()   # [K][M], [K][N]: MN-major, as X and dY are stored
+    out = torch.full((M, N), float("nan"), device=dev)
+    for _ in range(2):  # the second launch reuses the stream-K tickets
+        tp.k_gemm(M, N, K, ptr(Ast), M, 1, ptr(Bst), N, 1, ptr(out), N, 0)
+        torch.cuda.synchronize()
+        assert rel(out, ref) < 1e-5, rel(out, ref)
+    # per output row: a mis-indexed tile or K-part is O(1) off in its rows
+    rr = ((out.double() - ref.double()).norm(dim=1) / ref.double().norm(dim=1)).max().item()
+    assert rr < 1e-4, rr
 
 
 def attn_ref(q, k, v, c, l):

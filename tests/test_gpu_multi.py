@@ -1,6 +1,7 @@
 """Multi-GPU (NCCL send/recv over NVLink) parity: K = world stages, one process per GPU, against
 the fp64 oracle. Skipped when fewer GPUs are visible."""
 import json
+import numpy as np
 import os
 import subprocess
 import sys
@@ -36,14 +37,6 @@ def test_small_two_stages_nccl_side_stream_dw(tmp_path):
         assert max(errs.values()) < 2e-2, errs
 
 
-@pytest.mark.parametrize("g", ["1", "2"])
-def test_small_two_stages_group_dw(g, tmp_path):
-    """TP_GROUP_DW=g: the first stage computes the weight gradients of every run of g finished groups
-    in order (three groups of different b: flushes of one or two groups, then the rest at the end)."""
-    for errs in run(2, "small", "bf16", "1:40,24,64;1:128;2:64,64", tmp_path, batch=4, env={"TP_GROUP_DW": g}):
-        assert max(errs.values()) < 2e-2, errs
-
-
 def test_small_four_stages_nccl(tmp_path):
     for errs in run(4, "small", "bf16", "40,24,64", tmp_path):
         assert max(errs.values()) < 2e-2, errs
@@ -54,3 +47,68 @@ def test_small_two_stages_heterogeneous_batch_plan(tmp_path):
     of different row counts and message sizes on the p2p edges)."""
     for errs in run(2, "small", "bf16", "2:40,24,64;1:128", tmp_path, batch=3):
         assert max(errs.values()) < 2e-2, errs
+
+
+# ---------------------------------------------------------------- NCCL p2p on one GPU
+# TP_FLAG_NCCL_LOOPBACK: all K stages in one context, every stage message (rows a11 / a16: the
+# slice's fp32 activation to stage k+1, its gradient back to stage k-1, PAPER.md:193) goes through
+# ncclSend / ncclRecv to self on a one-rank communicator, on the same per-direction comm streams,
+# split communicators and events as the one-process-per-GPU path. Runs on a one-GPU box.
+from synth import CONFIGS as _CONFIGS  # noqa: E402
+import paper_2102_07988_b200 as tp  # noqa: E402
+from tests.gpu_util import gpu_run, gpu_run_plan, oracle_run, worst_errors  # noqa: E402
+
+NL = tp.TP_FLAG_KEEP_LOGITS | tp.TP_FLAG_NCCL_LOOPBACK
+
+
+@pytest.mark.parametrize("precision,tol", [(tp.TP_BF16, 2e-2), (tp.TP_FP32, 1e-4)])
+@pytest.mark.parametrize("lengths", [[5, 9, 2, 16], [32], [1] * 32])
+def test_tiny_nccl_loopback(precision, tol, lengths):
+    cfg, B = _CONFIGS["tiny"]
+    params, tokens, ref = oracle_run(cfg, B, 0, precision == tp.TP_BF16)
+    loss, logits, grads, launches = gpu_run(cfg, B, params, tokens, lengths, precision, flags=NL)
+    errs = worst_errors(loss, logits, grads, ref)
+    assert max(errs.values()) < tol, errs
+
+
+@pytest.mark.parametrize("K", [2, 4])
+def test_small_nccl_loopback(K):
+    base, B = _CONFIGS["small"]
+    cfg = base.with_(n_stages=K)
+    params, tokens, ref = oracle_run(cfg, B, 3, True)
+    loss, logits, grads, _ = gpu_run(cfg, B, params, tokens, [40, 24, 64], tp.TP_BF16, flags=NL)
+    errs = worst_errors(loss, logits, grads, ref)
+    assert max(errs.values()) < 2e-2, errs
+
+
+@pytest.mark.parametrize("K,groups", [(2, [(2, [40, 24, 64]), (1, [128]), (1, [8] * 16)]),
+                                      (4, [(3, [128]), (1, [32, 32, 32, 32])])])
+def test_heterogeneous_plan_nccl_loopback(K, groups):
+    base, _ = _CONFIGS["small"]
+    cfg = base.with_(n_stages=K)
+    params, tokens, ref = oracle_run(cfg, 4, 9, True)
+    loss, logits, grads = gpu_run_plan(cfg, 4, params, tokens, groups, tp.TP_BF16, flags=NL)
+    errs = worst_errors(loss, logits, grads, ref)
+    assert max(errs.values()) < 2e-2, errs
+
+
+def test_nccl_loopback_equals_aliasing_loopback():
+    """The same step with messages through NCCL and with aliased buffers gives identical results
+    up to the order of float atomics in the gradient reductions (the messages are exact fp32 copies),
+    and the captured NCCL graph replays the eager step."""
+    base, B = _CONFIGS["small"]
+    cfg = base.with_(n_stages=4)
+    params, tokens, _ = oracle_run(cfg, B, 5, False)
+    from synth import pack_all_stages, unpack_all_stages
+    outs = []
+    for fl in (0, tp.TP_FLAG_NCCL_LOOPBACK):
+        ctx = tp.Context(cfg, precision=tp.TP_FP32, max_batch=B, device=0, flags=fl)
+        try:
+            ctx.load_params(pack_all_stages(params, cfg))
+            ls = [ctx.step(tp.Slicing([40, 24, 64]), tokens) for _ in range(3)]
+            outs.append((ls, ctx.grads()))
+        finally:
+            ctx.close()
+    (la, ga), (lb, gb) = outs
+    assert abs(la[0] - lb[0]) <= 1e-6 * abs(la[0]) and abs(lb[0] - lb[2]) <= 1e-6 * abs(lb[0])
+    assert float(np.linalg.norm(ga - gb) / np.linalg.norm(ga)) < 1e-6

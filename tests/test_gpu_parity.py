@@ -198,3 +198,61 @@ def test_graph_replay_identical():
         assert abs(outs[0][0] - ref["loss"]) < 2e-2 * abs(ref["loss"])
     finally:
         ctx.close()
+
+
+def test_rejects_token_ids_outside_vocab():
+    """Token ids outside [0, V) are rejected (TP_EINVAL), never clamped: host tokens before the step
+    runs, device tokens by the device-side count read back with the loss (include/tp.h)."""
+    import torch
+    params, tokens, _ = oracle_run(TINY, 1, 0, True)
+    from synth import pack_all_stages
+    ctx = tp.Context(TINY, precision=tp.TP_BF16, max_batch=1, device=0)
+    try:
+        ctx.load_params(pack_all_stages(params, TINY))
+        sl = tp.Slicing([16, 16])
+        for bad in (-1, TINY.vocab):
+            t = tokens.copy()
+            t[0, 7] = bad
+            with pytest.raises(tp.TpError) as e:
+                ctx.step(sl, t)
+            assert e.value.status == tp.TP_EINVAL
+            dt = torch.from_numpy(t.astype(np.int32)).cuda()
+            with pytest.raises(tp.TpError) as e:
+                ctx.step_device(sl, dt.data_ptr(), 1)
+            assert e.value.status == tp.TP_EINVAL
+        # valid tokens still work afterwards (device and host)
+        dt = torch.from_numpy(tokens.astype(np.int32)).cuda()
+        a = ctx.step_device(sl, dt.data_ptr(), 1)
+        b = ctx.step(sl, tokens)
+        assert np.isfinite(a) and abs(a - b) <= 1e-6 * abs(b)
+        with pytest.raises(tp.TpError):
+            ctx.step(sl, tokens[:, :-1])  # wrong token row length
+    finally:
+        ctx.close()
+
+
+def test_tiny_measured_table_vs_2pow31_brute_force():
+    """SURVEY.md §8 acceptance (i) with a MEASURED table: tp_profile of the tiny config (s = 32,
+    g = 1, BASELINE.json:7) feeds tp_plan (K = 2, D = 1), and the result equals the oracle's brute
+    force over all 2^31 compositions (oracle/bf_compositions.c) on the same table, bit-exactly in T,
+    t_max and the slice boundaries."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    bf = os.path.join(root, "oracle", "bf_compositions")
+    if not os.path.exists(bf):
+        subprocess.run(["gcc", "-O2", "-fopenmp", "-o", bf, bf + ".c"], check=True)
+    params, tokens, _ = oracle_run(TINY, 1, 0, True)
+    from synth import pack_all_stages
+    ctx = tp.Context(TINY, precision=tp.TP_BF16, max_batch=1, device=0)
+    try:
+        ctx.load_params(pack_all_stages(params, TINY))
+        ticks, _ = ctx.profile(1, reps=3)
+    finally:
+        ctx.close()
+    n = TINY.seq_len
+    inp = f"{n} 2 1\n" + " ".join(str(int(v)) for v in ticks.reshape(-1))
+    out = [int(x) for x in subprocess.run([bf], input=inp, capture_output=True, text=True, check=True,
+                                          timeout=600).stdout.split()]
+    s = tp.plan(ticks, 1, TINY.n_layer, TINY.hidden, n, 2)
+    assert (s.predicted, s.t_max, s.lengths) == (out[0], out[1], out[3:3 + out[2]])
