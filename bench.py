@@ -231,13 +231,16 @@ def main():
         [x for x in (1, 2, 4, 8, 16) if B % x == 0 and x <= B]
     dp, fit, t_prof, t_plan, plans = None, None, 0.0, 0.0, []
     gpipe = tp.BatchPlan.uniform(tp.Slicing([cfg.seq_len]), B)
+    comm, t_wgrad = None, None
     if args.slicing in ("dp", "gpipe") and (args.slicing == "dp" or len(bsl) > 1):
         t0 = time.time()
         tables = {}
+        if world > 1:  # alpha / beta of a stage message, folded into every table entry
+            comm = ctx.profile_comm(reps=5)
         for b in bsl:
+            # the library measures every stage type this rank owns and (world > 1) takes the max over
+            # all ranks: the bottleneck table of DESIGN.md A-16
             ticks, f = ctx.profile(g, reps=args.profile_reps, batch_slice=b)
-            if world > 1:
-                ticks = tdist.bottleneck_table(ticks)
             tables[b] = ticks
             t1 = time.time()
             sl = tp.plan(ticks, g, cfg.n_layer, cfg.hidden, cfg.seq_len, K, n_micro=B // b, eps_ticks=0)
@@ -246,6 +249,7 @@ def main():
             n = cfg.seq_len // g
             gp_pred = (B // b + K - 1) * int(ticks[n - 1, 0])   # unsliced [(b, [s])] * (B/b)
             plans.append({"b": b, "slicing": sl, "fit": f, "gpipe_pred": gp_pred})
+        t_wgrad = ctx.profile_wgrad(B, reps=3)  # slicing-independent constant of the step model
         t1 = time.time()
         dp = tp.plan_joint(tables, g, cfg.n_layer, cfg.hidden, cfg.seq_len, K, B, eps_ticks=0)
         t_plan += time.time() - t1
@@ -331,10 +335,15 @@ def main():
             "speedup_of_dp": ms_gpipe / ms},
         "plan": None if dp is None else {
             "predicted_ms": dp.predicted / 1e6, "t_max_ms": dp.t_max / 1e6, "profile_s": t_prof, "plan_s": t_plan,
+            "wgrad_ms": t_wgrad / 1e6,
+            "predicted_step_ms": (dp.predicted + t_wgrad) / 1e6,
+            "predicted_step_err": ((dp.predicted + t_wgrad) / 1e6 - ms) / ms if main_sl is dp else None,
+            "comm": None if comm is None else {"alpha_us": comm[0] / 1e3, "gbs": comm[1]},
             "fit": {"a": [float(x) for x in fit[:4]], "max_rel_err": float(fit[4])},
             "joint": "tp_plan_joint over b in " + str(bsl),
             "candidates": [{"b": p["b"], "slicing": p["slicing"].notation(B), "predicted_ms": p["slicing"].predicted / 1e6,
-                            "gpipe_predicted_ms": p["gpipe_pred"] / 1e6} for p in plans]},
+                            "gpipe_predicted_ms": p["gpipe_pred"] / 1e6} for p in plans],
+            "gpipe_predicted_step_ms": (gbest["gpipe_pred"] + t_wgrad) / 1e6},
         "loss": loss,
         "clocks": clk,
         "e2e": {"value": tokens_per_step / (ms_e2e / 1e3), "unit": "tokens/s",

@@ -206,17 +206,39 @@ tp_status tp_get_grads(tp_ctx* ctx, float* host_out, size_t n);
  * TP_FLAG_KEEP_LOGITS and a context owning the last stage (else TP_ESTATE). */
 tp_status tp_get_logits(tp_ctx* ctx, float* host_out, size_t n);
 
-/* Measures this context's (first owned) stage: t_{fwd+bwd}(l, c) of one job of batch_slice
- * sequences x l tokens with c tokens of context, in ns (median of `reps` after 2 warm-ups). The base
- * curve t(l, 0) is measured for every l = g, 2g, .., s; the context term t_ctx(l, c)
- * is measured on a grid (l in {g 2^k} U {s}, c in multiples of s/8 U {s - l}) and
- * ticks_out[(l/g-1)*(n+1) + c/g] = t(l,0) + t_ctx(l,c) with t_ctx interpolated from the grid
- * (env TP_CTX_FIT=linear: the paper's least-squares t_ctx = a0 + a1 l + a2 c + a3 l c instead,
- * PAPER.md:292-296). n = s/g; caller-owned, n*(n+1) int64. fit_out (may be NULL): the linear fit's
+/* The cost table t_{fwd+bwd}(l, c) of PAPER.md:292-298 for jobs of batch_slice sequences x l tokens
+ * with c tokens of context, in ns (median of `reps` after 2 warm-ups), measured the way tp_step runs
+ * each job (the slice ending at seq_len stores dK/dV, every other one reduce-adds them into its
+ * prefix rows). The base curve t(l, 0) is measured for every l = g, 2g, .., s; the
+ * context term t_ctx(l, c) on a grid (l in {g 2^k} U {s}, c in multiples of s/8 U {s - l}), and
+ * ticks_out[(l/g-1)*(n+1) + c/g] = t(l,0) + t_ctx(l,c) with t_ctx interpolated from the grid (env
+ * TP_CTX_FIT=linear: the paper's least-squares t_ctx = a0 + a1 l + a2 c + a3 l c instead,
+ * PAPER.md:292-296). Every owned stage TYPE is measured (first: embedding + layers; middle: layers;
+ * last: layers + LM head + CE) and the table is their element-wise max (the bottleneck stage,
+ * DESIGN.md A-16); with world > 1 the max is also taken over all ranks (COLLECTIVE: every rank must
+ * call tp_profile with the same arguments). With n_stages > 1 the data-transmission term of
+ * PAPER.md:243 is added to every entry: 2 * (alpha + 4 * hidden * batch_slice * l / beta) (one
+ * fp32 activation forward, one gradient backward), alpha / beta from tp_profile_comm (world > 1) or
+ * the env TP_COMM_ALPHA_NS / TP_COMM_GBS (e.g. to plan a K-GPU pipeline from one GPU); none if
+ * neither is set. n = s/g; caller-owned, n*(n+1) int64. fit_out (may be NULL): the linear fit's
  * a0..a3 (ns, ns/token, ns/token, ns/token^2) and its max relative error on the grid samples (the
- * paper reports < 2%). Parameters must be loaded. */
+ * paper reports < 2%), for the stage type with the largest t(s, 0). Parameters must be loaded. */
 tp_status tp_profile(tp_ctx* ctx, int32_t granularity, int32_t batch_slice, int32_t reps,
                      int64_t* ticks_out, double* fit_out /* [5] */);
+
+/* Time of the deferred weight-gradient GEMMs of one step of `batch` sequences (K = batch * seq_len,
+ * slicing-independent, so not part of the cost table): median of `reps`, ns, for the slowest owned
+ * stage type, max over ranks when world > 1 (COLLECTIVE then). The step latency model is
+ * predicted_ticks of the plan + this constant (the last stage's dW overlaps, the first stage's does
+ * not). */
+tp_status tp_profile_wgrad(tp_ctx* ctx, int32_t batch, int32_t reps, int64_t* ns_out);
+
+/* alpha (ns) and beta (GB/s = bytes/ns) of one stage-to-stage message, measured with
+ * NCCL ping-pongs between neighbouring ranks (median one-way time of a 4 KiB and a large message),
+ * worst over the edges, identical on every rank. COLLECTIVE; requires world > 1 (TP_ESTATE
+ * otherwise). Stored in the context and added by later tp_profile calls. Either output may be
+ * NULL. */
+tp_status tp_profile_comm(tp_ctx* ctx, int32_t reps, double* alpha_ns, double* gbs);
 
 /* The CUDA stream (cudaStream_t) all compute of this context is issued on. */
 tp_status tp_get_stream(tp_ctx* ctx, void** stream_out);

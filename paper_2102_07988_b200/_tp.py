@@ -19,7 +19,7 @@ TP_FLAG_KEEP_LOGITS, TP_FLAG_KERNEL_STATS, TP_FLAG_FORCE_SIMT, TP_FLAG_NCCL_LOOP
 
 EXPORTED = ["tp_plan", "tp_plan_joint", "tp_step_plan", "tp_step_plan_device", "tp_stage_param_count", "tp_nccl_unique_id", "tp_init", "tp_param_count",
             "tp_load_params", "tp_step", "tp_step_device", "tp_get_grads", "tp_get_logits",
-            "tp_profile", "tp_get_stream", "tp_kernel_stats", "tp_kernel_stats_reset", "tp_kernel_stats_enable",
+            "tp_profile", "tp_profile_wgrad", "tp_profile_comm", "tp_get_stream", "tp_kernel_stats", "tp_kernel_stats_reset", "tp_kernel_stats_enable",
             "tp_last_step_launches", "tp_destroy", "tp_last_error"]
 KEXPORTED = ["tpk_gemm", "tpk_attention_fwd", "tpk_attention_bwd"]
 
@@ -76,6 +76,8 @@ def _load() -> C.CDLL:
         "tp_get_grads": (C.c_int, [P, P, C.c_size_t]),
         "tp_get_logits": (C.c_int, [P, P, C.c_size_t]),
         "tp_profile": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, P, P]),
+        "tp_profile_wgrad": (C.c_int, [P, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]),
+        "tp_profile_comm": (C.c_int, [P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "tp_get_stream": (C.c_int, [P, C.POINTER(P)]),
         "tp_kernel_stats": (C.c_int, [P, C.c_int32, C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                       C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
@@ -306,6 +308,18 @@ class Context:
         fit = np.zeros(5, dtype=np.float64)
         _check(_lib.tp_profile(self._h, granularity, batch_slice, reps, ticks.ctypes.data, fit.ctypes.data))
         return ticks, fit
+
+    def profile_wgrad(self, batch: int, reps: int = 3) -> int:
+        """ns of one step's deferred weight-gradient GEMMs (slowest stage type / rank)."""
+        ns = C.c_int64()
+        _check(_lib.tp_profile_wgrad(self._h, batch, reps, C.byref(ns)))
+        return ns.value
+
+    def profile_comm(self, reps: int = 5) -> Tuple[float, float]:
+        """(alpha_ns, GB/s) of one stage message, measured by NCCL ping-pong (collective, world > 1)."""
+        a, b = C.c_double(), C.c_double()
+        _check(_lib.tp_profile_comm(self._h, reps, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def stream(self) -> int:
         p = C.c_void_p()

@@ -170,6 +170,8 @@ struct EngineBase {
   virtual tp_status grads(float* host, size_t n) = 0;
   virtual tp_status logits(float* host, size_t n) = 0;
   virtual tp_status profile(int g, int b, int reps, int64_t* ticks, double* fit) = 0;
+  virtual tp_status profile_wgrad(int batch, int reps, int64_t* ns_out) = 0;
+  virtual tp_status profile_comm(int reps, double* alpha_ns, double* gbs) = 0;
   virtual size_t param_count() const = 0;
   Instr instr;
   cudaStream_t stream = nullptr;
@@ -1023,19 +1025,23 @@ class Engine final : public EngineBase {
     return TP_OK;
   }
   tp_status profile(int g, int b, int reps, int64_t* ticks, double* fit) override;
+  tp_status profile_wgrad(int batch, int reps, int64_t* ns_out) override;
+  tp_status profile_comm(int reps, double* alpha_ns, double* gbs) override;
+  tp_status profile_stage(Stage<T>& S, int g, int bsl, int reps, std::vector<int64_t>& ticks, double* fit);
+  std::vector<int> stage_types() const;
+  double comm_alpha_ns = 0.0, comm_gbs = 0.0;  // tp_profile_comm (0: no transmission term)
 };
 
 // ---------------------------------------------------------------- tp_profile
 // measure t(l, 0) for every l, fit t_ctx(l, c) = a0 + a1 l + a2 c + a3 l c on a
-// subset of (l, c) by least squares, fill the table with t(l, 0) + t_ctx(l, c).
+// subset of (l, c) by least squares, fill the table with t(l, 0) + t_ctx(l, c). Done for every
+// owned stage TYPE (first: embedding + layers, middle: layers, last: layers + head + CE; DESIGN.md
+// A-16) and reduced by element-wise max — over the owned types here, over the ranks with an NCCL
+// max when world > 1 — plus the data-transmission term of PAPER.md:243 when stages talk.
 template <typename T>
-tp_status Engine<T>::profile(int g, int bsl, int reps, int64_t* ticks, double* fit) {
-  if (g < 1 || m.s % g != 0) return fail(TP_EINVAL, "tp_profile: granularity %d must divide seq_len %d", g, m.s);
-  if (reps < 1) return fail(TP_EINVAL, "tp_profile: reps must be >= 1");
-  if (bsl < 1 || bsl > max_batch) return fail(TP_EINVAL, "tp_profile: batch_slice %d not in [1, max_batch]", bsl);
-  if (!ticks) return fail(TP_EINVAL, "tp_profile: null ticks_out");
+tp_status Engine<T>::profile_stage(Stage<T>& S, int g, int bsl, int reps, std::vector<int64_t>& ticks,
+                                   double* fit) {
   const int n = m.s / g;
-  Stage<T>& S = stages[0];
   cudaEvent_t e0, e1;
   CU(cudaEventCreate(&e0));
   CU(cudaEventCreate(&e1));
@@ -1064,8 +1070,6 @@ tp_status Engine<T>::profile(int g, int bsl, int reps, int64_t* ticks, double* f
     *out_ns = 1e6 * v[v.size() / 2];
     return TP_OK;
   };
-  bool saved = instr.on;
-  instr.on = false;
   std::vector<double> base(n + 1, 0.0);
   for (int u = 1; u <= n; ++u) TRY(time_job(u * g, 0, &base[u]));
   // context samples on a grid: l in {g * 2^k} U {s}, c in {0, s/8, 2s/8, ...} U {s - l}
@@ -1087,7 +1091,6 @@ tp_status Engine<T>::profile(int g, int bsl, int reps, int64_t* ticks, double* f
       samp.push_back({(double)lu * g, (double)cu * g, t - base[lu]});
     }
   }
-  instr.on = saved;
   CU(cudaEventDestroy(e0));
   CU(cudaEventDestroy(e1));
   // least squares for a0..a3 via normal equations (4x4, Gaussian elimination with pivoting)
@@ -1101,7 +1104,6 @@ tp_status Engine<T>::profile(int g, int bsl, int reps, int64_t* ticks, double* f
   }
   double coef[4] = {0, 0, 0, 0};
   {
-    int piv[4] = {0, 1, 2, 3};
     bool ok = true;
     for (int col = 0; col < 4 && ok; ++col) {
       int best = col;
@@ -1114,7 +1116,6 @@ tp_status Engine<T>::profile(int g, int bsl, int reps, int64_t* ticks, double* f
         for (int j = 0; j < 5; ++j) A[r][j] -= f * A[col][j];
       }
     }
-    (void)piv;
     if (ok) for (int i = 0; i < 4; ++i) coef[i] = A[i][4] / A[i][i];
   }
   double maxrel = 0.0;
@@ -1137,6 +1138,7 @@ tp_status Engine<T>::profile(int g, int bsl, int reps, int64_t* ticks, double* f
     const double x0 = v[k - 1].first, x1 = v[k].first, y0 = v[k - 1].second, y1 = v[k].second;
     return y0 + (y1 - y0) * (cu - x0) / (x1 - x0);  // extrapolates past the last point
   };
+  ticks.assign((size_t)n * (n + 1), 0);
   for (int lu = 1; lu <= n; ++lu)
     for (int cu = 0; cu + lu <= n; ++cu) {
       const double l = lu * g, c = cu * g;
@@ -1159,6 +1161,194 @@ tp_status Engine<T>::profile(int g, int bsl, int reps, int64_t* ticks, double* f
       ticks[(size_t)(lu - 1) * (n + 1) + cu] = std::max<int64_t>(1, (int64_t)std::llround(base[lu] + tc));
     }
   if (fit) { for (int i = 0; i < 4; ++i) fit[i] = coef[i]; fit[4] = maxrel; }
+  return TP_OK;
+}
+
+// indices (into `stages`) of the first owned stage of each type: first / middle / last (A-16)
+template <typename T>
+std::vector<int> Engine<T>::stage_types() const {
+  std::vector<int> out;
+  int seen = 0;
+  for (size_t i = 0; i < stages.size(); ++i) {
+    const int k = stages[i].k;
+    const int type = (k == 0 ? 1 : 0) | (k == m.K - 1 ? 2 : 0);  // 0 middle, 1 first, 2 last, 3 both
+    if (!(seen & (1 << type))) { seen |= 1 << type; out.push_back((int)i); }
+  }
+  // a middle stage does a subset of the first stage's work (no embedding): skip it when a first
+  // stage is measured too
+  if ((seen & 2) && (seen & 1)) {
+    std::vector<int> kept;
+    for (int i : out) if (stages[i].k == 0 || stages[i].k == m.K - 1) kept.push_back(i);
+    out = kept;
+  }
+  return out;
+}
+
+template <typename T>
+tp_status Engine<T>::profile(int g, int bsl, int reps, int64_t* ticks, double* fit) {
+  if (g < 1 || m.s % g != 0) return fail(TP_EINVAL, "tp_profile: granularity %d must divide seq_len %d", g, m.s);
+  if (reps < 1) return fail(TP_EINVAL, "tp_profile: reps must be >= 1");
+  if (bsl < 1 || bsl > max_batch) return fail(TP_EINVAL, "tp_profile: batch_slice %d not in [1, max_batch]", bsl);
+  if (!ticks) return fail(TP_EINVAL, "tp_profile: null ticks_out");
+  CU(cudaSetDevice(device));
+  const int n = m.s / g;
+  const size_t N = (size_t)n * (n + 1);
+  bool saved = instr.on;
+  instr.on = false;
+  std::vector<int64_t> best(N, 0), t;
+  double best_base = -1.0;
+  for (int si : stage_types()) {
+    double f[5];
+    tp_status st = profile_stage(stages[si], g, bsl, reps, t, f);
+    if (st != TP_OK) { instr.on = saved; return st; }
+    for (size_t i = 0; i < N; ++i) best[i] = std::max(best[i], t[i]);
+    const double tb = (double)t[(size_t)(n - 1) * (n + 1)];  // t(s, 0): the heaviest stage's fit is reported
+    if (tb > best_base) { best_base = tb; if (fit) std::memcpy(fit, f, sizeof f); }
+  }
+  instr.on = saved;
+  // data transmission (t = computation latency + data transmission latency): one fp32
+  // T x H activation forward and one gradient backward per job, t_comm(T) = alpha + 4 H T / beta,
+  // with alpha / beta measured by tp_profile_comm (world > 1) or set by the caller (TP_COMM_ALPHA_NS,
+  // TP_COMM_GBS; e.g. to plan K > 1 stages from one GPU). Loopback without NCCL has no messages.
+  double alpha = comm_alpha_ns, gbs = comm_gbs;
+  if (const char* e = std::getenv("TP_COMM_ALPHA_NS")) alpha = std::atof(e);
+  if (const char* e = std::getenv("TP_COMM_GBS")) gbs = std::atof(e);
+  if (m.K > 1 && gbs > 0) {
+    for (int lu = 1; lu <= n; ++lu) {
+      const double bytes = 4.0 * m.H * (double)bsl * lu * g;
+      const int64_t tc = (int64_t)std::llround(2.0 * (alpha + bytes / gbs));  // GB/s == bytes/ns
+      for (int cu = 0; cu + lu <= n; ++cu) best[(size_t)(lu - 1) * (n + 1) + cu] += tc;
+    }
+  }
+  if (world > 1) {  // bottleneck over the ranks' stages (collective: every rank calls tp_profile)
+    int64_t* d = nullptr;
+    CU(cudaMalloc(&d, N * sizeof(int64_t)));
+    cudaError_t ce = cudaMemcpy(d, best.data(), N * sizeof(int64_t), cudaMemcpyHostToDevice);
+    ncclResult_t nr = ncclSuccess;
+    if (ce == cudaSuccess) nr = ncclAllReduce(d, d, N, ncclInt64, ncclMax, base, stream);
+    if (ce == cudaSuccess && nr == ncclSuccess) ce = cudaStreamSynchronize(stream);
+    if (ce == cudaSuccess && nr == ncclSuccess) ce = cudaMemcpy(best.data(), d, N * sizeof(int64_t), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (nr != ncclSuccess) return fail(TP_ENCCL, "tp_profile: max over ranks: %s", ncclGetErrorString(nr));
+    if (ce != cudaSuccess) return fail(TP_ECUDA, "tp_profile: max over ranks: %s", cudaGetErrorString(ce));
+  }
+  std::memcpy(ticks, best.data(), N * sizeof(int64_t));
+  return TP_OK;
+}
+
+// Deferred weight-gradient GEMMs of one step (slicing-independent, excluded from the table): the
+// time of the slowest owned stage type for `batch` sequences, max over ranks when world > 1.
+template <typename T>
+tp_status Engine<T>::profile_wgrad(int batch, int reps, int64_t* ns_out) {
+  if (batch < 1 || batch > max_batch) return fail(TP_EINVAL, "tp_profile_wgrad: batch %d not in [1, max_batch]", batch);
+  if (reps < 1 || !ns_out) return fail(TP_EINVAL, "tp_profile_wgrad: bad arguments");
+  CU(cudaSetDevice(device));
+  cudaEvent_t e0, e1;
+  CU(cudaEventCreate(&e0));
+  CU(cudaEventCreate(&e1));
+  bool saved = instr.on;
+  instr.on = false;
+  double worst = 0.0;
+  for (int si : stage_types()) {
+    std::vector<float> v;
+    for (int r = 0; r < reps + 1; ++r) {
+      CU(cudaEventRecord(e0, stream));
+      tp_status st = wgrad(stages[si], batch);
+      if (st != TP_OK) { instr.on = saved; return st; }
+      CU(cudaEventRecord(e1, stream));
+      CU(cudaEventSynchronize(e1));
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, e0, e1));
+      if (r >= 1) v.push_back(ms);
+    }
+    std::sort(v.begin(), v.end());
+    worst = std::max(worst, 1e6 * v[v.size() / 2]);
+  }
+  instr.on = saved;
+  CU(cudaEventDestroy(e0));
+  CU(cudaEventDestroy(e1));
+  int64_t t = (int64_t)std::llround(worst);
+  if (world > 1) {
+    int64_t* d = nullptr;
+    CU(cudaMalloc(&d, sizeof(int64_t)));
+    CU(cudaMemcpy(d, &t, sizeof t, cudaMemcpyHostToDevice));
+    NC(ncclAllReduce(d, d, 1, ncclInt64, ncclMax, base, stream));
+    CU(cudaStreamSynchronize(stream));
+    CU(cudaMemcpy(&t, d, sizeof t, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+  }
+  *ns_out = t;
+  return TP_OK;
+}
+
+// alpha / beta of one stage-to-stage message, measured with ncclSend / ncclRecv
+// ping-pongs between neighbouring ranks (edges (0,1), (2,3), .. then (1,2), (3,4), ..): the median
+// one-way time of a small (4 KiB) and a large (the largest job's T x H fp32) message; alpha = t_small,
+// beta = (bytes_large - bytes_small) / (t_large - t_small). Worst (max alpha, min beta) over the
+// edges, identical on every rank; stored in the context and folded into later tp_profile tables.
+template <typename T>
+tp_status Engine<T>::profile_comm(int reps, double* alpha_ns, double* gbs) {
+  if (world < 2) return fail(TP_ESTATE, "tp_profile_comm: needs world > 1 (one stage per GPU)");
+  if (reps < 1) return fail(TP_EINVAL, "tp_profile_comm: reps must be >= 1");
+  CU(cudaSetDevice(device));
+  Stage<T>& S = stages[0];
+  const size_t big = std::min((size_t)max_batch * m.s * m.H, (size_t)64 << 20);  // floats
+  const size_t sizes[2] = {1024, big};
+  double t1[2] = {0.0, 0.0};
+  cudaEvent_t e0, e1;
+  CU(cudaEventCreate(&e0));
+  CU(cudaEventCreate(&e1));
+  double my_alpha = 0.0, my_gbs = 1e30;
+  for (int phase = 0; phase < 2; ++phase) {
+    // this rank's partner in the phase, initiator = the lower rank of the edge
+    int peer = -1;
+    if ((rank & 1) == phase) peer = rank + 1 < world ? rank + 1 : -1;
+    else peer = rank - 1 >= 0 ? rank - 1 : -1;
+    if (phase == 1 && rank == 0) peer = -1;
+    const bool init = peer > rank;
+    for (int z = 0; z < 2; ++z) {
+      std::vector<float> v;
+      for (int r = 0; r < reps + 2 && peer >= 0; ++r) {
+        CU(cudaEventRecord(e0, stream));
+        if (init) {
+          NC(ncclSend(S.grad_out, sizes[z], ncclFloat32, peer, base, stream));
+          NC(ncclRecv(S.grad_out, sizes[z], ncclFloat32, peer, base, stream));
+        } else {
+          NC(ncclRecv(S.grad_out, sizes[z], ncclFloat32, peer, base, stream));
+          NC(ncclSend(S.grad_out, sizes[z], ncclFloat32, peer, base, stream));
+        }
+        CU(cudaEventRecord(e1, stream));
+        CU(cudaEventSynchronize(e1));
+        float ms = 0;
+        CU(cudaEventElapsedTime(&ms, e0, e1));
+        if (r >= 2) v.push_back(ms);
+      }
+      if (!v.empty()) { std::sort(v.begin(), v.end()); t1[z] = 0.5e6 * v[v.size() / 2]; }
+    }
+    if (peer >= 0 && init) {
+      const double a = t1[0];
+      const double b = (double)(sizes[1] - sizes[0]) * 4.0 / std::max(1.0, t1[1] - t1[0]);
+      my_alpha = std::max(my_alpha, a);
+      my_gbs = std::min(my_gbs, b);
+    }
+    // all ranks finish the phase before the next one (a 1-float all-reduce as the barrier)
+    NC(ncclAllReduce(d_loss, d_loss, 1, ncclFloat32, ncclSum, base, stream));
+    CU(cudaStreamSynchronize(stream));
+  }
+  CU(cudaEventDestroy(e0));
+  CU(cudaEventDestroy(e1));
+  double* d = nullptr;
+  double h[2] = {my_alpha, -my_gbs};
+  CU(cudaMalloc(&d, 2 * sizeof(double)));
+  CU(cudaMemcpy(d, h, sizeof h, cudaMemcpyHostToDevice));
+  NC(ncclAllReduce(d, d, 2, ncclFloat64, ncclMax, base, stream));
+  CU(cudaStreamSynchronize(stream));
+  CU(cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  comm_alpha_ns = h[0];
+  comm_gbs = -h[1];
+  if (alpha_ns) *alpha_ns = comm_alpha_ns;
+  if (gbs) *gbs = comm_gbs;
   return TP_OK;
 }
 
@@ -1263,6 +1453,14 @@ extern "C" tp_status tp_profile(tp_ctx* ctx, int32_t g, int32_t batch_slice, int
                                 double* fit) {
   TP_CHECK_ARG(ctx, "tp_profile: null ctx");
   return ctx->eng->profile(g, batch_slice, reps, ticks, fit);
+}
+extern "C" tp_status tp_profile_wgrad(tp_ctx* ctx, int32_t batch, int32_t reps, int64_t* ns_out) {
+  TP_CHECK_ARG(ctx, "tp_profile_wgrad: null ctx");
+  return ctx->eng->profile_wgrad(batch, reps, ns_out);
+}
+extern "C" tp_status tp_profile_comm(tp_ctx* ctx, int32_t reps, double* alpha_ns, double* gbs) {
+  TP_CHECK_ARG(ctx, "tp_profile_comm: null ctx");
+  return ctx->eng->profile_comm(reps, alpha_ns, gbs);
 }
 extern "C" tp_status tp_get_stream(tp_ctx* ctx, void** out) {
   TP_CHECK_ARG(ctx && out, "tp_get_stream: null argument");

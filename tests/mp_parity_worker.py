@@ -51,6 +51,14 @@ def main():
         errs["logits"] = rel(ctx.logits(B), ref["logits"])
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
         json.dump(errs, f)
+    if os.environ.get("TP_TEST_PROFILE") == "1":
+        # collective profiling calls: alpha / beta by NCCL ping-pong, the bottleneck table (max over
+        # ranks inside the library), the dW constant — identical on every rank
+        a, gbs = ctx.profile_comm(reps=3)
+        t, _ = ctx.profile(16, reps=3)
+        w = ctx.profile_wgrad(B, reps=2)
+        with open(os.path.join(out_dir, f"rank{rank}_prof.json"), "w") as f:
+            json.dump({"alpha_ns": a, "gbs": gbs, "table": t.tolist(), "wgrad": w}, f)
     ctx.close()
     dist.destroy_process_group()
 

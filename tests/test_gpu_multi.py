@@ -37,6 +37,19 @@ def test_small_two_stages_nccl_side_stream_dw(tmp_path):
         assert max(errs.values()) < 2e-2, errs
 
 
+def test_profile_collectives_two_ranks(tmp_path):
+    """tp_profile_comm (NCCL ping-pong alpha / beta), tp_profile (bottleneck table: max
+    over the ranks' stages inside the library, A-16, plus the transmission term) and
+    tp_profile_wgrad give identical results on every rank."""
+    import json as _json
+    run(2, "small", "bf16", "40,24,64", tmp_path, env={"TP_TEST_PROFILE": "1"})
+    p = [_json.load(open(tmp_path / f"rank{k}_prof.json")) for k in range(2)]
+    assert p[0] == p[1]
+    assert 0 < p[0]["alpha_ns"] < 1e6 and 1.0 < p[0]["gbs"] < 5000.0
+    t = np.array(p[0]["table"])
+    assert (t[:, 0] > 0).all()
+
+
 def test_small_four_stages_nccl(tmp_path):
     for errs in run(4, "small", "bf16", "40,24,64", tmp_path):
         assert max(errs.values()) < 2e-2, errs

@@ -256,3 +256,34 @@ def test_tiny_measured_table_vs_2pow31_brute_force():
                                           timeout=600).stdout.split()]
     s = tp.plan(ticks, 1, TINY.n_layer, TINY.hidden, n, 2)
     assert (s.predicted, s.t_max, s.lengths) == (out[0], out[1], out[3:3 + out[2]])
+
+
+def test_profile_stage_types_comm_term_and_wgrad(monkeypatch):
+    """tp_profile over a K = 2 loopback context measures both stage types (first: embedding, last:
+    LM head + CE) and returns their element-wise max (A-16); TP_COMM_ALPHA_NS / TP_COMM_GBS add the
+    transmission term 2 (alpha + 4 H b l / beta) of PAPER.md:243 to every entry; tp_profile_wgrad
+    times the slicing-independent dW GEMMs; tp_profile_comm needs world > 1."""
+    cfg = SMALL.with_(n_stages=2)
+    params, tokens, _ = oracle_run(cfg, 2, 9, True)
+    from synth import pack_all_stages
+    ctx = tp.Context(cfg, precision=tp.TP_BF16, max_batch=2, device=0)
+    try:
+        ctx.load_params(pack_all_stages(params, cfg))
+        g, b = 32, 2
+        t0, _ = ctx.profile(g, reps=5, batch_slice=b)
+        alpha, gbs = 2.0e6, 0.5  # 2 ms + 0.5 GB/s: far above the measurement noise
+        monkeypatch.setenv("TP_COMM_ALPHA_NS", str(alpha))
+        monkeypatch.setenv("TP_COMM_GBS", str(gbs))
+        t1, _ = ctx.profile(g, reps=5, batch_slice=b)
+        n = cfg.seq_len // g
+        for lu in range(1, n + 1):
+            want = 2.0 * (alpha + 4.0 * cfg.hidden * b * lu * g / gbs)
+            got = t1[lu - 1, 0] - t0[lu - 1, 0]
+            assert abs(got - want) < 0.05 * want, (lu, got, want)
+        w = ctx.profile_wgrad(2, reps=3)
+        assert 0 < w < 1e9
+        with pytest.raises(tp.TpError) as e:
+            ctx.profile_comm()
+        assert e.value.status == tp.TP_ESTATE
+    finally:
+        ctx.close()
