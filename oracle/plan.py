@@ -24,7 +24,7 @@ flow-shop simulation (SPEC.md:253-264 examples and random vectors); epsilon gap 
 from __future__ import annotations
 
 import itertools
-from typing import Iterable, List, Optional, Sequence, Tuple
+from typing import Dict, Iterable, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -290,3 +290,94 @@ def oplist_makespan(tf: Sequence[Sequence[float]], tb: Sequence[Sequence[float]]
             bend[k][j] = st + tb[k][j]
             free[k] = bend[k][j]
     return max(free)
+
+
+def gpipe_oplists(groups: Sequence[int], K: int) -> List[List[Tuple[str, int]]]:
+    """GPipe order (reading A-21): every stage runs F of all jobs in order, then B in exact reverse.
+    groups[d] = number of token-slice jobs of group d; jobs are numbered group-major."""
+    J = sum(groups)
+    ops = [("F", j) for j in range(J)] + [("B", j) for j in reversed(range(J))]
+    return [list(ops) for _ in range(K)]
+
+
+def one_f_one_b_oplists(groups: Sequence[int], K: int) -> List[List[Tuple[str, int]]]:
+    """1F1B at sequence (group) granularity (north star "1F1B-style", DESIGN.md
+    A-21: inside one group the backward of its last slice needs every forward, so the unit that
+    interleaves is the group): stage k first runs the forwards of w_k = min(D, K - k) groups (the
+    warm-up), then alternates the backward of its oldest in-flight group (slices in reverse) with
+    the forward of the next group, then drains the remaining backwards. Each stage holds at most
+    w_k groups' activations (the memory bound the schedule exists for)."""
+    D = len(groups)
+    first = [sum(groups[:d]) for d in range(D)]
+    F = lambda d: [("F", first[d] + i) for i in range(groups[d])]
+    Bk = lambda d: [("B", first[d] + i) for i in reversed(range(groups[d]))]
+    out = []
+    for k in range(K):
+        w = min(D, K - k)
+        ops: List[Tuple[str, int]] = []
+        for d in range(w):
+            ops += F(d)
+        for d in range(D):
+            ops += Bk(d)
+            if d + w < D:
+                ops += F(d + w)
+        out.append(ops)
+    return out
+
+
+def oplist_replay(oplists: Sequence[Sequence[Tuple[str, int]]], tf: Sequence[Sequence[float]],
+                  tb: Sequence[Sequence[float]], comm: float = 0.0) -> float:
+    """Replays arbitrary per-stage op lists with the pipeline's data dependencies: F(j) on stage k
+    starts after F(j) on k-1 (+ comm), B(j) on stage k after B(j) on k+1 (+ comm), B(j) on the last
+    stage after its own F(j); each stage executes its list in order, one op at a time. Returns the
+    makespan; raises ValueError on a deadlocking order. tf[k][j], tb[k][j]: per-stage durations."""
+    K = len(oplists)
+    end: Dict[Tuple[str, int, int], float] = {}
+    pos = [0] * K
+    free = [0.0] * K
+    remaining = sum(len(o) for o in oplists)
+    while remaining:
+        progressed = False
+        for k in range(K):
+            while pos[k] < len(oplists[k]):
+                kind, j = oplists[k][pos[k]]
+                if kind == "F":
+                    dep = ("F", k - 1, j) if k > 0 else None
+                    extra = comm if k > 0 else 0.0
+                else:
+                    dep = ("B", k + 1, j) if k < K - 1 else ("F", k, j)
+                    extra = comm if k < K - 1 else 0.0
+                if dep is not None and dep not in end:
+                    break
+                ready = end[dep] + extra if dep is not None else 0.0
+                st = max(free[k], ready)
+                free[k] = st + (tf[k][j] if kind == "F" else tb[k][j])
+                end[(kind, k, j)] = free[k]
+                pos[k] += 1
+                remaining -= 1
+                progressed = True
+        if not progressed:
+            raise ValueError("op lists deadlock")
+    return max(free)
+
+
+def max_inflight_groups(oplists: Sequence[Sequence[Tuple[str, int]]], groups: Sequence[int]) -> List[int]:
+    """Per stage: the largest number of groups whose forward has started and whose backward has not
+    finished (the activation-memory footprint of the schedule, in groups)."""
+    gid = [d for d, m in enumerate(groups) for _ in range(m)]
+    out = []
+    for ops in oplists:
+        started, done_b = set(), {}
+        live = peak = 0
+        for kind, j in ops:
+            d = gid[j]
+            if kind == "F" and d not in started:
+                started.add(d)
+                live += 1
+            if kind == "B":
+                done_b[d] = done_b.get(d, 0) + 1
+                if done_b[d] == groups[d]:
+                    live -= 1
+            peak = max(peak, live)
+        out.append(peak)
+    return out

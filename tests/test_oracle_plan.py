@@ -180,3 +180,51 @@ def test_joint_reduces_to_uniform_objective():
     T, plan = joint_optimize({b: t}, n, B, K)
     T_u, _, lengths = op.optimize(t, n, K, D=B // b)
     assert T == T_u and [x for x, _ in plan] == [b, b]
+
+
+# ---------------------------------------------------------------- op-list schedules (GPipe, 1F1B)
+def test_generic_replay_equals_gpipe_replay():
+    rng = np.random.default_rng(17)
+    for _ in range(100):
+        K, J = int(rng.integers(1, 6)), int(rng.integers(1, 9))
+        tf = rng.uniform(0.5, 3.0, size=(K, J)).tolist()
+        tb = rng.uniform(0.5, 3.0, size=(K, J)).tolist()
+        comm = float(rng.uniform(0, 0.5))
+        assert abs(op.oplist_replay(op.gpipe_oplists([J], K), tf, tb, comm) -
+                   op.oplist_makespan(tf, tb, comm)) < 1e-9
+
+
+def test_1f1b_textbook_closed_form():
+    """One job per group (microbatch) and uniform durations: 1F1B's makespan is the textbook
+    (D + K - 1)(t_f + t_b) (the same bubble as GPipe), and stage k holds min(D, K - k) groups."""
+    for K in range(1, 6):
+        for D in range(1, 9):
+            tf, tb = 1.0, 2.0
+            ops = op.one_f_one_b_oplists([1] * D, K)
+            ms = op.oplist_replay(ops, [[tf] * D] * K, [[tb] * D] * K)
+            assert abs(ms - (D + K - 1) * (tf + tb)) < 1e-9, (K, D, ms)
+            assert op.max_inflight_groups(ops, [1] * D) == [min(D, K - k) for k in range(K)]
+            assert op.max_inflight_groups(op.gpipe_oplists([1] * D, K), [1] * D) == [D] * K
+
+
+def test_1f1b_single_group_is_gpipe_and_lists_are_permutations():
+    rng = np.random.default_rng(5)
+    for _ in range(50):
+        K = int(rng.integers(1, 6))
+        groups = [int(x) for x in rng.integers(1, 5, size=int(rng.integers(1, 6)))]
+        a, b = op.one_f_one_b_oplists(groups, K), op.gpipe_oplists(groups, K)
+        for x, y in zip(a, b):
+            assert sorted(x) == sorted(y)
+        if len(groups) == 1:
+            assert a == b
+        J = sum(groups)
+        tf = rng.uniform(0.5, 2.0, size=(K, J)).tolist()
+        tb = rng.uniform(0.5, 2.0, size=(K, J)).tolist()
+        ms = op.oplist_replay(a, tf, tb)           # never deadlocks
+        lower = max(sum(tf[k]) + sum(tb[k]) for k in range(K))
+        assert ms >= lower - 1e-9
+
+
+def test_replay_detects_deadlock():
+    with pytest.raises(ValueError):
+        op.oplist_replay([[("B", 0), ("F", 0)], [("F", 0), ("B", 0)]], [[1.0], [1.0]], [[1.0], [1.0]])
