@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                           const __grid_constant__ CUtensorMap tmdQ, const __grid_constant__ CUtensorMap tmdK,
                           const __grid_constant__ CUtensorMap tmdV, const float* __restrict__ ldg, int s, int c, int l,
                           float scale, float scale_log2, int accumulate, int nheads, volatile int* dbg,
-                          long long* trace, float* __restrict__ dq_acc, int dq_mode) {
+                          long long* trace, int pf_dist) {
   extern __shared__ uint8_t smem_raw[];
 #define DBG(role, v)                                                                    \
   do {                                                                                  \
@@ -546,6 +546,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       tma_load_4d(qd + QHALF, &tmQ, 64, c + qt * BQB, head, sq, qfull + b);
       tma_load_3d(od, &tmdO, head * AT, qt * BQB, sq, qfull + b);
       tma_load_3d(od + QHALF, &tmdO, head * AT + 64, qt * BQB, sq, qfull + b);
+      // the ring is only NQB deep and a tile's slot frees late (its dV / dK MMAs): pull the tile
+      // pf_dist ahead into L2 now so its TMA load later is an L2 hit, not a DRAM round trip
+      if (pf_dist > 0 && i + pf_dist < ntile) {
+        const int qp = qt + pf_dist;
+        tma_prefetch_4d(&tmQ, 0, c + qp * BQB, head, sq);
+        tma_prefetch_4d(&tmQ, 64, c + qp * BQB, head, sq);
+        tma_prefetch_3d(&tmdO, head * AT, qp * BQB, sq);
+        tma_prefetch_3d(&tmdO, head * AT + 64, qp * BQB, sq);
+      }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (whole warp, warp-uniform control flow; one elected lane issues)
@@ -632,72 +641,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     float* dqs = reinterpret_cast<float*>(sm + BwdSmem::DQ);
     const bool leader = threadIdx.x == 320;
-    if (dq_mode != 0) {
-      // dQ^T -> registers -> fp32 L2 reductions straight into dq_acc [seq][l][H] (no shared-memory
-      // staging: the backward is shared-memory-bandwidth bound, and the staging tile cost 64 KB of
-      // smem traffic per tile: the drain's writes plus the TMA's reads)
-      const int H = nheads * AT;
-      float* base = dq_acc + (int64_t)sq * l * H + head * AT;
-      for (int j = 0; j < ntile; ++j) {
-        const int bb = j & 1;
-        const int qr0 = (qt0 + j) * BQB;
-        mbar_wait(dqfull + bb, (j >> 1) & 1);
-        tc_fence_after();
-        uint32_t r[2][32];
-        tmem_ld32_nowait(lane_base + bb * 128 + 64, r[0]);
-        tmem_ld32_nowait(lane_base + bb * 128 + 96, r[1]);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(dqfree + bb);
-        if (dq_mode == 1) {
-          // thread = head-dim index `row`, 64 query columns: a warp's 32 lanes cover 32 consecutive
-          // floats of one dq_acc row per instruction (one 128-byte L2 reduction)
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int t = 0; t < 32; ++t) {
-              const int qr = qr0 + h * 32 + t;
-              if (qr < l)
-                asm volatile("red.global.add.f32 [%0], %1;" ::"l"(base + (int64_t)qr * H + row),
-                             "f"(__uint_as_float(r[h][t]) * scale) : "memory");
-            }
-        } else {
-          // 4 x 4 transposes inside lane quads: lane 4g + i ends up with queries 4m + i of head dims
-          // 4g .. 4g + 3 -> one 16-byte vector reduction per (query, quad)
-          const int i4 = lane & 3;
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int m4 = 0; m4 < 8; ++m4) {
-              // v_e = dQ[query 4 m4 + e][dim = lane]; want w_k = dQ[query 4 m4 + i4][dim 4 g + k]
-              const float v0 = __uint_as_float(r[h][m4 * 4 + 0]) * scale, v1 = __uint_as_float(r[h][m4 * 4 + 1]) * scale;
-              const float v2 = __uint_as_float(r[h][m4 * 4 + 2]) * scale, v3 = __uint_as_float(r[h][m4 * 4 + 3]) * scale;
-              float w0 = 0.f, w1 = 0.f, w2 = 0.f, w3 = 0.f;
-              // rotation-based quad transpose: in round k a lane sends v_{(i4 + k) & 3} (destined to the
-              // lane whose query index that is) and receives, from lane i4' = (i4 - k) & 3, that lane's
-              // v_{i4} = dQ[4 m4 + i4][dim 4 g + i4']
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int js = (i4 + k) & 3;
-                const float send = js == 0 ? v0 : js == 1 ? v1 : js == 2 ? v2 : v3;
-                const int kk = (i4 - k) & 3;
-                const float got = __shfl_sync(0xffffffffu, send, (lane & ~3) | kk);
-                w0 = kk == 0 ? got : w0;
-                w1 = kk == 1 ? got : w1;
-                w2 = kk == 2 ? got : w2;
-                w3 = kk == 3 ? got : w3;
-              }
-              const int qr = qr0 + h * 32 + m4 * 4 + i4;
-              if (qr < l) {
-                float* d = base + (int64_t)qr * H + (lane & ~3);
-                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d), "f"(w0), "f"(w1), "f"(w2),
-                             "f"(w3) : "memory");
-              }
-            }
-        }
-      }
-    } else
     for (int j = 0; j < ntile; ++j) {
       const int bb = j & 1;
       if (leader) tma_wait_reads();  // the previous reduce has finished reading the staging tile
@@ -1023,13 +966,13 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
   static long long* trace = nullptr;
   if (trace_left > 0 && !trace) cudaMalloc(&trace, 4 * 8 * 64 * sizeof(long long));
   if (trace_left > 0) cudaMemsetAsync(trace, 0, 4 * 8 * 64 * sizeof(long long), st);
-  // dQ drain: 2 = register quad transpose + 16-byte L2 vector reductions (default), 1 = scalar L2
-  // reductions, 0 = smem staging tile + TMA bulk reduce-add (env TP_ATTN_DQ)
-  const int dq_mode = getenv("TP_ATTN_DQ") ? atoi(getenv("TP_ATTN_DQ")) : 2;
+  // L2 prefetch distance of the Q / dO tiles, in tiles ahead of the TMA load (env TP_ATTN_PF; default
+  // off: distances 1-4 measured neutral at c = 576, l = 1472, 128 heads, 565-567 us — the kernel is
+  // bound by shared-memory bandwidth, ~288 KB per 128 x 64 tile, not by load latency)
+  static const int pf_dist = getenv("TP_ATTN_PF") ? atoi(getenv("TP_ATTN_PF")) : 0;
   attn_bwd_sm100_kernel<<<grid, BWD_THREADS, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, mdq, mdk, mdv, Dvec,
                                                            s, c, l, scale, scale * LOG2E_F, accumulate,
-                                                           a, dbg_dev, trace_left > 0 ? trace : nullptr, dq_acc,
-                                                           dq_mode);
+                                                           a, dbg_dev, trace_left > 0 ? trace : nullptr, pf_dist);
   e = cudaGetLastError();
   if (trace_left > 0) {
     --trace_left;
