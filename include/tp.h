@@ -59,11 +59,19 @@ enum { TP_BF16 = 0, /* bf16 GEMM/attention operands, fp32 accumulation, fp32 res
 enum { TP_FLAG_KEEP_LOGITS = 1,   /* keep fp32 logits of the last step for tp_get_logits     */
        TP_FLAG_KERNEL_STATS = 2,  /* bracket launches with CUDA events (tp_kernel_stats)      */
        TP_FLAG_FORCE_SIMT = 4,    /* bf16 mode: use SIMT GEMM/attention (kernel cross-checks)  */
-       TP_FLAG_NCCL_LOOPBACK = 8  /* world == 1, n_stages > 1: send every stage message through
+       TP_FLAG_NCCL_LOOPBACK = 8, /* world == 1, n_stages > 1: send every stage message through
                                      ncclSend/ncclRecv to self on a one-rank communicator (grouped
                                      per message, on the same per-direction comm streams, NCCL
                                      communicators and events as world == n_stages) instead of
-                                     aliasing the buffers; lets the p2p path run on one GPU        */ };
+                                     aliasing the buffers; lets the p2p path run on one GPU        */
+       TP_FLAG_DEVICE_P2P = 16    /* world == n_stages > 1: device-initiated messages instead of
+                                     ncclSend/ncclRecv — each stage's receive buffers are NCCL
+                                     symmetric windows (ncclMemAlloc + ncclCommWindowRegister); the
+                                     last layer's FC2 epilogue and the first layer's LayerNorm
+                                     backward write straight into the neighbour's buffer over
+                                     NVLink, a release-store flag per job signals it, the consumer
+                                     spins on its flag before the job; env
+                                     TP_DEVICE_P2P=1 sets it too                                   */ };
 
 /* Model shape. n_layer % n_stages == 0; hidden % n_head == 0; head_dim = hidden / n_head must be
  * a multiple of 16 and <= 128; hidden % 64 == 0; seq_len >= 1. */

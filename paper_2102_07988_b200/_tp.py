@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libtp.so")
 
 TP_OK, TP_EINVAL, TP_EINFEASIBLE, TP_ETOOBIG, TP_ECUDA, TP_ENCCL, TP_ENOMEM, TP_ESTATE = 0, -1, -2, -3, -4, -5, -6, -7
 TP_BF16, TP_FP32 = 0, 1
-TP_FLAG_KEEP_LOGITS, TP_FLAG_KERNEL_STATS, TP_FLAG_FORCE_SIMT, TP_FLAG_NCCL_LOOPBACK = 1, 2, 4, 8
+TP_FLAG_KEEP_LOGITS, TP_FLAG_KERNEL_STATS, TP_FLAG_FORCE_SIMT, TP_FLAG_NCCL_LOOPBACK, TP_FLAG_DEVICE_P2P = 1, 2, 4, 8, 16
 
 EXPORTED = ["tp_plan", "tp_plan_joint", "tp_step_plan", "tp_step_plan_device", "tp_stage_param_count", "tp_nccl_unique_id", "tp_init", "tp_param_count",
             "tp_load_params", "tp_step", "tp_step_device", "tp_get_grads", "tp_get_logits",

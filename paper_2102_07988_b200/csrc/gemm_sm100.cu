@@ -24,6 +24,7 @@
 
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "kernels.h"
 #include "tc5.cuh"
@@ -101,7 +102,158 @@ __device__ __forceinline__ void tile_mn(int tile, int m_tiles, int n_tiles, int 
   mt = first + w % rows;
   nt = w / rows;
 }
-template <int CG, int BN, bool A_MN, bool B_MN, int WN = 1>
+// One output tile's fused epilogue for this warp (TMEM lane quarter q, column chunks [ch0, ch1)),
+// specialised on the epilogue kind. mode 0: TMEM -> fused epilogue; 1: TMEM -> raw fp32 partial to
+// `wsp`; 2: sum of the S stream-K partials at `wsp` (stride 128 * TILE_N * CG per part) -> fused
+// epilogue. Per-column work (bias, the QKV column -> (part, head, dim) decode) is done once per
+// 32-column chunk and per-row work (the QKV row -> (sequence, position) decode) once per tile, so
+// the inner loop is loads, math and stores only.
+template <int KIND, int CG, int TILE_N, int BN>
+__device__ __forceinline__ void epi_tile(const Epi& epi, const SplitK& sk, float* scr, uint32_t tmem_base, int acc, int q,
+                                         int lane, int ch0, int ch1, int M, int N, int mode, int m0, int n0, float* wsp,
+                                         bool has_dbias) {
+  constexpr bool AUX = KIND == EPI_RESID || KIND == EPI_DGELU;
+  constexpr bool BIAS = KIND == EPI_STORE || KIND == EPI_RESID || KIND == EPI_GELU || KIND == EPI_QKV;
+  int rows[4];
+  int64_t qoff[4];  // QKV: sequence / position offset of each of the thread's 4 rows
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    rows[it] = m0 + q * 32 + it * 8 + (lane >> 2);
+    qoff[it] = 0;
+    if constexpr (KIND == EPI_QKV) {
+      const int sq = rows[it] % epi.bs, pos = epi.row0 + rows[it] / epi.bs;
+      qoff[it] = (int64_t)sq * epi.s_len * epi.hidden + (int64_t)pos * epi.head_dim;
+    }
+  }
+#pragma unroll 1
+  for (int ch = ch0; ch < ch1; ++ch) {
+    const int n = n0 + ch * 32 + (lane & 3) * 8;
+    const int nc = n + epi.n_off;  // column in the epilogue's column space
+    const bool nok = n < N;
+    float aux[4][8];
+    if constexpr (AUX) {
+      if (mode != 1) {
+#pragma unroll
+        for (int it = 0; it < 4; ++it)
+          if (rows[it] < M && nok) epi_prefetch8<bf16>(epi, rows[it], nc, aux[it]);
+      }
+    }
+    float bias[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if constexpr (BIAS) {
+      if (mode != 1 && nok && epi.bias) load8<float>(epi.bias + nc, bias);
+    }
+    bf16* qkv_col = nullptr;
+    if constexpr (KIND == EPI_QKV) {
+      const int part = nc / epi.hidden;
+      const int within = nc - part * epi.hidden;
+      const int head = within / epi.head_dim;
+      const int dd = within - head * epi.head_dim;
+      qkv_col = reinterpret_cast<bf16*>(part == 0 ? epi.q : (part == 1 ? epi.k : epi.v)) +
+                (int64_t)head * epi.s_len * epi.head_dim + dd;
+    }
+    // the tile's 32 x 32 chunk lands in the warp's padded smem scratch: from TMEM (modes 0, 1) or
+    // as the sum of the stream-K partials (mode 2)
+    if (mode != 2) {
+      uint32_t r[32];
+      tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 32, r);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) scr[lane * 33 + i] = __uint_as_float(r[i]);
+    } else {
+#pragma unroll 1
+      for (int it = 0; it < 4; ++it) {
+        const int rr = it * 8 + (lane >> 2);
+        const int64_t woff = (int64_t)(q * 32 + rr) * TILE_N + (ch * 32 + (lane & 3) * 8);
+        float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int p = 0; p < sk.S; ++p) {
+          float w[8];
+          load8<float>(wsp + (int64_t)p * CG * 128 * TILE_N + woff, w);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] += w[i];
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) scr[rr * 33 + (lane & 3) * 8 + i] = v[i];
+      }
+    }
+    __syncwarp();
+    if (mode == 1) {  // raw fp32 partial of this K-part to the workspace
+#pragma unroll 1
+      for (int it = 0; it < 4; ++it) {
+        const int rr = it * 8 + (lane >> 2);
+        const int64_t woff = (int64_t)(q * 32 + rr) * TILE_N + (ch * 32 + (lane & 3) * 8);
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = scr[rr * 33 + (lane & 3) * 8 + i];
+        if (rows[it] < M && nok) store8<float>(wsp + woff, v);
+      }
+      __syncwarp();
+      continue;
+    }
+    float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // column sums (Epi::dbias)
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int rr = it * 8 + (lane >> 2);
+      const int row = rows[it];
+      if (row >= M || !nok) continue;
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = scr[rr * 33 + (lane & 3) * 8 + i] + bias[i];
+      if constexpr (KIND == EPI_STORE) {
+        if (epi.out_f32) store8<float>(reinterpret_cast<float*>(epi.out) + (int64_t)row * epi.ldo + nc, v);
+        else store8<bf16>(reinterpret_cast<bf16*>(epi.out) + (int64_t)row * epi.ldo + nc, v);
+      } else if constexpr (KIND == EPI_RESID) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] += aux[it][i];
+        store8<float>(reinterpret_cast<float*>(epi.out) + (int64_t)row * epi.ldo + nc, v);
+      } else if constexpr (KIND == EPI_GELU) {
+        float u[8], g[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) u[i] = to_f<bf16>(from_f<bf16>(v[i]));
+#pragma unroll
+        for (int i = 0; i < 8; ++i) g[i] = gelu_f<bf16>(u[i]);
+        store8<bf16>(reinterpret_cast<bf16*>(epi.out) + (int64_t)row * epi.ldo + nc, u);
+        store8<bf16>(reinterpret_cast<bf16*>(epi.out2) + (int64_t)row * epi.ldo2 + nc, g);
+      } else if constexpr (KIND == EPI_DGELU) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] *= gelu_grad_f<bf16>(aux[it][i]);
+        store8<bf16>(reinterpret_cast<bf16*>(epi.out) + (int64_t)row * epi.ldo + nc, v);
+        if (has_dbias)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) cs[i] += v[i];
+      } else if constexpr (KIND == EPI_QKV) {
+        store8<bf16>(qkv_col + qoff[it], v);
+      } else {  // EPI_ACCUM
+        float* o = reinterpret_cast<float*>(epi.out) + (int64_t)row * epi.ldo + nc;
+        float r0[8];
+        load8<float>(o, r0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r0[i] += v[i];
+        store8<float>(o, r0);
+      }
+    }
+    if constexpr (KIND == EPI_DGELU) {
+      if (has_dbias) {  // the 8 lanes holding the same 8 columns reduce the warp's 32 rows
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 4);
+          cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 8);
+          cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 16);
+        }
+        if (lane < 4 && nok) {
+          float* d = epi.dbias + nc;
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d), "f"(cs[0]), "f"(cs[1]),
+                       "f"(cs[2]), "f"(cs[3]) : "memory");
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d + 4), "f"(cs[4]), "f"(cs[5]),
+                       "f"(cs[6]), "f"(cs[7]) : "memory");
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// KIND: the epilogue (Epi::kind), a template parameter so each kernel compiles only its own
+// epilogue (a runtime switch over all kinds in one kernel made ptxas spill the hot epilogue loop)
+template <int CG, int BN, bool A_MN, bool B_MN, int WN, int KIND>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                       int K, Epi epi, SplitK sk, int group_m) {
@@ -240,76 +392,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // TMEM (thread = row) -> padded smem transpose -> 4 lanes per row, 8 columns each: every
     // global access of the fused epilogue is a 64/128-byte contiguous row segment.
     float* scr = epi_scratch + (warp - 2) * 32 * 33;
-    const bool has_aux = epi.kind == EPI_RESID || epi.kind == EPI_DGELU;
     const bool has_dbias = epi.kind == EPI_DGELU && epi.dbias != nullptr;
     const int ch0 = ((warp - 2) >> 2) * (C::TILE_N / 64), ch1 = ch0 + C::TILE_N / 64;
-    // mode 0: TMEM -> fused epilogue; 1: TMEM -> raw fp32 partial to `wsp`; 2: sum of the S partials
-    // at `wsp` (stride 128 * TILE_N * CG per part) -> fused epilogue
-    auto chunk = [&](int ch, int mode, int m0, int n0, float* wsp) {
-      const int n = n0 + ch * 32 + (lane & 3) * 8;
-      // issue this chunk's residual / U loads first: 4 independent 32-byte loads in flight per thread
-      float aux[4][8];
-      if (mode != 1 && has_aux) {
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          const int row = m0 + q * 32 + it * 8 + (lane >> 2);
-          if (row < M && n < N) epi_prefetch8<bf16>(epi, row, n + epi.n_off, aux[it]);
-        }
-      }
-      if (mode != 2) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 32, r);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) scr[lane * 33 + i] = __uint_as_float(r[i]);
-        __syncwarp();
-      }
-      float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // column sums (Epi::dbias)
-#pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        const int rr = it * 8 + (lane >> 2);
-        const int row = m0 + q * 32 + rr;
-        const int64_t woff = (int64_t)(q * 32 + rr) * C::TILE_N + (ch * 32 + (lane & 3) * 8);
-        float v[8];
-        if (mode != 2) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = scr[rr * 33 + (lane & 3) * 8 + i];
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = 0.f;
-          for (int p = 0; p < sk.S; ++p) {
-            float w[8];
-            load8<float>(wsp + (int64_t)p * CG * 128 * C::TILE_N + woff, w);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) v[i] += w[i];
-          }
-        }
-        if (row < M && n < N) {
-          if (mode == 1) {
-            store8<float>(wsp + woff, v);
-          } else {
-            epi_apply8<bf16>(epi, row, n + epi.n_off, v, aux[it]);
-            if (has_dbias)
-#pragma unroll
-              for (int i = 0; i < 8; ++i) cs[i] += v[i];
-          }
-        }
-      }
-      if (mode != 1 && has_dbias) {  // the 8 lanes holding the same 8 columns (lane bits 2-4) reduce the warp's 32 rows
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 4);
-          cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 8);
-          cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 16);
-        }
-        if (lane < 4 && n < N) {
-          float* d = epi.dbias + n + epi.n_off;
-          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d), "f"(cs[0]), "f"(cs[1]), "f"(cs[2]),
-                       "f"(cs[3]) : "memory");
-          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d + 4), "f"(cs[4]), "f"(cs[5]),
-                       "f"(cs[6]), "f"(cs[7]) : "memory");
-        }
-      }
-      __syncwarp();
+    auto tile_epilogue = [&](int mode, int m0, int n0, float* wsp) {
+      epi_tile<KIND, CG, C::TILE_N, BN>(epi, sk, scr, tmem_base, acc, q, lane, ch0, ch1, M, N, mode, m0, n0, wsp, has_dbias);
     };
     int tile, k0, k1, part;
     for (int item = 0; gemm_item(item, unit, nunits, tiles, kbs, sk, tile, k0, k1, part); ++item) {
@@ -319,9 +405,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
       float* wst = part < 0 ? nullptr : sk.ws + ((int64_t)(tile - sk.dp_tiles) * sk.S * CG + crank) * 128 * C::TILE_N;
-#pragma unroll 1
-      for (int ch = ch0; ch < ch1; ++ch)
-        chunk(ch, part < 0 ? 0 : 1, m0, n0, part < 0 ? nullptr : wst + (int64_t)part * CG * 128 * C::TILE_N);
+      tile_epilogue(part < 0 ? 0 : 1, m0, n0, part < 0 ? nullptr : wst + (int64_t)part * CG * 128 * C::TILE_N);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -338,8 +422,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         named_bar(1, 256);
         if (*sk_ticket == sk.S - 1) {
           __threadfence();
-#pragma unroll 1
-          for (int ch = ch0; ch < ch1; ++ch) chunk(ch, 2, m0, n0, wst);
+          tile_epilogue(2, m0, n0, wst);
           if (threadIdx.x == 64) *cnt = 0;
         }
         named_bar(1, 256);  // nobody overwrites sk_ticket before every thread has read it
@@ -396,10 +479,10 @@ bool make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
   return r == CUDA_SUCCESS;
 }
 
-template <int CG, int BN, bool A_MN, bool B_MN, int WN = 1>
+template <int CG, int BN, bool A_MN, bool B_MN, int WN, int KIND>
 cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   using C = Cfg<CG, BN, WN>;
-  auto kern = gemm_sm100_kernel<CG, BN, A_MN, B_MN, WN>;
+  auto kern = gemm_sm100_kernel<CG, BN, A_MN, B_MN, WN, KIND>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -455,10 +538,30 @@ cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
 
 template <int CG, int BN, int WN = 1>
 cudaError_t launch_major(const GemmDesc& g, const Epi& e, cudaStream_t st) {
-  if (!g.a_mn && !g.b_mn) return launch_bn<CG, BN, false, false, WN>(g, e, st);
-  if (g.a_mn && g.b_mn) return launch_bn<CG, BN, true, true, WN>(g, e, st);
-  if (g.a_mn) return launch_bn<CG, BN, true, false, WN>(g, e, st);
-  return launch_bn<CG, BN, false, true, WN>(g, e, st);
+  // instantiated (majors x epilogue) pairs: K-major x K-major carries every layer epilogue, the
+  // weight-gradient MN-major x MN-major the fp32 store / accumulate, the mixed majors (kernel tests)
+  // the store
+  if (!g.a_mn && !g.b_mn) {
+    switch (e.kind) {
+      case EPI_STORE: return launch_bn<CG, BN, false, false, WN, EPI_STORE>(g, e, st);
+      case EPI_RESID: return launch_bn<CG, BN, false, false, WN, EPI_RESID>(g, e, st);
+      case EPI_GELU: return launch_bn<CG, BN, false, false, WN, EPI_GELU>(g, e, st);
+      case EPI_DGELU: return launch_bn<CG, BN, false, false, WN, EPI_DGELU>(g, e, st);
+      case EPI_QKV: return launch_bn<CG, BN, false, false, WN, EPI_QKV>(g, e, st);
+      case EPI_ACCUM: return launch_bn<CG, BN, false, false, WN, EPI_ACCUM>(g, e, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  if (g.a_mn && g.b_mn) {
+    switch (e.kind) {
+      case EPI_STORE: return launch_bn<CG, BN, true, true, WN, EPI_STORE>(g, e, st);
+      case EPI_ACCUM: return launch_bn<CG, BN, true, true, WN, EPI_ACCUM>(g, e, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  if (e.kind != EPI_STORE) return cudaErrorInvalidValue;
+  if (g.a_mn) return launch_bn<CG, BN, true, false, WN, EPI_STORE>(g, e, st);
+  return launch_bn<CG, BN, false, true, WN, EPI_STORE>(g, e, st);
 }
 
 }  // namespace

@@ -96,6 +96,13 @@ cudaError_t attn_dkv_finalize(const float* dk_acc, const float* dv_acc, T* dqkv,
                               int s, int d, int c, int l, cudaStream_t st, int nseq = 1, int64_t acc_sstride = 0,
                               int64_t out_sstride = 0);
 
+// device-initiated p2p (p2p.cu): peer address of an NCCL symmetric window (host readback), the step
+// epoch counter, and the release-store signal / acquire-spin wait on per-job flag slots
+cudaError_t p2p_peer_pointer(void* window, int peer, void** host_out, cudaStream_t st);
+cudaError_t p2p_epoch_inc(unsigned long long* epoch, cudaStream_t st);
+cudaError_t p2p_signal(unsigned long long* remote_slot, const unsigned long long* epoch, cudaStream_t st);
+cudaError_t p2p_wait(const unsigned long long* local_slot, const unsigned long long* epoch, cudaStream_t st);
+
 template <typename T> cudaError_t convert_f32(const float* src, T* dst, int64_t n, cudaStream_t st);
 template <typename T>
 cudaError_t transpose_convert(const float* src, T* dst, int R, int C, cudaStream_t st);

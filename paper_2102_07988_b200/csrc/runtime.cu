@@ -233,6 +233,17 @@ class Engine final : public EngineBase {
   int64_t g_launches = 0;
   // NCCL (multi-rank, or the single-GPU NCCL loopback of TP_FLAG_NCCL_LOOPBACK)
   bool nccl_lb = false;  // world == 1, K > 1: stage messages through ncclSend/ncclRecv to self
+  // device-initiated p2p (TP_FLAG_DEVICE_P2P, world > 1; p2p.cu): hs[0] / grad_out of the owned stage
+  // are NCCL symmetric windows written directly by the neighbours' kernels
+  bool dev_p2p = false;
+  ncclWindow_t win_in = nullptr, win_gout = nullptr, win_flag = nullptr;
+  void *p_in = nullptr, *p_gout = nullptr, *p_flag = nullptr;
+  float* peer_in = nullptr;                       // rank + 1's hs[0]
+  float* peer_gout = nullptr;                     // rank - 1's grad_out
+  unsigned long long* peer_flag_next = nullptr;   // rank + 1's flag slots
+  unsigned long long* peer_flag_prev = nullptr;   // rank - 1's flag slots
+  unsigned long long* d_epoch = nullptr;
+  size_t n_slots = 0;                             // per direction: max jobs per step
   ncclComm_t base = nullptr, commF[2] = {nullptr, nullptr}, commB[2] = {nullptr, nullptr};
   cudaStream_t s_recv_f = nullptr, s_send_f = nullptr, s_recv_b = nullptr, s_send_b = nullptr;
   cudaStream_t s_wgrad = nullptr;  // low priority: deferred weight gradients (multi-rank)
@@ -243,6 +254,10 @@ class Engine final : public EngineBase {
     if (stream) cudaStreamSynchronize(stream);
     if (g_exec) cudaGraphExecDestroy(g_exec);
     if (h_tokens) cudaFreeHost(h_tokens);
+    for (ncclWindow_t w : {win_in, win_gout, win_flag})
+      if (w) ncclCommWindowDeregister(base, w);
+    for (void* p : {p_in, p_gout, p_flag})
+      if (p) ncclMemFree(p);
     for (ncclComm_t c : {commF[0], commF[1], commB[0], commB[1], base})
       if (c) ncclCommDestroy(c);
     for (void* p : allocs) cudaFree(p);
@@ -289,6 +304,8 @@ class Engine final : public EngineBase {
     if (const char* e = std::getenv("TP_LEGACY_ATTN")) legacy_attn = std::atoi(e) != 0;
     if (world == 1) { k0 = 0; k1 = m.K; } else { k0 = rank; k1 = rank + 1; }
     nccl_lb = world == 1 && m.K > 1 && (flags & TP_FLAG_NCCL_LOOPBACK) != 0;
+    dev_p2p = world > 1 && ((flags & TP_FLAG_DEVICE_P2P) != 0 ||
+                            (std::getenv("TP_DEVICE_P2P") && std::atoi(std::getenv("TP_DEVICE_P2P")) != 0));
     CU(cudaSetDevice(device));
     int major = 0;
     CU(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
@@ -332,6 +349,7 @@ class Engine final : public EngineBase {
         NC(ncclCommSplit(base, 0, rank, &commF[i], nullptr));
         NC(ncclCommSplit(base, 0, rank, &commB[i], nullptr));
       }
+      if (dev_p2p) TRY(setup_device_p2p());
       CU(cudaStreamCreateWithPriority(&s_recv_f, cudaStreamNonBlocking, hi));
       CU(cudaStreamCreateWithPriority(&s_send_f, cudaStreamNonBlocking, hi));
       CU(cudaStreamCreateWithPriority(&s_recv_b, cudaStreamNonBlocking, hi));
@@ -367,7 +385,8 @@ class Engine final : public EngineBase {
     // loopback: stage k's input buffer IS stage k-1's output buffer (the "send" is free)
     const bool alias = world == 1 && k > k0 && !nccl_lb;
     if (alias) S.hs[0] = stages[k - 1 - k0].hs[stages[k - 1 - k0].nl];
-    for (size_t j = alias ? 1 : 0; j <= nl; ++j) TRY(alloc(&S.hs[j], B * s * H));
+    // device p2p: hs[0] and grad_out become NCCL symmetric windows (setup_device_p2p, after the comm)
+    for (size_t j = (alias || dev_p2p) ? 1 : 0; j <= nl; ++j) TRY(alloc(&S.hs[j], B * s * H));
     TRY(vec(S.hmid, nl, B * s * H));
     TRY(vec(S.A1, nl, B * s * H)); TRY(vec(S.A2, nl, B * s * H)); TRY(vec(S.O, nl, B * s * H));
     TRY(vec(S.st1, nl, 2 * B * s)); TRY(vec(S.st2, nl, 2 * B * s));
@@ -379,7 +398,7 @@ class Engine final : public EngineBase {
       TRY(alloc(&S.Z, B * s * (size_t)m.V)); TRY(alloc(&S.loss_rows, B * s));
       if (flags & TP_FLAG_KEEP_LOGITS) TRY(alloc(&S.logits_keep, B * s * (size_t)m.V));
     }
-    TRY(alloc(&S.grad_out, B * s * H));
+    if (!dev_p2p) TRY(alloc(&S.grad_out, B * s * H));
     if (alias) {
       // stage k-1's grad_out IS stage k's grad_in
       Stage<T>& P = stages[k - 1 - k0];
@@ -397,6 +416,37 @@ class Engine final : public EngineBase {
     TRY(alloc(&S.Dvec, 2 * B * a * (s + 64))); TRY(alloc(&S.dO, B * s * H));
     TRY(alloc(&S.lnws, 2 * H * ((B * s + 3) / 4)));
     TRY(alloc(&S.dqacc, B * s * H));
+    return TP_OK;
+  }
+
+  // Symmetric windows for the stage's receive buffers and flag slots (collective over the ranks,
+  // identical sizes everywhere), and the neighbours' addresses inside them.
+  tp_status setup_device_p2p() {
+    Stage<T>& S = stages[0];
+    const size_t act = (size_t)max_batch * m.s * m.H * sizeof(float);
+    const size_t abytes = (act + 4095) / 4096 * 4096;
+    n_slots = (size_t)max_batch * m.s;
+    const size_t fbytes = (2 * n_slots * sizeof(unsigned long long) + 4095) / 4096 * 4096;
+    NC(ncclMemAlloc(&p_in, abytes));
+    NC(ncclMemAlloc(&p_gout, abytes));
+    NC(ncclMemAlloc(&p_flag, fbytes));
+    CU(cudaMemset(p_flag, 0, fbytes));
+    NC(ncclCommWindowRegister(base, p_in, abytes, &win_in, NCCL_WIN_COLL_SYMMETRIC));
+    NC(ncclCommWindowRegister(base, p_gout, abytes, &win_gout, NCCL_WIN_COLL_SYMMETRIC));
+    NC(ncclCommWindowRegister(base, p_flag, fbytes, &win_flag, NCCL_WIN_COLL_SYMMETRIC));
+    S.hs[0] = reinterpret_cast<float*>(p_in);
+    S.grad_out = reinterpret_cast<float*>(p_gout);
+    void* q = nullptr;
+    if (rank + 1 < world) {
+      CU(p2p_peer_pointer(win_in, rank + 1, &q, stream)); peer_in = reinterpret_cast<float*>(q);
+      CU(p2p_peer_pointer(win_flag, rank + 1, &q, stream)); peer_flag_next = reinterpret_cast<unsigned long long*>(q);
+    }
+    if (rank > 0) {
+      CU(p2p_peer_pointer(win_gout, rank - 1, &q, stream)); peer_gout = reinterpret_cast<float*>(q);
+      CU(p2p_peer_pointer(win_flag, rank - 1, &q, stream)); peer_flag_prev = reinterpret_cast<unsigned long long*>(q);
+    }
+    TRY(alloc(&d_epoch, 1));
+    CU(cudaMemset(d_epoch, 0, sizeof(unsigned long long)));
     return TP_OK;
   }
 
@@ -500,7 +550,9 @@ class Engine final : public EngineBase {
   // position p in row seq0*s + p*b + j, so the job (group, slice [c, c+l)) is the contiguous row
   // range [seq0*s + c*b, seq0*s + (c+l)*b) of T = b*l tokens (PAPER.md:362-364 joint batch x token
   // slicing; b = 1 is the plain token slicing of §3.2; groups may differ in b).
-  tp_status fwd(Stage<T>& S, size_t seq0, int c, int l, int b, int batch) {
+  // out_next (device p2p): the stage output rows of this job go straight into the next stage's input
+  // buffer (peer memory) from the last layer's FC2 epilogue instead of S.hs[nl]
+  tp_status fwd(Stage<T>& S, size_t seq0, int c, int l, int b, int batch, float* out_next = nullptr) {
     const int H = m.H, s = m.s, a = m.a, dh = m.d, V = m.V;
     const int Tn = b * l;
     const size_t row = seq0 * s + (size_t)c * b;  // first row of this job
@@ -558,7 +610,8 @@ class Engine final : public EngineBase {
       }));
       Epi eg; eg.kind = EPI_GELU; eg.bias = P + f.b_1; eg.out = S.U[j] + row * 4 * H; eg.ldo = 4 * H; eg.out2 = S.G[j] + row * 4 * H; eg.ldo2 = 4 * H;
       TRY(gemm(KC_GEMM_FWD, gd(Tn, 4 * H, H, S.A2[j] + row * H, H, false, S.w1_t[j], H, false), eg));
-      Epi e2; e2.kind = EPI_RESID; e2.bias = P + f.b_2; e2.out = S.hs[j + 1] + row * H; e2.ldo = H; e2.resid = S.hmid[j] + row * H; e2.ldr = H;
+      Epi e2; e2.kind = EPI_RESID; e2.bias = P + f.b_2; e2.ldo = H; e2.resid = S.hmid[j] + row * H; e2.ldr = H;
+      e2.out = (out_next && j == S.nl - 1) ? out_next : S.hs[j + 1] + row * H;
       TRY(gemm(KC_GEMM_FWD, gd(Tn, H, 4 * H, S.G[j] + row * 4 * H, 4 * H, false, S.w2_t[j], 4 * H, false), e2));
     }
     if (S.k == m.K - 1) {
@@ -579,7 +632,10 @@ class Engine final : public EngineBase {
   }
 
   // ------------------------------------------------------------ backward of one job on one stage
-  tp_status bwd(Stage<T>& S, size_t seq0, int c, int l, int b, int batch, bool first_bwd_slice) {
+  // gin_prev (device p2p): the input-gradient rows of this job go straight into the previous stage's
+  // grad_out buffer (peer memory) from the first layer's LayerNorm backward instead of S.grad_in
+  tp_status bwd(Stage<T>& S, size_t seq0, int c, int l, int b, int batch, bool first_bwd_slice,
+                float* gin_prev = nullptr) {
     const int H = m.H, s = m.s, a = m.a, dh = m.d, V = m.V;
     const int Tn = b * l;
     const size_t row = seq0 * s + (size_t)c * b;
@@ -662,7 +718,7 @@ class Engine final : public EngineBase {
       }));
       Epi e4; e4.kind = EPI_STORE; e4.out = S.dA; e4.ldo = H; e4.out_f32 = std::is_same<T, float>::value;
       TRY(gemm(KC_GEMM_DX, gd(Tn, H, 3 * H, dq, 3 * H, false, S.wqkv_io[j], 3 * H, false), e4));
-      float* gnext = j == 0 ? S.grad_in + row * H : (gr == S.gA ? S.gB : S.gA);
+      float* gnext = j == 0 ? (gin_prev ? gin_prev : S.grad_in + row * H) : (gr == S.gA ? S.gB : S.gA);
       T* copy = j == 0 ? nullptr : S.dhout_b[j - 1] + row * H;
       float* st1 = S.st1[j];
       TRY(launch(KC_LN, 0, (16.0 + ebytes) * Tn * H, [&] {
@@ -796,6 +852,13 @@ class Engine final : public EngineBase {
       for (cudaStream_t cs : {s_send_f, s_recv_f, s_send_b, s_recv_b}) CU(cudaStreamWaitEvent(cs, e, 0));
     }
     for (auto& S : stages) CU(cudaMemsetAsync(S.gflat, 0, S.L.total * sizeof(float), stream));
+    std::vector<size_t> job0(D + 1, 0);  // global job index of (group d, slice 0): the p2p flag slot
+    for (int d = 0; d < D; ++d) job0[d + 1] = job0[d] + G[d].len.size();
+    if (dev_p2p) {
+      if (job0[D] > n_slots) return fail(TP_EINVAL, "tp_step: %zu jobs exceed the %zu p2p slots", job0[D], n_slots);
+      CU(p2p_epoch_inc(d_epoch, stream));
+    }
+    unsigned long long* flag_local = reinterpret_cast<unsigned long long*>(p_flag);
     // forward: F(d, i) for groups d = 0..D-1 (b_d sequences each), slices i = 1..M_d (stage order
     // inside a job in loopback); a job is b_d*l_i tokens, contiguous rows (see fwd())
     for (int d = 0; d < D; ++d)
@@ -805,6 +868,13 @@ class Engine final : public EngineBase {
           const int b = G[d].b;
           const size_t row = G[d].seq0 * m.s + (size_t)G[d].off[i] * b;
           const int Tn = b * G[d].len[i];
+          const size_t jb = job0[d] + i;
+          if (dev_p2p) {
+            if (S.k > 0) CU(p2p_wait(flag_local + jb, d_epoch, stream));
+            TRY(fwd(S, G[d].seq0, G[d].off[i], G[d].len[i], b, batch, S.k < m.K - 1 ? peer_in + row * m.H : nullptr));
+            if (S.k < m.K - 1) CU(p2p_signal(peer_flag_next + jb, d_epoch, stream));
+            continue;
+          }
           if (multi && S.k > 0) TRY(recv_fwd(S, row, Tn));
           TRY(fwd(S, G[d].seq0, G[d].off[i], G[d].len[i], b, batch));
           if (multi && S.k < m.K - 1) TRY(send_fwd(S, row, Tn));
@@ -823,6 +893,14 @@ class Engine final : public EngineBase {
           Stage<T>& S = stages[si];
           const size_t row = G[d].seq0 * m.s + (size_t)G[d].off[i] * b;
           const int Tn = b * G[d].len[i];
+          const size_t jb = job0[d] + i;
+          if (dev_p2p) {
+            if (S.k < m.K - 1) CU(p2p_wait(flag_local + n_slots + jb, d_epoch, stream));
+            TRY(bwd(S, G[d].seq0, G[d].off[i], G[d].len[i], b, batch, i == M - 1,
+                    S.k > 0 ? peer_gout + row * m.H : nullptr));
+            if (S.k > 0) CU(p2p_signal(peer_flag_prev + n_slots + jb, d_epoch, stream));
+            continue;
+          }
           if (multi && S.k < m.K - 1) TRY(recv_bwd(S, row, Tn));
           TRY(bwd(S, G[d].seq0, G[d].off[i], G[d].len[i], b, batch, i == M - 1));
           if (multi && S.k > 0) TRY(send_bwd(S, row, Tn));

@@ -81,7 +81,13 @@ if __name__ == "__main__":
                                        (8192, H, H, 0, 0, "1b o-proj b=4 (3.46 waves)"),
                                        (8192, H, 4 * H, 0, 0, "1b fc2 b=4 (3.46 waves)"),
                                        (768, 15360, 5120, 0, 0, "13b qkv b=2 l=384 (2.43 waves)"),
-                                       (1536, 5120, 20480, 0, 0, "13b fc2 b=2 l=768 (1.62 waves)")]:
+                                       (1536, 5120, 20480, 0, 0, "13b fc2 b=2 l=768 (1.62 waves)"),
+                                       # the 1B bench's jobs: b = 8 x l = 576 / 1472, and its dW (K = B s)
+                                       (4608, 3 * H, H, 0, 0, "1b qkv b=8 l=576"), (11776, 3 * H, H, 0, 0, "1b qkv b=8 l=1472"),
+                                       (11776, H, H, 0, 0, "1b o-proj b=8 l=1472"), (11776, 4 * H, H, 0, 0, "1b fc1 b=8 l=1472"),
+                                       (11776, H, 4 * H, 0, 0, "1b fc2 b=8 l=1472"), (11776, 50304, H, 0, 0, "1b head l=1472"),
+                                       (H, 3 * H, 16384, 1, 1, "1b qkv dW K=16384"), (4 * H, H, 16384, 1, 1, "1b fc2 dW K=16384"),
+                                       (H, 4 * H, 16384, 1, 1, "1b fc1 dW K=16384")]:
             gemm(M, N, K, am, bm, 0, tag)
     if args.which in ("all", "attn"):
         for (a, s, d, c, l, tag) in [(16, 2048, 128, 0, 2048, "1b full"), (40, 2048, 128, 1536, 512, "13b last slice"),

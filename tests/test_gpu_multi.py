@@ -50,6 +50,16 @@ def test_profile_collectives_two_ranks(tmp_path):
     assert (t[:, 0] > 0).all()
 
 
+@pytest.mark.parametrize("world,cfg,lengths,batch", [(2, "tiny", "5,9,2,16", None), (2, "small", "40,24,64", None),
+                                                     (2, "small", "2:40,24,64;1:128", 3), (4, "small", "40,24,64", None)])
+def test_device_initiated_p2p(world, cfg, lengths, batch, tmp_path):
+    """TP_DEVICE_P2P=1: stage messages written by the producing kernels straight
+    into the neighbour's NCCL symmetric window, signalled by per-job release flags, no ncclSend/Recv
+    on the data path; same parity bar, repeated steps (epoch-based flags) and graph replay."""
+    for errs in run(world, cfg, "bf16", lengths, tmp_path, env={"TP_DEVICE_P2P": "1"}, batch=batch):
+        assert max(errs.values()) < 2e-2, errs
+
+
 def test_small_four_stages_nccl(tmp_path):
     for errs in run(4, "small", "bf16", "40,24,64", tmp_path):
         assert max(errs.values()) < 2e-2, errs
