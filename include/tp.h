@@ -64,14 +64,22 @@ enum { TP_FLAG_KEEP_LOGITS = 1,   /* keep fp32 logits of the last step for tp_ge
                                      per message, on the same per-direction comm streams, NCCL
                                      communicators and events as world == n_stages) instead of
                                      aliasing the buffers; lets the p2p path run on one GPU        */
-       TP_FLAG_DEVICE_P2P = 16    /* world == n_stages > 1: device-initiated messages instead of
+       TP_FLAG_DEVICE_P2P = 16,   /* world == n_stages > 1: device-initiated messages instead of
                                      ncclSend/ncclRecv — each stage's receive buffers are NCCL
                                      symmetric windows (ncclMemAlloc + ncclCommWindowRegister); the
                                      last layer's FC2 epilogue and the first layer's LayerNorm
                                      backward write straight into the neighbour's buffer over
                                      NVLink, a release-store flag per job signals it, the consumer
                                      spins on its flag before the job; env
-                                     TP_DEVICE_P2P=1 sets it too                                   */ };
+                                     TP_DEVICE_P2P=1 sets it too                                   */
+       TP_FLAG_SCHEDULE_1F1B = 32 /* 1F1B at sequence-group granularity instead of GPipe order
+                                     (A-21): stage k runs the forwards
+                                     of w_k = min(D, K - k) groups, then alternates the backward of
+                                     its oldest group with the forward of the next; each group's
+                                     weight gradients run right after its backward; the stage
+                                     buffers hold only w_k groups (slots), so a step's batch may
+                                     exceed max_batch as long as w_k x (largest group) <= max_batch;
+                                     env TP_SCHEDULE=1f1b sets it too                              */ };
 
 /* Model shape. n_layer % n_stages == 0; hidden % n_head == 0; head_dim = hidden / n_head must be
  * a multiple of 16 and <= 128; hidden % 64 == 0; seq_len >= 1. */
@@ -151,6 +159,15 @@ typedef struct {
 tp_status tp_plan_joint(int32_t n_layer, int32_t hidden, int32_t seq_len, int32_t n_stages, int32_t n_b,
                         const int32_t* b_values, const tp_cost_table* const* costs, int32_t batch,
                         int64_t eps_ticks, tp_batch_plan* out);
+
+/* The op list tp_step runs on stage `stage` of n_stages (A-21) for groups with
+ * n_slices[d] token slices each (jobs numbered group-major: job j = slice i of group d, j = first(d) +
+ * i): ops_out[t] = j + 1 for the forward of job j, -(j + 1) for its backward. schedule 0 = GPipe
+ * (all forwards in order, then all backwards in exact reverse), 1 = 1F1B at group granularity
+ * (TP_FLAG_SCHEDULE_1F1B). capacity >= 2 * total jobs; *n_ops = 2 * total jobs. Pure host function
+ * (pinned to oracle/plan.py gpipe_oplists / one_f_one_b_oplists). */
+tp_status tp_schedule_oplist(int32_t n_stages, int32_t stage, int32_t schedule, int32_t n_groups,
+                             const int32_t* n_slices, int32_t capacity, int32_t* ops_out, int32_t* n_ops);
 
 /* Number of float32 parameters of stage `stage` (see "Parameter layout"). */
 tp_status tp_stage_param_count(const tp_model_cfg* cfg, int32_t stage, size_t* out);

@@ -16,8 +16,9 @@ LIB_PATH = os.path.join(_HERE, "libtp.so")
 TP_OK, TP_EINVAL, TP_EINFEASIBLE, TP_ETOOBIG, TP_ECUDA, TP_ENCCL, TP_ENOMEM, TP_ESTATE = 0, -1, -2, -3, -4, -5, -6, -7
 TP_BF16, TP_FP32 = 0, 1
 TP_FLAG_KEEP_LOGITS, TP_FLAG_KERNEL_STATS, TP_FLAG_FORCE_SIMT, TP_FLAG_NCCL_LOOPBACK, TP_FLAG_DEVICE_P2P = 1, 2, 4, 8, 16
+TP_FLAG_SCHEDULE_1F1B = 32
 
-EXPORTED = ["tp_plan", "tp_plan_joint", "tp_step_plan", "tp_step_plan_device", "tp_stage_param_count", "tp_nccl_unique_id", "tp_init", "tp_param_count",
+EXPORTED = ["tp_plan", "tp_plan_joint", "tp_schedule_oplist", "tp_step_plan", "tp_step_plan_device", "tp_stage_param_count", "tp_nccl_unique_id", "tp_init", "tp_param_count",
             "tp_load_params", "tp_step", "tp_step_device", "tp_get_grads", "tp_get_logits",
             "tp_profile", "tp_profile_wgrad", "tp_profile_comm", "tp_get_stream", "tp_kernel_stats", "tp_kernel_stats_reset", "tp_kernel_stats_enable",
             "tp_last_step_launches", "tp_destroy", "tp_last_error"]
@@ -66,6 +67,8 @@ def _load() -> C.CDLL:
         "tp_step_plan": (C.c_int, [P, C.POINTER(BatchPlanC), P, C.c_int32, C.POINTER(C.c_float)]),
         "tp_step_plan_device": (C.c_int, [P, C.POINTER(BatchPlanC), P, C.c_int32, C.POINTER(C.c_float)]),
         "tp_stage_param_count": (C.c_int, [C.POINTER(ModelCfgC), C.c_int32, C.POINTER(C.c_size_t)]),
+        "tp_schedule_oplist": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32,
+                                         C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
         "tp_nccl_unique_id": (C.c_int, [P]),
         "tp_init": (C.c_int, [C.POINTER(ModelCfgC), C.c_int32, C.c_int32, P, C.c_int32, C.c_int32, C.c_int32,
                               C.c_int32, C.POINTER(P)]),
@@ -216,6 +219,17 @@ def plan_joint(tables: Dict[int, np.ndarray], granularity: int, n_layer: int, hi
         groups.append((gb[d], [lens[pos + i] for i in range(gm[d])]))
         pos += gm[d]
     return BatchPlan(groups, out.t_max_ticks, out.predicted_ticks)
+
+
+def schedule_oplist(n_stages: int, stage: int, groups: Sequence[int], one_f_one_b: bool = False) -> List[Tuple[str, int]]:
+    """tp_schedule_oplist: the op list tp_step runs on `stage` for groups of groups[d] slices, as
+    ("F" | "B", job) pairs (oracle/plan.py's format)."""
+    g = (C.c_int32 * max(1, len(groups)))(*groups)
+    cap = 2 * sum(groups)
+    out = (C.c_int32 * max(1, cap))()
+    n = C.c_int32()
+    _check(_lib.tp_schedule_oplist(n_stages, stage, 1 if one_f_one_b else 0, len(groups), g, cap, out, C.byref(n)))
+    return [("F", v - 1) if v > 0 else ("B", -v - 1) for v in out[:n.value]]
 
 
 def stage_param_count(cfg, stage: int) -> int:

@@ -160,6 +160,35 @@ class Instr {
   }
 };
 
+// ---------------------------------------------------------------- schedule
+// Per-stage op lists (A-21): GPipe — every F(d, i) in order, then every B in exact
+// reverse; 1F1B at group granularity — stage k runs the forwards of its first
+// w_k = min(D, K - k) groups, then alternates the backward of its oldest group (slices in reverse)
+// with the forward of the next one, then drains. Exported as tp_schedule_oplist and pinned to
+// oracle/plan.py (gpipe_oplists / one_f_one_b_oplists).
+struct Op {
+  bool fwd;
+  int d, i;
+};
+static std::vector<Op> build_oplist(int K, int k, bool one_f_one_b, const std::vector<int>& M) {
+  const int D = (int)M.size();
+  std::vector<Op> ops;
+  auto F = [&](int d) { for (int i = 0; i < M[d]; ++i) ops.push_back({true, d, i}); };
+  auto B = [&](int d) { for (int i = M[d] - 1; i >= 0; --i) ops.push_back({false, d, i}); };
+  if (!one_f_one_b) {
+    for (int d = 0; d < D; ++d) F(d);
+    for (int d = D - 1; d >= 0; --d) B(d);
+    return ops;
+  }
+  const int w = std::min(D, K - k);
+  for (int d = 0; d < w; ++d) F(d);
+  for (int d = 0; d < D; ++d) {
+    B(d);
+    if (d + w < D) F(d + w);
+  }
+  return ops;
+}
+
 // ---------------------------------------------------------------- engine
 struct EngineBase {
   virtual ~EngineBase() = default;
@@ -180,6 +209,7 @@ struct EngineBase {
 template <typename T>
 struct Stage {
   int k = 0, nl = 0;
+  bool aliased = false;  // loopback: hs[0] / grad_in are the previous stage's hs[nl] / grad_out buffers
   StageLayout L;
   float* psmall = nullptr;  // fp32 LayerNorm / bias / embedding parameters (StageLayout::small offsets)
   float* gflat = nullptr;  // fp32 grads (flat layout)
@@ -233,6 +263,7 @@ class Engine final : public EngineBase {
   int64_t g_launches = 0;
   // NCCL (multi-rank, or the single-GPU NCCL loopback of TP_FLAG_NCCL_LOOPBACK)
   bool nccl_lb = false;  // world == 1, K > 1: stage messages through ncclSend/ncclRecv to self
+  bool sched_1f1b = false;  // TP_FLAG_SCHEDULE_1F1B: group-granular 1F1B op lists, slot-mapped stash
   // device-initiated p2p (TP_FLAG_DEVICE_P2P, world > 1; p2p.cu): hs[0] / grad_out of the owned stage
   // are NCCL symmetric windows written directly by the neighbours' kernels
   bool dev_p2p = false;
@@ -254,6 +285,8 @@ class Engine final : public EngineBase {
     if (stream) cudaStreamSynchronize(stream);
     if (g_exec) cudaGraphExecDestroy(g_exec);
     if (h_tokens) cudaFreeHost(h_tokens);
+    if (d_tokens) cudaFree(d_tokens);
+    for (auto& S : stages) if (S.loss_rows) cudaFree(S.loss_rows);
     for (ncclWindow_t w : {win_in, win_gout, win_flag})
       if (w) ncclCommWindowDeregister(base, w);
     for (void* p : {p_in, p_gout, p_flag})
@@ -304,6 +337,8 @@ class Engine final : public EngineBase {
     if (const char* e = std::getenv("TP_LEGACY_ATTN")) legacy_attn = std::atoi(e) != 0;
     if (world == 1) { k0 = 0; k1 = m.K; } else { k0 = rank; k1 = rank + 1; }
     nccl_lb = world == 1 && m.K > 1 && (flags & TP_FLAG_NCCL_LOOPBACK) != 0;
+    sched_1f1b = (flags & TP_FLAG_SCHEDULE_1F1B) != 0 ||
+                 (std::getenv("TP_SCHEDULE") && std::string(std::getenv("TP_SCHEDULE")) == "1f1b");
     dev_p2p = world > 1 && ((flags & TP_FLAG_DEVICE_P2P) != 0 ||
                             (std::getenv("TP_DEVICE_P2P") && std::atoi(std::getenv("TP_DEVICE_P2P")) != 0));
     CU(cudaSetDevice(device));
@@ -314,9 +349,8 @@ class Engine final : public EngineBase {
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CU(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, hi));
     CU(cudaHostAlloc(&h_loss, sizeof(float), cudaHostAllocDefault));
-    CU(cudaHostAlloc(&h_tokens, sizeof(int32_t) * (size_t)max_batch * (m.s + 1), cudaHostAllocDefault));
+
     use_graphs = std::getenv("TP_NO_GRAPHS") == nullptr && std::getenv("TP_ATTN_DEBUG") == nullptr;
-    TRY(alloc(&d_tokens, (size_t)max_batch * (m.s + 1)));
     TRY(alloc(&d_loss, 4));
     CU(cudaHostAlloc(&h_bad_tok, sizeof(int), cudaHostAllocDefault));
     TRY(alloc(&d_bad_tok, 1));
@@ -332,6 +366,7 @@ class Engine final : public EngineBase {
     }
     stages.resize(k1 - k0);
     for (int k = k0; k < k1; ++k) TRY(alloc_stage(stages[k - k0], k));
+    TRY(ensure_batch_capacity(max_batch));
     if (world > 1 || nccl_lb) {
       if (world > 1) {
         ncclUniqueId id;
@@ -383,7 +418,9 @@ class Engine final : public EngineBase {
     if (last) { TRY(alloc(&S.wout_t, H * m.V)); TRY(alloc(&S.wout_io, H * m.V)); }
     S.hs.assign(nl + 1, nullptr);
     // loopback: stage k's input buffer IS stage k-1's output buffer (the "send" is free)
-    const bool alias = world == 1 && k > k0 && !nccl_lb;
+    // (1F1B: stages use different slot rows for the same group, so messages are copies)
+    const bool alias = world == 1 && k > k0 && !nccl_lb && !sched_1f1b;
+    S.aliased = alias;
     if (alias) S.hs[0] = stages[k - 1 - k0].hs[stages[k - 1 - k0].nl];
     // device p2p: hs[0] and grad_out become NCCL symmetric windows (setup_device_p2p, after the comm)
     for (size_t j = (alias || dev_p2p) ? 1 : 0; j <= nl; ++j) TRY(alloc(&S.hs[j], B * s * H));
@@ -395,7 +432,7 @@ class Engine final : public EngineBase {
     TRY(vec(S.U, nl, B * s * 4 * H)); TRY(vec(S.G, nl, B * s * 4 * H));
     if (last) {
       TRY(alloc(&S.Af, B * s * H)); TRY(alloc(&S.stf, 2 * B * s));
-      TRY(alloc(&S.Z, B * s * (size_t)m.V)); TRY(alloc(&S.loss_rows, B * s));
+      TRY(alloc(&S.Z, B * s * (size_t)m.V));  // loss_rows: ensure_batch_capacity (batch rows)
       if (flags & TP_FLAG_KEEP_LOGITS) TRY(alloc(&S.logits_keep, B * s * (size_t)m.V));
     }
     if (!dev_p2p) TRY(alloc(&S.grad_out, B * s * H));
@@ -416,6 +453,33 @@ class Engine final : public EngineBase {
     TRY(alloc(&S.Dvec, 2 * B * a * (s + 64))); TRY(alloc(&S.dO, B * s * H));
     TRY(alloc(&S.lnws, 2 * H * ((B * s + 3) / 4)));
     TRY(alloc(&S.dqacc, B * s * H));
+    return TP_OK;
+  }
+
+  // Per-batch (not per-slot) buffers: tokens (device + pinned staging) and the last stage's per-row
+  // losses, grown when a 1F1B step's batch exceeds the current capacity (outside any capture; the
+  // cached step graph referencing the old buffers is dropped).
+  size_t tok_cap = 0;
+  tp_status ensure_batch_capacity(int batch) {
+    if ((size_t)batch <= tok_cap) return TP_OK;
+    if (stream) CU(cudaStreamSynchronize(stream));
+    if (g_exec) { cudaGraphExecDestroy(g_exec); g_exec = nullptr; g_key.clear(); }
+    if (d_tokens) cudaFree(d_tokens);
+    if (h_tokens) cudaFreeHost(h_tokens);
+    if (d_tokens) cudaFree(d_tokens);
+    for (auto& S : stages) if (S.loss_rows) cudaFree(S.loss_rows);
+    d_tokens = nullptr; h_tokens = nullptr;
+    const size_t n = (size_t)batch * (m.s + 1);
+    if (cudaMalloc(&d_tokens, n * sizeof(int32_t)) != cudaSuccess) return fail(TP_ENOMEM, "tokens: cudaMalloc");
+    CU(cudaHostAlloc(&h_tokens, n * sizeof(int32_t), cudaHostAllocDefault));
+    for (auto& S : stages)
+      if (S.k == m.K - 1) {
+        if (S.loss_rows) cudaFree(S.loss_rows);
+        S.loss_rows = nullptr;
+        if (cudaMalloc(&S.loss_rows, (size_t)batch * m.s * sizeof(float)) != cudaSuccess)
+          return fail(TP_ENOMEM, "loss rows: cudaMalloc");
+      }
+    tok_cap = batch;
     return TP_OK;
   }
 
@@ -552,11 +616,15 @@ class Engine final : public EngineBase {
   // slicing; b = 1 is the plain token slicing of §3.2; groups may differ in b).
   // out_next (device p2p): the stage output rows of this job go straight into the next stage's input
   // buffer (peer memory) from the last layer's FC2 epilogue instead of S.hs[nl]
-  tp_status fwd(Stage<T>& S, size_t seq0, int c, int l, int b, int batch, float* out_next = nullptr) {
+  // tseq0: the job's first sequence in the batch (tokens, loss rows, kept logits); seq0: its first
+  // sequence in this stage's buffers (= tseq0 store-all; the group's slot under 1F1B)
+  tp_status fwd(Stage<T>& S, size_t tseq0, size_t seq0, int c, int l, int b, int batch, float* out_next = nullptr) {
     const int H = m.H, s = m.s, a = m.a, dh = m.d, V = m.V;
     const int Tn = b * l;
-    const size_t row = seq0 * s + (size_t)c * b;  // first row of this job
-    const int32_t* tok0 = d_tokens + seq0 * (s + 1);
+    const size_t row = seq0 * s + (size_t)c * b;  // first buffer row of this job
+    const size_t trow = tseq0 * s + (size_t)c * b;  // first batch row of this job
+    const size_t cap = (size_t)max_batch * s;      // rows of the stage buffers (LN stats: mean | rstd)
+    const int32_t* tok0 = d_tokens + tseq0 * (s + 1);
     const double ebytes = sizeof(T);
     if (S.k == 0) {
       TRY(launch(KC_EMBED, 0, 8.0 * Tn * H, [&] {
@@ -569,7 +637,7 @@ class Engine final : public EngineBase {
       float* x = S.hs[j] + row * H;
       float* st1 = S.st1[j];
       TRY(launch(KC_LN, 0, (4.0 + ebytes) * Tn * H, [&] {
-        return layernorm_fwd<T>(x, P + f.ln1_g, P + f.ln1_b, S.A1[j] + row * H, st1 + row, st1 + (size_t)batch * s + row, Tn, H, stream);
+        return layernorm_fwd<T>(x, P + f.ln1_g, P + f.ln1_b, S.A1[j] + row * H, st1 + row, st1 + cap + row, Tn, H, stream);
       }));
       Epi eq; eq.kind = EPI_QKV; eq.bias = P + f.b_qkv;
       eq.q = S.Q[j] + seq0 * s * H; eq.k = S.Kc[j] + seq0 * s * H; eq.v = S.Vc[j] + seq0 * s * H;
@@ -606,7 +674,7 @@ class Engine final : public EngineBase {
       TRY(gemm(KC_GEMM_FWD, gd(Tn, H, H, o, H, false, S.wo_t[j], H, false), er));
       float* st2 = S.st2[j];
       TRY(launch(KC_LN, 0, (4.0 + ebytes) * Tn * H, [&] {
-        return layernorm_fwd<T>(S.hmid[j] + row * H, P + f.ln2_g, P + f.ln2_b, S.A2[j] + row * H, st2 + row, st2 + (size_t)batch * s + row, Tn, H, stream);
+        return layernorm_fwd<T>(S.hmid[j] + row * H, P + f.ln2_g, P + f.ln2_b, S.A2[j] + row * H, st2 + row, st2 + cap + row, Tn, H, stream);
       }));
       Epi eg; eg.kind = EPI_GELU; eg.bias = P + f.b_1; eg.out = S.U[j] + row * 4 * H; eg.ldo = 4 * H; eg.out2 = S.G[j] + row * 4 * H; eg.ldo2 = 4 * H;
       TRY(gemm(KC_GEMM_FWD, gd(Tn, 4 * H, H, S.A2[j] + row * H, H, false, S.w1_t[j], H, false), eg));
@@ -618,14 +686,14 @@ class Engine final : public EngineBase {
       const float* P = S.psmall;
       float* x = S.hs[S.nl] + row * H;
       TRY(launch(KC_LN, 0, (4.0 + ebytes) * Tn * H, [&] {
-        return layernorm_fwd<T>(x, P + S.L.s_lnf_g, P + S.L.s_lnf_b, S.Af + row * H, S.stf + row, S.stf + (size_t)batch * s + row, Tn, H, stream);
+        return layernorm_fwd<T>(x, P + S.L.s_lnf_g, P + S.L.s_lnf_b, S.Af + row * H, S.stf + row, S.stf + cap + row, Tn, H, stream);
       }));
       Epi ez; ez.kind = EPI_STORE; ez.out = S.Z + row * V; ez.ldo = V;
       TRY(gemm(KC_GEMM_FWD, gd(Tn, V, H, S.Af + row * H, H, false, S.wout_t, H, false), ez));
       const float scale = 1.0f / (float)((double)batch * s);
-      float* keep = S.logits_keep ? S.logits_keep + row * V : nullptr;
+      float* keep = S.logits_keep ? S.logits_keep + trow * V : nullptr;
       TRY(launch(KC_CE, 0, 2.0 * ebytes * Tn * V, [&] {
-        return ce_fwd_bwd<T>(S.Z + row * V, tok0, c, b, s, S.loss_rows + row, keep, Tn, V, scale, stream);
+        return ce_fwd_bwd<T>(S.Z + row * V, tok0, c, b, s, S.loss_rows + trow, keep, Tn, V, scale, stream);
       }));
     }
     return TP_OK;
@@ -634,12 +702,13 @@ class Engine final : public EngineBase {
   // ------------------------------------------------------------ backward of one job on one stage
   // gin_prev (device p2p): the input-gradient rows of this job go straight into the previous stage's
   // grad_out buffer (peer memory) from the first layer's LayerNorm backward instead of S.grad_in
-  tp_status bwd(Stage<T>& S, size_t seq0, int c, int l, int b, int batch, bool first_bwd_slice,
+  tp_status bwd(Stage<T>& S, size_t tseq0, size_t seq0, int c, int l, int b, int batch, bool first_bwd_slice,
                 float* gin_prev = nullptr) {
     const int H = m.H, s = m.s, a = m.a, dh = m.d, V = m.V;
     const int Tn = b * l;
     const size_t row = seq0 * s + (size_t)c * b;
-    const int32_t* tok0 = d_tokens + seq0 * (s + 1);
+    const size_t cap = (size_t)max_batch * s;
+    const int32_t* tok0 = d_tokens + tseq0 * (s + 1);
     const double ebytes = sizeof(T);
     float* gr = S.grad_out + row * H;  // fp32 gradient at the stage output, rows of this job
     if (S.k == m.K - 1) {
@@ -647,7 +716,7 @@ class Engine final : public EngineBase {
       Epi e; e.kind = EPI_STORE; e.out = S.dA; e.ldo = H; e.out_f32 = std::is_same<T, float>::value;
       TRY(gemm(KC_GEMM_DX, gd(Tn, H, V, S.Z + row * V, V, false, S.wout_io, V, false), e));
       TRY(launch(KC_LN, 0, (12.0 + ebytes) * Tn * H, [&] {
-        return layernorm_bwd<T>(reinterpret_cast<const T*>(S.dA), S.hs[S.nl] + row * H, S.stf + row, S.stf + (size_t)batch * s + row, P + S.L.s_lnf_g, nullptr, gr,
+        return layernorm_bwd<T>(reinterpret_cast<const T*>(S.dA), S.hs[S.nl] + row * H, S.stf + row, S.stf + cap + row, P + S.L.s_lnf_g, nullptr, gr,
                                 S.dhout_b[S.nl - 1] + row * H, S.gflat + S.L.lnf_g, S.gflat + S.L.lnf_b, S.lnws, Tn, H, stream,
                                 S.gflat + S.L.layers[S.nl - 1].b_2);
       }));
@@ -669,7 +738,7 @@ class Engine final : public EngineBase {
       TRY(gemm(KC_GEMM_DX, gd(Tn, H, 4 * H, S.dU[j] + row * 4 * H, 4 * H, false, S.w1_io[j], 4 * H, false), e2));
       float* st2 = S.st2[j];
       TRY(launch(KC_LN, 0, (16.0 + ebytes) * Tn * H, [&] {
-        return layernorm_bwd<T>(reinterpret_cast<const T*>(S.dA), S.hmid[j] + row * H, st2 + row, st2 + (size_t)batch * s + row, P + fs.ln2_g, gr, S.gm,
+        return layernorm_bwd<T>(reinterpret_cast<const T*>(S.dA), S.hmid[j] + row * H, st2 + row, st2 + cap + row, P + fs.ln2_g, gr, S.gm,
                                 S.dhmid_b[j] + row * H, GR + f.ln2_g, GR + f.ln2_b, S.lnws, Tn, H, stream, GR + f.b_o);
       }));
       // attention: dO = dh_mid W_o^T, then slice-vs-prefix attention backward with dK/dV push
@@ -722,7 +791,7 @@ class Engine final : public EngineBase {
       T* copy = j == 0 ? nullptr : S.dhout_b[j - 1] + row * H;
       float* st1 = S.st1[j];
       TRY(launch(KC_LN, 0, (16.0 + ebytes) * Tn * H, [&] {
-        return layernorm_bwd<T>(reinterpret_cast<const T*>(S.dA), S.hs[j] + row * H, st1 + row, st1 + (size_t)batch * s + row, P + fs.ln1_g, S.gm, gnext, copy,
+        return layernorm_bwd<T>(reinterpret_cast<const T*>(S.dA), S.hs[j] + row * H, st1 + row, st1 + cap + row, P + fs.ln1_g, S.gm, gnext, copy,
                                 GR + f.ln1_g, GR + f.ln1_b, S.lnws, Tn, H, stream,
                                 j == 0 ? nullptr : GR + S.L.layers[j - 1].b_2);
       }));
@@ -839,10 +908,30 @@ class Engine final : public EngineBase {
   // Everything one step puts on the device after the tokens are in d_tokens: zero the gradients, the
   // forward and backward op lists of every owned stage, the deferred weight gradients, the loss.
   struct Group {
-    size_t seq0;
+    size_t seq0;                // first sequence of the group in the batch (tokens, loss, logits)
     int b;
     std::vector<int> off, len;  // slice offsets (M + 1) and lengths (M), tokens
   };
+  // Per-stage op lists (A-21): GPipe — every F(d, i) in order, then every B in exact
+  // reverse; 1F1B at group granularity (TP_FLAG_SCHEDULE_1F1B) — stage k runs
+  // the forwards of its first w_k = min(D, K - k) groups, then alternates the backward of its oldest
+  // group (slices in reverse) with the forward of the next one, then drains; oracle/plan.py
+  // one_f_one_b_oplists is the same list (tests compare the replayed makespans).
+  int inflight(int k, int D) const { return sched_1f1b ? std::min(D, m.K - k) : D; }
+  std::vector<Op> oplist(int k, const std::vector<Group>& G) const {
+    std::vector<int> M;
+    for (const Group& g : G) M.push_back((int)g.len.size());
+    return build_oplist(m.K, k, sched_1f1b, M);
+  }
+  // buffer sequence index of group d on stage k: the group's own sequences (store-all, GPipe) or its
+  // slot (d mod w_k) x the largest group size (1F1B: only w_k groups are ever live on stage k)
+  size_t bseq0(int k, const std::vector<Group>& G, int d) const {
+    if (!sched_1f1b) return G[d].seq0;
+    int bmax = 0;
+    for (const Group& g : G) bmax = std::max(bmax, g.b);
+    return (size_t)(d % inflight(k, (int)G.size())) * bmax;
+  }
+
   tp_status enqueue_step(const std::vector<Group>& G, int batch) {
     const int D = (int)G.size();
     const bool multi = world > 1;
@@ -859,66 +948,98 @@ class Engine final : public EngineBase {
       CU(p2p_epoch_inc(d_epoch, stream));
     }
     unsigned long long* flag_local = reinterpret_cast<unsigned long long*>(p_flag);
-    // forward: F(d, i) for groups d = 0..D-1 (b_d sequences each), slices i = 1..M_d (stage order
-    // inside a job in loopback); a job is b_d*l_i tokens, contiguous rows (see fwd())
-    for (int d = 0; d < D; ++d)
-      for (size_t i = 0; i < G[d].len.size(); ++i)
-        for (size_t si = 0; si < stages.size(); ++si) {
-          Stage<T>& S = stages[si];
-          const int b = G[d].b;
-          const size_t row = G[d].seq0 * m.s + (size_t)G[d].off[i] * b;
-          const int Tn = b * G[d].len[i];
-          const size_t jb = job0[d] + i;
-          if (dev_p2p) {
-            if (S.k > 0) CU(p2p_wait(flag_local + jb, d_epoch, stream));
-            TRY(fwd(S, G[d].seq0, G[d].off[i], G[d].len[i], b, batch, S.k < m.K - 1 ? peer_in + row * m.H : nullptr));
-            if (S.k < m.K - 1) CU(p2p_signal(peer_flag_next + jb, d_epoch, stream));
-            continue;
-          }
-          if (multi && S.k > 0) TRY(recv_fwd(S, row, Tn));
-          TRY(fwd(S, G[d].seq0, G[d].off[i], G[d].len[i], b, batch));
-          if (multi && S.k < m.K - 1) TRY(send_fwd(S, row, Tn));
-          if (nccl_lb && si + 1 < stages.size())
-            TRY(p2p_self(S.hs[S.nl] + row * m.H, stages[si + 1].hs[0] + row * m.H, (size_t)Tn * m.H, true, S.k));
+    // TP_SIDE_DW=1 (GPipe, one stage per GPU, D >= 2): group d's weight gradients go to a low-priority
+    // stream as soon as its last backward job is done. 1F1B: group d's weight gradients run in order
+    // right after its backward on each stage (its stash slot is reused by a later group).
+    const bool side_dw = multi && D >= 2 && s_wgrad && !sched_1f1b;
+    std::vector<int> seen_dw(stages.size(), 0);
+
+    auto run_op = [&](size_t si, const Op& op) -> tp_status {
+      Stage<T>& S = stages[si];
+      const int d = op.d, i = op.i, b = G[d].b;
+      const size_t bs0 = bseq0(S.k, G, d);
+      const size_t row = bs0 * m.s + (size_t)G[d].off[i] * b;  // this stage's rows of the job
+      const int Tn = b * G[d].len[i];
+      const size_t jb = job0[d] + i;
+      if (op.fwd) {
+        float* out_next = nullptr;
+        if (dev_p2p && S.k < m.K - 1) out_next = peer_in + (bseq0(S.k + 1, G, d) * m.s + (size_t)G[d].off[i] * b) * m.H;
+        if (dev_p2p && S.k > 0) CU(p2p_wait(flag_local + jb, d_epoch, stream));
+        else if (multi && S.k > 0) TRY(recv_fwd(S, row, Tn));
+        TRY(fwd(S, G[d].seq0, bs0, G[d].off[i], G[d].len[i], b, batch, out_next));
+        if (dev_p2p && S.k < m.K - 1) CU(p2p_signal(peer_flag_next + jb, d_epoch, stream));
+        else if (multi && S.k < m.K - 1) TRY(send_fwd(S, row, Tn));
+        if (world == 1 && si + 1 < stages.size() && !stages[si + 1].aliased) {
+          // loopback without aliasing: the message to the next owned stage's input rows
+          Stage<T>& R = stages[si + 1];
+          float* dst = R.hs[0] + (bseq0(R.k, G, d) * m.s + (size_t)G[d].off[i] * b) * m.H;
+          if (nccl_lb) TRY(p2p_self(S.hs[S.nl] + row * m.H, dst, (size_t)Tn * m.H, true, S.k));
+          else CU(cudaMemcpyAsync(dst, S.hs[S.nl] + row * m.H, sizeof(float) * Tn * m.H, cudaMemcpyDeviceToDevice, stream));
         }
-    // backward: exact reverse order (GPipe order, A-21). Weight gradients: one K = B*s GEMM per
-    // weight at the end (the last stage's overlaps the other stages' remaining backward); with
-    // TP_SIDE_DW=1, one stage per GPU and D >= 2 groups, group d's go to a low-priority stream as
-    // soon as its last backward job is done.
-    const bool side_dw = multi && D >= 2 && s_wgrad;
-    for (int d = D - 1; d >= 0; --d) {
-      const int M = (int)G[d].len.size(), b = G[d].b;
-      for (int i = M - 1; i >= 0; --i)
-        for (int si = (int)stages.size() - 1; si >= 0; --si) {
-          Stage<T>& S = stages[si];
-          const size_t row = G[d].seq0 * m.s + (size_t)G[d].off[i] * b;
-          const int Tn = b * G[d].len[i];
-          const size_t jb = job0[d] + i;
-          if (dev_p2p) {
-            if (S.k < m.K - 1) CU(p2p_wait(flag_local + n_slots + jb, d_epoch, stream));
-            TRY(bwd(S, G[d].seq0, G[d].off[i], G[d].len[i], b, batch, i == M - 1,
-                    S.k > 0 ? peer_gout + row * m.H : nullptr));
-            if (S.k > 0) CU(p2p_signal(peer_flag_prev + n_slots + jb, d_epoch, stream));
-            continue;
-          }
-          if (multi && S.k < m.K - 1) TRY(recv_bwd(S, row, Tn));
-          TRY(bwd(S, G[d].seq0, G[d].off[i], G[d].len[i], b, batch, i == M - 1));
-          if (multi && S.k > 0) TRY(send_bwd(S, row, Tn));
-          if (nccl_lb && si > 0)
-            TRY(p2p_self(S.grad_in + row * m.H, stages[si - 1].grad_out + row * m.H, (size_t)Tn * m.H, false, S.k - 1));
-        }
-      if (side_dw) {
+        return TP_OK;
+      }
+      const bool first_b = i == (int)G[d].len.size() - 1;  // the slice ending at s: first in backward
+      float* gin_prev = nullptr;
+      if (dev_p2p && S.k > 0) gin_prev = peer_gout + (bseq0(S.k - 1, G, d) * m.s + (size_t)G[d].off[i] * b) * m.H;
+      if (dev_p2p && S.k < m.K - 1) CU(p2p_wait(flag_local + n_slots + jb, d_epoch, stream));
+      else if (multi && S.k < m.K - 1) TRY(recv_bwd(S, row, Tn));
+      TRY(bwd(S, G[d].seq0, bs0, G[d].off[i], G[d].len[i], b, batch, first_b, gin_prev));
+      if (dev_p2p && S.k > 0) CU(p2p_signal(peer_flag_prev + n_slots + jb, d_epoch, stream));
+      else if (multi && S.k > 0) TRY(send_bwd(S, row, Tn));
+      if (world == 1 && si > 0 && !S.aliased) {
+        Stage<T>& R = stages[si - 1];
+        float* dst = R.grad_out + (bseq0(R.k, G, d) * m.s + (size_t)G[d].off[i] * b) * m.H;
+        if (nccl_lb) TRY(p2p_self(S.grad_in + row * m.H, dst, (size_t)Tn * m.H, false, S.k - 1));
+        else CU(cudaMemcpyAsync(dst, S.grad_in + row * m.H, sizeof(float) * Tn * m.H, cudaMemcpyDeviceToDevice, stream));
+      }
+      if (i == 0 && sched_1f1b) {  // group d's backward done on this stage: its weight gradients, in order
+        TRY(wgrad_rows(S, bs0 * m.s, b * m.s, seen_dw[si] > 0, stream, true));
+        ++seen_dw[si];
+      }
+      if (i == 0 && side_dw) {
         cudaEvent_t e = event();
         CU(cudaEventRecord(e, stream));
         CU(cudaStreamWaitEvent(s_wgrad, e, 0));
-        for (auto& S : stages) TRY(wgrad_rows(S, G[d].seq0 * m.s, b * m.s, d != D - 1, s_wgrad, false));
+        TRY(wgrad_rows(S, bs0 * m.s, b * m.s, d != D - 1, s_wgrad, false));
+      }
+      return TP_OK;
+    };
+
+    std::vector<std::vector<Op>> lists;
+    for (auto& S : stages) lists.push_back(oplist(S.k, G));
+    if (stages.size() == 1) {
+      for (const Op& op : lists[0]) TRY(run_op(0, op));
+    } else {
+      // all stages on one stream (loopback): a topological merge of the per-stage lists — an op runs
+      // once its producer (F on the stage before, B on the stage after, or F on the last stage) ran
+      const size_t NS = stages.size();
+      std::vector<size_t> pos(NS, 0);
+      std::vector<std::vector<char>> fdone(NS, std::vector<char>(job0[D], 0)), bdone = fdone;
+      size_t left = 0;
+      for (auto& l : lists) left += l.size();
+      while (left) {
+        bool progressed = false;
+        for (size_t si = 0; si < NS; ++si) {
+          while (pos[si] < lists[si].size()) {
+            const Op& op = lists[si][pos[si]];
+            const size_t jb = job0[op.d] + op.i;
+            const bool ready = op.fwd ? (si == 0 || fdone[si - 1][jb]) : (si + 1 == NS ? fdone[si][jb] : bdone[si + 1][jb]);
+            if (!ready) break;
+            TRY(run_op(si, op));
+            (op.fwd ? fdone : bdone)[si][jb] = 1;
+            ++pos[si];
+            --left;
+            progressed = true;
+          }
+        }
+        if (!progressed) return fail(TP_EINVAL, "tp_step: schedule deadlock (internal)");
       }
     }
     if (side_dw) {
       cudaEvent_t e = event();
       CU(cudaEventRecord(e, s_wgrad));
       CU(cudaStreamWaitEvent(stream, e, 0));
-    } else {
+    } else if (!sched_1f1b) {
       for (auto& S : stages) TRY(wgrad(S, batch));
     }
     // loss: sum of per-token NLL on the last stage, mean over batch*seq_len (A-9)
@@ -944,7 +1065,7 @@ class Engine final : public EngineBase {
 
   tp_status step(const tp_slicing* sl, const int32_t* tokens, bool host_tokens, int batch, float* loss_out) override {
     if (!sl || !sl->lengths) return fail(TP_EINVAL, "tp_step: null slicing");
-    if (batch < 1 || batch > max_batch) return fail(TP_EINVAL, "tp_step: batch %d not in [1, max_batch=%d]", batch, max_batch);
+    if (batch < 1) return fail(TP_EINVAL, "tp_step: batch %d < 1", batch);
     const int b = sl->batch_slice;
     if (b < 1 || batch % b != 0)
       return fail(TP_EINVAL, "tp_step: batch_slice %d must be >= 1 and divide batch %d", b, batch);
@@ -967,8 +1088,7 @@ class Engine final : public EngineBase {
   tp_status step_plan(const tp_batch_plan* pl, const int32_t* tokens, bool host_tokens, int batch,
                       float* loss_out) override {
     if (!pl || !pl->batch_slice || !pl->n_slices || !pl->lengths) return fail(TP_EINVAL, "tp_step_plan: null plan");
-    if (batch < 1 || batch > max_batch)
-      return fail(TP_EINVAL, "tp_step_plan: batch %d not in [1, max_batch=%d]", batch, max_batch);
+    if (batch < 1) return fail(TP_EINVAL, "tp_step_plan: batch %d < 1", batch);
     if (pl->n_groups < 1 || pl->n_groups > batch) return fail(TP_EINVAL, "tp_step_plan: n_groups %d", pl->n_groups);
     if (pl->n_groups > pl->capacity_groups)
       return fail(TP_EINVAL, "tp_step_plan: n_groups %d exceeds capacity_groups %d", pl->n_groups, pl->capacity_groups);
@@ -1001,6 +1121,22 @@ class Engine final : public EngineBase {
                      float* loss_out) {
     if (!tokens) return fail(TP_EINVAL, "tp_step: null tokens");
     CU(cudaSetDevice(device));
+    // capacity: store-all (GPipe) holds the whole batch in the stage buffers (batch <= max_batch);
+    // 1F1B holds at most w_k = min(D, K - k) groups per stage, so the batch may exceed max_batch as
+    // long as w_k * (largest group) <= max_batch on every owned stage (the memory bound of 1F1B)
+    int bmax = 0;
+    for (const Group& g : G) bmax = std::max(bmax, g.b);
+    if (!sched_1f1b) {
+      if (batch > max_batch) return fail(TP_EINVAL, "tp_step: batch %d > max_batch %d", batch, max_batch);
+    } else {
+      for (auto& S : stages)
+        if ((size_t)inflight(S.k, (int)G.size()) * bmax > (size_t)max_batch)
+          return fail(TP_EINVAL, "tp_step (1F1B): stage %d holds %d groups of up to %d sequences > max_batch %d", S.k,
+                      inflight(S.k, (int)G.size()), bmax, max_batch);
+      if ((flags & TP_FLAG_KEEP_LOGITS) && batch > max_batch)
+        return fail(TP_EINVAL, "tp_step: TP_FLAG_KEEP_LOGITS keeps at most max_batch = %d sequences", max_batch);
+    }
+    TRY(ensure_batch_capacity(batch));
     last_batch = batch;
     last_groups.clear();
     for (const Group& g : G) last_groups.push_back({g.seq0, g.b});
@@ -1134,10 +1270,10 @@ tp_status Engine<T>::profile_stage(Stage<T>& S, int g, int bsl, int reps, std::v
     std::vector<float> v;
     for (int r = 0; r < reps + 2; ++r) {
       CU(cudaEventRecord(e0, stream));
-      TRY(fwd(S, 0, c, l, bsl, bsl));
+      TRY(fwd(S, 0, 0, c, l, bsl, bsl));
       // as the step runs it: the slice ending at s (the first in backward) stores dK/dV, every other
       // slice reduce-adds into the c + l prefix rows
-      TRY(bwd(S, 0, c, l, bsl, bsl, c + l == m.s));
+      TRY(bwd(S, 0, 0, c, l, bsl, bsl, c + l == m.s));
       CU(cudaEventRecord(e1, stream));
       CU(cudaEventSynchronize(e1));
       float ms = 0;
@@ -1446,6 +1582,27 @@ extern "C" tp_status tp_stage_param_count(const tp_model_cfg* cfg, int32_t stage
   ModelShape m{cfg->n_layer, cfg->hidden, cfg->n_head, cfg->n_head ? cfg->hidden / cfg->n_head : 0,
                cfg->vocab, cfg->seq_len, cfg->n_stages};
   *out = stage_layout(m, stage).total;
+  return TP_OK;
+}
+
+extern "C" tp_status tp_schedule_oplist(int32_t n_stages, int32_t stage, int32_t schedule, int32_t n_groups,
+                                        const int32_t* n_slices, int32_t capacity, int32_t* ops_out, int32_t* n_ops) {
+  TP_CHECK_ARG(n_stages >= 1 && stage >= 0 && stage < n_stages, "tp_schedule_oplist: bad stage %d of %d", stage, n_stages);
+  TP_CHECK_ARG(schedule == 0 || schedule == 1, "tp_schedule_oplist: schedule %d", schedule);
+  TP_CHECK_ARG(n_groups >= 1 && n_slices && ops_out && n_ops, "tp_schedule_oplist: null / empty argument");
+  std::vector<int> M(n_slices, n_slices + n_groups);
+  std::vector<int> first(n_groups + 1, 0);
+  for (int d = 0; d < n_groups; ++d) {
+    TP_CHECK_ARG(M[d] >= 1, "tp_schedule_oplist: group %d has %d slices", d, M[d]);
+    first[d + 1] = first[d] + M[d];
+  }
+  TP_CHECK_ARG(capacity >= 2 * first[n_groups], "tp_schedule_oplist: capacity %d < %d", capacity, 2 * first[n_groups]);
+  const std::vector<Op> ops = build_oplist(n_stages, stage, schedule == 1, M);
+  for (size_t t = 0; t < ops.size(); ++t) {
+    const int j = first[ops[t].d] + ops[t].i;
+    ops_out[t] = ops[t].fwd ? j + 1 : -(j + 1);
+  }
+  *n_ops = (int32_t)ops.size();
   return TP_OK;
 }
 

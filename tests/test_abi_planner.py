@@ -197,3 +197,29 @@ def test_plan_joint_rejects_bad_input():
 def test_batch_plan_notation():
     p = tp.BatchPlan([(2, [384, 384]), (2, [384, 384]), (1, [768])])
     assert p.notation() == "[(2, [384, 384])] * 2 + [(1, [768])] * 1" and p.batch() == 5
+
+
+# ---------------------------------------------------------------- schedules (A-21)
+@pytest.mark.parametrize("seed", range(30))
+def test_schedule_oplist_equals_oracle(seed):
+    """tp_schedule_oplist (the op lists tp_step executes) equals oracle/plan.py's GPipe and 1F1B lists
+    on every stage, and the 1F1B lists never deadlock and keep at most min(D, K - k) groups live."""
+    rng = np.random.default_rng(300 + seed)
+    K = int(rng.integers(1, 7))
+    groups = [int(x) for x in rng.integers(1, 5, size=int(rng.integers(1, 7)))]
+    ref_g, ref_1 = op.gpipe_oplists(groups, K), op.one_f_one_b_oplists(groups, K)
+    for k in range(K):
+        assert tp.schedule_oplist(K, k, groups, False) == ref_g[k]
+        assert tp.schedule_oplist(K, k, groups, True) == ref_1[k]
+    lists = [tp.schedule_oplist(K, k, groups, True) for k in range(K)]
+    J = sum(groups)
+    ms = op.oplist_replay(lists, [[1.0] * J] * K, [[2.0] * J] * K)
+    assert ms > 0
+    assert op.max_inflight_groups(lists, groups) == [min(len(groups), K - k) for k in range(K)]
+
+
+def test_schedule_oplist_rejects_bad_input():
+    with pytest.raises(tp.TpError):
+        tp.schedule_oplist(2, 2, [1], True)
+    with pytest.raises(tp.TpError):
+        tp.schedule_oplist(2, 0, [0, 1], True)

@@ -60,6 +60,14 @@ def test_device_initiated_p2p(world, cfg, lengths, batch, tmp_path):
         assert max(errs.values()) < 2e-2, errs
 
 
+@pytest.mark.parametrize("world,env", [(2, {"TP_SCHEDULE": "1f1b"}), (4, {"TP_SCHEDULE": "1f1b"}),
+                                       (4, {"TP_SCHEDULE": "1f1b", "TP_DEVICE_P2P": "1"})])
+def test_1f1b_nccl(world, env, tmp_path):
+    """1F1B over NCCL (and over device-initiated p2p): four groups of b = 1, one stage per GPU."""
+    for errs in run(world, "small", "bf16", "1:40,24,64;1:40,24,64;1:40,24,64;1:40,24,64", tmp_path, env=env, batch=4):
+        assert max(errs.values()) < 2e-2, errs
+
+
 def test_small_four_stages_nccl(tmp_path):
     for errs in run(4, "small", "bf16", "40,24,64", tmp_path):
         assert max(errs.values()) < 2e-2, errs

@@ -287,3 +287,51 @@ def test_profile_stage_types_comm_term_and_wgrad(monkeypatch):
         assert e.value.status == tp.TP_ESTATE
     finally:
         ctx.close()
+
+
+# ---------------------------------------------------------------- 1F1B schedule
+@pytest.mark.parametrize("K,groups,flags", [
+    (2, [(1, [40, 24, 64])] * 4, 0),
+    (4, [(1, [40, 24, 64])] * 4, 0),
+    (4, [(2, [40, 24, 64]), (1, [128]), (1, [8] * 16)], 0),
+    (2, [(1, [64, 64])] * 4, tp.TP_FLAG_NCCL_LOOPBACK),
+])
+@pytest.mark.parametrize("precision,tol", [(tp.TP_BF16, 2e-2), (tp.TP_FP32, 1e-4)])
+def test_1f1b_schedule_parity(K, groups, flags, precision, tol):
+    """TP_FLAG_SCHEDULE_1F1B: the group-granular 1F1B op lists (tp_schedule_oplist), slot-mapped stage
+    buffers and per-group weight gradients compute the same function as the unsliced oracle."""
+    cfg = SMALL.with_(n_stages=K)
+    B = sum(b for b, _ in groups)
+    params, tokens, ref = oracle_run(cfg, B, 9, precision == tp.TP_BF16)
+    loss, logits, grads = gpu_run_plan(cfg, B, params, tokens, groups, precision,
+                                       flags=tp.TP_FLAG_KEEP_LOGITS | tp.TP_FLAG_SCHEDULE_1F1B | flags)
+    check(worst_errors(loss, logits, grads, ref), tol)
+
+
+def test_1f1b_batch_exceeds_max_batch():
+    """1F1B bounds the stage memory: stage k holds w_k = min(D, K - k) groups, so with K = 2 a batch of
+    6 single-sequence groups runs in buffers sized for max_batch = 2 (GPipe would need 6), with the
+    same loss and gradients as the oracle; GPipe rejects it."""
+    from synth import pack_all_stages, unpack_all_stages
+    cfg = SMALL.with_(n_stages=2)
+    B = 6
+    params, tokens, ref = oracle_run(cfg, B, 14, True)
+    ctx = tp.Context(cfg, precision=tp.TP_BF16, max_batch=2, device=0, flags=tp.TP_FLAG_SCHEDULE_1F1B)
+    try:
+        ctx.load_params(pack_all_stages(params, cfg))
+        losses = [ctx.step(tp.Slicing([40, 24, 64]), tokens) for _ in range(3)]  # eager, capture, replay
+        grads = unpack_all_stages(ctx.grads(), cfg)
+    finally:
+        ctx.close()
+    errs = {"loss": abs(losses[-1] - ref["loss"]) / abs(ref["loss"])}
+    errs.update({k: rel(grads[k], g) for k, g in ref["grads"].items()})
+    check(errs, 2e-2)
+    assert abs(losses[0] - losses[2]) <= 1e-5 * abs(losses[0])
+    ctx = tp.Context(cfg, precision=tp.TP_BF16, max_batch=2, device=0)
+    try:
+        ctx.load_params(pack_all_stages(params, cfg))
+        with pytest.raises(tp.TpError) as e:
+            ctx.step(tp.Slicing([40, 24, 64]), tokens)
+        assert e.value.status == tp.TP_EINVAL
+    finally:
+        ctx.close()
