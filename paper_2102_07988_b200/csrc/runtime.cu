@@ -466,8 +466,6 @@ class Engine final : public EngineBase {
     if (g_exec) { cudaGraphExecDestroy(g_exec); g_exec = nullptr; g_key.clear(); }
     if (d_tokens) cudaFree(d_tokens);
     if (h_tokens) cudaFreeHost(h_tokens);
-    if (d_tokens) cudaFree(d_tokens);
-    for (auto& S : stages) if (S.loss_rows) cudaFree(S.loss_rows);
     d_tokens = nullptr; h_tokens = nullptr;
     const size_t n = (size_t)batch * (m.s + 1);
     if (cudaMalloc(&d_tokens, n * sizeof(int32_t)) != cudaSuccess) return fail(TP_ENOMEM, "tokens: cudaMalloc");
@@ -618,23 +616,27 @@ class Engine final : public EngineBase {
   // buffer (peer memory) from the last layer's FC2 epilogue instead of S.hs[nl]
   // tseq0: the job's first sequence in the batch (tokens, loss rows, kept logits); seq0: its first
   // sequence in this stage's buffers (= tseq0 store-all; the group's slot under 1F1B)
-  tp_status fwd(Stage<T>& S, size_t tseq0, size_t seq0, int c, int l, int b, int batch, float* out_next = nullptr) {
+  // in_seq0: its first sequence in the stage INPUT buffer hs[0], which the previous stage fills
+  // (1F1B: a slot of the sender's in-flight window, one more than this stage's own)
+  tp_status fwd(Stage<T>& S, size_t tseq0, size_t seq0, size_t in_seq0, int c, int l, int b, int batch,
+                float* out_next = nullptr) {
     const int H = m.H, s = m.s, a = m.a, dh = m.d, V = m.V;
     const int Tn = b * l;
     const size_t row = seq0 * s + (size_t)c * b;  // first buffer row of this job
+    const size_t row_in = in_seq0 * s + (size_t)c * b;  // its first row in hs[0]
     const size_t trow = tseq0 * s + (size_t)c * b;  // first batch row of this job
     const size_t cap = (size_t)max_batch * s;      // rows of the stage buffers (LN stats: mean | rstd)
     const int32_t* tok0 = d_tokens + tseq0 * (s + 1);
     const double ebytes = sizeof(T);
     if (S.k == 0) {
       TRY(launch(KC_EMBED, 0, 8.0 * Tn * H, [&] {
-        return embed_fwd(tok0, S.psmall + S.L.s_wte, S.psmall + S.L.s_wpe, S.hs[0] + row * H, c, l, b, s, H, V, stream);
+        return embed_fwd(tok0, S.psmall + S.L.s_wte, S.psmall + S.L.s_wpe, S.hs[0] + row_in * H, c, l, b, s, H, V, stream);
       }));
     }
     for (int j = 0; j < S.nl; ++j) {
       const SmallOff& f = S.L.small[j];
       const float* P = S.psmall;
-      float* x = S.hs[j] + row * H;
+      float* x = S.hs[j] + (j == 0 ? row_in : row) * H;
       float* st1 = S.st1[j];
       TRY(launch(KC_LN, 0, (4.0 + ebytes) * Tn * H, [&] {
         return layernorm_fwd<T>(x, P + f.ln1_g, P + f.ln1_b, S.A1[j] + row * H, st1 + row, st1 + cap + row, Tn, H, stream);
@@ -702,11 +704,12 @@ class Engine final : public EngineBase {
   // ------------------------------------------------------------ backward of one job on one stage
   // gin_prev (device p2p): the input-gradient rows of this job go straight into the previous stage's
   // grad_out buffer (peer memory) from the first layer's LayerNorm backward instead of S.grad_in
-  tp_status bwd(Stage<T>& S, size_t tseq0, size_t seq0, int c, int l, int b, int batch, bool first_bwd_slice,
-                float* gin_prev = nullptr) {
+  tp_status bwd(Stage<T>& S, size_t tseq0, size_t seq0, size_t in_seq0, int c, int l, int b, int batch,
+                bool first_bwd_slice, float* gin_prev = nullptr) {
     const int H = m.H, s = m.s, a = m.a, dh = m.d, V = m.V;
     const int Tn = b * l;
     const size_t row = seq0 * s + (size_t)c * b;
+    const size_t row_in = in_seq0 * s + (size_t)c * b;
     const size_t cap = (size_t)max_batch * s;
     const int32_t* tok0 = d_tokens + tseq0 * (s + 1);
     const double ebytes = sizeof(T);
@@ -791,7 +794,7 @@ class Engine final : public EngineBase {
       T* copy = j == 0 ? nullptr : S.dhout_b[j - 1] + row * H;
       float* st1 = S.st1[j];
       TRY(launch(KC_LN, 0, (16.0 + ebytes) * Tn * H, [&] {
-        return layernorm_bwd<T>(reinterpret_cast<const T*>(S.dA), S.hs[j] + row * H, st1 + row, st1 + cap + row, P + fs.ln1_g, S.gm, gnext, copy,
+        return layernorm_bwd<T>(reinterpret_cast<const T*>(S.dA), S.hs[j] + (j == 0 ? row_in : row) * H, st1 + row, st1 + cap + row, P + fs.ln1_g, S.gm, gnext, copy,
                                 GR + f.ln1_g, GR + f.ln1_b, S.lnws, Tn, H, stream,
                                 j == 0 ? nullptr : GR + S.L.layers[j - 1].b_2);
       }));
@@ -932,6 +935,16 @@ class Engine final : public EngineBase {
     return (size_t)(d % inflight(k, (int)G.size())) * bmax;
   }
 
+  // hs[0] of stage k > 0 is written by stage k-1 when IT runs F(d); under 1F1B that can happen before
+  // this stage has finished with group d - w_k, so the input buffer cycles through w_{k-1} = w_k + 1
+  // slots (stage k-1's window; F(d) on k-1 follows B(d - w_{k-1}) on k-1, hence on k)
+  size_t in_bseq0(int k, const std::vector<Group>& G, int d) const {
+    if (!sched_1f1b) return G[d].seq0;
+    int bmax = 0;
+    for (const Group& g : G) bmax = std::max(bmax, g.b);
+    return (size_t)(d % inflight(k > 0 ? k - 1 : 0, (int)G.size())) * bmax;
+  }
+
   tp_status enqueue_step(const std::vector<Group>& G, int batch) {
     const int D = (int)G.size();
     const bool multi = world > 1;
@@ -957,22 +970,23 @@ class Engine final : public EngineBase {
     auto run_op = [&](size_t si, const Op& op) -> tp_status {
       Stage<T>& S = stages[si];
       const int d = op.d, i = op.i, b = G[d].b;
-      const size_t bs0 = bseq0(S.k, G, d);
+      const size_t bs0 = bseq0(S.k, G, d), is0 = in_bseq0(S.k, G, d);
       const size_t row = bs0 * m.s + (size_t)G[d].off[i] * b;  // this stage's rows of the job
+      const size_t row_in = is0 * m.s + (size_t)G[d].off[i] * b;  // ... in its input buffer hs[0]
       const int Tn = b * G[d].len[i];
       const size_t jb = job0[d] + i;
       if (op.fwd) {
         float* out_next = nullptr;
-        if (dev_p2p && S.k < m.K - 1) out_next = peer_in + (bseq0(S.k + 1, G, d) * m.s + (size_t)G[d].off[i] * b) * m.H;
+        if (dev_p2p && S.k < m.K - 1) out_next = peer_in + (in_bseq0(S.k + 1, G, d) * m.s + (size_t)G[d].off[i] * b) * m.H;
         if (dev_p2p && S.k > 0) CU(p2p_wait(flag_local + jb, d_epoch, stream));
-        else if (multi && S.k > 0) TRY(recv_fwd(S, row, Tn));
-        TRY(fwd(S, G[d].seq0, bs0, G[d].off[i], G[d].len[i], b, batch, out_next));
+        else if (multi && S.k > 0) TRY(recv_fwd(S, row_in, Tn));
+        TRY(fwd(S, G[d].seq0, bs0, is0, G[d].off[i], G[d].len[i], b, batch, out_next));
         if (dev_p2p && S.k < m.K - 1) CU(p2p_signal(peer_flag_next + jb, d_epoch, stream));
         else if (multi && S.k < m.K - 1) TRY(send_fwd(S, row, Tn));
         if (world == 1 && si + 1 < stages.size() && !stages[si + 1].aliased) {
           // loopback without aliasing: the message to the next owned stage's input rows
           Stage<T>& R = stages[si + 1];
-          float* dst = R.hs[0] + (bseq0(R.k, G, d) * m.s + (size_t)G[d].off[i] * b) * m.H;
+          float* dst = R.hs[0] + (in_bseq0(R.k, G, d) * m.s + (size_t)G[d].off[i] * b) * m.H;
           if (nccl_lb) TRY(p2p_self(S.hs[S.nl] + row * m.H, dst, (size_t)Tn * m.H, true, S.k));
           else CU(cudaMemcpyAsync(dst, S.hs[S.nl] + row * m.H, sizeof(float) * Tn * m.H, cudaMemcpyDeviceToDevice, stream));
         }
@@ -983,7 +997,7 @@ class Engine final : public EngineBase {
       if (dev_p2p && S.k > 0) gin_prev = peer_gout + (bseq0(S.k - 1, G, d) * m.s + (size_t)G[d].off[i] * b) * m.H;
       if (dev_p2p && S.k < m.K - 1) CU(p2p_wait(flag_local + n_slots + jb, d_epoch, stream));
       else if (multi && S.k < m.K - 1) TRY(recv_bwd(S, row, Tn));
-      TRY(bwd(S, G[d].seq0, bs0, G[d].off[i], G[d].len[i], b, batch, first_b, gin_prev));
+      TRY(bwd(S, G[d].seq0, bs0, is0, G[d].off[i], G[d].len[i], b, batch, first_b, gin_prev));
       if (dev_p2p && S.k > 0) CU(p2p_signal(peer_flag_prev + n_slots + jb, d_epoch, stream));
       else if (multi && S.k > 0) TRY(send_bwd(S, row, Tn));
       if (world == 1 && si > 0 && !S.aliased) {
@@ -1129,10 +1143,12 @@ class Engine final : public EngineBase {
     if (!sched_1f1b) {
       if (batch > max_batch) return fail(TP_EINVAL, "tp_step: batch %d > max_batch %d", batch, max_batch);
     } else {
-      for (auto& S : stages)
-        if ((size_t)inflight(S.k, (int)G.size()) * bmax > (size_t)max_batch)
-          return fail(TP_EINVAL, "tp_step (1F1B): stage %d holds %d groups of up to %d sequences > max_batch %d", S.k,
-                      inflight(S.k, (int)G.size()), bmax, max_batch);
+      for (auto& S : stages) {
+        const int w = std::max(inflight(S.k, (int)G.size()), S.k > 0 ? inflight(S.k - 1, (int)G.size()) : 0);
+        if ((size_t)w * bmax > (size_t)max_batch)
+          return fail(TP_EINVAL, "tp_step (1F1B): stage %d holds %d groups of up to %d sequences > max_batch %d", S.k, w,
+                      bmax, max_batch);
+      }
       if ((flags & TP_FLAG_KEEP_LOGITS) && batch > max_batch)
         return fail(TP_EINVAL, "tp_step: TP_FLAG_KEEP_LOGITS keeps at most max_batch = %d sequences", max_batch);
     }
@@ -1270,10 +1286,10 @@ tp_status Engine<T>::profile_stage(Stage<T>& S, int g, int bsl, int reps, std::v
     std::vector<float> v;
     for (int r = 0; r < reps + 2; ++r) {
       CU(cudaEventRecord(e0, stream));
-      TRY(fwd(S, 0, 0, c, l, bsl, bsl));
+      TRY(fwd(S, 0, 0, 0, c, l, bsl, bsl));
       // as the step runs it: the slice ending at s (the first in backward) stores dK/dV, every other
       // slice reduce-adds into the c + l prefix rows
-      TRY(bwd(S, 0, 0, c, l, bsl, bsl, c + l == m.s));
+      TRY(bwd(S, 0, 0, 0, c, l, bsl, bsl, c + l == m.s));
       CU(cudaEventRecord(e1, stream));
       CU(cudaEventSynchronize(e1));
       float ms = 0;

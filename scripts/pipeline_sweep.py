@@ -47,9 +47,11 @@ def main():
     peak = load_peaks()[0]
     flops = model_flops(cfg, B)
 
-    ticks, fit = ctx.profile(args.granularity, reps=5, batch_slice=b)
     if world > 1:
-        ticks = tdist.bottleneck_table(ticks)
+        ctx.profile_comm(reps=5)  # alpha / beta of a stage message, folded into the table
+    # bottleneck table: max over the stage types / ranks inside the library (A-16)
+    ticks, fit = ctx.profile(args.granularity, reps=5, batch_slice=b)
+    wgrad = ctx.profile_wgrad(B, reps=3)
     dp = tp.plan(ticks, args.granularity, cfg.n_layer, cfg.hidden, cfg.seq_len, world, n_micro=B // b)
     schemes = [("dp", tp.Slicing(dp.lengths, b, dp.t_max, dp.predicted))]
     for m in [int(x) for x in args.uniform.split(",")]:
@@ -71,6 +73,7 @@ def main():
         ms = e0.elapsed_time(e1) / args.steps
         return tdist.max_over_ranks(ms) if world > 1 else ms
 
+    rows = []
     for name, sl in schemes:
         ms = timed(sl)
         # predicted T of this scheme from the same table (Eq. 5 with D = B/b)
@@ -79,10 +82,19 @@ def main():
             ts.append(int(ticks[l // g - 1, c // g]))
             c += l
         pred = (B // b) * sum(ts) + (world - 1) * max(ts)
+        rows.append((name, ms, pred))
         if rank == 0:
             print(json.dumps({"config": args.config, "stages": world, "scheme": name, "slicing": sl.notation(B),
                               "ms_per_step": ms, "mfu": flops / (ms / 1e3) / (world * peak * 1e12),
-                              "predicted_ms": pred / 1e6}), flush=True)
+                              "predicted_ms": pred / 1e6, "predicted_step_ms": (pred + wgrad) / 1e6}), flush=True)
+    # SPEC.md:165 "DP dominates uniform" at the model level: the DP scheme's measured step vs the best
+    # uniform scheme's, with a 3 % allowance for run-to-run noise
+    dp_ms = rows[0][1]
+    best = min(rows[1:], key=lambda r: r[1]) if len(rows) > 1 else rows[0]
+    if rank == 0:
+        print(json.dumps({"config": args.config, "stages": world, "summary": True, "dp_ms": dp_ms,
+                          "best_uniform": best[0], "best_uniform_ms": best[1], "dp_over_best_uniform": dp_ms / best[1],
+                          "dp_le_best_uniform_within_3pct": dp_ms <= 1.03 * best[1]}), flush=True)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()

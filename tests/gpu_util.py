@@ -45,9 +45,9 @@ def worst_errors(loss, logits, grads, ref):
     return errs
 
 
-def gpu_run_plan(cfg, B, params, tokens, groups, precision, flags=tp.TP_FLAG_KEEP_LOGITS):
+def gpu_run_plan(cfg, B, params, tokens, groups, precision, flags=tp.TP_FLAG_KEEP_LOGITS, max_batch=None):
     """One step with a heterogeneous batch plan [(b_d, lengths_d), ..] (tp_step_plan)."""
-    ctx = tp.Context(cfg, precision=precision, max_batch=B, device=0, flags=flags)
+    ctx = tp.Context(cfg, precision=precision, max_batch=max_batch or B, device=0, flags=flags)
     try:
         ctx.load_params(pack_all_stages(params, cfg))
         loss = ctx.step_plan(tp.BatchPlan(groups), tokens)

@@ -303,8 +303,10 @@ def test_1f1b_schedule_parity(K, groups, flags, precision, tol):
     cfg = SMALL.with_(n_stages=K)
     B = sum(b for b, _ in groups)
     params, tokens, ref = oracle_run(cfg, B, 9, precision == tp.TP_BF16)
+    # 1F1B slots hold the largest group: w_k x max b sequences per stage (here <= 2 x B)
     loss, logits, grads = gpu_run_plan(cfg, B, params, tokens, groups, precision,
-                                       flags=tp.TP_FLAG_KEEP_LOGITS | tp.TP_FLAG_SCHEDULE_1F1B | flags)
+                                       flags=tp.TP_FLAG_KEEP_LOGITS | tp.TP_FLAG_SCHEDULE_1F1B | flags,
+                                       max_batch=2 * B)
     check(worst_errors(loss, logits, grads, ref), tol)
 
 
