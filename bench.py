@@ -172,7 +172,10 @@ def main():
     base_cfg, B0 = CONFIGS[args.config]
     B = args.batch or B0
     K = max(world, 1)
-    cfg = base_cfg.with_(n_stages=K)
+    # stage partition: balanced for the LM head by default (A-30; identical to uniform cells
+    # when the head is lighter than a layer, e.g. 13B); TP_PARTITION=uniform for n/K layers per stage
+    part = 0 if os.environ.get("TP_PARTITION", "balanced") == "uniform" else 1
+    cfg = base_cfg.with_(n_stages=K, partition=part)
 
     if args.impl == "reference":
         # The reference arm is the CPU oracle (tier framing): rank 0 only, on the host cores.
@@ -211,8 +214,12 @@ def main():
         return tdist.sum_over_ranks(x) if world > 1 else x
 
     stage = rank if world > 1 else 0
+    # stage messages (world > 1): device-initiated p2p over NCCL symmetric windows by default (the
+    # producing kernels store into the neighbour's buffer; measured faster than
+    # ncclSend/ncclRecv on 4 x B200); TP_DEVICE_P2P=0 selects ncclSend/ncclRecv
+    p2p_device = world > 1 and os.environ.get("TP_DEVICE_P2P", "1") != "0"
     ctx = tp.Context(cfg, rank=rank, world=world, nccl_id=nid, precision=tp.TP_BF16, max_batch=B,
-                     device=local_rank, flags=0)
+                     device=local_rank, flags=tp.TP_FLAG_DEVICE_P2P if p2p_device else 0)
     flat = make_stage_flat(cfg, stage, seed=0) if world > 1 else np.concatenate(
         [make_stage_flat(cfg, k, seed=0) for k in range(K)])
     ctx.load_params(flat)
@@ -327,6 +334,9 @@ def main():
         "config": {"workload": args.config, "n_layer": cfg.n_layer, "hidden": cfg.hidden, "heads": cfg.n_head,
                    "seq_len": cfg.seq_len, "batch": B, "vocab": cfg.vocab, "stages": K,
                    "parallelism": f"pipeline{K}", "slicing": main_sl.notation(), "granularity": g,
+                   "p2p": ("device" if p2p_device else "nccl") if world > 1 else None,
+                   "stage_layers": tp.stage_layers(cfg),
+                   "schedule": "1f1b" if os.environ.get("TP_SCHEDULE") == "1f1b" else "gpipe",
                    "l2": "working set > L2 (bf16 weights alone exceed 126 MB); no flush"},
         "mfu": mfu, "mfu_sustained_peak": flops / (ms / 1e3) / (args.gpus * peak_sust * 1e12),
         "gpipe": None if ms_gpipe is None else {

@@ -23,7 +23,8 @@
  * Parameter layout (shared DATA, not code, with oracle/ and synth/): for stage k of K, one flat
  * float32 array, in this order —
  *     stage 0 only:   wte[V][H], wpe[s][H]
- *     each owned layer l (layers k*n/K .. (k+1)*n/K - 1, uniform cells):
+ *     each owned layer l (stage k's contiguous block: k*n/K .. (k+1)*n/K - 1 for uniform cells,
+ *       PAPER.md:193-194; tp_stage_layers for TP_PARTITION_BALANCED):
  *         ln1_g[H], ln1_b[H], w_qkv[H][3H], b_qkv[3H], w_o[H][H], b_o[H],
  *         ln2_g[H], ln2_b[H], w_1[H][4H], b_1[4H], w_2[4H][H], b_2[H]
  *       (matrices row-major [in][out]; w_qkv columns are [q | k | v], head j at j*d..(j+1)*d)
@@ -81,11 +82,21 @@ enum { TP_FLAG_KEEP_LOGITS = 1,   /* keep fp32 logits of the last step for tp_ge
                                      exceed max_batch as long as w_k x (largest group) <= max_batch;
                                      env TP_SCHEDULE=1f1b sets it too                              */ };
 
-/* Model shape. n_layer % n_stages == 0; hidden % n_head == 0; head_dim = hidden / n_head must be
- * a multiple of 16 and <= 128; hidden % 64 == 0; seq_len >= 1. */
+enum { TP_PARTITION_UNIFORM = 0,  /* stage k owns n_layer / n_stages layers   */
+       TP_PARTITION_BALANCED = 1  /* the last stage, which also runs the LM head + CE, owns fewer
+                                     layers so the per-stage FLOPs balance (A-30;
+                                     counts: tp_stage_layers)                                      */ };
+
+/* Model shape. hidden % n_head == 0; head_dim = hidden / n_head must be a multiple of 16 and <= 128;
+ * hidden % 64 == 0; seq_len >= 1; partition TP_PARTITION_UNIFORM (n_layer % n_stages == 0) or
+ * TP_PARTITION_BALANCED (n_layer >= n_stages). Stage k owns a contiguous block of layers. */
 typedef struct {
   int32_t n_layer, hidden, n_head, vocab, seq_len, n_stages;
+  int32_t partition;
 } tp_model_cfg;
+
+/* Layers owned by each stage (counts_out[n_stages], in stage order) under cfg->partition. */
+tp_status tp_stage_layers(const tp_model_cfg* cfg, int32_t* counts_out);
 
 /* Cost table t_{fwd+bwd}(l, c) of ONE pipeline stage (the bottleneck stage; A-16), in
  * integer ticks (A-15). l and c are in units of `granularity` tokens (g | seq_len, n_units =
@@ -121,7 +132,7 @@ typedef struct {
  * on strict improvement; stop once (n_micro + K - 1) * t_max >= best (A-14).
  * eps_ticks = 0 gives the exact optimum, identical (T and boundaries) to brute force over all
  * compositions with the tie-break (T, max t, reversed lengths). n_layer and hidden are validated
- * (n_layer % n_stages == 0, hidden > 0) and otherwise informational. Pure, deterministic,
+ * (n_layer >= n_stages, hidden > 0) and otherwise informational. Pure, deterministic,
  * thread-safe. Threads: env TP_PLAN_THREADS (default: hardware concurrency, max 64).
  * Errors: TP_EINVAL (shape, table, capacity), TP_EINFEASIBLE (cannot happen for valid tables). */
 tp_status tp_plan(int32_t n_layer, int32_t hidden, int32_t seq_len, int32_t n_stages,

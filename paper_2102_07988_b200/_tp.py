@@ -17,8 +17,9 @@ TP_OK, TP_EINVAL, TP_EINFEASIBLE, TP_ETOOBIG, TP_ECUDA, TP_ENCCL, TP_ENOMEM, TP_
 TP_BF16, TP_FP32 = 0, 1
 TP_FLAG_KEEP_LOGITS, TP_FLAG_KERNEL_STATS, TP_FLAG_FORCE_SIMT, TP_FLAG_NCCL_LOOPBACK, TP_FLAG_DEVICE_P2P = 1, 2, 4, 8, 16
 TP_FLAG_SCHEDULE_1F1B = 32
+TP_PARTITION_UNIFORM, TP_PARTITION_BALANCED = 0, 1
 
-EXPORTED = ["tp_plan", "tp_plan_joint", "tp_schedule_oplist", "tp_step_plan", "tp_step_plan_device", "tp_stage_param_count", "tp_nccl_unique_id", "tp_init", "tp_param_count",
+EXPORTED = ["tp_plan", "tp_plan_joint", "tp_schedule_oplist", "tp_stage_layers", "tp_step_plan", "tp_step_plan_device", "tp_stage_param_count", "tp_nccl_unique_id", "tp_init", "tp_param_count",
             "tp_load_params", "tp_step", "tp_step_device", "tp_get_grads", "tp_get_logits",
             "tp_profile", "tp_profile_wgrad", "tp_profile_comm", "tp_get_stream", "tp_kernel_stats", "tp_kernel_stats_reset", "tp_kernel_stats_enable",
             "tp_last_step_launches", "tp_destroy", "tp_last_error"]
@@ -33,7 +34,7 @@ class TpError(RuntimeError):
 
 class ModelCfgC(C.Structure):
     _fields_ = [("n_layer", C.c_int32), ("hidden", C.c_int32), ("n_head", C.c_int32),
-                ("vocab", C.c_int32), ("seq_len", C.c_int32), ("n_stages", C.c_int32)]
+                ("vocab", C.c_int32), ("seq_len", C.c_int32), ("n_stages", C.c_int32), ("partition", C.c_int32)]
 
 
 class CostTableC(C.Structure):
@@ -67,6 +68,7 @@ def _load() -> C.CDLL:
         "tp_step_plan": (C.c_int, [P, C.POINTER(BatchPlanC), P, C.c_int32, C.POINTER(C.c_float)]),
         "tp_step_plan_device": (C.c_int, [P, C.POINTER(BatchPlanC), P, C.c_int32, C.POINTER(C.c_float)]),
         "tp_stage_param_count": (C.c_int, [C.POINTER(ModelCfgC), C.c_int32, C.POINTER(C.c_size_t)]),
+        "tp_stage_layers": (C.c_int, [C.POINTER(ModelCfgC), C.POINTER(C.c_int32)]),
         "tp_schedule_oplist": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32,
                                          C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
         "tp_nccl_unique_id": (C.c_int, [P]),
@@ -115,7 +117,8 @@ def _check(st: int) -> None:
 
 
 def _cfg(cfg) -> ModelCfgC:
-    return ModelCfgC(cfg.n_layer, cfg.hidden, cfg.n_head, cfg.vocab, cfg.seq_len, cfg.n_stages)
+    return ModelCfgC(cfg.n_layer, cfg.hidden, cfg.n_head, cfg.vocab, cfg.seq_len, cfg.n_stages,
+                     int(getattr(cfg, "partition", 0)))
 
 
 class Slicing:
@@ -230,6 +233,13 @@ def schedule_oplist(n_stages: int, stage: int, groups: Sequence[int], one_f_one_
     n = C.c_int32()
     _check(_lib.tp_schedule_oplist(n_stages, stage, 1 if one_f_one_b else 0, len(groups), g, cap, out, C.byref(n)))
     return [("F", v - 1) if v > 0 else ("B", -v - 1) for v in out[:n.value]]
+
+
+def stage_layers(cfg) -> List[int]:
+    """tp_stage_layers: layers per stage under cfg.partition."""
+    out = (C.c_int32 * cfg.n_stages)()
+    _check(_lib.tp_stage_layers(C.byref(_cfg(cfg)), out))
+    return list(out)
 
 
 def stage_param_count(cfg, stage: int) -> int:

@@ -434,6 +434,234 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------ forward, one query tile per CTA
+// Per (128 query rows, head, sequence), heaviest first. TMEM: S_0 (cols 0-127), S_1 (128-255), O
+// (256-383): S is double-buffered, so S_{j+1} = Q K_{j+1}^T is computed while the softmax works on
+// S_j — the two-tile kernel above must wait for O += P_j V_j before it can reuse S (P lives in S's
+// columns), which serialises softmax -> PV -> S per tile. The price is K_j / V_j read once per tile
+// instead of once per two tiles (shared-memory traffic ~160 KB per 128 x 128 block vs MMA 1024 clk).
+//   warp 0   TMA: Q once; K_j into a 3-deep ring, V_j into a 2-deep ring;
+//   warp 1   MMA: S_{j+1} (into buffer (j+1) & 1 once O += P_{j-1} V_{j-1} has read it), then
+//            O += P_j V_j (P_j from buffer j & 1, TS-MMA);
+//   warps 2-5 softmax, thread = query row (same one-pass exp2 / lazy-rescale scheme as above).
+constexpr int F1_THREADS = 192;
+struct Fwd1Smem {
+  static constexpr uint32_t Q = 0, K = TILE, V = K + NKS * TILE;
+  static constexpr uint32_t BAR = V + NVS * TILE;
+  static constexpr uint32_t BYTES = BAR + 256 + 1024;
+  static_assert(BYTES <= 232448, "forward tile set exceeds 227 KB of shared memory");
+};
+
+__global__ void __launch_bounds__(F1_THREADS, 1)
+    attn_fwd1_sm100_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                           const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ o, int64_t ldo,
+                           float* __restrict__ lse, int s, int c, int l, float scale_log2, int64_t o_sstride,
+                           int64_t lse_sstride) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (tc5::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Fwd1Smem::BAR);
+  uint64_t* qfull = bars + 0;
+  uint64_t* kfull = bars + 1;    // [3]
+  uint64_t* kfree = bars + 4;    // [3]
+  uint64_t* vfull = bars + 7;    // [2]
+  uint64_t* vfree = bars + 9;    // [2]
+  uint64_t* sfull = bars + 11;   // [2] S buffer b holds S_j, j & 1 == b
+  uint64_t* pfull = bars + 13;   // [2] P_j written over buffer b (4 warps)
+  uint64_t* ofull = bars + 15;   // [2] O += P_j V_j complete (j & 1 == b)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int head = blockIdx.y, sq = blockIdx.z, r0 = (gridDim.x - 1 - blockIdx.x) * AT;
+  o += sq * o_sstride;
+  lse += sq * lse_sstride;
+  const int nkb = (c + min(l, r0 + AT) - 1) / AT + 1;
+
+  if (threadIdx.x == 0) {
+    mbar_init(qfull, 1);
+    for (int i = 0; i < NKS; ++i) { mbar_init(kfull + i, 1); mbar_init(kfree + i, 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(vfull + i, 1); mbar_init(vfree + i, 1);
+      mbar_init(sfull + i, 1); mbar_init(pfull + i, 4); mbar_init(ofull + i, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    mbar_expect_tx(qfull, TILE);
+    tma_load_4d(sm + Fwd1Smem::Q, &tmQ, 0, c + r0, head, sq, qfull);
+    tma_load_4d(sm + Fwd1Smem::Q + HALF, &tmQ, 64, c + r0, head, sq, qfull);
+    for (int j = 0; j < nkb; ++j) {
+      const int bk = j % NKS, bv = j & 1;
+      if (j >= NKS) mbar_wait(kfree + bk, ((j / NKS) - 1) & 1);
+      uint8_t* kd = sm + Fwd1Smem::K + bk * TILE;
+      mbar_expect_tx(kfull + bk, TILE);
+      tma_load_4d(kd, &tmK, 0, j * AT, head, sq, kfull + bk);
+      tma_load_4d(kd + HALF, &tmK, 64, j * AT, head, sq, kfull + bk);
+      if (j >= NVS) mbar_wait(vfree + bv, ((j >> 1) - 1) & 1);
+      uint8_t* vd = sm + Fwd1Smem::V + bv * TILE;
+      mbar_expect_tx(vfull + bv, TILE);
+      tma_load_4d(vd, &tmV, 0, j * AT, head, sq, vfull + bv);
+      tma_load_4d(vd + HALF, &tmV, 64, j * AT, head, sq, vfull + bv);
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idS = idesc_bf16(128, 128, false, false);
+    constexpr uint32_t idO = idesc_bf16(128, 128, false, true);
+    const uint32_t q_base = smem_u32(sm + Fwd1Smem::Q);
+    auto issue_s = [&](int j) {  // S_j = Q K_j^T into buffer j & 1 (K_j resident)
+      const uint32_t k_base = smem_u32(sm + Fwd1Smem::K + (j % NKS) * TILE);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < AT / 16; ++kk) {
+        const uint32_t off = (kk >> 2) * HALF + (kk & 3) * 32;
+        mma_bf16_w(tmem + (j & 1) * 128, make_desc(q_base + off, 16, 1024), make_desc(k_base + off, 16, 1024), idS, kk > 0);
+      }
+      mma_commit_w(sfull + (j & 1));
+      mma_commit_w(kfree + j % NKS);
+    };
+    mbar_wait(qfull, 0);
+    mbar_wait(kfull, 0);
+    issue_s(0);
+    for (int j = 0; j < nkb; ++j) {
+      const int b = j & 1;
+      if (j + 1 < nkb) {
+        mbar_wait(kfull + (j + 1) % NKS, ((j + 1) / NKS) & 1);
+        // buffer (j + 1) & 1 held P_{j-1}: O += P_{j-1} V_{j-1} must have read it
+        if (j >= 1) mbar_wait(ofull + ((j - 1) & 1), ((j - 1) >> 1) & 1);
+        issue_s(j + 1);
+      }
+      mbar_wait(vfull + b, (j >> 1) & 1);
+      mbar_wait(pfull + b, (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t v_base = smem_u32(sm + Fwd1Smem::V + b * TILE);
+#pragma unroll
+      for (int kk = 0; kk < AT / 16; ++kk)
+        mma_bf16_ts_w(tmem + 256, tmem + b * 128 + kk * 8, make_desc(v_base + kk * 2048, HALF, 1024), idO,
+                      (j | kk) != 0);
+      mma_commit_w(ofull + b);
+      mma_commit_w(vfree + b);
+    }
+  } else if (warp >= 2) {
+    // ---------------- softmax: thread = query row (TMEM lane)
+    const int q = warp & 3, row = q * 32 + lane;
+    const int qabs = c + r0 + row;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    constexpr uint32_t o_col = 256;
+    float m_ref = -INFINITY, lsum = 0.f;
+    for (int j = 0; j < nkb; ++j) {
+      const int b = j & 1;
+      const uint32_t s_col = b * 128;
+      mbar_wait(sfull + b, (j >> 1) & 1);
+      tc_fence_after();
+      const int nvis = qabs - j * AT + 1;
+      const bool diag = __any_sync(0xffffffffu, nvis < AT);
+      float rs4[4] = {0.f, 0.f, 0.f, 0.f}, m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      uint32_t pk[64];
+      const float nm = -m_ref;
+      if (j > 0) {
+#pragma unroll
+        for (int ch = 0; ch < AT / 32; ++ch) {
+          uint32_t r[32];
+          tmem_ld32_nowait(lane_base + s_col + ch * 32, r);
+          tmem_wait_ld();
+          if (diag) exp_max_chunk<true>(r, ch * 32, nvis, scale_log2, nm, rs4, m4, pk, ch * 16);
+          else exp_max_chunk<false>(r, ch * 32, nvis, scale_log2, nm, rs4, m4, pk, ch * 16);
+        }
+      } else {
+#pragma unroll
+        for (int ch = 0; ch < AT / 32; ch += 2) {
+          uint32_t r[2][32];
+          tmem_ld32_nowait(lane_base + s_col + ch * 32, r[0]);
+          tmem_ld32_nowait(lane_base + s_col + ch * 32 + 32, r[1]);
+          tmem_wait_ld();
+          if (diag) row_max_chunk<true>(r, ch * 32, nvis, m4);
+          else row_max_chunk<false>(r, ch * 32, nvis, m4);
+        }
+      }
+      const float m_blk = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
+      const bool grow = m_blk > m_ref + RESCALE_LOG2;
+      if (__any_sync(0xffffffffu, grow)) {
+        const float m_new = grow ? m_blk : m_ref;
+        const float f = ex2(m_ref - m_new);
+        if (j >= 1) {
+          mbar_wait(ofull + ((j - 1) & 1), ((j - 1) >> 1) & 1);  // O += P_{j-1} V_{j-1} complete
+          tc_fence_after();
+#pragma unroll 1
+          for (int ch = 0; ch < AT / 32; ++ch) {
+            uint32_t r[32];
+            tmem_ld32_nowait(lane_base + o_col + ch * 32, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int u = 0; u < 32; ++u) r[u] = __float_as_uint(__uint_as_float(r[u]) * f);
+            tmem_st32(lane_base + o_col + ch * 32, r);
+          }
+          tmem_wait_st();
+        }
+        lsum *= f;
+        m_ref = m_new;
+        const float nm2 = -m_ref;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) rs4[i] = 0.f;
+#pragma unroll
+        for (int ch = 0; ch < AT / 32; ++ch) {
+          uint32_t r[32];
+          tmem_ld32_nowait(lane_base + s_col + ch * 32, r);
+          tmem_wait_ld();
+          uint32_t pk16[16];
+          float mm[4];
+          exp_max_chunk16<true>(r, ch * 32, nvis, scale_log2, nm2, rs4, mm, pk16);
+#pragma unroll
+          for (int u = 0; u < 16; ++u) pk[ch * 16 + u] = pk16[u];
+        }
+      }
+      const float rsum = (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t pk16[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) pk16[u] = pk[ch * 16 + u];
+        tmem_st16(lane_base + s_col + ch * 16, pk16);
+      }
+      lsum += rsum;
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(pfull + b);
+    }
+    mbar_wait(ofull + ((nkb - 1) & 1), ((nkb - 1) >> 1) & 1);
+    tc_fence_after();
+    const int r = r0 + row;
+    const float inv = 1.f / lsum;
+    bf16* orow = o + (int64_t)r * ldo + head * AT;
+#pragma unroll 1
+    for (int ch = 0; ch < AT / 32; ++ch) {
+      uint32_t rr[32];
+      tmem_ld32_nowait(lane_base + o_col + ch * 32, rr);
+      tmem_wait_ld();
+      if (r < l) {
+#pragma unroll
+        for (int u = 0; u < 32; u += 8) {
+          float v8[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v8[e] = __uint_as_float(rr[u + e]) * inv;
+          store8<bf16>(orow + ch * 32 + u, v8);
+        }
+      }
+    }
+    if (r < l) lse[(int64_t)head * s + c + r] = (m_ref + log2f(lsum)) / LOG2E_F;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // ======================================================================== backward
 // Per (128-key block of the prefix [0, c+l), head, sequence); loop over the slice's 64-query tiles
 // that can see the block. The tile loop is software-pipelined so the tensor pipe never waits for
@@ -873,6 +1101,25 @@ cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o,
   if (!encode_bf16_map(&mq, q, 4, dims, strides, box) || !encode_bf16_map(&mk, k, 4, dims, strides, box) ||
       !encode_bf16_map(&mv, v, 4, dims, strides, box))
     return cudaErrorInvalidValue;
+  // TP_ATTN_FWD=1: one query tile per CTA with S double-buffered; =2: two tiles per CTA sharing K/V;
+  // default by slice length: measured (scripts/attn_bench.py, one B200) the one-tile kernel is faster
+  // for short slices (l = 512 at c = 1536, 80 heads: 79.8 vs 90.9 us; l = 576 at c = 0: 53.0 vs 55.6)
+  // and slower for long ones (l = 1472: 212 vs 203 us), where the shared K/V reads dominate
+  static const int fwd_env = getenv("TP_ATTN_FWD") ? atoi(getenv("TP_ATTN_FWD")) : 0;
+  const int fwd_impl = fwd_env ? fwd_env : (l <= 640 ? 1 : 2);
+  if (fwd_impl == 1) {
+    static bool attr1 = false;
+    if (!attr1) {
+      cudaError_t e = cudaFuncSetAttribute(attn_fwd1_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)Fwd1Smem::BYTES);
+      if (e != cudaSuccess) return e;
+      attr1 = true;
+    }
+    dim3 grid1((l + AT - 1) / AT, a, nseq);
+    attn_fwd1_sm100_kernel<<<grid1, F1_THREADS, Fwd1Smem::BYTES, st>>>(mq, mk, mv, o, ldo, lse, s, c, l,
+                                                                      rsqrtf((float)d) * LOG2E_F, o_sstride, lse_sstride);
+    return cudaGetLastError();
+  }
   {
     static bool attr2 = false;
     if (!attr2) {

@@ -66,27 +66,44 @@ struct Cfg {
   static_assert(SMEM <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
-// Stream-K tail: the tiles that would form a partial last wave are split along K into `S` parts
-// processed by different work units; each part writes its fp32 partial tile to a workspace, and
-// the last part to finish (atomic ticket per tile and CTA) sums them and runs the fused epilogue.
+// Stream-K (data-parallel waves + one stream-K wave): tiles [0, dp_tiles) run whole, round robin
+// over the units; the remaining tiles' k-blocks, sk_iters = (tiles - dp_tiles) * kbs in all, are
+// cut into one contiguous range per unit (processed last segment first), so every unit ends the
+// launch at the same point whatever the tile count. A range that stops inside a tile leaves a fp32 partial in the unit's own
+// workspace slot and raises its flag; the unit that processes the tile's LAST k-block (the
+// finisher) adds the partials of the earlier units that covered the tile's beginning (waiting on
+// their flags; they are lower units, all co-resident: the grid is one CTA per SM) and runs the
+// fused epilogue. Each unit leaves at most one partial per launch, so a slot per unit suffices.
 struct SplitK {
-  int dp_tiles = 0;    // tiles [0, dp_tiles) run whole; [dp_tiles, tiles) run as S K-parts each
-  int S = 1;
-  float* ws = nullptr;  // [(tile - dp_tiles) * S + part][CG][128][TILE_N] fp32
-  int* cnt = nullptr;   // [(tile - dp_tiles) * CG + crank], zero between launches (the last part resets)
+  int dp_tiles = 0;       // whole tiles; [dp_tiles, tiles) are processed stream-K
+  long long sk_iters = 0; // (tiles - dp_tiles) * kbs
+  float* ws = nullptr;    // [unit * CG + crank][128][TILE_N] fp32 partial slots
+  int* flag = nullptr;    // [unit * CG + crank]: 1 = partial ready (reset to 0 by the finisher)
 };
-// Work item `it` of unit `unit`: first its whole tiles (round robin), then its tail K-parts.
+__device__ __forceinline__ long long sk_r0(int unit, int nunits, long long iters) {
+  return iters * unit / nunits;
+}
+// Work item `it` of unit `unit`: first its whole tiles (round robin), then the tile segments of its
+// stream-K range. kind: 0 = whole tile, 1 = partial (the range ends inside the tile), 2 = finisher
+// (the segment ends the tile but does not start it).
 __device__ __forceinline__ bool gemm_item(int it, int unit, int nunits, int tiles, int kbs, const SplitK& sk,
-                                          int& tile, int& k0, int& k1, int& part) {
+                                          int& tile, int& k0, int& k1, int& kind) {
   const int ndp = unit < sk.dp_tiles ? (sk.dp_tiles - unit + nunits - 1) / nunits : 0;
-  if (it < ndp) { tile = unit + it * nunits; k0 = 0; k1 = kbs; part = -1; return true; }
-  if (sk.S <= 1) return false;  // no split: dp_tiles == tiles
-  const int w = unit + (it - ndp) * nunits;
-  if (w >= (tiles - sk.dp_tiles) * sk.S) return false;
-  tile = sk.dp_tiles + w / sk.S;
-  part = w % sk.S;
-  k0 = (int)((int64_t)part * kbs / sk.S);
-  k1 = (int)((int64_t)(part + 1) * kbs / sk.S);
+  if (it < ndp) { tile = unit + it * nunits; k0 = 0; k1 = kbs; kind = 0; return true; }
+  if (sk.sk_iters <= 0) return false;
+  const long long r0 = sk_r0(unit, nunits, sk.sk_iters), r1 = sk_r0(unit + 1, nunits, sk.sk_iters);
+  if (r1 <= r0) return false;
+  // segments in REVERSE order: the range's last segment (a partial other units' finishers wait for)
+  // first, its first segment (possibly a finisher, which waits for lower units' partials) last — so
+  // no unit waits on a partial that is produced at the end of another unit's range
+  const long long t0 = r0 / kbs, nseg = (r1 + kbs - 1) / kbs - t0;
+  const long long n = nseg - 1 - (it - ndp);
+  if (n < 0) return false;
+  const long long pos = n == 0 ? r0 : (t0 + n) * (long long)kbs;
+  tile = sk.dp_tiles + (int)(pos / kbs);
+  k0 = (int)(pos % kbs);
+  k1 = (int)std::min<long long>(kbs, k0 + (r1 - pos));
+  kind = (k0 == 0 && k1 == kbs) ? 0 : (k1 < kbs ? 1 : 2);
   return true;
 }
 
@@ -104,14 +121,15 @@ __device__ __forceinline__ void tile_mn(int tile, int m_tiles, int n_tiles, int 
 }
 // One output tile's fused epilogue for this warp (TMEM lane quarter q, column chunks [ch0, ch1)),
 // specialised on the epilogue kind. mode 0: TMEM -> fused epilogue; 1: TMEM -> raw fp32 partial to
-// `wsp`; 2: sum of the S stream-K partials at `wsp` (stride 128 * TILE_N * CG per part) -> fused
-// epilogue. Per-column work (bias, the QKV column -> (part, head, dim) decode) is done once per
-// 32-column chunk and per-row work (the QKV row -> (sequence, position) decode) once per tile, so
-// the inner loop is loads, math and stores only.
+// this CTA's stream-K slot `wsp`; 2 (finisher): TMEM + the partial slots of units [v_lo, v_hi)
+// (slot of unit v = ws + (v * CG + crank) * 128 * TILE_N) -> fused epilogue. Per-column work (bias,
+// the QKV column -> (part, head, dim) decode) is done once per 32-column chunk and per-row work
+// (the QKV row -> (sequence, position) decode) once per tile, so the inner loop is loads, math and
+// stores only.
 template <int KIND, int CG, int TILE_N, int BN>
 __device__ __forceinline__ void epi_tile(const Epi& epi, const SplitK& sk, float* scr, uint32_t tmem_base, int acc, int q,
                                          int lane, int ch0, int ch1, int M, int N, int mode, int m0, int n0, float* wsp,
-                                         bool has_dbias) {
+                                         bool has_dbias, int crank, int v_lo, int v_hi) {
   constexpr bool AUX = KIND == EPI_RESID || KIND == EPI_DGELU;
   constexpr bool BIAS = KIND == EPI_STORE || KIND == EPI_RESID || KIND == EPI_GELU || KIND == EPI_QKV;
   int rows[4];
@@ -151,30 +169,34 @@ __device__ __forceinline__ void epi_tile(const Epi& epi, const SplitK& sk, float
       qkv_col = reinterpret_cast<bf16*>(part == 0 ? epi.q : (part == 1 ? epi.k : epi.v)) +
                 (int64_t)head * epi.s_len * epi.head_dim + dd;
     }
-    // the tile's 32 x 32 chunk lands in the warp's padded smem scratch: from TMEM (modes 0, 1) or
-    // as the sum of the stream-K partials (mode 2)
-    if (mode != 2) {
+    // the tile's 32 x 32 chunk lands in the warp's padded smem scratch from TMEM; a finisher adds the
+    // earlier units' partials of the same rows / columns
+    {
       uint32_t r[32];
       tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 32, r);
 #pragma unroll
       for (int i = 0; i < 32; ++i) scr[lane * 33 + i] = __uint_as_float(r[i]);
-    } else {
+    }
+    __syncwarp();
+    if (mode == 2) {
 #pragma unroll 1
       for (int it = 0; it < 4; ++it) {
         const int rr = it * 8 + (lane >> 2);
         const int64_t woff = (int64_t)(q * 32 + rr) * TILE_N + (ch * 32 + (lane & 3) * 8);
-        float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        for (int p = 0; p < sk.S; ++p) {
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = scr[rr * 33 + (lane & 3) * 8 + i];
+        for (int u = v_lo; u < v_hi; ++u) {
           float w[8];
-          load8<float>(wsp + (int64_t)p * CG * 128 * TILE_N + woff, w);
+          load8<float>(sk.ws + (int64_t)(u * CG + crank) * 128 * TILE_N + woff, w);
 #pragma unroll
           for (int i = 0; i < 8; ++i) v[i] += w[i];
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) scr[rr * 33 + (lane & 3) * 8 + i] = v[i];
       }
+      __syncwarp();
     }
-    __syncwarp();
     if (mode == 1) {  // raw fp32 partial of this K-part to the workspace
 #pragma unroll 1
       for (int it = 0; it < 4; ++it) {
@@ -268,7 +290,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* tfull = empty + C::NS;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  volatile int* sk_ticket = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = CG == 2 ? cluster_rank() : 0;
@@ -394,18 +415,35 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     float* scr = epi_scratch + (warp - 2) * 32 * 33;
     const bool has_dbias = epi.kind == EPI_DGELU && epi.dbias != nullptr;
     const int ch0 = ((warp - 2) >> 2) * (C::TILE_N / 64), ch1 = ch0 + C::TILE_N / 64;
-    auto tile_epilogue = [&](int mode, int m0, int n0, float* wsp) {
-      epi_tile<KIND, CG, C::TILE_N, BN>(epi, sk, scr, tmem_base, acc, q, lane, ch0, ch1, M, N, mode, m0, n0, wsp, has_dbias);
+    auto tile_epilogue = [&](int mode, int m0, int n0, float* wsp, int v_lo, int v_hi) {
+      epi_tile<KIND, CG, C::TILE_N, BN>(epi, sk, scr, tmem_base, acc, q, lane, ch0, ch1, M, N, mode, m0, n0, wsp, has_dbias,
+                                        crank, v_lo, v_hi);
     };
-    int tile, k0, k1, part;
-    for (int item = 0; gemm_item(item, unit, nunits, tiles, kbs, sk, tile, k0, k1, part); ++item) {
+    int tile, k0, k1, kind;
+    for (int item = 0; gemm_item(item, unit, nunits, tiles, kbs, sk, tile, k0, k1, kind); ++item) {
       int mt, nt;
       tile_mn(tile, m_tiles, n_tiles, group_m, mt, nt);
       const int m0 = mt * C::TILE_M + crank * BM, n0 = nt * C::TILE_N;
+      int v_lo = unit, v_hi = unit;
+      if (kind == 2) {
+        // finisher: the units below whose ranges cover [tile start, this segment's start) left partials
+        const long long tstart = (long long)(tile - sk.dp_tiles) * kbs;
+        while (v_lo > 0 && sk_r0(v_lo, nunits, sk.sk_iters) > tstart) --v_lo;
+        if (threadIdx.x == 64) {
+          for (int u = v_lo; u < v_hi; ++u) {
+            const int* f = sk.flag + u * CG + crank;
+            int ready = 0;
+            do {
+              asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(ready) : "l"(f) : "memory");
+            } while (!ready);
+          }
+        }
+        named_bar(1, 256);
+      }
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
-      float* wst = part < 0 ? nullptr : sk.ws + ((int64_t)(tile - sk.dp_tiles) * sk.S * CG + crank) * 128 * C::TILE_N;
-      tile_epilogue(part < 0 ? 0 : 1, m0, n0, part < 0 ? nullptr : wst + (int64_t)part * CG * 128 * C::TILE_N);
+      float* wsp = kind == 1 ? sk.ws + (int64_t)(unit * CG + crank) * 128 * C::TILE_N : nullptr;
+      tile_epilogue(kind == 0 ? 0 : (kind == 1 ? 1 : 2), m0, n0, wsp, v_lo, v_hi);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -413,19 +451,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         else mbar_arrive_cluster(tempty_leader + acc * 8);
       }
       if (++acc == C::NACC) { acc = 0; acc_phase ^= 1; }
-      if (part >= 0) {
-        // stream-K: the last of the S parts (per tile and CTA) reduces the partials and runs the epilogue
-        __threadfence();
+      if (kind == 1) {
+        // partial written by all 8 epilogue warps: publish it
         named_bar(1, 256);
-        int* cnt = sk.cnt + (tile - sk.dp_tiles) * CG + crank;
-        if (threadIdx.x == 64) *sk_ticket = atomicAdd(cnt, 1);
-        named_bar(1, 256);
-        if (*sk_ticket == sk.S - 1) {
+        if (threadIdx.x == 64) {
           __threadfence();
-          tile_epilogue(2, m0, n0, wst);
-          if (threadIdx.x == 64) *cnt = 0;
+          asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(sk.flag + unit * CG + crank), "r"(1) : "memory");
         }
-        named_bar(1, 256);  // nobody overwrites sk_ticket before every thread has read it
+      } else if (kind == 2) {
+        named_bar(1, 256);  // every warp has read the partials: reset the flags for the next launch
+        if (threadIdx.x == 64)
+          for (int u = v_lo; u < v_hi; ++u) sk.flag[u * CG + crank] = 0;
       }
     }
   }
@@ -502,19 +538,23 @@ cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
     const char* e = getenv("TP_GEMM_STREAMK");
     g_stream_k = e ? atoi(e) : 1;
   }
-  if (g.persistent && WN == 1 && g_stream_k) {
+  if (g.persistent && g_stream_k && g.sk_ws && g.sk_cnt) {
+    // DP + one stream-K wave when the last wave would leave > 6 % of the units idle and each unit's
+    // stream-K range keeps >= 160 k-blocks of MMA work: measured (scripts/bench_kernels.py, one
+    // B200) +3-8 % at 173-664 k-blocks per unit (13B FC2 K = 20480, dW K = 16384, FC2 K = 8192 at
+    // 3.5 waves) and 12-35 % slower at 51-130 (K <= 5120, or < 1 tile per unit at K = 8192): the
+    // partial writes / finisher reads (~128 KB per CTA) and the un-overlapped finisher epilogue
+    // need long ranges to amortise
     const int full_units = g_num_sms / CG;
-    const int tail = tiles % full_units;
-    // each part must keep >= 32 k-blocks of MMA work to amortise its fp32 partial write and the
-    // last part's S-way read (e.g. K = 2048 -> no split, K = 5120 -> S <= 2)
-    const int S = tail > 0 ? std::min(std::min(4, full_units / tail), kbs / 32) : 1;
-    if (S >= 2 && g.sk_ws && g.sk_cnt) {
-      // tail * S * CG <= #SMs partial tiles of 128 x TILE_N <= 128 x 256 fp32: the fixed workspace
-      // of gemm_sm100_workspace always fits
-      sk.dp_tiles = tiles - tail;
-      sk.S = S;
+    const int waves = (tiles + full_units - 1) / full_units;
+    const double eff = (double)tiles / ((double)waves * full_units);
+    const int dp = tiles > full_units ? (tiles / full_units - 1) * full_units : 0;
+    const long long iters = (long long)(tiles - dp) * kbs;
+    if (eff < 0.94 && iters / full_units >= 160) {
+      sk.dp_tiles = dp;
+      sk.sk_iters = iters;
       sk.ws = g.sk_ws;
-      sk.cnt = g.sk_cnt;
+      sk.flag = g.sk_cnt;
       units = full_units;
     }
   }
@@ -604,7 +644,7 @@ bool encode_f32_map_sw128(CUtensorMap* map, const void* ptr, int rank, const uin
 }
 void gemm_sm100_workspace(size_t* ws_floats, size_t* cnt_ints) {
   init_once();
-  *ws_floats = (size_t)g_num_sms * 128 * 256;
+  *ws_floats = (size_t)g_num_sms * 128 * 512;  // one 128 x TILE_N (<= 512) fp32 partial slot per CTA
   *cnt_ints = (size_t)g_num_sms;
 }
 bool tensor_maps_available() {

@@ -31,8 +31,8 @@ template <typename T> cudaError_t gemm_simt(const GemmDesc& g, const Epi& e, cud
 // tcgen05 / TMEM / TMA GEMM for sm_100a, bf16 operands, fp32 accumulation (gemm_sm100.cu).
 cudaError_t gemm_sm100(const GemmDesc& g, const Epi& e, cudaStream_t st);
 bool gemm_sm100_supported(const GemmDesc& g);
-// Fixed stream-K workspace size that covers every launch on this device: tail tiles x parts x CTAs
-// per tile <= #SMs, each a 128 x 256 fp32 partial (floats), plus one int ticket per SM.
+// Fixed stream-K workspace size that covers every launch on this device: one 128 x 512 fp32 partial
+// slot per CTA of a persistent grid (floats), plus one int flag per CTA.
 void gemm_sm100_workspace(size_t* ws_floats, size_t* cnt_ints);
 // false when the driver's cuTensorMapEncodeTiled entry point is unavailable (no TMA descriptors)
 bool tensor_maps_available();

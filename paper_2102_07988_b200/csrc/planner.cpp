@@ -77,7 +77,7 @@ extern "C" tp_status tp_plan(int32_t n_layer, int32_t hidden, int32_t seq_len, i
                              tp_slicing* out) {
   TP_CHECK_ARG(cost && out, "tp_plan: null cost table or output");
   TP_CHECK_ARG(n_stages >= 1, "tp_plan: n_stages must be >= 1 (got %d)", n_stages);
-  TP_CHECK_ARG(n_layer >= 1 && n_layer % n_stages == 0,
+  TP_CHECK_ARG(n_layer >= 1 && n_layer >= n_stages,
                "tp_plan: n_layer (%d) must be a positive multiple of n_stages (%d)", n_layer, n_stages);
   TP_CHECK_ARG(hidden > 0, "tp_plan: hidden must be > 0");
   TP_CHECK_ARG(n_micro >= 1, "tp_plan: n_micro must be >= 1");
@@ -165,7 +165,7 @@ extern "C" tp_status tp_plan_joint(int32_t n_layer, int32_t hidden, int32_t seq_
   TP_CHECK_ARG(out && b_values && costs, "tp_plan_joint: null argument");
   TP_CHECK_ARG(n_b >= 1, "tp_plan_joint: n_b must be >= 1");
   TP_CHECK_ARG(batch >= 1, "tp_plan_joint: batch must be >= 1");
-  TP_CHECK_ARG(n_stages >= 1 && n_layer >= 1 && n_layer % n_stages == 0 && hidden > 0,
+  TP_CHECK_ARG(n_stages >= 1 && n_layer >= 1 && n_layer >= n_stages && hidden > 0,
                "tp_plan_joint: bad model shape (n_layer %d, n_stages %d, hidden %d)", n_layer, n_stages, hidden);
   TP_CHECK_ARG(eps_ticks >= 0, "tp_plan_joint: eps_ticks must be >= 0");
   TP_CHECK_ARG(costs[0] != nullptr, "tp_plan_joint: null cost table 0");

@@ -49,7 +49,40 @@ namespace tp {
 
 struct ModelShape {
   int n_layer, H, a, d, V, s, K;
+  int partition = 0;  // TP_PARTITION_*
 };
+
+// Layers owned by each stage (A-30). Uniform: n/K each. Balanced: the
+// last stage also runs the LM head + CE, h = V / (12 H + s) layers' worth of FLOPs per token (head
+// 6 H V vs a layer's 72 H^2 + 6 s H); choose the last stage's count nl minimising
+// max(ceil((n - nl) / (K - 1)), nl + h) (ties: the larger nl), spread the rest evenly, stages
+// 1.. taking the remainder (stage 0 also holds the embedding). synth/__init__.py has the same rule.
+static std::vector<int> stage_layer_counts(int n, int K, int H, int V, int s, int partition) {
+  std::vector<int> out(K, K > 0 ? n / K : 0);
+  if (partition != TP_PARTITION_BALANCED || K == 1) return out;
+  const double h = (double)V / (12.0 * H + s);
+  int best_nl = n / K;
+  double best = 1e300;
+  for (int nl = 1; nl <= n - (K - 1); ++nl) {
+    const int r = n - nl;
+    const double cost = std::max((double)((r + K - 2) / (K - 1)), nl + h);
+    if (cost < best || (cost == best && nl > best_nl)) { best = cost; best_nl = nl; }
+  }
+  const int r = n - best_nl, base = r / (K - 1), extra = r % (K - 1);
+  for (int k = 0; k < K - 1; ++k) out[k] = base + ((k >= 1 && k <= extra) ? 1 : 0);
+  if (extra == K - 1) out[0] += 1;  // (cannot happen: extra < K - 1)
+  out[K - 1] = best_nl;
+  return out;
+}
+static int stage_first_layer(const ModelShape& m, int k) {
+  const std::vector<int> c = stage_layer_counts(m.n_layer, m.K, m.H, m.V, m.s, m.partition);
+  int f = 0;
+  for (int i = 0; i < k; ++i) f += c[i];
+  return f;
+}
+static int stage_nl(const ModelShape& m, int k) {
+  return stage_layer_counts(m.n_layer, m.K, m.H, m.V, m.s, m.partition)[k];
+}
 
 // Offsets (in floats) of every tensor inside one stage's flat parameter array (include/tp.h).
 struct LayerOff {
@@ -72,7 +105,7 @@ static StageLayout stage_layout(const ModelShape& m, int k) {
   size_t o = 0;
   const size_t H = m.H;
   if (k == 0) { L.wte = o; o += (size_t)m.V * H; L.wpe = o; o += (size_t)m.s * H; }
-  const int nl = m.n_layer / m.K;
+  const int nl = stage_nl(m, k);
   for (int j = 0; j < nl; ++j) {
     LayerOff f;
     f.ln1_g = o; o += H; f.ln1_b = o; o += H;
@@ -330,7 +363,8 @@ class Engine final : public EngineBase {
 
   tp_status init(const tp_model_cfg* cfg, int rank_, int world_, const void* nccl_id, int precision_,
                  int max_batch_, int device_, int flags_) {
-    m = {cfg->n_layer, cfg->hidden, cfg->n_head, cfg->hidden / cfg->n_head, cfg->vocab, cfg->seq_len, cfg->n_stages};
+    m = {cfg->n_layer, cfg->hidden, cfg->n_head, cfg->hidden / cfg->n_head, cfg->vocab, cfg->seq_len, cfg->n_stages,
+         cfg->partition};
     rank = rank_; world = world_; precision = precision_; flags = flags_; max_batch = max_batch_; device = device_;
     force_simt = (flags & TP_FLAG_FORCE_SIMT) != 0 || precision == TP_FP32;
     instr.on = (flags & TP_FLAG_KERNEL_STATS) != 0;
@@ -400,7 +434,7 @@ class Engine final : public EngineBase {
 
   tp_status alloc_stage(Stage<T>& S, int k) {
     S.k = k;
-    S.nl = m.n_layer / m.K;
+    S.nl = stage_nl(m, k);
     S.L = stage_layout(m, k);
     const size_t B = max_batch, s = m.s, H = m.H, a = m.a, nl = S.nl;
     TRY(alloc(&S.psmall, S.L.small_total));
@@ -1321,8 +1355,6 @@ tp_status Engine<T>::profile_stage(Stage<T>& S, int g, int bsl, int reps, std::v
       samp.push_back({(double)lu * g, (double)cu * g, t - base[lu]});
     }
   }
-  CU(cudaEventDestroy(e0));
-  CU(cudaEventDestroy(e1));
   // least squares for a0..a3 via normal equations (4x4, Gaussian elimination with pivoting)
   double A[4][5] = {};
   for (auto& sp : samp) {
@@ -1360,6 +1392,8 @@ tp_status Engine<T>::profile_stage(Stage<T>& S, int g, int bsl, int reps, std::v
   // latency-bound, so t_ctx is not the bilinear a0 + a1 l + a2 c + a3 l c of PAPER.md:294 (the fit
   // above is still reported). TP_CTX_FIT=linear fills the table from the paper's linear fit.
   const bool linear = std::getenv("TP_CTX_FIT") && std::string(std::getenv("TP_CTX_FIT")) == "linear";
+  // TP_PROFILE_DENSE=1 (cost-model study, NEXT(3)): every (l, c) entry measured directly
+  const bool dense = std::getenv("TP_PROFILE_DENSE") && std::atoi(std::getenv("TP_PROFILE_DENSE")) != 0;
   auto ctx_at = [&](size_t li, int cu) -> double {  // t_ctx at grid l index li, any cu >= 0
     const auto& v = cs_of[li];
     if (v.size() == 1) return v[0].second;
@@ -1375,6 +1409,10 @@ tp_status Engine<T>::profile_stage(Stage<T>& S, int g, int bsl, int reps, std::v
       double tc;
       if (cu == 0) {
         tc = 0.0;
+      } else if (dense) {
+        double t = 0.0;
+        TRY(time_job(lu * g, cu * g, &t));
+        tc = t - base[lu];
       } else if (linear) {
         tc = coef[0] + coef[1] * l + coef[2] * c + coef[3] * l * c;
       } else {
@@ -1390,6 +1428,8 @@ tp_status Engine<T>::profile_stage(Stage<T>& S, int g, int bsl, int reps, std::v
       }
       ticks[(size_t)(lu - 1) * (n + 1) + cu] = std::max<int64_t>(1, (int64_t)std::llround(base[lu] + tc));
     }
+  CU(cudaEventDestroy(e0));
+  CU(cudaEventDestroy(e1));
   if (fit) { for (int i = 0; i < 4; ++i) fit[i] = coef[i]; fit[4] = maxrel; }
   return TP_OK;
 }
@@ -1594,9 +1634,11 @@ using namespace tp;
 extern "C" tp_status tp_stage_param_count(const tp_model_cfg* cfg, int32_t stage, size_t* out) {
   TP_CHECK_ARG(cfg && out, "tp_stage_param_count: null argument");
   TP_CHECK_ARG(cfg->n_stages >= 1 && stage >= 0 && stage < cfg->n_stages, "tp_stage_param_count: bad stage");
-  TP_CHECK_ARG(cfg->n_layer % cfg->n_stages == 0, "n_layer %% n_stages != 0");
+  TP_CHECK_ARG(cfg->partition == TP_PARTITION_UNIFORM || cfg->partition == TP_PARTITION_BALANCED, "bad partition");
+  TP_CHECK_ARG(cfg->partition == TP_PARTITION_BALANCED ? cfg->n_layer >= cfg->n_stages : cfg->n_layer % cfg->n_stages == 0,
+               "n_layer %d does not split over %d stages", cfg->n_layer, cfg->n_stages);
   ModelShape m{cfg->n_layer, cfg->hidden, cfg->n_head, cfg->n_head ? cfg->hidden / cfg->n_head : 0,
-               cfg->vocab, cfg->seq_len, cfg->n_stages};
+               cfg->vocab, cfg->seq_len, cfg->n_stages, cfg->partition};
   *out = stage_layout(m, stage).total;
   return TP_OK;
 }
@@ -1622,6 +1664,16 @@ extern "C" tp_status tp_schedule_oplist(int32_t n_stages, int32_t stage, int32_t
   return TP_OK;
 }
 
+extern "C" tp_status tp_stage_layers(const tp_model_cfg* cfg, int32_t* counts_out) {
+  TP_CHECK_ARG(cfg && counts_out && cfg->n_stages >= 1 && cfg->n_layer >= cfg->n_stages, "tp_stage_layers: bad argument");
+  TP_CHECK_ARG(cfg->partition == TP_PARTITION_BALANCED || cfg->n_layer % cfg->n_stages == 0,
+               "tp_stage_layers: n_layer %% n_stages != 0");
+  const std::vector<int> c = stage_layer_counts(cfg->n_layer, cfg->n_stages, cfg->hidden, cfg->vocab, cfg->seq_len,
+                                                cfg->partition);
+  for (int k = 0; k < cfg->n_stages; ++k) counts_out[k] = c[k];
+  return TP_OK;
+}
+
 extern "C" tp_status tp_nccl_unique_id(void* out128) {
   TP_CHECK_ARG(out128, "tp_nccl_unique_id: null");
   ncclUniqueId id;
@@ -1636,8 +1688,12 @@ extern "C" tp_status tp_init(const tp_model_cfg* cfg, int32_t rank, int32_t worl
                              int32_t precision, int32_t max_batch, int32_t device, int32_t flags, tp_ctx** out) {
   TP_CHECK_ARG(cfg && out, "tp_init: null argument");
   *out = nullptr;
-  TP_CHECK_ARG(cfg->n_layer >= 1 && cfg->n_stages >= 1 && cfg->n_layer % cfg->n_stages == 0,
-               "tp_init: n_layer (%d) must be a positive multiple of n_stages (%d)", cfg->n_layer, cfg->n_stages);
+  TP_CHECK_ARG(cfg->partition == TP_PARTITION_UNIFORM || cfg->partition == TP_PARTITION_BALANCED,
+               "tp_init: bad partition %d", cfg->partition);
+  TP_CHECK_ARG(cfg->n_layer >= 1 && cfg->n_stages >= 1 &&
+               (cfg->partition == TP_PARTITION_BALANCED ? cfg->n_layer >= cfg->n_stages : cfg->n_layer % cfg->n_stages == 0),
+               "tp_init: n_layer (%d) must be a positive multiple of n_stages (%d) (balanced: >= n_stages)", cfg->n_layer,
+               cfg->n_stages);
   TP_CHECK_ARG(cfg->n_head >= 1 && cfg->hidden % cfg->n_head == 0, "tp_init: hidden %% n_head != 0");
   const int d = cfg->hidden / cfg->n_head;
   TP_CHECK_ARG(d % 16 == 0 && d <= 128, "tp_init: head_dim %d must be a multiple of 16 and <= 128", d);

@@ -37,10 +37,13 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     base, B = CONFIGS[args.config]
-    cfg = base.with_(n_stages=world)
+    part = 0 if os.environ.get("TP_PARTITION", "balanced") == "uniform" else 1  # as bench.py
+    cfg = base.with_(n_stages=world, partition=part)
     b = args.batch_slice
     nid = tdist.share_nccl_id(rank) if world > 1 else None
-    ctx = tp.Context(cfg, rank=rank, world=world, nccl_id=nid, max_batch=B, device=local)
+    p2p_device = world > 1 and os.environ.get("TP_DEVICE_P2P", "1") != "0"  # as bench.py
+    ctx = tp.Context(cfg, rank=rank, world=world, nccl_id=nid, max_batch=B, device=local,
+                     flags=tp.TP_FLAG_DEVICE_P2P if p2p_device else 0)
     ctx.load_params(make_stage_flat(cfg, rank, seed=0) if world > 1 else make_stage_flat(cfg, 0, seed=0))
     tok = torch.from_numpy(make_tokens(cfg, B, seed=1)).cuda()
     stream = torch.cuda.ExternalStream(ctx.stream())

@@ -36,6 +36,7 @@ class ModelCfg:
     vocab: int
     seq_len: int
     n_stages: int = 1
+    partition: int = 0          # 0 uniform n/K layers per stage; 1 balanced for the LM head (A-30)
 
     @property
     def head_dim(self) -> int:
@@ -54,6 +55,8 @@ CONFIGS: Dict[str, Tuple[ModelCfg, int]] = {
     "gpt3-175b-24l": (ModelCfg(24, 12288, 96, 50304, 2048, 8), 2),  # BASELINE.json:11
     "parity-mid": (ModelCfg(2, 5120, 40, 1024, 512, 2), 1),   # SURVEY.md §8(c) parity-mid (vocab reduced)
     "small": (ModelCfg(4, 256, 2, 512, 128, 2), 2),           # several tiles, d=128
+    # a head worth ~1.3 layers: the balanced partition (A-30) gives non-uniform stages
+    "small-deep": (ModelCfg(8, 256, 2, 4096, 128, 2, 1), 2),
 }
 
 LAYER_PARAMS = ("ln1_g", "ln1_b", "w_qkv", "b_qkv", "w_o", "b_o",
@@ -66,10 +69,32 @@ def _layer_shapes(H: int) -> List[Tuple[str, Tuple[int, ...]]]:
             ("w_1", (H, 4 * H)), ("b_1", (4 * H,)), ("w_2", (4 * H, H)), ("b_2", (H,))]
 
 
+def stage_layer_counts(cfg: ModelCfg) -> List[int]:
+    """Layers per stage (the parameter LAYOUT shared with the library, tp_stage_layers; no method
+    arithmetic). partition 0: n/K each (uniform cells). partition 1 (DESIGN.md
+    A-30): the last stage, which also holds the LM head worth h = V / (12 H + s) layers, gets the nl
+    minimising max(ceil((n - nl) / (K - 1)), nl + h) (ties: larger nl); stages 1..r%(K-1) get one
+    more of the remaining layers."""
+    n, K = cfg.n_layer, cfg.n_stages
+    if cfg.partition == 0 or K == 1:
+        return [n // K] * K
+    h = cfg.vocab / (12.0 * cfg.hidden + cfg.seq_len)
+    best_nl, best = n // K, float("inf")
+    for nl in range(1, n - (K - 1) + 1):
+        r = n - nl
+        cost = max(float((r + K - 2) // (K - 1)), nl + h)
+        if cost < best or (cost == best and nl > best_nl):
+            best, best_nl = cost, nl
+    r = n - best_nl
+    base, extra = divmod(r, K - 1)
+    return [base + (1 if 1 <= k <= extra else 0) for k in range(K - 1)] + [best_nl]
+
+
 def stage_layers(cfg: ModelCfg, k: int) -> range:
-    """Stage k owns layers [k*n/K, (k+1)*n/K) (uniform cells)."""
-    per = cfg.n_layer // cfg.n_stages
-    return range(k * per, (k + 1) * per)
+    """Stage k owns a contiguous block of layers (stage_layer_counts)."""
+    c = stage_layer_counts(cfg)
+    first = sum(c[:k])
+    return range(first, first + c[k])
 
 
 def stage_param_specs(cfg: ModelCfg, k: int) -> List[Tuple[str, Tuple[int, ...]]]:

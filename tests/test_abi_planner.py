@@ -223,3 +223,40 @@ def test_schedule_oplist_rejects_bad_input():
         tp.schedule_oplist(2, 2, [1], True)
     with pytest.raises(tp.TpError):
         tp.schedule_oplist(2, 0, [0, 1], True)
+
+
+# ---------------------------------------------------------------- stage partition (A-30)
+def test_stage_layers_uniform_and_balanced_match_synth():
+    """tp_stage_layers (the library's layout) equals synth's stage_layer_counts for both partitions
+    over many shapes, every stage owns >= 1 layer, the counts sum to n_layer, and the balanced split
+    never has a larger max per-stage FLOP cost (layers + h on the last stage) than the uniform one."""
+    from synth import ModelCfg, stage_layer_counts
+    rng = np.random.default_rng(42)
+    shapes = [(24, 2048, 2048, 50304, K) for K in (1, 2, 3, 4, 6, 8)] + \
+             [(40, 5120, 2048, 50304, K) for K in (1, 2, 4, 5, 8)] + [(24, 12288, 2048, 50304, 8)]
+    for _ in range(60):
+        K = int(rng.integers(1, 9))
+        shapes.append((int(rng.integers(K, 5 * K + 1)), int(rng.choice([256, 1024, 2048, 5120])),
+                       int(rng.choice([128, 2048, 8192])), int(rng.choice([512, 50304])), K))
+    for n, H, s, V, K in shapes:
+        for part in (0, 1):
+            if part == 0 and n % K:
+                continue
+            cfg = ModelCfg(n, H, 16, V, s, K, part)
+            got = tp.stage_layers(cfg)
+            assert got == stage_layer_counts(cfg), (n, H, s, V, K, part)
+            assert sum(got) == n and min(got) >= 1
+        if n % K == 0:
+            h = V / (12.0 * H + s)
+            bal = stage_layer_counts(ModelCfg(n, H, 16, V, s, K, 1))
+            cost = lambda c: max(max(c[:-1], default=0), c[-1] + h)
+            assert cost(bal) <= cost([n // K] * K) + 1e-12
+
+
+def test_balanced_partition_1b_examples():
+    from synth import ModelCfg
+    assert tp.stage_layers(ModelCfg(24, 2048, 16, 50304, 2048, 4, 1)) == [6, 7, 6, 5]
+    assert tp.stage_layers(ModelCfg(24, 2048, 16, 50304, 2048, 8, 1)) == [3, 4, 3, 3, 3, 3, 3, 2]
+    assert tp.stage_layers(ModelCfg(40, 5120, 40, 50304, 2048, 4, 1)) == [10] * 4   # 13B: uniform is optimal
+    with pytest.raises(tp.TpError):
+        tp.stage_layers(ModelCfg(3, 64, 4, 128, 32, 2, 0))

@@ -68,6 +68,13 @@ def test_1f1b_nccl(world, env, tmp_path):
         assert max(errs.values()) < 2e-2, errs
 
 
+@pytest.mark.parametrize("world,env", [(2, {}), (4, {}), (4, {"TP_DEVICE_P2P": "1"})])
+def test_balanced_partition_multi(world, env, tmp_path):
+    """TP_PARTITION_BALANCED over NCCL / device p2p: stages of different layer counts."""
+    for errs in run(world, "small-deep", "bf16", "40,24,64", tmp_path, env=env):
+        assert max(errs.values()) < 2e-2, errs
+
+
 def test_small_four_stages_nccl(tmp_path):
     for errs in run(4, "small", "bf16", "40,24,64", tmp_path):
         assert max(errs.values()) < 2e-2, errs

@@ -337,3 +337,16 @@ def test_1f1b_batch_exceeds_max_batch():
         assert e.value.status == tp.TP_EINVAL
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("K,flags", [(2, 0), (3, 0), (4, 0), (4, tp.TP_FLAG_NCCL_LOOPBACK), (4, tp.TP_FLAG_SCHEDULE_1F1B)])
+def test_balanced_partition_parity(K, flags):
+    """TP_PARTITION_BALANCED (A-30): non-uniform contiguous layer blocks per stage (the last
+    stage, which runs the LM head, owns fewer layers); same function as the unsliced oracle."""
+    base, B = CONFIGS["small-deep"]
+    cfg = base.with_(n_stages=K)
+    assert K == 2 or len(set(tp.stage_layers(cfg))) > 1
+    params, tokens, ref = oracle_run(cfg, B, 15, True)
+    loss, logits, grads = gpu_run_plan(cfg, B, params, tokens, [(1, [40, 24, 64])] * B, tp.TP_BF16,
+                                       flags=tp.TP_FLAG_KEEP_LOGITS | flags)
+    check(worst_errors(loss, logits, grads, ref), 2e-2)
