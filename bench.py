@@ -218,8 +218,20 @@ def main():
     # producing kernels store into the neighbour's buffer; measured faster than
     # ncclSend/ncclRecv on 4 x B200); TP_DEVICE_P2P=0 selects ncclSend/ncclRecv
     p2p_device = world > 1 and os.environ.get("TP_DEVICE_P2P", "1") != "0"
-    ctx = tp.Context(cfg, rank=rank, world=world, nccl_id=nid, precision=tp.TP_BF16, max_batch=B,
-                     device=local_rank, flags=tp.TP_FLAG_DEVICE_P2P if p2p_device else 0)
+    p2p_note = None
+    try:
+        ctx = tp.Context(cfg, rank=rank, world=world, nccl_id=nid, precision=tp.TP_BF16, max_batch=B,
+                         device=local_rank, flags=tp.TP_FLAG_DEVICE_P2P if p2p_device else 0)
+    except tp.TpError as e:
+        if not p2p_device:
+            raise
+        # symmetric-memory windows unavailable on this box: the ncclSend/ncclRecv transport (every
+        # rank fails the collective registration alike, so all retry with a fresh communicator)
+        p2p_device, p2p_note = False, f"device p2p unavailable ({e}); ncclSend/ncclRecv used"
+        print(p2p_note, file=sys.stderr)
+        nid = tdist.share_nccl_id(rank)
+        ctx = tp.Context(cfg, rank=rank, world=world, nccl_id=nid, precision=tp.TP_BF16, max_batch=B,
+                         device=local_rank, flags=0)
     flat = make_stage_flat(cfg, stage, seed=0) if world > 1 else np.concatenate(
         [make_stage_flat(cfg, k, seed=0) for k in range(K)])
     ctx.load_params(flat)
@@ -334,7 +346,7 @@ def main():
         "config": {"workload": args.config, "n_layer": cfg.n_layer, "hidden": cfg.hidden, "heads": cfg.n_head,
                    "seq_len": cfg.seq_len, "batch": B, "vocab": cfg.vocab, "stages": K,
                    "parallelism": f"pipeline{K}", "slicing": main_sl.notation(), "granularity": g,
-                   "p2p": ("device" if p2p_device else "nccl") if world > 1 else None,
+                   "p2p": (("device" if p2p_device else "nccl") if world > 1 else None) if not p2p_note else p2p_note,
                    "stage_layers": tp.stage_layers(cfg),
                    "schedule": "1f1b" if os.environ.get("TP_SCHEDULE") == "1f1b" else "gpipe",
                    "l2": "working set > L2 (bf16 weights alone exceed 126 MB); no flush"},

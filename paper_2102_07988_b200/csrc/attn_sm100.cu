@@ -700,7 +700,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                           const __grid_constant__ CUtensorMap tmdQ, const __grid_constant__ CUtensorMap tmdK,
                           const __grid_constant__ CUtensorMap tmdV, const float* __restrict__ ldg, int s, int c, int l,
                           float scale, float scale_log2, int accumulate, int nheads, volatile int* dbg,
-                          long long* trace, int pf_dist) {
+                          long long* trace, int pf_dist, const float* __restrict__ dk_raw,
+                          const float* __restrict__ dv_raw, int64_t dkv_sstride, bf16* __restrict__ dkv_out,
+                          int64_t ldq, int64_t dq_sstride) {
   extern __shared__ uint8_t smem_raw[];
 #define DBG(role, v)                                                                    \
   do {                                                                                  \
@@ -999,6 +1001,29 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       tmem_ld32_nowait(lane_base + T_DK + ch * 32, rk);
       tmem_ld32_nowait(lane_base + T_DV + ch * 32, rv);
       tmem_wait_ld();
+      if (dkv_out && kabs >= c && kabs < c + l) {
+        // rows of this slice are final after this launch (later slices were processed before it):
+        // dK / dV = this launch's contribution + the earlier launches' accumulator rows, straight to
+        // the bf16 dQKV columns [H, 3H) of the job (the separate finalise pass is not needed)
+        const int H = nheads * AT;
+        bf16* outk = dkv_out + sq * dq_sstride + (int64_t)(kabs - c) * ldq + H + head * AT + ch * 32;
+        const int64_t src = sq * dkv_sstride + ((int64_t)head * s + kabs) * AT + ch * 32;
+#pragma unroll
+        for (int u = 0; u < 32; u += 8) {
+          float fk[8], fv[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) { fk[e] = __uint_as_float(rk[u + e]) * scale; fv[e] = __uint_as_float(rv[u + e]); }
+          if (accumulate) {
+            float ok[8], ov[8];
+            load8<float>(dk_raw + src + u, ok);
+            load8<float>(dv_raw + src + u, ov);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) { fk[e] += ok[e]; fv[e] += ov[e]; }
+          }
+          store8<bf16>(outk + u, fk);
+          store8<bf16>(outk + H + u, fv);
+        }
+      }
       uint8_t* bk = reinterpret_cast<uint8_t*>(stg + ch * 4096) + row * 128;
       uint8_t* bv = reinterpret_cast<uint8_t*>(stg + 16384 + ch * 4096) + row * 128;
 #pragma unroll
@@ -1013,7 +1038,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     }
     fence_proxy_async();
     named_bar(1, 256);
-    if (threadIdx.x == 64) {
+    // a key block entirely inside the slice needs no fp32 accumulator update (its rows were
+    // finalised above and no earlier slice reads them)
+    if (threadIdx.x == 64 && !(dkv_out && key0 >= c)) {
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         if (accumulate) {
@@ -1159,7 +1186,7 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
                            const bf16* v, const float* lse, float* Dvec, float* dq_acc, bf16* dq, int64_t ldq,
                            float* dk_acc, float* dv_acc, int a, int s, int d, int c, int l, int accumulate,
                            cudaStream_t st, int nseq, int64_t qkv_sstride, int64_t o_sstride, int64_t lse_sstride,
-                           int64_t dq_sstride, int64_t dkv_sstride) {
+                           int64_t dq_sstride, int64_t dkv_sstride, int finalize_dkv) {
   if (l == 0 || nseq == 0) return cudaSuccess;
   if (d != AT) return cudaErrorInvalidValue;
   static bool attr = false;
@@ -1217,9 +1244,16 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
   // off: distances 1-4 measured neutral at c = 576, l = 1472, 128 heads, 565-567 us — the kernel is
   // bound by shared-memory bandwidth, ~288 KB per 128 x 64 tile, not by load latency)
   static const int pf_dist = getenv("TP_ATTN_PF") ? atoi(getenv("TP_ATTN_PF")) : 0;
+  // dK / dV of the slice's own rows written as bf16 into dQKV by the kernel (TP_ATTN_DKV_FUSED=0: the
+  // fp32 accumulators only, finalised by attn_dkv_finalize)
+  static const bool dkv_fused_env = !getenv("TP_ATTN_DKV_FUSED") || atoi(getenv("TP_ATTN_DKV_FUSED")) != 0;
+  const bool dkv_fused = dkv_fused_env && finalize_dkv;
   attn_bwd_sm100_kernel<<<grid, BWD_THREADS, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, mdq, mdk, mdv, Dvec,
                                                            s, c, l, scale, scale * LOG2E_F, accumulate,
-                                                           a, dbg_dev, trace_left > 0 ? trace : nullptr, pf_dist);
+                                                           a, dbg_dev, trace_left > 0 ? trace : nullptr, pf_dist,
+                                                           dk_acc, dv_acc,
+                                                           nseq > 1 ? dkv_sstride : (int64_t)a * s * d, dkv_fused ? dq : nullptr,
+                                                           ldq, nseq > 1 ? dq_sstride : 0);
   e = cudaGetLastError();
   if (trace_left > 0) {
     --trace_left;
@@ -1254,7 +1288,11 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
   }
   if (e != cudaSuccess) return e;
   dq_convert_kernel<<<dim3(l, nseq), 128, 0, st>>>(dq_acc, H, dq, ldq, H, l, dq_sstride);
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (e == cudaSuccess && finalize_dkv && !dkv_fused)  // requested but switched off: the separate pass
+    e = attn_dkv_finalize<bf16>(dk_acc, dv_acc, dq, ldq, a, s, d, c, l, st, nseq, nseq > 1 ? dkv_sstride : 0,
+                                nseq > 1 ? dq_sstride : 0);
+  return e;
 }
 
 }  // namespace tp

@@ -90,7 +90,11 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
                            const bf16* v, const float* lse, float* Dvec, float* dq_acc, bf16* dq, int64_t ldq,
                            float* dk_acc, float* dv_acc, int a, int s, int d, int c, int l, int accumulate,
                            cudaStream_t st, int nseq = 1, int64_t qkv_sstride = 0, int64_t o_sstride = 0,
-                           int64_t lse_sstride = 0, int64_t dq_sstride = 0, int64_t dkv_sstride = 0);
+                           int64_t lse_sstride = 0, int64_t dq_sstride = 0, int64_t dkv_sstride = 0,
+                           int finalize_dkv = 0 /* 1: also write the slice rows' final dK / dV (bf16) into
+                                                   dq's columns [H, 3H) (row r of the slice: dq + r*ldq),
+                                                   replacing attn_dkv_finalize; their fp32 accumulator
+                                                   rows are then not maintained */);
 template <typename T>
 cudaError_t attn_dkv_finalize(const float* dk_acc, const float* dv_acc, T* dqkv, int64_t ld, int a,
                               int s, int d, int c, int l, cudaStream_t st, int nseq = 1, int64_t acc_sstride = 0,

@@ -787,14 +787,11 @@ class Engine final : public EngineBase {
       TRY(launch(KC_ATTN_BWD, attn_flops, b * (ebytes * 4.0 * H * (c + l) + 16.0 * H * (c + l)), [&] {
         if constexpr (std::is_same<T, bf16>::value)
           if (!force_simt && attn_sm100_supported(dh) && !legacy_attn) {  // all b sequences in one launch
-            cudaError_t e = attn_bwd_sm100(S.dO, (int64_t)b * H, S.O[j] + row * H, (int64_t)b * H, S.Q[j] + seq0 * s * H,
-                                           S.Kc[j] + seq0 * s * H, S.Vc[j] + seq0 * s * H, S.LSE[j] + seq0 * a * s, S.Dvec,
-                                           S.dqacc, dq, (int64_t)b * 3 * H, S.dk_acc[j], S.dv_acc[j], a, s, dh, c, l, accum,
-                                           stream, b, (int64_t)s * H, H, (int64_t)a * s, 3 * H, (int64_t)s * H);
-            if (e == cudaSuccess)
-              e = attn_dkv_finalize<T>(S.dk_acc[j], S.dv_acc[j], dq, (int64_t)b * 3 * H, a, s, dh, c, l, stream, b,
-                                       (int64_t)s * H, 3 * H);
-            return e;
+            // the kernel also writes the slice rows' final dK / dV into dQKV (no finalise pass)
+            return attn_bwd_sm100(S.dO, (int64_t)b * H, S.O[j] + row * H, (int64_t)b * H, S.Q[j] + seq0 * s * H,
+                                  S.Kc[j] + seq0 * s * H, S.Vc[j] + seq0 * s * H, S.LSE[j] + seq0 * a * s, S.Dvec,
+                                  S.dqacc, dq, (int64_t)b * 3 * H, S.dk_acc[j], S.dv_acc[j], a, s, dh, c, l, accum,
+                                  stream, b, (int64_t)s * H, H, (int64_t)a * s, 3 * H, (int64_t)s * H, 1);
           }
         for (int jj = 0; jj < b; ++jj) {
           const size_t sq = seq0 + jj;

@@ -40,7 +40,7 @@ def main():
     for K in [int(x) for x in args.stages.split(",")]:
         L = base.n_layer // K
         types = min(K, 2)
-        cfg = base.with_(n_layer=L * types, n_stages=types)
+        cfg = base.with_(n_layer=L * types, n_stages=types, partition=0)  # uniform cells
         ctx = tp.Context(cfg, max_batch=B, device=0)
         ctx.load_params(np.concatenate([make_stage_flat(cfg, k, seed=0) for k in range(types)]))
         bsl = [b for b in (1, 2, 4, 8, 16) if B % b == 0 and b <= B]
