@@ -20,6 +20,12 @@ Parity status: pinned (tests/test_oracle_plan.py) — optimize() == brute_force(
 random integer instances; SPEC.md:146-147 worked examples (T = 4, T = 10); closed form ==
 flow-shop simulation (SPEC.md:253-264 examples and random vectors); epsilon gap <= K*eps
 (PAPER.md:290); pruning soundness.
+
+Schedules (A-21, A-27): gpipe_oplists / one_f_one_b_oplists are the per-stage op lists
+(GPipe order of PAPER.md:373; 1F1B at group granularity) and oplist_replay replays any lists with
+the pipeline's data dependencies. Pinned: replay of the GPipe lists == oplist_makespan (the
+two-wave replay, itself == the A-19 closed form); 1F1B with one-job groups and uniform durations
+== the textbook (D + K - 1)(t_f + t_b); in-flight groups == min(D, K - k); deadlock detection.
 """
 from __future__ import annotations
 

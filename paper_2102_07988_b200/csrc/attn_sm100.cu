@@ -694,6 +694,9 @@ struct BwdSmem {
   static_assert(BYTES <= 232448, "backward tile set exceeds 227 KB of shared memory");
 };
 
+// DQ = false: dK / dV only (the split backward: dQ comes from attn_bwd_dq_sm100_kernel) — no dQ^T
+// MMA, no dS^T shared-memory copy, no drain warps.
+template <bool DQ>
 __global__ void __launch_bounds__(BWD_THREADS, 1)
     attn_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                           const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
@@ -817,7 +820,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     auto issue_dp = [&](int j) {
       const int bq = j % NQB, bb = j & 1;
       const uint32_t o_base = smem_u32(sm + BwdSmem::O + bq * QT);
-      if (j >= 2) mbar_wait(dqfree + bb, ((j >> 1) - 1) & 1);
+      if (DQ && j >= 2) mbar_wait(dqfree + bb, ((j >> 1) - 1) & 1);
       if (lane == 0) TRC(1, 2, j);
       tc_fence_after();
 #pragma unroll
@@ -853,18 +856,23 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
       mma_commit_w(qfree + bq);
       if (i + 1 < ntile) issue_dp(i + 1);
+      if constexpr (DQ) {
 #pragma unroll
-      for (int kk = 0; kk < AT / 16; ++kk)
-        mma_bf16_w(tb + 64, make_desc(k_base + kk * 2048, HALF, 1024), make_desc(ds_base + kk * 2048, 8192, 1024), idQ,
-                 kk > 0);
-      mma_commit_w(dqfull + bb);
-      mma_commit_w(dsfree + bb);
+        for (int kk = 0; kk < AT / 16; ++kk)
+          mma_bf16_w(tb + 64, make_desc(k_base + kk * 2048, HALF, 1024), make_desc(ds_base + kk * 2048, 8192, 1024), idQ,
+                   kk > 0);
+        mma_commit_w(dqfull + bb);
+        mma_commit_w(dsfree + bb);
+      }
       if (lane == 0) TRC(1, 4, i);
       if (lane == 0) DBG(1, 105 + 10 * i);
     }
     mma_commit_w(done);
     if (lane == 0) DBG(1, 999);
   } else if (warp >= 10) {
+    if constexpr (!DQ) {
+      // no dQ^T to drain
+    } else {
     // ---------------- dQ drain warps (one per TMEM lane quarter; thread = head-dim index `row`):
     // dQ^T of tile j -> smem [64 q][128 d] -> one TMA reduce-add into dq_acc
     const int q = warp & 3, row = q * 32 + lane;
@@ -894,6 +902,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       if (leader) { tma_reduce_add_3d(&tmdQ, dqs, head * AT, (qt0 + j) * BQB, sq); TRC(2, 5, j); }
     }
     if (leader) tma_wait_all();
+    }
   } else if (warp >= 2) {
     // ---------------- softmax-gradient warps: two per TMEM lane quarter; thread owns key row `row`
     // and query columns [half*32, half*32+32) of the tile (head-dim columns for dK / dV)
@@ -947,7 +956,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
       // phase 2 (needs dP^T): dS^T = P^T (dP^T - D) -> bf16 -> smem (K-major swizzled)
       mbar_wait(dpfull + bb, (i >> 1) & 1);
-      if (i >= 2) mbar_wait(dsfree + bb, ((i >> 1) - 1) & 1);  // dK / dQ MMAs of tile i-2 read dS^T buffer bb
+      if (DQ && i >= 2) mbar_wait(dsfree + bb, ((i >> 1) - 1) & 1);  // dK / dQ MMAs of tile i-2 read dS^T buffer bb
       tc_fence_after();
       uint8_t* dSt = sm + BwdSmem::DS + bb * PT;
 #pragma unroll
@@ -970,10 +979,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           __nv_bfloat162 hd = __floats2bfloat162_rn(d0, d1);
           dk[t >> 1] = *reinterpret_cast<uint32_t*>(&hd);
         }
+        if constexpr (DQ) {
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int cc = half * 4 + ch * 2 + u;
-          *reinterpret_cast<uint4*>(dSt + swz(row, cc)) = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+          for (int u = 0; u < 2; ++u) {
+            const int cc = half * 4 + ch * 2 + u;
+            *reinterpret_cast<uint4*>(dSt + swz(row, cc)) = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+          }
         }
         // and packed into TMEM (second 16 of this half's S^T columns) as dK's A operand
         tmem_st8(lane_base + bb * 128 + half * HQ + 16 + ch * 8, dk);
@@ -1054,6 +1065,199 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       tma_commit_group();
       tma_wait_all();
       TRC(2, 7, 0);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------ backward, dQ (split backward)
+// Per (128 query rows of the slice, head, sequence), heaviest first; loop over the key blocks the
+// rows see. dQ = scale * sum_j dS_j K_j with dS = P (dP - D), P = exp2(S scale_log2 - lse log2e):
+// the same function as the fused kernel's dQ^T, but accumulated in TMEM over the key blocks and
+// written once as bf16 (no fp32 partials, no atomics, no conversion pass).
+// TMEM: S_0 (cols 0-127), S_1 (128-255), dP (256-383), dQ (384-511).
+//   warp 0    TMA: Q and dO once; K_j, V_j through 2-deep rings;
+//   warp 1    MMA: S_{j+1} = Q K_{j+1}^T (once dQ has read dS_{j-1} from that buffer), then
+//             dQ += dS_j K_j (TS-MMA, dS from TMEM), then dP_{j+1} = dO V_{j+1}^T;
+//   warps 2-5 thread = query row: P, dS = P (dP - D), packed bf16 over S_j's first 64 columns.
+constexpr int DQ_THREADS = 192;
+struct DqSmem {
+  static constexpr uint32_t Q = 0, O = TILE, K = 2 * TILE, V = K + 2 * TILE;
+  static constexpr uint32_t BAR = V + 2 * TILE;
+  static constexpr uint32_t BYTES = BAR + 256 + 1024;
+  static_assert(BYTES <= 232448, "dQ tile set exceeds 227 KB of shared memory");
+};
+
+__global__ void __launch_bounds__(DQ_THREADS, 1)
+    attn_bwd_dq_sm100_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
+                             const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                             const float* __restrict__ ldg, bf16* __restrict__ dq, int64_t ldq, int64_t dq_sstride,
+                             int s, int c, int l, float scale, float scale_log2, int nheads) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (tc5::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + DqSmem::BAR);
+  uint64_t* qfull = bars + 0;
+  uint64_t* kfull = bars + 1;   // [2]
+  uint64_t* kfree = bars + 3;   // [2]
+  uint64_t* vfull = bars + 5;   // [2]
+  uint64_t* vfree = bars + 7;   // [2]
+  uint64_t* sfull = bars + 9;   // [2]
+  uint64_t* dpfull = bars + 11;
+  uint64_t* pfull = bars + 12;  // [2] dS_j written, dP_j consumed (4 warps)
+  uint64_t* dqdone = bars + 14; // [2] dQ += dS_j K_j complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int head = blockIdx.y, sq = blockIdx.z, r0 = (gridDim.x - 1 - blockIdx.x) * AT;
+  const int nkb = (c + min(l, r0 + AT) - 1) / AT + 1;
+
+  if (threadIdx.x == 0) {
+    mbar_init(qfull, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(kfull + i, 1); mbar_init(kfree + i, 1); mbar_init(vfull + i, 1); mbar_init(vfree + i, 1);
+      mbar_init(sfull + i, 1); mbar_init(pfull + i, 4); mbar_init(dqdone + i, 1);
+    }
+    mbar_init(dpfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t T_DP = 256, T_DQ = 384;
+
+  if (warp == 0 && lane == 0) {
+    mbar_expect_tx(qfull, 2 * TILE);
+    tma_load_4d(sm + DqSmem::Q, &tmQ, 0, c + r0, head, sq, qfull);
+    tma_load_4d(sm + DqSmem::Q + HALF, &tmQ, 64, c + r0, head, sq, qfull);
+    tma_load_3d(sm + DqSmem::O, &tmdO, head * AT, r0, sq, qfull);
+    tma_load_3d(sm + DqSmem::O + HALF, &tmdO, head * AT + 64, r0, sq, qfull);
+    for (int j = 0; j < nkb; ++j) {
+      const int b = j & 1;
+      if (j >= 2) mbar_wait(kfree + b, ((j >> 1) - 1) & 1);
+      mbar_expect_tx(kfull + b, TILE);
+      tma_load_4d(sm + DqSmem::K + b * TILE, &tmK, 0, j * AT, head, sq, kfull + b);
+      tma_load_4d(sm + DqSmem::K + b * TILE + HALF, &tmK, 64, j * AT, head, sq, kfull + b);
+      if (j >= 2) mbar_wait(vfree + b, ((j >> 1) - 1) & 1);
+      mbar_expect_tx(vfull + b, TILE);
+      tma_load_4d(sm + DqSmem::V + b * TILE, &tmV, 0, j * AT, head, sq, vfull + b);
+      tma_load_4d(sm + DqSmem::V + b * TILE + HALF, &tmV, 64, j * AT, head, sq, vfull + b);
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idS = idesc_bf16(128, 128, false, false);  // S, dP (both operands K-major)
+    constexpr uint32_t idQ = idesc_bf16(128, 128, false, true);   // dQ += dS K (B = K as [keys][d], MN-major)
+    const uint32_t q_base = smem_u32(sm + DqSmem::Q), o_base = smem_u32(sm + DqSmem::O);
+    auto issue_s = [&](int j) {
+      const uint32_t k_base = smem_u32(sm + DqSmem::K + (j & 1) * TILE);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < AT / 16; ++kk) {
+        const uint32_t off = (kk >> 2) * HALF + (kk & 3) * 32;
+        mma_bf16_w(tmem + (j & 1) * 128, make_desc(q_base + off, 16, 1024), make_desc(k_base + off, 16, 1024), idS, kk > 0);
+      }
+      mma_commit_w(sfull + (j & 1));
+    };
+    auto issue_dp = [&](int j) {
+      const uint32_t v_base = smem_u32(sm + DqSmem::V + (j & 1) * TILE);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < AT / 16; ++kk) {
+        const uint32_t off = (kk >> 2) * HALF + (kk & 3) * 32;
+        mma_bf16_w(tmem + T_DP, make_desc(o_base + off, 16, 1024), make_desc(v_base + off, 16, 1024), idS, kk > 0);
+      }
+      mma_commit_w(dpfull);
+      mma_commit_w(vfree + (j & 1));
+    };
+    mbar_wait(qfull, 0);
+    mbar_wait(kfull, 0);
+    issue_s(0);
+    mbar_wait(vfull, 0);
+    issue_dp(0);
+    for (int j = 0; j < nkb; ++j) {
+      const int b = j & 1;
+      if (j + 1 < nkb) {
+        mbar_wait(kfull + (b ^ 1), ((j + 1) >> 1) & 1);
+        if (j >= 1) mbar_wait(dqdone + (b ^ 1), ((j - 1) >> 1) & 1);  // dS_{j-1} read from that buffer
+        issue_s(j + 1);
+      }
+      mbar_wait(pfull + b, (j >> 1) & 1);  // dS_j in S buffer b, dP_j consumed
+      tc_fence_after();
+      const uint32_t k_base = smem_u32(sm + DqSmem::K + b * TILE);
+#pragma unroll
+      for (int kk = 0; kk < AT / 16; ++kk)
+        mma_bf16_ts_w(tmem + T_DQ, tmem + b * 128 + kk * 8, make_desc(k_base + kk * 2048, HALF, 1024), idQ,
+                      (j | kk) != 0);
+      mma_commit_w(dqdone + b);
+      mma_commit_w(kfree + b);
+      if (j + 1 < nkb) {
+        mbar_wait(vfull + (b ^ 1), ((j + 1) >> 1) & 1);
+        issue_dp(j + 1);
+      }
+    }
+  } else if (warp >= 2) {
+    const int q = warp & 3, row = q * 32 + lane;
+    const int qr = r0 + row;                // row of the slice
+    const int qabs = c + qr;
+    const bool live = qr < l;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    // lse * log2e and D of this query from the per-64-query-tile staging of bwd_stage_kernel
+    const int ntq = (l + BQB - 1) / BQB;
+    const float* st = ldg + ((int64_t)sq * nheads + head) * ntq * (2 * BQB) + (qr / BQB) * (2 * BQB) + (qr % BQB);
+    const float lse2 = live ? st[0] : 0.f;
+    const float Dq = live ? st[BQB] : 0.f;
+    for (int j = 0; j < nkb; ++j) {
+      const int b = j & 1;
+      mbar_wait(sfull + b, (j >> 1) & 1);
+      mbar_wait(dpfull, j & 1);
+      tc_fence_after();
+      const int nvis = live ? qabs - j * AT + 1 : 0;  // keys j*128 .. qabs visible
+#pragma unroll
+      for (int ch = 0; ch < AT / 32; ++ch) {
+        uint32_t rs[32], rp[32];
+        tmem_ld32_nowait(lane_base + b * 128 + ch * 32, rs);
+        tmem_ld32_nowait(lane_base + T_DP + ch * 32, rp);
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int u = 0; u < 32; u += 2) {
+          const int col = ch * 32 + u;
+          const float p0 = col < nvis ? ex2(fmaf(__uint_as_float(rs[u]), scale_log2, -lse2)) : 0.f;
+          const float p1 = col + 1 < nvis ? ex2(fmaf(__uint_as_float(rs[u + 1]), scale_log2, -lse2)) : 0.f;
+          const float d0 = p0 * (__uint_as_float(rp[u]) - Dq), d1 = p1 * (__uint_as_float(rp[u + 1]) - Dq);
+          __nv_bfloat162 h = __floats2bfloat162_rn(d0, d1);
+          pk[u >> 1] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        // dS packed over S_j's columns [16 ch, 16 ch + 16): already read (chunks 0 .. ch)
+        tmem_st16(lane_base + b * 128 + ch * 16, pk);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(pfull + b);
+    }
+    mbar_wait(dqdone + ((nkb - 1) & 1), ((nkb - 1) >> 1) & 1);
+    tc_fence_after();
+    bf16* out = dq + sq * dq_sstride + (int64_t)qr * ldq + head * AT;
+#pragma unroll 1
+    for (int ch = 0; ch < AT / 32; ++ch) {
+      uint32_t rr[32];
+      tmem_ld32_nowait(lane_base + T_DQ + ch * 32, rr);
+      tmem_wait_ld();
+      if (live) {
+#pragma unroll
+        for (int u = 0; u < 32; u += 8) {
+          float v8[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v8[e] = __uint_as_float(rr[u + e]) * scale;
+          store8<bf16>(out + ch * 32 + u, v8);
+        }
+      }
     }
   }
   tc_fence_before();
@@ -1191,14 +1395,23 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
   if (d != AT) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_sm100_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)BwdSmem::BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_bwd_sm100_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)BwdSmem::BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_bwd_dq_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)DqSmem::BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  // split backward (TP_ATTN_BWD_SPLIT, default on): the key-block kernel computes dK / dV only and
+  // a query-tile kernel computes dQ in TMEM (no fp32 partials, no atomics, no conversion pass)
+  static const bool split = !getenv("TP_ATTN_BWD_SPLIT") || atoi(getenv("TP_ATTN_BWD_SPLIT")) != 0;
   const int H = a * d;
   const int ntq = (l + BQB - 1) / BQB;
-  cudaError_t e = cudaMemsetAsync(dq_acc, 0, sizeof(float) * (size_t)l * H * nseq, st);
+  cudaError_t e = split ? cudaSuccess : cudaMemsetAsync(dq_acc, 0, sizeof(float) * (size_t)l * H * nseq, st);
   if (e != cudaSuccess) return e;
   bwd_stage_kernel<<<dim3((ntq * BQB + 3) / 4, nseq), 128, 0, st>>>(dO, ld_do, o, ldo, lse, lse_sstride, Dvec, a, s, c,
                                                                      l, ntq, o_sstride);
@@ -1248,7 +1461,8 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
   // fp32 accumulators only, finalised by attn_dkv_finalize)
   static const bool dkv_fused_env = !getenv("TP_ATTN_DKV_FUSED") || atoi(getenv("TP_ATTN_DKV_FUSED")) != 0;
   const bool dkv_fused = dkv_fused_env && finalize_dkv;
-  attn_bwd_sm100_kernel<<<grid, BWD_THREADS, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, mdq, mdk, mdv, Dvec,
+  auto bwd_kernel = split ? attn_bwd_sm100_kernel<false> : attn_bwd_sm100_kernel<true>;
+  bwd_kernel<<<grid, BWD_THREADS, BwdSmem::BYTES, st>>>(mk, mv, mq, mo, mdq, mdk, mdv, Dvec,
                                                            s, c, l, scale, scale * LOG2E_F, accumulate,
                                                            a, dbg_dev, trace_left > 0 ? trace : nullptr, pf_dist,
                                                            dk_acc, dv_acc,
@@ -1287,7 +1501,16 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
     }
   }
   if (e != cudaSuccess) return e;
-  dq_convert_kernel<<<dim3(l, nseq), 128, 0, st>>>(dq_acc, H, dq, ldq, H, l, dq_sstride);
+  if (split) {
+    const uint32_t obox128[3] = {64, AT, 1};
+    CUtensorMap mq128, mo128;
+    if (!encode_bf16_map(&mq128, q, 4, kdims, kstr, kbox) || !encode_bf16_map(&mo128, dO, 3, odims, ostr, obox128))
+      return cudaErrorInvalidValue;
+    attn_bwd_dq_sm100_kernel<<<dim3((l + AT - 1) / AT, a, nseq), DQ_THREADS, DqSmem::BYTES, st>>>(
+        mq128, mo128, mk, mv, Dvec, dq, ldq, nseq > 1 ? dq_sstride : 0, s, c, l, scale, scale * LOG2E_F, a);
+  } else {
+    dq_convert_kernel<<<dim3(l, nseq), 128, 0, st>>>(dq_acc, H, dq, ldq, H, l, dq_sstride);
+  }
   e = cudaGetLastError();
   if (e == cudaSuccess && finalize_dkv && !dkv_fused)  // requested but switched off: the separate pass
     e = attn_dkv_finalize<bf16>(dk_acc, dv_acc, dq, ldq, a, s, d, c, l, st, nseq, nseq > 1 ? dkv_sstride : 0,

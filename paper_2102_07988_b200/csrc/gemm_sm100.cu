@@ -278,7 +278,7 @@ __device__ __forceinline__ void epi_tile(const Epi& epi, const SplitK& sk, float
 template <int CG, int BN, bool A_MN, bool B_MN, int WN, int KIND>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                      int K, Epi epi, SplitK sk, int group_m) {
+                      int K, Epi epi, SplitK sk, int group_m, int epi_pf) {
   using C = Cfg<CG, BN, WN>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-aligned base derived by pointer arithmetic on the __shared__ array (not through an
@@ -424,6 +424,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int mt, nt;
       tile_mn(tile, m_tiles, n_tiles, group_m, mt, nt);
       const int m0 = mt * C::TILE_M + crank * BM, n0 = nt * C::TILE_N;
+      // the tile's epilogue operand (RESID: fp32 residual rows, DGELU: U) pulled into L2 while the
+      // tile's MMAs run, so the epilogue's loads are L2 hits: one prefetch per 128-byte row segment
+      if constexpr (KIND == EPI_RESID || KIND == EPI_DGELU) {
+        if (epi_pf && (lane & 3) == 0) {
+#pragma unroll 1
+          for (int ch = ch0; ch < ch1; ++ch) {
+            const int n = n0 + ch * 32;
+            if (n >= N) break;
+#pragma unroll
+            for (int it = 0; it < 4; ++it) {
+              const int row = m0 + q * 32 + it * 8 + (lane >> 2);
+              if (row >= M) break;
+              const void* a = KIND == EPI_RESID
+                                  ? (const void*)(epi.resid + (int64_t)row * epi.ldr + n + epi.n_off)
+                                  : (const void*)(reinterpret_cast<const bf16*>(epi.aux) + (int64_t)row * epi.ld_aux + n + epi.n_off);
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+            }
+          }
+        }
+      }
       int v_lo = unit, v_hi = unit;
       if (kind == 2) {
         // finisher: the units below whose ranges cover [tile start, this segment's start) left partials
@@ -481,9 +501,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 int g_force_cg = 0;  // test hook: TP_GEMM_CG=1|2 forces the CTA-group size
-// Stream-K tail (TP_GEMM_STREAMK=0 disables, read per launch): ~2 % on the 13B 4-stage pipeline
-// step (its slice GEMMs leave partial waves), neutral at N = 1.
-int g_stream_k = 1;
+// Stream-K (TP_GEMM_STREAMK=1 enables, read per launch; off by default, see launch_bn).
+int g_stream_k = 0;
 int g_num_sms = 0;
 std::once_flag g_once;
 
@@ -535,8 +554,11 @@ cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   sk.dp_tiles = tiles;
   const int kbs = (g.K + BK - 1) / BK;
   {
+    // stream-K is opt-in (TP_GEMM_STREAMK=1): inside the full N = 1 step it measured 3-5 ms slower
+    // (144.3-146.5 vs 141.1-141.4 ms, alternating runs on one box) although isolated long-K shapes
+    // gain 3-8 % — the partial tiles' fp32 traffic competes with the rest of the step
     const char* e = getenv("TP_GEMM_STREAMK");
-    g_stream_k = e ? atoi(e) : 1;
+    g_stream_k = e ? atoi(e) : 0;
   }
   if (g.persistent && g_stream_k && g.sk_ws && g.sk_cnt) {
     // DP + one stream-K wave when the last wave would leave > 6 % of the units idle and each unit's
@@ -573,7 +595,9 @@ cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   // raster group: TP_GEMM_GROUP rows of M per group (default 2048; >= M gives the plain m-fastest order)
   const int group_rows = getenv("TP_GEMM_GROUP") ? std::max(1, atoi(getenv("TP_GEMM_GROUP"))) : 2048;
   const int group_m = std::max(1, group_rows / C::TILE_M);
-  return cudaLaunchKernelEx(&cfg, kern, ta, tb, g.M, g.N, g.K, e, sk, group_m);
+  // L2 prefetch of the epilogue operand ahead of each tile (TP_GEMM_EPI_PF=0 disables)
+  static const int epi_pf = getenv("TP_GEMM_EPI_PF") ? atoi(getenv("TP_GEMM_EPI_PF")) : 1;
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, g.M, g.N, g.K, e, sk, group_m, epi_pf);
 }
 
 template <int CG, int BN, int WN = 1>
@@ -712,7 +736,7 @@ cudaError_t gemm_sm100(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   // half a wave. The second launch sees its columns through Epi::n_off.
   // stream-K (launch_bn) supersedes this split where it can apply: K long enough for >= 2 parts of
   // >= 32 k-blocks each
-  const bool sk_on = (!getenv("TP_GEMM_STREAMK") || atoi(getenv("TP_GEMM_STREAMK")) != 0) && (g.K + BK - 1) / BK >= 64;
+  const bool sk_on = getenv("TP_GEMM_STREAMK") && atoi(getenv("TP_GEMM_STREAMK")) != 0 && (g.K + BK - 1) / BK >= 64;
   if (!sk_on && g.persistent && !g_force_cg && (best == 0 || best == 2)) {
     const Cand& c = cands[best];
     const Cand& h = cands[best + 1];  // same CTA group, BN / 2
