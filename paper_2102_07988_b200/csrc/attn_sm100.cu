@@ -1406,9 +1406,10 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  // split backward (TP_ATTN_BWD_SPLIT, default on): the key-block kernel computes dK / dV only and
-  // a query-tile kernel computes dQ in TMEM (no fp32 partials, no atomics, no conversion pass)
-  static const bool split = !getenv("TP_ATTN_BWD_SPLIT") || atoi(getenv("TP_ATTN_BWD_SPLIT")) != 0;
+  // split backward (TP_ATTN_BWD_SPLIT=1, opt-in): the key-block kernel computes dK / dV only and a
+  // query-tile kernel computes dQ in TMEM (no fp32 partials, no atomics, no conversion pass).
+  // Measured slower in the N = 1 step (attention backward 25.6-26.3 vs 20.5 ms per step)
+  static const bool split = getenv("TP_ATTN_BWD_SPLIT") && atoi(getenv("TP_ATTN_BWD_SPLIT")) != 0;
   const int H = a * d;
   const int ntq = (l + BQB - 1) / BQB;
   cudaError_t e = split ? cudaSuccess : cudaMemsetAsync(dq_acc, 0, sizeof(float) * (size_t)l * H * nseq, st);

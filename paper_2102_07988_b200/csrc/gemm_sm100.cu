@@ -595,8 +595,9 @@ cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   // raster group: TP_GEMM_GROUP rows of M per group (default 2048; >= M gives the plain m-fastest order)
   const int group_rows = getenv("TP_GEMM_GROUP") ? std::max(1, atoi(getenv("TP_GEMM_GROUP"))) : 2048;
   const int group_m = std::max(1, group_rows / C::TILE_M);
-  // L2 prefetch of the epilogue operand ahead of each tile (TP_GEMM_EPI_PF=0 disables)
-  static const int epi_pf = getenv("TP_GEMM_EPI_PF") ? atoi(getenv("TP_GEMM_EPI_PF")) : 1;
+  // L2 prefetch of the epilogue operand ahead of each tile (TP_GEMM_EPI_PF=1; measured neutral in the
+  // N = 1 step, off by default)
+  static const int epi_pf = getenv("TP_GEMM_EPI_PF") ? atoi(getenv("TP_GEMM_EPI_PF")) : 0;
   return cudaLaunchKernelEx(&cfg, kern, ta, tb, g.M, g.N, g.K, e, sk, group_m, epi_pf);
 }
 
