@@ -840,6 +840,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       const uint32_t tb = tmem + bb * 128;
       if (lane == 0) DBG(1, 100 + 10 * i);
       if (i + 1 < ntile) issue_s(i + 1);
+      // without dQ^T the dP^T columns of buffer (i+1)&1 only held dP^T(i-1), consumed before pfull(i-1):
+      // issue dP^T(i+1) right away, so tile i+1's softmax finds both S^T and dP^T ready
+      if (!DQ && i + 1 < ntile) issue_dp(i + 1);
       if (lane == 0) DBG(1, 101 + 10 * i);
       mbar_wait(pfull + bb, (i >> 1) & 1);
       if (lane == 0) TRC(1, 3, i);
@@ -855,7 +858,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                       idKV, (i | kk) != 0);
       }
       mma_commit_w(qfree + bq);
-      if (i + 1 < ntile) issue_dp(i + 1);
+      if (DQ && i + 1 < ntile) issue_dp(i + 1);
       if constexpr (DQ) {
 #pragma unroll
         for (int kk = 0; kk < AT / 16; ++kk)
@@ -1083,9 +1086,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 // TMEM: S_0 (cols 0-127), S_1 (128-255), dP (256-383), dQ (384-511).
 //   warp 0    TMA: Q and dO once; K_j, V_j through 2-deep rings;
 //   warp 1    MMA: S_{j+1} = Q K_{j+1}^T (once dQ has read dS_{j-1} from that buffer), then
-//             dQ += dS_j K_j (TS-MMA, dS from TMEM), then dP_{j+1} = dO V_{j+1}^T;
-//   warps 2-5 thread = query row: P, dS = P (dP - D), packed bf16 over S_j's first 64 columns.
-constexpr int DQ_THREADS = 192;
+//             dP_{j+1} = dO V_{j+1}^T (the softmax has read dP_j), then dQ += dS_j K_j (TS-MMA);
+//   warps 2-9 two per query row (TMEM lane), 64 key columns each: P, dS = P (dP - D), packed bf16
+//             over S_j's first 64 columns.
+constexpr int DQ_THREADS = 320;  // TMA, MMA, 8 softmax warps (two per TMEM lane quarter)
 struct DqSmem {
   static constexpr uint32_t Q = 0, O = TILE, K = 2 * TILE, V = K + 2 * TILE;
   static constexpr uint32_t BAR = V + 2 * TILE;
@@ -1108,7 +1112,7 @@ __global__ void __launch_bounds__(DQ_THREADS, 1)
   uint64_t* vfree = bars + 7;   // [2]
   uint64_t* sfull = bars + 9;   // [2]
   uint64_t* dpfull = bars + 11;
-  uint64_t* pfull = bars + 12;  // [2] dS_j written, dP_j consumed (4 warps)
+  uint64_t* pfull = bars + 12;  // [2] dS_j written, dP_j consumed (8 warps)
   uint64_t* dqdone = bars + 14; // [2] dQ += dS_j K_j complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
@@ -1120,7 +1124,7 @@ __global__ void __launch_bounds__(DQ_THREADS, 1)
     mbar_init(qfull, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(kfull + i, 1); mbar_init(kfree + i, 1); mbar_init(vfull + i, 1); mbar_init(vfree + i, 1);
-      mbar_init(sfull + i, 1); mbar_init(pfull + i, 4); mbar_init(dqdone + i, 1);
+      mbar_init(sfull + i, 1); mbar_init(pfull + i, 8); mbar_init(dqdone + i, 1);
     }
     mbar_init(dpfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1187,6 +1191,10 @@ __global__ void __launch_bounds__(DQ_THREADS, 1)
         issue_s(j + 1);
       }
       mbar_wait(pfull + b, (j >> 1) & 1);  // dS_j in S buffer b, dP_j consumed
+      if (j + 1 < nkb) {  // first, so the next block's softmax is not behind dQ_j
+        mbar_wait(vfull + (b ^ 1), ((j + 1) >> 1) & 1);
+        issue_dp(j + 1);
+      }
       tc_fence_after();
       const uint32_t k_base = smem_u32(sm + DqSmem::K + b * TILE);
 #pragma unroll
@@ -1195,13 +1203,9 @@ __global__ void __launch_bounds__(DQ_THREADS, 1)
                       (j | kk) != 0);
       mma_commit_w(dqdone + b);
       mma_commit_w(kfree + b);
-      if (j + 1 < nkb) {
-        mbar_wait(vfull + (b ^ 1), ((j + 1) >> 1) & 1);
-        issue_dp(j + 1);
-      }
     }
   } else if (warp >= 2) {
-    const int q = warp & 3, row = q * 32 + lane;
+    const int q = warp & 3, row = q * 32 + lane, half = (warp - 2) >> 2;  // key columns [64 half, +64)
     const int qr = r0 + row;                // row of the slice
     const int qabs = c + qr;
     const bool live = qr < l;
@@ -1218,7 +1222,8 @@ __global__ void __launch_bounds__(DQ_THREADS, 1)
       tc_fence_after();
       const int nvis = live ? qabs - j * AT + 1 : 0;  // keys j*128 .. qabs visible
 #pragma unroll
-      for (int ch = 0; ch < AT / 32; ++ch) {
+      for (int cc = 0; cc < 2; ++cc) {
+        const int ch = half * 2 + cc;
         uint32_t rs[32], rp[32];
         tmem_ld32_nowait(lane_base + b * 128 + ch * 32, rs);
         tmem_ld32_nowait(lane_base + T_DP + ch * 32, rp);
@@ -1233,7 +1238,10 @@ __global__ void __launch_bounds__(DQ_THREADS, 1)
           __nv_bfloat162 h = __floats2bfloat162_rn(d0, d1);
           pk[u >> 1] = *reinterpret_cast<uint32_t*>(&h);
         }
-        // dS packed over S_j's columns [16 ch, 16 ch + 16): already read (chunks 0 .. ch)
+        // dS packed over S_j's columns [16 ch, 16 ch + 16): for half 0 these are its own already-read
+        // columns; for half 1 (ch = 2, 3: columns 32-63) they belong to half 0's second chunk, so half
+        // 1 waits until half 0 of the same lane quarter has read them (named barrier per quarter)
+        if (cc == (half == 0 ? 1 : 0)) named_bar(3 + q, 64);  // half 0: after reading chunk 1
         tmem_st16(lane_base + b * 128 + ch * 16, pk);
       }
       tmem_wait_st();
@@ -1245,7 +1253,7 @@ __global__ void __launch_bounds__(DQ_THREADS, 1)
     tc_fence_after();
     bf16* out = dq + sq * dq_sstride + (int64_t)qr * ldq + head * AT;
 #pragma unroll 1
-    for (int ch = 0; ch < AT / 32; ++ch) {
+    for (int ch = half * 2; ch < half * 2 + 2; ++ch) {
       uint32_t rr[32];
       tmem_ld32_nowait(lane_base + T_DQ + ch * 32, rr);
       tmem_wait_ld();
