@@ -156,6 +156,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="gpt3-1b")
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--max-batch", type=int, default=0,
+                    help="sequences the stage buffers hold (default: the batch; 1F1B may use fewer, DESIGN.md A-27)")
     ap.add_argument("--granularity", type=int, default=64)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-gpipe", action="store_true")
@@ -219,8 +221,10 @@ def main():
     # ncclSend/ncclRecv on 4 x B200); TP_DEVICE_P2P=0 selects ncclSend/ncclRecv
     p2p_device = world > 1 and os.environ.get("TP_DEVICE_P2P", "1") != "0"
     p2p_note = None
+    mb = args.max_batch or B
+    free0 = torch.cuda.mem_get_info()[0]
     try:
-        ctx = tp.Context(cfg, rank=rank, world=world, nccl_id=nid, precision=tp.TP_BF16, max_batch=B,
+        ctx = tp.Context(cfg, rank=rank, world=world, nccl_id=nid, precision=tp.TP_BF16, max_batch=mb,
                          device=local_rank, flags=tp.TP_FLAG_DEVICE_P2P if p2p_device else 0)
     except tp.TpError as e:
         if not p2p_device:
@@ -230,8 +234,9 @@ def main():
         p2p_device, p2p_note = False, f"device p2p unavailable ({e}); ncclSend/ncclRecv used"
         print(p2p_note, file=sys.stderr)
         nid = tdist.share_nccl_id(rank)
-        ctx = tp.Context(cfg, rank=rank, world=world, nccl_id=nid, precision=tp.TP_BF16, max_batch=B,
+        ctx = tp.Context(cfg, rank=rank, world=world, nccl_id=nid, precision=tp.TP_BF16, max_batch=mb,
                          device=local_rank, flags=0)
+    ctx_mem_gb = (free0 - torch.cuda.mem_get_info()[0]) / 1e9  # the library's device allocations
     flat = make_stage_flat(cfg, stage, seed=0) if world > 1 else np.concatenate(
         [make_stage_flat(cfg, k, seed=0) for k in range(K)])
     ctx.load_params(flat)
@@ -247,7 +252,7 @@ def main():
     # the per-b uniform plans (tp_plan with D = B/b, A-20) are reported as candidates.
     g = args.granularity
     bsl = [int(x) for x in args.batch_slices.split(",")] if args.batch_slices != "auto" else \
-        [x for x in (1, 2, 4, 8, 16) if B % x == 0 and x <= B]
+        [x for x in (1, 2, 4, 8, 16) if B % x == 0 and x <= min(B, mb)]
     dp, fit, t_prof, t_plan, plans = None, None, 0.0, 0.0, []
     gpipe = tp.BatchPlan.uniform(tp.Slicing([cfg.seq_len]), B)
     comm, t_wgrad = None, None
@@ -347,7 +352,8 @@ def main():
                    "seq_len": cfg.seq_len, "batch": B, "vocab": cfg.vocab, "stages": K,
                    "parallelism": f"pipeline{K}", "slicing": main_sl.notation(), "granularity": g,
                    "p2p": (("device" if p2p_device else "nccl") if world > 1 else None) if not p2p_note else p2p_note,
-                   "stage_layers": tp.stage_layers(cfg),
+                   "stage_layers": tp.stage_layers(cfg), "max_batch": mb,
+                   "device_mem_gb": allmax(ctx_mem_gb),
                    "schedule": "1f1b" if os.environ.get("TP_SCHEDULE") == "1f1b" else "gpipe",
                    "l2": "working set > L2 (bf16 weights alone exceed 126 MB); no flush"},
         "mfu": mfu, "mfu_sustained_peak": flops / (ms / 1e3) / (args.gpus * peak_sust * 1e12),
