@@ -273,7 +273,10 @@ def main():
             n = cfg.seq_len // g
             gp_pred = (B // b + K - 1) * int(ticks[n - 1, 0])   # unsliced [(b, [s])] * (B/b)
             plans.append({"b": b, "slicing": sl, "fit": f, "gpipe_pred": gp_pred})
-        t_wgrad = ctx.profile_wgrad(B, reps=3)  # slicing-independent constant of the step model
+        # slicing-independent constant of the step model (the stage buffers hold at most max_batch
+        # sequences; a 1F1B batch beyond that is modelled as proportionally more dW)
+        wb = min(B, mb)
+        t_wgrad = ctx.profile_wgrad(wb, reps=3) * B // wb
         t1 = time.time()
         dp = tp.plan_joint(tables, g, cfg.n_layer, cfg.hidden, cfg.seq_len, K, B, eps_ticks=0)
         t_plan += time.time() - t1

@@ -326,13 +326,21 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
         uint32_t pk[64];
         const float nm = -m_ref;
         if (j > 0) {
+          // software-pipelined TMEM loads: chunk ch + 1 is in flight while chunk ch is exponentiated
+          // (one load latency per block instead of four)
+          uint32_t ra[32], rb[32];
+          tmem_ld32_nowait(lane_base + s_col, ra);
+          tmem_wait_ld();
 #pragma unroll
-          for (int ch = 0; ch < AT / 32; ++ch) {
-            uint32_t r[32];
-            tmem_ld32_nowait(lane_base + s_col + ch * 32, r);
+          for (int ch = 0; ch < AT / 32; ch += 2) {
+            tmem_ld32_nowait(lane_base + s_col + (ch + 1) * 32, rb);
+            if (diag) exp_max_chunk<true>(ra, ch * 32, nvis, scale_log2, nm, rs4, m4, pk, ch * 16);
+            else exp_max_chunk<false>(ra, ch * 32, nvis, scale_log2, nm, rs4, m4, pk, ch * 16);
             tmem_wait_ld();
-            if (diag) exp_max_chunk<true>(r, ch * 32, nvis, scale_log2, nm, rs4, m4, pk, ch * 16);
-            else exp_max_chunk<false>(r, ch * 32, nvis, scale_log2, nm, rs4, m4, pk, ch * 16);
+            if (ch + 2 < AT / 32) tmem_ld32_nowait(lane_base + s_col + (ch + 2) * 32, ra);
+            if (diag) exp_max_chunk<true>(rb, (ch + 1) * 32, nvis, scale_log2, nm, rs4, m4, pk, (ch + 1) * 16);
+            else exp_max_chunk<false>(rb, (ch + 1) * 32, nvis, scale_log2, nm, rs4, m4, pk, (ch + 1) * 16);
+            if (ch + 2 < AT / 32) tmem_wait_ld();
           }
         } else {
           // first block: only the max (m_ref = -inf would make every P infinite)
@@ -563,13 +571,19 @@ __global__ void __launch_bounds__(F1_THREADS, 1)
       uint32_t pk[64];
       const float nm = -m_ref;
       if (j > 0) {
+        uint32_t ra[32], rb[32];  // software-pipelined TMEM loads (see the two-tile kernel)
+        tmem_ld32_nowait(lane_base + s_col, ra);
+        tmem_wait_ld();
 #pragma unroll
-        for (int ch = 0; ch < AT / 32; ++ch) {
-          uint32_t r[32];
-          tmem_ld32_nowait(lane_base + s_col + ch * 32, r);
+        for (int ch = 0; ch < AT / 32; ch += 2) {
+          tmem_ld32_nowait(lane_base + s_col + (ch + 1) * 32, rb);
+          if (diag) exp_max_chunk<true>(ra, ch * 32, nvis, scale_log2, nm, rs4, m4, pk, ch * 16);
+          else exp_max_chunk<false>(ra, ch * 32, nvis, scale_log2, nm, rs4, m4, pk, ch * 16);
           tmem_wait_ld();
-          if (diag) exp_max_chunk<true>(r, ch * 32, nvis, scale_log2, nm, rs4, m4, pk, ch * 16);
-          else exp_max_chunk<false>(r, ch * 32, nvis, scale_log2, nm, rs4, m4, pk, ch * 16);
+          if (ch + 2 < AT / 32) tmem_ld32_nowait(lane_base + s_col + (ch + 2) * 32, ra);
+          if (diag) exp_max_chunk<true>(rb, (ch + 1) * 32, nvis, scale_log2, nm, rs4, m4, pk, (ch + 1) * 16);
+          else exp_max_chunk<false>(rb, (ch + 1) * 32, nvis, scale_log2, nm, rs4, m4, pk, (ch + 1) * 16);
+          if (ch + 2 < AT / 32) tmem_wait_ld();
         }
       } else {
 #pragma unroll
@@ -929,10 +943,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       const int vis0 = kabs - c - qrow0 - half * HQ;  // first visible column of this key row, in this half
       // phase 1 (needs S^T only): P^T = exp2(S^T scale - lse) -> registers and, packed, into TMEM
       float pv[HQ];
+      // this half's 32 S^T columns in one TMEM load (one load latency per tile, not two)
+      uint32_t rs32[32];
+      tmem_ld32_nowait(lane_base + bb * 128 + half * HQ, rs32);
 #pragma unroll
       for (int ch = 0; ch < 2; ++ch) {  // 16 query columns at a time
-        uint32_t rs[16];
-        tmem_ld16_nowait(lane_base + bb * 128 + half * HQ + ch * 16, rs);
+        const uint32_t* rs = rs32 + ch * 16;
         const float4* L4 = reinterpret_cast<const float4*>(Ls + half * HQ + ch * 16);
         float Lv[16];
 #pragma unroll
@@ -940,7 +956,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           const float4 a4 = L4[u];
           Lv[4 * u] = a4.x; Lv[4 * u + 1] = a4.y; Lv[4 * u + 2] = a4.z; Lv[4 * u + 3] = a4.w;
         }
-        tmem_wait_ld();
+        if (ch == 0) tmem_wait_ld();
         uint32_t pk[8];
 #pragma unroll
         for (int t = 0; t < 16; t += 2) {
@@ -963,9 +979,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       tc_fence_after();
       uint8_t* dSt = sm + BwdSmem::DS + bb * PT;
 #pragma unroll
+      uint32_t rp32[32];  // this half's 32 dP^T columns in one TMEM load
+      tmem_ld32_nowait(lane_base + bb * 128 + 64 + half * HQ, rp32);
+#pragma unroll
       for (int ch = 0; ch < 2; ++ch) {
-        uint32_t rp[16];
-        tmem_ld16_nowait(lane_base + bb * 128 + 64 + half * HQ + ch * 16, rp);
+        const uint32_t* rp = rp32 + ch * 16;
         const float4* D4 = reinterpret_cast<const float4*>(Ds + half * HQ + ch * 16);
         float Dv[16];
 #pragma unroll
@@ -973,7 +991,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           const float4 d4 = D4[u];
           Dv[4 * u] = d4.x; Dv[4 * u + 1] = d4.y; Dv[4 * u + 2] = d4.z; Dv[4 * u + 3] = d4.w;
         }
-        tmem_wait_ld();
+        if (ch == 0) tmem_wait_ld();
         uint32_t dk[8];
 #pragma unroll
         for (int t = 0; t < 16; t += 2) {
