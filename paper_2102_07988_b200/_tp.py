@@ -11,7 +11,8 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtp.so")
+# TP_LIB: an alternative build of the same library (A/B of kernel variants across two builds)
+LIB_PATH = os.environ.get("TP_LIB") or os.path.join(_HERE, "libtp.so")
 
 TP_OK, TP_EINVAL, TP_EINFEASIBLE, TP_ETOOBIG, TP_ECUDA, TP_ENCCL, TP_ENOMEM, TP_ESTATE = 0, -1, -2, -3, -4, -5, -6, -7
 TP_BF16, TP_FP32 = 0, 1

@@ -143,6 +143,9 @@ __device__ __forceinline__ void epi_tile(const Epi& epi, const SplitK& sk, float
       qoff[it] = (int64_t)sq * epi.s_len * epi.hidden + (int64_t)pos * epi.head_dim;
     }
   }
+  // TMEM loads run one chunk ahead: chunk ch + 1 is loaded while chunk ch's rows are processed
+  uint32_t r[32];
+  tmem_ld32_async(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch0 * 32, r);
 #pragma unroll 1
   for (int ch = ch0; ch < ch1; ++ch) {
     const int n = n0 + ch * 32 + (lane & 3) * 8;
@@ -171,12 +174,10 @@ __device__ __forceinline__ void epi_tile(const Epi& epi, const SplitK& sk, float
     }
     // the tile's 32 x 32 chunk lands in the warp's padded smem scratch from TMEM; a finisher adds the
     // earlier units' partials of the same rows / columns
-    {
-      uint32_t r[32];
-      tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 32, r);
+    tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) scr[lane * 33 + i] = __uint_as_float(r[i]);
-    }
+    for (int i = 0; i < 32; ++i) scr[lane * 33 + i] = __uint_as_float(r[i]);
+    if (ch + 1 < ch1) tmem_ld32_async(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + (ch + 1) * 32, r);
     __syncwarp();
     if (mode == 2) {
 #pragma unroll 1
