@@ -14,6 +14,15 @@
  * Backward: dO[l][a*d]; writes dq[l][a*d] (bf16, ld = ldq) and adds (accumulate=1) or writes
  * (accumulate=0) dK/dV of key rows [0, c+l) into dk_acc/dv_acc[a][s][d] fp32.
  *   impl: 0 = tensor-core kernel, 1 = SIMT kernel.
+ *
+ * tpk_layernorm_fwd / _bwd: the pre-LN LayerNorm of the block ("LayerNorm";
+ * DESIGN.md reading A-3: fp32 statistics, eps = 1e-5) over `rows` rows of H (H % 8 == 0,
+ * H <= 12288) fp32 values, all buffers row-major with ld = H, device pointers 16-byte aligned.
+ * Forward: y = (x - mean) * rstd * gamma + beta as bf16, mean[r] / rstd[r] fp32.
+ * Backward (dy bf16, mean / rstd from the forward): dx_out = resid + dLN/dx (fp32; resid may be
+ * NULL = 0), dx_copy (bf16, may be NULL) = the same values; dgamma, dbeta and (if non-NULL) dbias
+ * = column sums of dx_out are ADDED to the caller's fp32 [H] accumulators. `impl` is ignored
+ * (one CUDA implementation, chosen by H; TP_LN_BULK=0 selects the register-prefetch variant).
  */
 #ifndef TP_KERNELS_H_
 #define TP_KERNELS_H_
@@ -35,6 +44,13 @@ tp_status tpk_attention_bwd(const void* dO, const void* o, const void* q, const 
                             const float* lse, void* dq, int64_t ldq, float* dk_acc, float* dv_acc, int32_t a,
                             int32_t s, int32_t d, int32_t c, int32_t l, int32_t accumulate, int32_t impl,
                             void* stream);
+
+tp_status tpk_layernorm_fwd(const float* x, const float* gamma, const float* beta, void* y, float* mean,
+                            float* rstd, int32_t rows, int32_t H, void* stream);
+
+tp_status tpk_layernorm_bwd(const void* dy, const float* x, const float* mean, const float* rstd, const float* gamma,
+                            const float* resid, float* dx_out, void* dx_copy, float* dgamma, float* dbeta,
+                            float* dbias, int32_t rows, int32_t H, void* stream);
 
 #ifdef __cplusplus
 }

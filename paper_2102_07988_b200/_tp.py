@@ -24,7 +24,7 @@ EXPORTED = ["tp_plan", "tp_plan_joint", "tp_schedule_oplist", "tp_stage_layers",
             "tp_load_params", "tp_step", "tp_step_device", "tp_get_grads", "tp_get_logits",
             "tp_profile", "tp_profile_wgrad", "tp_profile_comm", "tp_get_stream", "tp_kernel_stats", "tp_kernel_stats_reset", "tp_kernel_stats_enable",
             "tp_last_step_launches", "tp_destroy", "tp_last_error"]
-KEXPORTED = ["tpk_gemm", "tpk_attention_fwd", "tpk_attention_bwd"]
+KEXPORTED = ["tpk_gemm", "tpk_attention_fwd", "tpk_attention_bwd", "tpk_layernorm_fwd", "tpk_layernorm_bwd"]
 
 
 class TpError(RuntimeError):
@@ -97,6 +97,8 @@ def _load() -> C.CDLL:
                                         C.c_int32, P]),
         "tpk_attention_bwd": (C.c_int, [P, P, P, P, P, P, P, C.c_int64, P, P, C.c_int32, C.c_int32, C.c_int32,
                                         C.c_int32, C.c_int32, C.c_int32, C.c_int32, P]),
+        "tpk_layernorm_fwd": (C.c_int, [P, P, P, P, P, P, C.c_int32, C.c_int32, P]),
+        "tpk_layernorm_bwd": (C.c_int, [P, P, P, P, P, P, P, P, P, P, P, C.c_int32, C.c_int32, P]),
         "tp_last_error": (C.c_char_p, []),
     }
     for name, (res, args) in sigs.items():
@@ -385,4 +387,13 @@ def k_attention_fwd(q, k, v, o, lse, a, s, d, c, l, impl=0, stream=0):
 
 def k_attention_bwd(dO, o, q, k, v, lse, dq, ldq, dk_acc, dv_acc, a, s, d, c, l, accumulate, impl=0, stream=0):
     _check(_lib.tpk_attention_bwd(dO, o, q, k, v, lse, dq, ldq, dk_acc, dv_acc, a, s, d, c, l, accumulate, impl,
+                                  stream))
+
+
+def k_layernorm_fwd(x, gamma, beta, y, mean, rstd, rows, H, stream=0):
+    _check(_lib.tpk_layernorm_fwd(x, gamma, beta, y, mean, rstd, rows, H, stream))
+
+
+def k_layernorm_bwd(dy, x, mean, rstd, gamma, resid, dx_out, dx_copy, dgamma, dbeta, dbias, rows, H, stream=0):
+    _check(_lib.tpk_layernorm_bwd(dy, x, mean, rstd, gamma, resid, dx_out, dx_copy, dgamma, dbeta, dbias, rows, H,
                                   stream))

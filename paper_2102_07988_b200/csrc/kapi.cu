@@ -94,3 +94,22 @@ extern "C" tp_status tpk_attention_bwd(const void* dO, const void* o, const void
            "attn_bwd_simt");
   return r;
 }
+
+extern "C" tp_status tpk_layernorm_fwd(const float* x, const float* gamma, const float* beta, void* y, float* mean,
+                                       float* rstd, int32_t rows, int32_t H, void* stream) {
+  TP_CHECK_ARG(x && gamma && beta && y && mean && rstd, "tpk_layernorm_fwd: null pointer");
+  TP_CHECK_ARG(rows >= 0 && H >= 8 && H % 8 == 0 && H <= 12288, "tpk_layernorm_fwd: bad shape");
+  return cu(layernorm_fwd<bf16>(x, gamma, beta, (bf16*)y, mean, rstd, rows, H, reinterpret_cast<cudaStream_t>(stream)),
+            "layernorm_fwd");
+}
+
+extern "C" tp_status tpk_layernorm_bwd(const void* dy, const float* x, const float* mean, const float* rstd,
+                                       const float* gamma, const float* resid, float* dx_out, void* dx_copy,
+                                       float* dgamma, float* dbeta, float* dbias, int32_t rows, int32_t H,
+                                       void* stream) {
+  TP_CHECK_ARG(dy && x && mean && rstd && gamma && dx_out && dgamma && dbeta, "tpk_layernorm_bwd: null pointer");
+  TP_CHECK_ARG(rows >= 0 && H >= 8 && H % 8 == 0 && H <= 12288, "tpk_layernorm_bwd: bad shape");
+  return cu(layernorm_bwd<bf16>((const bf16*)dy, x, mean, rstd, gamma, resid, dx_out, (bf16*)dx_copy, dgamma, dbeta,
+                                nullptr, rows, H, reinterpret_cast<cudaStream_t>(stream), dbias),
+            "layernorm_bwd");
+}

@@ -5,6 +5,7 @@
 #include <algorithm>
 
 #include "kernels.h"
+#include "tc5.cuh"
 
 namespace tp {
 
@@ -320,6 +321,189 @@ __global__ void __launch_bounds__(NT, 1) ln_bwd_wide_kernel(const T* __restrict_
   }
 }
 
+// ---- bulk-staged variants (H <= 2048): rows move HBM -> shared memory by cp.async.bulk into a
+// ring of stages completing on mbarriers (thread 0 issues them), so each SM keeps ~160-190 KB of
+// loads in flight (the register-prefetch kernels above: 40-128 KB, with a warp's / CTA's loads
+// stalled behind its own reductions and stores). One CTA of 256 threads (8 columns each) per group
+// of `rpb` consecutive rows; the block reduction's barrier doubles as the "stage consumed" signal,
+// after which thread 0 refills the stage with the row LN*_STAGES ahead.
+// Forward: 4 stages of one row (4H bytes); 48 registers -> 5 CTAs per SM.
+constexpr int LNF_STAGES = 4;
+template <typename T>
+__global__ void __launch_bounds__(256) ln_fwd_bulk_kernel(const float* __restrict__ x, const float* __restrict__ gam,
+                                                          const float* __restrict__ bet, T* __restrict__ y,
+                                                          float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                                                          int rows, int H, int rpb) {
+  extern __shared__ __align__(128) float lnf_ring[];  // [LNF_STAGES][H]
+  __shared__ __align__(8) uint64_t full[LNF_STAGES];
+  __shared__ float red[2][2][8];
+  const int tid = threadIdx.x, col = tid * 8;
+  const bool act = col < H;
+  const uint32_t bytes = (uint32_t)H * 4u;
+  const int r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
+  if (tid == 0) {
+#pragma unroll
+    for (int d = 0; d < LNF_STAGES; ++d) tc5::mbar_init(&full[d], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int d = 0; d < LNF_STAGES && r0 + d < r1; ++d) {
+      tc5::mbar_expect_tx(&full[d], bytes);
+      tc5::bulk_load(lnf_ring + d * H, x + (int64_t)(r0 + d) * H, bytes, &full[d]);
+    }
+  }
+  float g[8], b[8];
+  if (act) { load8<float>(gam + col, g); load8<float>(bet + col, b); }
+  __syncthreads();  // barrier initialisation visible to every waiter
+  for (int i = 0, r = r0; r < r1; ++i, ++r) {
+    const int d = i % LNF_STAGES;
+    tc5::mbar_wait(&full[d], (uint32_t)(i / LNF_STAGES) & 1u);
+    float v[8];
+    if (act) load8<float>(lnf_ring + d * H + col, v);
+    else
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = 0.f;
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += v[k];
+    float (*rd)[8] = red[i & 1];
+    s = warp_sum(s);
+    if ((tid & 31) == 0) rd[0][tid >> 5] = s;
+    __syncthreads();  // also: every thread has read stage d
+    if (tid == 0 && r + LNF_STAGES < r1) {
+      tc5::mbar_expect_tx(&full[d], bytes);
+      tc5::bulk_load(lnf_ring + d * H, x + (int64_t)(r + LNF_STAGES) * H, bytes, &full[d]);
+    }
+    float m = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) m += rd[0][w];
+    const float mean = m / H;
+    float q = 0.f;
+    if (act)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) { const float dd = v[k] - mean; q += dd * dd; }
+    q = warp_sum(q);
+    if ((tid & 31) == 0) rd[1][tid >> 5] = q;
+    __syncthreads();
+    float qq = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) qq += rd[1][w];
+    const float rstd = rsqrtf(qq / H + 1e-5f);
+    if (tid == 0) { mean_out[r] = mean; rstd_out[r] = rstd; }
+    if (act) {
+      float o[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o[k] = (v[k] - mean) * rstd * g[k] + b[k];
+      store8<T>(y + (int64_t)r * H + col, o);
+    }
+  }
+}
+
+// Backward: the CTA-per-row-group structure of ln_bwd_kernel (256 threads x 8 columns, dgamma /
+// dbeta / dbias partials in registers), with the row's x, resid and dy staged through a ring of
+// LNB_STAGES shared-memory stages by thread 0. The per-row block reduction's barrier doubles as the
+// "stage consumed" signal: after it, thread 0 refills the stage with row r + LNB_STAGES. The
+// group's mean / rstd are read into shared memory 128 rows at a time.
+constexpr int LNB_STAGES = 4;
+template <typename T>
+__global__ void __launch_bounds__(256, 2) ln_bwd_bulk_kernel(const T* __restrict__ dy, const float* __restrict__ x,
+                                                             const float* __restrict__ mean_in,
+                                                             const float* __restrict__ rstd_in,
+                                                             const float* __restrict__ gam, const float* __restrict__ resid,
+                                                             float* __restrict__ dx_out, T* __restrict__ dx_copy,
+                                                             float* __restrict__ dgam, float* __restrict__ dbet,
+                                                             float* __restrict__ dbias, int rows, int H, int rpb) {
+  extern __shared__ __align__(128) uint8_t lnb_ring[];  // [LNB_STAGES][x: 4H | resid: 4H | dy: H*sizeof(T)]
+  __shared__ __align__(8) uint64_t full[LNB_STAGES];
+  __shared__ float red[2][2][8];
+  __shared__ float st[2][128];
+  const int tid = threadIdx.x, col = tid * 8;
+  const bool act = col < H;
+  const size_t stage_bytes = (size_t)H * (8 + sizeof(T));
+  const uint32_t row_bytes = (uint32_t)H * (resid ? 8u : 4u) + (uint32_t)(H * sizeof(T));
+  const int r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
+  auto issue = [&](int r, int d) {
+    uint8_t* sb = lnb_ring + d * stage_bytes;
+    tc5::mbar_expect_tx(&full[d], row_bytes);
+    tc5::bulk_load(sb, x + (int64_t)r * H, H * 4u, &full[d]);
+    if (resid) tc5::bulk_load(sb + H * 4, resid + (int64_t)r * H, H * 4u, &full[d]);
+    tc5::bulk_load(sb + H * 8, dy + (int64_t)r * H, (uint32_t)(H * sizeof(T)), &full[d]);
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int d = 0; d < LNB_STAGES; ++d) tc5::mbar_init(&full[d], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int d = 0; d < LNB_STAGES && r0 + d < r1; ++d) issue(r0 + d, d);
+  }
+  float g[8], pg[8], pb[8], pd[8];
+  if (act) load8<float>(gam + col, g);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { pg[i] = 0.f; pb[i] = 0.f; pd[i] = 0.f; if (!act) g[i] = 0.f; }
+  for (int i = 0, r = r0; r < r1; ++i, ++r) {
+    if ((i & 127) == 0) {  // stats of the next (up to) 128 rows of the group
+      __syncthreads();     // previous chunk's readers are done (first pass: barrier init visible)
+      if (tid < 128) { if (r + tid < r1) st[0][tid] = mean_in[r + tid]; }
+      else if (r + tid - 128 < r1) st[1][tid - 128] = rstd_in[r + tid - 128];
+      __syncthreads();
+    }
+    const float mean = st[0][i & 127], rstd = st[1][i & 127];
+    const int d = i % LNB_STAGES;
+    tc5::mbar_wait(&full[d], (uint32_t)(i / LNB_STAGES) & 1u);
+    const uint8_t* sb = lnb_ring + d * stage_bytes;
+    float dv[8], xh[8], rs[8];
+    if (act) {
+      load8<float>(reinterpret_cast<const float*>(sb) + col, xh);
+      load8<T>(reinterpret_cast<const T*>(sb + H * 8) + col, dv);
+      if (resid) load8<float>(reinterpret_cast<const float*>(sb + H * 4) + col, rs);
+      else
+#pragma unroll
+        for (int k = 0; k < 8; ++k) rs[k] = 0.f;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) { dv[k] = 0.f; xh[k] = 0.f; rs[k] = 0.f; }
+    }
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      xh[k] = (xh[k] - mean) * rstd;
+      const float dxh = dv[k] * g[k];
+      s1 += dxh;
+      s2 += dxh * xh[k];
+      pg[k] += dv[k] * xh[k];
+      pb[k] += dv[k];
+    }
+    float (*rd)[8] = red[i & 1];
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if ((tid & 31) == 0) { rd[0][tid >> 5] = s1; rd[1][tid >> 5] = s2; }
+    __syncthreads();  // also: every thread has read stage d
+    if (tid == 0 && r + LNB_STAGES < r1) issue(r + LNB_STAGES, d);
+    float m1 = 0.f, m2 = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) { m1 += rd[0][w]; m2 += rd[1][w]; }
+    m1 /= H;
+    m2 /= H;
+    if (act) {
+      float o[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        o[k] = rstd * (dv[k] * g[k] - m1 - xh[k] * m2) + rs[k];
+        pd[k] += o[k];
+      }
+      store8<float>(dx_out + (int64_t)r * H + col, o);
+      if (dx_copy) store8<T>(dx_copy + (int64_t)r * H + col, o);
+    }
+  }
+  if (act) {
+    red_add4(dgam + col, pg[0], pg[1], pg[2], pg[3]);
+    red_add4(dgam + col + 4, pg[4], pg[5], pg[6], pg[7]);
+    red_add4(dbet + col, pb[0], pb[1], pb[2], pb[3]);
+    red_add4(dbet + col + 4, pb[4], pb[5], pb[6], pb[7]);
+    if (dbias) {
+      red_add4(dbias + col, pd[0], pd[1], pd[2], pd[3]);
+      red_add4(dbias + col + 4, pd[4], pd[5], pd[6], pd[7]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- embedding
 __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const float* __restrict__ wte,
                                  const float* __restrict__ wpe, float* __restrict__ h, int c, int b, int s, int H,
@@ -520,13 +704,29 @@ __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ src, 
   }
 }
 
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+// TP_LN_BULK=0 selects the register-prefetch LayerNorm kernels (A/B knob)
+bool ln_bulk_enabled() {
+  static const bool on = !(getenv("TP_LN_BULK") && atoi(getenv("TP_LN_BULK")) == 0);
+  return on;
+}
+
 }  // namespace
 
 template <typename T>
 cudaError_t layernorm_fwd(const float* x, const float* gam, const float* bet, T* y, float* mean, float* rstd,
                           int rows, int H, cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
-  if (H <= 2048) ln_fwd_warp_kernel<T, 8><<<(rows + 7) / 8, 256, 0, st>>>(x, gam, bet, y, mean, rstd, rows, H);
+  if (H <= 2048 && ln_bulk_enabled() && aligned16(x) && aligned16(y)) {
+    const int smem = LNF_STAGES * H * (int)sizeof(float);
+    static int per_sm = 0;  // resident CTAs per SM at H = 2048 (the row groups form one wave)
+    if (!per_sm && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ln_fwd_bulk_kernel<T>, 256,
+                                                                 LNF_STAGES * 2048 * (int)sizeof(float)) != cudaSuccess)
+      per_sm = 4;
+    const int nsm = std::max(1, num_sms()) * std::max(1, per_sm);
+    const int rpb = std::max(4, (rows + nsm - 1) / nsm);
+    ln_fwd_bulk_kernel<T><<<(rows + rpb - 1) / rpb, 256, smem, st>>>(x, gam, bet, y, mean, rstd, rows, H, rpb);
+  } else if (H <= 2048) ln_fwd_warp_kernel<T, 8><<<(rows + 7) / 8, 256, 0, st>>>(x, gam, bet, y, mean, rstd, rows, H);
   else if (H <= 4096) ln_fwd_kernel<T, 256, 2><<<rows, 256, 0, st>>>(x, gam, bet, y, mean, rstd, H);
   else if (H <= 6144) ln_fwd_kernel<T, 256, 3><<<rows, 256, 0, st>>>(x, gam, bet, y, mean, rstd, H);
   else if (H <= 12288) ln_fwd_kernel<T, 512, 3><<<rows, 512, 0, st>>>(x, gam, bet, y, mean, rstd, H);
@@ -562,7 +762,20 @@ cudaError_t layernorm_bwd(const T* dy, const float* x, const float* mean, const 
     ln_bwd_wide_kernel<T, NT, NCH><<<grid, NT, smem, st>>>(dy, x, mean, rstd, gam, resid, dx_out, dx_copy, \
                                                           dgam, dbet, dbias, rows, H, rpb);               \
   } while (0)
-  if (H <= 2048) LNB(256, 1);
+  if (H <= 2048 && ln_bulk_enabled() && aligned16(x) && aligned16(dy) && aligned16(resid)) {
+    const int smem = LNB_STAGES * H * (8 + (int)sizeof(T));
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(ln_bwd_bulk_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           LNB_STAGES * 2048 * (8 + (int)sizeof(T)));
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    const int nsm = std::max(1, num_sms());
+    const int rpb2 = std::max(4, (rows + 2 * nsm - 1) / (2 * nsm));
+    ln_bwd_bulk_kernel<T><<<(rows + rpb2 - 1) / rpb2, 256, smem, st>>>(dy, x, mean, rstd, gam, resid, dx_out, dx_copy,
+                                                                       dgam, dbet, dbias, rows, H, rpb2);
+  } else if (H <= 2048) LNB(256, 1);
   else if (H <= 4096) LNBW(512, 1);
   else if (H <= 6144) LNBW(768, 1);
   else if (H <= 12288) LNBW(768, 2);

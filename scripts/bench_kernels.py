@@ -64,6 +64,41 @@ def attn(a, s, d, c, l, impl=0, tag=""):
           flush=True)
 
 
+def layernorm(rows, H, tag=""):
+    """LayerNorm fwd / bwd (the bench's resid + dx_copy form) at algorithmic bytes: fwd 4H in + 2H out,
+    bwd 2H (dy) + 4H (x) + 4H (resid) in, 4H + 2H out, per row. NB buffer sets rotate so the
+    working set (> 2x the 126 MB L2) is not cache-resident between launches."""
+    NB = 3
+    xs = [torch.randn(rows, H, device="cuda") for _ in range(NB)]
+    ys = [torch.empty(rows, H, device="cuda", dtype=torch.bfloat16) for _ in range(NB)]
+    dys = [torch.randn(rows, H, device="cuda").to(torch.bfloat16) for _ in range(NB)]
+    rs = [torch.randn(rows, H, device="cuda") for _ in range(NB)]
+    dxs = [torch.empty(rows, H, device="cuda") for _ in range(NB)]
+    dcs = [torch.empty(rows, H, device="cuda", dtype=torch.bfloat16) for _ in range(NB)]
+    gam, bet = torch.ones(H, device="cuda"), torch.zeros(H, device="cuda")
+    mean, rstd = torch.empty(rows, device="cuda"), torch.empty(rows, device="cuda")
+    dg, db, dbias = (torch.zeros(H, device="cuda") for _ in range(3))
+    it = [0]
+
+    def f():
+        i = it[0] % NB
+        it[0] += 1
+        tp.k_layernorm_fwd(xs[i].data_ptr(), gam.data_ptr(), bet.data_ptr(), ys[i].data_ptr(), mean.data_ptr(),
+                           rstd.data_ptr(), rows, H)
+
+    def b():
+        i = it[0] % NB
+        it[0] += 1
+        tp.k_layernorm_bwd(dys[i].data_ptr(), xs[i].data_ptr(), mean.data_ptr(), rstd.data_ptr(), gam.data_ptr(),
+                           rs[i].data_ptr(), dxs[i].data_ptr(), dcs[i].data_ptr(), dg.data_ptr(), db.data_ptr(),
+                           dbias.data_ptr(), rows, H)
+    msf, msb = time_it(f), time_it(b)
+    bf, bb = 6.0 * H * rows, 16.0 * H * rows
+    print(json.dumps({"kernel": "layernorm", "tag": tag, "rows": rows, "H": H, "bulk": os.environ.get("TP_LN_BULK", "1"),
+                      "fwd_us": msf * 1e3, "fwd_gbs": bf / msf / 1e6, "bwd_us": msb * 1e3, "bwd_gbs": bb / msb / 1e6}),
+          flush=True)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", default="all")
@@ -93,3 +128,7 @@ if __name__ == "__main__":
         for (a, s, d, c, l, tag) in [(16, 2048, 128, 0, 2048, "1b full"), (40, 2048, 128, 1536, 512, "13b last slice"),
                                      (40, 2048, 128, 0, 512, "13b first slice"), (40, 8192, 128, 7680, 512, "13b-8k last")]:
             attn(a, s, d, c, l, 0, tag)
+    if args.which in ("all", "ln"):
+        for (rows, H, tag) in [(16384, 2048, "1b b=8 l=2048"), (4608, 2048, "1b b=8 l=576"),
+                               (11776, 2048, "1b b=8 l=1472"), (4096, 5120, "13b b=8 l=512")]:
+            layernorm(rows, H, tag)

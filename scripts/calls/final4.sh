@@ -7,3 +7,8 @@ timeout 600 $TR --nproc-per-node 2 bench.py --gpus 2 > gpurun_out/final4/bench_n
 timeout 600 $TR --nproc-per-node 4 bench.py --gpus 4 > gpurun_out/final4/bench_n4.json 2> gpurun_out/final4/bench_n4.err
 timeout 1200 $TR --nproc-per-node 4 bench.py --gpus 4 --config gpt3-13b --steps 3 --warmup 2 --no-cpu-baseline \
   > gpurun_out/final4/pipe_13b_n4.json 2> gpurun_out/final4/pipe_13b_n4.err
+# 1F1B bounds the stage buffers: B = 32 in buffers sized for 8 sequences (vs GPipe store-all)
+timeout 900 $TR --nproc-per-node 4 bench.py --gpus 4 --batch 32 --batch-slices 1,2 --no-gpipe --no-cpu-baseline --steps 3 \
+  > gpurun_out/final4/gpipe_b32.json 2> gpurun_out/final4/gpipe_b32.err
+TP_SCHEDULE=1f1b timeout 900 $TR --nproc-per-node 4 bench.py --gpus 4 --batch 32 --max-batch 8 --batch-slices 1,2 --no-gpipe \
+  --no-cpu-baseline --steps 3 > gpurun_out/final4/1f1b_b32_mb8.json 2> gpurun_out/final4/1f1b_b32_mb8.err

@@ -145,3 +145,45 @@ def test_attention_fwd_bwd(a, s, d, c, l, impl):
                        a, s, d, c, l, 0, impl)
     torch.cuda.synchronize()
     assert rel(dk[:, :c + l], dK) < 2e-2 and rel(dv[:, :c + l], dV) < 2e-2
+
+
+@pytest.mark.parametrize("rows,H", [(1, 8), (7, 136), (300, 2048), (4099, 2048), (16384, 2048), (33, 1000),
+                                    (513, 5120), (64, 12288)])
+@pytest.mark.parametrize("with_resid", [False, True])
+def test_layernorm_fwd_bwd(rows, H, with_resid):
+    """LayerNorm fwd / bwd kernels (bulk-staged for H <= 2048, register kernels above) against the
+    fp64 definition (reading A-3) on the same fp32 x and bf16 dy: ragged row counts (partial last
+    CTA, rows < warps of one CTA), H not a multiple of 256 (masked lanes), the 1B / 13B / 175B widths."""
+    g = torch.Generator(device="cpu").manual_seed(rows * 31 + H)
+    x = (torch.randn(rows, H, generator=g) * 2 + 0.5).to(dev)
+    gam = (1 + 0.1 * torch.randn(H, generator=g)).to(dev)
+    bet = (0.1 * torch.randn(H, generator=g)).to(dev)
+    dy = torch.randn(rows, H, generator=g).to(dev, torch.bfloat16)
+    resid = torch.randn(rows, H, generator=g).to(dev) if with_resid else None
+    y = torch.empty(rows, H, device=dev, dtype=torch.bfloat16)
+    mean = torch.empty(rows, device=dev)
+    rstd = torch.empty(rows, device=dev)
+    tp.k_layernorm_fwd(ptr(x), ptr(gam), ptr(bet), ptr(y), ptr(mean), ptr(rstd), rows, H)
+    dx = torch.empty(rows, H, device=dev)
+    dxc = torch.empty(rows, H, device=dev, dtype=torch.bfloat16)
+    dg = torch.zeros(H, device=dev); db = torch.zeros(H, device=dev); dbias = torch.full((H,), 0.25, device=dev)
+    tp.k_layernorm_bwd(ptr(dy), ptr(x), ptr(mean), ptr(rstd), ptr(gam), ptr(resid) if with_resid else None, ptr(dx),
+                       ptr(dxc), ptr(dg), ptr(db), ptr(dbias), rows, H)
+    torch.cuda.synchronize()
+    xd = x.double().cpu().requires_grad_(True)
+    mu = xd.mean(1, keepdim=True)
+    var = ((xd - mu) ** 2).mean(1, keepdim=True)
+    xhat = (xd - mu) / torch.sqrt(var + 1e-5)
+    yd = xhat * gam.double().cpu() + bet.double().cpu()
+    (gx,) = torch.autograd.grad(yd, xd, dy.double().cpu())
+    if with_resid:
+        gx = gx + resid.double().cpu()
+    assert rel(mean.cpu(), mu[:, 0].detach()) < 1e-6
+    assert rel(rstd.cpu(), (1 / torch.sqrt(var + 1e-5))[:, 0].detach()) < 1e-5
+    assert rel(y.cpu(), yd.detach()) < 5e-3
+    assert (y.cpu().double() - yd.detach()).abs().max() < 1e-2 * (1 + yd.detach().abs().max())
+    assert rel(dx.cpu(), gx) < 1e-5
+    assert rel(dxc.cpu(), gx) < 5e-3
+    assert rel(dg.cpu(), (dy.double().cpu() * xhat.detach()).sum(0)) < 1e-4
+    assert rel(db.cpu(), dy.double().cpu().sum(0)) < 1e-4
+    assert rel(dbias.cpu() - 0.25, gx.sum(0)) < 1e-4
