@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     attn_fwd2_sm100_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                            const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ o, int64_t ldo,
                            float* __restrict__ lse, int s, int c, int l, float scale_log2, int64_t o_sstride,
-                           int64_t lse_sstride, long long* trace) {
+                           int64_t lse_sstride, long long* trace, int inorder) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (tc5::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Fwd2Smem::BAR);
@@ -294,9 +294,11 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
         if (j + 1 < nkb[t]) {
           if (!k_waited) { mbar_wait(kfull + (j + 1) % NKS, ((j + 1) / NKS) & 1); k_waited = true; }
           if (lane == 0) TRF(1, 0, j + 1);
-          // S_t's columns hold P_t, read by O_t += P_t V_j just issued; S_{j+1} overwrites them only
-          // after that MMA has completed (measured: the wait is off the critical path)
-          mbar_wait(ofull + t, j & 1);
+          // S_t's columns hold P_t, read by O_t += P_t V_j just issued. tcgen05.mma instructions of
+          // one thread execute in issue order, so S_{j+1} (issued after it) cannot overwrite P_t
+          // before that MMA has read it: no completion wait, the MMA warp goes straight on to the
+          // other tile (inorder = 0, TP_ATTN_INORDER=0: wait for O_t += P_t V_j to complete first)
+          if (!inorder) mbar_wait(ofull + t, j & 1);
           issue_s(t, j + 1);
         }
       }
@@ -464,7 +466,7 @@ __global__ void __launch_bounds__(F1_THREADS, 1)
     attn_fwd1_sm100_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                            const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ o, int64_t ldo,
                            float* __restrict__ lse, int s, int c, int l, float scale_log2, int64_t o_sstride,
-                           int64_t lse_sstride) {
+                           int64_t lse_sstride, int inorder) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (tc5::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Fwd1Smem::BAR);
@@ -538,8 +540,9 @@ __global__ void __launch_bounds__(F1_THREADS, 1)
       const int b = j & 1;
       if (j + 1 < nkb) {
         mbar_wait(kfull + (j + 1) % NKS, ((j + 1) / NKS) & 1);
-        // buffer (j + 1) & 1 held P_{j-1}: O += P_{j-1} V_{j-1} must have read it
-        if (j >= 1) mbar_wait(ofull + ((j - 1) & 1), ((j - 1) >> 1) & 1);
+        // buffer (j + 1) & 1 held P_{j-1}: O += P_{j-1} V_{j-1}, issued earlier, reads it first
+        // (in-order tcgen05.mma execution; inorder = 0: wait for its completion)
+        if (j >= 1 && !inorder) mbar_wait(ofull + ((j - 1) & 1), ((j - 1) >> 1) & 1);
         issue_s(j + 1);
       }
       mbar_wait(vfull + b, (j >> 1) & 1);
@@ -719,7 +722,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                           float scale, float scale_log2, int accumulate, int nheads, volatile int* dbg,
                           long long* trace, int pf_dist, const float* __restrict__ dk_raw,
                           const float* __restrict__ dv_raw, int64_t dkv_sstride, bf16* __restrict__ dkv_out,
-                          int64_t ldq, int64_t dq_sstride) {
+                          int64_t ldq, int64_t dq_sstride, int inorder) {
   extern __shared__ uint8_t smem_raw[];
 #define DBG(role, v)                                                                    \
   do {                                                                                  \
@@ -819,8 +822,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       mbar_wait(qfull + bq, (j / NQB) & 1);
       if (lane == 0) TRC(1, 0, j);
       // buffer bb last held tile j-2: its S^T was read by the softmax (pfull(j-2), waited before
-      // the MMAs of j-2), its P^T by dV(j-2) (qfree(j-2))
-      if (j >= 2) mbar_wait(qfree + (j - 2) % NQB, ((j - 2) / NQB) & 1);
+      // the MMAs of j-2), its P^T by dV(j-2), issued before this MMA (in-order tcgen05.mma
+      // execution; inorder = 0: wait for dV(j-2) to complete, qfree(j-2))
+      if (j >= 2 && !inorder) mbar_wait(qfree + (j - 2) % NQB, ((j - 2) / NQB) & 1);
       if (lane == 0) TRC(1, 1, j);
       tc_fence_after();
 #pragma unroll
@@ -1345,6 +1349,13 @@ __global__ void dq_convert_kernel(const float* __restrict__ dq_acc, int64_t ld_a
 
 bool attn_sm100_supported(int d) { return d == AT; }
 
+// TP_ATTN_INORDER=0: the MMA warps wait for an MMA's completion before issuing the next MMA that
+// overwrites its TMEM operand (A/B knob; default: rely on in-order tcgen05.mma execution)
+static int attn_inorder() {
+  static const int v = !(getenv("TP_ATTN_INORDER") && atoi(getenv("TP_ATTN_INORDER")) == 0);
+  return v;
+}
+
 cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o, int64_t ldo, float* lse, int a, int s,
                            int d, int c, int l, cudaStream_t st, int nseq, int64_t qkv_sstride, int64_t o_sstride,
                            int64_t lse_sstride) {
@@ -1374,7 +1385,8 @@ cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o,
     }
     dim3 grid1((l + AT - 1) / AT, a, nseq);
     attn_fwd1_sm100_kernel<<<grid1, F1_THREADS, Fwd1Smem::BYTES, st>>>(mq, mk, mv, o, ldo, lse, s, c, l,
-                                                                      rsqrtf((float)d) * LOG2E_F, o_sstride, lse_sstride);
+                                                                      rsqrtf((float)d) * LOG2E_F, o_sstride, lse_sstride,
+                                                                      attn_inorder());
     return cudaGetLastError();
   }
   {
@@ -1392,7 +1404,7 @@ cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o,
     if (trace2_left > 0) cudaMemsetAsync(trace2, 0, 4 * 8 * 64 * sizeof(long long), st);
     attn_fwd2_sm100_kernel<<<grid2, F2_THREADS, Fwd2Smem::BYTES, st>>>(mq, mk, mv, o, ldo, lse, s, c, l,
                                                                       rsqrtf((float)d) * LOG2E_F, o_sstride, lse_sstride,
-                                                                      trace2_left > 0 ? trace2 : nullptr);
+                                                                      trace2_left > 0 ? trace2 : nullptr, attn_inorder());
     if (trace2_left > 0) {
       --trace2_left;
       long long h[4 * 8 * 64];
@@ -1494,7 +1506,7 @@ cudaError_t attn_bwd_sm100(const bf16* dO, int64_t ld_do, const bf16* o, int64_t
                                                            a, dbg_dev, trace_left > 0 ? trace : nullptr, pf_dist,
                                                            dk_acc, dv_acc,
                                                            nseq > 1 ? dkv_sstride : (int64_t)a * s * d, dkv_fused ? dq : nullptr,
-                                                           ldq, nseq > 1 ? dq_sstride : 0);
+                                                           ldq, nseq > 1 ? dq_sstride : 0, attn_inorder());
   e = cudaGetLastError();
   if (trace_left > 0) {
     --trace_left;
