@@ -327,16 +327,18 @@ __global__ void __launch_bounds__(NT, 1) ln_bwd_wide_kernel(const T* __restrict_
 // stalled behind its own reductions and stores). One CTA of 256 threads (8 columns each) per group
 // of `rpb` consecutive rows; the block reduction's barrier doubles as the "stage consumed" signal,
 // after which thread 0 refills the stage with the row LN*_STAGES ahead.
-// Forward: 4 stages of one row (4H bytes); 48 registers -> 5 CTAs per SM.
+// NT threads x 8 columns per row (NT = 256 for H <= 2048, 640 for H <= 5120, e.g. 13B).
+// Forward (H <= 2048): 4 stages of one row (4H bytes); 48 registers -> 5 CTAs per SM.
 constexpr int LNF_STAGES = 4;
-template <typename T>
-__global__ void __launch_bounds__(256) ln_fwd_bulk_kernel(const float* __restrict__ x, const float* __restrict__ gam,
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) ln_fwd_bulk_kernel(const float* __restrict__ x, const float* __restrict__ gam,
                                                           const float* __restrict__ bet, T* __restrict__ y,
                                                           float* __restrict__ mean_out, float* __restrict__ rstd_out,
                                                           int rows, int H, int rpb) {
   extern __shared__ __align__(128) float lnf_ring[];  // [LNF_STAGES][H]
   __shared__ __align__(8) uint64_t full[LNF_STAGES];
-  __shared__ float red[2][2][8];
+  constexpr int NW = NT / 32;
+  __shared__ float red[2][2][NW];
   const int tid = threadIdx.x, col = tid * 8;
   const bool act = col < H;
   const uint32_t bytes = (uint32_t)H * 4u;
@@ -364,7 +366,7 @@ __global__ void __launch_bounds__(256) ln_fwd_bulk_kernel(const float* __restric
     float s = 0.f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) s += v[k];
-    float (*rd)[8] = red[i & 1];
+    float (*rd)[NW] = red[i & 1];
     s = warp_sum(s);
     if ((tid & 31) == 0) rd[0][tid >> 5] = s;
     __syncthreads();  // also: every thread has read stage d
@@ -374,7 +376,7 @@ __global__ void __launch_bounds__(256) ln_fwd_bulk_kernel(const float* __restric
     }
     float m = 0.f;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) m += rd[0][w];
+    for (int w = 0; w < NW; ++w) m += rd[0][w];
     const float mean = m / H;
     float q = 0.f;
     if (act)
@@ -385,7 +387,7 @@ __global__ void __launch_bounds__(256) ln_fwd_bulk_kernel(const float* __restric
     __syncthreads();
     float qq = 0.f;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) qq += rd[1][w];
+    for (int w = 0; w < NW; ++w) qq += rd[1][w];
     const float rstd = rsqrtf(qq / H + 1e-5f);
     if (tid == 0) { mean_out[r] = mean; rstd_out[r] = rstd; }
     if (act) {
@@ -401,10 +403,10 @@ __global__ void __launch_bounds__(256) ln_fwd_bulk_kernel(const float* __restric
 // dbeta / dbias partials in registers), with the row's x, resid and dy staged through a ring of
 // LNB_STAGES shared-memory stages by thread 0. The per-row block reduction's barrier doubles as the
 // "stage consumed" signal: after it, thread 0 refills the stage with row r + LNB_STAGES. The
-// group's mean / rstd are read into shared memory 128 rows at a time.
-constexpr int LNB_STAGES = 4;
-template <typename T>
-__global__ void __launch_bounds__(256, 2) ln_bwd_bulk_kernel(const T* __restrict__ dy, const float* __restrict__ x,
+// group's mean / rstd are read into shared memory 128 rows at a time. ~100 registers: 2 CTAs per SM
+// at NT = 256 (4 stages of 20 KB), 1 at NT = 640 (3 stages of 50 KB at H = 5120).
+template <typename T, int NT, int LNB_STAGES>
+__global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) ln_bwd_bulk_kernel(const T* __restrict__ dy, const float* __restrict__ x,
                                                              const float* __restrict__ mean_in,
                                                              const float* __restrict__ rstd_in,
                                                              const float* __restrict__ gam, const float* __restrict__ resid,
@@ -413,7 +415,8 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_bulk_kernel(const T* __restrict
                                                              float* __restrict__ dbias, int rows, int H, int rpb) {
   extern __shared__ __align__(128) uint8_t lnb_ring[];  // [LNB_STAGES][x: 4H | resid: 4H | dy: H*sizeof(T)]
   __shared__ __align__(8) uint64_t full[LNB_STAGES];
-  __shared__ float red[2][2][8];
+  constexpr int NW = NT / 32;
+  __shared__ float red[2][2][NW];
   __shared__ float st[2][128];
   const int tid = threadIdx.x, col = tid * 8;
   const bool act = col < H;
@@ -441,7 +444,7 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_bulk_kernel(const T* __restrict
     if ((i & 127) == 0) {  // stats of the next (up to) 128 rows of the group
       __syncthreads();     // previous chunk's readers are done (first pass: barrier init visible)
       if (tid < 128) { if (r + tid < r1) st[0][tid] = mean_in[r + tid]; }
-      else if (r + tid - 128 < r1) st[1][tid - 128] = rstd_in[r + tid - 128];
+      else if (tid < 256 && r + tid - 128 < r1) st[1][tid - 128] = rstd_in[r + tid - 128];
       __syncthreads();
     }
     const float mean = st[0][i & 127], rstd = st[1][i & 127];
@@ -470,7 +473,7 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_bulk_kernel(const T* __restrict
       pg[k] += dv[k] * xh[k];
       pb[k] += dv[k];
     }
-    float (*rd)[8] = red[i & 1];
+    float (*rd)[NW] = red[i & 1];
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
     if ((tid & 31) == 0) { rd[0][tid >> 5] = s1; rd[1][tid >> 5] = s2; }
@@ -478,7 +481,7 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_bulk_kernel(const T* __restrict
     if (tid == 0 && r + LNB_STAGES < r1) issue(r + LNB_STAGES, d);
     float m1 = 0.f, m2 = 0.f;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) { m1 += rd[0][w]; m2 += rd[1][w]; }
+    for (int w = 0; w < NW; ++w) { m1 += rd[0][w]; m2 += rd[1][w]; }
     m1 /= H;
     m2 /= H;
     if (act) {
@@ -717,15 +720,30 @@ template <typename T>
 cudaError_t layernorm_fwd(const float* x, const float* gam, const float* bet, T* y, float* mean, float* rstd,
                           int rows, int H, cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
+  // bulk forward for H <= 2048 only: at H = 5120 the 640-thread variant measured slower than the
+  // block-per-row kernel (3.45 vs 3.70 TB/s, profiles/r02_ln_bulk_ab.txt)
   if (H <= 2048 && ln_bulk_enabled() && aligned16(x) && aligned16(y)) {
     const int smem = LNF_STAGES * H * (int)sizeof(float);
-    static int per_sm = 0;  // resident CTAs per SM at H = 2048 (the row groups form one wave)
-    if (!per_sm && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ln_fwd_bulk_kernel<T>, 256,
-                                                                 LNF_STAGES * 2048 * (int)sizeof(float)) != cudaSuccess)
-      per_sm = 4;
-    const int nsm = std::max(1, num_sms()) * std::max(1, per_sm);
-    const int rpb = std::max(4, (rows + nsm - 1) / nsm);
-    ln_fwd_bulk_kernel<T><<<(rows + rpb - 1) / rpb, 256, smem, st>>>(x, gam, bet, y, mean, rstd, rows, H, rpb);
+    auto launch = [&](auto kern, int nt, int hmax) -> cudaError_t {
+      static int per_sm[2] = {0, 0};  // resident CTAs per SM at the widest H of the variant
+      int& ps = per_sm[nt > 256];
+      if (!ps) {
+        if (nt > 256) {
+          cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               LNF_STAGES * hmax * (int)sizeof(float));
+          if (e != cudaSuccess) return e;
+        }
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, nt, LNF_STAGES * hmax * (int)sizeof(float)) !=
+            cudaSuccess || ps < 1)
+          ps = 1;
+      }
+      const int units = std::max(1, num_sms()) * ps;
+      const int rpb = std::max(4, (rows + units - 1) / units);
+      kern<<<(rows + rpb - 1) / rpb, nt, smem, st>>>(x, gam, bet, y, mean, rstd, rows, H, rpb);
+      return cudaSuccess;
+    };
+    cudaError_t e = launch(ln_fwd_bulk_kernel<T, 256>, 256, 2048);
+    if (e != cudaSuccess) return e;
   } else if (H <= 2048) ln_fwd_warp_kernel<T, 8><<<(rows + 7) / 8, 256, 0, st>>>(x, gam, bet, y, mean, rstd, rows, H);
   else if (H <= 4096) ln_fwd_kernel<T, 256, 2><<<rows, 256, 0, st>>>(x, gam, bet, y, mean, rstd, H);
   else if (H <= 6144) ln_fwd_kernel<T, 256, 3><<<rows, 256, 0, st>>>(x, gam, bet, y, mean, rstd, H);
@@ -762,19 +780,24 @@ cudaError_t layernorm_bwd(const T* dy, const float* x, const float* mean, const 
     ln_bwd_wide_kernel<T, NT, NCH><<<grid, NT, smem, st>>>(dy, x, mean, rstd, gam, resid, dx_out, dx_copy, \
                                                           dgam, dbet, dbias, rows, H, rpb);               \
   } while (0)
-  if (H <= 2048 && ln_bulk_enabled() && aligned16(x) && aligned16(dy) && aligned16(resid)) {
-    const int smem = LNB_STAGES * H * (8 + (int)sizeof(T));
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(ln_bwd_bulk_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           LNB_STAGES * 2048 * (8 + (int)sizeof(T)));
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    const int nsm = std::max(1, num_sms());
-    const int rpb2 = std::max(4, (rows + 2 * nsm - 1) / (2 * nsm));
-    ln_bwd_bulk_kernel<T><<<(rows + rpb2 - 1) / rpb2, 256, smem, st>>>(dy, x, mean, rstd, gam, resid, dx_out, dx_copy,
-                                                                       dgam, dbet, dbias, rows, H, rpb2);
+  if (H <= 5120 && ln_bulk_enabled() && aligned16(x) && aligned16(dy) && aligned16(resid)) {
+    auto launch = [&](auto kern, int nt, int stages, int ctas, int hmax) -> cudaError_t {
+      static bool attr[2] = {false, false};
+      if (!attr[nt > 256]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             stages * hmax * (8 + (int)sizeof(T)));
+        if (e != cudaSuccess) return e;
+        attr[nt > 256] = true;
+      }
+      const int units = std::max(1, num_sms()) * ctas;
+      const int rpb2 = std::max(4, (rows + units - 1) / units);
+      kern<<<(rows + rpb2 - 1) / rpb2, nt, stages * H * (8 + (int)sizeof(T)), st>>>(
+          dy, x, mean, rstd, gam, resid, dx_out, dx_copy, dgam, dbet, dbias, rows, H, rpb2);
+      return cudaSuccess;
+    };
+    cudaError_t e = H <= 2048 ? launch(ln_bwd_bulk_kernel<T, 256, 4>, 256, 4, 2, 2048)
+                              : launch(ln_bwd_bulk_kernel<T, 640, 3>, 640, 3, 1, 5120);
+    if (e != cudaSuccess) return e;
   } else if (H <= 2048) LNB(256, 1);
   else if (H <= 4096) LNBW(512, 1);
   else if (H <= 6144) LNBW(768, 1);

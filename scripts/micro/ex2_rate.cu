@@ -81,6 +81,11 @@ int main() {
       cudaDeviceSynchronize();
     }
     long long h; cudaMemcpy(&h, clk, 8, cudaMemcpyDeviceToHost);
+    if (mode == 3) {  // the same mix with one warp per SM sub-partition (4 warps per CTA)
+      for (int rep = 0; rep < 2; ++rep) { kern<3><<<148, 128>>>(iters, out, clk); cudaDeviceSynchronize(); }
+      long long h1; cudaMemcpy(&h1, clk, 8, cudaMemcpyDeviceToHost);
+      printf("%-26s %8.2f elements/clk/SM  (%lld clk)\n", "softmax mix, 1 warp/SMSP", 128.0 * iters * 4 / h1, h1);
+    }
     const double elems = 256.0 * iters * 4 * (mode == 1 || mode == 2 || mode == 4 ? 2 : 1);
     printf("%-26s %8.2f elements/clk/SM  (%lld clk)\n", names[mode], elems / h, h);
   }
