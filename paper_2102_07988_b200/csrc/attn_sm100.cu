@@ -679,6 +679,275 @@ __global__ void __launch_bounds__(F1_THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------ forward, two query tiles, 64-key blocks
+// The two-tile kernel above serialises, per tile, softmax(j) -> O += P_j V_j -> S_{j+1} = Q K_{j+1}^T
+// (P_j lives in S's TMEM columns, and S is single-buffered because O_0, O_1, S_0, S_1 fill the 512
+// columns). Here key blocks are 64 wide, so each tile's S is double-buffered in the same 128
+// columns: S_{t,b} = cols t*128 + b*64 (P_{t,b} packed into its first 32), O_t at 256 + t*128.
+// S_{j+1} is computed while the softmax works on S_j, and the softmax runs block after block
+// without waiting for the tensor pipe. The price: S MMAs at N = 64 (shared-memory bound, 2/3 rate).
+//   warp 0     TMA: Q_0, Q_1 once; K_j / V_j (64 x 128) into 4-deep rings;
+//   warp 1     MMA: per block j and tile t, once the softmax has written P_t(j): O_t += P_t(j) V_j,
+//              then S_t(j+2) into the same buffer (tcgen05.mma executes in issue order, so it cannot
+//              overwrite P_t(j) before that MMA has read it): S runs two blocks ahead;
+//   warps 2-9  softmax (4 per tile, thread = query row), the one-pass lazy-rescale scheme above.
+constexpr int BK3 = 64;                         // keys per block
+constexpr uint32_t KT3 = BK3 * AT * 2;          // 16 KiB: [64 keys][128 d]
+constexpr uint32_t KHALF3 = KT3 / 2;            // 8 KiB: second 64-column (d) atom
+constexpr int NK3 = 4, NV3 = 4;
+struct Fwd3Smem {
+  static constexpr uint32_t Q = 0, K = 2 * TILE, V = K + NK3 * KT3;
+  static constexpr uint32_t BAR = V + NV3 * KT3;
+  static constexpr uint32_t BYTES = BAR + 512 + 1024;
+  static_assert(BYTES <= 232448, "forward tile set exceeds 227 KB of shared memory");
+};
+template <bool MASK>
+__device__ __forceinline__ void exp_max_chunk32(const uint32_t (&r)[32], int col0, int nvis, float scale_log2,
+                                                float nm, float (&rs4)[4], float (&m4)[4], uint32_t (&pk)[32],
+                                                int pk0) {
+#pragma unroll
+  for (int u = 0; u < 32; u += 2) {
+    float x0 = __uint_as_float(r[u]), x1 = __uint_as_float(r[u + 1]);
+    if (MASK) {
+      x0 = col0 + u < nvis ? x0 : -INFINITY;
+      x1 = col0 + u + 1 < nvis ? x1 : -INFINITY;
+    }
+    m4[(u >> 1) & 3] = fmaxf(m4[(u >> 1) & 3], fmaxf(x0, x1));
+    const float p0 = ex2(fmaf(x0, scale_log2, nm));
+    const float p1 = ex2(fmaf(x1, scale_log2, nm));
+    rs4[(u >> 1) & 3] += p0 + p1;
+    __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+    pk[pk0 + (u >> 1)] = *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+
+__global__ void __launch_bounds__(F2_THREADS, 1)
+    attn_fwd3_sm100_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                           const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ o, int64_t ldo,
+                           float* __restrict__ lse, int s, int c, int l, float scale_log2, int64_t o_sstride,
+                           int64_t lse_sstride) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (tc5::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Fwd3Smem::BAR);
+  uint64_t* qfull = bars + 0;
+  uint64_t* kfull = bars + 1;    // [NK3]
+  uint64_t* kfree = bars + 5;    // [NK3]
+  uint64_t* vfull = bars + 9;    // [NV3]
+  uint64_t* vfree = bars + 13;   // [NV3]
+  uint64_t* sfull = bars + 17;   // [tile][buffer]: S_t(j) in buffer j & 1
+  uint64_t* pfull = bars + 21;   // [tile][buffer]: P_t(j) written (4 warps)
+  uint64_t* ofull = bars + 25;   // [tile][buffer]: O_t += P_t(j) V_j complete, buffer j & 1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 29);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int head = blockIdx.y, sq = blockIdx.z, r0 = (gridDim.x - 1 - blockIdx.x) * 2 * AT;
+  o += sq * o_sstride;
+  lse += sq * lse_sstride;
+  const int ntiles = r0 + AT < l ? 2 : 1;
+  int nkb[2];
+  for (int t = 0; t < 2; ++t) nkb[t] = (c + min(l, r0 + (t + 1) * AT) - 1) / BK3 + 1;
+  const int nkbmax = nkb[ntiles - 1];
+
+  if (threadIdx.x == 0) {
+    mbar_init(qfull, 1);
+    for (int i = 0; i < NK3; ++i) { mbar_init(kfull + i, 1); mbar_init(kfree + i, 1); }
+    for (int i = 0; i < NV3; ++i) { mbar_init(vfull + i, 1); mbar_init(vfree + i, 1); }
+    for (int i = 0; i < 4; ++i) { mbar_init(sfull + i, 1); mbar_init(pfull + i, 4); mbar_init(ofull + i, 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    mbar_expect_tx(qfull, 2 * TILE);
+    for (int t = 0; t < 2; ++t) {
+      tma_load_4d(sm + Fwd3Smem::Q + t * TILE, &tmQ, 0, c + r0 + t * AT, head, sq, qfull);
+      tma_load_4d(sm + Fwd3Smem::Q + t * TILE + HALF, &tmQ, 64, c + r0 + t * AT, head, sq, qfull);
+    }
+    for (int j = 0; j < nkbmax; ++j) {
+      const int bk = j % NK3, bv = j % NV3;
+      if (j >= NK3) mbar_wait(kfree + bk, ((j / NK3) - 1) & 1);
+      uint8_t* kd = sm + Fwd3Smem::K + bk * KT3;
+      mbar_expect_tx(kfull + bk, KT3);
+      tma_load_4d(kd, &tmK, 0, j * BK3, head, sq, kfull + bk);
+      tma_load_4d(kd + KHALF3, &tmK, 64, j * BK3, head, sq, kfull + bk);
+      if (j >= NV3) mbar_wait(vfree + bv, ((j / NV3) - 1) & 1);
+      uint8_t* vd = sm + Fwd3Smem::V + bv * KT3;
+      mbar_expect_tx(vfull + bv, KT3);
+      tma_load_4d(vd, &tmV, 0, j * BK3, head, sq, vfull + bv);
+      tma_load_4d(vd + KHALF3, &tmV, 64, j * BK3, head, sq, vfull + bv);
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idS = idesc_bf16(128, BK3, false, false);
+    constexpr uint32_t idO = idesc_bf16(128, 128, false, true);
+    auto issue_s1 = [&](int t, int j) {  // S_t(j) = Q_t K_j^T into buffer j & 1 (K_j resident)
+      const uint32_t k_base = smem_u32(sm + Fwd3Smem::K + (j % NK3) * KT3);
+      const uint32_t q_base = smem_u32(sm + Fwd3Smem::Q + t * TILE);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < AT / 16; ++kk)
+        mma_bf16_w(tmem + t * 128 + (j & 1) * BK3, make_desc(q_base + (kk >> 2) * HALF + (kk & 3) * 32, 16, 1024),
+                   make_desc(k_base + (kk >> 2) * KHALF3 + (kk & 3) * 32, 16, 1024), idS, kk > 0);
+      mma_commit_w(sfull + t * 2 + (j & 1));
+    };
+    mbar_wait(qfull, 0);
+    for (int j = 0; j < 2 && j < nkbmax; ++j) {  // S(0), S(1): both buffers
+      mbar_wait(kfull + j, 0);
+      for (int t = 0; t < ntiles; ++t)
+        if (j < nkb[t]) issue_s1(t, j);
+      mma_commit_w(kfree + j);
+    }
+    // per block j and tile t, as soon as the softmax has written P_t(j): O_t += P_t(j) V_j, then
+    // S_t(j+2) into the same buffer (in issue order after the MMA that reads P_t(j)), so S runs two
+    // blocks ahead of the softmax
+    for (int j = 0; j < nkbmax; ++j) {
+      const int bv = j % NV3, b = j & 1;
+      mbar_wait(vfull + bv, (j / NV3) & 1);
+      const uint32_t v_base = smem_u32(sm + Fwd3Smem::V + bv * KT3);
+      bool k_waited = false;
+      for (int t = 0; t < ntiles; ++t) {
+        if (j >= nkb[t]) continue;
+        mbar_wait(pfull + t * 2 + b, (j >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BK3 / 16; ++kk)
+          mma_bf16_ts_w(tmem + 256 + t * 128, tmem + t * 128 + b * BK3 + kk * 8, make_desc(v_base + kk * 2048, KHALF3, 1024),
+                        idO, (j | kk) != 0);
+        mma_commit_w(ofull + t * 2 + b);
+        if (j + 2 < nkb[t]) {
+          if (!k_waited) { mbar_wait(kfull + (j + 2) % NK3, ((j + 2) / NK3) & 1); k_waited = true; }
+          issue_s1(t, j + 2);
+        }
+      }
+      mma_commit_w(vfree + bv);
+      if (k_waited) mma_commit_w(kfree + (j + 2) % NK3);
+    }
+  } else if (warp >= 2) {
+    // ---------------- softmax: tile t = (warp - 2) / 4, thread = query row of the tile
+    const int t = (warp - 2) >> 2, q = warp & 3, row = q * 32 + lane;
+    if (t < ntiles) {
+      const int qabs = c + r0 + t * AT + row;
+      const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+      const uint32_t o_col = 256 + t * 128;
+      float m_ref = -INFINITY, lsum = 0.f;
+      for (int j = 0; j < nkb[t]; ++j) {
+        const int b = j & 1;
+        const uint32_t s_col = t * 128 + b * BK3;
+        mbar_wait(sfull + t * 2 + b, (j >> 1) & 1);
+        tc_fence_after();
+        const int nvis = qabs - j * BK3 + 1;
+        const bool diag = __any_sync(0xffffffffu, nvis < BK3);
+        float rs4[4] = {0.f, 0.f, 0.f, 0.f}, m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        uint32_t pk[32];
+        const float nm = -m_ref;
+        {
+          uint32_t r[2][32];
+          tmem_ld32_nowait(lane_base + s_col, r[0]);
+          tmem_ld32_nowait(lane_base + s_col + 32, r[1]);
+          tmem_wait_ld();
+          if (j > 0) {
+            if (diag) {
+              exp_max_chunk32<true>(r[0], 0, nvis, scale_log2, nm, rs4, m4, pk, 0);
+              exp_max_chunk32<true>(r[1], 32, nvis, scale_log2, nm, rs4, m4, pk, 16);
+            } else {
+              exp_max_chunk32<false>(r[0], 0, nvis, scale_log2, nm, rs4, m4, pk, 0);
+              exp_max_chunk32<false>(r[1], 32, nvis, scale_log2, nm, rs4, m4, pk, 16);
+            }
+          } else {
+            if (diag) row_max_chunk<true>(r, 0, nvis, m4);
+            else row_max_chunk<false>(r, 0, nvis, m4);
+          }
+        }
+        const float m_blk = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
+        const bool grow = m_blk > m_ref + RESCALE_LOG2;
+        if (__any_sync(0xffffffffu, grow)) {
+          const float m_new = grow ? m_blk : m_ref;
+          const float f = ex2(m_ref - m_new);
+          if (j >= 1) {
+            // O_t += P_t(j-1) V_{j-1} complete (its buffer's previous phase, P_t(j-3), completed before
+            // S_t(j) was computed: in-order MMAs)
+            mbar_wait(ofull + t * 2 + ((j - 1) & 1), ((j - 1) >> 1) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int ch = 0; ch < AT / 32; ++ch) {
+              uint32_t r[32];
+              tmem_ld32_nowait(lane_base + o_col + ch * 32, r);
+              tmem_wait_ld();
+#pragma unroll
+              for (int u = 0; u < 32; ++u) r[u] = __float_as_uint(__uint_as_float(r[u]) * f);
+              tmem_st32(lane_base + o_col + ch * 32, r);
+            }
+            tmem_wait_st();
+          }
+          lsum *= f;
+          m_ref = m_new;
+          const float nm2 = -m_ref;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) rs4[i] = 0.f;
+#pragma unroll
+          for (int ch = 0; ch < BK3 / 32; ++ch) {
+            uint32_t r[32];
+            tmem_ld32_nowait(lane_base + s_col + ch * 32, r);
+            tmem_wait_ld();
+            uint32_t pk16[16];
+            float mm[4];
+            exp_max_chunk16<true>(r, ch * 32, nvis, scale_log2, nm2, rs4, mm, pk16);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) pk[ch * 16 + u] = pk16[u];
+          }
+        }
+        const float rsum = (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          uint32_t pk16[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) pk16[u] = pk[ch * 16 + u];
+          tmem_st16(lane_base + s_col + ch * 16, pk16);
+        }
+        lsum += rsum;
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(pfull + t * 2 + b);
+      }
+      // epilogue: the last O_t += P V complete (commits track every earlier MMA of the thread)
+      const int jl = nkb[t] - 1;
+      mbar_wait(ofull + t * 2 + (jl & 1), (jl >> 1) & 1);
+      tc_fence_after();
+      const int r = r0 + t * AT + row;
+      const float inv = 1.f / lsum;
+      bf16* orow = o + (int64_t)r * ldo + head * AT;
+#pragma unroll 1
+      for (int ch = 0; ch < AT / 32; ++ch) {
+        uint32_t rr[32];
+        tmem_ld32_nowait(lane_base + o_col + ch * 32, rr);
+        tmem_wait_ld();
+        if (r < l) {
+#pragma unroll
+          for (int u = 0; u < 32; u += 8) {
+            float v8[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v8[e] = __uint_as_float(rr[u + e]) * inv;
+            store8<bf16>(orow + ch * 32 + u, v8);
+          }
+        }
+      }
+      if (r < l) lse[(int64_t)head * s + c + r] = (m_ref + log2f(lsum)) / LOG2E_F;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // ======================================================================== backward
 // Per (128-key block of the prefix [0, c+l), head, sequence); loop over the slice's 64-query tiles
 // that can see the block. The tile loop is software-pipelined so the tensor pipe never waits for
@@ -1370,11 +1639,32 @@ cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o,
       !encode_bf16_map(&mv, v, 4, dims, strides, box))
     return cudaErrorInvalidValue;
   // TP_ATTN_FWD=1: one query tile per CTA with S double-buffered; =2: two tiles per CTA sharing K/V;
-  // default by slice length: measured (scripts/attn_bench.py, one B200) the one-tile kernel is faster
-  // for short slices (l = 512 at c = 1536, 80 heads: 79.8 vs 90.9 us; l = 576 at c = 0: 53.0 vs 55.6)
-  // and slower for long ones (l = 1472: 212 vs 203 us), where the shared K/V reads dominate
+  // =3: two tiles, 64-key blocks, S double-buffered per tile. Default: the two-tile 64-key kernel when
+  // its grid fills at least two waves, else the one-tile kernel (wave quantisation of the half-size
+  // grid dominates). Measured (scripts/attn_bench.py, one B200; profiles/r02_attn_fwd3.txt):
+  // c = 0, l = 2048, 128 heads: 3: 203, 2: 214, 1: 222 us; c = 576, l = 1472: 188 / 200 / 204;
+  // c = 0, l = 576: 45.7 / 52.7 / 52.6; c = 1536, l = 512, 80 heads (160 two-tile CTAs): 89 / 86 / 76.
   static const int fwd_env = getenv("TP_ATTN_FWD") ? atoi(getenv("TP_ATTN_FWD")) : 0;
-  const int fwd_impl = fwd_env ? fwd_env : (l <= 640 ? 1 : 2);
+  const long pair_ctas = (long)((l + 2 * AT - 1) / (2 * AT)) * a * nseq;
+  const int fwd_impl = fwd_env ? fwd_env : (pair_ctas >= 2L * num_sms() ? 3 : 1);
+  if (fwd_impl == 3) {  // two tiles, 64-key blocks, S double-buffered (attn_fwd3_sm100_kernel)
+    static bool attr3 = false;
+    if (!attr3) {
+      cudaError_t e = cudaFuncSetAttribute(attn_fwd3_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)Fwd3Smem::BYTES);
+      if (e != cudaSuccess) return e;
+      attr3 = true;
+    }
+    const uint32_t box64[4] = {64, BK3, 1, 1};
+    CUtensorMap mk64, mv64;
+    if (!encode_bf16_map(&mk64, k, 4, dims, strides, box64) || !encode_bf16_map(&mv64, v, 4, dims, strides, box64))
+      return cudaErrorInvalidValue;
+    dim3 grid3((l + 2 * AT - 1) / (2 * AT), a, nseq);
+    attn_fwd3_sm100_kernel<<<grid3, F2_THREADS, Fwd3Smem::BYTES, st>>>(mq, mk64, mv64, o, ldo, lse, s, c, l,
+                                                                      rsqrtf((float)d) * LOG2E_F, o_sstride,
+                                                                      lse_sstride);
+    return cudaGetLastError();
+  }
   if (fwd_impl == 1) {
     static bool attr1 = false;
     if (!attr1) {

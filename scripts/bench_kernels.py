@@ -102,6 +102,7 @@ def layernorm(rows, H, tag=""):
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", default="all")
+    ap.add_argument("--filter", default="")
     args = ap.parse_args()
     if args.which in ("all", "gemm"):
         H = 2048
@@ -122,8 +123,15 @@ if __name__ == "__main__":
                                        (11776, H, H, 0, 0, "1b o-proj b=8 l=1472"), (11776, 4 * H, H, 0, 0, "1b fc1 b=8 l=1472"),
                                        (11776, H, 4 * H, 0, 0, "1b fc2 b=8 l=1472"), (11776, 50304, H, 0, 0, "1b head l=1472"),
                                        (H, 3 * H, 16384, 1, 1, "1b qkv dW K=16384"), (4 * H, H, 16384, 1, 1, "1b fc2 dW K=16384"),
-                                       (H, 4 * H, 16384, 1, 1, "1b fc1 dW K=16384")]:
-            gemm(M, N, K, am, bm, 0, tag)
+                                       (H, 4 * H, 16384, 1, 1, "1b fc1 dW K=16384"),
+                                       # the default N = 1 bench plan [(8, [2048])]: T = 16384 rows
+                                       (16384, 3 * H, H, 0, 0, "T=16384 qkv fwd"), (16384, H, H, 0, 0, "T=16384 o-proj fwd"),
+                                       (16384, 4 * H, H, 0, 0, "T=16384 fc1 fwd"), (16384, H, 4 * H, 0, 0, "T=16384 fc2 fwd"),
+                                       (16384, 50304, H, 0, 0, "T=16384 head fwd"), (16384, H, 3 * H, 0, 1, "T=16384 qkv dX"),
+                                       (16384, H, 4 * H, 0, 1, "T=16384 fc1 dX"), (16384, 4 * H, H, 0, 1, "T=16384 fc2 dX"),
+                                       (16384, H, 50304, 0, 1, "T=16384 head dX"), (4 * H, H, 16384, 1, 1, "T=16384 fc2 dW")]:
+            if args.filter in tag:
+                gemm(M, N, K, am, bm, 0, tag)
     if args.which in ("all", "attn"):
         for (a, s, d, c, l, tag) in [(16, 2048, 128, 0, 2048, "1b full"), (40, 2048, 128, 1536, 512, "13b last slice"),
                                      (40, 2048, 128, 0, 512, "13b first slice"), (40, 8192, 128, 7680, 512, "13b-8k last")]:

@@ -147,6 +147,26 @@ def test_attention_fwd_bwd(a, s, d, c, l, impl):
     assert rel(dk[:, :c + l], dK) < 2e-2 and rel(dv[:, :c + l], dV) < 2e-2
 
 
+@pytest.mark.parametrize("a,s,c,l", [(64, 1536, 264, 1200), (40, 2048, 0, 2048)])
+def test_attention_fwd_wide_grid(a, s, c, l):
+    """Grids of >= 2 waves of two-tile CTAs take the 64-key double-buffered forward kernel by default
+    (attn_sm100.cu dispatch): unaligned prefix c, a ragged last tile pair (l = 1200: 48 rows in its
+    second tile), full causal s = 2048; O per element and lse against fp32 math on the same inputs."""
+    d = 128
+    g = torch.Generator(device="cpu").manual_seed(a + s + c + l)
+    q, k, v = (torch.randn(a, s, d, generator=g).to(dev, torch.bfloat16) for _ in range(3))
+    o = torch.zeros(l, a * d, device=dev, dtype=torch.bfloat16)
+    lse = torch.zeros(a, s, device=dev)
+    tp.k_attention_fwd(ptr(q), ptr(k), ptr(v), ptr(o), ptr(lse), a, s, d, c, l, 0)
+    torch.cuda.synchronize()
+    o_ref, lse_ref, _ = attn_ref(q, k, v, c, l)
+    o_ref_tok = o_ref.transpose(0, 1).reshape(l, a * d)
+    assert rel(o.float(), o_ref_tok) < 1e-2
+    assert (o.float() - o_ref_tok).abs().max() < 0.05
+    assert rel(lse[:, c:c + l], lse_ref) < 1e-4
+    assert torch.all(lse[:, :c] == 0) and torch.all(lse[:, c + l:] == 0)
+
+
 @pytest.mark.parametrize("rows,H", [(1, 8), (7, 136), (300, 2048), (4099, 2048), (16384, 2048), (33, 1000),
                                     (513, 5120), (64, 12288)])
 @pytest.mark.parametrize("with_resid", [False, True])

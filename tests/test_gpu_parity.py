@@ -350,3 +350,17 @@ def test_balanced_partition_parity(K, flags):
     loss, logits, grads = gpu_run_plan(cfg, B, params, tokens, [(1, [40, 24, 64])] * B, tp.TP_BF16,
                                        flags=tp.TP_FLAG_KEEP_LOGITS | flags)
     check(worst_errors(loss, logits, grads, ref), 2e-2)
+
+
+@pytest.mark.parametrize("flags", [0, tp.TP_FLAG_NCCL_LOOPBACK, tp.TP_FLAG_SCHEDULE_1F1B])
+def test_eight_stage_pipeline_parity(flags):
+    """K = 8 stages (one layer each, the depth of an 8-GPU run) executed on one GPU: GPipe and 1F1B op
+    lists, in-process and NCCL-loopback transports, heterogeneous slicing; same function as the
+    unsliced fp64 oracle."""
+    base, B = CONFIGS["small-deep"]
+    cfg = base.with_(n_stages=8)
+    assert tp.stage_layers(cfg) == [1] * 8
+    params, tokens, ref = oracle_run(cfg, B, 17, True)
+    loss, logits, grads = gpu_run_plan(cfg, B, params, tokens, [(1, [40, 24, 64]), (1, [64, 64])], tp.TP_BF16,
+                                       flags=tp.TP_FLAG_KEEP_LOGITS | flags)
+    check(worst_errors(loss, logits, grads, ref), 2e-2)
