@@ -203,7 +203,9 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
   uint64_t* ofull = bars + 15;   // [2 tiles] O_t += P_t V_j complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: provably warp-uniform, so the role branches below keep the
+  // uniform datapath (descriptor arithmetic in uniform registers for tcgen05.mma)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   // raster: the query-tile pairs of one (head, sequence) are consecutive CTAs (heaviest first), so
   // they run concurrently and read that head's K / V blocks from L2 instead of DRAM
   const int head = blockIdx.y, sq = blockIdx.z, r0 = (gridDim.x - 1 - blockIdx.x) * 2 * AT;
@@ -211,9 +213,11 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
   lse += sq * lse_sstride;
   // key blocks of each tile: tile t covers rows [r0 + t*128, +128) of the slice (absolute c + ...)
   const int ntiles = r0 + AT < l ? 2 : 1;
-  int nkb[2];
-  for (int t = 0; t < 2; ++t) nkb[t] = (c + min(l, r0 + (t + 1) * AT) - 1) / AT + 1;
-  const int nkbmax = nkb[ntiles - 1];
+  // key blocks per tile as scalars (a dynamically indexed array would live in local memory and its
+  // values would not be provably warp-uniform in the MMA warp)
+  const int nkb0 = (c + min(l, r0 + AT) - 1) / AT + 1, nkb1 = (c + min(l, r0 + 2 * AT) - 1) / AT + 1;
+  auto nkb = [&](int t) { return t ? nkb1 : nkb0; };
+  const int nkbmax = ntiles > 1 ? nkb1 : nkb0;
 
   if (threadIdx.x == 0) {
     mbar_init(qfull, 1);
@@ -230,7 +234,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 0) {
+    if (lane == 0) {
     // ---------------- TMA producer
     mbar_expect_tx(qfull, 2 * TILE);
     for (int t = 0; t < 2; ++t) {
@@ -249,6 +254,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       mbar_expect_tx(vfull + bv, TILE);
       tma_load_4d(vd, &tmV, 0, j * AT, head, sq, vfull + bv);
       tma_load_4d(vd + HALF, &tmV, 64, j * AT, head, sq, vfull + bv);
+    }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer
@@ -281,7 +287,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       mbar_wait(vfull + bv, (j >> 1) & 1);
       const uint32_t v_base = smem_u32(sm + Fwd2Smem::V + bv * TILE);
       for (int t = 0; t < ntiles; ++t) {
-        if (j >= nkb[t]) continue;
+        if (j >= nkb(t)) continue;
         mbar_wait(pfull + t, j & 1);
         if (lane == 0) TRF(1, 3 + t, j);
         tc_fence_after();
@@ -291,7 +297,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
                         (j | kk) != 0);
         mma_commit_w(ofull + t);
         if (lane == 0) TRF(1, 5 + t, j);
-        if (j + 1 < nkb[t]) {
+        if (j + 1 < nkb(t)) {
           if (!k_waited) { mbar_wait(kfull + (j + 1) % NKS, ((j + 1) / NKS) & 1); k_waited = true; }
           if (lane == 0) TRF(1, 0, j + 1);
           // S_t's columns hold P_t, read by O_t += P_t V_j just issued. tcgen05.mma instructions of
@@ -313,7 +319,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
       const uint32_t s_col = t * 128, o_col = 256 + t * 128;
       float m_ref = -INFINITY, lsum = 0.f;
-      for (int j = 0; j < nkb[t]; ++j) {
+      for (int j = 0; j < nkb(t); ++j) {
         mbar_wait(sfull + t, j & 1);
         if (row == 0) TRF(2 + t, 0, j);
         tc_fence_after();
@@ -413,7 +419,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
         if (row == 0) TRF(2 + t, 2, j);
       }
       // epilogue: O / lsum -> bf16 rows, lse
-      mbar_wait(ofull + t, (nkb[t] - 1) & 1);
+      mbar_wait(ofull + t, (nkb(t) - 1) & 1);
       tc_fence_after();
       const int r = r0 + t * AT + row;
       const float inv = 1.f / lsum;
@@ -480,7 +486,9 @@ __global__ void __launch_bounds__(F1_THREADS, 1)
   uint64_t* ofull = bars + 15;   // [2] O += P_j V_j complete (j & 1 == b)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: provably warp-uniform, so the role branches below keep the
+  // uniform datapath (descriptor arithmetic in uniform registers for tcgen05.mma)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int head = blockIdx.y, sq = blockIdx.z, r0 = (gridDim.x - 1 - blockIdx.x) * AT;
   o += sq * o_sstride;
   lse += sq * lse_sstride;
@@ -501,7 +509,8 @@ __global__ void __launch_bounds__(F1_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 0) {
+    if (lane == 0) {
     mbar_expect_tx(qfull, TILE);
     tma_load_4d(sm + Fwd1Smem::Q, &tmQ, 0, c + r0, head, sq, qfull);
     tma_load_4d(sm + Fwd1Smem::Q + HALF, &tmQ, 64, c + r0, head, sq, qfull);
@@ -517,6 +526,7 @@ __global__ void __launch_bounds__(F1_THREADS, 1)
       mbar_expect_tx(vfull + bv, TILE);
       tma_load_4d(vd, &tmV, 0, j * AT, head, sq, vfull + bv);
       tma_load_4d(vd + HALF, &tmV, 64, j * AT, head, sq, vfull + bv);
+    }
     }
   } else if (warp == 1) {
     constexpr uint32_t idS = idesc_bf16(128, 128, false, false);
@@ -725,7 +735,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     attn_fwd3_sm100_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                            const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ o, int64_t ldo,
                            float* __restrict__ lse, int s, int c, int l, float scale_log2, int64_t o_sstride,
-                           int64_t lse_sstride) {
+                           int64_t lse_sstride, long long* trace) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (tc5::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Fwd3Smem::BAR);
@@ -739,14 +749,19 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
   uint64_t* ofull = bars + 25;   // [tile][buffer]: O_t += P_t(j) V_j complete, buffer j & 1
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 29);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: provably warp-uniform, so ptxas can use the uniform datapath for
+  // the MMA warp's descriptor arithmetic
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int head = blockIdx.y, sq = blockIdx.z, r0 = (gridDim.x - 1 - blockIdx.x) * 2 * AT;
   o += sq * o_sstride;
   lse += sq * lse_sstride;
   const int ntiles = r0 + AT < l ? 2 : 1;
-  int nkb[2];
-  for (int t = 0; t < 2; ++t) nkb[t] = (c + min(l, r0 + (t + 1) * AT) - 1) / BK3 + 1;
-  const int nkbmax = nkb[ntiles - 1];
+  // key blocks per tile as scalars (a dynamically indexed array lands in local memory, and values
+  // loaded from it are not provably warp-uniform: the MMA warp's control flow then loses the uniform
+  // datapath and every tcgen05.mma pays an elect + register broadcast)
+  const int nkb0 = (c + min(l, r0 + AT) - 1) / BK3 + 1, nkb1 = (c + min(l, r0 + 2 * AT) - 1) / BK3 + 1;
+  auto nkb = [&](int t) { return t ? nkb1 : nkb0; };
+  const int nkbmax = ntiles > 1 ? nkb1 : nkb0;
 
   if (threadIdx.x == 0) {
     mbar_init(qfull, 1);
@@ -761,7 +776,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 0) {  // warp-uniform role branches (lets ptxas use the uniform datapath in the MMA warp)
+    if (lane == 0) {
     // ---------------- TMA producer
     mbar_expect_tx(qfull, 2 * TILE);
     for (int t = 0; t < 2; ++t) {
@@ -781,13 +797,17 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       tma_load_4d(vd, &tmV, 0, j * BK3, head, sq, vfull + bv);
       tma_load_4d(vd + KHALF3, &tmV, 64, j * BK3, head, sq, vfull + bv);
     }
+    }
   } else if (warp == 1) {
     // ---------------- MMA issuer
     constexpr uint32_t idS = idesc_bf16(128, BK3, false, false);
     constexpr uint32_t idO = idesc_bf16(128, 128, false, true);
+    // shared-memory addresses as 32-bit arithmetic on the (warp-uniform) window base, so ptxas keeps
+    // the descriptors in uniform registers (no per-MMA elect / R2UR broadcast)
+    const uint32_t sbase = smem_u32(smem_raw) + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     auto issue_s1 = [&](int t, int j) {  // S_t(j) = Q_t K_j^T into buffer j & 1 (K_j resident)
-      const uint32_t k_base = smem_u32(sm + Fwd3Smem::K + (j % NK3) * KT3);
-      const uint32_t q_base = smem_u32(sm + Fwd3Smem::Q + t * TILE);
+      const uint32_t k_base = sbase + Fwd3Smem::K + (j % NK3) * KT3;
+      const uint32_t q_base = sbase + Fwd3Smem::Q + t * TILE;
       tc_fence_after();
 #pragma unroll
       for (int kk = 0; kk < AT / 16; ++kk)
@@ -799,7 +819,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     for (int j = 0; j < 2 && j < nkbmax; ++j) {  // S(0), S(1): both buffers
       mbar_wait(kfull + j, 0);
       for (int t = 0; t < ntiles; ++t)
-        if (j < nkb[t]) issue_s1(t, j);
+        if (j < nkb(t)) issue_s1(t, j);
       mma_commit_w(kfree + j);
     }
     // per block j and tile t, as soon as the softmax has written P_t(j): O_t += P_t(j) V_j, then
@@ -808,20 +828,24 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     for (int j = 0; j < nkbmax; ++j) {
       const int bv = j % NV3, b = j & 1;
       mbar_wait(vfull + bv, (j / NV3) & 1);
-      const uint32_t v_base = smem_u32(sm + Fwd3Smem::V + bv * KT3);
+      if (lane == 0) TRF(1, 0, j);
+      const uint32_t v_base = sbase + Fwd3Smem::V + bv * KT3;
       bool k_waited = false;
       for (int t = 0; t < ntiles; ++t) {
-        if (j >= nkb[t]) continue;
+        if (j >= nkb(t)) continue;
         mbar_wait(pfull + t * 2 + b, (j >> 1) & 1);
+        if (lane == 0) TRF(1, 1 + t, j);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BK3 / 16; ++kk)
           mma_bf16_ts_w(tmem + 256 + t * 128, tmem + t * 128 + b * BK3 + kk * 8, make_desc(v_base + kk * 2048, KHALF3, 1024),
                         idO, (j | kk) != 0);
         mma_commit_w(ofull + t * 2 + b);
-        if (j + 2 < nkb[t]) {
+        if (lane == 0) TRF(1, 3 + t, j);
+        if (j + 2 < nkb(t)) {
           if (!k_waited) { mbar_wait(kfull + (j + 2) % NK3, ((j + 2) / NK3) & 1); k_waited = true; }
           issue_s1(t, j + 2);
+          if (lane == 0) TRF(1, 5 + t, j + 2);
         }
       }
       mma_commit_w(vfree + bv);
@@ -835,10 +859,12 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
       const uint32_t o_col = 256 + t * 128;
       float m_ref = -INFINITY, lsum = 0.f;
-      for (int j = 0; j < nkb[t]; ++j) {
+      for (int j = 0; j < nkb(t); ++j) {
         const int b = j & 1;
         const uint32_t s_col = t * 128 + b * BK3;
+        if (row == 0) TRF(2 + t, 0, j);
         mbar_wait(sfull + t * 2 + b, (j >> 1) & 1);
+        if (row == 0) TRF(2 + t, 1, j);
         tc_fence_after();
         const int nvis = qabs - j * BK3 + 1;
         const bool diag = __any_sync(0xffffffffu, nvis < BK3);
@@ -914,9 +940,10 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(pfull + t * 2 + b);
+        if (row == 0) TRF(2 + t, 2, j);
       }
       // epilogue: the last O_t += P V complete (commits track every earlier MMA of the thread)
-      const int jl = nkb[t] - 1;
+      const int jl = nkb(t) - 1;
       mbar_wait(ofull + t * 2 + (jl & 1), (jl >> 1) & 1);
       tc_fence_after();
       const int r = r0 + t * AT + row;
@@ -1018,7 +1045,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint64_t* dpfull = bars + 18;  // [2] dP^T in TMEM buffer (sfull: S^T)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: provably warp-uniform, so the role branches below keep the
+  // uniform datapath (descriptor arithmetic in uniform registers for tcgen05.mma)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   // raster: the key blocks of one (sequence, head) are consecutive CTAs (heaviest, key block 0,
   // first), so they run concurrently: that head's Q / dO tiles are read from DRAM once and shared
   // through L2, and the fp32 dQ reduce-adds of all its key blocks meet in L2
@@ -1045,7 +1074,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   if (threadIdx.x == 0) DBG(6, ntile);
   constexpr uint32_t T_DV = 256, T_DK = 384;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 0) {
+    if (lane == 0) {
     // ---------------- TMA producer: K, V once; Q_i, dO_i through the 3-deep ring
     mbar_expect_tx(kvfull, 2 * TILE);
     tma_load_4d(sm + BwdSmem::K, &tmK, 0, key0, head, sq, kvfull);
@@ -1075,19 +1105,22 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tma_prefetch_3d(&tmdO, head * AT + 64, qp * BQB, sq);
       }
     }
+    }
   } else if (warp == 1) {
     // ---------------- MMA issuer (whole warp, warp-uniform control flow; one elected lane issues)
     constexpr uint32_t idS = idesc_bf16(128, BQB, false, false);   // S^T, dP^T
     constexpr uint32_t idKV = idesc_bf16(128, 128, false, true);   // dV (A = P^T in TMEM), dK (B = dO / Q, MN-major)
     constexpr uint32_t idQ = idesc_bf16(128, BQB, true, true);     // dQ^T (A = K MN-major, B = dS^T MN-major)
-    const uint32_t k_base = smem_u32(sm + BwdSmem::K), v_base = smem_u32(sm + BwdSmem::V);
+    // shared-memory addresses as 32-bit arithmetic on the warp-uniform window base (uniform datapath)
+    const uint32_t sbase = smem_u32(smem_raw) + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t k_base = sbase + BwdSmem::K, v_base = sbase + BwdSmem::V;
     mbar_wait(kvfull, 0);
     // Per tile j (TMEM buffer j & 1): S^T is issued as early as possible (the softmax warps start the
     // exp2 work on it while dV / dK of the previous tile run), dP^T after dV / dK of j-1 (its
     // columns held dQ^T of j-2, which the drain warps must have read).
     auto issue_s = [&](int j) {
       const int bq = j % NQB, bb = j & 1;
-      const uint32_t q_base = smem_u32(sm + BwdSmem::Q + bq * QT);
+      const uint32_t q_base = sbase + BwdSmem::Q + bq * QT;
       mbar_wait(qfull + bq, (j / NQB) & 1);
       if (lane == 0) TRC(1, 0, j);
       // buffer bb last held tile j-2: its S^T was read by the softmax (pfull(j-2), waited before
@@ -1106,7 +1139,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     };
     auto issue_dp = [&](int j) {
       const int bq = j % NQB, bb = j & 1;
-      const uint32_t o_base = smem_u32(sm + BwdSmem::O + bq * QT);
+      const uint32_t o_base = sbase + BwdSmem::O + bq * QT;
       if (DQ && j >= 2) mbar_wait(dqfree + bb, ((j >> 1) - 1) & 1);
       if (lane == 0) TRC(1, 2, j);
       tc_fence_after();
@@ -1122,8 +1155,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     issue_dp(0);
     for (int i = 0; i < ntile; ++i) {
       const int bq = i % NQB, bb = i & 1;
-      const uint32_t q_base = smem_u32(sm + BwdSmem::Q + bq * QT), o_base = smem_u32(sm + BwdSmem::O + bq * QT);
-      const uint32_t ds_base = smem_u32(sm + BwdSmem::DS + bb * PT);
+      const uint32_t q_base = sbase + BwdSmem::Q + bq * QT, o_base = sbase + BwdSmem::O + bq * QT;
+      const uint32_t ds_base = sbase + BwdSmem::DS + bb * PT;
       const uint32_t tb = tmem + bb * 128;
       if (lane == 0) DBG(1, 100 + 10 * i);
       if (i + 1 < ntile) issue_s(i + 1);
@@ -1407,7 +1440,9 @@ __global__ void __launch_bounds__(DQ_THREADS, 1)
   uint64_t* dqdone = bars + 14; // [2] dQ += dS_j K_j complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: provably warp-uniform, so the role branches below keep the
+  // uniform datapath (descriptor arithmetic in uniform registers for tcgen05.mma)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int head = blockIdx.y, sq = blockIdx.z, r0 = (gridDim.x - 1 - blockIdx.x) * AT;
   const int nkb = (c + min(l, r0 + AT) - 1) / AT + 1;
 
@@ -1427,7 +1462,8 @@ __global__ void __launch_bounds__(DQ_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   constexpr uint32_t T_DP = 256, T_DQ = 384;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 0) {
+    if (lane == 0) {
     mbar_expect_tx(qfull, 2 * TILE);
     tma_load_4d(sm + DqSmem::Q, &tmQ, 0, c + r0, head, sq, qfull);
     tma_load_4d(sm + DqSmem::Q + HALF, &tmQ, 64, c + r0, head, sq, qfull);
@@ -1443,6 +1479,7 @@ __global__ void __launch_bounds__(DQ_THREADS, 1)
       mbar_expect_tx(vfull + b, TILE);
       tma_load_4d(sm + DqSmem::V + b * TILE, &tmV, 0, j * AT, head, sq, vfull + b);
       tma_load_4d(sm + DqSmem::V + b * TILE + HALF, &tmV, 64, j * AT, head, sq, vfull + b);
+    }
     }
   } else if (warp == 1) {
     constexpr uint32_t idS = idesc_bf16(128, 128, false, false);  // S, dP (both operands K-major)
@@ -1660,9 +1697,28 @@ cudaError_t attn_fwd_sm100(const bf16* q, const bf16* k, const bf16* v, bf16* o,
     if (!encode_bf16_map(&mk64, k, 4, dims, strides, box64) || !encode_bf16_map(&mv64, v, 4, dims, strides, box64))
       return cudaErrorInvalidValue;
     dim3 grid3((l + 2 * AT - 1) / (2 * AT), a, nseq);
+    static int trace3_left = getenv("TP_ATTN_TRACE") ? atoi(getenv("TP_ATTN_TRACE")) : 0;
+    static long long* trace3 = nullptr;
+    if (trace3_left > 0 && !trace3) cudaMalloc(&trace3, 4 * 8 * 64 * sizeof(long long));
+    if (trace3_left > 0) cudaMemsetAsync(trace3, 0, 4 * 8 * 64 * sizeof(long long), st);
     attn_fwd3_sm100_kernel<<<grid3, F2_THREADS, Fwd3Smem::BYTES, st>>>(mq, mk64, mv64, o, ldo, lse, s, c, l,
                                                                       rsqrtf((float)d) * LOG2E_F, o_sstride,
-                                                                      lse_sstride);
+                                                                      lse_sstride, trace3_left > 0 ? trace3 : nullptr);
+    if (trace3_left > 0) {
+      --trace3_left;
+      long long h[4 * 8 * 64];
+      cudaMemcpyAsync(h, trace3, sizeof(h), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      long long t0 = 0;
+      for (int i = 0; i < 4 * 8 * 64; ++i) if (h[i] && (!t0 || h[i] < t0)) t0 = h[i];
+      fprintf(stderr, "attn_fwd3 trace c=%d l=%d: kb | M:vfull M:pfull0 M:pfull1 M:PV0 M:PV1 M:S0 M:S1 | T0:wait T0:sfull T0:pfull | T1:wait T1:sfull T1:pfull\n", c, l);
+      for (int i = 0; i < 64; ++i) {
+        auto g = [&](int r, int e) { long long v = h[(r * 8 + e) * 64 + i]; return v ? (long long)(v - t0) : -1LL; };
+        if (g(1, 0) < 0) break;
+        fprintf(stderr, "%3d | %7lld %7lld %7lld %7lld %7lld %7lld %7lld | %7lld %7lld %7lld | %7lld %7lld %7lld\n", i,
+                g(1, 0), g(1, 1), g(1, 2), g(1, 3), g(1, 4), g(1, 5), g(1, 6), g(2, 0), g(2, 1), g(2, 2), g(3, 0), g(3, 1), g(3, 2));
+      }
+    }
     return cudaGetLastError();
   }
   if (fwd_impl == 1) {

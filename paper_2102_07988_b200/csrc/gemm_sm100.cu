@@ -292,8 +292,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t crank = CG == 2 ? cluster_rank() : 0;
+  // warp index through a shuffle: provably warp-uniform, so the role branches below keep the
+  // uniform datapath (descriptor arithmetic in uniform registers for tcgen05.mma)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const uint32_t crank = CG == 2 ? __shfl_sync(0xffffffffu, cluster_rank(), 0) : 0;  // warp-uniform
   const bool leader = crank == 0;
   const int m_tiles = (M + C::TILE_M - 1) / C::TILE_M, n_tiles = (N + C::TILE_N - 1) / C::TILE_N;
   const int tiles = m_tiles * n_tiles, kbs = (K + BK - 1) / BK;
@@ -324,7 +326,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 0) {
+    if (lane == 0) {
     // ---------------- TMA producer (both CTAs of a pair; bytes land on the leader's barrier)
     int stage = 0;
     uint32_t phase = 0;
@@ -371,6 +374,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (++stage == C::NS) { stage = 0; phase ^= 1; }
       }
     }
+    }
   } else if (warp == 1 && leader) {
     // ---------------- MMA issuer (whole warp, one elected lane issues for the CTA / CTA pair)
     const uint32_t idesc = (1u << 4)                       // D = fp32
@@ -380,6 +384,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int stage = 0, acc = 0;
     uint32_t phase = 0, acc_phase = 0;
     int tile, k0, k1, part;
+    // stage addresses as 32-bit arithmetic on the warp-uniform window base (uniform datapath)
+    const uint32_t sbase = smem_u32(smem_raw) + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     for (int item = 0; gemm_item(item, unit, nunits, tiles, kbs, sk, tile, k0, k1, part); ++item) {
       mbar_wait(tempty + acc, acc_phase ^ 1);
       tc_fence_after();
@@ -387,7 +393,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int kb = k0; kb < k1; ++kb) {
         mbar_wait(full + stage, phase);
         tc_fence_after();
-        const uint32_t a_base = smem_u32(smem + stage * C::STAGE);
+        const uint32_t a_base = sbase + stage * C::STAGE;
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k) {
           const uint64_t ad = A_MN ? make_desc(a_base + k * 2048, 8192, 1024) : make_desc(a_base + k * 32, 16, 1024);

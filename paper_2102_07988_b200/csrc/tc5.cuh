@@ -38,15 +38,19 @@ __device__ __forceinline__ uint64_t global_ns() {
   return t;
 }
 // Waits for the phase with the given parity. A watchdog turns a protocol deadlock into a trap
-// (a CUDA error on the host) instead of a hung GPU: after 4 s of waiting it prints the barrier and
-// traps.
+// (a CUDA error on the host) instead of a hung GPU after 4 s of waiting. Build with
+// -DTP_WATCHDOG_PRINTF to also print the barrier: the printf call in every wait loop costs the MMA
+// warps the uniform datapath (ptxas then issues each tcgen05.mma through an elect + register
+// broadcast sequence, ~3x the instructions per MMA), so it is off in normal builds.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try(bar, parity)) return;
   const uint64_t t0 = global_ns();
   while (!mbar_try(bar, parity)) {
     if (global_ns() - t0 > 4000000000ull) {
+#ifdef TP_WATCHDOG_PRINTF
       printf("tp: mbarrier watchdog: block (%d,%d) thread %d bar smem+%u parity %u\n", blockIdx.x, blockIdx.y,
              threadIdx.x, smem_u32(bar), parity);
+#endif
       __trap();
     }
   }
