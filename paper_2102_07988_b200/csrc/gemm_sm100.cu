@@ -76,12 +76,14 @@ struct Cfg {
 // fused epilogue. Each unit leaves at most one partial per launch, so a slot per unit suffices.
 struct SplitK {
   int dp_tiles = 0;       // whole tiles; [dp_tiles, tiles) are processed stream-K
-  long long sk_iters = 0; // (tiles - dp_tiles) * kbs
+  int sk_iters = 0;       // (tiles - dp_tiles) * kbs; the host keeps sk_iters * units < 2^31, so the
+                          // device index math stays 32-bit (a 64-bit division is a helper CALL, which
+                          // would cost the MMA and TMA warps the uniform datapath)
   float* ws = nullptr;    // [unit * CG + crank][128][TILE_N] fp32 partial slots
   int* flag = nullptr;    // [unit * CG + crank]: 1 = partial ready (reset to 0 by the finisher)
 };
-__device__ __forceinline__ long long sk_r0(int unit, int nunits, long long iters) {
-  return iters * unit / nunits;
+__device__ __forceinline__ int sk_r0(int unit, int nunits, int iters) {
+  return (int)((unsigned)(iters * unit) / (unsigned)nunits);
 }
 // Work item `it` of unit `unit`: first its whole tiles (round robin), then the tile segments of its
 // stream-K range. kind: 0 = whole tile, 1 = partial (the range ends inside the tile), 2 = finisher
@@ -91,18 +93,18 @@ __device__ __forceinline__ bool gemm_item(int it, int unit, int nunits, int tile
   const int ndp = unit < sk.dp_tiles ? (sk.dp_tiles - unit + nunits - 1) / nunits : 0;
   if (it < ndp) { tile = unit + it * nunits; k0 = 0; k1 = kbs; kind = 0; return true; }
   if (sk.sk_iters <= 0) return false;
-  const long long r0 = sk_r0(unit, nunits, sk.sk_iters), r1 = sk_r0(unit + 1, nunits, sk.sk_iters);
+  const int r0 = sk_r0(unit, nunits, sk.sk_iters), r1 = sk_r0(unit + 1, nunits, sk.sk_iters);
   if (r1 <= r0) return false;
   // segments in REVERSE order: the range's last segment (a partial other units' finishers wait for)
   // first, its first segment (possibly a finisher, which waits for lower units' partials) last — so
   // no unit waits on a partial that is produced at the end of another unit's range
-  const long long t0 = r0 / kbs, nseg = (r1 + kbs - 1) / kbs - t0;
-  const long long n = nseg - 1 - (it - ndp);
+  const int t0 = r0 / kbs, nseg = (r1 + kbs - 1) / kbs - t0;
+  const int n = nseg - 1 - (it - ndp);
   if (n < 0) return false;
-  const long long pos = n == 0 ? r0 : (t0 + n) * (long long)kbs;
-  tile = sk.dp_tiles + (int)(pos / kbs);
-  k0 = (int)(pos % kbs);
-  k1 = (int)std::min<long long>(kbs, k0 + (r1 - pos));
+  const int pos = n == 0 ? r0 : (t0 + n) * kbs;
+  tile = sk.dp_tiles + pos / kbs;
+  k0 = pos % kbs;
+  k1 = min(kbs, k0 + (r1 - pos));
   kind = (k0 == 0 && k1 == kbs) ? 0 : (k1 < kbs ? 1 : 2);
   return true;
 }
@@ -454,7 +456,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int v_lo = unit, v_hi = unit;
       if (kind == 2) {
         // finisher: the units below whose ranges cover [tile start, this segment's start) left partials
-        const long long tstart = (long long)(tile - sk.dp_tiles) * kbs;
+        const int tstart = (tile - sk.dp_tiles) * kbs;
         while (v_lo > 0 && sk_r0(v_lo, nunits, sk.sk_iters) > tstart) --v_lo;
         if (threadIdx.x == 64) {
           for (int u = v_lo; u < v_hi; ++u) {
@@ -579,9 +581,9 @@ cudaError_t launch_bn(const GemmDesc& g, const Epi& e, cudaStream_t st) {
     const double eff = (double)tiles / ((double)waves * full_units);
     const int dp = tiles > full_units ? (tiles / full_units - 1) * full_units : 0;
     const long long iters = (long long)(tiles - dp) * kbs;
-    if (eff < 0.94 && iters / full_units >= 160) {
+    if (eff < 0.94 && iters / full_units >= 160 && iters * (long long)full_units < (1LL << 31)) {
       sk.dp_tiles = dp;
-      sk.sk_iters = iters;
+      sk.sk_iters = (int)iters;
       sk.ws = g.sk_ws;
       sk.flag = g.sk_cnt;
       units = full_units;
