@@ -711,14 +711,19 @@ cudaError_t gemm_sm100(const GemmDesc& g, const Epi& e, cudaStream_t st) {
   static const Cand cands[4] = {{2, 256, 1.0}, {2, 128, 0.8}, {1, 256, 0.8}, {1, 128, 0.65}};
   // Wide pair tiles (256 x 512, WN = 2) for long K: 48 instead of 64 B/clk/SM of operands, with the
   // epilogue no longer hidden behind the next tile's MMAs (relative cost ~ 1 + 4 / (K/64) k-blocks).
-  // TP_GEMM_WIDE=0 disables, =1 forces (when the shape allows).
+  // Per-tile efficiency relative to 256 x 256, measured at equal wave quantisation
+  // (scripts/bench_kernels.py, profiles/r02_gemm_wide_ab.txt): 1.11 with both operands MN-major (the
+  // weight-gradient GEMMs); with K-major A (forward / dX GEMMs, where the 4-stage ring of 48 KB
+  // stages hides less latency than the 6-stage ring of the 256 x 256 tiles) ~0.99 at K = 6144-8192
+  // and ~1.04 at K = 20480 (13B FC2). TP_GEMM_WIDE=0 disables, =1 forces (when the shape allows).
   const int wide_env = getenv("TP_GEMM_WIDE") ? atoi(getenv("TP_GEMM_WIDE")) : -1;
   if (wide_env != 0 && !g_force_cg && g.persistent && g.M > BM && g.N >= 512 && (g.K >= 4096 || wide_env == 1)) {
     const long units = g_num_sms / 2;
     const long tw = (long)((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + 511) / 512);
     const long t2 = (long)((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + 255) / 256);
     const double kbs = (g.K + BK - 1) / BK;
-    const double cost_wide = (double)((tw + units - 1) / units) * 512 / 1.25 * (1.0 + 4.0 / kbs);
+    const double wide_eff = (g.a_mn && g.b_mn) ? 1.11 : (kbs >= 256 ? 1.05 : 0.99);
+    const double cost_wide = (double)((tw + units - 1) / units) * 512 / wide_eff * (1.0 + 4.0 / kbs);
     const double cost_256 = (double)((t2 + units - 1) / units) * 256;
     if (wide_env == 1 || cost_wide < cost_256 * 0.97) return launch_major<2, 256, 2>(g, e, st);
   }

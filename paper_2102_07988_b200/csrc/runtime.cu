@@ -311,6 +311,10 @@ class Engine final : public EngineBase {
   ncclComm_t base = nullptr, commF[2] = {nullptr, nullptr}, commB[2] = {nullptr, nullptr};
   cudaStream_t s_recv_f = nullptr, s_send_f = nullptr, s_recv_b = nullptr, s_send_b = nullptr;
   cudaStream_t s_wgrad = nullptr;  // low priority: deferred weight gradients (multi-rank)
+  // second stream of the deferred weight-gradient phase: consecutive dW GEMMs alternate between
+  // `stream` and this one, so the partial last wave of one persistent GEMM overlaps the first tiles of
+  // the next (TP_DW_STREAMS=1: one stream)
+  cudaStream_t s_dw2 = nullptr;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_next = 0;
 
@@ -330,7 +334,7 @@ class Engine final : public EngineBase {
     if (h_loss) cudaFreeHost(h_loss);
     if (h_bad_tok) cudaFreeHost(h_bad_tok);
     for (auto e : ev_pool) cudaEventDestroy(e);
-    for (cudaStream_t s : {s_recv_f, s_send_f, s_recv_b, s_send_b, s_wgrad, stream})
+    for (cudaStream_t s : {s_recv_f, s_send_f, s_recv_b, s_send_b, s_wgrad, s_dw2, stream})
       if (s) cudaStreamDestroy(s);
   }
 
@@ -382,6 +386,8 @@ class Engine final : public EngineBase {
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CU(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, hi));
+    if (!(std::getenv("TP_DW_STREAMS") && std::atoi(std::getenv("TP_DW_STREAMS")) == 1))
+      CU(cudaStreamCreateWithPriority(&s_dw2, cudaStreamNonBlocking, hi));
     CU(cudaHostAlloc(&h_loss, sizeof(float), cudaHostAllocDefault));
 
     use_graphs = std::getenv("TP_NO_GRAPHS") == nullptr && std::getenv("TP_ATTN_DEBUG") == nullptr;
@@ -843,13 +849,29 @@ class Engine final : public EngineBase {
   // One GEMM per weight over all B*s tokens of the step (K = B*s, both operands MN-major), written
   // once (the gradients start at zero), plus the bias column sums: off the per-job critical path and
   // with no fp32 read-modify-write.
-  tp_status wgrad(Stage<T>& S, int batch) { return wgrad_rows(S, 0, batch * m.s, false, stream, true); }
+  // the instrumented (per-launch CUDA-event) runs keep the dW GEMMs on one stream: overlapping launches
+  // would charge each other's time to their event intervals
+  tp_status wgrad(Stage<T>& S, int batch) {
+    return wgrad_rows(S, 0, batch * m.s, false, stream, true, instr.on ? nullptr : s_dw2);
+  }
 
   // Weight gradients over rows [row0, row0 + K) of the step (K = tokens), written (accum = false) or
   // added; `persistent` = false launches one tile per CTA so a higher-priority stream interleaves.
-  tp_status wgrad_rows(Stage<T>& S, size_t row0, int K, bool accum, cudaStream_t st, bool persistent) {
+  tp_status wgrad_rows(Stage<T>& S, size_t row0, int K, bool accum, cudaStream_t st, bool persistent,
+                       cudaStream_t st2 = nullptr) {
     const int H = m.H, V = m.V;
     float* GR = S.gflat;
+    // dW GEMMs alternate between st and st2 (fork here, join at the end): each writes its own weight's
+    // gradient, so they are independent
+    int gi = 0;
+    if (st2) {
+      cudaEvent_t e = event();
+      CU(cudaEventRecord(e, st));
+      CU(cudaStreamWaitEvent(st2, e, 0));
+    }
+    auto gemm = [&](int cls, const GemmDesc& g, const Epi& e, cudaStream_t) {
+      return this->gemm(cls, g, e, (st2 && (gi++ & 1)) ? st2 : st);
+    };
     auto G = [&](int M_, int N_, const void* A_, int64_t lda, const void* B_, int64_t ldb) {
       GemmDesc g = gd(M_, N_, K, A_, lda, true, B_, ldb, true);
       g.persistent = persistent;
@@ -880,6 +902,11 @@ class Engine final : public EngineBase {
     if (S.k == m.K - 1) {
       Epi e; e.kind = accum ? EPI_ACCUM : EPI_STORE; e.out_f32 = 1; e.out = GR + S.L.w_out; e.ldo = V;
       TRY(gemm(KC_GEMM_DW, G(H, V, S.Af + row0 * H, H, S.Z + row0 * V, V), e, st));
+    }
+    if (st2) {
+      cudaEvent_t e = event();
+      CU(cudaEventRecord(e, st2));
+      CU(cudaStreamWaitEvent(st, e, 0));
     }
     return TP_OK;
   }
