@@ -287,8 +287,15 @@ def main():
         flat_plan = [x for bb, ls in dp.groups for x in [bb] + ls] + [gbest["b"]]
         if world > 1 and not tdist.agreed(flat_plan):
             raise RuntimeError("ranks planned different slicings")
+    # tie-break (A-31): a DP plan predicted to beat the unsliced GPipe plan by less than
+    # TIE_MARGIN of the step is within the cost table's per-job timing noise (the step model's error
+    # is a few %), and the plan with fewer slices is taken — at K = 1 slicing cannot remove a bubble
+    TIE_MARGIN = 0.02
+    tie_break = False
     if args.slicing == "dp":
         main_sl = dp
+        if dp.groups != gpipe.groups and dp.predicted + t_wgrad > (1 - TIE_MARGIN) * (gbest["gpipe_pred"] + t_wgrad):
+            main_sl, tie_break = gpipe, True
     elif args.slicing == "gpipe":
         main_sl = gpipe
     else:
@@ -368,7 +375,11 @@ def main():
             "predicted_ms": dp.predicted / 1e6, "t_max_ms": dp.t_max / 1e6, "profile_s": t_prof, "plan_s": t_plan,
             "wgrad_ms": t_wgrad / 1e6,
             "predicted_step_ms": (dp.predicted + t_wgrad) / 1e6,
-            "predicted_step_err": ((dp.predicted + t_wgrad) / 1e6 - ms) / ms if main_sl is dp else None,
+            "predicted_step_err": ((dp.predicted + t_wgrad) / 1e6 - ms) / ms if main_sl is dp else
+                                  (((gbest["gpipe_pred"] + t_wgrad) / 1e6 - ms) / ms if tie_break else None),
+            "dp_slicing": dp.notation(),
+            "tie_break": ("DP plan predicted within %d %% of the unsliced GPipe plan: GPipe timed" % round(100 * TIE_MARGIN))
+                         if tie_break else None,
             "comm": None if comm is None else {"alpha_us": comm[0] / 1e3, "gbs": comm[1]},
             "fit": {"a": [float(x) for x in fit[:4]], "max_rel_err": float(fit[4])},
             "joint": "tp_plan_joint over b in " + str(bsl),
