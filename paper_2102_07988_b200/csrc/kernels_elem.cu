@@ -363,32 +363,29 @@ __global__ void __launch_bounds__(NT) ln_fwd_bulk_kernel(const float* __restrict
     else
 #pragma unroll
       for (int k = 0; k < 8; ++k) v[k] = 0.f;
-    float s = 0.f;
+    // one-pass statistics with one block barrier: sums of (x - x0) and (x - x0)^2, x0 = the row's
+    // first element (a value of the row, so E[x - x0]^2 stays of the order of the variance and the
+    // difference below does not cancel catastrophically)
+    const float x0 = lnf_ring[d * H];
+    float s = 0.f, q = 0.f;
+    if (act)
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s += v[k];
+      for (int k = 0; k < 8; ++k) { const float dd = v[k] - x0; s += dd; q += dd * dd; }
     float (*rd)[NW] = red[i & 1];
     s = warp_sum(s);
-    if ((tid & 31) == 0) rd[0][tid >> 5] = s;
+    q = warp_sum(q);
+    if ((tid & 31) == 0) { rd[0][tid >> 5] = s; rd[1][tid >> 5] = q; }
     __syncthreads();  // also: every thread has read stage d
     if (tid == 0 && r + LNF_STAGES < r1) {
       tc5::mbar_expect_tx(&full[d], bytes);
       tc5::bulk_load(lnf_ring + d * H, x + (int64_t)(r + LNF_STAGES) * H, bytes, &full[d]);
     }
-    float m = 0.f;
+    float m = 0.f, qq = 0.f;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) m += rd[0][w];
-    const float mean = m / H;
-    float q = 0.f;
-    if (act)
-#pragma unroll
-      for (int k = 0; k < 8; ++k) { const float dd = v[k] - mean; q += dd * dd; }
-    q = warp_sum(q);
-    if ((tid & 31) == 0) rd[1][tid >> 5] = q;
-    __syncthreads();
-    float qq = 0.f;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) qq += rd[1][w];
-    const float rstd = rsqrtf(qq / H + 1e-5f);
+    for (int w = 0; w < NW; ++w) { m += rd[0][w]; qq += rd[1][w]; }
+    const float dm = m / H;
+    const float mean = x0 + dm;
+    const float rstd = rsqrtf(fmaxf(qq / H - dm * dm, 0.f) + 1e-5f);
     if (tid == 0) { mean_out[r] = mean; rstd_out[r] = rstd; }
     if (act) {
       float o[8];
